@@ -1,0 +1,209 @@
+"""CPU ORACLE for the RaftGP embedding hot path — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline / --impl reference) may import this
+package. The product package paper_2312_01560_b200/ never imports it and shares no code with it.
+
+Thin ctypes wrapper over oracle/oracle.c (plain C, fp64; the Gaussian generator is fp32 bit-exact
+per docs/SKETCH_SPEC.md). Every function cites the passage it follows in oracle.c's header.
+Parity status of each function is listed in DESIGN.md §"Oracle pins"; none is "parity unpinned"
+except the Θ/W bit pattern, which is fixed by the spec rather than by the paper (the paper names no
+generator).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+NCUT, MOD, MOD_REDUCED, PROP = 0, 1, 2, 3
+VARIANTS = {"ncut": NCUT, "mod": MOD, "mod_reduced": MOD_REDUCED}
+
+
+def build() -> str:
+    src = os.path.join(_HERE, "oracle.c")
+    if (not os.path.exists(_SO)) or os.path.getmtime(_SO) < os.path.getmtime(src):
+        subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-ffp-contract=off", "-fno-fast-math",
+                               "-o", _SO, src, "-lm"])
+    return _SO
+
+
+def _L():
+    global _lib
+    if _lib is None:
+        build()
+        _lib = ctypes.CDLL(_SO)
+        for name in ("oracle_gaussian", "oracle_build_csr", "oracle_apply", "oracle_project", "oracle_gcn",
+                     "oracle_embed_rows", "oracle_modularity", "oracle_ncut", "oracle_local_modularity"):
+            getattr(_lib, name).restype = ctypes.c_int
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code):
+        super().__init__(f"oracle status {code}")
+        self.code = code
+
+
+def _check(rc):
+    if rc != 0:
+        raise OracleError(rc)
+
+
+# ------------------------------------------------------------------ generator (SKETCH_SPEC)
+def philox(ctr, key) -> np.ndarray:
+    c = np.ascontiguousarray(ctr, np.uint32)
+    k = np.ascontiguousarray(key, np.uint32)
+    out = np.zeros(4, np.uint32)
+    _L().oracle_philox4x32_10(_p(c), _p(k), _p(out))
+    return out
+
+
+def ln_spec(u: np.ndarray) -> np.ndarray:
+    u = np.ascontiguousarray(u, np.float32)
+    out = np.empty_like(u)
+    _L().oracle_ln_spec_batch(_p(u), _p(out), ctypes.c_int64(u.size))
+    return out
+
+
+def sincos_spec(k2: np.ndarray):
+    k2 = np.ascontiguousarray(k2, np.uint32)
+    c = np.empty(k2.shape, np.float32)
+    s = np.empty(k2.shape, np.float32)
+    _L().oracle_sincos_spec_batch(_p(k2), _p(c), _p(s), ctypes.c_int64(k2.size))
+    return c, s
+
+
+def gaussian(seed: int, tag: int, row_begin: int, rows: int, cols: int, den: int) -> np.ndarray:
+    """rows x cols block (global rows row_begin..) of the spec generator, fp32 bit-exact."""
+    out = np.empty((rows, cols), np.float32)
+    _check(_L().oracle_gaussian(ctypes.c_uint64(seed), ctypes.c_uint32(tag), ctypes.c_int64(row_begin),
+                                ctypes.c_int64(rows), ctypes.c_int32(cols), ctypes.c_int32(den), _p(out)))
+    return out
+
+
+def theta(n: int, r: int, seed: int, row_begin: int = 0) -> np.ndarray:
+    """Θ of Eq. 5 (tag 0, variance 1/r)."""
+    return gaussian(seed, 0, row_begin, n, r, r)
+
+
+def weights(k: int, fan_in: int, fan_out: int, seed: int) -> np.ndarray:
+    """W^(k) of Eq. 6 (tag k, variance 1/fan_in)."""
+    return gaussian(seed, k, 0, fan_in, fan_out, fan_in)
+
+
+# ------------------------------------------------------------------ graph
+class CSR:
+    def __init__(self, n, row_ptr, col):
+        self.n = int(n)
+        self.row_ptr = row_ptr
+        self.col = col
+
+    @property
+    def nnz(self):
+        return int(self.row_ptr[-1])
+
+    @property
+    def deg(self):
+        return np.diff(self.row_ptr).astype(np.int32)
+
+
+def build_csr(n: int, src, dst) -> CSR:
+    src = np.ascontiguousarray(src, np.int32)
+    dst = np.ascontiguousarray(dst, np.int32)
+    m = src.size
+    row_ptr = np.zeros(n + 1, np.int64)
+    col = np.zeros(max(1, 2 * m), np.int32)
+    nnz = ctypes.c_int64(0)
+    _check(_L().oracle_build_csr(ctypes.c_int64(n), ctypes.c_int64(m), _p(src), _p(dst), _p(row_ptr), _p(col),
+                                 ctypes.byref(nnz)))
+    return CSR(n, row_ptr, col[: nnz.value].copy())
+
+
+def apply(g: CSR, op: int, X: np.ndarray) -> np.ndarray:
+    X = np.ascontiguousarray(X, np.float64)
+    if X.ndim == 1:
+        return apply(g, op, X[:, None])[:, 0]
+    out = np.empty_like(X)
+    _check(_L().oracle_apply(ctypes.c_int64(g.n), _p(g.row_ptr), _p(g.col), ctypes.c_int(op),
+                             ctypes.c_int32(X.shape[1]), _p(X), _p(out)))
+    return out
+
+
+def project(g: CSR, variant, r: int, seed: int) -> np.ndarray:
+    v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
+    Y = np.empty((g.n, r), np.float64)
+    _check(_L().oracle_project(ctypes.c_int64(g.n), _p(g.row_ptr), _p(g.col), ctypes.c_int(v), ctypes.c_int32(r),
+                               ctypes.c_uint64(seed), _p(Y)))
+    return Y
+
+
+def gcn(g: CSR, dims, seed: int, Y: np.ndarray):
+    """Returns [Z^(1), ..., Z^(K)] (Z^(K) = the embedding Z)."""
+    dims = np.ascontiguousarray(dims, np.int32)
+    K = len(dims) - 1
+    Y = np.ascontiguousarray(Y, np.float64)
+    tot = int(sum(int(d) for d in dims[1:]))
+    Zc = np.empty(g.n * tot, np.float64)
+    _check(_L().oracle_gcn(ctypes.c_int64(g.n), _p(g.row_ptr), _p(g.col), ctypes.c_int32(K), _p(dims),
+                           ctypes.c_uint64(seed), _p(Y), _p(Zc)))
+    out, off = [], 0
+    for k in range(1, K + 1):
+        out.append(Zc[off: off + g.n * dims[k]].reshape(g.n, dims[k]))
+        off += g.n * dims[k]
+    return out
+
+
+def embed_rows(g: CSR, variant, r: int, dims, seed: int, rows):
+    """(Y[rows], [Z^(k)[rows]]) via the receptive field; identical arithmetic to project + gcn."""
+    v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
+    dims = np.ascontiguousarray(dims if dims is not None else [r], np.int32)
+    K = len(dims) - 1
+    rows = np.ascontiguousarray(rows, np.int64)
+    S = rows.size
+    Y = np.empty((S, r), np.float64)
+    tot = int(sum(int(d) for d in dims[1:]))
+    Zc = np.empty(max(1, S * tot), np.float64)
+    _check(_L().oracle_embed_rows(ctypes.c_int64(g.n), _p(g.row_ptr), _p(g.col), ctypes.c_int(v), ctypes.c_int32(r),
+                                  ctypes.c_int32(K), _p(dims), ctypes.c_uint64(seed), _p(rows), ctypes.c_int64(S),
+                                  _p(Y), _p(Zc)))
+    out, off = [], 0
+    for k in range(1, K + 1):
+        out.append(Zc[off: off + S * dims[k]].reshape(S, dims[k]))
+        off += S * dims[k]
+    return Y, out
+
+
+# ------------------------------------------------------------------ scoring
+def modularity(g: CSR, assign, k: int) -> float:
+    a = np.ascontiguousarray(assign, np.int32)
+    out = ctypes.c_double(0)
+    _check(_L().oracle_modularity(ctypes.c_int64(g.n), _p(g.row_ptr), _p(g.col), _p(a), ctypes.c_int32(k),
+                                  ctypes.byref(out)))
+    return out.value
+
+
+def ncut(g: CSR, assign, k: int) -> float:
+    a = np.ascontiguousarray(assign, np.int32)
+    out = ctypes.c_double(0)
+    _check(_L().oracle_ncut(ctypes.c_int64(g.n), _p(g.row_ptr), _p(g.col), _p(a), ctypes.c_int32(k),
+                            ctypes.byref(out)))
+    return out.value
+
+
+def local_modularity(g: CSR, nodes, block_of_node, k: int) -> float:
+    nd = np.ascontiguousarray(nodes, np.int64)
+    b = np.ascontiguousarray(block_of_node, np.int32)
+    out = ctypes.c_double(0)
+    _check(_L().oracle_local_modularity(ctypes.c_int64(g.n), _p(g.row_ptr), _p(g.col), _p(nd), ctypes.c_int64(nd.size),
+                                        _p(b), ctypes.c_int32(k), ctypes.byref(out)))
+    return out.value

@@ -1,0 +1,483 @@
+/*
+ * oracle/oracle.c — plain, slow, obviously-correct CPU ORACLE of the RaftGP embedding path.
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library. The product path (paper_2312_01560_b200/) never
+ * imports, links or executes it, and shares no code, header, constant or table with it.
+ *
+ * Precision: fp64 for all method arithmetic, except the Gaussian generator, whose fp32 values are
+ * defined bit-exactly by docs/SKETCH_SPEC.md (the paper fixes no generator).
+ * Compile with -ffp-contract=off (no silent FMA contraction); fmaf() is the C99 fused multiply-add.
+ *
+ * What each function follows:
+ *   oracle_philox4x32_10   SKETCH_SPEC §1 (pinned against curand's host Philox)
+ *   oracle_ln_spec_batch,
+ *   oracle_sincos_spec_batch,
+ *   oracle_gaussian        SKETCH_SPEC §2-§5; Eq. 5 Theta_ir ~ N(0, 1/L) (reading #2)
+ *   oracle_build_csr       PAPER.md:56 (§II: undirected, unweighted, A_ij = A_ji in {0,1})
+ *   oracle_apply           X in {M, Q (Eq. 4), Q~,
+ *                          P = D^-1/2 (A+I) D^-1/2 (Eq. 6)} times a dense block
+ *   oracle_project         Eq. 5: Y = X Theta
+ *   oracle_gcn             Eq. 6 + row l2 normalisation
+ *   oracle_embed_rows      the same, for selected output rows only (receptive field)
+ *   oracle_modularity      Eq. 3
+ *   oracle_ncut            Eq. 1
+ *   oracle_local_modularity Eq. 7
+ *
+ * Status codes: 0 ok, 2 parameter error, 3 data error (same numbering as include/raftgp.h, which
+ * is NOT included here).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ---------------------------------------------------------------- Philox4x32-10 (SKETCH_SPEC §1) */
+void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    uint32_t x0 = ctr[0], x1 = ctr[1], x2 = ctr[2], x3 = ctr[3];
+    uint32_t k0 = key[0], k1 = key[1];
+    for (int round = 0; round < 10; ++round) {
+        uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)x0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)x2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t y0 = hi1 ^ x1 ^ k0, y1 = lo1, y2 = hi0 ^ x3 ^ k1, y3 = lo0;
+        x0 = y0; x1 = y1; x2 = y2; x3 = y3;
+        if (round < 9) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    }
+    out[0] = x0; out[1] = x1; out[2] = x2; out[3] = x3;
+}
+
+/* ---------------------------------------------------------------- ln_spec (SKETCH_SPEC §3) */
+static float ln_spec(float u) {
+    uint32_t bits;
+    memcpy(&bits, &u, 4);
+    int e = (int)((bits >> 23) & 0xFFu) - 127;
+    uint32_t mbits = (bits & 0x7FFFFFu) | 0x3F800000u;
+    float m;
+    memcpy(&m, &mbits, 4);
+    if (m > 0x1.6a09e6p+0f) { m = m * 0.5f; e = e + 1; }
+    float t = (m - 1.0f) / (m + 1.0f);
+    float t2 = t * t;
+    float p = fmaf(t2, 0x1.745d18p-3f, 0x1.c71c72p-3f);
+    p = fmaf(t2, p, 0x1.24924ap-2f);
+    p = fmaf(t2, p, 0x1.99999ap-2f);
+    p = fmaf(t2, p, 0x1.555556p-1f);
+    p = fmaf(t2, p, 0x1.000000p+1f);
+    float lnm = t * p;
+    return fmaf((float)e, 0x1.62e430p-1f, lnm);
+}
+
+/* ---------------------------------------------------------------- sincos2pi_spec (SKETCH_SPEC §3) */
+static void sincos2pi_spec(uint32_t k2, float *c, float *s) {
+    uint32_t q = k2 >> 22;
+    float f = (float)(k2 & 0x3FFFFFu) * 0x1p-22f;
+    float phi = f * 0x1.921fb6p+0f;
+    float p2 = phi * phi;
+    float sp = fmaf(p2, -0x1.ae6456p-26f, 0x1.71de3ap-19f);
+    sp = fmaf(p2, sp, -0x1.a01a02p-13f);
+    sp = fmaf(p2, sp, 0x1.111112p-7f);
+    sp = fmaf(p2, sp, -0x1.555556p-3f);
+    float phi3 = phi * p2;
+    float sn = fmaf(phi3, sp, phi);
+    float cp = fmaf(p2, 0x1.1eed8ep-29f, -0x1.27e4fcp-22f);
+    cp = fmaf(p2, cp, 0x1.a01a02p-16f);
+    cp = fmaf(p2, cp, -0x1.6c16c2p-10f);
+    cp = fmaf(p2, cp, 0x1.555556p-5f);
+    cp = fmaf(p2, cp, -0x1.000000p-1f);
+    float cs = fmaf(p2, cp, 1.0f);
+    switch (q) {
+        case 0: *c = cs; *s = sn; break;
+        case 1: *c = -sn; *s = cs; break;
+        case 2: *c = -cs; *s = -sn; break;
+        default: *c = sn; *s = -cs; break;
+    }
+}
+
+void oracle_ln_spec_batch(const float *u, float *out, int64_t n) {
+    for (int64_t i = 0; i < n; ++i) out[i] = ln_spec(u[i]);
+}
+
+void oracle_sincos_spec_batch(const uint32_t *k2, float *c, float *s, int64_t n) {
+    for (int64_t i = 0; i < n; ++i) sincos2pi_spec(k2[i], &c[i], &s[i]);
+}
+
+/* One Gaussian element per SKETCH_SPEC §1-§4 (computed independently per element, on purpose). */
+static float gaussian_element(uint64_t seed, uint32_t tag, uint64_t i, uint32_t col, float sigma) {
+    uint32_t ctr[4] = {col >> 2, (uint32_t)(i & 0xFFFFFFFFu), (uint32_t)(i >> 32), tag};
+    uint32_t key[2] = {(uint32_t)(seed & 0xFFFFFFFFu), (uint32_t)(seed >> 32)};
+    uint32_t x[4];
+    oracle_philox4x32_10(ctr, key, x);
+    uint32_t pair = (col & 3u) >> 1;
+    uint32_t xa = x[2 * pair], xb = x[2 * pair + 1];
+    float u1 = (float)((xa >> 8) + 1u) * 0x1p-24f;
+    uint32_t k2 = xb >> 8;
+    float R = sqrtf(-2.0f * ln_spec(u1));
+    float c, s;
+    sincos2pi_spec(k2, &c, &s);
+    float z = (col & 1u) ? R * s : R * c;
+    return z * sigma;
+}
+
+static float sigma_of(int32_t den) { return 1.0f / sqrtf((float)den); }
+
+/* rows x cols block of the generator matrix, global rows row_begin.. (SKETCH_SPEC §5) */
+int oracle_gaussian(uint64_t seed, uint32_t tag, int64_t row_begin, int64_t rows, int32_t cols, int32_t den,
+                    float *out) {
+    if (rows < 0 || cols <= 0 || den <= 0 || row_begin < 0) return 2;
+    float sigma = sigma_of(den);
+    for (int64_t i = 0; i < rows; ++i)
+        for (int32_t c = 0; c < cols; ++c)
+            out[i * (int64_t)cols + c] = gaussian_element(seed, tag, (uint64_t)(row_begin + i), (uint32_t)c, sigma);
+    return 0;
+}
+
+/* ---------------------------------------------------------------- CSR build */
+static int cmp_u64(const void *a, const void *b) {
+    uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
+    return (x > y) - (x < y);
+}
+
+/*
+ * Canonical CSR of the simple undirected graph of the raw pairs (src[e], dst[e]):
+ * drop u == v, add (u,v) and (v,u), sort lexicographically, drop duplicates.
+ * row_ptr: int64[n+1]; col: int32[capacity >= 2m]; *nnz_out = row_ptr[n] = 2e.
+ */
+int oracle_build_csr(int64_t n, int64_t m, const int32_t *src, const int32_t *dst, int64_t *row_ptr, int32_t *col,
+                     int64_t *nnz_out) {
+    if (n < 0 || m < 0) return 2;
+    for (int64_t e = 0; e < m; ++e)
+        if (src[e] < 0 || src[e] >= n || dst[e] < 0 || dst[e] >= n) return 3;
+    uint64_t *key = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(2 * m + 1));
+    if (!key) return 4;
+    int64_t cnt = 0;
+    for (int64_t e = 0; e < m; ++e) {
+        uint64_t u = (uint64_t)src[e], v = (uint64_t)dst[e];
+        if (u == v) continue;
+        key[cnt++] = (u << 32) | v;
+        key[cnt++] = (v << 32) | u;
+    }
+    qsort(key, (size_t)cnt, sizeof(uint64_t), cmp_u64);
+    int64_t nnz = 0;
+    for (int64_t k = 0; k < cnt; ++k)
+        if (k == 0 || key[k] != key[k - 1]) key[nnz++] = key[k];
+    for (int64_t i = 0; i <= n; ++i) row_ptr[i] = 0;
+    for (int64_t k = 0; k < nnz; ++k) row_ptr[(key[k] >> 32) + 1] += 1;
+    for (int64_t i = 0; i < n; ++i) row_ptr[i + 1] += row_ptr[i];
+    for (int64_t k = 0; k < nnz; ++k) col[k] = (int32_t)(key[k] & 0xFFFFFFFFu);
+    *nnz_out = nnz;
+    free(key);
+    return 0;
+}
+
+/* ---------------------------------------------------------------- operators */
+enum { OP_NCUT = 0, OP_MOD = 1, OP_MOD_REDUCED = 2, OP_PROP = 3 };
+
+static int64_t deg_of(const int64_t *row_ptr, int64_t i) { return row_ptr[i + 1] - row_ptr[i]; }
+
+/* out[i, :] = (X_op @ X)[i, :] for the rows i in rows[0..S) (all rows if rows == NULL, S = n).
+ *   NCUT:        M_ij = A_ij / sqrt(d_i d_j), 0 row if d_i = 0
+ *   MOD:         Q X = A X - d (d^T X) / 2e             (Q_ij = A_ij - d_i d_j / 2e)
+ *   MOD_REDUCED: Q~_ij = A_ij (1 - d_i d_j / 2e)        (Q restricted to edges)
+ *   PROP:        P_ij = Ahat_ij / sqrt(dhat_i dhat_j), Ahat = A + I, dhat = d + 1 (Eq. 6)
+ * X is addressed through xslot: row j of X is X[xslot ? xslot[j] : j]; dTX (length w) is required for MOD.
+ * Each output row is summed sequentially in CSR order (self term first for PROP). */
+static void apply_rows(int64_t n, const int64_t *row_ptr, const int32_t *col, int op, int32_t w, const double *X,
+                       const int32_t *xslot, const double *dTX, double two_e, const int64_t *rows, int64_t S,
+                       double *out) {
+    for (int64_t s = 0; s < S; ++s) {
+        int64_t i = rows ? rows[s] : s;
+        double *o = out + s * (int64_t)w;
+        for (int32_t c = 0; c < w; ++c) o[c] = 0.0;
+        double di = (double)deg_of(row_ptr, i);
+        if (op == OP_PROP) {
+            double shi = 1.0 / sqrt(di + 1.0);
+            const double *xi = X + (int64_t)(xslot ? xslot[i] : i) * w;
+            double wii = shi * shi;
+            for (int32_t c = 0; c < w; ++c) o[c] += wii * xi[c];
+        }
+        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+            int64_t j = col[p];
+            double dj = (double)deg_of(row_ptr, j);
+            double wij;
+            switch (op) {
+                case OP_NCUT: wij = (1.0 / sqrt(di)) * (1.0 / sqrt(dj)); break;
+                case OP_MOD: wij = 1.0; break;
+                case OP_MOD_REDUCED: wij = 1.0 - di * dj / two_e; break;
+                default: wij = (1.0 / sqrt(di + 1.0)) * (1.0 / sqrt(dj + 1.0)); break;
+            }
+            const double *xj = X + (int64_t)(xslot ? xslot[j] : j) * w;
+            for (int32_t c = 0; c < w; ++c) o[c] += wij * xj[c];
+        }
+        if (op == OP_MOD)
+            for (int32_t c = 0; c < w; ++c) o[c] -= di * dTX[c] / two_e;
+    }
+}
+
+int oracle_apply(int64_t n, const int64_t *row_ptr, const int32_t *col, int op, int32_t w, const double *X,
+                 double *out) {
+    if (n < 0 || w <= 0 || op < 0 || op > 3) return 2;
+    double two_e = (double)row_ptr[n];
+    if ((op == OP_MOD || op == OP_MOD_REDUCED) && two_e == 0.0) return 3;
+    double *dTX = NULL;
+    if (op == OP_MOD) {
+        dTX = (double *)calloc((size_t)w, sizeof(double));
+        for (int64_t j = 0; j < n; ++j) {
+            double dj = (double)deg_of(row_ptr, j);
+            for (int32_t c = 0; c < w; ++c) dTX[c] += dj * X[j * (int64_t)w + c];
+        }
+    }
+    apply_rows(n, row_ptr, col, op, w, X, NULL, dTX, two_e, NULL, n, out);
+    free(dTX);
+    return 0;
+}
+
+/* Eq. 5: Y = X Theta, Theta from the spec generator (seed, tag 0, den r), promoted to fp64. */
+int oracle_project(int64_t n, const int64_t *row_ptr, const int32_t *col, int variant, int32_t r, uint64_t seed,
+                   double *Y) {
+    if (r <= 0 || variant < 0 || variant > 2) return 2;
+    if (variant != OP_NCUT && row_ptr[n] == 0) return 3;
+    float *th = (float *)malloc(sizeof(float) * (size_t)(n * (int64_t)r + 1));
+    double *X = (double *)malloc(sizeof(double) * (size_t)(n * (int64_t)r + 1));
+    oracle_gaussian(seed, 0u, 0, n, r, r, th);
+    for (int64_t k = 0; k < n * (int64_t)r; ++k) X[k] = (double)th[k];
+    int rc = oracle_apply(n, row_ptr, col, variant, r, X, Y);
+    free(th);
+    free(X);
+    return rc;
+}
+
+/* tanh then row l2 normalisation of one row; a zero row stays zero. */
+static void act_normalize(double *h, int32_t w) {
+    double ss = 0.0;
+    for (int32_t c = 0; c < w; ++c) { h[c] = tanh(h[c]); ss += h[c] * h[c]; }
+    if (ss > 0.0) {
+        double nrm = sqrt(ss);
+        for (int32_t c = 0; c < w; ++c) h[c] = h[c] / nrm;
+    }
+}
+
+static double *weights_f64(uint64_t seed, int k, int32_t fan_in, int32_t fan_out) {
+    float *wf = (float *)malloc(sizeof(float) * (size_t)fan_in * fan_out);
+    double *wd = (double *)malloc(sizeof(double) * (size_t)fan_in * fan_out);
+    oracle_gaussian(seed, (uint32_t)k, 0, fan_in, fan_out, fan_in, wf);
+    for (int64_t q = 0; q < (int64_t)fan_in * fan_out; ++q) wd[q] = (double)wf[q];
+    free(wf);
+    return wd;
+}
+
+/* Eq. 6 with l2 normalisation: Z^(k) = rownorm(tanh((P Z^(k-1)) W^(k))), Z^(0) = Y.
+ * Zcat receives Z^(1), ..., Z^(K) back to back (block k is n x dims[k]). */
+int oracle_gcn(int64_t n, const int64_t *row_ptr, const int32_t *col, int32_t layers, const int32_t *dims,
+               uint64_t seed, const double *Y, double *Zcat) {
+    if (layers < 1) return 2;
+    for (int k = 0; k <= layers; ++k) if (dims[k] <= 0) return 2;
+    const double *Zin = Y;
+    double *Zout = Zcat;
+    for (int k = 1; k <= layers; ++k) {
+        int32_t a = dims[k - 1], b = dims[k];
+        double *Wk = weights_f64(seed, k, a, b);
+        double *AZ = (double *)malloc(sizeof(double) * (size_t)(n * (int64_t)a + 1));
+        oracle_apply(n, row_ptr, col, OP_PROP, a, Zin, AZ);
+        for (int64_t i = 0; i < n; ++i) {
+            double *h = Zout + i * (int64_t)b;
+            for (int32_t c = 0; c < b; ++c) {
+                double acc = 0.0;
+                for (int32_t t = 0; t < a; ++t) acc += AZ[i * (int64_t)a + t] * Wk[(int64_t)t * b + c];
+                h[c] = acc;
+            }
+            act_normalize(h, b);
+        }
+        free(AZ);
+        free(Wk);
+        Zin = Zout;
+        Zout += n * (int64_t)b;
+    }
+    return 0;
+}
+
+/* ---------------------------------------------------------------- selected rows (receptive field) */
+typedef struct { int64_t *v; int64_t len, cap; } vec64;
+static void vpush(vec64 *a, int64_t x) {
+    if (a->len == a->cap) { a->cap = a->cap ? 2 * a->cap : 1024; a->v = (int64_t *)realloc(a->v, sizeof(int64_t) * a->cap); }
+    a->v[a->len++] = x;
+}
+
+/* closure: set out = in  U  N(in); mark[] must be all -1 on entry for the ids in question and is
+ * left holding the slot (position in out) of each member. */
+static void closure(const int64_t *row_ptr, const int32_t *col, const vec64 *in, vec64 *out, int32_t *mark) {
+    for (int64_t s = 0; s < in->len; ++s) {
+        int64_t i = in->v[s];
+        if (mark[i] < 0) { mark[i] = (int32_t)out->len; vpush(out, i); }
+    }
+    for (int64_t s = 0; s < in->len; ++s) {
+        int64_t i = in->v[s];
+        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+            int64_t j = col[p];
+            if (mark[j] < 0) { mark[j] = (int32_t)out->len; vpush(out, j); }
+        }
+    }
+}
+
+/*
+ * Y and Z^(1..K) for the rows rows[0..S) only, by walking the receptive field: Z^(K) rows need
+ * Z^(K-1) on rows U N(rows), ..., Y on the (K)-hop closure, Theta on the (K+1)-hop closure.
+ * Same arithmetic, same order per row as oracle_project + oracle_gcn, so the results are identical.
+ * MOD needs g = d^T Theta over all n rows: one streaming pass regenerating Theta row by row.
+ * Yrows: S x r. Zrows: layer-major, block k is S x dims[k]. layers may be 0 (Y only).
+ */
+int oracle_embed_rows(int64_t n, const int64_t *row_ptr, const int32_t *col, int variant, int32_t r,
+                      int32_t layers, const int32_t *dims, uint64_t seed, const int64_t *rows, int64_t S,
+                      double *Yrows, double *Zrows) {
+    if (r <= 0 || variant < 0 || variant > 2 || layers < 0) return 2;
+    if (layers > 0 && dims[0] != r) return 2;
+    for (int64_t s = 0; s < S; ++s) if (rows[s] < 0 || rows[s] >= n) return 2;
+    double two_e = (double)row_ptr[n];
+    if (variant != OP_NCUT && two_e == 0.0) return 3;
+    int L = layers;
+    /* chain[0] = output rows; chain[t+1] = chain[t] U N(chain[t]). chain[L-k] holds the rows of Z^(k)
+     * that are needed (Z^(0) = Y), chain[L+1] the Theta rows. cslot[t][i] = position of i in chain[t]. */
+    vec64 *chain = (vec64 *)calloc((size_t)L + 2, sizeof(vec64));
+    int32_t **cslot = (int32_t **)calloc((size_t)L + 2, sizeof(int32_t *));
+    for (int k = 0; k <= L + 1; ++k) {
+        cslot[k] = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n + 1));
+        for (int64_t i = 0; i < n; ++i) cslot[k][i] = -1;
+    }
+    for (int64_t s = 0; s < S; ++s)
+        if (cslot[0][rows[s]] < 0) { cslot[0][rows[s]] = (int32_t)chain[0].len; vpush(&chain[0], rows[s]); }
+    for (int t = 0; t < L + 1; ++t) closure(row_ptr, col, &chain[t], &chain[t + 1], cslot[t + 1]);
+    /* chain[L - k] holds the rows of Z^(k) needed (Z^(0) = Y); chain[L + 1] the Theta rows. */
+    const vec64 *thr = &chain[L + 1];
+    double *TH = (double *)malloc(sizeof(double) * (size_t)(thr->len * (int64_t)r + 1));
+    float *tmp = (float *)malloc(sizeof(float) * (size_t)r);
+    for (int64_t q = 0; q < thr->len; ++q) {
+        oracle_gaussian(seed, 0u, thr->v[q], 1, r, r, tmp);
+        for (int32_t c = 0; c < r; ++c) TH[q * r + c] = (double)tmp[c];
+    }
+    double *dTX = NULL;
+    if (variant == OP_MOD) {
+        dTX = (double *)calloc((size_t)r, sizeof(double));
+        for (int64_t j = 0; j < n; ++j) {
+            double dj = (double)deg_of(row_ptr, j);
+            oracle_gaussian(seed, 0u, j, 1, r, r, tmp);
+            for (int32_t c = 0; c < r; ++c) dTX[c] += dj * (double)tmp[c];
+        }
+    }
+    free(tmp);
+    /* Y on chain[L] */
+    const vec64 *yr = &chain[L];
+    double *Zprev = (double *)malloc(sizeof(double) * (size_t)(yr->len * (int64_t)r + 1));
+    apply_rows(n, row_ptr, col, variant, r, TH, cslot[L + 1], dTX, two_e, yr->v, yr->len, Zprev);
+    free(TH);
+    free(dTX);
+    for (int64_t s = 0; s < S; ++s)
+        memcpy(Yrows + s * (int64_t)r, Zprev + (int64_t)cslot[L][rows[s]] * r, sizeof(double) * (size_t)r);
+    double *zout = Zrows;
+    for (int k = 1; k <= L; ++k) {
+        int32_t a = dims[k - 1], b = dims[k];
+        const vec64 *zr = &chain[L - k];
+        double *Wk = weights_f64(seed, k, a, b);
+        double *AZ = (double *)malloc(sizeof(double) * (size_t)(zr->len * (int64_t)a + 1));
+        apply_rows(n, row_ptr, col, OP_PROP, a, Zprev, cslot[L - k + 1], NULL, two_e, zr->v, zr->len, AZ);
+        double *Zk = (double *)malloc(sizeof(double) * (size_t)(zr->len * (int64_t)b + 1));
+        for (int64_t q = 0; q < zr->len; ++q) {
+            double *h = Zk + q * (int64_t)b;
+            for (int32_t c = 0; c < b; ++c) {
+                double acc = 0.0;
+                for (int32_t t = 0; t < a; ++t) acc += AZ[q * (int64_t)a + t] * Wk[(int64_t)t * b + c];
+                h[c] = acc;
+            }
+            act_normalize(h, b);
+        }
+        for (int64_t s = 0; s < S; ++s)
+            memcpy(zout + s * (int64_t)b, Zk + (int64_t)cslot[L - k][rows[s]] * b, sizeof(double) * (size_t)b);
+        zout += S * (int64_t)b;
+        free(AZ);
+        free(Wk);
+        free(Zprev);
+        Zprev = Zk;
+    }
+    free(Zprev);
+    for (int k = 0; k <= L + 1; ++k) { free(chain[k].v); free(cslot[k]); }
+    free(chain);
+    free(cslot);
+    return 0;
+}
+
+/* ---------------------------------------------------------------- scoring */
+/* Eq. 3: Mod = (1/2e) sum_r sum_{i,j in C_r} [A_ij - d_i d_j / 2e]
+ *            = sum_r [ (sum_{i,j in C_r} A_ij) / 2e - (sum_{i in C_r} d_i)^2 / (2e)^2 ]. */
+int oracle_modularity(int64_t n, const int64_t *row_ptr, const int32_t *col, const int32_t *assign, int32_t k,
+                      double *out) {
+    if (k <= 0) return 2;
+    for (int64_t i = 0; i < n; ++i) if (assign[i] < 0 || assign[i] >= k) return 2;
+    double two_e = (double)row_ptr[n];
+    if (two_e == 0.0) return 3;
+    double *in_sum = (double *)calloc((size_t)k, sizeof(double)), *vol = (double *)calloc((size_t)k, sizeof(double));
+    for (int64_t i = 0; i < n; ++i) {
+        vol[assign[i]] += (double)deg_of(row_ptr, i);
+        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p)
+            if (assign[col[p]] == assign[i]) in_sum[assign[i]] += 1.0;
+    }
+    double q = 0.0;
+    for (int32_t c = 0; c < k; ++c) q += in_sum[c] / two_e - (vol[c] / two_e) * (vol[c] / two_e);
+    free(in_sum);
+    free(vol);
+    *out = q;
+    return 0;
+}
+
+/* Eq. 1: NCut = 1/2 sum_r cut(C_r, V - C_r) / vol(C_r); a block with vol = 0 contributes 0 (reading #17). */
+int oracle_ncut(int64_t n, const int64_t *row_ptr, const int32_t *col, const int32_t *assign, int32_t k,
+                double *out) {
+    if (k <= 0) return 2;
+    for (int64_t i = 0; i < n; ++i) if (assign[i] < 0 || assign[i] >= k) return 2;
+    double *cut = (double *)calloc((size_t)k, sizeof(double)), *vol = (double *)calloc((size_t)k, sizeof(double));
+    for (int64_t i = 0; i < n; ++i) {
+        vol[assign[i]] += (double)deg_of(row_ptr, i);
+        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p)
+            if (assign[col[p]] != assign[i]) cut[assign[i]] += 1.0;
+    }
+    double s = 0.0;
+    for (int32_t c = 0; c < k; ++c) if (vol[c] > 0.0) s += cut[c] / vol[c];
+    free(cut);
+    free(vol);
+    *out = 0.5 * s;
+    return 0;
+}
+
+/* Eq. 7: LMod(U_1..U_K; G) = sum_r [ m_r / e - (mbar_r / 2e)^2 ], m_r = #edges of G inside U_r,
+ * mbar_r = sum_{v in U_r} deg_G(v) (full-graph degree), 2e = sum_r mbar_r. */
+int oracle_local_modularity(int64_t n, const int64_t *row_ptr, const int32_t *col, const int64_t *nodes,
+                            int64_t count, const int32_t *block_of_node, int32_t k, double *out) {
+    if (k <= 0 || count < 0) return 2;
+    int32_t *blk = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n + 1));
+    for (int64_t i = 0; i < n; ++i) blk[i] = -1;
+    for (int64_t t = 0; t < count; ++t) {
+        if (nodes[t] < 0 || nodes[t] >= n || block_of_node[t] < 0 || block_of_node[t] >= k || blk[nodes[t]] >= 0) {
+            free(blk);
+            return 2;
+        }
+        blk[nodes[t]] = block_of_node[t];
+    }
+    double *m2 = (double *)calloc((size_t)k, sizeof(double)), *mbar = (double *)calloc((size_t)k, sizeof(double));
+    for (int64_t t = 0; t < count; ++t) {
+        int64_t i = nodes[t];
+        mbar[blk[i]] += (double)deg_of(row_ptr, i);
+        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p)
+            if (blk[col[p]] == blk[i]) m2[blk[i]] += 1.0;   /* counts each intra edge twice */
+    }
+    double two_e = 0.0;
+    for (int32_t c = 0; c < k; ++c) two_e += mbar[c];
+    int rc = 0;
+    if (two_e == 0.0) rc = 3;
+    else {
+        double e = two_e / 2.0, q = 0.0;
+        for (int32_t c = 0; c < k; ++c) q += (m2[c] / 2.0) / e - (mbar[c] / two_e) * (mbar[c] / two_e);
+        *out = q;
+    }
+    free(blk);
+    free(m2);
+    free(mbar);
+    return rc;
+}

@@ -1,0 +1,21 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (CUDA) — run on the GPU box")
+    config.addinivalue_line("markers", "slow: long-running (large configs)")
+
+
+@pytest.fixture(scope="session")
+def cuda_required():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("gpu test collected on a machine without CUDA")
+    return torch.device("cuda:0")
