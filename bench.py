@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""Benchmark of the RaftGP embedding hot path (BASELINE.json metric) on 1..8 B200s.
+
+One step = the whole hot path over one synthetic DC-SBM graph resident in HBM:
+canonical CSR build + degree pass (a1, a2), Gaussian sketch (a3), feature hop (a4) and the GCN hops with
+fused epilogues (a5) for BOTH feature operators (NCut M and modularity Q; north_star (i)), plus the per-hop
+all-gather (a6) when N > 1. value = work units / time, units = sum over variants and hops of
+(gathered rows G_h) x (gathered width w_h) ("nnz*r").
+
+Prints ONE JSON line on rank 0. `--impl reference` times the CPU oracle instead (the reference arm for
+this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "embedding nnz*r/s and achieved HBM GB/s vs roofline at 1/2/4/8 B200"
+UNIT = "nnz*r/s"
+L2_BYTES = 126 * 2 ** 20
+SAMPLE_N = 50_000      # oracle sample: the same DC-SBM recipe at 1/100 of C4's nodes
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="raftgp", choices=["raftgp", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--variants", default="ncut,mod")
+    ap.add_argument("--rule", default="stated", choices=["stated", "law"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([x.strip() for x in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def work_units(nnz, n, r, dims, nvar):
+    """sum_h G_h * w_h per step: feature hop gathers nnz rows of width r; GCN hop k gathers nnz + n rows
+    of width dims[k] (GEMM-first: the operand of hop k is T_k = s^ (.) Z^(k-1) W^(k), dims[k] wide)."""
+    u = nnz * r
+    for k in range(1, len(dims)):
+        u += (nnz + n) * dims[k]
+    return nvar * u
+
+
+def algorithmic_bytes(nnz, n, r, dims, nvar, kernel):
+    """SURVEY.md §8(d) gather model per launch, summed over one step's launches of that kernel:
+    B_h = 8(N+1) + 4 nnz + 4 w_h G_h + 4 w'_h N + 4 N."""
+    L = len(dims) - 1
+    if kernel == "feature_hop":
+        b = 8 * (n + 1) + 4 * nnz + 4 * r * nnz + 4 * dims[1] * n + 4 * n
+        return nvar * b, nvar
+    if kernel == "gcn_hop":
+        b = 0
+        for k in range(1, L + 1):
+            w_out = dims[k + 1] if k < L else dims[L]
+            b += 8 * (n + 1) + 4 * nnz + 4 * dims[k] * (nnz + n) + 4 * w_out * n + 4 * n
+        return nvar * b, nvar * L
+    return None, None
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def host_info():
+    info = {"cores": os.cpu_count()}
+    try:
+        info["cpu"] = [l.split(":", 1)[1].strip() for l in subprocess.run(["lscpu"], capture_output=True, text=True)
+                       .stdout.splitlines() if l.startswith("Model name")][0]
+    except Exception:
+        pass
+    try:
+        info["mem_gb"] = int(subprocess.run(["free", "-g"], capture_output=True, text=True).stdout.splitlines()[1]
+                             .split()[1])
+    except Exception:
+        pass
+    return info
+
+
+# ------------------------------------------------------------------ oracle (cpu baseline / reference arm)
+def oracle_step(gr, variants, r, dims, seed):
+    import oracle
+    t0 = time.perf_counter()
+    g = oracle.build_csr(gr.n, gr.src, gr.dst)
+    for v in variants:
+        Y = oracle.project(g, v, r, seed)
+        oracle.gcn(g, dims, seed, Y)
+    return time.perf_counter() - t0, g.nnz
+
+
+def cpu_baseline(cfg, variants, seed, rule, steps=1):
+    import synth
+    gr = synth.generate(cfg, seed, rule=rule, n=SAMPLE_N)
+    times, nnz = [], 0
+    for _ in range(steps):
+        dt, nnz = oracle_step(gr, variants, cfg.r, cfg.dims, seed)
+        times.append(dt)
+    units = work_units(nnz, gr.n, cfg.r, cfg.dims, len(variants))
+    return units / statistics.mean(times), gr, nnz, times
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import synth
+    cfg = synth.CONFIGS[args.config]
+    variants = args.variants.split(",")
+    import oracle
+    oracle.build()
+    synth.build()
+    gr = synth.generate(cfg, args.seed, rule=args.rule, n=SAMPLE_N)
+    for _ in range(args.warmup):
+        oracle_step(gr, variants, cfg.r, cfg.dims, args.seed)
+    times, nnz = [], 0
+    for _ in range(args.steps):
+        dt, nnz = oracle_step(gr, variants, cfg.r, cfg.dims, args.seed)
+        times.append(dt)
+    units = work_units(nnz, gr.n, cfg.r, cfg.dims, len(variants))
+    total = sum(times)
+    value = units * args.steps / total
+    sample = (f"full oracle step (CSR build + both variants' projection + GCN) on the {cfg.name} DC-SBM recipe "
+              f"at N={gr.n} (nnz={nnz}), single thread")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name} recipe sample, N={gr.n}", "n": gr.n, "nnz": nnz, "r": cfg.r,
+                   "dims": list(cfg.dims), "variants": variants, "rule": args.rule},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "host": host_info(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import synth
+    from paper_2312_01560_b200 import build as _build
+    from paper_2312_01560_b200 import dist as rdist
+    from paper_2312_01560_b200 import raftgp as rg
+
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as tdist
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    if rank == 0:
+        _build.build()
+    if world > 1:
+        tdist.barrier()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cfg = synth.CONFIGS[args.config]
+    variants = args.variants.split(",")
+    dims = tuple(cfg.dims)
+    gr = synth.generate(cfg, args.seed, rule=args.rule)
+    m = gr.src.size
+    src_h = torch.from_numpy(gr.src).pin_memory()
+    dst_h = torch.from_numpy(gr.dst).pin_memory()
+    src_d, dst_d = src_h.to(dev), dst_h.to(dev)
+    ctx = rg.Context(dev.index)
+    stream = ctx.stream
+    ranges, _ = rdist.row_partition(gr.n, world)
+    rb, re = ranges[rank]
+    rows = re - rb
+    Zbuf = {v: torch.empty((rows, dims[-1]), dtype=torch.float32, device=dev) for v in variants}
+
+    def step_single(src, dst, out_host=None):
+        g = rg.raftgp_build_csr(ctx, gr.n, src, dst)
+        for v in variants:
+            rg.raftgp_embed(g, v, dims, args.seed, Z=Zbuf[v], want_Y=False)
+            if out_host is not None:
+                out_host[v].copy_(Zbuf[v], non_blocking=True)
+        nnz = g.info()["nnz_local"]
+        g.close()
+        return nnz
+
+    def step_multi(src, dst, out_host=None):
+        keep = {}
+        gen = rdist.rank_pipeline(rdist.CudaEngine(ctx), gr.n, src, dst, rank, world, variants, dims, args.seed, keep)
+        Z = rdist.run_distributed(gen)
+        for v in variants:
+            Zbuf[v].copy_(Z[v])
+            if out_host is not None:
+                out_host[v].copy_(Z[v], non_blocking=True)
+        nnz = keep["graph"].info()["nnz_local"]
+        keep["graph"].close()
+        return nnz
+
+    step = step_single if world == 1 else step_multi
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            tdist.barrier()
+            torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t)
+        return float(t.item())
+
+    # ---------------- warm-up
+    nnz_local = 0
+    for _ in range(max(3, args.warmup)):
+        nnz_local = step(src_d, dst_d)
+    nnz = int(sum_over_ranks(nnz_local))
+    # ---------------- timed region (device-resident inputs)
+    ctx.prof_reset()
+    ctx.set_profiling(True)
+    ctx.launch_count(reset=True)
+    barrier()
+    with ClockSampler(dev.index) as clocks:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            step(src_d, dst_d)
+        t1.record(stream)
+        barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    launches = ctx.launch_count()
+    prof = ctx.prof_read()
+    ctx.set_profiling(False)
+    ms_max = max_over_ranks(ms)
+    units = work_units(nnz, gr.n, cfg.r, dims, len(variants))
+    value = units / (ms_max * 1e-3)
+
+    # ---------------- roofline of the dominant kernel (of this rank's launches)
+    peak, peak_src = measured_peak()
+    kernel_times = {k: v[0] / args.steps for k, v in prof.items()}        # ms per step
+    dom = max((k for k in prof if k in ("feature_hop", "gcn_hop")), key=lambda k: prof[k][0], default=None)
+    roof = None
+    hop_stats = {}
+    for k in ("feature_hop", "gcn_hop"):
+        if k not in prof:
+            continue
+        b_step, l_step = algorithmic_bytes(nnz if world == 1 else nnz_local, rows if world > 1 else gr.n, cfg.r, dims,
+                                           len(variants), k)
+        t_step = prof[k][0] / args.steps * 1e-3
+        ach = b_step / t_step / 1e9
+        hop_stats[k] = {"gb_s": ach, "ms_per_step": t_step * 1e3, "launches_per_step": prof[k][1] / args.steps,
+                        "bytes_per_launch": b_step / l_step}
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if dom and os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get(args.config, {}).get(dom)
+        except Exception:
+            traffic = None
+    if dom:
+        ach = hop_stats[dom]["gb_s"]
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "peak_source": peak_src, "frac_of_8TBs_nominal": ach / 8000.0, "traffic": traffic,
+                "bytes_per_launch": hop_stats[dom]["bytes_per_launch"]}
+
+    # ---------------- e2e through the C-ABI with host buffers (H2D of edges, D2H of Z inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        out_host = {v: torch.empty((rows, dims[-1]), dtype=torch.float32).pin_memory() for v in variants}
+        step(src_h, dst_h, out_host)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step(src_h, dst_h, out_host)
+        e1.record(stream)
+        barrier()
+        ems = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+        e2e = {"value": units / (ems * 1e-3), "unit": UNIT, "ms_per_step": ems, "h2d_bytes_per_step": 8 * m,
+               "d2h_bytes_per_step": int(sum(rows * dims[-1] * 4 for _ in variants))}
+
+    # ---------------- CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        v, sg, snnz, times = cpu_baseline(cfg, variants, args.seed, args.rule)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": (f"full oracle step (CSR build + {'/'.join(variants)} projection + GCN {list(dims)}) on the "
+                          f"{cfg.name} DC-SBM recipe at N={sg.n} (nnz={snnz}); {times[0]:.2f} s, single thread, fp64"),
+               "host": host_info()}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: DC-SBM N={gr.n:,} K={gr.info['k']} nnz={nnz:,} r={cfg.r} "
+                                   f"dims={list(dims)} variants={'+'.join(variants)}",
+                       "n": gr.n, "nnz": nnz, "m_raw_pairs": m, "r": cfg.r, "dims": list(dims), "variants": variants,
+                       "rule": args.rule, "parallelism": f"rowpart{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (gathered operands >= 1.28 GB vs 126 MB L2); no flush"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "kernels_ms_per_step": {k: round(v, 4) for k, v in sorted(kernel_times.items(), key=lambda x: -x[1])},
+            "hops": hop_stats,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,185 @@
+/*
+ * raftgp.h — C-ABI of the B200-native RaftGP embedding hot path (arxiv 2312.01560).
+ *
+ * The path: canonical CSR build (a1) -> degree/normalisation pass (a2) ->
+ * Gaussian sketch (a3) -> feature hop Y = X Theta (a4, Eq. 5) -> untrained GCN hops with fused
+ * tanh / row-l2 / next-layer transform (a5, Eq. 6) -> [per-hop all-gather when row-partitioned (a6)]
+ * -> host scoring (a7, Eq. 1/3/7). Every compute step runs in this library's sm_100a kernels.
+ *
+ * Conventions for every entry point
+ *  - Plain C types only. "dev" pointers are CUDA device pointers on the context's device; "host"
+ *    pointers are ordinary host memory. Dense matrices are fp32, row-major, contiguous (row stride =
+ *    width). Fast kernels are used when a matrix pointer is 16-byte aligned and its width is 32, 64 or
+ *    128; other widths/alignments take a slower generic kernel with the same results up to rounding.
+ *  - Asynchrony: calls enqueue work on the context's stream and return; outputs are valid after the
+ *    caller synchronises that stream (raftgp_ctx_sync). Exceptions are noted ("synchronous").
+ *  - Ownership: the library owns raftgp_ctx and raftgp_graph handles and the graph's device CSR. The
+ *    caller owns every array passed in. Device inputs must stay valid until the stream work completes.
+ *  - Errors: every function returns raftgp_status; on non-OK, raftgp_last_error() holds a message for
+ *    the calling thread. No C++ exception crosses this ABI. Handles are not thread-safe.
+ *  - Multi-GPU: one process and one context per GPU. A graph may hold only the rows [row_begin,
+ *    row_end) of the global CSR (1-D row partition); column ids are always global. Row-indexed
+ *    outputs (Y, Z, T) hold the local rows only. The exchange between hops (all-gather of the next
+ *    operand) is done by the caller (paper_2312_01560_b200/dist.py, torch.distributed/NCCL).
+ */
+#ifndef RAFTGP_H
+#define RAFTGP_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define RAFTGP_API __attribute__((visibility("default")))
+#else
+#define RAFTGP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct raftgp_ctx_s *raftgp_ctx;     /* device + stream + profiling state; library-owned */
+typedef struct raftgp_graph_s *raftgp_graph; /* device CSR (local rows) + degree scalars; library-owned */
+
+typedef enum {
+    RAFTGP_OK = 0,
+    RAFTGP_ERR_PARAM = 2,    /* bad argument: r <= 0, dims <= 0, bad variant, label out of [0,k), ... */
+    RAFTGP_ERR_DATA = 3,     /* bad data: node id outside [0,n), 2e = 0 for MOD variants, zero degree sum */
+    RAFTGP_ERR_INTERNAL = 4,
+    RAFTGP_ERR_CUDA = 5,     /* a CUDA runtime call or kernel launch failed */
+    RAFTGP_ERR_NOMEM = 6,    /* device allocation failed */
+    RAFTGP_ERR_STATE = 7     /* handle not ready (e.g. partial graph without raftgp_graph_set_degrees) */
+} raftgp_status;
+
+/* The feature operator X of Eq. 5 ("X in {M, Q~}"; PAPER.md:289 RaftGP-C / RaftGP-M). */
+typedef enum {
+    RAFTGP_NCUT = 0,         /* X = M = D^-1/2 A D^-1/2; isolated rows give zero rows */
+    RAFTGP_MOD = 1,          /* X = Q = A - d d^T / 2e (Eq. 4), applied as A Theta minus the
+                                fused rank-1 term d (d^T Theta) / 2e; never materialised */
+    RAFTGP_MOD_REDUCED = 2   /* X = Q~ = Q on the edges of A, 0 elsewhere */
+} raftgp_variant;
+
+#define RAFTGP_HOST_PTRS 0u    /* edge arrays are host memory: copied to the device inside the call */
+#define RAFTGP_DEVICE_PTRS 1u  /* edge arrays are device memory on the context's device */
+
+/* ---------------------------------------------------------------- context */
+RAFTGP_API const char *raftgp_last_error(void);          /* thread-local message of the last non-OK status */
+RAFTGP_API const char *raftgp_version(void);
+
+/* device: CUDA ordinal. cuda_stream: a cudaStream_t to enqueue on (NULL = a new non-blocking stream
+ * owned by the context). */
+RAFTGP_API raftgp_status raftgp_ctx_create(int device, void *cuda_stream, raftgp_ctx *out);
+RAFTGP_API raftgp_status raftgp_ctx_destroy(raftgp_ctx ctx);
+RAFTGP_API raftgp_status raftgp_ctx_sync(raftgp_ctx ctx);                     /* synchronous */
+RAFTGP_API raftgp_status raftgp_ctx_stream(raftgp_ctx ctx, void **cuda_stream_out);
+
+/* Per-kernel device timing with CUDA events recorded around every launch on the ctx stream.
+ * raftgp_prof_read is synchronous; kernel ids are 0..raftgp_prof_kernels()-1. */
+RAFTGP_API raftgp_status raftgp_ctx_set_profiling(raftgp_ctx ctx, int enable);
+RAFTGP_API int raftgp_prof_kernels(void);
+RAFTGP_API const char *raftgp_prof_name(int kernel_id);
+RAFTGP_API raftgp_status raftgp_prof_read(raftgp_ctx ctx, int kernel_id, double *total_ms, int64_t *launches);
+RAFTGP_API raftgp_status raftgp_prof_reset(raftgp_ctx ctx);
+/* number of kernels this context has launched since creation (or since the last reset) */
+RAFTGP_API raftgp_status raftgp_launch_count(raftgp_ctx ctx, int64_t *out, int reset);
+
+/* ---------------------------------------------------------------- a1 + a2: CSR build, degrees
+ * Canonical CSR of the simple undirected graph given by m raw pairs (src[e], dst[e]) over n nodes
+ * (§II: A_ij = A_ji in {0,1}): pairs with u == v are dropped, both orientations are
+ * added, rows are sorted ascending and duplicates removed. Only the rows
+ * [row_begin, row_end) are kept (pass 0, n for the whole graph).
+ *   n: node count (ids in [0, n)), 0 <= n < 2^31.  m: pair count >= 0.
+ *   src, dst: int32[m], host or device per flags (RAFTGP_HOST_PTRS / RAFTGP_DEVICE_PTRS).
+ * Errors: PARAM (n, m or the range invalid), DATA (an id outside [0, n)), NOMEM, CUDA.
+ * Synchronous at its end (reads the local nnz and the data-error flag back).
+ * When the range is the whole graph the degree pass (a2) runs too: deg, 2e, s = deg^-1/2 (0 if
+ * deg = 0), s^ = (deg+1)^-1/2 over all n nodes. A partial graph is not usable by the compute calls
+ * until raftgp_graph_set_degrees has supplied the global degree vector. */
+RAFTGP_API raftgp_status raftgp_build_csr(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src, const int32_t *dst,
+                               int64_t row_begin, int64_t row_end, uint32_t flags, raftgp_graph *out);
+
+/* n, local rows, local nnz (entries of A in the local rows = sum of their degrees), 2e (global; -1
+ * while a partial graph has no global degrees yet). */
+RAFTGP_API raftgp_status raftgp_graph_info(raftgp_graph g, int64_t *n, int64_t *row_begin, int64_t *row_end,
+                                int64_t *nnz_local, int64_t *two_e);
+
+/* Copy the local CSR out (parity checks / host use). row_ptr: int64[rows+1] (local offsets from 0);
+ * col_idx: int32[nnz_local] (global ids); deg: int32[rows] local degrees. Any pointer may be NULL.
+ * flags: RAFTGP_HOST_PTRS (synchronous) or RAFTGP_DEVICE_PTRS (async, device buffers). */
+RAFTGP_API raftgp_status raftgp_graph_export(raftgp_graph g, int64_t *row_ptr, int32_t *col_idx, int32_t *deg, uint32_t flags);
+
+/* Local degrees of the rows [row_begin, row_end) into a device int32 buffer (async). */
+RAFTGP_API raftgp_status raftgp_graph_local_degrees(raftgp_graph g, int32_t *deg_dev);
+
+/* Multi-GPU degree pass (a2): deg_all_dev = device int32[n], the degrees of ALL n nodes (the
+ * concatenation of every rank's raftgp_graph_local_degrees). Computes 2e, s and s^ over all nodes. */
+RAFTGP_API raftgp_status raftgp_graph_set_degrees(raftgp_graph g, const int32_t *deg_all_dev);
+
+RAFTGP_API raftgp_status raftgp_graph_destroy(raftgp_graph g);
+
+/* ---------------------------------------------------------------- a3: Gaussian sketch
+ * rows x cols block (global rows row_begin..) of the generator of docs/SKETCH_SPEC.md: element (i,c)
+ * = z(seed, tag, i, c) * fp32(1/sqrt(den)), z a standard normal from Philox4x32-10 + Box-Muller.
+ * Theta of Eq. 5 is tag 0, den = r (variance 1/r, reading #2); W^(k) of
+ * Eq. 6 is tag k, den = fan-in (reading #4). out: device fp32 rows x cols. Bit-exact with the oracle. */
+RAFTGP_API raftgp_status raftgp_sketch(raftgp_ctx ctx, uint64_t seed, uint32_t tag, int64_t row_begin, int64_t rows,
+                            int32_t cols, int32_t den, float *out_dev);
+
+/* W^(k) of Eq. 6, untrained: fan_in x fan_out, tag k, den fan_in. */
+RAFTGP_API raftgp_status raftgp_weights(raftgp_ctx ctx, uint64_t seed, int32_t k, int32_t fan_in, int32_t fan_out,
+                             float *W_dev);
+
+/* ---------------------------------------------------------------- a4: feature hop (Eq. 5)
+ * Y = X Theta for the graph's local rows, Theta = raftgp_sketch(seed, tag 0, den r)
+ * over all n rows (generated inside the call; no exchange is needed across ranks).
+ *   NCUT:        Y_i = s_i sum_j s_j Theta_j
+ *   MOD:         Y_i = sum_j Theta_j - d_i g / 2e,  g = sum_{all j} d_j Theta_j (fp64, fixed order)
+ *   MOD_REDUCED: Y_i = sum_j (1 - d_i d_j / 2e) Theta_j
+ * Y_dev: device fp32 local_rows x r. Errors: PARAM (r <= 0, bad variant), DATA (2e = 0 and variant
+ * != NCUT), STATE (partial graph without degrees). Workspace: Theta (n x r fp32) is allocated from
+ * the stream-ordered pool and released at the end of the call. */
+RAFTGP_API raftgp_status raftgp_project(raftgp_graph g, raftgp_variant variant, int32_t r, uint64_t seed, float *Y_dev);
+
+/* ---------------------------------------------------------------- a5: GCN (Eq. 6 + l2 norm)
+ * Transform: T = s^ (.) (Z W) for the local rows: Z local_rows x lin, W lin x lout (device), T
+ * local_rows x lout. This is the "GEMM-first" half of Eq. 6: P Z W = s^ (.) ((A + I)(s^ (.) Z W)). */
+RAFTGP_API raftgp_status raftgp_gcn_transform(raftgp_graph g, const float *Z_dev, int32_t lin, const float *W_dev,
+                                   int32_t lout, float *T_dev);
+
+/* One GCN hop on the local rows: H_i = s^_i (T_i + sum_{j in N(i)} T_j) = (P Z W)_i,
+ * Z'_i = tanh(H_i) / ||tanh(H_i)||_2 (a zero row stays zero), then optionally the next transform
+ * T'_i = s^_i (Z'_i W_next).
+ *   T_full_dev: fp32 n x w, the operand for ALL n rows (on P > 1 ranks: the all-gathered block).
+ *   Z_out_dev: local_rows x w, or NULL.  W_next_dev: w x w_next, or NULL (w_next = 0).
+ *   T_next_dev: local_rows x w_next, or NULL. */
+RAFTGP_API raftgp_status raftgp_gcn_hop(raftgp_graph g, const float *T_full_dev, int32_t w, float *Z_out_dev,
+                             const float *W_next_dev, int32_t w_next, float *T_next_dev);
+
+/* The whole untrained GCN on one GPU (whole-graph handle): Z^(k) = rownorm(tanh(P Z^(k-1) W^(k))),
+ * Z^(0) = Y, k = 1..layers, W^(k) = raftgp_weights(seed, k, dims[k-1], dims[k]).
+ *   dims: host int32[layers+1], dims[0] = width of Y.  Y_dev: n x dims[0].  Z_dev: n x dims[layers].
+ *   Zk_dev: NULL, or host array of layers-1 device pointers receiving Z^(1..layers-1) (NULL entries
+ *   skipped). Workspace (T buffers) comes from the stream-ordered pool. */
+RAFTGP_API raftgp_status raftgp_gnn_embed(raftgp_graph g, int32_t layers, const int32_t *dims, uint64_t seed,
+                               const float *Y_dev, float *Z_dev, float *const *Zk_dev);
+
+/* project + gnn_embed in one call with the first transform fused into the feature-hop epilogue.
+ * Y_dev may be NULL (Y is then not written). Same arguments and errors as the two calls. */
+RAFTGP_API raftgp_status raftgp_embed(raftgp_graph g, raftgp_variant variant, int32_t layers, const int32_t *dims,
+                           uint64_t seed, float *Y_dev, float *Z_dev, float *const *Zk_dev);
+
+/* ---------------------------------------------------------------- a7: scoring (host, synchronous)
+ * On a whole-graph handle. assign: host int32[n] labels in [0, k).
+ * Modularity, Eq. 3. Errors: PARAM (label outside [0,k), k <= 0), DATA (2e = 0). */
+RAFTGP_API raftgp_status raftgp_modularity(raftgp_graph g, const int32_t *assign, int32_t k, double *out);
+/* NCut, Eq. 1; a block with vol = 0 contributes 0 (reading #17). */
+RAFTGP_API raftgp_status raftgp_ncut(raftgp_graph g, const int32_t *assign, int32_t k, double *out);
+/* Local modularity, Eq. 7 of the blocks U_1..U_k of U = nodes[0..count): node
+ * nodes[t] is in block block_of_node[t]; degrees are full-graph degrees, 2e = their sum over U.
+ * Errors: PARAM (duplicate or out-of-range node, label outside [0,k)), DATA (zero degree sum). */
+RAFTGP_API raftgp_status raftgp_local_modularity(raftgp_graph g, const int64_t *nodes, int64_t count,
+                                      const int32_t *block_of_node, int32_t k, double *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RAFTGP_H */

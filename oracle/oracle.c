@@ -102,21 +102,23 @@ void oracle_sincos_spec_batch(const uint32_t *k2, float *c, float *s, int64_t n)
     for (int64_t i = 0; i < n; ++i) sincos2pi_spec(k2[i], &c[i], &s[i]);
 }
 
-/* One Gaussian element per SKETCH_SPEC §1-§4 (computed independently per element, on purpose). */
-static float gaussian_element(uint64_t seed, uint32_t tag, uint64_t i, uint32_t col, float sigma) {
-    uint32_t ctr[4] = {col >> 2, (uint32_t)(i & 0xFFFFFFFFu), (uint32_t)(i >> 32), tag};
+/* The four consecutive elements (i, 4q..4q+3) of SKETCH_SPEC §1-§4, from one Philox call. */
+static void gaussian_quad(uint64_t seed, uint32_t tag, uint64_t i, uint32_t q, float sigma, float out[4]) {
+    uint32_t ctr[4] = {q, (uint32_t)(i & 0xFFFFFFFFu), (uint32_t)(i >> 32), tag};
     uint32_t key[2] = {(uint32_t)(seed & 0xFFFFFFFFu), (uint32_t)(seed >> 32)};
     uint32_t x[4];
     oracle_philox4x32_10(ctr, key, x);
-    uint32_t pair = (col & 3u) >> 1;
-    uint32_t xa = x[2 * pair], xb = x[2 * pair + 1];
-    float u1 = (float)((xa >> 8) + 1u) * 0x1p-24f;
-    uint32_t k2 = xb >> 8;
-    float R = sqrtf(-2.0f * ln_spec(u1));
-    float c, s;
-    sincos2pi_spec(k2, &c, &s);
-    float z = (col & 1u) ? R * s : R * c;
-    return z * sigma;
+    for (int pair = 0; pair < 2; ++pair) {
+        uint32_t xa = x[2 * pair], xb = x[2 * pair + 1];
+        float u1 = (float)((xa >> 8) + 1u) * 0x1p-24f;
+        uint32_t k2 = xb >> 8;
+        float R = sqrtf(-2.0f * ln_spec(u1));
+        float c, s;
+        sincos2pi_spec(k2, &c, &s);
+        float za = R * c, zb = R * s;
+        out[2 * pair] = za * sigma;
+        out[2 * pair + 1] = zb * sigma;
+    }
 }
 
 static float sigma_of(int32_t den) { return 1.0f / sqrtf((float)den); }
@@ -127,8 +129,11 @@ int oracle_gaussian(uint64_t seed, uint32_t tag, int64_t row_begin, int64_t rows
     if (rows < 0 || cols <= 0 || den <= 0 || row_begin < 0) return 2;
     float sigma = sigma_of(den);
     for (int64_t i = 0; i < rows; ++i)
-        for (int32_t c = 0; c < cols; ++c)
-            out[i * (int64_t)cols + c] = gaussian_element(seed, tag, (uint64_t)(row_begin + i), (uint32_t)c, sigma);
+        for (int32_t q = 0; 4 * q < cols; ++q) {
+            float v[4];
+            gaussian_quad(seed, tag, (uint64_t)(row_begin + i), (uint32_t)q, sigma, v);
+            for (int32_t c = 4 * q; c < cols && c < 4 * q + 4; ++c) out[i * (int64_t)cols + c] = v[c - 4 * q];
+        }
     return 0;
 }
 

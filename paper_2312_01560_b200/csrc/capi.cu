@@ -1,0 +1,563 @@
+// capi.cu — the extern "C" boundary of libraftgp (include/raftgp.h): contexts, graph handles, argument
+// checks, orchestration of the kernels in csr.cu / sketch.cu / spmm.cu, per-launch profiling, and the
+// host-side scoring functions (a7: Eq. 1, 3, 7).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "gauss.cuh"
+#include "internal.cuh"
+
+namespace raftgp {
+
+const char *const kKernelNames[K_NUM] = {
+    "csr_count", "scan", "csr_scatter", "csr_sort_warp", "csr_sort_block", "csr_compact", "degree_scalars",
+    "sketch", "g_partials", "g_final", "feature_hop", "transform", "gcn_hop", "hop_generic", "misc"};
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+raftgp_status fail(raftgp_status st, const std::string &msg) {
+    set_error(msg);
+    return st;
+}
+
+raftgp_status cuda_fail(cudaError_t e, const char *what) {
+    std::string m = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+    set_error(m);
+    return e == cudaErrorMemoryAllocation ? RAFTGP_ERR_NOMEM : RAFTGP_ERR_CUDA;
+}
+
+static cudaEvent_t take_event(raftgp_ctx ctx) {
+    if (!ctx->event_pool.empty()) {
+        cudaEvent_t e = ctx->event_pool.back();
+        ctx->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+LaunchScope::LaunchScope(raftgp_ctx c, int k) : ctx(c), kid(k) {
+    ctx->launches += 1;
+    if (ctx->prof) {
+        a = take_event(ctx);
+        b = take_event(ctx);
+        cudaEventRecord(a, ctx->stream);
+    }
+}
+
+LaunchScope::~LaunchScope() {
+    if (ctx->prof && a && b) {
+        cudaEventRecord(b, ctx->stream);
+        ctx->recs.push_back({kid, a, b});
+    }
+}
+
+raftgp_status dalloc(raftgp_ctx ctx, void **p, size_t bytes) {
+    cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 16, ctx->stream);
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        cudaGetLastError();
+        return cuda_fail(e, "cudaMallocAsync");
+    }
+    return RAFTGP_OK;
+}
+
+void dfree(raftgp_ctx ctx, void *p) {
+    if (p) cudaFreeAsync(p, ctx->stream);
+}
+
+}  // namespace raftgp
+
+using namespace raftgp;
+
+#define RG_GUARD_BEGIN try {
+#define RG_GUARD_END                                                      \
+    }                                                                     \
+    catch (const std::bad_alloc &) {                                      \
+        return fail(RAFTGP_ERR_NOMEM, "host allocation failed");          \
+    }                                                                     \
+    catch (...) {                                                         \
+        return fail(RAFTGP_ERR_INTERNAL, "unexpected C++ exception");    \
+    }
+
+static raftgp_status set_device(raftgp_ctx ctx) {
+    RG_CUDA(cudaSetDevice(ctx->device));
+    return RAFTGP_OK;
+}
+
+static raftgp_status need_ready(raftgp_graph g) {
+    if (!g) return fail(RAFTGP_ERR_PARAM, "null graph");
+    if (g->two_e < 0) return fail(RAFTGP_ERR_STATE, "partial graph: call raftgp_graph_set_degrees first");
+    return RAFTGP_OK;
+}
+
+extern "C" {
+
+const char *raftgp_last_error(void) { return g_last_error.c_str(); }
+
+const char *raftgp_version(void) { return "raftgp-b200 0.1 (sm_100a)"; }
+
+raftgp_status raftgp_ctx_create(int device, void *cuda_stream, raftgp_ctx *out) {
+    RG_GUARD_BEGIN
+    if (!out) return fail(RAFTGP_ERR_PARAM, "null out");
+    *out = nullptr;
+    int ndev = 0;
+    RG_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(RAFTGP_ERR_PARAM, "device ordinal out of range");
+    RG_CUDA(cudaSetDevice(device));
+    raftgp_ctx c = new raftgp_ctx_s();
+    c->device = device;
+    if (cuda_stream) {
+        c->stream = static_cast<cudaStream_t>(cuda_stream);
+    } else {
+        cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            delete c;
+            return cuda_fail(e, "cudaStreamCreate");
+        }
+        c->own_stream = true;
+    }
+    cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+    // keep freed blocks in the stream-ordered pool (hot calls then never hit the driver allocator)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    *out = c;
+    return RAFTGP_OK;
+    RG_GUARD_END
+}
+
+raftgp_status raftgp_ctx_destroy(raftgp_ctx ctx) {
+    if (!ctx) return RAFTGP_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto &r : ctx->recs) {
+        cudaEventDestroy(r.start);
+        cudaEventDestroy(r.stop);
+    }
+    for (auto e : ctx->event_pool) cudaEventDestroy(e);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return RAFTGP_OK;
+}
+
+raftgp_status raftgp_ctx_sync(raftgp_ctx ctx) {
+    if (!ctx) return fail(RAFTGP_ERR_PARAM, "null ctx");
+    RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RAFTGP_OK;
+}
+
+raftgp_status raftgp_ctx_stream(raftgp_ctx ctx, void **s) {
+    if (!ctx || !s) return fail(RAFTGP_ERR_PARAM, "null argument");
+    *s = ctx->stream;
+    return RAFTGP_OK;
+}
+
+raftgp_status raftgp_ctx_set_profiling(raftgp_ctx ctx, int enable) {
+    if (!ctx) return fail(RAFTGP_ERR_PARAM, "null ctx");
+    ctx->prof = enable != 0;
+    return RAFTGP_OK;
+}
+
+int raftgp_prof_kernels(void) { return K_NUM; }
+
+const char *raftgp_prof_name(int kid) { return (kid >= 0 && kid < K_NUM) ? kKernelNames[kid] : "?"; }
+
+raftgp_status raftgp_prof_read(raftgp_ctx ctx, int kid, double *total_ms, int64_t *launches) {
+    if (!ctx || kid < 0 || kid >= K_NUM) return fail(RAFTGP_ERR_PARAM, "bad ctx or kernel id");
+    RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    double t = 0;
+    int64_t c = 0;
+    for (auto &r : ctx->recs) {
+        if (r.kid != kid) continue;
+        float ms = 0;
+        RG_CUDA(cudaEventElapsedTime(&ms, r.start, r.stop));
+        t += ms;
+        c += 1;
+    }
+    if (total_ms) *total_ms = t;
+    if (launches) *launches = c;
+    return RAFTGP_OK;
+}
+
+raftgp_status raftgp_prof_reset(raftgp_ctx ctx) {
+    if (!ctx) return fail(RAFTGP_ERR_PARAM, "null ctx");
+    RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (auto &r : ctx->recs) {
+        ctx->event_pool.push_back(r.start);
+        ctx->event_pool.push_back(r.stop);
+    }
+    ctx->recs.clear();
+    return RAFTGP_OK;
+}
+
+raftgp_status raftgp_launch_count(raftgp_ctx ctx, int64_t *out, int reset) {
+    if (!ctx || !out) return fail(RAFTGP_ERR_PARAM, "null argument");
+    *out = ctx->launches;
+    if (reset) ctx->launches = 0;
+    return RAFTGP_OK;
+}
+
+// ---------------------------------------------------------------- graph
+raftgp_status raftgp_build_csr(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src, const int32_t *dst,
+                               int64_t row_begin, int64_t row_end, uint32_t flags, raftgp_graph *out) {
+    RG_GUARD_BEGIN
+    if (!ctx || !out) return fail(RAFTGP_ERR_PARAM, "null argument");
+    *out = nullptr;
+    if (n < 0 || n >= (int64_t)INT32_MAX || m < 0) return fail(RAFTGP_ERR_PARAM, "n must be in [0, 2^31-1), m >= 0");
+    if (row_begin < 0 || row_end < row_begin || row_end > n) return fail(RAFTGP_ERR_PARAM, "bad row range");
+    if (m > 0 && (!src || !dst)) return fail(RAFTGP_ERR_PARAM, "null edge arrays");
+    if (flags > 1u) return fail(RAFTGP_ERR_PARAM, "bad flags");
+    RG_TRY(set_device(ctx));
+    const int32_t *dsrc = src, *ddst = dst;
+    int32_t *tmp = nullptr;
+    if (flags == RAFTGP_HOST_PTRS && m > 0) {
+        RG_TRY(dalloc_t(ctx, &tmp, 2 * (size_t)m));
+        RG_CUDA(cudaMemcpyAsync(tmp, src, sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
+        RG_CUDA(cudaMemcpyAsync(tmp + m, dst, sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
+        dsrc = tmp;
+        ddst = tmp + m;
+    }
+    raftgp_graph g = new raftgp_graph_s();
+    g->ctx = ctx;
+    raftgp_status st = csr_build(ctx, n, m, dsrc, ddst, row_begin, row_end, g);
+    dfree(ctx, tmp);
+    if (st != RAFTGP_OK) {
+        std::string msg = g_last_error;
+        raftgp_graph_destroy(g);
+        set_error(msg);
+        return st;
+    }
+    *out = g;
+    return RAFTGP_OK;
+    RG_GUARD_END
+}
+
+raftgp_status raftgp_graph_info(raftgp_graph g, int64_t *n, int64_t *row_begin, int64_t *row_end, int64_t *nnz_local,
+                                int64_t *two_e) {
+    if (!g) return fail(RAFTGP_ERR_PARAM, "null graph");
+    if (n) *n = g->n;
+    if (row_begin) *row_begin = g->row_begin;
+    if (row_end) *row_end = g->row_end;
+    if (nnz_local) *nnz_local = g->nnz_local;
+    if (two_e) *two_e = g->two_e;
+    return RAFTGP_OK;
+}
+
+raftgp_status raftgp_graph_export(raftgp_graph g, int64_t *row_ptr, int32_t *col_idx, int32_t *deg, uint32_t flags) {
+    if (!g) return fail(RAFTGP_ERR_PARAM, "null graph");
+    if (flags > 1u) return fail(RAFTGP_ERR_PARAM, "bad flags");
+    RG_TRY(set_device(g->ctx));
+    const cudaMemcpyKind k = flags == RAFTGP_HOST_PTRS ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    cudaStream_t st = g->ctx->stream;
+    if (row_ptr) RG_CUDA(cudaMemcpyAsync(row_ptr, g->row_ptr, sizeof(int64_t) * (g->nl + 1), k, st));
+    if (col_idx && g->nnz_local) RG_CUDA(cudaMemcpyAsync(col_idx, g->col, sizeof(int32_t) * g->nnz_local, k, st));
+    if (deg && g->nl) RG_CUDA(cudaMemcpyAsync(deg, g->deg_local, sizeof(int32_t) * g->nl, k, st));
+    if (flags == RAFTGP_HOST_PTRS) RG_CUDA(cudaStreamSynchronize(st));
+    return RAFTGP_OK;
+}
+
+raftgp_status raftgp_graph_local_degrees(raftgp_graph g, int32_t *deg_dev) {
+    if (!g || (!deg_dev && g->nl)) return fail(RAFTGP_ERR_PARAM, "null argument");
+    RG_TRY(set_device(g->ctx));
+    if (g->nl)
+        RG_CUDA(cudaMemcpyAsync(deg_dev, g->deg_local, sizeof(int32_t) * g->nl, cudaMemcpyDeviceToDevice, g->ctx->stream));
+    return RAFTGP_OK;
+}
+
+raftgp_status raftgp_graph_set_degrees(raftgp_graph g, const int32_t *deg_all_dev) {
+    RG_GUARD_BEGIN
+    if (!g || (!deg_all_dev && g->n)) return fail(RAFTGP_ERR_PARAM, "null argument");
+    RG_TRY(set_device(g->ctx));
+    if (g->n)
+        RG_CUDA(cudaMemcpyAsync(g->deg_all, deg_all_dev, sizeof(int32_t) * g->n, cudaMemcpyDeviceToDevice, g->ctx->stream));
+    return degrees_finalize(g);
+    RG_GUARD_END
+}
+
+raftgp_status raftgp_graph_destroy(raftgp_graph g) {
+    if (!g) return RAFTGP_OK;
+    raftgp_ctx ctx = g->ctx;
+    cudaSetDevice(ctx->device);
+    dfree(ctx, g->row_ptr);
+    dfree(ctx, g->col);
+    dfree(ctx, g->deg_local);
+    dfree(ctx, g->deg_all);
+    dfree(ctx, g->s_all);
+    dfree(ctx, g->sh_all);
+    delete g;
+    return RAFTGP_OK;
+}
+
+// ---------------------------------------------------------------- sketch / weights
+raftgp_status raftgp_sketch(raftgp_ctx ctx, uint64_t seed, uint32_t tag, int64_t row_begin, int64_t rows, int32_t cols,
+                            int32_t den, float *out_dev) {
+    if (!ctx) return fail(RAFTGP_ERR_PARAM, "null ctx");
+    if (rows < 0 || cols <= 0 || den <= 0 || row_begin < 0) return fail(RAFTGP_ERR_PARAM, "bad sketch shape");
+    if (rows > 0 && !out_dev) return fail(RAFTGP_ERR_PARAM, "null output");
+    RG_TRY(set_device(ctx));
+    return sketch_fill(ctx, seed, tag, row_begin, rows, cols, den, out_dev);
+}
+
+raftgp_status raftgp_weights(raftgp_ctx ctx, uint64_t seed, int32_t k, int32_t fan_in, int32_t fan_out, float *W_dev) {
+    if (k < 1) return fail(RAFTGP_ERR_PARAM, "layer index k must be >= 1");
+    if (fan_in <= 0 || fan_out <= 0) return fail(RAFTGP_ERR_PARAM, "layer widths must be > 0");
+    return raftgp_sketch(ctx, seed, static_cast<uint32_t>(k), 0, fan_in, fan_out, fan_in, W_dev);
+}
+
+// ---------------------------------------------------------------- project / gcn
+static raftgp_status check_variant(raftgp_graph g, int variant, int32_t r) {
+    if (variant < 0 || variant > 2) return fail(RAFTGP_ERR_PARAM, "bad variant");
+    if (r <= 0) return fail(RAFTGP_ERR_PARAM, "r must be > 0");
+    if (variant != RAFTGP_NCUT && g->two_e == 0)
+        return fail(RAFTGP_ERR_DATA, "modularity operator needs at least one edge (2e = 0)");
+    return RAFTGP_OK;
+}
+
+// Theta (+ g for MOD) into pool workspace; caller frees
+static raftgp_status make_theta(raftgp_graph g, int variant, int32_t r, uint64_t seed, float **theta, double **gvec) {
+    raftgp_ctx ctx = g->ctx;
+    *theta = nullptr;
+    *gvec = nullptr;
+    RG_TRY(dalloc_t(ctx, theta, (size_t)g->n * r));
+    if (variant == RAFTGP_MOD) RG_TRY(dalloc_t(ctx, gvec, (size_t)r));
+    return sketch_theta(g, seed, r, *theta, *gvec);
+}
+
+raftgp_status raftgp_project(raftgp_graph g, raftgp_variant variant, int32_t r, uint64_t seed, float *Y_dev) {
+    RG_GUARD_BEGIN
+    RG_TRY(need_ready(g));
+    RG_TRY(check_variant(g, variant, r));
+    if (g->nl > 0 && !Y_dev) return fail(RAFTGP_ERR_PARAM, "null Y");
+    RG_TRY(set_device(g->ctx));
+    float *theta = nullptr;
+    double *gvec = nullptr;
+    raftgp_status st = make_theta(g, variant, r, seed, &theta, &gvec);
+    if (st == RAFTGP_OK) st = feature_hop(g, variant, r, theta, gvec, Y_dev, nullptr, 0, nullptr);
+    dfree(g->ctx, theta);
+    dfree(g->ctx, gvec);
+    return st;
+    RG_GUARD_END
+}
+
+raftgp_status raftgp_gcn_transform(raftgp_graph g, const float *Z_dev, int32_t lin, const float *W_dev, int32_t lout,
+                                   float *T_dev) {
+    RG_GUARD_BEGIN
+    RG_TRY(need_ready(g));
+    if (lin <= 0 || lout <= 0) return fail(RAFTGP_ERR_PARAM, "widths must be > 0");
+    if (g->nl > 0 && (!Z_dev || !W_dev || !T_dev)) return fail(RAFTGP_ERR_PARAM, "null argument");
+    RG_TRY(set_device(g->ctx));
+    return gcn_transform(g, Z_dev, lin, W_dev, lout, T_dev);
+    RG_GUARD_END
+}
+
+raftgp_status raftgp_gcn_hop(raftgp_graph g, const float *T_full_dev, int32_t w, float *Z_out_dev,
+                             const float *W_next_dev, int32_t w_next, float *T_next_dev) {
+    RG_GUARD_BEGIN
+    RG_TRY(need_ready(g));
+    if (w <= 0) return fail(RAFTGP_ERR_PARAM, "width must be > 0");
+    if (W_next_dev && (w_next <= 0 || !T_next_dev)) return fail(RAFTGP_ERR_PARAM, "W_next needs w_next > 0 and T_next");
+    if (g->nl > 0 && !T_full_dev) return fail(RAFTGP_ERR_PARAM, "null T_full");
+    RG_TRY(set_device(g->ctx));
+    return gcn_hop(g, T_full_dev, w, Z_out_dev, W_next_dev, W_next_dev ? w_next : 0, W_next_dev ? T_next_dev : nullptr);
+    RG_GUARD_END
+}
+
+static raftgp_status check_dims(int32_t layers, const int32_t *dims) {
+    if (layers < 1 || !dims) return fail(RAFTGP_ERR_PARAM, "layers must be >= 1");
+    for (int k = 0; k <= layers; ++k)
+        if (dims[k] <= 0) return fail(RAFTGP_ERR_PARAM, "every layer width must be > 0");
+    return RAFTGP_OK;
+}
+
+// GCN layers 1..L given T1 = s^ (.) (Y W1) already computed.
+static raftgp_status gcn_stack(raftgp_graph g, int32_t layers, const int32_t *dims, uint64_t seed, float *T1,
+                               float *Z_dev, float *const *Zk_dev) {
+    raftgp_ctx ctx = g->ctx;
+    std::vector<float *> Ws(layers + 1, nullptr);
+    raftgp_status st = RAFTGP_OK;
+    for (int k = 2; k <= layers && st == RAFTGP_OK; ++k) {
+        st = dalloc_t(ctx, &Ws[k], (size_t)dims[k - 1] * dims[k]);
+        if (st == RAFTGP_OK) st = sketch_fill(ctx, seed, (uint32_t)k, 0, dims[k - 1], dims[k], dims[k - 1], Ws[k]);
+    }
+    float *Tcur = T1;
+    for (int k = 1; k <= layers && st == RAFTGP_OK; ++k) {
+        float *Zout = (k == layers) ? Z_dev : (Zk_dev ? Zk_dev[k - 1] : nullptr);
+        float *Tnext = nullptr;
+        if (k < layers) st = dalloc_t(ctx, &Tnext, (size_t)g->n * dims[k + 1]);
+        if (st == RAFTGP_OK)
+            st = gcn_hop(g, Tcur, dims[k], Zout, k < layers ? Ws[k + 1] : nullptr, k < layers ? dims[k + 1] : 0, Tnext);
+        if (Tcur != T1) dfree(ctx, Tcur);
+        Tcur = Tnext;
+    }
+    if (Tcur != T1) dfree(ctx, Tcur);
+    for (auto w : Ws) dfree(ctx, w);
+    return st;
+}
+
+static raftgp_status whole_graph(raftgp_graph g) {
+    if (g->row_begin != 0 || g->row_end != g->n)
+        return fail(RAFTGP_ERR_PARAM, "this call needs a whole-graph handle (use raftgp_gcn_hop per rank)");
+    return RAFTGP_OK;
+}
+
+raftgp_status raftgp_gnn_embed(raftgp_graph g, int32_t layers, const int32_t *dims, uint64_t seed, const float *Y_dev,
+                               float *Z_dev, float *const *Zk_dev) {
+    RG_GUARD_BEGIN
+    RG_TRY(need_ready(g));
+    RG_TRY(whole_graph(g));
+    RG_TRY(check_dims(layers, dims));
+    if (g->n > 0 && (!Y_dev || !Z_dev)) return fail(RAFTGP_ERR_PARAM, "null Y or Z");
+    RG_TRY(set_device(g->ctx));
+    raftgp_ctx ctx = g->ctx;
+    float *W1 = nullptr, *T1 = nullptr;
+    raftgp_status st = dalloc_t(ctx, &W1, (size_t)dims[0] * dims[1]);
+    if (st == RAFTGP_OK) st = dalloc_t(ctx, &T1, (size_t)g->n * dims[1]);
+    if (st == RAFTGP_OK) st = sketch_fill(ctx, seed, 1u, 0, dims[0], dims[1], dims[0], W1);
+    if (st == RAFTGP_OK) st = gcn_transform(g, Y_dev, dims[0], W1, dims[1], T1);
+    if (st == RAFTGP_OK) st = gcn_stack(g, layers, dims, seed, T1, Z_dev, Zk_dev);
+    dfree(ctx, W1);
+    dfree(ctx, T1);
+    return st;
+    RG_GUARD_END
+}
+
+raftgp_status raftgp_embed(raftgp_graph g, raftgp_variant variant, int32_t layers, const int32_t *dims, uint64_t seed,
+                           float *Y_dev, float *Z_dev, float *const *Zk_dev) {
+    RG_GUARD_BEGIN
+    RG_TRY(need_ready(g));
+    RG_TRY(whole_graph(g));
+    RG_TRY(check_dims(layers, dims));
+    RG_TRY(check_variant(g, variant, dims[0]));
+    if (g->n > 0 && !Z_dev) return fail(RAFTGP_ERR_PARAM, "null Z");
+    RG_TRY(set_device(g->ctx));
+    raftgp_ctx ctx = g->ctx;
+    const int32_t r = dims[0];
+    float *theta = nullptr, *W1 = nullptr, *T1 = nullptr;
+    double *gvec = nullptr;
+    raftgp_status st = make_theta(g, variant, r, seed, &theta, &gvec);
+    if (st == RAFTGP_OK) st = dalloc_t(ctx, &W1, (size_t)dims[0] * dims[1]);
+    if (st == RAFTGP_OK) st = dalloc_t(ctx, &T1, (size_t)g->n * dims[1]);
+    if (st == RAFTGP_OK) st = sketch_fill(ctx, seed, 1u, 0, dims[0], dims[1], dims[0], W1);
+    if (st == RAFTGP_OK) st = feature_hop(g, variant, r, theta, gvec, Y_dev, W1, dims[1], T1);
+    dfree(ctx, theta);
+    dfree(ctx, gvec);
+    if (st == RAFTGP_OK) st = gcn_stack(g, layers, dims, seed, T1, Z_dev, Zk_dev);
+    dfree(ctx, W1);
+    dfree(ctx, T1);
+    return st;
+    RG_GUARD_END
+}
+
+// ---------------------------------------------------------------- a7: host scoring
+static raftgp_status host_mirror(raftgp_graph g) {
+    RG_TRY(whole_graph(g));
+    if (g->host_valid) return RAFTGP_OK;
+    g->h_row_ptr.resize(g->nl + 1);
+    g->h_col.resize(g->nnz_local);
+    RG_TRY(raftgp_graph_export(g, g->h_row_ptr.data(), g->h_col.data(), nullptr, RAFTGP_HOST_PTRS));
+    g->host_valid = true;
+    return RAFTGP_OK;
+}
+
+static raftgp_status check_labels(const int32_t *assign, int64_t n, int32_t k) {
+    if (k <= 0) return fail(RAFTGP_ERR_PARAM, "k must be > 0");
+    if (n > 0 && !assign) return fail(RAFTGP_ERR_PARAM, "null labels");
+    for (int64_t i = 0; i < n; ++i)
+        if (assign[i] < 0 || assign[i] >= k) return fail(RAFTGP_ERR_PARAM, "label outside [0, k)");
+    return RAFTGP_OK;
+}
+
+raftgp_status raftgp_modularity(raftgp_graph g, const int32_t *assign, int32_t k, double *out) {
+    RG_GUARD_BEGIN
+    if (!g || !out) return fail(RAFTGP_ERR_PARAM, "null argument");
+    RG_TRY(host_mirror(g));
+    RG_TRY(check_labels(assign, g->n, k));
+    const int64_t two_e = g->h_row_ptr[g->n];
+    if (two_e == 0) return fail(RAFTGP_ERR_DATA, "modularity of a graph without edges");
+    // per-block intra (directed) edge counts and volumes, Eq. 3 regrouped by block
+    std::vector<int64_t> intra(k, 0), vol(k, 0);
+    for (int64_t i = 0; i < g->n; ++i) {
+        const int32_t bi = assign[i];
+        vol[bi] += g->h_row_ptr[i + 1] - g->h_row_ptr[i];
+        for (int64_t p = g->h_row_ptr[i]; p < g->h_row_ptr[i + 1]; ++p) intra[bi] += (assign[g->h_col[p]] == bi);
+    }
+    const double e2 = static_cast<double>(two_e);
+    double q = 0.0;
+    for (int32_t b = 0; b < k; ++b) {
+        const double f = static_cast<double>(vol[b]) / e2;
+        q += static_cast<double>(intra[b]) / e2 - f * f;
+    }
+    *out = q;
+    return RAFTGP_OK;
+    RG_GUARD_END
+}
+
+raftgp_status raftgp_ncut(raftgp_graph g, const int32_t *assign, int32_t k, double *out) {
+    RG_GUARD_BEGIN
+    if (!g || !out) return fail(RAFTGP_ERR_PARAM, "null argument");
+    RG_TRY(host_mirror(g));
+    RG_TRY(check_labels(assign, g->n, k));
+    std::vector<int64_t> cut(k, 0), vol(k, 0);
+    for (int64_t i = 0; i < g->n; ++i) {
+        const int32_t bi = assign[i];
+        vol[bi] += g->h_row_ptr[i + 1] - g->h_row_ptr[i];
+        for (int64_t p = g->h_row_ptr[i]; p < g->h_row_ptr[i + 1]; ++p) cut[bi] += (assign[g->h_col[p]] != bi);
+    }
+    double s = 0.0;
+    for (int32_t b = 0; b < k; ++b)
+        if (vol[b] > 0) s += static_cast<double>(cut[b]) / static_cast<double>(vol[b]);
+    *out = 0.5 * s;
+    return RAFTGP_OK;
+    RG_GUARD_END
+}
+
+raftgp_status raftgp_local_modularity(raftgp_graph g, const int64_t *nodes, int64_t count, const int32_t *block_of_node,
+                                      int32_t k, double *out) {
+    RG_GUARD_BEGIN
+    if (!g || !out || count < 0 || (count > 0 && (!nodes || !block_of_node))) return fail(RAFTGP_ERR_PARAM, "bad argument");
+    if (k <= 0) return fail(RAFTGP_ERR_PARAM, "k must be > 0");
+    RG_TRY(host_mirror(g));
+    std::vector<int32_t> blk(g->n, -1);
+    for (int64_t t = 0; t < count; ++t) {
+        const int64_t v = nodes[t];
+        if (v < 0 || v >= g->n) return fail(RAFTGP_ERR_PARAM, "node outside [0, n)");
+        if (block_of_node[t] < 0 || block_of_node[t] >= k) return fail(RAFTGP_ERR_PARAM, "label outside [0, k)");
+        if (blk[v] >= 0) return fail(RAFTGP_ERR_PARAM, "node listed twice");
+        blk[v] = block_of_node[t];
+    }
+    std::vector<int64_t> intra(k, 0), mbar(k, 0);
+    for (int64_t t = 0; t < count; ++t) {
+        const int64_t v = nodes[t];
+        const int32_t b = blk[v];
+        mbar[b] += g->h_row_ptr[v + 1] - g->h_row_ptr[v];
+        for (int64_t p = g->h_row_ptr[v]; p < g->h_row_ptr[v + 1]; ++p) intra[b] += (blk[g->h_col[p]] == b);
+    }
+    int64_t two_e = 0;
+    for (int32_t b = 0; b < k; ++b) two_e += mbar[b];
+    if (two_e == 0) return fail(RAFTGP_ERR_DATA, "local modularity with zero total degree");
+    // Eq. 7: sum_r m_r / e - (mbar_r / 2e)^2 with m_r = intra_r / 2 (each intra edge seen from both ends)
+    const double e2 = static_cast<double>(two_e);
+    double q = 0.0;
+    for (int32_t b = 0; b < k; ++b) {
+        const double f = static_cast<double>(mbar[b]) / e2;
+        q += static_cast<double>(intra[b]) / e2 - f * f;
+    }
+    *out = q;
+    return RAFTGP_OK;
+    RG_GUARD_END
+}
+
+}  // extern "C"

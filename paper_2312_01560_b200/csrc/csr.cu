@@ -1,0 +1,465 @@
+// csr.cu — a1/a2 of the hot path: canonical CSR build of the simple undirected graph
+// and the degree / normalisation pass (deg, 2e, s = D^-1/2 for M, s^ = (D+I)^-1/2 for
+// Eq. 6's propagation matrix).
+//
+// Build pipeline (all on the ctx stream, one host sync at the end):
+//   count     : one pass over the raw pairs; int atomics count both orientations of every u != v pair
+//               whose row falls in [rb, re); ids outside [0, n) raise a device data-error flag.
+//   scan      : exclusive int64 scan of the raw counts -> raw_ptr.
+//   scatter   : second pass; atomic slot claim per row, writes the neighbour into col_raw.
+//   sort+dedup: per-row ascending sort and duplicate removal, in place inside the raw segment.
+//               Rows <= 32 entries: one warp, register bitonic network; rows <= 512: one warp, bitonic
+//               in shared memory; longer rows are deferred to a block-per-row kernel (shared memory up to
+//               24K entries, global memory beyond). The unique count is the degree.
+//   scan      : exclusive int64 scan of the degrees -> row_ptr.
+//   compact   : copies each row's unique prefix into the final col array.
+// The result is canonical (sorted, unique), hence independent of atomic ordering: bit-exact.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+
+#include "internal.cuh"
+
+namespace raftgp {
+
+namespace {
+
+constexpr int kScanBlock = 1024;
+constexpr int kScanItems = 8;   // elements per thread per tile
+constexpr int kWarpSortCap = 512;
+constexpr int kBlockSortSmemCap = 24576;   // ints (96 KB)
+
+__device__ __forceinline__ int64_t warp_incl_scan(int64_t v, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int64_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+// block-wide inclusive scan of one int64 per thread (blockDim = kScanBlock)
+__device__ __forceinline__ int64_t block_incl_scan(int64_t v, int64_t *sh_warp, int64_t &total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    v = warp_incl_scan(v, lane);
+    if (lane == 31) sh_warp[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        int64_t w = lane < (kScanBlock / 32) ? sh_warp[lane] : 0;
+        w = warp_incl_scan(w, lane);
+        sh_warp[lane] = w;
+    }
+    __syncthreads();
+    if (wid > 0) v += sh_warp[wid - 1];
+    total = sh_warp[kScanBlock / 32 - 1];
+    __syncthreads();
+    return v;
+}
+
+__global__ void __launch_bounds__(kScanBlock) scan_tile_sums(const int32_t *__restrict__ in, int64_t n,
+                                                            int64_t *__restrict__ tile_sums) {
+    __shared__ int64_t sh[32];
+    const int64_t tile = blockIdx.x;
+    const int64_t base = tile * (int64_t)kScanBlock * kScanItems;
+    int64_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        int64_t idx = base + (int64_t)k * kScanBlock + threadIdx.x;
+        if (idx < n) s += in[idx];
+    }
+    int64_t total;
+    block_incl_scan(s, sh, total);
+    if (threadIdx.x == 0) tile_sums[tile] = total;
+}
+
+// single block: exclusive scan of the tile sums in place, total written to tile_sums[ntiles]
+__global__ void __launch_bounds__(kScanBlock) scan_tile_offsets(int64_t *__restrict__ tile_sums, int64_t ntiles) {
+    __shared__ int64_t sh[32];
+    int64_t carry = 0;
+    for (int64_t base = 0; base < ntiles; base += kScanBlock) {
+        int64_t idx = base + threadIdx.x;
+        int64_t v = idx < ntiles ? tile_sums[idx] : 0;
+        int64_t total;
+        int64_t incl = block_incl_scan(v, sh, total);
+        if (idx < ntiles) tile_sums[idx] = carry + incl - v;
+        carry += total;
+    }
+    if (threadIdx.x == 0) tile_sums[ntiles] = carry;
+}
+
+__global__ void __launch_bounds__(kScanBlock) scan_apply(const int32_t *__restrict__ in, int64_t n,
+                                                        const int64_t *__restrict__ tile_off,
+                                                        int64_t *__restrict__ out) {
+    __shared__ int64_t sh[32];
+    const int64_t tile = blockIdx.x;
+    // each thread owns kScanItems CONSECUTIVE elements so the scan is in order
+    const int64_t base = tile * (int64_t)kScanBlock * kScanItems + (int64_t)threadIdx.x * kScanItems;
+    int32_t v[kScanItems];
+    int64_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        v[k] = (base + k < n) ? in[base + k] : 0;
+        s += v[k];
+    }
+    int64_t total;
+    int64_t incl = block_incl_scan(s, sh, total);
+    int64_t run = tile_off[tile] + incl - s;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        if (base + k < n) out[base + k] = run;
+        run += v[k];
+    }
+    if (tile == gridDim.x - 1 && threadIdx.x == 0) out[n] = tile_off[gridDim.x];
+}
+
+// ---------------------------------------------------------------- count / scatter
+__global__ void csr_count(const int32_t *__restrict__ src, const int32_t *__restrict__ dst, int64_t m, int64_t n,
+                          int64_t rb, int64_t re, int32_t *__restrict__ cnt, int *__restrict__ err) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+        const int32_t u = __ldg(src + e), v = __ldg(dst + e);
+        if (u < 0 || v < 0 || u >= n || v >= n) {
+            atomicOr(err, 1);
+            continue;
+        }
+        if (u == v) continue;
+        if (u >= rb && u < re) atomicAdd(cnt + (u - rb), 1);
+        if (v >= rb && v < re) atomicAdd(cnt + (v - rb), 1);
+    }
+}
+
+// cnt counts down to 0 again while slots are claimed
+__global__ void csr_scatter(const int32_t *__restrict__ src, const int32_t *__restrict__ dst, int64_t m, int64_t n,
+                            int64_t rb, int64_t re, const int64_t *__restrict__ raw_ptr, int32_t *__restrict__ cnt,
+                            int32_t *__restrict__ col_raw) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+        const int32_t u = __ldg(src + e), v = __ldg(dst + e);
+        if (u < 0 || v < 0 || u >= n || v >= n || u == v) continue;
+        if (u >= rb && u < re) {
+            const int32_t k = atomicSub(cnt + (u - rb), 1) - 1;
+            col_raw[raw_ptr[u - rb] + k] = v;
+        }
+        if (v >= rb && v < re) {
+            const int32_t k = atomicSub(cnt + (v - rb), 1) - 1;
+            col_raw[raw_ptr[v - rb] + k] = u;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- sort + dedup
+// In-place ascending bitonic sort of a[0..len) for ANY len, all stages ascending ("flip" form):
+// virtual +inf padding beyond len never moves, so no padding storage is needed.
+// Work is split over `nthr` threads with index t; `sync` is the barrier between stages.
+template <typename Sync>
+__device__ __forceinline__ void bitonic_any(int32_t *a, int len, int t, int nthr, Sync sync) {
+    int P = 1;
+    while (P < len) P <<= 1;
+    for (int k = 2; k <= P; k <<= 1) {
+        // flip stage: i in lower half of each k-block paired with its mirror
+        for (int x = t; x < P / 2; x += nthr) {
+            const int blk = x / (k / 2);
+            const int off = x % (k / 2);
+            const int i = blk * k + off;
+            const int j = blk * k + k - 1 - off;
+            if (j < len) {
+                int32_t ai = a[i], aj = a[j];
+                if (ai > aj) { a[i] = aj; a[j] = ai; }
+            }
+        }
+        sync();
+        for (int h = k / 4; h >= 1; h >>= 1) {
+            for (int x = t; x < P / 2; x += nthr) {
+                const int blk = x / h;
+                const int off = x % h;
+                const int i = blk * 2 * h + off;
+                const int j = i + h;
+                if (j < len) {
+                    int32_t ai = a[i], aj = a[j];
+                    if (ai > aj) { a[i] = aj; a[j] = ai; }
+                }
+            }
+            sync();
+        }
+    }
+}
+
+struct WarpSync {
+    __device__ __forceinline__ void operator()() const { __syncwarp(); }
+};
+struct BlockSync {
+    __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+
+// warp register bitonic sort of 32 values (ascending by lane)
+__device__ __forceinline__ int32_t warp_sort32(int32_t v, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j >= 1; j >>= 1) {
+            const int32_t o = __shfl_xor_sync(0xffffffffu, v, j);
+            const bool up = ((lane & k) == 0);
+            const bool lower = ((lane & j) == 0);
+            // lower partner keeps min when ascending block, max when descending
+            const int32_t mn = min(v, o), mx = max(v, o);
+            v = (lower == up) ? mn : mx;
+        }
+    }
+    return v;
+}
+
+// one warp per row; rows longer than kWarpSortCap are pushed to big_rows
+__global__ void __launch_bounds__(256) csr_sort_warp(int64_t nl, const int64_t *__restrict__ raw_ptr,
+                                                     int32_t *__restrict__ col_raw, int32_t *__restrict__ deg,
+                                                     int64_t *__restrict__ big_rows, int32_t *__restrict__ big_count) {
+    __shared__ int32_t sh[8][kWarpSortCap];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t warps = (int64_t)gridDim.x * 8;
+    for (int64_t row = (int64_t)blockIdx.x * 8 + wib; row < nl; row += warps) {
+        const int64_t beg = raw_ptr[row];
+        const int len = static_cast<int>(raw_ptr[row + 1] - beg);
+        int32_t *a = col_raw + beg;
+        if (len <= 32) {
+            int32_t v = lane < len ? a[lane] : INT_MAX;
+            v = warp_sort32(v, lane);
+            const int32_t prev = __shfl_up_sync(0xffffffffu, v, 1);
+            const bool keep = lane < len && (lane == 0 || v != prev);
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (keep) a[__popc(bal & ((1u << lane) - 1u))] = v;
+            if (lane == 0) deg[row] = __popc(bal);
+        } else if (len <= kWarpSortCap) {
+            int32_t *s = sh[wib];
+            for (int x = lane; x < len; x += 32) s[x] = a[x];
+            __syncwarp();
+            bitonic_any(s, len, lane, 32, WarpSync());
+            int written = 0;
+            for (int base = 0; base < len; base += 32) {
+                const int x = base + lane;
+                const int32_t v = x < len ? s[x] : INT_MAX;
+                const bool keep = x < len && (x == 0 || v != s[x - 1]);
+                const unsigned bal = __ballot_sync(0xffffffffu, keep);
+                if (keep) a[written + __popc(bal & ((1u << lane) - 1u))] = v;
+                written += __popc(bal);
+            }
+            if (lane == 0) deg[row] = written;
+            __syncwarp();
+        } else if (lane == 0) {
+            big_rows[atomicAdd(big_count, 1)] = row;
+        }
+    }
+}
+
+// one block (1024 threads) per long row
+__global__ void __launch_bounds__(1024) csr_sort_block(const int64_t *__restrict__ big_rows,
+                                                       const int32_t *__restrict__ big_count,
+                                                       const int64_t *__restrict__ raw_ptr,
+                                                       int32_t *__restrict__ col_raw, int32_t *__restrict__ deg) {
+    extern __shared__ int32_t smem[];
+    __shared__ int32_t wsum[32];
+    const int nb = *big_count;
+    for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+        const int64_t row = big_rows[b];
+        const int64_t beg = raw_ptr[row];
+        const int len = static_cast<int>(raw_ptr[row + 1] - beg);
+        int32_t *a = col_raw + beg;
+        int32_t *s = len <= kBlockSortSmemCap ? smem : a;
+        if (s == smem) {
+            for (int x = threadIdx.x; x < len; x += blockDim.x) s[x] = a[x];
+        }
+        __syncthreads();
+        bitonic_any(s, len, (int)threadIdx.x, (int)blockDim.x, BlockSync());
+        // dedup with a block scan over chunks of blockDim, writing in place (writes never pass reads)
+        int written = 0;
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        for (int base = 0; base < len; base += blockDim.x) {
+            const int x = base + threadIdx.x;
+            const int32_t v = x < len ? s[x] : INT_MAX;
+            const bool keep = x < len && (x == 0 || v != s[x - 1]);
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (lane == 0) wsum[wid] = __popc(bal);
+            __syncthreads();
+            int before = 0, total = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+                if (w < wid) before += wsum[w];
+                total += wsum[w];
+            }
+            __syncthreads();   // all reads of s[x-1] in this chunk done before anyone writes
+            if (keep) a[written + before + __popc(bal & ((1u << lane) - 1u))] = v;
+            written += total;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) deg[row] = written;
+        __syncthreads();
+    }
+}
+
+__global__ void csr_compact(int64_t nl, const int64_t *__restrict__ raw_ptr, const int32_t *__restrict__ col_raw,
+                            const int64_t *__restrict__ row_ptr, int32_t *__restrict__ col) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < nl; row += warps) {
+        const int64_t src = raw_ptr[row], dst = row_ptr[row];
+        const int len = static_cast<int>(row_ptr[row + 1] - dst);
+        for (int x = lane; x < len; x += 32) col[dst + x] = col_raw[src + x];
+    }
+}
+
+// deg_all -> s, s^ ; two_e = sum deg (int64) via one atomic per block
+__global__ void degree_scalars(const int32_t *__restrict__ deg, int64_t n, float *__restrict__ s,
+                               float *__restrict__ sh, unsigned long long *__restrict__ two_e) {
+    __shared__ unsigned long long part;
+    if (threadIdx.x == 0) part = 0;
+    __syncthreads();
+    unsigned long long local = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const int32_t d = deg[i];
+        local += static_cast<unsigned long long>(d);
+        s[i] = d > 0 ? __frsqrt_rn(static_cast<float>(d)) : 0.0f;
+        sh[i] = __frsqrt_rn(static_cast<float>(d) + 1.0f);
+    }
+    atomicAdd(&part, local);
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(two_e, part);
+}
+
+}  // namespace
+
+raftgp_status scan_i32_to_i64(raftgp_ctx ctx, const int32_t *in, int64_t *out, int64_t n) {
+    const int64_t per_tile = (int64_t)kScanBlock * kScanItems;
+    const int64_t ntiles = n > 0 ? ceil_div(n, per_tile) : 0;
+    if (ntiles == 0) {
+        RG_CUDA(cudaMemsetAsync(out, 0, sizeof(int64_t), ctx->stream));
+        return RAFTGP_OK;
+    }
+    int64_t *tiles = nullptr;
+    RG_TRY(dalloc_t(ctx, &tiles, ntiles + 1));
+    {
+        LaunchScope L(ctx, K_SCAN);
+        scan_tile_sums<<<(unsigned)ntiles, kScanBlock, 0, ctx->stream>>>(in, n, tiles);
+    }
+    RG_CHECK_LAUNCH(ctx);
+    {
+        LaunchScope L(ctx, K_SCAN);
+        scan_tile_offsets<<<1, kScanBlock, 0, ctx->stream>>>(tiles, ntiles);
+    }
+    RG_CHECK_LAUNCH(ctx);
+    {
+        LaunchScope L(ctx, K_SCAN);
+        scan_apply<<<(unsigned)ntiles, kScanBlock, 0, ctx->stream>>>(in, n, tiles, out);
+    }
+    RG_CHECK_LAUNCH(ctx);
+    dfree(ctx, tiles);
+    return RAFTGP_OK;
+}
+
+raftgp_status degrees_finalize(raftgp_graph g) {
+    raftgp_ctx ctx = g->ctx;
+    unsigned long long *d_two_e = nullptr;
+    RG_TRY(dalloc_t(ctx, &d_two_e, 1));
+    RG_CUDA(cudaMemsetAsync(d_two_e, 0, sizeof(unsigned long long), ctx->stream));
+    if (g->n > 0) {
+        const int grid = static_cast<int>(std::min<int64_t>(ceil_div(g->n, 256), (int64_t)ctx->sm_count * 8));
+        LaunchScope L(ctx, K_DEGREES);
+        degree_scalars<<<grid, 256, 0, ctx->stream>>>(g->deg_all, g->n, g->s_all, g->sh_all, d_two_e);
+    }
+    RG_CHECK_LAUNCH(ctx);
+    unsigned long long h = 0;
+    RG_CUDA(cudaMemcpyAsync(&h, d_two_e, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    dfree(ctx, d_two_e);
+    g->two_e = static_cast<int64_t>(h);
+    return RAFTGP_OK;
+}
+
+raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src, const int32_t *dst, int64_t rb,
+                        int64_t re, raftgp_graph g) {
+    cudaStream_t st = ctx->stream;
+    const int64_t nl = re - rb;
+    g->n = n;
+    g->row_begin = rb;
+    g->row_end = re;
+    g->nl = nl;
+    const int64_t cap = 2 * m;   // upper bound of raw entries in any row range
+    int32_t *cnt = nullptr, *col_raw = nullptr, *big_count = nullptr, *err = nullptr;
+    int64_t *raw_ptr = nullptr, *big_rows = nullptr;
+    RG_TRY(dalloc_t(ctx, &cnt, nl));
+    RG_TRY(dalloc_t(ctx, &raw_ptr, nl + 1));
+    RG_TRY(dalloc_t(ctx, &col_raw, cap));
+    RG_TRY(dalloc_t(ctx, &big_rows, nl));
+    RG_TRY(dalloc_t(ctx, &big_count, 2));
+    err = big_count + 1;
+    RG_TRY(dalloc_t(ctx, &g->row_ptr, nl + 1));
+    RG_TRY(dalloc_t(ctx, &g->deg_local, nl));
+    RG_TRY(dalloc_t(ctx, &g->deg_all, n));
+    RG_TRY(dalloc_t(ctx, &g->s_all, n));
+    RG_TRY(dalloc_t(ctx, &g->sh_all, n));
+    RG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nl ? nl : 1), st));
+    RG_CUDA(cudaMemsetAsync(big_count, 0, sizeof(int32_t) * 2, st));
+    const int egrid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 256), (int64_t)ctx->sm_count * 16)));
+    if (m > 0) {
+        LaunchScope L(ctx, K_CSR_COUNT);
+        csr_count<<<egrid, 256, 0, st>>>(src, dst, m, n, rb, re, cnt, err);
+    }
+    RG_CHECK_LAUNCH(ctx);
+    RG_TRY(scan_i32_to_i64(ctx, cnt, raw_ptr, nl));
+    if (m > 0) {
+        LaunchScope L(ctx, K_CSR_SCATTER);
+        csr_scatter<<<egrid, 256, 0, st>>>(src, dst, m, n, rb, re, raw_ptr, cnt, col_raw);
+    }
+    RG_CHECK_LAUNCH(ctx);
+    const int rgrid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nl, 8), (int64_t)ctx->sm_count * 8)));
+    if (nl > 0) {
+        {
+            LaunchScope L(ctx, K_CSR_SORT_WARP);
+            csr_sort_warp<<<rgrid, 256, 0, st>>>(nl, raw_ptr, col_raw, g->deg_local, big_rows, big_count);
+        }
+        RG_CHECK_LAUNCH(ctx);
+        {
+            static bool attr_set = false;
+            if (!attr_set) {
+                RG_CUDA(cudaFuncSetAttribute(csr_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kBlockSortSmemCap * (int)sizeof(int32_t)));
+                attr_set = true;
+            }
+            LaunchScope L(ctx, K_CSR_SORT_BLOCK);
+            csr_sort_block<<<ctx->sm_count, 1024, kBlockSortSmemCap * sizeof(int32_t), st>>>(big_rows, big_count,
+                                                                                             raw_ptr, col_raw,
+                                                                                             g->deg_local);
+        }
+        RG_CHECK_LAUNCH(ctx);
+    }
+    RG_TRY(scan_i32_to_i64(ctx, g->deg_local, g->row_ptr, nl));
+    int64_t nnz = 0;
+    int herr = 0;
+    RG_CUDA(cudaMemcpyAsync(&nnz, g->row_ptr + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    RG_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    RG_CUDA(cudaStreamSynchronize(st));
+    if (herr) {
+        dfree(ctx, cnt); dfree(ctx, raw_ptr); dfree(ctx, col_raw); dfree(ctx, big_rows); dfree(ctx, big_count);
+        return fail(RAFTGP_ERR_DATA, "build_csr: node id outside [0, n)");
+    }
+    g->nnz_local = nnz;
+    RG_TRY(dalloc_t(ctx, &g->col, nnz));
+    if (nl > 0 && nnz > 0) {
+        LaunchScope L(ctx, K_CSR_COMPACT);
+        const int cgrid = static_cast<int>(std::min<int64_t>(ceil_div(nl, 8), (int64_t)ctx->sm_count * 16));
+        csr_compact<<<cgrid, 256, 0, st>>>(nl, raw_ptr, col_raw, g->row_ptr, g->col);
+    }
+    RG_CHECK_LAUNCH(ctx);
+    dfree(ctx, cnt);
+    dfree(ctx, raw_ptr);
+    dfree(ctx, col_raw);
+    dfree(ctx, big_rows);
+    dfree(ctx, big_count);
+    if (rb == 0 && re == n) {
+        if (n > 0) RG_CUDA(cudaMemcpyAsync(g->deg_all, g->deg_local, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
+        RG_TRY(degrees_finalize(g));
+    }
+    return RAFTGP_OK;
+}
+
+}  // namespace raftgp

@@ -1,0 +1,136 @@
+// internal.cuh — shared internals of libraftgp (context/graph structs, errors, launch accounting).
+// Product code only: nothing here is shared with oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/raftgp.h"
+
+namespace raftgp {
+
+// ---------------------------------------------------------------- kernel ids (profiling)
+enum KernelId : int {
+    K_CSR_COUNT = 0,
+    K_SCAN,
+    K_CSR_SCATTER,
+    K_CSR_SORT_WARP,
+    K_CSR_SORT_BLOCK,
+    K_CSR_COMPACT,
+    K_DEGREES,
+    K_SKETCH,
+    K_SKETCH_G,
+    K_G_FINAL,
+    K_FEATURE_HOP,
+    K_TRANSFORM,
+    K_GCN_HOP,
+    K_GENERIC,
+    K_MISC,
+    K_NUM
+};
+extern const char *const kKernelNames[K_NUM];
+
+struct ProfRec {
+    int kid;
+    cudaEvent_t start, stop;
+};
+
+}  // namespace raftgp
+
+struct raftgp_ctx_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int sm_count = 148;
+    int64_t launches = 0;
+    bool prof = false;
+    std::vector<raftgp::ProfRec> recs;
+    std::vector<cudaEvent_t> event_pool;
+};
+
+struct raftgp_graph_s {
+    raftgp_ctx ctx = nullptr;
+    int64_t n = 0, row_begin = 0, row_end = 0, nl = 0;
+    int64_t nnz_local = 0;
+    int64_t two_e = -1;            // global 2e; -1 until degrees are global
+    int64_t *row_ptr = nullptr;    // device int64[nl+1], local offsets
+    int32_t *col = nullptr;        // device int32[nnz_local], global ids
+    int32_t *deg_local = nullptr;  // device int32[nl]
+    int32_t *deg_all = nullptr;    // device int32[n] (global degrees)
+    float *s_all = nullptr;        // device fp32[n]: deg^-1/2, 0 for isolated nodes
+    float *sh_all = nullptr;       // device fp32[n]: (deg+1)^-1/2
+    // host mirror (scoring), filled lazily
+    bool host_valid = false;
+    std::vector<int64_t> h_row_ptr;
+    std::vector<int32_t> h_col;
+};
+
+namespace raftgp {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string &msg);
+raftgp_status fail(raftgp_status st, const std::string &msg);
+raftgp_status cuda_fail(cudaError_t e, const char *what);
+
+#define RG_CUDA(call)                                               \
+    do {                                                            \
+        cudaError_t _e = (call);                                    \
+        if (_e != cudaSuccess) return ::raftgp::cuda_fail(_e, #call); \
+    } while (0)
+
+#define RG_CHECK_LAUNCH(ctx)                                                     \
+    do {                                                                         \
+        cudaError_t _e = cudaGetLastError();                                     \
+        if (_e != cudaSuccess) return ::raftgp::cuda_fail(_e, "kernel launch"); \
+    } while (0)
+
+#define RG_TRY(expr)                             \
+    do {                                         \
+        raftgp_status _s = (expr);               \
+        if (_s != RAFTGP_OK) return _s;          \
+    } while (0)
+
+// ---------------------------------------------------------------- launch accounting
+// Scope object placed around ONE kernel launch: counts it, and when profiling is on records CUDA
+// events before/after it on the context stream.
+struct LaunchScope {
+    raftgp_ctx ctx;
+    int kid;
+    cudaEvent_t a = nullptr, b = nullptr;
+    LaunchScope(raftgp_ctx c, int k);
+    ~LaunchScope();
+};
+
+// ---------------------------------------------------------------- memory (stream-ordered pool)
+raftgp_status dalloc(raftgp_ctx ctx, void **p, size_t bytes);
+void dfree(raftgp_ctx ctx, void *p);
+
+template <typename T>
+raftgp_status dalloc_t(raftgp_ctx ctx, T **p, size_t count) {
+    return dalloc(ctx, reinterpret_cast<void **>(p), sizeof(T) * (count ? count : 1));
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ---------------------------------------------------------------- components (csr.cu, sketch.cu, spmm.cu)
+raftgp_status scan_i32_to_i64(raftgp_ctx ctx, const int32_t *in, int64_t *out, int64_t n);
+raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src, const int32_t *dst, int64_t rb,
+                        int64_t re, raftgp_graph g);
+raftgp_status degrees_finalize(raftgp_graph g);   // deg_all -> two_e, s_all, sh_all
+
+raftgp_status sketch_fill(raftgp_ctx ctx, uint64_t seed, uint32_t tag, int64_t row_begin, int64_t rows, int32_t cols,
+                          int32_t den, float *out);
+// Theta for all n rows + g = sum_j d_j Theta_j (fp64) when g_out != nullptr.
+raftgp_status sketch_theta(raftgp_graph g, uint64_t seed, int32_t r, float *theta, double *g_out);
+
+raftgp_status feature_hop(raftgp_graph g, int variant, int32_t r, const float *theta, const double *gvec, float *Y,
+                          const float *W1, int32_t l1, float *T1);
+raftgp_status gcn_transform(raftgp_graph g, const float *Z, int32_t lin, const float *W, int32_t lout, float *T);
+raftgp_status gcn_hop(raftgp_graph g, const float *Tfull, int32_t w, float *Zout, const float *Wn, int32_t wn,
+                      float *Tnext);
+
+}  // namespace raftgp

@@ -1,0 +1,417 @@
+// spmm.cu — a4/a5 of the hot path: the sparse-times-dense hops with fused epilogues.
+//
+//   feature hop (Eq. 5):  Y = X Theta, X in {M, Q, Q~}
+//   GCN hop     (Eq. 6):  Z'_i = rownorm(tanh(s^_i (T_i + sum_{j in N(i)} T_j))),
+//                                           T = s^ (.) (Z W) produced by the previous hop's epilogue
+//   transform:                              T = s^ (.) (Z W)   (row GEMM, W in shared memory)
+//
+// Fast kernel ("hop_kernel"): one warp per row, operand rows gathered with 128-bit loads. A gathered
+// row of width W is W/4 lanes wide, so a warp gathers 32/(W/4) neighbours at once and unrolls U such
+// steps (U x 16 B in flight per lane); col_idx is read 32 entries at a time, coalesced, and broadcast
+// with shuffles. The per-row sum order is fixed (lane sub-slot order, then a fixed xor butterfly), so
+// results are deterministic and independent of the grid. After a group of RB rows the warp runs the
+// fused epilogue GEMM against W_next held in shared memory (FFMA; Z rows staged per warp in shared
+// memory and read as broadcasts). HBM-bound: bytes per edge = 4 (col) + 4W (row), see DESIGN.md.
+//
+// Generic kernel ("hop_generic"): one block per row, one thread per column, any width / alignment.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "internal.cuh"
+
+namespace raftgp {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+enum Kind : int { KIND_NCUT = 0, KIND_MOD = 1, KIND_MOD_REDUCED = 2, KIND_GCN = 3, KIND_LOAD = 4 };
+
+struct HopArgs {
+    int64_t nl, rb, n;
+    const int64_t *row_ptr;    // local CSR
+    const int32_t *col;
+    const float *X;            // operand, n x W (global rows); for KIND_LOAD: local rows x W
+    const float *s_all;        // deg^-1/2
+    const float *sh_all;       // (deg+1)^-1/2
+    const int32_t *deg_all;
+    const double *gvec;        // MOD: g = d^T Theta (W doubles)
+    double inv2e;              // 1 / 2e
+    float *out;                // local rows x W (Y or Z'), may be null
+    const float *Wn;           // W x WN, may be null
+    float *Tn;                 // local rows x WN, may be null
+};
+
+__device__ __forceinline__ float4 ldg4(const float4 *p) { return __ldg(p); }
+
+__device__ __forceinline__ void fma4(float4 &a, float w, const float4 &v) {
+    a.x = fmaf(w, v.x, a.x);
+    a.y = fmaf(w, v.y, a.y);
+    a.z = fmaf(w, v.z, a.z);
+    a.w = fmaf(w, v.w, a.w);
+}
+__device__ __forceinline__ void add4(float4 &a, const float4 &v) {
+    a.x += v.x;
+    a.y += v.y;
+    a.z += v.z;
+    a.w += v.w;
+}
+__device__ __forceinline__ float4 shfl_xor4(const float4 &v, int o) {
+    return make_float4(__shfl_xor_sync(FULL, v.x, o), __shfl_xor_sync(FULL, v.y, o), __shfl_xor_sync(FULL, v.z, o),
+                       __shfl_xor_sync(FULL, v.w, o));
+}
+
+// Gather-sum over the neighbours of one row. MODE 0: acc += X_j; 1: acc += s_j X_j; 2: acc += X_j and
+// acc2 += d_j X_j. Lane layout: sub = lane / LPN picks the neighbour slot, cl = lane % LPN the float4
+// column slice. Returns the full row sum in every sub-slot (xor butterfly over sub-slots).
+template <int W, int U, int MODE>
+__device__ __forceinline__ void gather_row(const HopArgs &a, int64_t beg, int64_t end, int lane, float4 &acc,
+                                           float4 &acc2) {
+    constexpr int LPN = W / 4, NPW = 32 / LPN;
+    static_assert(NPW * U <= 32 && 32 % (NPW * U) == 0, "unroll must tile a 32-entry col chunk");
+    const int sub = lane / LPN, cl = lane % LPN;
+    const float4 *X4 = reinterpret_cast<const float4 *>(a.X);
+    acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    acc2 = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t base = beg; base < end; base += 32) {
+        const int cnt = (end - base < 32) ? static_cast<int>(end - base) : 32;
+        const int32_t myj = lane < cnt ? __ldg(a.col + base + lane) : 0;
+        float myw = 0.f;
+        if (MODE == 1) myw = lane < cnt ? __ldg(a.s_all + myj) : 0.f;
+        if (MODE == 2) myw = lane < cnt ? static_cast<float>(__ldg(a.deg_all + myj)) : 0.f;
+        for (int k0 = 0; k0 < cnt; k0 += NPW * U) {
+            float4 v[U];
+            float w[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int k = k0 + u * NPW + sub;
+                const int32_t j = __shfl_sync(FULL, myj, k);
+                w[u] = (MODE != 0) ? __shfl_sync(FULL, myw, k) : 1.f;
+                v[u] = (k < cnt) ? ldg4(X4 + (int64_t)j * LPN + cl) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (MODE == 1) {
+                    fma4(acc, w[u], v[u]);
+                } else {
+                    add4(acc, v[u]);
+                    if (MODE == 2) fma4(acc2, w[u], v[u]);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int o = LPN; o < 32; o <<= 1) {
+        add4(acc, shfl_xor4(acc, o));
+        if (MODE == 2) add4(acc2, shfl_xor4(acc2, o));
+    }
+}
+
+template <int W, int WN, int RB>
+struct HopSmem {
+    static constexpr int kWn = W * WN;       // floats
+};
+
+// One hop for groups of RB consecutive local rows per warp (grid-stride over groups).
+template <int KIND, int W, int WN, int RB, int U, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1024 / THREADS) hop_kernel(HopArgs a) {
+    extern __shared__ float4 smem4[];
+    float *smem = reinterpret_cast<float *>(smem4);
+    constexpr int LPN = W / 4;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int wpb = blockDim.x >> 5;
+    float *Wsm = smem;                                              // W x WN
+    float *stage = smem + HopSmem<W, WN, RB>::kWn + wib * RB * W;   // RB x W
+    if constexpr (WN > 0) {
+        const float4 *src = reinterpret_cast<const float4 *>(a.Wn);
+        float4 *dst = reinterpret_cast<float4 *>(Wsm);
+        for (int t = threadIdx.x; t < W * WN / 4; t += blockDim.x) dst[t] = src[t];
+        __syncthreads();
+    }
+    const int sub = lane / LPN, cl = lane % LPN;
+    double g0 = 0, g1 = 0, g2 = 0, g3 = 0;
+    if constexpr (KIND == KIND_MOD) {
+        g0 = a.gvec[4 * cl + 0];
+        g1 = a.gvec[4 * cl + 1];
+        g2 = a.gvec[4 * cl + 2];
+        g3 = a.gvec[4 * cl + 3];
+    }
+    const int64_t ngroups = (a.nl + RB - 1) / RB;
+    const int64_t gw = (int64_t)gridDim.x * wpb;
+    for (int64_t grp = (int64_t)blockIdx.x * wpb + wib; grp < ngroups; grp += gw) {
+        const int64_t row0 = grp * RB;
+        const int rows_here = (a.nl - row0 < RB) ? static_cast<int>(a.nl - row0) : RB;
+        for (int rr = 0; rr < rows_here; ++rr) {
+            const int64_t row = row0 + rr;          // local row
+            const int64_t gi = a.rb + row;          // global row id
+            float4 acc, acc2;
+            float4 y;
+            if constexpr (KIND == KIND_LOAD) {
+                y = ldg4(reinterpret_cast<const float4 *>(a.X) + row * LPN + cl);
+            } else {
+                const int64_t beg = a.row_ptr[row], end = a.row_ptr[row + 1];
+                constexpr int MODE = KIND == KIND_NCUT ? 1 : (KIND == KIND_MOD_REDUCED ? 2 : 0);
+                gather_row<W, U, MODE>(a, beg, end, lane, acc, acc2);
+                if constexpr (KIND == KIND_NCUT) {
+                    const float si = __ldg(a.s_all + gi);
+                    y = make_float4(si * acc.x, si * acc.y, si * acc.z, si * acc.w);
+                } else if constexpr (KIND == KIND_MOD) {
+                    const double c = static_cast<double>(__ldg(a.deg_all + gi)) * a.inv2e;
+                    y = make_float4(static_cast<float>(acc.x - c * g0), static_cast<float>(acc.y - c * g1),
+                                    static_cast<float>(acc.z - c * g2), static_cast<float>(acc.w - c * g3));
+                } else if constexpr (KIND == KIND_MOD_REDUCED) {
+                    const double c = static_cast<double>(__ldg(a.deg_all + gi)) * a.inv2e;
+                    y = make_float4(static_cast<float>(acc.x - c * acc2.x), static_cast<float>(acc.y - c * acc2.y),
+                                    static_cast<float>(acc.z - c * acc2.z), static_cast<float>(acc.w - c * acc2.w));
+                } else {   // KIND_GCN: H_i = s^_i (T_i + sum_j T_j); tanh; row l2 normalisation
+                    const float4 self = ldg4(reinterpret_cast<const float4 *>(a.X) + gi * LPN + cl);
+                    add4(acc, self);
+                    const float shi = __ldg(a.sh_all + gi);
+                    y = make_float4(tanhf(shi * acc.x), tanhf(shi * acc.y), tanhf(shi * acc.z), tanhf(shi * acc.w));
+                    float ss = y.x * y.x + y.y * y.y + y.z * y.z + y.w * y.w;
+#pragma unroll
+                    for (int o = 1; o < LPN; o <<= 1) ss += __shfl_xor_sync(FULL, ss, o);
+                    if (ss > 0.f) {
+                        const float nrm = sqrtf(ss);
+                        y = make_float4(y.x / nrm, y.y / nrm, y.z / nrm, y.w / nrm);
+                    }
+                }
+            }
+            if (a.out != nullptr && sub == 0) reinterpret_cast<float4 *>(a.out)[row * LPN + cl] = y;
+            if constexpr (WN > 0) {
+                if (sub == 0) reinterpret_cast<float4 *>(stage)[rr * LPN + cl] = y;
+            }
+        }
+        if constexpr (WN > 0) {
+            // fused transform: Tn_i = s^_i (y_i W_next) for the rows of this group
+            constexpr int OL = WN / 4;        // lanes per output row
+            constexpr int RS = 32 / OL;       // rows in parallel
+            constexpr int RR = RB / RS;       // rows per lane
+            static_assert(RR >= 1 && RB % RS == 0, "RB must be a multiple of the parallel row count");
+            __syncwarp();
+            const int rs = lane / OL, oc = lane % OL;
+            float4 o[RR];
+#pragma unroll
+            for (int q = 0; q < RR; ++q) o[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 *W4 = reinterpret_cast<const float4 *>(Wsm);
+            const float4 *S4 = reinterpret_cast<const float4 *>(stage);
+#pragma unroll 2
+            for (int k = 0; k < W; k += 4) {
+                const float4 w0 = W4[(k + 0) * OL + oc];
+                const float4 w1 = W4[(k + 1) * OL + oc];
+                const float4 w2 = W4[(k + 2) * OL + oc];
+                const float4 w3 = W4[(k + 3) * OL + oc];
+#pragma unroll
+                for (int q = 0; q < RR; ++q) {
+                    const int rr = rs + q * RS;
+                    const float4 z = S4[rr * (W / 4) + k / 4];
+                    fma4(o[q], z.x, w0);
+                    fma4(o[q], z.y, w1);
+                    fma4(o[q], z.z, w2);
+                    fma4(o[q], z.w, w3);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < RR; ++q) {
+                const int rr = rs + q * RS;
+                if (rr < rows_here) {
+                    const int64_t row = row0 + rr;
+                    const float shi = __ldg(a.sh_all + a.rb + row);
+                    reinterpret_cast<float4 *>(a.Tn)[row * OL + oc] =
+                        make_float4(shi * o[q].x, shi * o[q].y, shi * o[q].z, shi * o[q].w);
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// ---------------------------------------------------------------- generic (any width / alignment)
+template <int KIND>
+__global__ void __launch_bounds__(128) hop_generic(HopArgs a, int W, int WN) {
+    extern __shared__ float gsm[];   // W floats (the finished row) + 32 scratch
+    float *rowbuf = gsm;
+    float *red = gsm + W;
+    for (int64_t row = blockIdx.x; row < a.nl; row += gridDim.x) {
+        const int64_t gi = a.rb + row;
+        float part = 0.f;
+        for (int c = threadIdx.x; c < W; c += blockDim.x) {
+            float y;
+            if (KIND == KIND_LOAD) {
+                y = a.X[row * W + c];
+            } else {
+                const int64_t beg = a.row_ptr[row], end = a.row_ptr[row + 1];
+                float acc = 0.f, acc2 = 0.f;
+                for (int64_t p = beg; p < end; ++p) {
+                    const int32_t j = __ldg(a.col + p);
+                    const float v = __ldg(a.X + (int64_t)j * W + c);
+                    if (KIND == KIND_NCUT) acc = fmaf(__ldg(a.s_all + j), v, acc);
+                    else acc += v;
+                    if (KIND == KIND_MOD_REDUCED) acc2 = fmaf(static_cast<float>(__ldg(a.deg_all + j)), v, acc2);
+                }
+                if (KIND == KIND_NCUT) {
+                    y = __ldg(a.s_all + gi) * acc;
+                } else if (KIND == KIND_MOD) {
+                    const double cc = static_cast<double>(__ldg(a.deg_all + gi)) * a.inv2e;
+                    y = static_cast<float>(acc - cc * a.gvec[c]);
+                } else if (KIND == KIND_MOD_REDUCED) {
+                    const double cc = static_cast<double>(__ldg(a.deg_all + gi)) * a.inv2e;
+                    y = static_cast<float>(acc - cc * acc2);
+                } else {
+                    acc += __ldg(a.X + gi * W + c);
+                    y = tanhf(__ldg(a.sh_all + gi) * acc);
+                    part += y * y;
+                }
+            }
+            rowbuf[c] = y;
+        }
+        if (KIND == KIND_GCN) {
+            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(FULL, part, o);
+            if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+            __syncthreads();
+            float ss = 0.f;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) ss += red[w];
+            __syncthreads();
+            if (ss > 0.f) {
+                const float nrm = sqrtf(ss);
+                for (int c = threadIdx.x; c < W; c += blockDim.x) rowbuf[c] = rowbuf[c] / nrm;
+            }
+        }
+        __syncthreads();
+        if (a.out != nullptr)
+            for (int c = threadIdx.x; c < W; c += blockDim.x) a.out[row * W + c] = rowbuf[c];
+        if (WN > 0) {
+            const float shi = __ldg(a.sh_all + gi);
+            for (int c = threadIdx.x; c < WN; c += blockDim.x) {
+                float acc = 0.f;
+                for (int k = 0; k < W; ++k) acc = fmaf(rowbuf[k], __ldg(a.Wn + (int64_t)k * WN + c), acc);
+                a.Tn[row * WN + c] = shi * acc;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- launch helpers
+template <int KIND, int W, int WN>
+raftgp_status launch_fast(raftgp_ctx ctx, const HopArgs &a) {
+    constexpr int RB = 4;
+    constexpr int U = 8;
+    constexpr int THREADS = WN > 0 ? 512 : 256;
+    constexpr int WPB = THREADS / 32;
+    const size_t smem = sizeof(float) * ((size_t)W * WN + (WN > 0 ? (size_t)WPB * RB * W : 0));
+    static int blocks_per_sm = -1;
+    auto kern = hop_kernel<KIND, W, WN, RB, U, THREADS>;
+    if (blocks_per_sm < 0) {
+        RG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        RG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, THREADS, smem));
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    const int64_t groups = ceil_div(a.nl, RB);
+    const int64_t want = ceil_div(groups, WPB);
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count * blocks_per_sm)));
+    const int kid = KIND == KIND_GCN ? K_GCN_HOP : (KIND == KIND_LOAD ? K_TRANSFORM : K_FEATURE_HOP);
+    {
+        LaunchScope L(ctx, kid);
+        kern<<<grid, THREADS, smem, ctx->stream>>>(a);
+    }
+    RG_CHECK_LAUNCH(ctx);
+    return RAFTGP_OK;
+}
+
+template <int KIND, int W>
+raftgp_status dispatch_wn(raftgp_ctx ctx, const HopArgs &a, int wn) {
+    switch (wn) {
+        case 0: return launch_fast<KIND, W, 0>(ctx, a);
+        case 32: return launch_fast<KIND, W, 32>(ctx, a);
+        case 64: return launch_fast<KIND, W, 64>(ctx, a);
+        case 128: return launch_fast<KIND, W, 128>(ctx, a);
+        default: return fail(RAFTGP_ERR_INTERNAL, "dispatch_wn: unsupported width");
+    }
+}
+
+template <int KIND>
+raftgp_status dispatch(raftgp_ctx ctx, const HopArgs &a, int w, int wn) {
+    const bool fast_w = (w == 32 || w == 64 || w == 128) && (wn == 0 || wn == 32 || wn == 64 || wn == 128);
+    const bool al = aligned16(a.X) && (a.out == nullptr || aligned16(a.out)) && (a.Wn == nullptr || aligned16(a.Wn)) &&
+                    (a.Tn == nullptr || aligned16(a.Tn));
+    if (a.nl == 0) return RAFTGP_OK;
+    if (fast_w && al) {
+        switch (w) {
+            case 32: return dispatch_wn<KIND, 32>(ctx, a, wn);
+            case 64: return dispatch_wn<KIND, 64>(ctx, a, wn);
+            default: return dispatch_wn<KIND, 128>(ctx, a, wn);
+        }
+    }
+    const size_t smem = sizeof(float) * ((size_t)w + 32);
+    if (smem > 48 * 1024) {
+        static bool set = false;
+        if (!set) {
+            RG_CUDA(cudaFuncSetAttribute(hop_generic<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            set = true;
+        }
+    }
+    const int grid = static_cast<int>(std::min<int64_t>(a.nl, (int64_t)ctx->sm_count * 16));
+    {
+        LaunchScope L(ctx, K_GENERIC);
+        hop_generic<KIND><<<grid, 128, smem, ctx->stream>>>(a, w, wn);
+    }
+    RG_CHECK_LAUNCH(ctx);
+    return RAFTGP_OK;
+}
+
+HopArgs base_args(raftgp_graph g) {
+    HopArgs a{};
+    a.nl = g->nl;
+    a.rb = g->row_begin;
+    a.n = g->n;
+    a.row_ptr = g->row_ptr;
+    a.col = g->col;
+    a.s_all = g->s_all;
+    a.sh_all = g->sh_all;
+    a.deg_all = g->deg_all;
+    a.inv2e = g->two_e > 0 ? 1.0 / static_cast<double>(g->two_e) : 0.0;
+    return a;
+}
+
+}  // namespace
+
+raftgp_status feature_hop(raftgp_graph g, int variant, int32_t r, const float *theta, const double *gvec, float *Y,
+                          const float *W1, int32_t l1, float *T1) {
+    HopArgs a = base_args(g);
+    a.X = theta;
+    a.gvec = gvec;
+    a.out = Y;
+    a.Wn = W1;
+    a.Tn = T1;
+    const int wn = W1 ? l1 : 0;
+    switch (variant) {
+        case RAFTGP_NCUT: return dispatch<KIND_NCUT>(g->ctx, a, r, wn);
+        case RAFTGP_MOD: return dispatch<KIND_MOD>(g->ctx, a, r, wn);
+        default: return dispatch<KIND_MOD_REDUCED>(g->ctx, a, r, wn);
+    }
+}
+
+raftgp_status gcn_transform(raftgp_graph g, const float *Z, int32_t lin, const float *W, int32_t lout, float *T) {
+    HopArgs a = base_args(g);
+    a.X = Z;
+    a.out = nullptr;
+    a.Wn = W;
+    a.Tn = T;
+    return dispatch<KIND_LOAD>(g->ctx, a, lin, lout);
+}
+
+raftgp_status gcn_hop(raftgp_graph g, const float *Tfull, int32_t w, float *Zout, const float *Wn, int32_t wn,
+                      float *Tnext) {
+    HopArgs a = base_args(g);
+    a.X = Tfull;
+    a.out = Zout;
+    a.Wn = Wn;
+    a.Tn = Tnext;
+    return dispatch<KIND_GCN>(g->ctx, a, w, Wn ? wn : 0);
+}
+
+}  // namespace raftgp

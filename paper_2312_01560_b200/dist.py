@@ -1,0 +1,148 @@
+"""Row-partitioned multi-GPU orchestration of the embedding path.
+
+One process per GPU. Rank p owns the contiguous rows [p*R, min((p+1)*R, n)) with R = ceil(n / P), so
+the all-gathered (P*R)-row block indexes global rows directly. Exchange steps — the only collectives:
+  1. after the CSR build: all-gather of the local degree vectors (n int32) -> every rank computes the
+     global 2e, s and s^ (raftgp_graph_set_degrees);
+  2. before every GCN hop: all-gather of the next operand T_k = s^ (.) (Z^(k-1) W^(k)) (n x L_k fp32).
+Hop 0 needs no exchange: Theta is counter-based, so every rank regenerates the rows it gathers, and
+the MOD rank-1 vector g = d^T Theta is reduced over global fixed chunks identically on every rank.
+Each row's arithmetic is a function of that row only, so the result is bit-identical for any P.
+
+The per-rank pipeline is a generator that yields ("gather", tensor) at each exchange point and
+receives the gathered block; drivers run it over torch.distributed (NCCL on B200, gloo on CPU tests)
+or, for single-GPU testing, over P shards in lockstep ("loopback"). The compute steps go through an
+`engine`: `CudaEngine` calls libraftgp (the product path); tests may plug a CPU engine.
+"""
+from __future__ import annotations
+
+from typing import Callable, Generator, List, Optional, Sequence
+
+import torch
+
+from . import raftgp as rg
+
+
+def row_partition(n: int, world: int):
+    """[(row_begin, row_end)] per rank and the padded block height R."""
+    R = max(1, -(-n // world))
+    return [(min(n, p * R), min(n, (p + 1) * R)) for p in range(world)], R
+
+
+def _pad(t: torch.Tensor, R: int) -> torch.Tensor:
+    if t.shape[0] == R:
+        return t.contiguous()
+    out = torch.zeros((R,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    out[: t.shape[0]] = t
+    return out
+
+
+class CudaEngine:
+    """Local compute steps on one GPU through the C-ABI."""
+
+    def __init__(self, ctx: rg.Context):
+        self.ctx = ctx
+
+    def build(self, n, src, dst, rb, re):
+        return rg.raftgp_build_csr(self.ctx, n, src, dst, rb, re)
+
+    def local_degrees(self, h):
+        return h.local_degrees()
+
+    def set_degrees(self, h, deg_all):
+        h.set_degrees(deg_all)
+
+    def project(self, h, variant, r, seed):
+        return rg.raftgp_project(h, variant, r, seed)
+
+    def weights(self, seed, k, a, b):
+        return rg.raftgp_weights(self.ctx, seed, k, a, b)
+
+    def transform(self, h, Z, W):
+        return rg.raftgp_gcn_transform(h, Z, W)
+
+    def hop(self, h, T_full, W_next, want_Z: bool):
+        rows = h.rows
+        Z = torch.empty((rows, T_full.shape[1]), dtype=torch.float32, device=self.ctx.device) if want_Z else None
+        _, T_next = rg.raftgp_gcn_hop(h, T_full, Z, W_next)
+        return Z, T_next
+
+
+def rank_pipeline(engine, n: int, src, dst, rank: int, world: int, variants, dims: Sequence[int], seed: int,
+                  keep: Optional[dict] = None) -> Generator:
+    """Yields ("gather", local_block) at each exchange; returns {variant: this rank's rows of Z}
+    (or the Z tensor itself when `variants` is a single variant)."""
+    single = isinstance(variants, (str, int))
+    vlist = [variants] if single else list(variants)
+    ranges, R = row_partition(n, world)
+    rb, re = ranges[rank]
+    h = engine.build(n, src, dst, rb, re)
+    deg_all = yield ("gather", _pad(engine.local_degrees(h), R))
+    engine.set_degrees(h, deg_all[:n].contiguous())
+    L = len(dims) - 1
+    out = {}
+    for variant in vlist:
+        Y = engine.project(h, variant, dims[0], seed)
+        T = engine.transform(h, Y, engine.weights(seed, 1, dims[0], dims[1]))
+        Z = None
+        for k in range(1, L + 1):
+            T_full = yield ("gather", _pad(T, R))
+            Wn = engine.weights(seed, k + 1, dims[k], dims[k + 1]) if k < L else None
+            Z, T = engine.hop(h, T_full[:n], Wn, want_Z=(k == L))
+        out[variant] = Z
+        if keep is not None:
+            keep.setdefault("Y", {})[variant] = Y
+    if keep is not None:
+        keep["graph"] = h
+    return out[vlist[0]] if single else out
+
+
+def run_loopback(gens: List[Generator]):
+    """Advance P rank pipelines in lockstep; a gather concatenates the P blocks in rank order."""
+    msgs = [next(g) for g in gens]
+    results: List[Optional[torch.Tensor]] = [None] * len(gens)
+    while True:
+        full = torch.cat([m[1] for m in msgs], 0)
+        nxt, done = [], 0
+        for p, g in enumerate(gens):
+            try:
+                nxt.append(g.send(full))
+            except StopIteration as stop:
+                results[p] = stop.value
+                nxt.append(None)
+                done += 1
+        if done == len(gens):
+            return results
+        if done:
+            raise RuntimeError("rank pipelines went out of step")
+        msgs = nxt
+
+
+def run_distributed(gen: Generator, group=None, gather: Optional[Callable] = None):
+    """Drive one rank's pipeline over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+    import torch.distributed as dist
+
+    def _all_gather(t: torch.Tensor) -> torch.Tensor:
+        world = dist.get_world_size(group)
+        if t.is_cuda:
+            out = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+            dist.all_gather_into_tensor(out, t.contiguous(), group=group)
+            return out
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t.contiguous(), group=group)
+        return torch.cat(parts, 0)
+
+    gather = gather or _all_gather
+    msg = next(gen)
+    while True:
+        try:
+            msg = gen.send(gather(msg[1]))
+        except StopIteration as stop:
+            return stop.value
+
+
+def loopback_embed(ctx: rg.Context, n: int, src, dst, world: int, variant, dims, seed: int):
+    """P logical ranks on ONE GPU (sequential per stage, no concurrent waiting kernels)."""
+    eng = CudaEngine(ctx)
+    gens = [rank_pipeline(eng, n, src, dst, p, world, variant, dims, seed) for p in range(world)]
+    return run_loopback(gens)

@@ -1,0 +1,345 @@
+"""Thin Python binding of the C-ABI in include/raftgp.h (ctypes; argument marshalling only).
+
+Every computation happens inside libraftgp.so (sm_100a kernels). PyTorch is used only to own device
+memory and to supply the CUDA stream. There is no fallback: if the library is missing or no GPU is
+present, calls raise.
+
+Function names are the C-ABI names; `Context` and `Graph` wrap the two opaque handles.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libraftgp.so")
+
+RAFTGP_OK, RAFTGP_ERR_PARAM, RAFTGP_ERR_DATA = 0, 2, 3
+RAFTGP_ERR_INTERNAL, RAFTGP_ERR_CUDA, RAFTGP_ERR_NOMEM, RAFTGP_ERR_STATE = 4, 5, 6, 7
+RAFTGP_NCUT, RAFTGP_MOD, RAFTGP_MOD_REDUCED = 0, 1, 2
+VARIANTS = {"ncut": RAFTGP_NCUT, "mod": RAFTGP_MOD, "mod_reduced": RAFTGP_MOD_REDUCED}
+RAFTGP_HOST_PTRS, RAFTGP_DEVICE_PTRS = 0, 1
+
+# every symbol declared in include/raftgp.h
+EXPORTS = (
+    "raftgp_last_error", "raftgp_version", "raftgp_ctx_create", "raftgp_ctx_destroy", "raftgp_ctx_sync",
+    "raftgp_ctx_stream", "raftgp_ctx_set_profiling", "raftgp_prof_kernels", "raftgp_prof_name", "raftgp_prof_read",
+    "raftgp_prof_reset", "raftgp_launch_count", "raftgp_build_csr", "raftgp_graph_info", "raftgp_graph_export",
+    "raftgp_graph_local_degrees", "raftgp_graph_set_degrees", "raftgp_graph_destroy", "raftgp_sketch",
+    "raftgp_weights", "raftgp_project", "raftgp_gcn_transform", "raftgp_gcn_hop", "raftgp_gnn_embed",
+    "raftgp_embed", "raftgp_modularity", "raftgp_ncut", "raftgp_local_modularity",
+)
+
+_lib = None
+c_i32, c_i64, c_u32, c_u64, c_vp, c_dbl = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64,
+                                           ctypes.c_void_p, ctypes.c_double)
+P = ctypes.POINTER
+
+_SIGS = {
+    "raftgp_last_error": (ctypes.c_char_p, []),
+    "raftgp_version": (ctypes.c_char_p, []),
+    "raftgp_ctx_create": (ctypes.c_int, [ctypes.c_int, c_vp, P(c_vp)]),
+    "raftgp_ctx_destroy": (ctypes.c_int, [c_vp]),
+    "raftgp_ctx_sync": (ctypes.c_int, [c_vp]),
+    "raftgp_ctx_stream": (ctypes.c_int, [c_vp, P(c_vp)]),
+    "raftgp_ctx_set_profiling": (ctypes.c_int, [c_vp, ctypes.c_int]),
+    "raftgp_prof_kernels": (ctypes.c_int, []),
+    "raftgp_prof_name": (ctypes.c_char_p, [ctypes.c_int]),
+    "raftgp_prof_read": (ctypes.c_int, [c_vp, ctypes.c_int, P(c_dbl), P(c_i64)]),
+    "raftgp_prof_reset": (ctypes.c_int, [c_vp]),
+    "raftgp_launch_count": (ctypes.c_int, [c_vp, P(c_i64), ctypes.c_int]),
+    "raftgp_build_csr": (ctypes.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_u32, P(c_vp)]),
+    "raftgp_graph_info": (ctypes.c_int, [c_vp, P(c_i64), P(c_i64), P(c_i64), P(c_i64), P(c_i64)]),
+    "raftgp_graph_export": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_u32]),
+    "raftgp_graph_local_degrees": (ctypes.c_int, [c_vp, c_vp]),
+    "raftgp_graph_set_degrees": (ctypes.c_int, [c_vp, c_vp]),
+    "raftgp_graph_destroy": (ctypes.c_int, [c_vp]),
+    "raftgp_sketch": (ctypes.c_int, [c_vp, c_u64, c_u32, c_i64, c_i64, c_i32, c_i32, c_vp]),
+    "raftgp_weights": (ctypes.c_int, [c_vp, c_u64, c_i32, c_i32, c_i32, c_vp]),
+    "raftgp_project": (ctypes.c_int, [c_vp, ctypes.c_int, c_i32, c_u64, c_vp]),
+    "raftgp_gcn_transform": (ctypes.c_int, [c_vp, c_vp, c_i32, c_vp, c_i32, c_vp]),
+    "raftgp_gcn_hop": (ctypes.c_int, [c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp]),
+    "raftgp_gnn_embed": (ctypes.c_int, [c_vp, c_i32, c_vp, c_u64, c_vp, c_vp, c_vp]),
+    "raftgp_embed": (ctypes.c_int, [c_vp, ctypes.c_int, c_i32, c_vp, c_u64, c_vp, c_vp, c_vp]),
+    "raftgp_modularity": (ctypes.c_int, [c_vp, c_vp, c_i32, P(c_dbl)]),
+    "raftgp_ncut": (ctypes.c_int, [c_vp, c_vp, c_i32, P(c_dbl)]),
+    "raftgp_local_modularity": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_i32, P(c_dbl)]),
+}
+
+
+class RaftGPError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"raftgp status {code}: {msg}")
+        self.code = code
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libraftgp.so (raises if it has not been built: there is no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _ck(rc: int):
+    if rc != RAFTGP_OK:
+        raise RaftGPError(rc, load_library().raftgp_last_error().decode())
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_contiguous():
+        raise ValueError("tensors passed to raftgp must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _dev(t: torch.Tensor, what: str):
+    if not t.is_cuda:
+        raise ValueError(f"{what} must be a CUDA tensor")
+    return t
+
+
+# ------------------------------------------------------------------ context
+class Context:
+    """raftgp_ctx on one device, enqueuing on a torch CUDA stream (the current one by default)."""
+
+    def __init__(self, device: int = 0, stream: Optional[torch.cuda.Stream] = None):
+        lib = load_library()
+        self.device = torch.device("cuda", device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        h = c_vp()
+        _ck(lib.raftgp_ctx_create(device, c_vp(self.stream.cuda_stream), ctypes.byref(h)))
+        self.h = h
+
+    def sync(self):
+        _ck(load_library().raftgp_ctx_sync(self.h))
+
+    def set_profiling(self, on: bool = True):
+        _ck(load_library().raftgp_ctx_set_profiling(self.h, int(on)))
+
+    def prof_read(self) -> dict:
+        """{kernel_name: (total_ms, launches)} of the launches recorded since the last reset."""
+        lib = load_library()
+        out = {}
+        for k in range(lib.raftgp_prof_kernels()):
+            ms, cnt = c_dbl(0), c_i64(0)
+            _ck(lib.raftgp_prof_read(self.h, k, ctypes.byref(ms), ctypes.byref(cnt)))
+            if cnt.value:
+                out[lib.raftgp_prof_name(k).decode()] = (ms.value, cnt.value)
+        return out
+
+    def prof_reset(self):
+        _ck(load_library().raftgp_prof_reset(self.h))
+
+    def launch_count(self, reset: bool = False) -> int:
+        v = c_i64(0)
+        _ck(load_library().raftgp_launch_count(self.h, ctypes.byref(v), int(reset)))
+        return v.value
+
+    def close(self):
+        if getattr(self, "h", None) is not None and _lib is not None:
+            _lib.raftgp_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------------ graph
+class Graph:
+    """raftgp_graph: the canonical CSR of rows [row_begin, row_end) plus degree scalars, on device."""
+
+    def __init__(self, ctx: Context, h):
+        self.ctx = ctx
+        self.h = h
+
+    def info(self):
+        v = [c_i64(0) for _ in range(5)]
+        _ck(load_library().raftgp_graph_info(self.h, *[ctypes.byref(x) for x in v]))
+        n, rb, re, nnz, two_e = (x.value for x in v)
+        return dict(n=n, row_begin=rb, row_end=re, nnz_local=nnz, two_e=two_e)
+
+    @property
+    def n(self):
+        return self.info()["n"]
+
+    @property
+    def rows(self):
+        i = self.info()
+        return i["row_end"] - i["row_begin"]
+
+    def export(self):
+        """Host copies (numpy) of the local row_ptr (int64), col_idx (int32) and degrees (int32)."""
+        i = self.info()
+        rows = i["row_end"] - i["row_begin"]
+        rp = np.zeros(rows + 1, np.int64)
+        col = np.zeros(max(1, i["nnz_local"]), np.int32)
+        deg = np.zeros(max(1, rows), np.int32)
+        _ck(load_library().raftgp_graph_export(self.h, c_vp(rp.ctypes.data), c_vp(col.ctypes.data),
+                                               c_vp(deg.ctypes.data), RAFTGP_HOST_PTRS))
+        return rp, col[: i["nnz_local"]], deg[:rows]
+
+    def local_degrees(self) -> torch.Tensor:
+        out = torch.empty(max(1, self.rows), dtype=torch.int32, device=self.ctx.device)
+        _ck(load_library().raftgp_graph_local_degrees(self.h, _ptr(out)))
+        return out[: self.rows]
+
+    def set_degrees(self, deg_all: torch.Tensor):
+        _ck(load_library().raftgp_graph_set_degrees(self.h, _ptr(_dev(deg_all.contiguous(), "deg_all"))))
+
+    def close(self):
+        if getattr(self, "h", None) is not None and _lib is not None:
+            _lib.raftgp_graph_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def raftgp_build_csr(ctx: Context, n: int, src: torch.Tensor, dst: torch.Tensor, row_begin: int = 0,
+                     row_end: Optional[int] = None) -> Graph:
+    """a1 + a2. src/dst: int32 tensors (CUDA -> device pointers; CPU -> host pointers copied in-call)."""
+    if src.dtype != torch.int32 or dst.dtype != torch.int32 or src.numel() != dst.numel():
+        raise ValueError("src/dst must be int32 tensors of equal length")
+    if src.is_cuda != dst.is_cuda:
+        raise ValueError("src and dst must live on the same side")
+    flags = RAFTGP_DEVICE_PTRS if src.is_cuda else RAFTGP_HOST_PTRS
+    src, dst = src.contiguous(), dst.contiguous()
+    h = c_vp()
+    re = n if row_end is None else row_end
+    _ck(load_library().raftgp_build_csr(ctx.h, n, src.numel(), _ptr(src), _ptr(dst), row_begin, re, flags,
+                                        ctypes.byref(h)))
+    return Graph(ctx, h)
+
+
+# ------------------------------------------------------------------ sketch
+def raftgp_sketch(ctx: Context, seed: int, tag: int, row_begin: int, rows: int, cols: int, den: int,
+                  out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty((rows, cols), dtype=torch.float32, device=ctx.device)
+    _ck(load_library().raftgp_sketch(ctx.h, seed, tag, row_begin, rows, cols, den, _ptr(out)))
+    return out
+
+
+def raftgp_weights(ctx: Context, seed: int, k: int, fan_in: int, fan_out: int,
+                   out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty((fan_in, fan_out), dtype=torch.float32, device=ctx.device)
+    _ck(load_library().raftgp_weights(ctx.h, seed, k, fan_in, fan_out, _ptr(out)))
+    return out
+
+
+# ------------------------------------------------------------------ project / gcn
+def _variant(v) -> int:
+    return VARIANTS[v] if isinstance(v, str) else int(v)
+
+
+def raftgp_project(g: Graph, variant, r: int, seed: int, Y: Optional[torch.Tensor] = None) -> torch.Tensor:
+    if Y is None:
+        Y = torch.empty((g.rows, r), dtype=torch.float32, device=g.ctx.device)
+    _ck(load_library().raftgp_project(g.h, _variant(variant), r, seed, _ptr(Y)))
+    return Y
+
+
+def raftgp_gcn_transform(g: Graph, Z: torch.Tensor, W: torch.Tensor, T: Optional[torch.Tensor] = None):
+    lin, lout = W.shape
+    if T is None:
+        T = torch.empty((g.rows, lout), dtype=torch.float32, device=g.ctx.device)
+    _ck(load_library().raftgp_gcn_transform(g.h, _ptr(Z), lin, _ptr(W), lout, _ptr(T)))
+    return T
+
+
+def raftgp_gcn_hop(g: Graph, T_full: torch.Tensor, Z_out: Optional[torch.Tensor] = None,
+                   W_next: Optional[torch.Tensor] = None, T_next: Optional[torch.Tensor] = None):
+    w = T_full.shape[1]
+    wn = 0 if W_next is None else W_next.shape[1]
+    if W_next is not None and T_next is None:
+        T_next = torch.empty((g.rows, wn), dtype=torch.float32, device=g.ctx.device)
+    _ck(load_library().raftgp_gcn_hop(g.h, _ptr(T_full), w, _ptr(Z_out), _ptr(W_next), wn, _ptr(T_next)))
+    return Z_out, T_next
+
+
+def _zk_array(Zk: Sequence[Optional[torch.Tensor]]):
+    arr = (c_vp * max(1, len(Zk)))()
+    for i, t in enumerate(Zk):
+        arr[i] = None if t is None else t.data_ptr()
+    return arr
+
+
+def raftgp_gnn_embed(g: Graph, dims: Sequence[int], seed: int, Y: torch.Tensor, Z: Optional[torch.Tensor] = None,
+                     intermediates: bool = False):
+    """Returns Z, or (Z, [Z^(1), ..., Z^(K-1)]) when intermediates=True."""
+    dims = [int(d) for d in dims]
+    L = len(dims) - 1
+    dev = g.ctx.device
+    if Z is None:
+        Z = torch.empty((g.rows, dims[-1]), dtype=torch.float32, device=dev)
+    Zk = [torch.empty((g.rows, dims[k]), dtype=torch.float32, device=dev) for k in range(1, L)] if intermediates else []
+    d = (c_i32 * len(dims))(*dims)
+    _ck(load_library().raftgp_gnn_embed(g.h, L, d, seed, _ptr(Y), _ptr(Z),
+                                        _zk_array(Zk) if intermediates else None))
+    return (Z, Zk) if intermediates else Z
+
+
+def raftgp_embed(g: Graph, variant, dims: Sequence[int], seed: int, Y: Optional[torch.Tensor] = None,
+                 Z: Optional[torch.Tensor] = None, want_Y: bool = True, intermediates: bool = False):
+    """Fused project + gnn_embed. Returns (Y or None, Z[, Zk])."""
+    dims = [int(d) for d in dims]
+    L = len(dims) - 1
+    dev = g.ctx.device
+    if Y is None and want_Y:
+        Y = torch.empty((g.rows, dims[0]), dtype=torch.float32, device=dev)
+    if Z is None:
+        Z = torch.empty((g.rows, dims[-1]), dtype=torch.float32, device=dev)
+    Zk = [torch.empty((g.rows, dims[k]), dtype=torch.float32, device=dev) for k in range(1, L)] if intermediates else []
+    d = (c_i32 * len(dims))(*dims)
+    _ck(load_library().raftgp_embed(g.h, _variant(variant), L, d, seed, _ptr(Y), _ptr(Z),
+                                    _zk_array(Zk) if intermediates else None))
+    return (Y, Z, Zk) if intermediates else (Y, Z)
+
+
+# ------------------------------------------------------------------ scoring (host)
+def _labels(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a), np.int32)
+
+
+def raftgp_modularity(g: Graph, assign, k: int) -> float:
+    a = _labels(assign)
+    out = c_dbl(0)
+    _ck(load_library().raftgp_modularity(g.h, c_vp(a.ctypes.data), k, ctypes.byref(out)))
+    return out.value
+
+
+def raftgp_ncut(g: Graph, assign, k: int) -> float:
+    a = _labels(assign)
+    out = c_dbl(0)
+    _ck(load_library().raftgp_ncut(g.h, c_vp(a.ctypes.data), k, ctypes.byref(out)))
+    return out.value
+
+
+def raftgp_local_modularity(g: Graph, nodes, block_of_node, k: int) -> float:
+    nd = np.ascontiguousarray(np.asarray(nodes), np.int64)
+    b = _labels(block_of_node)
+    out = c_dbl(0)
+    _ck(load_library().raftgp_local_modularity(g.h, c_vp(nd.ctypes.data), nd.size, c_vp(b.ctypes.data), k,
+                                               ctypes.byref(out)))
+    return out.value
