@@ -65,8 +65,8 @@ typedef enum {
 RAFTGP_API const char *raftgp_last_error(void);          /* thread-local message of the last non-OK status */
 RAFTGP_API const char *raftgp_version(void);
 
-/* device: CUDA ordinal. cuda_stream: a cudaStream_t to enqueue on (NULL = a new non-blocking stream
- * owned by the context). */
+/* device: CUDA ordinal. cuda_stream: the cudaStream_t every call of this context enqueues on (NULL =
+ * the legacy default stream). The stream stays owned by the caller and must outlive the context. */
 RAFTGP_API raftgp_status raftgp_ctx_create(int device, void *cuda_stream, raftgp_ctx *out);
 RAFTGP_API raftgp_status raftgp_ctx_destroy(raftgp_ctx ctx);
 RAFTGP_API raftgp_status raftgp_ctx_sync(raftgp_ctx ctx);                     /* synchronous */

@@ -117,16 +117,8 @@ raftgp_status raftgp_ctx_create(int device, void *cuda_stream, raftgp_ctx *out) 
     RG_CUDA(cudaSetDevice(device));
     raftgp_ctx c = new raftgp_ctx_s();
     c->device = device;
-    if (cuda_stream) {
-        c->stream = static_cast<cudaStream_t>(cuda_stream);
-    } else {
-        cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
-        if (e != cudaSuccess) {
-            delete c;
-            return cuda_fail(e, "cudaStreamCreate");
-        }
-        c->own_stream = true;
-    }
+    c->stream = static_cast<cudaStream_t>(cuda_stream);   // NULL = the legacy default stream
+    c->own_stream = false;
     cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
     // keep freed blocks in the stream-ordered pool (hot calls then never hit the driver allocator)
     cudaMemPool_t pool;

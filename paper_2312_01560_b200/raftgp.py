@@ -8,6 +8,7 @@ Function names are the C-ABI names; `Context` and `Graph` wrap the two opaque ha
 """
 from __future__ import annotations
 
+import atexit
 import ctypes
 import os
 from typing import Optional, Sequence
@@ -35,6 +36,15 @@ EXPORTS = (
 )
 
 _lib = None
+_exiting = False
+
+
+def _mark_exit():
+    global _exiting
+    _exiting = True
+
+
+atexit.register(_mark_exit)   # no library calls from __del__ once the interpreter (and CUDA) shut down
 c_i32, c_i64, c_u32, c_u64, c_vp, c_dbl = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64,
                                            ctypes.c_void_p, ctypes.c_double)
 P = ctypes.POINTER
@@ -150,9 +160,9 @@ class Context:
         return v.value
 
     def close(self):
-        if getattr(self, "h", None) is not None and _lib is not None:
+        if getattr(self, "h", None) is not None and _lib is not None and not _exiting:
             _lib.raftgp_ctx_destroy(self.h)
-            self.h = None
+        self.h = None
 
     def __del__(self):
         try:
@@ -204,9 +214,9 @@ class Graph:
         _ck(load_library().raftgp_graph_set_degrees(self.h, _ptr(_dev(deg_all.contiguous(), "deg_all"))))
 
     def close(self):
-        if getattr(self, "h", None) is not None and _lib is not None:
+        if getattr(self, "h", None) is not None and _lib is not None and not _exiting:
             _lib.raftgp_graph_destroy(self.h)
-            self.h = None
+        self.h = None
 
     def __del__(self):
         try:
