@@ -18,7 +18,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -42,41 +41,56 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--clock-period-ms", type=int, default=200)
+    ap.add_argument("--clock-query", default=None)
+    ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--no-fuse-variants", action="store_true",
+                    help="one raftgp_embed per variant instead of raftgp_embed_multi (shared Theta gather)")
     return ap.parse_args()
 
 
 # ------------------------------------------------------------------ helpers
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """Clocks + throttle reasons during the timed region: ONE `nvidia-smi -lms 200` process started before
+    the region and stopped after it (no fork inside the timed region)."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_ms: int = 200, enabled: bool = True, query: str = None):
         self.index = index
+        self.period_ms = period_ms
+        self.enabled = enabled
+        self.query = query or self.Q
         self.rows = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                for line in out.stdout.strip().splitlines():
-                    self.rows.append([x.strip() for x in line.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        self._p = None
+        self._f = None
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        import tempfile
+        self._f = tempfile.TemporaryFile(mode="w+")
+        if not self.enabled:
+            return self
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.query}",
+                                        "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
+                                       stdout=self._f, stderr=subprocess.DEVNULL)
+            time.sleep(0.5)
+        except Exception:
+            self._p = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._p is not None:
+            self._p.terminate()
+            try:
+                self._p.wait(timeout=5)
+            except Exception:
+                self._p.kill()
+        self._f.seek(0)
+        for line in self._f.read().strip().splitlines():
+            self.rows.append([x.strip() for x in line.split(",")])
+        self._f.close()
 
     def summary(self):
         if not self.rows:
@@ -107,11 +121,15 @@ def work_units(nnz, n, r, dims, nvar):
     return nvar * u
 
 
-def algorithmic_bytes(nnz, n, r, dims, nvar, kernel):
+def algorithmic_bytes(nnz, n, r, dims, nvar, kernel, fused_pair=False):
     """SURVEY.md §8(d) gather model per launch, summed over one step's launches of that kernel:
-    B_h = 8(N+1) + 4 nnz + 4 w_h G_h + 4 w'_h N + 4 N."""
+    B_h = 8(N+1) + 4 nnz + 4 w_h G_h + 4 w'_h N + 4 N. With fused_pair the NCUT and MOD feature hops share
+    one launch (one gather of Theta, two written T1 blocks)."""
     L = len(dims) - 1
     if kernel == "feature_hop":
+        if fused_pair:
+            b = 8 * (n + 1) + 4 * nnz + 4 * r * nnz + 2 * 4 * dims[1] * n + 4 * n
+            return b + (nvar - 2) * (b - 4 * dims[1] * n), nvar - 1
         b = 8 * (n + 1) + 4 * nnz + 4 * r * nnz + 4 * dims[1] * n + 4 * n
         return nvar * b, nvar
     if kernel == "gcn_hop":
@@ -240,11 +258,17 @@ def main():
     rows = re - rb
     Zbuf = {v: torch.empty((rows, dims[-1]), dtype=torch.float32, device=dev) for v in variants}
 
+    fused_pair = (not args.no_fuse_variants) and "ncut" in variants and "mod" in variants
+
     def step_single(src, dst, out_host=None):
         g = rg.raftgp_build_csr(ctx, gr.n, src, dst)
-        for v in variants:
-            rg.raftgp_embed(g, v, dims, args.seed, Z=Zbuf[v], want_Y=False)
-            if out_host is not None:
+        if args.no_fuse_variants:
+            for v in variants:
+                rg.raftgp_embed(g, v, dims, args.seed, Z=Zbuf[v], want_Y=False)
+        else:
+            rg.raftgp_embed_multi(g, variants, dims, args.seed, Z=Zbuf)
+        if out_host is not None:
+            for v in variants:
                 out_host[v].copy_(Zbuf[v], non_blocking=True)
         nnz = g.info()["nnz_local"]
         g.close()
@@ -294,7 +318,7 @@ def main():
     ctx.set_profiling(True)
     ctx.launch_count(reset=True)
     barrier()
-    with ClockSampler(dev.index) as clocks:
+    with ClockSampler(dev.index, args.clock_period_ms, not args.no_clocks, args.clock_query) as clocks:
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
@@ -320,7 +344,7 @@ def main():
         if k not in prof:
             continue
         b_step, l_step = algorithmic_bytes(nnz if world == 1 else nnz_local, rows if world > 1 else gr.n, cfg.r, dims,
-                                           len(variants), k)
+                                           len(variants), k, fused_pair and world == 1)
         t_step = prof[k][0] / args.steps * 1e-3
         ach = b_step / t_step / 1e9
         hop_stats[k] = {"gb_s": ach, "ms_per_step": t_step * 1e3, "launches_per_step": prof[k][1] / args.steps,
@@ -374,7 +398,8 @@ def main():
             "config": {"workload": f"{cfg.name}: DC-SBM N={gr.n:,} K={gr.info['k']} nnz={nnz:,} r={cfg.r} "
                                    f"dims={list(dims)} variants={'+'.join(variants)}",
                        "n": gr.n, "nnz": nnz, "m_raw_pairs": m, "r": cfg.r, "dims": list(dims), "variants": variants,
-                       "rule": args.rule, "parallelism": f"rowpart{world}" if world > 1 else "single",
+                       "rule": args.rule, "fused_variant_pair": fused_pair and world == 1,
+                       "parallelism": f"rowpart{world}" if world > 1 else "single",
                        "l2": "inputs larger than L2 (gathered operands >= 1.28 GB vs 126 MB L2); no flush"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks.summary(),

@@ -167,6 +167,16 @@ RAFTGP_API raftgp_status raftgp_gnn_embed(raftgp_graph g, int32_t layers, const 
 RAFTGP_API raftgp_status raftgp_embed(raftgp_graph g, raftgp_variant variant, int32_t layers, const int32_t *dims,
                            uint64_t seed, float *Y_dev, float *Z_dev, float *const *Zk_dev);
 
+/* Several feature operators of the same graph in one call (the RaftGP-C and RaftGP-M embeddings of
+ * PAPER.md:289 side by side): Theta is generated once, and when both NCUT and MOD are requested their
+ * feature hops share ONE gather of Theta (Y_ncut and Y_mod come out of the same pass; their arithmetic
+ * per row is identical to raftgp_embed's). variants: host int32[nvariants] (distinct raftgp_variant
+ * values). Y_dev: NULL or host array of nvariants device pointers (NULL entries skipped). Z_dev: host
+ * array of nvariants device pointers (n x dims[layers]). Same errors as raftgp_embed. */
+RAFTGP_API raftgp_status raftgp_embed_multi(raftgp_graph g, int32_t nvariants, const int32_t *variants, int32_t layers,
+                                            const int32_t *dims, uint64_t seed, float *const *Y_dev,
+                                            float *const *Z_dev);
+
 /* ---------------------------------------------------------------- a7: scoring (host, synchronous)
  * On a whole-graph handle. assign: host int32[n] labels in [0, k).
  * Modularity, Eq. 3. Errors: PARAM (label outside [0,k), k <= 0), DATA (2e = 0). */

@@ -18,7 +18,7 @@ namespace raftgp {
 
 const char *const kKernelNames[K_NUM] = {
     "csr_count", "scan", "csr_scatter", "csr_sort_warp", "csr_sort_block", "csr_compact", "degree_scalars",
-    "sketch", "g_partials", "g_final", "feature_hop", "transform", "gcn_hop", "hop_generic", "misc"};
+    "sketch", "g_partials", "g_final", "feature_hop", "transform", "gcn_hop", "hop_generic", "misc", "csr_partition", "csr_bucket_sort"};
 
 static thread_local std::string g_last_error;
 
@@ -62,18 +62,58 @@ LaunchScope::~LaunchScope() {
     }
 }
 
+static size_t round_block(size_t bytes) {
+    const size_t mb = size_t(1) << 20;
+    if (bytes >= mb) return (bytes + 2 * mb - 1) / (2 * mb) * (2 * mb);
+    return (bytes + 511) / 512 * 512;
+}
+
+// Stream-ordered workspace: every user of a block runs on ctx->stream, so a block released by dfree may
+// be handed out again immediately — the next user is ordered after the previous one on the stream.
 raftgp_status dalloc(raftgp_ctx ctx, void **p, size_t bytes) {
-    cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 16, ctx->stream);
+    const size_t want = round_block(bytes ? bytes : 16);
+    auto it = ctx->free_blocks.lower_bound(want);
+    if (it != ctx->free_blocks.end() && it->first <= want + want / 4 + (size_t(2) << 20)) {
+        *p = it->second;
+        ctx->live_blocks[it->second] = it->first;
+        ctx->cached_bytes -= it->first;
+        ctx->free_blocks.erase(it);
+        return RAFTGP_OK;
+    }
+    cudaError_t e = cudaMallocAsync(p, want, ctx->stream);
+    if (e == cudaErrorMemoryAllocation && !ctx->free_blocks.empty()) {   // give the cache back, retry once
+        cudaGetLastError();
+        for (auto &kv : ctx->free_blocks) cudaFreeAsync(kv.second, ctx->stream);
+        ctx->free_blocks.clear();
+        ctx->cached_bytes = 0;
+        cudaStreamSynchronize(ctx->stream);
+        e = cudaMallocAsync(p, want, ctx->stream);
+    }
     if (e != cudaSuccess) {
         *p = nullptr;
         cudaGetLastError();
         return cuda_fail(e, "cudaMallocAsync");
     }
+    ctx->live_blocks[*p] = want;
     return RAFTGP_OK;
 }
 
 void dfree(raftgp_ctx ctx, void *p) {
-    if (p) cudaFreeAsync(p, ctx->stream);
+    if (!p) return;
+    auto it = ctx->live_blocks.find(p);
+    if (it == ctx->live_blocks.end()) {
+        cudaFreeAsync(p, ctx->stream);
+        return;
+    }
+    ctx->free_blocks.emplace(it->second, p);
+    ctx->cached_bytes += it->second;
+    ctx->live_blocks.erase(it);
+}
+
+void release_cache(raftgp_ctx ctx) {
+    for (auto &kv : ctx->free_blocks) cudaFreeAsync(kv.second, ctx->stream);
+    ctx->free_blocks.clear();
+    ctx->cached_bytes = 0;
 }
 
 }  // namespace raftgp
@@ -140,6 +180,8 @@ raftgp_status raftgp_ctx_destroy(raftgp_ctx ctx) {
         cudaEventDestroy(r.stop);
     }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
+    release_cache(ctx);
+    cudaStreamSynchronize(ctx->stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return RAFTGP_OK;
@@ -449,6 +491,51 @@ raftgp_status raftgp_embed(raftgp_graph g, raftgp_variant variant, int32_t layer
     if (st == RAFTGP_OK) st = gcn_stack(g, layers, dims, seed, T1, Z_dev, Zk_dev);
     dfree(ctx, W1);
     dfree(ctx, T1);
+    return st;
+    RG_GUARD_END
+}
+
+raftgp_status raftgp_embed_multi(raftgp_graph g, int32_t nvariants, const int32_t *variants, int32_t layers,
+                                 const int32_t *dims, uint64_t seed, float *const *Y_dev, float *const *Z_dev) {
+    RG_GUARD_BEGIN
+    RG_TRY(need_ready(g));
+    RG_TRY(whole_graph(g));
+    RG_TRY(check_dims(layers, dims));
+    if (nvariants < 1 || !variants || !Z_dev) return fail(RAFTGP_ERR_PARAM, "need >= 1 variant and Z outputs");
+    int where[3] = {-1, -1, -1};
+    for (int v = 0; v < nvariants; ++v) {
+        RG_TRY(check_variant(g, variants[v], dims[0]));
+        if (where[variants[v]] >= 0) return fail(RAFTGP_ERR_PARAM, "variant listed twice");
+        where[variants[v]] = v;
+        if (g->n > 0 && !Z_dev[v]) return fail(RAFTGP_ERR_PARAM, "null Z");
+    }
+    RG_TRY(set_device(g->ctx));
+    raftgp_ctx ctx = g->ctx;
+    const int32_t r = dims[0];
+    float *theta = nullptr, *W1 = nullptr;
+    double *gvec = nullptr;
+    std::vector<float *> T1(nvariants, nullptr);
+    raftgp_status st = dalloc_t(ctx, &theta, (size_t)g->n * r);
+    if (st == RAFTGP_OK && where[RAFTGP_MOD] >= 0) st = dalloc_t(ctx, &gvec, (size_t)r);
+    if (st == RAFTGP_OK) st = sketch_theta(g, seed, r, theta, gvec);
+    if (st == RAFTGP_OK) st = dalloc_t(ctx, &W1, (size_t)dims[0] * dims[1]);
+    if (st == RAFTGP_OK) st = sketch_fill(ctx, seed, 1u, 0, dims[0], dims[1], dims[0], W1);
+    for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v) st = dalloc_t(ctx, &T1[v], (size_t)g->n * dims[1]);
+    auto Yp = [&](int v) { return Y_dev ? Y_dev[v] : nullptr; };
+    const bool dual = where[RAFTGP_NCUT] >= 0 && where[RAFTGP_MOD] >= 0;
+    if (st == RAFTGP_OK && dual) {
+        const int a = where[RAFTGP_NCUT], b = where[RAFTGP_MOD];
+        st = feature_hop_dual(g, r, theta, gvec, Yp(a), Yp(b), W1, dims[1], T1[a], T1[b]);
+    }
+    for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v) {
+        if (dual && (variants[v] == RAFTGP_NCUT || variants[v] == RAFTGP_MOD)) continue;
+        st = feature_hop(g, variants[v], r, theta, gvec, Yp(v), W1, dims[1], T1[v]);
+    }
+    dfree(ctx, theta);
+    dfree(ctx, gvec);
+    for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v) st = gcn_stack(g, layers, dims, seed, T1[v], Z_dev[v], nullptr);
+    dfree(ctx, W1);
+    for (auto t : T1) dfree(ctx, t);
     return st;
     RG_GUARD_END
 }

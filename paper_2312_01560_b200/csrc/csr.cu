@@ -20,6 +20,8 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -156,29 +158,27 @@ __global__ void csr_scatter(const int32_t *__restrict__ src, const int32_t *__re
 // Work is split over `nthr` threads with index t; `sync` is the barrier between stages.
 template <typename Sync>
 __device__ __forceinline__ void bitonic_any(int32_t *a, int len, int t, int nthr, Sync sync) {
-    int P = 1;
-    while (P < len) P <<= 1;
-    for (int k = 2; k <= P; k <<= 1) {
-        // flip stage: i in lower half of each k-block paired with its mirror
-        for (int x = t; x < P / 2; x += nthr) {
-            const int blk = x / (k / 2);
-            const int off = x % (k / 2);
-            const int i = blk * k + off;
-            const int j = blk * k + k - 1 - off;
+    int lg = 0;
+    while ((1 << lg) < len) ++lg;
+    const int half = (1 << lg) >> 1;      // compare-exchange pairs per stage
+    for (int lk = 1; lk <= lg; ++lk) {
+        // flip stage of block size k = 2^lk: i in the lower half of its k-block, partner = its mirror
+        const int lh = lk - 1;
+        for (int x = t; x < half; x += nthr) {
+            const int i = ((x >> lh) << lk) | (x & ((1 << lh) - 1));
+            const int j = i ^ ((1 << lk) - 1);
             if (j < len) {
-                int32_t ai = a[i], aj = a[j];
+                const int32_t ai = a[i], aj = a[j];
                 if (ai > aj) { a[i] = aj; a[j] = ai; }
             }
         }
         sync();
-        for (int h = k / 4; h >= 1; h >>= 1) {
-            for (int x = t; x < P / 2; x += nthr) {
-                const int blk = x / h;
-                const int off = x % h;
-                const int i = blk * 2 * h + off;
-                const int j = i + h;
+        for (int lj = lk - 2; lj >= 0; --lj) {
+            for (int x = t; x < half; x += nthr) {
+                const int i = ((x >> lj) << (lj + 1)) | (x & ((1 << lj) - 1));
+                const int j = i + (1 << lj);
                 if (j < len) {
-                    int32_t ai = a[i], aj = a[j];
+                    const int32_t ai = a[i], aj = a[j];
                     if (ai > aj) { a[i] = aj; a[j] = ai; }
                 }
             }
@@ -192,6 +192,13 @@ struct WarpSync {
 };
 struct BlockSync {
     __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+// barrier over a group of `nthreads` threads (named barrier `id`, 1..15)
+struct GroupSync {
+    int id, nthreads;
+    __device__ __forceinline__ void operator()() const {
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+    }
 };
 
 // warp register bitonic sort of 32 values (ascending by lane)
@@ -212,13 +219,17 @@ __device__ __forceinline__ int32_t warp_sort32(int32_t v, int lane) {
 }
 
 // one warp per row; rows longer than kWarpSortCap are pushed to big_rows
-__global__ void __launch_bounds__(256) csr_sort_warp(int64_t nl, const int64_t *__restrict__ raw_ptr,
+__global__ void __launch_bounds__(256) csr_sort_warp(int64_t nl, const int64_t *__restrict__ rows_list,
+                                                     const int32_t *__restrict__ rows_count,
+                                                     const int64_t *__restrict__ raw_ptr,
                                                      int32_t *__restrict__ col_raw, int32_t *__restrict__ deg,
                                                      int64_t *__restrict__ big_rows, int32_t *__restrict__ big_count) {
     __shared__ int32_t sh[8][kWarpSortCap];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t warps = (int64_t)gridDim.x * 8;
-    for (int64_t row = (int64_t)blockIdx.x * 8 + wib; row < nl; row += warps) {
+    const int64_t nrows = rows_list ? *rows_count : nl;
+    for (int64_t it = (int64_t)blockIdx.x * 8 + wib; it < nrows; it += warps) {
+        const int64_t row = rows_list ? rows_list[it] : it;
         const int64_t beg = raw_ptr[row];
         const int len = static_cast<int>(raw_ptr[row + 1] - beg);
         int32_t *a = col_raw + beg;
@@ -296,6 +307,202 @@ __global__ void __launch_bounds__(1024) csr_sort_block(const int64_t *__restrict
     }
 }
 
+// ---------------------------------------------------------------- bucketed build (main path)
+// Rows are grouped in buckets of B = 2^shift consecutive rows. Pass "partition" moves every directed entry
+// (local row, neighbour) into its bucket's region of `pairs` (the bucket's rows' raw segments, back to
+// back): per tile a shared-memory histogram, ONE global atomic per (tile, bucket) to reserve space, then
+// shared-memory ranks — no per-entry global atomics. Pass "bucket_sort" gives each bucket to one CTA, which
+// places the entries into their rows in shared memory, sorts and dedups every row (one warp per row) and
+// writes the unique prefix of each row to col_raw. Buckets that do not fit shared memory are placed into
+// col_raw in global memory and their rows handed to the warp / block sort kernels above.
+constexpr int kPartTile = 131072;       // raw pairs per partition tile
+constexpr int kMaxBuckets = 12288;      // partition smem: 12 B per bucket
+constexpr int kMaxBucketRows = 4096;    // bucket_sort smem for row cursors/offsets
+constexpr int kBucketCap = 44032;       // entries of one bucket held in shared memory (172 KB)
+constexpr int kGroupRow = 256;          // rows longer than this are sorted by a group of 4 warps
+
+__global__ void __launch_bounds__(1024) csr_partition(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
+                                                      int64_t m, int64_t n, int64_t rb, int64_t re, int shift, int nb,
+                                                      const int64_t *__restrict__ raw_ptr,
+                                                      unsigned long long *__restrict__ bcur, int2 *__restrict__ pairs) {
+    extern __shared__ long long psm[];
+    long long *base = psm;                                              // nb
+    unsigned int *hist = reinterpret_cast<unsigned int *>(psm + nb);    // nb
+    const int64_t ntiles = (m + kPartTile - 1) / kPartTile;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t e0 = tile * kPartTile;
+        const int64_t e1 = min(m, e0 + (int64_t)kPartTile);
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
+        __syncthreads();
+        for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+            const int32_t u = __ldg(src + e), v = __ldg(dst + e);
+            if (u < 0 || v < 0 || u >= n || v >= n || u == v) continue;
+            if (u >= rb && u < re) atomicAdd(&hist[(u - rb) >> shift], 1u);
+            if (v >= rb && v < re) atomicAdd(&hist[(v - rb) >> shift], 1u);
+        }
+        __syncthreads();
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+            const unsigned int h = hist[b];
+            if (h) base[b] = raw_ptr[(int64_t)b << shift] + (long long)atomicAdd(&bcur[b], (unsigned long long)h);
+            hist[b] = 0u;
+        }
+        __syncthreads();
+        for (int64_t eb = e0 + threadIdx.x; eb < e1; eb += 4 * (int64_t)blockDim.x) {
+            int32_t us[4], vs[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int64_t e = eb + (int64_t)k * blockDim.x;
+                us[k] = e < e1 ? __ldg(src + e) : -1;
+                vs[k] = e < e1 ? __ldg(dst + e) : -1;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int32_t u = us[k], v = vs[k];
+                if (u < 0 || v < 0 || u >= n || v >= n || u == v) continue;
+                if (u >= rb && u < re) {
+                    const int b = static_cast<int>((u - rb) >> shift);
+                    pairs[base[b] + atomicAdd(&hist[b], 1u)] = make_int2(static_cast<int32_t>(u - rb), v);
+                }
+                if (v >= rb && v < re) {
+                    const int b = static_cast<int>((v - rb) >> shift);
+                    pairs[base[b] + atomicAdd(&hist[b], 1u)] = make_int2(static_cast<int32_t>(v - rb), u);
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// warp sort + dedup of one row held in shared memory; writes the unique prefix to outp, returns its length
+__device__ __forceinline__ int warp_sort_dedup(int32_t *a, int len, int32_t *outp, int lane) {
+    if (len <= 32) {
+        int32_t v = lane < len ? a[lane] : INT_MAX;
+        v = warp_sort32(v, lane);
+        const int32_t prev = __shfl_up_sync(0xffffffffu, v, 1);
+        const bool keep = lane < len && (lane == 0 || v != prev);
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) outp[__popc(bal & ((1u << lane) - 1u))] = v;
+        return __popc(bal);
+    }
+    bitonic_any(a, len, lane, 32, WarpSync());
+    int written = 0;
+    for (int base = 0; base < len; base += 32) {
+        const int x = base + lane;
+        const int32_t v = x < len ? a[x] : INT_MAX;
+        const bool keep = x < len && (x == 0 || v != a[x - 1]);
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) outp[written + __popc(bal & ((1u << lane) - 1u))] = v;
+        written += __popc(bal);
+    }
+    return written;
+}
+
+__global__ void __launch_bounds__(1024) csr_bucket_sort(const int2 *__restrict__ pairs,
+                                                        const int64_t *__restrict__ raw_ptr, int64_t nl, int shift,
+                                                        int nb, int32_t *__restrict__ col_raw,
+                                                        int32_t *__restrict__ deg, int64_t *__restrict__ fb_rows,
+                                                        int32_t *__restrict__ fb_count) {
+    extern __shared__ int32_t bsm[];
+    int32_t *s = bsm;                                   // kBucketCap values
+    int32_t *cur = bsm + kBucketCap;                    // B cursors
+    int32_t *off = cur + kMaxBucketRows;                // B + 1 offsets (relative to the bucket start)
+    int32_t *big = off + kMaxBucketRows + 1;            // rows longer than 32, longest work first
+    __shared__ int fb_base, nbig, qnext;
+    const int lane = threadIdx.x & 31;
+    constexpr int kLoadBatch = 8;
+    for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+        const int64_t r0 = (int64_t)b << shift;
+        const int nr = static_cast<int>(min(nl, r0 + ((int64_t)1 << shift)) - r0);
+        const int64_t e0 = raw_ptr[r0];
+        const int64_t E = raw_ptr[r0 + nr] - e0;
+        const bool fits = E <= kBucketCap;
+        if (threadIdx.x == 0) {
+            nbig = 0;
+            qnext = 0;
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t <= nr; t += blockDim.x) {
+            off[t] = static_cast<int32_t>(fits ? raw_ptr[r0 + t] - e0 : 0);
+            if (t < nr) {
+                cur[t] = 0;
+                if (fits && raw_ptr[r0 + t + 1] - raw_ptr[r0 + t] > kGroupRow) big[atomicAdd(&nbig, 1)] = t;
+            }
+        }
+        __syncthreads();
+        if (fits) {
+            // placement: batched loads for memory-level parallelism, warp-aggregated slot claims per row
+            for (int64_t i0 = (int64_t)threadIdx.x * kLoadBatch; i0 < E; i0 += (int64_t)blockDim.x * kLoadBatch) {
+                int2 p[kLoadBatch];
+#pragma unroll
+                for (int k = 0; k < kLoadBatch; ++k)
+                    p[k] = (i0 + k < E) ? pairs[e0 + i0 + k] : make_int2(-1, 0);
+#pragma unroll
+                for (int k = 0; k < kLoadBatch; ++k) {
+                    if (p[k].x >= 0) {
+                        const int lr = static_cast<int>(p[k].x - r0);
+                        s[off[lr] + atomicAdd(&cur[lr], 1)] = p[k].y;
+                    }
+                }
+            }
+            __syncthreads();
+            // long rows (> kGroupRow, the hubs): 8 groups of 4 warps, one row per group at a time
+            const int nbr = nbig;
+            const int wid = threadIdx.x >> 5, grp = wid >> 2, gt = threadIdx.x & 127;
+            const GroupSync gsync{1 + grp, 128};
+            for (int q = grp; q < nbr; q += 8) {
+                const int t = big[q];
+                int32_t *a = s + off[t];
+                const int len = off[t + 1] - off[t];
+                bitonic_any(a, len, gt, 128, gsync);
+                // dedup: running count over 128-wide chunks (group-shared partial counts in `cur`)
+                int written = 0;
+                for (int base = 0; base < len; base += 128) {
+                    const int x = base + gt;
+                    const int32_t v = x < len ? a[x] : INT_MAX;
+                    const bool keep = x < len && (x == 0 || v != a[x - 1]);
+                    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+                    const int lw = gt >> 5;
+                    int32_t *wc = cur + grp * 4;        // cursors are free after placement
+                    if (lane == 0) wc[lw] = __popc(bal);
+                    gsync();
+                    int before = 0, total = 0;
+                    for (int w = 0; w < 4; ++w) {
+                        if (w < lw) before += wc[w];
+                        total += wc[w];
+                    }
+                    if (keep) col_raw[e0 + off[t] + written + before + __popc(bal & ((1u << lane) - 1u))] = v;
+                    written += total;
+                    gsync();
+                }
+                if (gt == 0) deg[r0 + t] = written;
+            }
+            // all other rows: one warp per row, fetched dynamically
+            for (;;) {
+                int t = 0;
+                if (lane == 0) t = atomicAdd(&qnext, 1);
+                t = __shfl_sync(0xffffffffu, t, 0);
+                if (t >= nr) break;
+                const int len = off[t + 1] - off[t];
+                if (len > kGroupRow) continue;
+                const int w = warp_sort_dedup(s + off[t], len, col_raw + e0 + off[t], lane);
+                if (lane == 0) deg[r0 + t] = w;
+            }
+        } else {
+            // too large for shared memory: place into col_raw (global), rows go to the warp/block sort kernels
+            for (int64_t idx = threadIdx.x; idx < E; idx += blockDim.x) {
+                const int2 p = pairs[e0 + idx];
+                const int64_t row = p.x;
+                const int64_t k = atomicAdd(&cur[row - r0], 1);
+                col_raw[raw_ptr[row] + k] = p.y;
+            }
+            if (threadIdx.x == 0) fb_base = atomicAdd(fb_count, nr);
+            __syncthreads();
+            for (int t = threadIdx.x; t < nr; t += blockDim.x) fb_rows[fb_base + t] = r0 + t;
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void csr_compact(int64_t nl, const int64_t *__restrict__ raw_ptr, const int32_t *__restrict__ col_raw,
                             const int64_t *__restrict__ row_ptr, int32_t *__restrict__ col) {
     const int lane = threadIdx.x & 31;
@@ -307,11 +514,14 @@ __global__ void csr_compact(int64_t nl, const int64_t *__restrict__ raw_ptr, con
     }
 }
 
-// deg_all -> s, s^ ; two_e = sum deg (int64) via one atomic per block
+// deg_all -> s, s^ ; two_e = sum deg (int64) via one atomic per block; degree histogram (capped bins)
 __global__ void degree_scalars(const int32_t *__restrict__ deg, int64_t n, float *__restrict__ s,
-                               float *__restrict__ sh, unsigned long long *__restrict__ two_e) {
+                               float *__restrict__ sh, unsigned long long *__restrict__ two_e,
+                               unsigned long long *__restrict__ hist) {
     __shared__ unsigned long long part;
+    __shared__ unsigned int hsh[kDegHistBins];
     if (threadIdx.x == 0) part = 0;
+    for (int b = threadIdx.x; b < kDegHistBins; b += blockDim.x) hsh[b] = 0;
     __syncthreads();
     unsigned long long local = 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -320,10 +530,13 @@ __global__ void degree_scalars(const int32_t *__restrict__ deg, int64_t n, float
         local += static_cast<unsigned long long>(d);
         s[i] = d > 0 ? __frsqrt_rn(static_cast<float>(d)) : 0.0f;
         sh[i] = __frsqrt_rn(static_cast<float>(d) + 1.0f);
+        atomicAdd(&hsh[d < kDegHistBins - 1 ? d : kDegHistBins - 1], 1u);
     }
     atomicAdd(&part, local);
     __syncthreads();
     if (threadIdx.x == 0) atomicAdd(two_e, part);
+    for (int b = threadIdx.x; b < kDegHistBins; b += blockDim.x)
+        if (hsh[b]) atomicAdd(&hist[b], static_cast<unsigned long long>(hsh[b]));
 }
 
 }  // namespace
@@ -358,20 +571,21 @@ raftgp_status scan_i32_to_i64(raftgp_ctx ctx, const int32_t *in, int64_t *out, i
 
 raftgp_status degrees_finalize(raftgp_graph g) {
     raftgp_ctx ctx = g->ctx;
-    unsigned long long *d_two_e = nullptr;
-    RG_TRY(dalloc_t(ctx, &d_two_e, 1));
-    RG_CUDA(cudaMemsetAsync(d_two_e, 0, sizeof(unsigned long long), ctx->stream));
+    unsigned long long *d_buf = nullptr;   // [0] = 2e, [1..] = degree histogram
+    RG_TRY(dalloc_t(ctx, &d_buf, 1 + kDegHistBins));
+    RG_CUDA(cudaMemsetAsync(d_buf, 0, sizeof(unsigned long long) * (1 + kDegHistBins), ctx->stream));
     if (g->n > 0) {
-        const int grid = static_cast<int>(std::min<int64_t>(ceil_div(g->n, 256), (int64_t)ctx->sm_count * 8));
+        const int grid = static_cast<int>(std::min<int64_t>(ceil_div(g->n, 256), (int64_t)ctx->sm_count * 4));
         LaunchScope L(ctx, K_DEGREES);
-        degree_scalars<<<grid, 256, 0, ctx->stream>>>(g->deg_all, g->n, g->s_all, g->sh_all, d_two_e);
+        degree_scalars<<<grid, 256, 0, ctx->stream>>>(g->deg_all, g->n, g->s_all, g->sh_all, d_buf, d_buf + 1);
     }
     RG_CHECK_LAUNCH(ctx);
-    unsigned long long h = 0;
-    RG_CUDA(cudaMemcpyAsync(&h, d_two_e, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    std::vector<unsigned long long> h(1 + kDegHistBins, 0);
+    RG_CUDA(cudaMemcpyAsync(h.data(), d_buf, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, ctx->stream));
     RG_CUDA(cudaStreamSynchronize(ctx->stream));
-    dfree(ctx, d_two_e);
-    g->two_e = static_cast<int64_t>(h);
+    dfree(ctx, d_buf);
+    g->two_e = static_cast<int64_t>(h[0]);
+    g->deg_hist.assign(h.begin() + 1, h.end());
     return RAFTGP_OK;
 }
 
@@ -406,32 +620,74 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
     }
     RG_CHECK_LAUNCH(ctx);
     RG_TRY(scan_i32_to_i64(ctx, cnt, raw_ptr, nl));
-    if (m > 0) {
-        LaunchScope L(ctx, K_CSR_SCATTER);
-        csr_scatter<<<egrid, 256, 0, st>>>(src, dst, m, n, rb, re, raw_ptr, cnt, col_raw);
-    }
-    RG_CHECK_LAUNCH(ctx);
+    int shift = 0;
+    while (shift < 31 && ceil_div(nl, (int64_t)1 << shift) > kMaxBuckets) ++shift;
+    const bool bucketed = nl > 0 && ((int64_t)1 << shift) <= kMaxBucketRows;
     const int rgrid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nl, 8), (int64_t)ctx->sm_count * 8)));
-    if (nl > 0) {
+    int64_t *fb_rows = nullptr;
+    int32_t *fb_count = nullptr;
+    if (bucketed) {
+        const int nb = static_cast<int>(ceil_div(nl, (int64_t)1 << shift));
+        unsigned long long *bcur = nullptr;
+        int2 *pairs = nullptr;
+        RG_TRY(dalloc_t(ctx, &bcur, (size_t)nb));
+        RG_TRY(dalloc_t(ctx, &pairs, (size_t)cap));
+        RG_TRY(dalloc_t(ctx, &fb_rows, (size_t)nl));
+        RG_TRY(dalloc_t(ctx, &fb_count, 1));
+        RG_CUDA(cudaMemsetAsync(bcur, 0, sizeof(unsigned long long) * nb, st));
+        RG_CUDA(cudaMemsetAsync(fb_count, 0, sizeof(int32_t), st));
+        static bool attrs = false;
+        if (!attrs) {
+            RG_CUDA(cudaFuncSetAttribute(csr_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 12));
+            RG_CUDA(cudaFuncSetAttribute(csr_bucket_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (kBucketCap + 3 * kMaxBucketRows + 1) * 4));
+            attrs = true;
+        }
+        if (m > 0) {
+            const int pgrid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, kPartTile), ctx->sm_count)));
+            LaunchScope L(ctx, K_CSR_PARTITION);
+            csr_partition<<<pgrid, 1024, (size_t)nb * 12, st>>>(src, dst, m, n, rb, re, shift, nb, raw_ptr, bcur, pairs);
+        }
+        RG_CHECK_LAUNCH(ctx);
+        {
+            LaunchScope L(ctx, K_CSR_BUCKET);
+            csr_bucket_sort<<<std::min(nb, ctx->sm_count), 1024, (size_t)(kBucketCap + 3 * kMaxBucketRows + 1) * 4, st>>>(
+                pairs, raw_ptr, nl, shift, nb, col_raw, g->deg_local, fb_rows, fb_count);
+        }
+        RG_CHECK_LAUNCH(ctx);
         {
             LaunchScope L(ctx, K_CSR_SORT_WARP);
-            csr_sort_warp<<<rgrid, 256, 0, st>>>(nl, raw_ptr, col_raw, g->deg_local, big_rows, big_count);
+            csr_sort_warp<<<rgrid, 256, 0, st>>>(nl, fb_rows, fb_count, raw_ptr, col_raw, g->deg_local, big_rows, big_count);
         }
         RG_CHECK_LAUNCH(ctx);
-        {
-            static bool attr_set = false;
-            if (!attr_set) {
-                RG_CUDA(cudaFuncSetAttribute(csr_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kBlockSortSmemCap * (int)sizeof(int32_t)));
-                attr_set = true;
-            }
-            LaunchScope L(ctx, K_CSR_SORT_BLOCK);
-            csr_sort_block<<<ctx->sm_count, 1024, kBlockSortSmemCap * sizeof(int32_t), st>>>(big_rows, big_count,
-                                                                                             raw_ptr, col_raw,
-                                                                                             g->deg_local);
+        dfree(ctx, bcur);
+        dfree(ctx, pairs);
+    } else {
+        if (m > 0) {
+            LaunchScope L(ctx, K_CSR_SCATTER);
+            csr_scatter<<<egrid, 256, 0, st>>>(src, dst, m, n, rb, re, raw_ptr, cnt, col_raw);
+        }
+        RG_CHECK_LAUNCH(ctx);
+        if (nl > 0) {
+            LaunchScope L(ctx, K_CSR_SORT_WARP);
+            csr_sort_warp<<<rgrid, 256, 0, st>>>(nl, nullptr, nullptr, raw_ptr, col_raw, g->deg_local, big_rows, big_count);
         }
         RG_CHECK_LAUNCH(ctx);
     }
+    if (nl > 0) {
+        static bool attr_set = false;
+        if (!attr_set) {
+            RG_CUDA(cudaFuncSetAttribute(csr_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kBlockSortSmemCap * (int)sizeof(int32_t)));
+            attr_set = true;
+        }
+        LaunchScope L(ctx, K_CSR_SORT_BLOCK);
+        csr_sort_block<<<ctx->sm_count, 1024, kBlockSortSmemCap * sizeof(int32_t), st>>>(big_rows, big_count, raw_ptr,
+                                                                                         col_raw, g->deg_local);
+    }
+    RG_CHECK_LAUNCH(ctx);
+    dfree(ctx, fb_rows);
+    dfree(ctx, fb_count);
     RG_TRY(scan_i32_to_i64(ctx, g->deg_local, g->row_ptr, nl));
     int64_t nnz = 0;
     int herr = 0;

@@ -5,7 +5,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/raftgp.h"
@@ -29,6 +31,8 @@ enum KernelId : int {
     K_GCN_HOP,
     K_GENERIC,
     K_MISC,
+    K_CSR_PARTITION,
+    K_CSR_BUCKET,
     K_NUM
 };
 extern const char *const kKernelNames[K_NUM];
@@ -49,6 +53,11 @@ struct raftgp_ctx_s {
     bool prof = false;
     std::vector<raftgp::ProfRec> recs;
     std::vector<cudaEvent_t> event_pool;
+    // workspace cache: blocks freed by the library are kept (keyed by size) and reused in stream order,
+    // so steady-state calls make no allocator calls at all
+    std::multimap<size_t, void *> free_blocks;
+    std::unordered_map<void *, size_t> live_blocks;
+    size_t cached_bytes = 0;
 };
 
 struct raftgp_graph_s {
@@ -57,11 +66,12 @@ struct raftgp_graph_s {
     int64_t nnz_local = 0;
     int64_t two_e = -1;            // global 2e; -1 until degrees are global
     int64_t *row_ptr = nullptr;    // device int64[nl+1], local offsets
-    int32_t *col = nullptr;        // device int32[nnz_local], global ids
+    int32_t *col = nullptr;        // device int32[nnz_local], global ids (canonical CSR)
     int32_t *deg_local = nullptr;  // device int32[nl]
     int32_t *deg_all = nullptr;    // device int32[n] (global degrees)
     float *s_all = nullptr;        // device fp32[n]: deg^-1/2, 0 for isolated nodes
     float *sh_all = nullptr;       // device fp32[n]: (deg+1)^-1/2
+    std::vector<int64_t> deg_hist;   // host: #nodes per degree (last bin = degree >= kDegHistBins-1)
     // host mirror (scoring), filled lazily
     bool host_valid = false;
     std::vector<int64_t> h_row_ptr;
@@ -107,11 +117,14 @@ struct LaunchScope {
 // ---------------------------------------------------------------- memory (stream-ordered pool)
 raftgp_status dalloc(raftgp_ctx ctx, void **p, size_t bytes);
 void dfree(raftgp_ctx ctx, void *p);
+void release_cache(raftgp_ctx ctx);
 
 template <typename T>
 raftgp_status dalloc_t(raftgp_ctx ctx, T **p, size_t count) {
     return dalloc(ctx, reinterpret_cast<void **>(p), sizeof(T) * (count ? count : 1));
 }
+
+constexpr int kDegHistBins = 4096;
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -120,7 +133,7 @@ inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 
 raftgp_status scan_i32_to_i64(raftgp_ctx ctx, const int32_t *in, int64_t *out, int64_t n);
 raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src, const int32_t *dst, int64_t rb,
                         int64_t re, raftgp_graph g);
-raftgp_status degrees_finalize(raftgp_graph g);   // deg_all -> two_e, s_all, sh_all
+raftgp_status degrees_finalize(raftgp_graph g);   // deg_all -> two_e, s_all, sh_all, deg_hist
 
 raftgp_status sketch_fill(raftgp_ctx ctx, uint64_t seed, uint32_t tag, int64_t row_begin, int64_t rows, int32_t cols,
                           int32_t den, float *out);
@@ -129,6 +142,9 @@ raftgp_status sketch_theta(raftgp_graph g, uint64_t seed, int32_t r, float *thet
 
 raftgp_status feature_hop(raftgp_graph g, int variant, int32_t r, const float *theta, const double *gvec, float *Y,
                           const float *W1, int32_t l1, float *T1);
+// NCut and full-modularity feature hops from ONE gather of Theta (+ both first transforms).
+raftgp_status feature_hop_dual(raftgp_graph g, int32_t r, const float *theta, const double *gvec, float *Y_ncut,
+                               float *Y_mod, const float *W1, int32_t l1, float *T_ncut, float *T_mod);
 raftgp_status gcn_transform(raftgp_graph g, const float *Z, int32_t lin, const float *W, int32_t lout, float *T);
 raftgp_status gcn_hop(raftgp_graph g, const float *Tfull, int32_t w, float *Zout, const float *Wn, int32_t wn,
                       float *Tnext);

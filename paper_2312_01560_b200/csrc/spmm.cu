@@ -28,12 +28,12 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-enum Kind : int { KIND_NCUT = 0, KIND_MOD = 1, KIND_MOD_REDUCED = 2, KIND_GCN = 3, KIND_LOAD = 4 };
+enum Kind : int { KIND_NCUT = 0, KIND_MOD = 1, KIND_MOD_REDUCED = 2, KIND_GCN = 3, KIND_LOAD = 4, KIND_DUAL = 5 };
 
 struct HopArgs {
     int64_t nl, rb, n;
     const int64_t *row_ptr;    // local CSR
-    const int32_t *col;
+    const int32_t *col;        // global neighbour ids
     const float *X;            // operand, n x W (global rows); for KIND_LOAD: local rows x W
     const float *s_all;        // deg^-1/2
     const float *sh_all;       // (deg+1)^-1/2
@@ -43,6 +43,8 @@ struct HopArgs {
     float *out;                // local rows x W (Y or Z'), may be null
     const float *Wn;           // W x WN, may be null
     float *Tn;                 // local rows x WN, may be null
+    float *out2;               // KIND_DUAL: second variant's Y (MOD), may be null
+    float *Tn2;                // KIND_DUAL: second variant's T
 };
 
 __device__ __forceinline__ float4 ldg4(const float4 *p) { return __ldg(p); }
@@ -64,67 +66,107 @@ __device__ __forceinline__ float4 shfl_xor4(const float4 &v, int o) {
                        __shfl_xor_sync(FULL, v.w, o));
 }
 
-// Gather-sum over the neighbours of one row. MODE 0: acc += X_j; 1: acc += s_j X_j; 2: acc += X_j and
-// acc2 += d_j X_j. Lane layout: sub = lane / LPN picks the neighbour slot, cl = lane % LPN the float4
-// column slice. Returns the full row sum in every sub-slot (xor butterfly over sub-slots).
+// Gather modes. SUM: acc += X_j. S: acc += s_j X_j. SUM_D: acc += X_j, acc2 += d_j X_j.
+// SUM_S: acc += X_j, acc2 += s_j X_j (NCut and full modularity from ONE gather of Theta).
+enum Mode : int { M_SUM = 0, M_S = 1, M_SUM_D = 2, M_SUM_S = 3 };
+
+// Gather-sum over the neighbours of one row. Lane layout: sub = lane / LPN picks the neighbour slot,
+// cl = lane % LPN the float4 column slice. Returns the full row sums in every sub-slot (xor butterfly).
+// `c0` is this row's first 32-entry col chunk, loaded by the caller one row ahead; later chunks are
+// prefetched one chunk ahead, so col latency overlaps the row gathers. (L2 eviction-priority hints for
+// high-degree rows were measured and made every hop slower; plain read-only loads are used.)
 template <int W, int U, int MODE>
-__device__ __forceinline__ void gather_row(const HopArgs &a, int64_t beg, int64_t end, int lane, float4 &acc,
-                                           float4 &acc2) {
+__device__ __forceinline__ void gather_row(const HopArgs &a, int64_t beg, int64_t end, int32_t c0, int lane,
+                                           float4 &acc, float4 &acc2) {
     constexpr int LPN = W / 4, NPW = 32 / LPN;
     static_assert(NPW * U <= 32 && 32 % (NPW * U) == 0, "unroll must tile a 32-entry col chunk");
     const int sub = lane / LPN, cl = lane % LPN;
     const float4 *X4 = reinterpret_cast<const float4 *>(a.X);
     acc = make_float4(0.f, 0.f, 0.f, 0.f);
     acc2 = make_float4(0.f, 0.f, 0.f, 0.f);
+    int32_t mycur = c0;
     for (int64_t base = beg; base < end; base += 32) {
         const int cnt = (end - base < 32) ? static_cast<int>(end - base) : 32;
-        const int32_t myj = lane < cnt ? __ldg(a.col + base + lane) : 0;
+        const int64_t nb = base + 32;
+        const int32_t mynext = (nb + lane < end) ? __ldg(a.col + nb + lane) : 0;
+        const int32_t myj = mycur;
         float myw = 0.f;
-        if (MODE == 1) myw = lane < cnt ? __ldg(a.s_all + myj) : 0.f;
-        if (MODE == 2) myw = lane < cnt ? static_cast<float>(__ldg(a.deg_all + myj)) : 0.f;
+        if (MODE == M_S || MODE == M_SUM_S) myw = lane < cnt ? __ldg(a.s_all + myj) : 0.f;
+        if (MODE == M_SUM_D) myw = lane < cnt ? static_cast<float>(__ldg(a.deg_all + myj)) : 0.f;
         for (int k0 = 0; k0 < cnt; k0 += NPW * U) {
             float4 v[U];
-            float w[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int k = k0 + u * NPW + sub;
                 const int32_t j = __shfl_sync(FULL, myj, k);
-                w[u] = (MODE != 0) ? __shfl_sync(FULL, myw, k) : 1.f;
                 v[u] = (k < cnt) ? ldg4(X4 + (int64_t)j * LPN + cl) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                if (MODE == 1) {
-                    fma4(acc, w[u], v[u]);
+                const int k = k0 + u * NPW + sub;
+                if (MODE == M_S) {
+                    fma4(acc, __shfl_sync(FULL, myw, k), v[u]);
                 } else {
                     add4(acc, v[u]);
-                    if (MODE == 2) fma4(acc2, w[u], v[u]);
+                    if (MODE == M_SUM_D || MODE == M_SUM_S) fma4(acc2, __shfl_sync(FULL, myw, k), v[u]);
                 }
             }
         }
+        mycur = mynext;
     }
 #pragma unroll
     for (int o = LPN; o < 32; o <<= 1) {
         add4(acc, shfl_xor4(acc, o));
-        if (MODE == 2) add4(acc2, shfl_xor4(acc2, o));
+        if (MODE == M_SUM_D || MODE == M_SUM_S) add4(acc2, shfl_xor4(acc2, o));
     }
 }
 
-template <int W, int WN, int RB>
-struct HopSmem {
-    static constexpr int kWn = W * WN;       // floats
+#ifndef RG_U_SUM
+#define RG_U_SUM 8
+#endif
+#ifndef RG_U_S
+#define RG_U_S 8
+#endif
+#ifndef RG_U_DUAL
+#define RG_U_DUAL 8
+#endif
+#ifndef RG_U_SUMD
+#define RG_U_SUMD 4
+#endif
+#ifndef RG_WARPS_PER_SM
+#define RG_WARPS_PER_SM 32
+#endif
+#ifndef RG_DUAL_WARPS_PER_SM
+#define RG_DUAL_WARPS_PER_SM 16
+#endif
+
+template <int KIND>
+struct KindTraits {
+    static constexpr int NV = KIND == KIND_DUAL ? 2 : 1;   // output rows per input row
+    // gather steps in flight per lane (register budget: 64 regs at 32 resident warps per SM)
+    static constexpr int U = KIND == KIND_NCUT ? RG_U_S
+                             : KIND == KIND_DUAL ? RG_U_DUAL
+                             : KIND == KIND_MOD_REDUCED ? RG_U_SUMD : RG_U_SUM;
+    // resident warps per SM the kernel is compiled for (sets the register cap)
+    static constexpr int WARPS = KIND == KIND_DUAL ? RG_DUAL_WARPS_PER_SM : RG_WARPS_PER_SM;
+    [[maybe_unused]] static constexpr int MODE = KIND == KIND_NCUT ? M_S
+                                : KIND == KIND_MOD_REDUCED ? M_SUM_D
+                                : KIND == KIND_DUAL ? M_SUM_S : M_SUM;
 };
 
 // One hop for groups of RB consecutive local rows per warp (grid-stride over groups).
 template <int KIND, int W, int WN, int RB, int U, int THREADS>
-__global__ void __launch_bounds__(THREADS, 1024 / THREADS) hop_kernel(HopArgs a) {
+__global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREADS) > 0 ? KindTraits<KIND>::WARPS * 32 / THREADS : 1)
+    hop_kernel(HopArgs a) {
     extern __shared__ float4 smem4[];
     float *smem = reinterpret_cast<float *>(smem4);
     constexpr int LPN = W / 4;
+    constexpr int NV = KindTraits<KIND>::NV;
+    constexpr int NR = NV * RB;                                     // staged rows per warp
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     float *Wsm = smem;                                              // W x WN
-    float *stage = smem + HopSmem<W, WN, RB>::kWn + wib * RB * W;   // RB x W
+    float *stage = smem + W * WN + wib * NR * W;                    // NR x W
     if constexpr (WN > 0) {
         const float4 *src = reinterpret_cast<const float4 *>(a.Wn);
         float4 *dst = reinterpret_cast<float4 *>(Wsm);
@@ -132,42 +174,61 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) hop_kernel(HopArgs a)
         __syncthreads();
     }
     const int sub = lane / LPN, cl = lane % LPN;
-    double g0 = 0, g1 = 0, g2 = 0, g3 = 0;
-    if constexpr (KIND == KIND_MOD) {
-        g0 = a.gvec[4 * cl + 0];
-        g1 = a.gvec[4 * cl + 1];
-        g2 = a.gvec[4 * cl + 2];
-        g3 = a.gvec[4 * cl + 3];
-    }
     const int64_t ngroups = (a.nl + RB - 1) / RB;
     const int64_t gw = (int64_t)gridDim.x * wpb;
     for (int64_t grp = (int64_t)blockIdx.x * wpb + wib; grp < ngroups; grp += gw) {
         const int64_t row0 = grp * RB;
         const int rows_here = (a.nl - row0 < RB) ? static_cast<int>(a.nl - row0) : RB;
+        // first col chunk of the group's first row; each row prefetches the next row's first chunk
+        int64_t beg = 0, end = 0;
+        int32_t c0 = 0;
+        if constexpr (KIND != KIND_LOAD) {
+            beg = a.row_ptr[row0];
+            end = a.row_ptr[row0 + 1];
+            c0 = (beg + lane < end) ? __ldg(a.col + beg + lane) : 0;
+        }
         for (int rr = 0; rr < rows_here; ++rr) {
             const int64_t row = row0 + rr;          // local row
             const int64_t gi = a.rb + row;          // global row id
             float4 acc, acc2;
-            float4 y;
+            float4 y, y2 = make_float4(0.f, 0.f, 0.f, 0.f);
             if constexpr (KIND == KIND_LOAD) {
                 y = ldg4(reinterpret_cast<const float4 *>(a.X) + row * LPN + cl);
             } else {
-                const int64_t beg = a.row_ptr[row], end = a.row_ptr[row + 1];
-                constexpr int MODE = KIND == KIND_NCUT ? 1 : (KIND == KIND_MOD_REDUCED ? 2 : 0);
-                gather_row<W, U, MODE>(a, beg, end, lane, acc, acc2);
+                int64_t nbeg = end, nend = end;
+                int32_t nc0 = 0;
+                if (rr + 1 < rows_here) {
+                    nend = a.row_ptr[row + 2];
+                    nc0 = (nbeg + lane < nend) ? __ldg(a.col + nbeg + lane) : 0;
+                }
+                float4 self = make_float4(0.f, 0.f, 0.f, 0.f);
+                if constexpr (KIND == KIND_GCN) self = ldg4(reinterpret_cast<const float4 *>(a.X) + gi * LPN + cl);
+                gather_row<W, U, KindTraits<KIND>::MODE>(a, beg, end, c0, lane, acc, acc2);
+                beg = nbeg;
+                end = nend;
+                c0 = nc0;
                 if constexpr (KIND == KIND_NCUT) {
                     const float si = __ldg(a.s_all + gi);
                     y = make_float4(si * acc.x, si * acc.y, si * acc.z, si * acc.w);
-                } else if constexpr (KIND == KIND_MOD) {
+                } else if constexpr (KIND == KIND_MOD || KIND == KIND_DUAL) {
                     const double c = static_cast<double>(__ldg(a.deg_all + gi)) * a.inv2e;
-                    y = make_float4(static_cast<float>(acc.x - c * g0), static_cast<float>(acc.y - c * g1),
-                                    static_cast<float>(acc.z - c * g2), static_cast<float>(acc.w - c * g3));
+                    const double2 ga = __ldg(reinterpret_cast<const double2 *>(a.gvec) + 2 * cl);
+                    const double2 gb = __ldg(reinterpret_cast<const double2 *>(a.gvec) + 2 * cl + 1);
+                    const double g0 = ga.x, g1 = ga.y, g2 = gb.x, g3 = gb.y;
+                    const float4 ym = make_float4(static_cast<float>(acc.x - c * g0), static_cast<float>(acc.y - c * g1),
+                                                  static_cast<float>(acc.z - c * g2), static_cast<float>(acc.w - c * g3));
+                    if constexpr (KIND == KIND_DUAL) {
+                        const float si = __ldg(a.s_all + gi);
+                        y = make_float4(si * acc2.x, si * acc2.y, si * acc2.z, si * acc2.w);   // NCut
+                        y2 = ym;                                                                // modularity
+                    } else {
+                        y = ym;
+                    }
                 } else if constexpr (KIND == KIND_MOD_REDUCED) {
                     const double c = static_cast<double>(__ldg(a.deg_all + gi)) * a.inv2e;
                     y = make_float4(static_cast<float>(acc.x - c * acc2.x), static_cast<float>(acc.y - c * acc2.y),
                                     static_cast<float>(acc.z - c * acc2.z), static_cast<float>(acc.w - c * acc2.w));
                 } else {   // KIND_GCN: H_i = s^_i (T_i + sum_j T_j); tanh; row l2 normalisation
-                    const float4 self = ldg4(reinterpret_cast<const float4 *>(a.X) + gi * LPN + cl);
                     add4(acc, self);
                     const float shi = __ldg(a.sh_all + gi);
                     y = make_float4(tanhf(shi * acc.x), tanhf(shi * acc.y), tanhf(shi * acc.z), tanhf(shi * acc.w));
@@ -180,17 +241,23 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) hop_kernel(HopArgs a)
                     }
                 }
             }
-            if (a.out != nullptr && sub == 0) reinterpret_cast<float4 *>(a.out)[row * LPN + cl] = y;
-            if constexpr (WN > 0) {
-                if (sub == 0) reinterpret_cast<float4 *>(stage)[rr * LPN + cl] = y;
+            if (sub == 0) {
+                if (a.out != nullptr) reinterpret_cast<float4 *>(a.out)[row * LPN + cl] = y;
+                if constexpr (NV == 2) {
+                    if (a.out2 != nullptr) reinterpret_cast<float4 *>(a.out2)[row * LPN + cl] = y2;
+                }
+                if constexpr (WN > 0) {
+                    reinterpret_cast<float4 *>(stage)[rr * LPN + cl] = y;
+                    if constexpr (NV == 2) reinterpret_cast<float4 *>(stage)[(RB + rr) * LPN + cl] = y2;
+                }
             }
         }
         if constexpr (WN > 0) {
-            // fused transform: Tn_i = s^_i (y_i W_next) for the rows of this group
+            // fused transform: T_i = s^_i (y_i W_next) for the NR staged rows of this group
             constexpr int OL = WN / 4;        // lanes per output row
             constexpr int RS = 32 / OL;       // rows in parallel
-            constexpr int RR = RB / RS;       // rows per lane
-            static_assert(RR >= 1 && RB % RS == 0, "RB must be a multiple of the parallel row count");
+            constexpr int RR = NR / RS;       // rows per lane
+            static_assert(RR >= 1 && NR % RS == 0, "staged rows must be a multiple of the parallel row count");
             __syncwarp();
             const int rs = lane / OL, oc = lane % OL;
             float4 o[RR];
@@ -217,11 +284,12 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) hop_kernel(HopArgs a)
 #pragma unroll
             for (int q = 0; q < RR; ++q) {
                 const int rr = rs + q * RS;
-                if (rr < rows_here) {
-                    const int64_t row = row0 + rr;
+                const int v = rr / RB, r_in = rr % RB;
+                if (r_in < rows_here) {
+                    const int64_t row = row0 + r_in;
                     const float shi = __ldg(a.sh_all + a.rb + row);
-                    reinterpret_cast<float4 *>(a.Tn)[row * OL + oc] =
-                        make_float4(shi * o[q].x, shi * o[q].y, shi * o[q].z, shi * o[q].w);
+                    float4 *T4 = reinterpret_cast<float4 *>(v == 0 ? a.Tn : a.Tn2);
+                    T4[row * OL + oc] = make_float4(shi * o[q].x, shi * o[q].y, shi * o[q].z, shi * o[q].w);
                 }
             }
             __syncwarp();
@@ -299,10 +367,11 @@ __global__ void __launch_bounds__(128) hop_generic(HopArgs a, int W, int WN) {
 template <int KIND, int W, int WN>
 raftgp_status launch_fast(raftgp_ctx ctx, const HopArgs &a) {
     constexpr int RB = 4;
-    constexpr int U = 8;
+    constexpr int U = KindTraits<KIND>::U;
     constexpr int THREADS = WN > 0 ? 512 : 256;
     constexpr int WPB = THREADS / 32;
-    const size_t smem = sizeof(float) * ((size_t)W * WN + (WN > 0 ? (size_t)WPB * RB * W : 0));
+    constexpr int NV = KindTraits<KIND>::NV;
+    const size_t smem = sizeof(float) * ((size_t)W * WN + (WN > 0 ? (size_t)WPB * NV * RB * W : 0));
     static int blocks_per_sm = -1;
     auto kern = hop_kernel<KIND, W, WN, RB, U, THREADS>;
     if (blocks_per_sm < 0) {
@@ -363,7 +432,7 @@ raftgp_status dispatch(raftgp_ctx ctx, const HopArgs &a, int w, int wn) {
     return RAFTGP_OK;
 }
 
-HopArgs base_args(raftgp_graph g) {
+HopArgs base_args(raftgp_graph g, int32_t /*w*/) {
     HopArgs a{};
     a.nl = g->nl;
     a.rb = g->row_begin;
@@ -381,7 +450,7 @@ HopArgs base_args(raftgp_graph g) {
 
 raftgp_status feature_hop(raftgp_graph g, int variant, int32_t r, const float *theta, const double *gvec, float *Y,
                           const float *W1, int32_t l1, float *T1) {
-    HopArgs a = base_args(g);
+    HopArgs a = base_args(g, r);
     a.X = theta;
     a.gvec = gvec;
     a.out = Y;
@@ -395,8 +464,33 @@ raftgp_status feature_hop(raftgp_graph g, int variant, int32_t r, const float *t
     }
 }
 
+raftgp_status feature_hop_dual(raftgp_graph g, int32_t r, const float *theta, const double *gvec, float *Y_ncut,
+                               float *Y_mod, const float *W1, int32_t l1, float *T_ncut, float *T_mod) {
+    const bool fast = (r == 32 || r == 64 || r == 128) && W1 && (l1 == 32 || l1 == 64 || l1 == 128) &&
+                      aligned16(theta) && aligned16(W1) && aligned16(T_ncut) && aligned16(T_mod) &&
+                      (!Y_ncut || aligned16(Y_ncut)) && (!Y_mod || aligned16(Y_mod));
+    if (!fast) {   // two single-variant hops (same results: per-row arithmetic is identical)
+        RG_TRY(feature_hop(g, RAFTGP_NCUT, r, theta, nullptr, Y_ncut, W1, l1, T_ncut));
+        return feature_hop(g, RAFTGP_MOD, r, theta, gvec, Y_mod, W1, l1, T_mod);
+    }
+    if (g->nl == 0) return RAFTGP_OK;
+    HopArgs a = base_args(g, r);
+    a.X = theta;
+    a.gvec = gvec;
+    a.out = Y_ncut;
+    a.out2 = Y_mod;
+    a.Wn = W1;
+    a.Tn = T_ncut;
+    a.Tn2 = T_mod;
+    switch (r) {
+        case 32: return dispatch_wn<KIND_DUAL, 32>(g->ctx, a, l1);
+        case 64: return dispatch_wn<KIND_DUAL, 64>(g->ctx, a, l1);
+        default: return dispatch_wn<KIND_DUAL, 128>(g->ctx, a, l1);
+    }
+}
+
 raftgp_status gcn_transform(raftgp_graph g, const float *Z, int32_t lin, const float *W, int32_t lout, float *T) {
-    HopArgs a = base_args(g);
+    HopArgs a = base_args(g, lin);
     a.X = Z;
     a.out = nullptr;
     a.Wn = W;
@@ -406,7 +500,7 @@ raftgp_status gcn_transform(raftgp_graph g, const float *Z, int32_t lin, const f
 
 raftgp_status gcn_hop(raftgp_graph g, const float *Tfull, int32_t w, float *Zout, const float *Wn, int32_t wn,
                       float *Tnext) {
-    HopArgs a = base_args(g);
+    HopArgs a = base_args(g, w);
     a.X = Tfull;
     a.out = Zout;
     a.Wn = Wn;

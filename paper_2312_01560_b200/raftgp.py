@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libraftgp.so")
+LIB_PATH = os.environ.get("RAFTGP_LIB") or os.path.join(_HERE, "libraftgp.so")
 
 RAFTGP_OK, RAFTGP_ERR_PARAM, RAFTGP_ERR_DATA = 0, 2, 3
 RAFTGP_ERR_INTERNAL, RAFTGP_ERR_CUDA, RAFTGP_ERR_NOMEM, RAFTGP_ERR_STATE = 4, 5, 6, 7
@@ -32,7 +32,7 @@ EXPORTS = (
     "raftgp_prof_reset", "raftgp_launch_count", "raftgp_build_csr", "raftgp_graph_info", "raftgp_graph_export",
     "raftgp_graph_local_degrees", "raftgp_graph_set_degrees", "raftgp_graph_destroy", "raftgp_sketch",
     "raftgp_weights", "raftgp_project", "raftgp_gcn_transform", "raftgp_gcn_hop", "raftgp_gnn_embed",
-    "raftgp_embed", "raftgp_modularity", "raftgp_ncut", "raftgp_local_modularity",
+    "raftgp_embed", "raftgp_embed_multi", "raftgp_modularity", "raftgp_ncut", "raftgp_local_modularity",
 )
 
 _lib = None
@@ -75,6 +75,7 @@ _SIGS = {
     "raftgp_gcn_hop": (ctypes.c_int, [c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp]),
     "raftgp_gnn_embed": (ctypes.c_int, [c_vp, c_i32, c_vp, c_u64, c_vp, c_vp, c_vp]),
     "raftgp_embed": (ctypes.c_int, [c_vp, ctypes.c_int, c_i32, c_vp, c_u64, c_vp, c_vp, c_vp]),
+    "raftgp_embed_multi": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i32, c_vp, c_u64, c_vp, c_vp]),
     "raftgp_modularity": (ctypes.c_int, [c_vp, c_vp, c_i32, P(c_dbl)]),
     "raftgp_ncut": (ctypes.c_int, [c_vp, c_vp, c_i32, P(c_dbl)]),
     "raftgp_local_modularity": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_i32, P(c_dbl)]),
@@ -325,6 +326,23 @@ def raftgp_embed(g: Graph, variant, dims: Sequence[int], seed: int, Y: Optional[
     _ck(load_library().raftgp_embed(g.h, _variant(variant), L, d, seed, _ptr(Y), _ptr(Z),
                                     _zk_array(Zk) if intermediates else None))
     return (Y, Z, Zk) if intermediates else (Y, Z)
+
+
+def raftgp_embed_multi(g: Graph, variants: Sequence, dims: Sequence[int], seed: int, Z=None, want_Y: bool = False):
+    """Several variants in one call (one Theta, one shared gather for NCUT + MOD).
+    Returns ({variant: Y} or None, {variant: Z})."""
+    dims = [int(d) for d in dims]
+    vs = [_variant(v) for v in variants]
+    names = [v if isinstance(v, str) else {0: "ncut", 1: "mod", 2: "mod_reduced"}[int(v)] for v in variants]
+    dev = g.ctx.device
+    Z = Z or {nm: torch.empty((g.rows, dims[-1]), dtype=torch.float32, device=dev) for nm in names}
+    Y = {nm: torch.empty((g.rows, dims[0]), dtype=torch.float32, device=dev) for nm in names} if want_Y else None
+    va = (c_i32 * len(vs))(*vs)
+    d = (c_i32 * len(dims))(*dims)
+    _ck(load_library().raftgp_embed_multi(g.h, len(vs), va, len(dims) - 1, d, seed,
+                                          _zk_array([Y[nm] for nm in names]) if want_Y else None,
+                                          _zk_array([Z[nm] for nm in names])))
+    return Y, Z
 
 
 # ------------------------------------------------------------------ scoring (host)

@@ -253,3 +253,20 @@ def test_errors(rg, ctx):
     with pytest.raises(rg.RaftGPError) as e:
         rg.raftgp_gnn_embed(g, (64, 0), 0, torch.empty(n, 64, device="cuda"))
     assert e.value.code == rg.RAFTGP_ERR_PARAM
+
+
+@pytest.mark.parametrize("name,dims", [("c2", (64, 64, 32)), ("hubs", (128, 128, 64)), ("rand_dups", (32, 64, 16)),
+                                       ("c1_s3", (12, 7, 5))])
+def test_embed_multi_equals_single(rg, ctx, name, dims):
+    """raftgp_embed_multi (one Theta, one shared gather for NCUT + MOD) is bit-identical to one
+    raftgp_embed per variant, and so inherits its oracle parity."""
+    n, src, dst, ref = graph_case(name)
+    g = rg.raftgp_build_csr(ctx, n, _t(src), _t(dst))
+    variants = ["mod", "ncut", "mod_reduced"]
+    Y, Z = rg.raftgp_embed_multi(g, variants, dims, 21, want_Y=True)
+    for v in variants:
+        Ys, Zs = rg.raftgp_embed(g, v, dims, 21)
+        assert torch.equal(Y[v], Ys), v
+        assert torch.equal(Z[v], Zs), v
+    Zo = oracle.gcn(ref, dims, 21, oracle.project(ref, "mod", dims[0], 21))[-1]
+    assert rel_fro(Z["mod"].cpu().numpy(), Zo) <= TOL
