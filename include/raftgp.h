@@ -114,6 +114,12 @@ RAFTGP_API raftgp_status raftgp_graph_local_degrees(raftgp_graph g, int32_t *deg
  * concatenation of every rank's raftgp_graph_local_degrees). Computes 2e, s and s^ over all nodes. */
 RAFTGP_API raftgp_status raftgp_graph_set_degrees(raftgp_graph g, const int32_t *deg_all_dev);
 
+/* Visiting order of the local rows used by the hop kernels (a permutation of 0..rows-1, device int32;
+ * NULL = natural order). Performance only: every row's arithmetic, and so every output bit, is the same
+ * for any order. With RAFTGP_ORDER_ROUNDS=k > 0 in the environment build_csr installs an order from k rounds
+ * of label propagation (paper_2312_01560_b200/csrc/order.cu); the default is the natural order. */
+RAFTGP_API raftgp_status raftgp_graph_set_order(raftgp_graph g, const int32_t *order_dev);
+
 RAFTGP_API raftgp_status raftgp_graph_destroy(raftgp_graph g);
 
 /* ---------------------------------------------------------------- a3: Gaussian sketch

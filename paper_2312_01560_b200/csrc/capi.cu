@@ -18,7 +18,7 @@ namespace raftgp {
 
 const char *const kKernelNames[K_NUM] = {
     "csr_count", "scan", "csr_scatter", "csr_sort_warp", "csr_sort_block", "csr_compact", "degree_scalars",
-    "sketch", "g_partials", "g_final", "feature_hop", "transform", "gcn_hop", "hop_generic", "misc", "csr_partition", "csr_bucket_sort"};
+    "sketch", "g_partials", "g_final", "feature_hop", "transform", "gcn_hop", "hop_generic", "misc", "csr_partition", "csr_bucket_sort", "row_order"};
 
 static thread_local std::string g_last_error;
 
@@ -321,6 +321,20 @@ raftgp_status raftgp_graph_set_degrees(raftgp_graph g, const int32_t *deg_all_de
     RG_GUARD_END
 }
 
+raftgp_status raftgp_graph_set_order(raftgp_graph g, const int32_t *order_dev) {
+    if (!g) return fail(RAFTGP_ERR_PARAM, "null graph");
+    RG_TRY(set_device(g->ctx));
+    if (!order_dev) {   // natural order
+        dfree(g->ctx, g->order);
+        g->order = nullptr;
+        return RAFTGP_OK;
+    }
+    if (g->order == nullptr && g->nl > 0) RG_TRY(dalloc_t(g->ctx, &g->order, (size_t)g->nl));
+    if (g->nl > 0)
+        RG_CUDA(cudaMemcpyAsync(g->order, order_dev, sizeof(int32_t) * g->nl, cudaMemcpyDeviceToDevice, g->ctx->stream));
+    return RAFTGP_OK;
+}
+
 raftgp_status raftgp_graph_destroy(raftgp_graph g) {
     if (!g) return RAFTGP_OK;
     raftgp_ctx ctx = g->ctx;
@@ -328,6 +342,7 @@ raftgp_status raftgp_graph_destroy(raftgp_graph g) {
     dfree(ctx, g->row_ptr);
     dfree(ctx, g->col);
     dfree(ctx, g->deg_local);
+    dfree(ctx, g->order);
     dfree(ctx, g->deg_all);
     dfree(ctx, g->s_all);
     dfree(ctx, g->sh_all);

@@ -711,6 +711,7 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
     dfree(ctx, col_raw);
     dfree(ctx, big_rows);
     dfree(ctx, big_count);
+    RG_TRY(compute_order(g));
     if (rb == 0 && re == n) {
         if (n > 0) RG_CUDA(cudaMemcpyAsync(g->deg_all, g->deg_local, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
         RG_TRY(degrees_finalize(g));

@@ -33,6 +33,7 @@ enum KernelId : int {
     K_MISC,
     K_CSR_PARTITION,
     K_CSR_BUCKET,
+    K_ORDER,
     K_NUM
 };
 extern const char *const kKernelNames[K_NUM];
@@ -68,6 +69,7 @@ struct raftgp_graph_s {
     int64_t *row_ptr = nullptr;    // device int64[nl+1], local offsets
     int32_t *col = nullptr;        // device int32[nnz_local], global ids (canonical CSR)
     int32_t *deg_local = nullptr;  // device int32[nl]
+    int32_t *order = nullptr;      // device int32[nl]: locality-aware visiting order of the local rows (order.cu)
     int32_t *deg_all = nullptr;    // device int32[n] (global degrees)
     float *s_all = nullptr;        // device fp32[n]: deg^-1/2, 0 for isolated nodes
     float *sh_all = nullptr;       // device fp32[n]: (deg+1)^-1/2
@@ -133,7 +135,8 @@ inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 
 raftgp_status scan_i32_to_i64(raftgp_ctx ctx, const int32_t *in, int64_t *out, int64_t n);
 raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src, const int32_t *dst, int64_t rb,
                         int64_t re, raftgp_graph g);
-raftgp_status degrees_finalize(raftgp_graph g);   // deg_all -> two_e, s_all, sh_all, deg_hist
+raftgp_status degrees_finalize(raftgp_graph g);
+raftgp_status compute_order(raftgp_graph g);      // g->order (label propagation + counting sort)   // deg_all -> two_e, s_all, sh_all, deg_hist
 
 raftgp_status sketch_fill(raftgp_ctx ctx, uint64_t seed, uint32_t tag, int64_t row_begin, int64_t rows, int32_t cols,
                           int32_t den, float *out);

@@ -28,11 +28,16 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+#ifndef RG_PREFETCH
+#define RG_PREFETCH 0   // 1: load the next row's first col chunk while gathering the current row
+#endif
+
 enum Kind : int { KIND_NCUT = 0, KIND_MOD = 1, KIND_MOD_REDUCED = 2, KIND_GCN = 3, KIND_LOAD = 4, KIND_DUAL = 5 };
 
 struct HopArgs {
     int64_t nl, rb, n;
     const int64_t *row_ptr;    // local CSR
+    const int32_t *order;      // visiting order of the local rows (may be null = natural order)
     const int32_t *col;        // global neighbour ids
     const float *X;            // operand, n x W (global rows); for KIND_LOAD: local rows x W
     const float *s_all;        // deg^-1/2
@@ -75,20 +80,26 @@ enum Mode : int { M_SUM = 0, M_S = 1, M_SUM_D = 2, M_SUM_S = 3 };
 // `c0` is this row's first 32-entry col chunk, loaded by the caller one row ahead; later chunks are
 // prefetched one chunk ahead, so col latency overlaps the row gathers. (L2 eviction-priority hints for
 // high-degree rows were measured and made every hop slower; plain read-only loads are used.)
-template <int W, int U, int MODE>
+template <int W, int U_REQ, int MODE>
 __device__ __forceinline__ void gather_row(const HopArgs &a, int64_t beg, int64_t end, int32_t c0, int lane,
                                            float4 &acc, float4 &acc2) {
     constexpr int LPN = W / 4, NPW = 32 / LPN;
+    constexpr int U = (NPW * U_REQ <= 32) ? U_REQ : 32 / NPW;
     static_assert(NPW * U <= 32 && 32 % (NPW * U) == 0, "unroll must tile a 32-entry col chunk");
     const int sub = lane / LPN, cl = lane % LPN;
     const float4 *X4 = reinterpret_cast<const float4 *>(a.X);
     acc = make_float4(0.f, 0.f, 0.f, 0.f);
     acc2 = make_float4(0.f, 0.f, 0.f, 0.f);
+#if RG_PREFETCH
     int32_t mycur = c0;
+#else
+    int32_t mycur = (beg + lane < end) ? __ldg(a.col + beg + lane) : 0;
+    (void)c0;
+#endif
     for (int64_t base = beg; base < end; base += 32) {
         const int cnt = (end - base < 32) ? static_cast<int>(end - base) : 32;
         const int64_t nb = base + 32;
-        const int32_t mynext = (nb + lane < end) ? __ldg(a.col + nb + lane) : 0;
+        const int32_t mynext = (nb < end && nb + lane < end) ? __ldg(a.col + nb + lane) : 0;
         const int32_t myj = mycur;
         float myw = 0.f;
         if (MODE == M_S || MODE == M_SUM_S) myw = lane < cnt ? __ldg(a.s_all + myj) : 0.f;
@@ -122,7 +133,7 @@ __device__ __forceinline__ void gather_row(const HopArgs &a, int64_t beg, int64_
 }
 
 #ifndef RG_U_SUM
-#define RG_U_SUM 8
+#define RG_U_SUM 4
 #endif
 #ifndef RG_U_S
 #define RG_U_S 8
@@ -183,12 +194,13 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
         int64_t beg = 0, end = 0;
         int32_t c0 = 0;
         if constexpr (KIND != KIND_LOAD) {
-            beg = a.row_ptr[row0];
-            end = a.row_ptr[row0 + 1];
-            c0 = (beg + lane < end) ? __ldg(a.col + beg + lane) : 0;
+            const int64_t r = a.order ? static_cast<int64_t>(__ldg(a.order + row0)) : row0;
+            beg = a.row_ptr[r];
+            end = a.row_ptr[r + 1];
+            c0 = (RG_PREFETCH && beg + lane < end) ? __ldg(a.col + beg + lane) : 0;
         }
         for (int rr = 0; rr < rows_here; ++rr) {
-            const int64_t row = row0 + rr;          // local row
+            const int64_t row = a.order ? static_cast<int64_t>(__ldg(a.order + row0 + rr)) : row0 + rr;   // local row
             const int64_t gi = a.rb + row;          // global row id
             float4 acc, acc2;
             float4 y, y2 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -198,8 +210,10 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
                 int64_t nbeg = end, nend = end;
                 int32_t nc0 = 0;
                 if (rr + 1 < rows_here) {
-                    nend = a.row_ptr[row + 2];
-                    nc0 = (nbeg + lane < nend) ? __ldg(a.col + nbeg + lane) : 0;
+                    const int64_t r = a.order ? static_cast<int64_t>(__ldg(a.order + row0 + rr + 1)) : row0 + rr + 1;
+                    nbeg = a.row_ptr[r];
+                    nend = a.row_ptr[r + 1];
+                    if (RG_PREFETCH) nc0 = (nbeg + lane < nend) ? __ldg(a.col + nbeg + lane) : 0;
                 }
                 float4 self = make_float4(0.f, 0.f, 0.f, 0.f);
                 if constexpr (KIND == KIND_GCN) self = ldg4(reinterpret_cast<const float4 *>(a.X) + gi * LPN + cl);
@@ -260,36 +274,41 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
             static_assert(RR >= 1 && NR % RS == 0, "staged rows must be a multiple of the parallel row count");
             __syncwarp();
             const int rs = lane / OL, oc = lane % OL;
-            float4 o[RR];
-#pragma unroll
-            for (int q = 0; q < RR; ++q) o[q] = make_float4(0.f, 0.f, 0.f, 0.f);
             const float4 *W4 = reinterpret_cast<const float4 *>(Wsm);
             const float4 *S4 = reinterpret_cast<const float4 *>(stage);
+            // rows per lane are processed RC at a time (caps the accumulator registers at 4 x float4)
+            constexpr int RC = RR < 4 ? RR : 4;
+#pragma unroll 1
+            for (int q0 = 0; q0 < RR; q0 += RC) {
+                float4 o[RC];
+#pragma unroll
+                for (int q = 0; q < RC; ++q) o[q] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 2
-            for (int k = 0; k < W; k += 4) {
-                const float4 w0 = W4[(k + 0) * OL + oc];
-                const float4 w1 = W4[(k + 1) * OL + oc];
-                const float4 w2 = W4[(k + 2) * OL + oc];
-                const float4 w3 = W4[(k + 3) * OL + oc];
+                for (int k = 0; k < W; k += 4) {
+                    const float4 w0 = W4[(k + 0) * OL + oc];
+                    const float4 w1 = W4[(k + 1) * OL + oc];
+                    const float4 w2 = W4[(k + 2) * OL + oc];
+                    const float4 w3 = W4[(k + 3) * OL + oc];
 #pragma unroll
-                for (int q = 0; q < RR; ++q) {
-                    const int rr = rs + q * RS;
-                    const float4 z = S4[rr * (W / 4) + k / 4];
-                    fma4(o[q], z.x, w0);
-                    fma4(o[q], z.y, w1);
-                    fma4(o[q], z.z, w2);
-                    fma4(o[q], z.w, w3);
+                    for (int q = 0; q < RC; ++q) {
+                        const int rr = rs + (q0 + q) * RS;
+                        const float4 z = S4[rr * (W / 4) + k / 4];
+                        fma4(o[q], z.x, w0);
+                        fma4(o[q], z.y, w1);
+                        fma4(o[q], z.z, w2);
+                        fma4(o[q], z.w, w3);
+                    }
                 }
-            }
 #pragma unroll
-            for (int q = 0; q < RR; ++q) {
-                const int rr = rs + q * RS;
-                const int v = rr / RB, r_in = rr % RB;
-                if (r_in < rows_here) {
-                    const int64_t row = row0 + r_in;
-                    const float shi = __ldg(a.sh_all + a.rb + row);
-                    float4 *T4 = reinterpret_cast<float4 *>(v == 0 ? a.Tn : a.Tn2);
-                    T4[row * OL + oc] = make_float4(shi * o[q].x, shi * o[q].y, shi * o[q].z, shi * o[q].w);
+                for (int q = 0; q < RC; ++q) {
+                    const int rr = rs + (q0 + q) * RS;
+                    const int v = rr / RB, r_in = rr % RB;
+                    if (r_in < rows_here) {
+                        const int64_t row = a.order ? static_cast<int64_t>(__ldg(a.order + row0 + r_in)) : row0 + r_in;
+                        const float shi = __ldg(a.sh_all + a.rb + row);
+                        float4 *T4 = reinterpret_cast<float4 *>(v == 0 ? a.Tn : a.Tn2);
+                        T4[row * OL + oc] = make_float4(shi * o[q].x, shi * o[q].y, shi * o[q].z, shi * o[q].w);
+                    }
                 }
             }
             __syncwarp();
@@ -438,6 +457,7 @@ HopArgs base_args(raftgp_graph g, int32_t /*w*/) {
     a.rb = g->row_begin;
     a.n = g->n;
     a.row_ptr = g->row_ptr;
+    a.order = g->order;
     a.col = g->col;
     a.s_all = g->s_all;
     a.sh_all = g->sh_all;

@@ -30,7 +30,7 @@ EXPORTS = (
     "raftgp_last_error", "raftgp_version", "raftgp_ctx_create", "raftgp_ctx_destroy", "raftgp_ctx_sync",
     "raftgp_ctx_stream", "raftgp_ctx_set_profiling", "raftgp_prof_kernels", "raftgp_prof_name", "raftgp_prof_read",
     "raftgp_prof_reset", "raftgp_launch_count", "raftgp_build_csr", "raftgp_graph_info", "raftgp_graph_export",
-    "raftgp_graph_local_degrees", "raftgp_graph_set_degrees", "raftgp_graph_destroy", "raftgp_sketch",
+    "raftgp_graph_local_degrees", "raftgp_graph_set_degrees", "raftgp_graph_set_order", "raftgp_graph_destroy", "raftgp_sketch",
     "raftgp_weights", "raftgp_project", "raftgp_gcn_transform", "raftgp_gcn_hop", "raftgp_gnn_embed",
     "raftgp_embed", "raftgp_embed_multi", "raftgp_modularity", "raftgp_ncut", "raftgp_local_modularity",
 )
@@ -67,6 +67,7 @@ _SIGS = {
     "raftgp_graph_export": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_u32]),
     "raftgp_graph_local_degrees": (ctypes.c_int, [c_vp, c_vp]),
     "raftgp_graph_set_degrees": (ctypes.c_int, [c_vp, c_vp]),
+    "raftgp_graph_set_order": (ctypes.c_int, [c_vp, c_vp]),
     "raftgp_graph_destroy": (ctypes.c_int, [c_vp]),
     "raftgp_sketch": (ctypes.c_int, [c_vp, c_u64, c_u32, c_i64, c_i64, c_i32, c_i32, c_vp]),
     "raftgp_weights": (ctypes.c_int, [c_vp, c_u64, c_i32, c_i32, c_i32, c_vp]),
@@ -213,6 +214,10 @@ class Graph:
 
     def set_degrees(self, deg_all: torch.Tensor):
         _ck(load_library().raftgp_graph_set_degrees(self.h, _ptr(_dev(deg_all.contiguous(), "deg_all"))))
+
+    def set_order(self, order: Optional[torch.Tensor]):
+        """Row visiting order (int32 permutation of the local rows) or None for the natural order."""
+        _ck(load_library().raftgp_graph_set_order(self.h, None if order is None else _ptr(order.contiguous())))
 
     def close(self):
         if getattr(self, "h", None) is not None and _lib is not None and not _exiting:

@@ -54,7 +54,19 @@ GRAPHS = {
     "c2": lambda: (lambda g: (g.n, g.src, g.dst))(synth.generate("C2", 0)),
     "rand_dups": lambda: (3001, *synth.random_edges(2900, 40000, seed=5)),        # isolated tail 2900..3000
     "hubs": lambda: _hubs(),
+    "bighub": lambda: _bighub(),
 }
+
+
+def _bighub():
+    # one row of 70,000 raw entries: larger than a bucket's shared-memory capacity (global fallback path)
+    n = 100_000
+    rng = np.random.default_rng(7)
+    leaves = rng.choice(np.arange(1, n), 50_000, replace=False).astype(np.int32)
+    src = np.concatenate([np.zeros(50_000, np.int32), leaves[:20_000], *synth.random_edges(n, 50_000, seed=4)[:1]])
+    dst = np.concatenate([leaves, np.zeros(20_000, np.int32), synth.random_edges(n, 50_000, seed=4)[1]])
+    perm = rng.permutation(src.size)
+    return n, src[perm], dst[perm]
 
 
 def _hubs():
@@ -140,7 +152,7 @@ def test_csr_data_error(rg, ctx):
 
 
 # ------------------------------------------------------------------ a4: feature hop
-@pytest.mark.parametrize("name", ["c1_s0", "c2", "rand_dups", "hubs"])
+@pytest.mark.parametrize("name", ["c1_s0", "c2", "rand_dups", "hubs", "bighub"])
 @pytest.mark.parametrize("variant", ["ncut", "mod", "mod_reduced"])
 @pytest.mark.parametrize("r", [64, 128, 32, 5])
 def test_project_parity(rg, ctx, name, variant, r):
@@ -151,9 +163,10 @@ def test_project_parity(rg, ctx, name, variant, r):
     Y = rg.raftgp_project(g, variant, r, seed=17).cpu().numpy()
     Yo = oracle.project(ref, variant, r, seed=17)
     assert rel_fro(Y, Yo) <= TOL
-    # row-wise too: no row is badly off (relative to the typical row norm)
+    # row-wise too: no row is badly off (relative to its own norm, floored at the typical row norm)
     scale = np.sqrt(np.mean(np.sum(Yo ** 2, 1))) + 1e-30
-    assert np.max(np.linalg.norm(Y - Yo, axis=1)) / scale < 1e-3
+    rown = np.maximum(np.linalg.norm(Yo, axis=1), scale)
+    assert np.max(np.linalg.norm(Y - Yo, axis=1) / rown) < 1e-4
 
 
 # ------------------------------------------------------------------ a5: GCN
@@ -270,3 +283,18 @@ def test_embed_multi_equals_single(rg, ctx, name, dims):
         assert torch.equal(Z[v], Zs), v
     Zo = oracle.gcn(ref, dims, 21, oracle.project(ref, "mod", dims[0], 21))[-1]
     assert rel_fro(Z["mod"].cpu().numpy(), Zo) <= TOL
+
+
+def test_row_order_does_not_change_results(rg, ctx):
+    """The visiting order of rows is a performance device only: outputs are bit-identical for the natural
+    order, a random permutation and the planted-block order."""
+    gr = synth.generate("C2", 1)
+    g = rg.raftgp_build_csr(ctx, gr.n, _t(gr.src), _t(gr.dst))
+    dims = (64, 64, 32)
+    Y0, Z0 = rg.raftgp_embed_multi(g, ["ncut", "mod"], dims, 2, want_Y=True)
+    for order in (np.random.default_rng(0).permutation(gr.n), np.argsort(gr.labels, kind="stable")):
+        g.set_order(_t(order.astype(np.int32)))
+        Y1, Z1 = rg.raftgp_embed_multi(g, ["ncut", "mod"], dims, 2, want_Y=True)
+        for v in ("ncut", "mod"):
+            assert torch.equal(Y0[v], Y1[v]) and torch.equal(Z0[v], Z1[v])
+    g.set_order(None)
