@@ -510,6 +510,37 @@ raftgp_status raftgp_embed(raftgp_graph g, raftgp_variant variant, int32_t layer
     RG_GUARD_END
 }
 
+// project + GCN without materialising Y: Theta' = Theta W1 is generated once (Theta on chip), every
+// variant's first operand T1 = s^ (.) (X Theta') comes from a GEMM-free feature hop (NCUT and MOD share
+// one gather), then the GCN stacks. Same results as the Y path up to fp32 rounding order (reading #13).
+static raftgp_status embed_pre(raftgp_graph g, int32_t nvariants, const int32_t *variants, int32_t layers,
+                               const int32_t *dims, uint64_t seed, float *const *Z_dev, const int where[3]) {
+    raftgp_ctx ctx = g->ctx;
+    const int32_t r = dims[0], l1 = dims[1];
+    float *W1 = nullptr, *thw = nullptr;
+    double *gw = nullptr;
+    std::vector<float *> T1(nvariants, nullptr);
+    raftgp_status st = dalloc_t(ctx, &W1, (size_t)r * l1);
+    if (st == RAFTGP_OK) st = sketch_fill(ctx, seed, 1u, 0, r, l1, r, W1);
+    if (st == RAFTGP_OK) st = dalloc_t(ctx, &thw, (size_t)g->n * l1);
+    if (st == RAFTGP_OK && where[RAFTGP_MOD] >= 0) st = dalloc_t(ctx, &gw, (size_t)l1);
+    if (st == RAFTGP_OK) st = sketch_theta_w(g, seed, r, W1, l1, thw, gw);
+    for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v) st = dalloc_t(ctx, &T1[v], (size_t)g->n * l1);
+    const bool dual = where[RAFTGP_NCUT] >= 0 && where[RAFTGP_MOD] >= 0;
+    if (st == RAFTGP_OK && dual)
+        st = feature_hop_pre(g, -1, l1, thw, gw, T1[where[RAFTGP_NCUT]], T1[where[RAFTGP_MOD]]);
+    for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v) {
+        if (dual && (variants[v] == RAFTGP_NCUT || variants[v] == RAFTGP_MOD)) continue;
+        st = feature_hop_pre(g, variants[v], l1, thw, gw, T1[v], nullptr);
+    }
+    dfree(ctx, thw);
+    dfree(ctx, gw);
+    for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v) st = gcn_stack(g, layers, dims, seed, T1[v], Z_dev[v], nullptr);
+    dfree(ctx, W1);
+    for (auto t : T1) dfree(ctx, t);
+    return st;
+}
+
 raftgp_status raftgp_embed_multi(raftgp_graph g, int32_t nvariants, const int32_t *variants, int32_t layers,
                                  const int32_t *dims, uint64_t seed, float *const *Y_dev, float *const *Z_dev) {
     RG_GUARD_BEGIN
@@ -527,6 +558,8 @@ raftgp_status raftgp_embed_multi(raftgp_graph g, int32_t nvariants, const int32_
     RG_TRY(set_device(g->ctx));
     raftgp_ctx ctx = g->ctx;
     const int32_t r = dims[0];
+    if (Y_dev == nullptr && sketch_w_supported(r, dims[1]))
+        return embed_pre(g, nvariants, variants, layers, dims, seed, Z_dev, where);
     float *theta = nullptr, *W1 = nullptr;
     double *gvec = nullptr;
     std::vector<float *> T1(nvariants, nullptr);

@@ -142,12 +142,22 @@ raftgp_status sketch_fill(raftgp_ctx ctx, uint64_t seed, uint32_t tag, int64_t r
                           int32_t den, float *out);
 // Theta for all n rows + g = sum_j d_j Theta_j (fp64) when g_out != nullptr.
 raftgp_status sketch_theta(raftgp_graph g, uint64_t seed, int32_t r, float *theta, double *g_out);
+// g = d^T X over all n rows (fp64, fixed chunk order); X is n x r
+raftgp_status g_reduce(raftgp_graph g, const float *X, int32_t r, double *g_out);
+// Theta' = Theta W1 (Theta generated on chip, n x l1 written) and optionally g' = d^T Theta'
+bool sketch_w_supported(int32_t r, int32_t l1);
+raftgp_status sketch_theta_w(raftgp_graph g, uint64_t seed, int32_t r, const float *W1, int32_t l1, float *out,
+                             double *g_out);
 
 raftgp_status feature_hop(raftgp_graph g, int variant, int32_t r, const float *theta, const double *gvec, float *Y,
                           const float *W1, int32_t l1, float *T1);
 // NCut and full-modularity feature hops from ONE gather of Theta (+ both first transforms).
 raftgp_status feature_hop_dual(raftgp_graph g, int32_t r, const float *theta, const double *gvec, float *Y_ncut,
                                float *Y_mod, const float *W1, int32_t l1, float *T_ncut, float *T_mod);
+// Feature hop on a pre-transformed operand Theta' = Theta W1 (no epilogue GEMM): writes
+// T1 = s^ (.) (X Theta') for NCUT (T_ncut) and/or MOD (T_mod), or MOD_REDUCED (T_ncut slot, variant 2).
+raftgp_status feature_hop_pre(raftgp_graph g, int variant_or_dual, int32_t l1, const float *theta_w,
+                              const double *gvec_w, float *T_a, float *T_b);
 raftgp_status gcn_transform(raftgp_graph g, const float *Z, int32_t lin, const float *W, int32_t lout, float *T);
 raftgp_status gcn_hop(raftgp_graph g, const float *Tfull, int32_t w, float *Zout, const float *Wn, int32_t wn,
                       float *Tnext);

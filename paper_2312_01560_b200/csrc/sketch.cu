@@ -66,6 +66,98 @@ __global__ void g_final(const double *__restrict__ partial, int64_t nchunks, int
     }
 }
 
+// Theta' = Theta W1 for all n rows, with Theta generated in shared memory (never written to HBM).
+// Every feature operator is linear in Theta, so (X Theta) W1 = X (Theta W1): gathering Theta' instead of
+// Theta lets the feature hop skip its per-row GEMM, and one Theta' serves every variant of a call.
+// Tile: TM = 128 rows x L1 columns per CTA; Theta is generated KC = 32 columns at a time into shared
+// memory and multiplied into the accumulators (256 threads, each an RPT x 8 block, FFMA, W1 resident in
+// shared memory), so two CTAs fit per SM and one generates while the other multiplies.
+template <int R, int L1>
+__global__ void __launch_bounds__(256, 2) sketch_w_kernel(uint64_t seed, int64_t n, float sigma,
+                                                          const float *__restrict__ W1, float *__restrict__ out) {
+    constexpr int TM = 128, KC = 32, KP = KC + 4;   // padded row stride of the Theta chunk
+    constexpr int CG = L1 / 8, RGN = 256 / CG, RPT = TM / RGN;
+    extern __shared__ float4 sw4[];
+    float *Wsm = reinterpret_cast<float *>(sw4);  // R x L1
+    float *Ts = Wsm + R * L1;                     // TM x KP
+    for (int t = threadIdx.x; t < R * L1 / 4; t += blockDim.x)
+        reinterpret_cast<float4 *>(Wsm)[t] = reinterpret_cast<const float4 *>(W1)[t];
+    const int cg = threadIdx.x % CG, rg = threadIdx.x / CG;
+    const int64_t ntiles = (n + TM - 1) / TM;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t r0 = tile * TM;
+        float acc[RPT][8];
+#pragma unroll
+        for (int i = 0; i < RPT; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+        for (int k0 = 0; k0 < R; k0 += KC) {
+            __syncthreads();
+            for (int t = threadIdx.x; t < TM * (KC / 4); t += blockDim.x) {
+                const int rr = t / (KC / 4), q = t % (KC / 4);
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (r0 + rr < n)
+                    v = spec_quad(seed, 0u, static_cast<uint64_t>(r0 + rr), static_cast<uint32_t>(k0 / 4 + q), sigma);
+                *reinterpret_cast<float4 *>(Ts + rr * KP + 4 * q) = v;
+            }
+            __syncthreads();
+#pragma unroll 4
+            for (int k = 0; k < KC; ++k) {
+                const float4 b0 = *reinterpret_cast<const float4 *>(Wsm + (k0 + k) * L1 + cg * 8);
+                const float4 b1 = *reinterpret_cast<const float4 *>(Wsm + (k0 + k) * L1 + cg * 8 + 4);
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                    const float a = Ts[(rg * RPT + i) * KP + k];
+                    acc[i][0] = fmaf(a, b0.x, acc[i][0]);
+                    acc[i][1] = fmaf(a, b0.y, acc[i][1]);
+                    acc[i][2] = fmaf(a, b0.z, acc[i][2]);
+                    acc[i][3] = fmaf(a, b0.w, acc[i][3]);
+                    acc[i][4] = fmaf(a, b1.x, acc[i][4]);
+                    acc[i][5] = fmaf(a, b1.y, acc[i][5]);
+                    acc[i][6] = fmaf(a, b1.z, acc[i][6]);
+                    acc[i][7] = fmaf(a, b1.w, acc[i][7]);
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            const int64_t row = r0 + rg * RPT + i;
+            if (row < n) {
+                float4 *o = reinterpret_cast<float4 *>(out + row * L1 + cg * 8);
+                o[0] = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+                o[1] = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+            }
+        }
+    }
+}
+
+template <int R, int L1>
+raftgp_status launch_sketch_w(raftgp_ctx ctx, uint64_t seed, int64_t n, float sigma, const float *W1, float *out) {
+    const size_t smem = sizeof(float) * ((size_t)R * L1 + 128 * 36);
+    static bool attr = false;
+    if (!attr) {
+        RG_CUDA(cudaFuncSetAttribute(sketch_w_kernel<R, L1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 128), 2 * ctx->sm_count)));
+    {
+        LaunchScope L(ctx, K_SKETCH);
+        sketch_w_kernel<R, L1><<<grid, 256, smem, ctx->stream>>>(seed, n, sigma, W1, out);
+    }
+    RG_CHECK_LAUNCH(ctx);
+    return RAFTGP_OK;
+}
+
+template <int R>
+raftgp_status dispatch_sketch_w(raftgp_ctx ctx, uint64_t seed, int64_t n, float sigma, const float *W1, int l1,
+                                float *out) {
+    switch (l1) {
+        case 32: return launch_sketch_w<R, 32>(ctx, seed, n, sigma, W1, out);
+        case 64: return launch_sketch_w<R, 64>(ctx, seed, n, sigma, W1, out);
+        default: return launch_sketch_w<R, 128>(ctx, seed, n, sigma, W1, out);
+    }
+}
+
 }  // namespace
 
 raftgp_status sketch_fill(raftgp_ctx ctx, uint64_t seed, uint32_t tag, int64_t row_begin, int64_t rows, int32_t cols,
@@ -83,9 +175,32 @@ raftgp_status sketch_fill(raftgp_ctx ctx, uint64_t seed, uint32_t tag, int64_t r
     return RAFTGP_OK;
 }
 
+bool sketch_w_supported(int32_t r, int32_t l1) {
+    return (r == 32 || r == 64 || r == 128) && (l1 == 32 || l1 == 64 || l1 == 128);
+}
+
+raftgp_status sketch_theta_w(raftgp_graph g, uint64_t seed, int32_t r, const float *W1, int32_t l1, float *out,
+                             double *g_out) {
+    raftgp_ctx ctx = g->ctx;
+    const float sigma = spec_sigma(r);
+    if (g->n > 0) {
+        switch (r) {
+            case 32: RG_TRY(dispatch_sketch_w<32>(ctx, seed, g->n, sigma, W1, l1, out)); break;
+            case 64: RG_TRY(dispatch_sketch_w<64>(ctx, seed, g->n, sigma, W1, l1, out)); break;
+            default: RG_TRY(dispatch_sketch_w<128>(ctx, seed, g->n, sigma, W1, l1, out)); break;
+        }
+    }
+    return g_reduce(g, out, l1, g_out);
+}
+
 raftgp_status sketch_theta(raftgp_graph g, uint64_t seed, int32_t r, float *theta, double *g_out) {
     raftgp_ctx ctx = g->ctx;
     RG_TRY(sketch_fill(ctx, seed, 0u, 0, g->n, r, r, theta));
+    return g_reduce(g, theta, r, g_out);
+}
+
+raftgp_status g_reduce(raftgp_graph g, const float *theta, int32_t r, double *g_out) {
+    raftgp_ctx ctx = g->ctx;
     if (g_out == nullptr) return RAFTGP_OK;
     const int64_t nchunks = ceil_div(g->n, kGChunk);
     if (nchunks == 0) {

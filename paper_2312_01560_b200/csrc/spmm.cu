@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 
 #include "internal.cuh"
 
@@ -50,6 +51,7 @@ struct HopArgs {
     float *Tn;                 // local rows x WN, may be null
     float *out2;               // KIND_DUAL: second variant's Y (MOD), may be null
     float *Tn2;                // KIND_DUAL: second variant's T
+    bool scale_sh;             // multiply the stored rows by s^_i (feature hop on Theta' = Theta W1)
 };
 
 __device__ __forceinline__ float4 ldg4(const float4 *p) { return __ldg(p); }
@@ -139,7 +141,7 @@ __device__ __forceinline__ void gather_row(const HopArgs &a, int64_t beg, int64_
 #define RG_U_S 8
 #endif
 #ifndef RG_U_DUAL
-#define RG_U_DUAL 8
+#define RG_U_DUAL 4
 #endif
 #ifndef RG_U_SUMD
 #define RG_U_SUMD 4
@@ -148,7 +150,7 @@ __device__ __forceinline__ void gather_row(const HopArgs &a, int64_t beg, int64_
 #define RG_WARPS_PER_SM 32
 #endif
 #ifndef RG_DUAL_WARPS_PER_SM
-#define RG_DUAL_WARPS_PER_SM 16
+#define RG_DUAL_WARPS_PER_SM 32
 #endif
 
 template <int KIND>
@@ -253,6 +255,13 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
                         const float nrm = sqrtf(ss);
                         y = make_float4(y.x / nrm, y.y / nrm, y.z / nrm, y.w / nrm);
                     }
+                }
+            }
+            if constexpr (WN == 0 && KIND != KIND_GCN && KIND != KIND_LOAD) {
+                if (a.scale_sh) {
+                    const float shi = __ldg(a.sh_all + gi);
+                    y = make_float4(shi * y.x, shi * y.y, shi * y.z, shi * y.w);
+                    y2 = make_float4(shi * y2.x, shi * y2.y, shi * y2.z, shi * y2.w);
                 }
             }
             if (sub == 0) {
@@ -506,6 +515,33 @@ raftgp_status feature_hop_dual(raftgp_graph g, int32_t r, const float *theta, co
         case 32: return dispatch_wn<KIND_DUAL, 32>(g->ctx, a, l1);
         case 64: return dispatch_wn<KIND_DUAL, 64>(g->ctx, a, l1);
         default: return dispatch_wn<KIND_DUAL, 128>(g->ctx, a, l1);
+    }
+}
+
+raftgp_status feature_hop_pre(raftgp_graph g, int variant_or_dual, int32_t l1, const float *theta_w,
+                              const double *gvec_w, float *T_a, float *T_b) {
+    if (g->nl == 0) return RAFTGP_OK;
+    HopArgs a = base_args(g, l1);
+    a.X = theta_w;
+    a.gvec = gvec_w;
+    a.out = T_a;
+    a.out2 = T_b;
+    a.scale_sh = true;
+    if (!((l1 == 32 || l1 == 64 || l1 == 128) && aligned16(theta_w) && aligned16(T_a) && (!T_b || aligned16(T_b))))
+        return fail(RAFTGP_ERR_INTERNAL, "feature_hop_pre: unsupported width/alignment");
+    auto go = [&](auto kind_tag) -> raftgp_status {
+        constexpr int K = decltype(kind_tag)::value;
+        switch (l1) {
+            case 32: return launch_fast<K, 32, 0>(g->ctx, a);
+            case 64: return launch_fast<K, 64, 0>(g->ctx, a);
+            default: return launch_fast<K, 128, 0>(g->ctx, a);
+        }
+    };
+    switch (variant_or_dual) {
+        case RAFTGP_NCUT: return go(std::integral_constant<int, KIND_NCUT>());
+        case RAFTGP_MOD: return go(std::integral_constant<int, KIND_MOD>());
+        case RAFTGP_MOD_REDUCED: return go(std::integral_constant<int, KIND_MOD_REDUCED>());
+        default: return go(std::integral_constant<int, KIND_DUAL>());
     }
 }
 

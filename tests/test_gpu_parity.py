@@ -298,3 +298,19 @@ def test_row_order_does_not_change_results(rg, ctx):
         for v in ("ncut", "mod"):
             assert torch.equal(Y0[v], Y1[v]) and torch.equal(Z0[v], Z1[v])
     g.set_order(None)
+
+
+@pytest.mark.parametrize("name,dims", [("c1_s0", (64, 64, 32)), ("c2", (64, 64, 32)), ("hubs", (128, 128, 64)),
+                                       ("rand_dups", (128, 64, 32)), ("bighub", (32, 32, 16)), ("c1_s3", (12, 7, 5))])
+def test_embed_multi_pre_transformed_parity(rg, ctx, name, dims):
+    """The Y-less path of raftgp_embed_multi (Theta' = Theta W1 generated on chip, GEMM-free feature hop;
+    GEMM before aggregation, reading #13) against the oracle's (X Theta) W1 order, all three variants."""
+    n, src, dst, ref = graph_case(name)
+    g = rg.raftgp_build_csr(ctx, n, _t(src), _t(dst))
+    variants = ["ncut", "mod", "mod_reduced"]
+    _, Z = rg.raftgp_embed_multi(g, variants, dims, 13)
+    for v in variants:
+        Zo = oracle.gcn(ref, dims, 13, oracle.project(ref, v, dims[0], 13))[-1]
+        assert rel_fro(Z[v].cpu().numpy(), Zo) <= TOL, v
+    _, Z2 = rg.raftgp_embed_multi(g, ["mod", "ncut"], dims, 13)     # deterministic, order-independent
+    assert torch.equal(Z2["mod"], Z["mod"]) and torch.equal(Z2["ncut"], Z["ncut"])
