@@ -315,19 +315,50 @@ __global__ void __launch_bounds__(1024) csr_sort_block(const int64_t *__restrict
 // places the entries into their rows in shared memory, sorts and dedups every row (one warp per row) and
 // writes the unique prefix of each row to col_raw. Buckets that do not fit shared memory are placed into
 // col_raw in global memory and their rows handed to the warp / block sort kernels above.
-constexpr int kPartTile = 131072;       // raw pairs per partition tile
+constexpr int kPartTile = 262144;       // raw pairs per partition tile
 constexpr int kMaxBuckets = 12288;      // partition smem: 12 B per bucket
 constexpr int kMaxBucketRows = 4096;    // bucket_sort smem for row cursors/offsets
 constexpr int kBucketCap = 44032;       // entries of one bucket held in shared memory (172 KB)
 constexpr int kGroupRow = 256;          // rows longer than this are sorted by a group of 4 warps
 
+// Bucket entries: (row within the bucket, neighbour id). PACKED = one 32-bit word (row << vbits | id) when
+// log2(B) + vbits <= 32 (C4: 9 + 23 bits), else an int2.
+template <bool PACKED>
+struct Entry;
+template <>
+struct Entry<true> {
+    using T = uint32_t;
+    __device__ __forceinline__ static T make(int lr, int32_t v, int vbits) {
+        return (static_cast<uint32_t>(lr) << vbits) | static_cast<uint32_t>(v);
+    }
+    __device__ __forceinline__ static int row(T e, int vbits) { return static_cast<int>(e >> vbits); }
+    __device__ __forceinline__ static int32_t col(T e, int vbits) {
+        return static_cast<int32_t>(e & ((vbits < 32 ? (1u << vbits) : 0u) - 1u));
+    }
+    __device__ __forceinline__ static T invalid() { return 0xffffffffu; }
+    __device__ __forceinline__ static bool valid(T e) { return e != 0xffffffffu; }
+};
+template <>
+struct Entry<false> {
+    using T = int2;
+    __device__ __forceinline__ static T make(int lr, int32_t v, int) { return make_int2(lr, v); }
+    __device__ __forceinline__ static int row(T e, int) { return e.x; }
+    __device__ __forceinline__ static int32_t col(T e, int) { return e.y; }
+    __device__ __forceinline__ static T invalid() { return make_int2(-1, 0); }
+    __device__ __forceinline__ static bool valid(T e) { return e.x >= 0; }
+};
+
+template <bool PACKED>
 __global__ void __launch_bounds__(1024) csr_partition(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
                                                       int64_t m, int64_t n, int64_t rb, int64_t re, int shift, int nb,
-                                                      const int64_t *__restrict__ raw_ptr,
-                                                      unsigned long long *__restrict__ bcur, int2 *__restrict__ pairs) {
+                                                      int vbits, const int64_t *__restrict__ raw_ptr,
+                                                      unsigned long long *__restrict__ bcur,
+                                                      typename Entry<PACKED>::T *__restrict__ pairs) {
+    using E = Entry<PACKED>;
     extern __shared__ long long psm[];
     long long *base = psm;                                              // nb
     unsigned int *hist = reinterpret_cast<unsigned int *>(psm + nb);    // nb
+    const int bmask = (1 << shift) - 1;
     const int64_t ntiles = (m + kPartTile - 1) / kPartTile;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t e0 = tile * kPartTile;
@@ -361,11 +392,11 @@ __global__ void __launch_bounds__(1024) csr_partition(const int32_t *__restrict_
                 if (u < 0 || v < 0 || u >= n || v >= n || u == v) continue;
                 if (u >= rb && u < re) {
                     const int b = static_cast<int>((u - rb) >> shift);
-                    pairs[base[b] + atomicAdd(&hist[b], 1u)] = make_int2(static_cast<int32_t>(u - rb), v);
+                    pairs[base[b] + atomicAdd(&hist[b], 1u)] = E::make(static_cast<int>(u - rb) & bmask, v, vbits);
                 }
                 if (v >= rb && v < re) {
                     const int b = static_cast<int>((v - rb) >> shift);
-                    pairs[base[b] + atomicAdd(&hist[b], 1u)] = make_int2(static_cast<int32_t>(v - rb), u);
+                    pairs[base[b] + atomicAdd(&hist[b], 1u)] = E::make(static_cast<int>(v - rb) & bmask, u, vbits);
                 }
             }
         }
@@ -397,9 +428,10 @@ __device__ __forceinline__ int warp_sort_dedup(int32_t *a, int len, int32_t *out
     return written;
 }
 
-__global__ void __launch_bounds__(1024) csr_bucket_sort(const int2 *__restrict__ pairs,
+template <bool PACKED>
+__global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PACKED>::T *__restrict__ pairs,
                                                         const int64_t *__restrict__ raw_ptr, int64_t nl, int shift,
-                                                        int nb, int32_t *__restrict__ col_raw,
+                                                        int nb, int vbits, int32_t *__restrict__ col_raw,
                                                         int32_t *__restrict__ deg, int64_t *__restrict__ fb_rows,
                                                         int32_t *__restrict__ fb_count) {
     extern __shared__ int32_t bsm[];
@@ -432,15 +464,15 @@ __global__ void __launch_bounds__(1024) csr_bucket_sort(const int2 *__restrict__
         if (fits) {
             // placement: batched loads for memory-level parallelism, warp-aggregated slot claims per row
             for (int64_t i0 = (int64_t)threadIdx.x * kLoadBatch; i0 < E; i0 += (int64_t)blockDim.x * kLoadBatch) {
-                int2 p[kLoadBatch];
+                typename Entry<PACKED>::T p[kLoadBatch];
 #pragma unroll
                 for (int k = 0; k < kLoadBatch; ++k)
-                    p[k] = (i0 + k < E) ? pairs[e0 + i0 + k] : make_int2(-1, 0);
+                    p[k] = (i0 + k < E) ? pairs[e0 + i0 + k] : Entry<PACKED>::invalid();
 #pragma unroll
                 for (int k = 0; k < kLoadBatch; ++k) {
-                    if (p[k].x >= 0) {
-                        const int lr = static_cast<int>(p[k].x - r0);
-                        s[off[lr] + atomicAdd(&cur[lr], 1)] = p[k].y;
+                    if (Entry<PACKED>::valid(p[k])) {
+                        const int lr = Entry<PACKED>::row(p[k], vbits);
+                        s[off[lr] + atomicAdd(&cur[lr], 1)] = Entry<PACKED>::col(p[k], vbits);
                     }
                 }
             }
@@ -490,10 +522,10 @@ __global__ void __launch_bounds__(1024) csr_bucket_sort(const int2 *__restrict__
         } else {
             // too large for shared memory: place into col_raw (global), rows go to the warp/block sort kernels
             for (int64_t idx = threadIdx.x; idx < E; idx += blockDim.x) {
-                const int2 p = pairs[e0 + idx];
-                const int64_t row = p.x;
-                const int64_t k = atomicAdd(&cur[row - r0], 1);
-                col_raw[raw_ptr[row] + k] = p.y;
+                const typename Entry<PACKED>::T p = pairs[e0 + idx];
+                const int lr = Entry<PACKED>::row(p, vbits);
+                const int64_t k = atomicAdd(&cur[lr], 1);
+                col_raw[raw_ptr[r0 + lr] + k] = Entry<PACKED>::col(p, vbits);
             }
             if (threadIdx.x == 0) fb_base = atomicAdd(fb_count, nr);
             __syncthreads();
@@ -628,31 +660,46 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
     int32_t *fb_count = nullptr;
     if (bucketed) {
         const int nb = static_cast<int>(ceil_div(nl, (int64_t)1 << shift));
+        int vbits = 1;
+        while (vbits < 31 && ((int64_t)1 << vbits) < n) ++vbits;
+        const bool packed = shift + vbits <= 32;
         unsigned long long *bcur = nullptr;
-        int2 *pairs = nullptr;
+        void *pairs = nullptr;
         RG_TRY(dalloc_t(ctx, &bcur, (size_t)nb));
-        RG_TRY(dalloc_t(ctx, &pairs, (size_t)cap));
+        RG_TRY(dalloc(ctx, &pairs, (size_t)cap * (packed ? 4 : 8)));
         RG_TRY(dalloc_t(ctx, &fb_rows, (size_t)nl));
         RG_TRY(dalloc_t(ctx, &fb_count, 1));
         RG_CUDA(cudaMemsetAsync(bcur, 0, sizeof(unsigned long long) * nb, st));
         RG_CUDA(cudaMemsetAsync(fb_count, 0, sizeof(int32_t), st));
+        const size_t bsmem = (size_t)(kBucketCap + 3 * kMaxBucketRows + 1) * 4;
         static bool attrs = false;
         if (!attrs) {
-            RG_CUDA(cudaFuncSetAttribute(csr_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 12));
-            RG_CUDA(cudaFuncSetAttribute(csr_bucket_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (kBucketCap + 3 * kMaxBucketRows + 1) * 4));
+            RG_CUDA(cudaFuncSetAttribute(csr_partition<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 12));
+            RG_CUDA(cudaFuncSetAttribute(csr_partition<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 12));
+            RG_CUDA(cudaFuncSetAttribute(csr_bucket_sort<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
+            RG_CUDA(cudaFuncSetAttribute(csr_bucket_sort<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
             attrs = true;
         }
         if (m > 0) {
             const int pgrid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, kPartTile), ctx->sm_count)));
             LaunchScope L(ctx, K_CSR_PARTITION);
-            csr_partition<<<pgrid, 1024, (size_t)nb * 12, st>>>(src, dst, m, n, rb, re, shift, nb, raw_ptr, bcur, pairs);
+            if (packed)
+                csr_partition<true><<<pgrid, 1024, (size_t)nb * 12, st>>>(src, dst, m, n, rb, re, shift, nb, vbits, raw_ptr,
+                                                                          bcur, static_cast<uint32_t *>(pairs));
+            else
+                csr_partition<false><<<pgrid, 1024, (size_t)nb * 12, st>>>(src, dst, m, n, rb, re, shift, nb, vbits, raw_ptr,
+                                                                           bcur, static_cast<int2 *>(pairs));
         }
         RG_CHECK_LAUNCH(ctx);
         {
             LaunchScope L(ctx, K_CSR_BUCKET);
-            csr_bucket_sort<<<std::min(nb, ctx->sm_count), 1024, (size_t)(kBucketCap + 3 * kMaxBucketRows + 1) * 4, st>>>(
-                pairs, raw_ptr, nl, shift, nb, col_raw, g->deg_local, fb_rows, fb_count);
+            const int bgrid = std::min(nb, ctx->sm_count);
+            if (packed)
+                csr_bucket_sort<true><<<bgrid, 1024, bsmem, st>>>(static_cast<const uint32_t *>(pairs), raw_ptr, nl, shift, nb,
+                                                                  vbits, col_raw, g->deg_local, fb_rows, fb_count);
+            else
+                csr_bucket_sort<false><<<bgrid, 1024, bsmem, st>>>(static_cast<const int2 *>(pairs), raw_ptr, nl, shift, nb,
+                                                                   vbits, col_raw, g->deg_local, fb_rows, fb_count);
         }
         RG_CHECK_LAUNCH(ctx);
         {
