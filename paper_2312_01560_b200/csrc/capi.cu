@@ -456,6 +456,46 @@ static raftgp_status gcn_stack(raftgp_graph g, int32_t layers, const int32_t *di
     return st;
 }
 
+// GCN stacks of two variants; their last hop runs as ONE pair hop over the interleaved operand
+// [T_a | T_b] written by the previous hops' epilogues (512-B instead of 256-B rows per gather at d = 64).
+static raftgp_status gcn_stack_pair(raftgp_graph g, int32_t layers, const int32_t *dims, uint64_t seed, float *T1a,
+                                    float *T1b, float *Za, float *Zb) {
+    const int32_t d = dims[layers];
+    if (layers < 2 || !gcn_pair_supported(d)) {
+        RG_TRY(gcn_stack(g, layers, dims, seed, T1a, Za, nullptr));
+        return gcn_stack(g, layers, dims, seed, T1b, Zb, nullptr);
+    }
+    raftgp_ctx ctx = g->ctx;
+    std::vector<float *> Ws(layers + 1, nullptr);
+    raftgp_status st = RAFTGP_OK;
+    for (int k = 2; k <= layers && st == RAFTGP_OK; ++k) {
+        st = dalloc_t(ctx, &Ws[k], (size_t)dims[k - 1] * dims[k]);
+        if (st == RAFTGP_OK) st = sketch_fill(ctx, seed, (uint32_t)k, 0, dims[k - 1], dims[k], dims[k - 1], Ws[k]);
+    }
+    float *Tboth = nullptr;
+    if (st == RAFTGP_OK) st = dalloc_t(ctx, &Tboth, (size_t)g->n * 2 * d);
+    float *cur[2] = {T1a, T1b};
+    for (int k = 1; k < layers && st == RAFTGP_OK; ++k) {
+        for (int v = 0; v < 2 && st == RAFTGP_OK; ++v) {
+            float *Tnext = nullptr;
+            int32_t ld = 0;
+            if (k + 1 == layers) {
+                Tnext = Tboth + v * d;
+                ld = 2 * d;
+            } else {
+                st = dalloc_t(ctx, &Tnext, (size_t)g->n * dims[k + 1]);
+            }
+            if (st == RAFTGP_OK) st = gcn_hop(g, cur[v], dims[k], nullptr, Ws[k + 1], dims[k + 1], Tnext, ld);
+            if (cur[v] != T1a && cur[v] != T1b) dfree(ctx, cur[v]);
+            cur[v] = (k + 1 == layers) ? nullptr : Tnext;
+        }
+    }
+    if (st == RAFTGP_OK) st = gcn_final_pair(g, Tboth, d, Za, Zb);
+    dfree(ctx, Tboth);
+    for (auto w : Ws) dfree(ctx, w);
+    return st;
+}
+
 static raftgp_status whole_graph(raftgp_graph g) {
     if (g->row_begin != 0 || g->row_end != g->n)
         return fail(RAFTGP_ERR_PARAM, "this call needs a whole-graph handle (use raftgp_gcn_hop per rank)");
@@ -535,7 +575,15 @@ static raftgp_status embed_pre(raftgp_graph g, int32_t nvariants, const int32_t 
     }
     dfree(ctx, thw);
     dfree(ctx, gw);
-    for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v) st = gcn_stack(g, layers, dims, seed, T1[v], Z_dev[v], nullptr);
+    for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v) {
+        if (dual && variants[v] == RAFTGP_MOD) continue;    // computed with its NCUT partner below
+        if (dual && variants[v] == RAFTGP_NCUT) {
+            const int a = where[RAFTGP_NCUT], b = where[RAFTGP_MOD];
+            st = gcn_stack_pair(g, layers, dims, seed, T1[a], T1[b], Z_dev[a], Z_dev[b]);
+        } else {
+            st = gcn_stack(g, layers, dims, seed, T1[v], Z_dev[v], nullptr);
+        }
+    }
     dfree(ctx, W1);
     for (auto t : T1) dfree(ctx, t);
     return st;

@@ -160,6 +160,9 @@ raftgp_status feature_hop_pre(raftgp_graph g, int variant_or_dual, int32_t l1, c
                               const double *gvec_w, float *T_a, float *T_b);
 raftgp_status gcn_transform(raftgp_graph g, const float *Z, int32_t lin, const float *W, int32_t lout, float *T);
 raftgp_status gcn_hop(raftgp_graph g, const float *Tfull, int32_t w, float *Zout, const float *Wn, int32_t wn,
-                      float *Tnext);
+                      float *Tnext, int32_t tn_ld = 0);
+// last GCN hop of two variants over the interleaved operand [T_a | T_b] (n x 2d); d in {32, 64}
+bool gcn_pair_supported(int32_t d);
+raftgp_status gcn_final_pair(raftgp_graph g, const float *Tboth, int32_t d, float *Za, float *Zb);
 
 }  // namespace raftgp

@@ -33,7 +33,10 @@ constexpr unsigned FULL = 0xffffffffu;
 #define RG_PREFETCH 0   // 1: load the next row's first col chunk while gathering the current row
 #endif
 
-enum Kind : int { KIND_NCUT = 0, KIND_MOD = 1, KIND_MOD_REDUCED = 2, KIND_GCN = 3, KIND_LOAD = 4, KIND_DUAL = 5 };
+// GCN2: the last GCN hop of two variants at once over an interleaved operand [T_a | T_b] (one 2d-wide
+// gather per neighbour instead of two d-wide ones); each half is tanh'd and l2-normalised on its own.
+enum Kind : int { KIND_NCUT = 0, KIND_MOD = 1, KIND_MOD_REDUCED = 2, KIND_GCN = 3, KIND_LOAD = 4, KIND_DUAL = 5,
+                  KIND_GCN2 = 6 };
 
 struct HopArgs {
     int64_t nl, rb, n;
@@ -52,6 +55,7 @@ struct HopArgs {
     float *out2;               // KIND_DUAL: second variant's Y (MOD), may be null
     float *Tn2;                // KIND_DUAL: second variant's T
     bool scale_sh;             // multiply the stored rows by s^_i (feature hop on Theta' = Theta W1)
+    int32_t tn_ld;             // row stride of Tn in floats (0 = WN)
 };
 
 __device__ __forceinline__ float4 ldg4(const float4 *p) { return __ldg(p); }
@@ -218,7 +222,8 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
                     if (RG_PREFETCH) nc0 = (nbeg + lane < nend) ? __ldg(a.col + nbeg + lane) : 0;
                 }
                 float4 self = make_float4(0.f, 0.f, 0.f, 0.f);
-                if constexpr (KIND == KIND_GCN) self = ldg4(reinterpret_cast<const float4 *>(a.X) + gi * LPN + cl);
+                if constexpr (KIND == KIND_GCN || KIND == KIND_GCN2)
+                    self = ldg4(reinterpret_cast<const float4 *>(a.X) + gi * LPN + cl);
                 gather_row<W, U, KindTraits<KIND>::MODE>(a, beg, end, c0, lane, acc, acc2);
                 beg = nbeg;
                 end = nend;
@@ -244,27 +249,32 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
                     const double c = static_cast<double>(__ldg(a.deg_all + gi)) * a.inv2e;
                     y = make_float4(static_cast<float>(acc.x - c * acc2.x), static_cast<float>(acc.y - c * acc2.y),
                                     static_cast<float>(acc.z - c * acc2.z), static_cast<float>(acc.w - c * acc2.w));
-                } else {   // KIND_GCN: H_i = s^_i (T_i + sum_j T_j); tanh; row l2 normalisation
+                } else {   // KIND_GCN(2): H_i = s^_i (T_i + sum_j T_j); tanh; row l2 normalisation
                     add4(acc, self);
                     const float shi = __ldg(a.sh_all + gi);
                     y = make_float4(tanhf(shi * acc.x), tanhf(shi * acc.y), tanhf(shi * acc.z), tanhf(shi * acc.w));
                     float ss = y.x * y.x + y.y * y.y + y.z * y.z + y.w * y.w;
+                    constexpr int RL = KIND == KIND_GCN2 ? LPN / 2 : LPN;   // lanes of one normalised row
 #pragma unroll
-                    for (int o = 1; o < LPN; o <<= 1) ss += __shfl_xor_sync(FULL, ss, o);
+                    for (int o = 1; o < RL; o <<= 1) ss += __shfl_xor_sync(FULL, ss, o);
                     if (ss > 0.f) {
                         const float nrm = sqrtf(ss);
                         y = make_float4(y.x / nrm, y.y / nrm, y.z / nrm, y.w / nrm);
                     }
                 }
             }
-            if constexpr (WN == 0 && KIND != KIND_GCN && KIND != KIND_LOAD) {
+            if constexpr (WN == 0 && KIND != KIND_GCN && KIND != KIND_GCN2 && KIND != KIND_LOAD) {
                 if (a.scale_sh) {
                     const float shi = __ldg(a.sh_all + gi);
                     y = make_float4(shi * y.x, shi * y.y, shi * y.z, shi * y.w);
                     y2 = make_float4(shi * y2.x, shi * y2.y, shi * y2.z, shi * y2.w);
                 }
             }
-            if (sub == 0) {
+            if constexpr (KIND == KIND_GCN2) {
+                constexpr int HL = LPN / 2;
+                float *o = cl < HL ? a.out : a.out2;
+                if (sub == 0 && o != nullptr) reinterpret_cast<float4 *>(o)[row * HL + (cl % HL)] = y;
+            } else if (sub == 0) {
                 if (a.out != nullptr) reinterpret_cast<float4 *>(a.out)[row * LPN + cl] = y;
                 if constexpr (NV == 2) {
                     if (a.out2 != nullptr) reinterpret_cast<float4 *>(a.out2)[row * LPN + cl] = y2;
@@ -316,7 +326,8 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
                         const int64_t row = a.order ? static_cast<int64_t>(__ldg(a.order + row0 + r_in)) : row0 + r_in;
                         const float shi = __ldg(a.sh_all + a.rb + row);
                         float4 *T4 = reinterpret_cast<float4 *>(v == 0 ? a.Tn : a.Tn2);
-                        T4[row * OL + oc] = make_float4(shi * o[q].x, shi * o[q].y, shi * o[q].z, shi * o[q].w);
+                        const int64_t ld4 = a.tn_ld > 0 ? a.tn_ld / 4 : OL;
+                        T4[row * ld4 + oc] = make_float4(shi * o[q].x, shi * o[q].y, shi * o[q].z, shi * o[q].w);
                     }
                 }
             }
@@ -410,7 +421,7 @@ raftgp_status launch_fast(raftgp_ctx ctx, const HopArgs &a) {
     const int64_t groups = ceil_div(a.nl, RB);
     const int64_t want = ceil_div(groups, WPB);
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count * blocks_per_sm)));
-    const int kid = KIND == KIND_GCN ? K_GCN_HOP : (KIND == KIND_LOAD ? K_TRANSFORM : K_FEATURE_HOP);
+    const int kid = (KIND == KIND_GCN || KIND == KIND_GCN2) ? K_GCN_HOP : (KIND == KIND_LOAD ? K_TRANSFORM : K_FEATURE_HOP);
     {
         LaunchScope L(ctx, kid);
         kern<<<grid, THREADS, smem, ctx->stream>>>(a);
@@ -555,13 +566,30 @@ raftgp_status gcn_transform(raftgp_graph g, const float *Z, int32_t lin, const f
 }
 
 raftgp_status gcn_hop(raftgp_graph g, const float *Tfull, int32_t w, float *Zout, const float *Wn, int32_t wn,
-                      float *Tnext) {
+                      float *Tnext, int32_t tn_ld) {
     HopArgs a = base_args(g, w);
     a.X = Tfull;
     a.out = Zout;
     a.Wn = Wn;
     a.Tn = Tnext;
+    a.tn_ld = tn_ld;
+    if (tn_ld > 0 && tn_ld != wn && !((w == 32 || w == 64 || w == 128) && (wn == 32 || wn == 64 || wn == 128) &&
+                                      aligned16(Tfull) && aligned16(Tnext) && aligned16(Wn) && tn_ld % 4 == 0))
+        return fail(RAFTGP_ERR_INTERNAL, "gcn_hop: strided T_next needs the fast kernel");
     return dispatch<KIND_GCN>(g->ctx, a, w, Wn ? wn : 0);
+}
+
+bool gcn_pair_supported(int32_t d) { return d == 32 || d == 64; }
+
+raftgp_status gcn_final_pair(raftgp_graph g, const float *Tboth, int32_t d, float *Za, float *Zb) {
+    if (g->nl == 0) return RAFTGP_OK;
+    HopArgs a = base_args(g, 2 * d);
+    a.X = Tboth;
+    a.out = Za;
+    a.out2 = Zb;
+    if (!(gcn_pair_supported(d) && aligned16(Tboth) && aligned16(Za) && aligned16(Zb)))
+        return fail(RAFTGP_ERR_INTERNAL, "gcn_final_pair: unsupported width/alignment");
+    return d == 32 ? launch_fast<KIND_GCN2, 64, 0>(g->ctx, a) : launch_fast<KIND_GCN2, 128, 0>(g->ctx, a);
 }
 
 }  // namespace raftgp
