@@ -404,6 +404,55 @@ __global__ void __launch_bounds__(1024) csr_partition(const int32_t *__restrict_
     }
 }
 
+// Register bitonic sort of up to 32*E values per warp: element e of lane l has index e*32 + l; stages with
+// j >= 32 swap inside a lane, the others exchange by shuffle. Then dedup and write the unique prefix.
+template <int E>
+__device__ __forceinline__ int warp_sort_dedup_reg(const int32_t *a, int len, int32_t *outp, int lane) {
+    int32_t v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = (e * 32 + lane < len) ? a[e * 32 + lane] : INT_MAX;
+#pragma unroll
+    for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j >= 1; j >>= 1) {
+            if (j >= 32) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int e2 = e ^ (j >> 5);
+                    if (e2 > e) {
+                        const bool up = (((e * 32 + lane) & k) == 0);
+                        const int32_t lo = min(v[e], v[e2]), hi = max(v[e], v[e2]);
+                        v[e] = up ? lo : hi;
+                        v[e2] = up ? hi : lo;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int32_t o = __shfl_xor_sync(0xffffffffu, v[e], j);
+                    const bool up = (((e * 32 + lane) & k) == 0);
+                    const bool lower = ((lane & j) == 0);
+                    v[e] = (lower == up) ? min(v[e], o) : max(v[e], o);
+                }
+            }
+        }
+    }
+    int written = 0;
+    int32_t last_prev = INT_MIN;   // last element of the previous 32-chunk (lane 31's value)
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        int32_t prev = __shfl_up_sync(0xffffffffu, v[e], 1);
+        if (lane == 0) prev = last_prev;
+        const int idx = e * 32 + lane;
+        const bool keep = idx < len && (idx == 0 || v[e] != prev);
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) outp[written + __popc(bal & ((1u << lane) - 1u))] = v[e];
+        written += __popc(bal);
+        last_prev = __shfl_sync(0xffffffffu, v[e], 31);
+    }
+    return written;
+}
+
 // warp sort + dedup of one row held in shared memory; writes the unique prefix to outp, returns its length
 __device__ __forceinline__ int warp_sort_dedup(int32_t *a, int len, int32_t *outp, int lane) {
     if (len <= 32) {
@@ -415,6 +464,8 @@ __device__ __forceinline__ int warp_sort_dedup(int32_t *a, int len, int32_t *out
         if (keep) outp[__popc(bal & ((1u << lane) - 1u))] = v;
         return __popc(bal);
     }
+    if (len <= 64) return warp_sort_dedup_reg<2>(a, len, outp, lane);
+    if (len <= 128) return warp_sort_dedup_reg<4>(a, len, outp, lane);
     bitonic_any(a, len, lane, 32, WarpSync());
     int written = 0;
     for (int base = 0; base < len; base += 32) {
