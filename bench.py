@@ -243,6 +243,9 @@ def main():
     if world > 1:
         tdist.barrier()
     dev = torch.device("cuda", torch.cuda.current_device())
+    if world > 1:
+        # a non-default compute stream: NCCL's all-gathers (own streams) then overlap the hop kernels
+        torch.cuda.set_stream(torch.cuda.Stream(dev))
     cfg = synth.CONFIGS[args.config]
     variants = args.variants.split(",")
     dims = tuple(cfg.dims)

@@ -183,6 +183,14 @@ RAFTGP_API raftgp_status raftgp_embed_multi(raftgp_graph g, int32_t nvariants, c
                                             const int32_t *dims, uint64_t seed, float *const *Y_dev,
                                             float *const *Z_dev);
 
+/* First GCN operand of every listed variant for the LOCAL rows (works on row-partitioned graphs):
+ * T1 = s^ (.) (X Theta W^(1)) = s^ (.) (Y W^(1)), X the variant's feature operator, Theta and W^(1) as in
+ * raftgp_embed. Theta' = Theta W^(1) is generated on chip (Theta never written) and NCUT + MOD share one
+ * gather of Theta' (GEMM before aggregation, reading #13). r = Theta width, l1 = W^(1) width.
+ * T1_dev: host array of nvariants device pointers (local_rows x l1). Same errors as raftgp_project. */
+RAFTGP_API raftgp_status raftgp_feature_transform(raftgp_graph g, int32_t nvariants, const int32_t *variants,
+                                                  int32_t r, int32_t l1, uint64_t seed, float *const *T1_dev);
+
 /* ---------------------------------------------------------------- a7: scoring (host, synchronous)
  * On a whole-graph handle. assign: host int32[n] labels in [0, k).
  * Modularity, Eq. 3. Errors: PARAM (label outside [0,k), k <= 0), DATA (2e = 0). */

@@ -553,19 +553,18 @@ raftgp_status raftgp_embed(raftgp_graph g, raftgp_variant variant, int32_t layer
 // project + GCN without materialising Y: Theta' = Theta W1 is generated once (Theta on chip), every
 // variant's first operand T1 = s^ (.) (X Theta') comes from a GEMM-free feature hop (NCUT and MOD share
 // one gather), then the GCN stacks. Same results as the Y path up to fp32 rounding order (reading #13).
-static raftgp_status embed_pre(raftgp_graph g, int32_t nvariants, const int32_t *variants, int32_t layers,
-                               const int32_t *dims, uint64_t seed, float *const *Z_dev, const int where[3]) {
+// T1 = s^ (.) (X Theta W1) of the local rows for every listed variant (Theta' = Theta W1 on chip, one
+// shared gather for NCUT + MOD). T1[v]: local_rows x l1 device buffers.
+static raftgp_status first_transform_pre(raftgp_graph g, int32_t nvariants, const int32_t *variants, int32_t r,
+                                         int32_t l1, uint64_t seed, float *const *T1, const int where[3]) {
     raftgp_ctx ctx = g->ctx;
-    const int32_t r = dims[0], l1 = dims[1];
     float *W1 = nullptr, *thw = nullptr;
     double *gw = nullptr;
-    std::vector<float *> T1(nvariants, nullptr);
     raftgp_status st = dalloc_t(ctx, &W1, (size_t)r * l1);
     if (st == RAFTGP_OK) st = sketch_fill(ctx, seed, 1u, 0, r, l1, r, W1);
     if (st == RAFTGP_OK) st = dalloc_t(ctx, &thw, (size_t)g->n * l1);
     if (st == RAFTGP_OK && where[RAFTGP_MOD] >= 0) st = dalloc_t(ctx, &gw, (size_t)l1);
     if (st == RAFTGP_OK) st = sketch_theta_w(g, seed, r, W1, l1, thw, gw);
-    for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v) st = dalloc_t(ctx, &T1[v], (size_t)g->n * l1);
     const bool dual = where[RAFTGP_NCUT] >= 0 && where[RAFTGP_MOD] >= 0;
     if (st == RAFTGP_OK && dual)
         st = feature_hop_pre(g, -1, l1, thw, gw, T1[where[RAFTGP_NCUT]], T1[where[RAFTGP_MOD]]);
@@ -575,6 +574,19 @@ static raftgp_status embed_pre(raftgp_graph g, int32_t nvariants, const int32_t 
     }
     dfree(ctx, thw);
     dfree(ctx, gw);
+    dfree(ctx, W1);
+    return st;
+}
+
+static raftgp_status embed_pre(raftgp_graph g, int32_t nvariants, const int32_t *variants, int32_t layers,
+                               const int32_t *dims, uint64_t seed, float *const *Z_dev, const int where[3]) {
+    raftgp_ctx ctx = g->ctx;
+    const int32_t r = dims[0], l1 = dims[1];
+    std::vector<float *> T1(nvariants, nullptr);
+    raftgp_status st = RAFTGP_OK;
+    for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v) st = dalloc_t(ctx, &T1[v], (size_t)g->n * l1);
+    if (st == RAFTGP_OK) st = first_transform_pre(g, nvariants, variants, r, l1, seed, T1.data(), where);
+    const bool dual = where[RAFTGP_NCUT] >= 0 && where[RAFTGP_MOD] >= 0;
     for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v) {
         if (dual && variants[v] == RAFTGP_MOD) continue;    // computed with its NCUT partner below
         if (dual && variants[v] == RAFTGP_NCUT) {
@@ -584,7 +596,6 @@ static raftgp_status embed_pre(raftgp_graph g, int32_t nvariants, const int32_t 
             st = gcn_stack(g, layers, dims, seed, T1[v], Z_dev[v], nullptr);
         }
     }
-    dfree(ctx, W1);
     for (auto t : T1) dfree(ctx, t);
     return st;
 }
@@ -632,6 +643,47 @@ raftgp_status raftgp_embed_multi(raftgp_graph g, int32_t nvariants, const int32_
     for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v) st = gcn_stack(g, layers, dims, seed, T1[v], Z_dev[v], nullptr);
     dfree(ctx, W1);
     for (auto t : T1) dfree(ctx, t);
+    return st;
+    RG_GUARD_END
+}
+
+raftgp_status raftgp_feature_transform(raftgp_graph g, int32_t nvariants, const int32_t *variants, int32_t r,
+                                       int32_t l1, uint64_t seed, float *const *T1_dev) {
+    RG_GUARD_BEGIN
+    RG_TRY(need_ready(g));
+    if (nvariants < 1 || !variants || !T1_dev) return fail(RAFTGP_ERR_PARAM, "need >= 1 variant and outputs");
+    if (l1 <= 0) return fail(RAFTGP_ERR_PARAM, "l1 must be > 0");
+    int where[3] = {-1, -1, -1};
+    for (int v = 0; v < nvariants; ++v) {
+        RG_TRY(check_variant(g, variants[v], r));
+        if (where[variants[v]] >= 0) return fail(RAFTGP_ERR_PARAM, "variant listed twice");
+        where[variants[v]] = v;
+        if (g->nl > 0 && !T1_dev[v]) return fail(RAFTGP_ERR_PARAM, "null T1");
+    }
+    RG_TRY(set_device(g->ctx));
+    if (sketch_w_supported(r, l1)) {
+        bool al = true;
+        for (int v = 0; v < nvariants; ++v) al = al && aligned16(T1_dev[v]);
+        if (al) return first_transform_pre(g, nvariants, variants, r, l1, seed, T1_dev, where);
+    }
+    // any other shape: Theta materialised, feature hop then transform per variant
+    raftgp_ctx ctx = g->ctx;
+    float *theta = nullptr, *W1 = nullptr, *Y = nullptr;
+    double *gvec = nullptr;
+    raftgp_status st = dalloc_t(ctx, &theta, (size_t)g->n * r);
+    if (st == RAFTGP_OK && where[RAFTGP_MOD] >= 0) st = dalloc_t(ctx, &gvec, (size_t)r);
+    if (st == RAFTGP_OK) st = sketch_theta(g, seed, r, theta, gvec);
+    if (st == RAFTGP_OK) st = dalloc_t(ctx, &W1, (size_t)r * l1);
+    if (st == RAFTGP_OK) st = sketch_fill(ctx, seed, 1u, 0, r, l1, r, W1);
+    if (st == RAFTGP_OK) st = dalloc_t(ctx, &Y, (size_t)g->nl * r);
+    for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v) {
+        st = feature_hop(g, variants[v], r, theta, gvec, Y, nullptr, 0, nullptr);
+        if (st == RAFTGP_OK) st = gcn_transform(g, Y, r, W1, l1, T1_dev[v]);
+    }
+    dfree(ctx, theta);
+    dfree(ctx, gvec);
+    dfree(ctx, W1);
+    dfree(ctx, Y);
     return st;
     RG_GUARD_END
 }

@@ -6,8 +6,9 @@ the all-gathered (P*R)-row block indexes global rows directly. Exchange steps â€
      global 2e, s and s^ (raftgp_graph_set_degrees);
   2. before every GCN hop: all-gather of the next operand T_k = s^ (.) (Z^(k-1) W^(k)) (n x L_k fp32).
 Hop 0 needs no exchange: Theta is counter-based, so every rank regenerates the rows it gathers, and
-the MOD rank-1 vector g = d^T Theta is reduced over global fixed chunks identically on every rank.
+the MOD rank-1 vector g = d^T Theta' is reduced over global fixed chunks identically on every rank.
 Each row's arithmetic is a function of that row only, so the result is bit-identical for any P.
+The per-hop all-gathers of two variants are software-pipelined against each other's compute.
 
 The per-rank pipeline is a generator that yields ("gather", tensor) at each exchange point and
 receives the gathered block; drivers run it over torch.distributed (NCCL on B200, gloo on CPU tests)
@@ -16,7 +17,7 @@ or, for single-GPU testing, over P shards in lockstep ("loopback"). The compute 
 """
 from __future__ import annotations
 
-from typing import Callable, Generator, List, Optional, Sequence
+from typing import Generator, List, Optional, Sequence
 
 import torch
 
@@ -52,14 +53,11 @@ class CudaEngine:
     def set_degrees(self, h, deg_all):
         h.set_degrees(deg_all)
 
-    def project(self, h, variant, r, seed):
-        return rg.raftgp_project(h, variant, r, seed)
+    def feature_transform(self, h, variants, dims, seed):
+        return rg.raftgp_feature_transform(h, variants, dims[0], dims[1], seed)
 
     def weights(self, seed, k, a, b):
         return rg.raftgp_weights(self.ctx, seed, k, a, b)
-
-    def transform(self, h, Z, W):
-        return rg.raftgp_gcn_transform(h, Z, W)
 
     def hop(self, h, T_full, W_next, want_Z: bool):
         rows = h.rows
@@ -70,8 +68,13 @@ class CudaEngine:
 
 def rank_pipeline(engine, n: int, src, dst, rank: int, world: int, variants, dims: Sequence[int], seed: int,
                   keep: Optional[dict] = None) -> Generator:
-    """Yields ("gather", local_block) at each exchange; returns {variant: this rank's rows of Z}
-    (or the Z tensor itself when `variants` is a single variant)."""
+    """One rank's share of the path. Yields exchange requests to its driver:
+        ("gather", block)  -> the all-gathered block (blocking; used for the degree vector)
+        ("start", block)   -> a handle; the all-gather runs while this rank keeps computing
+        ("wait", handle)   -> the all-gathered block
+    With several variants the exchanges are software-pipelined: variant A's hop-k gather is in flight
+    while variant B's hop k computes and vice versa, so comm overlaps compute without changing any
+    arithmetic. Returns {variant: this rank's rows of Z} (or Z itself for a single variant)."""
     single = isinstance(variants, (str, int))
     vlist = [variants] if single else list(variants)
     ranges, R = row_partition(n, world)
@@ -80,21 +83,30 @@ def rank_pipeline(engine, n: int, src, dst, rank: int, world: int, variants, dim
     deg_all = yield ("gather", _pad(engine.local_degrees(h), R))
     engine.set_degrees(h, deg_all[:n].contiguous())
     L = len(dims) - 1
+    T = engine.feature_transform(h, vlist, dims, seed)          # {v: T1}, local rows
+    W = {k: engine.weights(seed, k, dims[k - 1], dims[k]) for k in range(2, L + 1)}
+    handles = {}
+    for v in vlist:
+        handles[v] = yield ("start", _pad(T[v], R))
     out = {}
-    for variant in vlist:
-        Y = engine.project(h, variant, dims[0], seed)
-        T = engine.transform(h, Y, engine.weights(seed, 1, dims[0], dims[1]))
-        Z = None
-        for k in range(1, L + 1):
-            T_full = yield ("gather", _pad(T, R))
-            Wn = engine.weights(seed, k + 1, dims[k], dims[k + 1]) if k < L else None
-            Z, T = engine.hop(h, T_full[:n], Wn, want_Z=(k == L))
-        out[variant] = Z
-        if keep is not None:
-            keep.setdefault("Y", {})[variant] = Y
+    for k in range(1, L + 1):
+        for v in vlist:
+            T_full = yield ("wait", handles[v])
+            Zv, Tn = engine.hop(h, T_full[:n], W.get(k + 1), want_Z=(k == L))
+            if k < L:
+                handles[v] = yield ("start", _pad(Tn, R))
+            else:
+                out[v] = Zv
     if keep is not None:
         keep["graph"] = h
     return out[vlist[0]] if single else out
+
+
+class _Done:
+    """A completed exchange (loopback / blocking drivers)."""
+
+    def __init__(self, value):
+        self.value = value
 
 
 def run_loopback(gens: List[Generator]):
@@ -102,11 +114,18 @@ def run_loopback(gens: List[Generator]):
     msgs = [next(g) for g in gens]
     results: List[Optional[torch.Tensor]] = [None] * len(gens)
     while True:
-        full = torch.cat([m[1] for m in msgs], 0)
+        kind = msgs[0][0]
+        if any(m[0] != kind for m in msgs):
+            raise RuntimeError("rank pipelines went out of step")
+        if kind == "wait":
+            replies = [m[1].value for m in msgs]
+        else:
+            full = torch.cat([m[1] for m in msgs], 0)
+            replies = [full if kind == "gather" else _Done(full) for _ in msgs]
         nxt, done = [], 0
         for p, g in enumerate(gens):
             try:
-                nxt.append(g.send(full))
+                nxt.append(g.send(replies[p]))
             except StopIteration as stop:
                 results[p] = stop.value
                 nxt.append(None)
@@ -118,25 +137,39 @@ def run_loopback(gens: List[Generator]):
         msgs = nxt
 
 
-def run_distributed(gen: Generator, group=None, gather: Optional[Callable] = None):
+class _Pending:
+    def __init__(self, work, out, parts=None):
+        self.work, self.out, self.parts = work, out, parts
+
+    def result(self):
+        self.work.wait()
+        return torch.cat(self.parts, 0) if self.parts is not None else self.out
+
+
+def run_distributed(gen: Generator, group=None):
     """Drive one rank's pipeline over torch.distributed (NCCL on GPUs, gloo on CPU)."""
     import torch.distributed as dist
 
-    def _all_gather(t: torch.Tensor) -> torch.Tensor:
+    def _start(t: torch.Tensor) -> _Pending:
         world = dist.get_world_size(group)
+        t = t.contiguous()
         if t.is_cuda:
             out = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-            dist.all_gather_into_tensor(out, t.contiguous(), group=group)
-            return out
+            return _Pending(dist.all_gather_into_tensor(out, t, group=group, async_op=True), out)
         parts = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(parts, t.contiguous(), group=group)
-        return torch.cat(parts, 0)
+        return _Pending(dist.all_gather(parts, t, group=group, async_op=True), None, parts)
 
-    gather = gather or _all_gather
     msg = next(gen)
     while True:
+        kind, payload = msg
+        if kind == "gather":
+            reply = _start(payload).result()
+        elif kind == "start":
+            reply = _start(payload)
+        else:
+            reply = payload.result()
         try:
-            msg = gen.send(gather(msg[1]))
+            msg = gen.send(reply)
         except StopIteration as stop:
             return stop.value
 

@@ -32,7 +32,7 @@ EXPORTS = (
     "raftgp_prof_reset", "raftgp_launch_count", "raftgp_build_csr", "raftgp_graph_info", "raftgp_graph_export",
     "raftgp_graph_local_degrees", "raftgp_graph_set_degrees", "raftgp_graph_set_order", "raftgp_graph_destroy", "raftgp_sketch",
     "raftgp_weights", "raftgp_project", "raftgp_gcn_transform", "raftgp_gcn_hop", "raftgp_gnn_embed",
-    "raftgp_embed", "raftgp_embed_multi", "raftgp_modularity", "raftgp_ncut", "raftgp_local_modularity",
+    "raftgp_embed", "raftgp_embed_multi", "raftgp_feature_transform", "raftgp_modularity", "raftgp_ncut", "raftgp_local_modularity",
 )
 
 _lib = None
@@ -77,6 +77,7 @@ _SIGS = {
     "raftgp_gnn_embed": (ctypes.c_int, [c_vp, c_i32, c_vp, c_u64, c_vp, c_vp, c_vp]),
     "raftgp_embed": (ctypes.c_int, [c_vp, ctypes.c_int, c_i32, c_vp, c_u64, c_vp, c_vp, c_vp]),
     "raftgp_embed_multi": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i32, c_vp, c_u64, c_vp, c_vp]),
+    "raftgp_feature_transform": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i32, c_i32, c_u64, c_vp]),
     "raftgp_modularity": (ctypes.c_int, [c_vp, c_vp, c_i32, P(c_dbl)]),
     "raftgp_ncut": (ctypes.c_int, [c_vp, c_vp, c_i32, P(c_dbl)]),
     "raftgp_local_modularity": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_i32, P(c_dbl)]),
@@ -348,6 +349,16 @@ def raftgp_embed_multi(g: Graph, variants: Sequence, dims: Sequence[int], seed: 
                                           _zk_array([Y[nm] for nm in names]) if want_Y else None,
                                           _zk_array([Z[nm] for nm in names])))
     return Y, Z
+
+
+def raftgp_feature_transform(g: Graph, variants: Sequence, r: int, l1: int, seed: int) -> dict:
+    """{variant: T1 = s^ (.) (X Theta W^(1))} for the graph's local rows."""
+    vs = [_variant(v) for v in variants]
+    names = [v if isinstance(v, str) else {0: "ncut", 1: "mod", 2: "mod_reduced"}[int(v)] for v in variants]
+    T = {nm: torch.empty((g.rows, l1), dtype=torch.float32, device=g.ctx.device) for nm in names}
+    va = (c_i32 * len(vs))(*vs)
+    _ck(load_library().raftgp_feature_transform(g.h, len(vs), va, r, l1, seed, _zk_array([T[nm] for nm in names])))
+    return T
 
 
 # ------------------------------------------------------------------ scoring (host)

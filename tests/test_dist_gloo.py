@@ -55,6 +55,10 @@ class NumpyEngine:
     def weights(self, seed, k, a, b):
         return torch.from_numpy(oracle.weights(k, a, b, seed).astype(np.float64))
 
+    def feature_transform(self, h, variants, dims, seed):
+        W1 = self.weights(seed, 1, dims[0], dims[1])
+        return {v: self.transform(h, self.project(h, v, dims[0], seed), W1) for v in variants}
+
     def transform(self, h, Z, W):
         sh = h["sh"][h["rb"]:h["re"], None]
         return torch.from_numpy(sh * (Z.numpy() @ W.numpy()))
@@ -123,11 +127,16 @@ def test_gloo_row_partitioned_pipeline_matches_oracle(world):
         np.testing.assert_allclose(Zd[v], Zo, atol=1e-10)
 
 
-def test_loopback_equals_single_rank_numpy():
+@pytest.mark.parametrize("variants", ["mod_reduced", ["ncut", "mod"], ["mod", "mod_reduced", "ncut"]])
+def test_loopback_equals_single_rank_numpy(variants):
     gr = synth.generate("C1", 4, n=120)
-    dims = (8, 8, 4)
+    dims = (8, 8, 6, 4)
     src, dst = torch.from_numpy(gr.src), torch.from_numpy(gr.dst)
-    one = rdist.run_loopback([rdist.rank_pipeline(NumpyEngine(), gr.n, src, dst, 0, 1, "mod_reduced", dims, 3)])[0]
-    three = rdist.run_loopback([rdist.rank_pipeline(NumpyEngine(), gr.n, src, dst, p, 3, "mod_reduced", dims, 3)
+    one = rdist.run_loopback([rdist.rank_pipeline(NumpyEngine(), gr.n, src, dst, 0, 1, variants, dims, 3)])[0]
+    three = rdist.run_loopback([rdist.rank_pipeline(NumpyEngine(), gr.n, src, dst, p, 3, variants, dims, 3)
                                 for p in range(3)])
-    np.testing.assert_allclose(torch.cat(three, 0).numpy(), one.numpy(), atol=1e-12)
+    if isinstance(variants, str):
+        np.testing.assert_allclose(torch.cat(three, 0).numpy(), one.numpy(), atol=1e-12)
+    else:
+        for v in variants:
+            np.testing.assert_allclose(torch.cat([t[v] for t in three], 0).numpy(), one[v].numpy(), atol=1e-12)

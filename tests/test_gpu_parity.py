@@ -217,17 +217,22 @@ def test_fused_equals_unfused_and_deterministic(rg, ctx):
 
 # ------------------------------------------------------------------ row partition on one GPU ("loopback")
 @pytest.mark.parametrize("P", [2, 3])
-@pytest.mark.parametrize("variant", ["ncut", "mod"])
-def test_partitioned_equals_whole(rg, ctx, P, variant):
-    """Rank shards (1-D row partition, all-gather emulated by concatenation) reproduce the whole-graph
-    result bit for bit: each row's arithmetic does not depend on the partition."""
+@pytest.mark.parametrize("variants", [["ncut", "mod"], ["mod_reduced"], ["mod", "ncut", "mod_reduced"]])
+def test_partitioned_equals_whole(rg, ctx, P, variants):
+    """Rank shards (1-D row partition; all-gathers emulated by concatenation, including the pipelined
+    start/wait protocol) reproduce the whole-graph result bit for bit: each row's arithmetic does not
+    depend on the partition. Reference: raftgp_embed_multi on the whole graph."""
     from paper_2312_01560_b200 import dist
     n, src, dst, ref = graph_case("c1_s3")
     dims = (64, 64, 32)
-    whole = rg.raftgp_build_csr(ctx, n, _t(src), _t(dst))
-    Yw, Zw = rg.raftgp_embed(whole, variant, dims, 4)
-    Zs = dist.loopback_embed(ctx, n, _t(src), _t(dst), P, variant, dims, 4)
-    assert torch.equal(torch.cat(Zs, 0), Zw)
+    eng = dist.CudaEngine(ctx)
+    gens = [dist.rank_pipeline(eng, n, _t(src), _t(dst), p, P, variants, dims, 4) for p in range(P)]
+    Zs = dist.run_loopback(gens)
+    one = dist.run_loopback([dist.rank_pipeline(eng, n, _t(src), _t(dst), 0, 1, variants, dims, 4)])[0]
+    for v in variants:
+        assert torch.equal(torch.cat([z[v] for z in Zs], 0), one[v]), v
+        Zo = oracle.gcn(ref, dims, 4, oracle.project(ref, v, dims[0], 4))[-1]
+        assert rel_fro(one[v].cpu().numpy(), Zo) <= TOL
 
 
 # ------------------------------------------------------------------ a7: scoring
