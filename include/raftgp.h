@@ -130,6 +130,12 @@ RAFTGP_API raftgp_status raftgp_graph_destroy(raftgp_graph g);
 RAFTGP_API raftgp_status raftgp_sketch(raftgp_ctx ctx, uint64_t seed, uint32_t tag, int64_t row_begin, int64_t rows,
                             int32_t cols, int32_t den, float *out_dev);
 
+/* Theta' = Theta W for the global rows 0..rows-1: Theta (tag 0, den r) is generated on chip and multiplied
+ * by W (device, r x l1 row-major) on the tcgen05 tensor cores with a 3xTF32 split (fp32-accurate); only
+ * Theta' (rows x l1, device) is written. r, l1 in {32, 64, 128}; 16-byte aligned buffers. */
+RAFTGP_API raftgp_status raftgp_sketch_transform(raftgp_ctx ctx, uint64_t seed, int64_t rows, int32_t r,
+                                                 const float *W_dev, int32_t l1, float *out_dev);
+
 /* W^(k) of Eq. 6, untrained: fan_in x fan_out, tag k, den fan_in. */
 RAFTGP_API raftgp_status raftgp_weights(raftgp_ctx ctx, uint64_t seed, int32_t k, int32_t fan_in, int32_t fan_out,
                              float *W_dev);

@@ -366,6 +366,16 @@ raftgp_status raftgp_weights(raftgp_ctx ctx, uint64_t seed, int32_t k, int32_t f
     return raftgp_sketch(ctx, seed, static_cast<uint32_t>(k), 0, fan_in, fan_out, fan_in, W_dev);
 }
 
+raftgp_status raftgp_sketch_transform(raftgp_ctx ctx, uint64_t seed, int64_t rows, int32_t r, const float *W_dev,
+                                      int32_t l1, float *out_dev) {
+    if (!ctx) return fail(RAFTGP_ERR_PARAM, "null ctx");
+    if (rows < 0 || !sketch_w_supported(r, l1)) return fail(RAFTGP_ERR_PARAM, "r and l1 must be 32, 64 or 128");
+    if (rows > 0 && (!W_dev || !out_dev || !aligned16(W_dev) || !aligned16(out_dev)))
+        return fail(RAFTGP_ERR_PARAM, "null or unaligned buffer");
+    RG_TRY(set_device(ctx));
+    return sketch_w_any(ctx, seed, rows, r, W_dev, l1, out_dev);
+}
+
 // ---------------------------------------------------------------- project / gcn
 static raftgp_status check_variant(raftgp_graph g, int variant, int32_t r) {
     if (variant < 0 || variant > 2) return fail(RAFTGP_ERR_PARAM, "bad variant");

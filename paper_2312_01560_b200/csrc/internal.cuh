@@ -146,6 +146,9 @@ raftgp_status sketch_theta(raftgp_graph g, uint64_t seed, int32_t r, float *thet
 raftgp_status g_reduce(raftgp_graph g, const float *X, int32_t r, double *g_out);
 // Theta' = Theta W1 (Theta generated on chip, n x l1 written) and optionally g' = d^T Theta'
 bool sketch_w_supported(int32_t r, int32_t l1);
+// Theta' = Theta W1 on tcgen05 tensor cores (3xTF32, fp32-accurate), Theta generated on chip
+raftgp_status sketch_w_tc(raftgp_ctx ctx, uint64_t seed, int64_t n, int32_t r, const float *W1, int32_t l1, float *out);
+raftgp_status sketch_w_any(raftgp_ctx ctx, uint64_t seed, int64_t n, int32_t r, const float *W1, int32_t l1, float *out);
 raftgp_status sketch_theta_w(raftgp_graph g, uint64_t seed, int32_t r, const float *W1, int32_t l1, float *out,
                              double *g_out);
 

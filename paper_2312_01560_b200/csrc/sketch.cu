@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "gauss.cuh"
 #include "internal.cuh"
@@ -179,17 +180,25 @@ bool sketch_w_supported(int32_t r, int32_t l1) {
     return (r == 32 || r == 64 || r == 128) && (l1 == 32 || l1 == 64 || l1 == 128);
 }
 
+// tcgen05 path by default (RAFTGP_TC=0 selects the FFMA kernel)
+raftgp_status sketch_w_any(raftgp_ctx ctx, uint64_t seed, int64_t n, int32_t r, const float *W1, int32_t l1, float *out) {
+    static const bool use_tc = [] {
+        const char *e = getenv("RAFTGP_TC");
+        return !(e && e[0] == '0');
+    }();
+    if (n == 0) return RAFTGP_OK;
+    if (use_tc) return sketch_w_tc(ctx, seed, n, r, W1, l1, out);
+    const float sigma = spec_sigma(r);
+    switch (r) {
+        case 32: return dispatch_sketch_w<32>(ctx, seed, n, sigma, W1, l1, out);
+        case 64: return dispatch_sketch_w<64>(ctx, seed, n, sigma, W1, l1, out);
+        default: return dispatch_sketch_w<128>(ctx, seed, n, sigma, W1, l1, out);
+    }
+}
+
 raftgp_status sketch_theta_w(raftgp_graph g, uint64_t seed, int32_t r, const float *W1, int32_t l1, float *out,
                              double *g_out) {
-    raftgp_ctx ctx = g->ctx;
-    const float sigma = spec_sigma(r);
-    if (g->n > 0) {
-        switch (r) {
-            case 32: RG_TRY(dispatch_sketch_w<32>(ctx, seed, g->n, sigma, W1, l1, out)); break;
-            case 64: RG_TRY(dispatch_sketch_w<64>(ctx, seed, g->n, sigma, W1, l1, out)); break;
-            default: RG_TRY(dispatch_sketch_w<128>(ctx, seed, g->n, sigma, W1, l1, out)); break;
-        }
-    }
+    RG_TRY(sketch_w_any(g->ctx, seed, g->n, r, W1, l1, out));
     return g_reduce(g, out, l1, g_out);
 }
 

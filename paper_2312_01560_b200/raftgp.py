@@ -29,7 +29,7 @@ RAFTGP_HOST_PTRS, RAFTGP_DEVICE_PTRS = 0, 1
 EXPORTS = (
     "raftgp_last_error", "raftgp_version", "raftgp_ctx_create", "raftgp_ctx_destroy", "raftgp_ctx_sync",
     "raftgp_ctx_stream", "raftgp_ctx_set_profiling", "raftgp_prof_kernels", "raftgp_prof_name", "raftgp_prof_read",
-    "raftgp_prof_reset", "raftgp_launch_count", "raftgp_build_csr", "raftgp_graph_info", "raftgp_graph_export",
+    "raftgp_prof_reset", "raftgp_launch_count", "raftgp_sketch_transform", "raftgp_build_csr", "raftgp_graph_info", "raftgp_graph_export",
     "raftgp_graph_local_degrees", "raftgp_graph_set_degrees", "raftgp_graph_set_order", "raftgp_graph_destroy", "raftgp_sketch",
     "raftgp_weights", "raftgp_project", "raftgp_gcn_transform", "raftgp_gcn_hop", "raftgp_gnn_embed",
     "raftgp_embed", "raftgp_embed_multi", "raftgp_feature_transform", "raftgp_modularity", "raftgp_ncut", "raftgp_local_modularity",
@@ -71,6 +71,7 @@ _SIGS = {
     "raftgp_graph_destroy": (ctypes.c_int, [c_vp]),
     "raftgp_sketch": (ctypes.c_int, [c_vp, c_u64, c_u32, c_i64, c_i64, c_i32, c_i32, c_vp]),
     "raftgp_weights": (ctypes.c_int, [c_vp, c_u64, c_i32, c_i32, c_i32, c_vp]),
+    "raftgp_sketch_transform": (ctypes.c_int, [c_vp, c_u64, c_i64, c_i32, c_vp, c_i32, c_vp]),
     "raftgp_project": (ctypes.c_int, [c_vp, ctypes.c_int, c_i32, c_u64, c_vp]),
     "raftgp_gcn_transform": (ctypes.c_int, [c_vp, c_vp, c_i32, c_vp, c_i32, c_vp]),
     "raftgp_gcn_hop": (ctypes.c_int, [c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp]),
@@ -262,6 +263,14 @@ def raftgp_weights(ctx: Context, seed: int, k: int, fan_in: int, fan_out: int,
     if out is None:
         out = torch.empty((fan_in, fan_out), dtype=torch.float32, device=ctx.device)
     _ck(load_library().raftgp_weights(ctx.h, seed, k, fan_in, fan_out, _ptr(out)))
+    return out
+
+
+def raftgp_sketch_transform(ctx: Context, seed: int, rows: int, W: torch.Tensor) -> torch.Tensor:
+    """Theta' = Theta W (Theta generated on chip, tcgen05 3xTF32 GEMM)."""
+    r, l1 = W.shape
+    out = torch.empty((rows, l1), dtype=torch.float32, device=ctx.device)
+    _ck(load_library().raftgp_sketch_transform(ctx.h, seed, rows, r, _ptr(W.contiguous()), l1, _ptr(out)))
     return out
 
 

@@ -319,3 +319,14 @@ def test_embed_multi_pre_transformed_parity(rg, ctx, name, dims):
         assert rel_fro(Z[v].cpu().numpy(), Zo) <= TOL, v
     _, Z2 = rg.raftgp_embed_multi(g, ["mod", "ncut"], dims, 13)     # deterministic, order-independent
     assert torch.equal(Z2["mod"], Z["mod"]) and torch.equal(Z2["ncut"], Z["ncut"])
+
+
+@pytest.mark.parametrize("n,r,l1", [(300, 128, 128), (777, 128, 64), (130, 32, 32), (5000, 64, 128), (1001, 64, 32)])
+def test_sketch_transform_tcgen05(rg, ctx, n, r, l1):
+    """Theta' = Theta W on the tcgen05 tensor cores (3xTF32 split) against the oracle's generator and an
+    fp64 product: ~1e-6 relative, i.e. fp32-accurate (the 1e-4 parity bar is not consumed here)."""
+    W = oracle.weights(1, r, l1, 5)
+    got = rg.raftgp_sketch_transform(ctx, 9, n, _t(W)).cpu().numpy().astype(np.float64)
+    ref = oracle.theta(n, r, 9).astype(np.float64) @ W.astype(np.float64)
+    assert rel_fro(got, ref) < 5e-6
+    assert np.max(np.abs(got - ref)) < 1e-5 * max(1.0, np.abs(ref).max())
