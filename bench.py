@@ -366,15 +366,15 @@ def main():
                 "bytes_per_launch": hop_stats[dom]["bytes_per_launch"]}
 
     # ---------------- e2e through the C-ABI with host buffers (H2D of edges, D2H of Z inside the timed region)
-    # N = 1: two contexts on two streams, steps alternate between them, so step k's copies overlap step
-    # k+1's kernels (double buffering with the public API); every step still copies its own edges in and
+    # N = 1: three contexts on three streams, steps rotate over them, so a step's copies overlap other
+    # steps' kernels (multi-buffering with the public API); every step still copies its own edges in and
     # its own Z out. N > 1: one stream, sequential.
     e2e = None
     if not args.no_e2e:
         d2h = int(sum(rows * dims[-1] * 4 for _ in variants))
         if world == 1 and not args.no_fuse_variants:
             lanes = []
-            for _ in range(2):
+            for _ in range(3):
                 s_ = torch.cuda.Stream(dev)
                 cs_ = torch.cuda.Stream(dev)          # D2H of this lane's Z, off the compute stream
                 c_ = rg.Context(dev.index, stream=s_)
@@ -383,12 +383,12 @@ def main():
                 lanes.append((s_, c_, Zl, Hl, cs_))
 
             def e2e_step(i):
-                s_, c_, Zl, Hl, cs_ = lanes[i % 2]
+                s_, c_, Zl, Hl, cs_ = lanes[i % len(lanes)]
                 with torch.cuda.stream(s_):
-                    s_.wait_stream(cs_)                # Zl is free again once its previous D2H is done
                     sd = src_h.to(dev, non_blocking=True)
                     dd = dst_h.to(dev, non_blocking=True)
                     g = rg.raftgp_build_csr(c_, gr.n, sd, dd)
+                    s_.wait_stream(cs_)                # Zl is free again once its previous D2H is done
                     rg.raftgp_embed_multi(g, variants, dims, args.seed, Z=Zl)
                     g.close()
                 cs_.wait_stream(s_)
@@ -396,13 +396,14 @@ def main():
                     for v in variants:
                         Hl[v].copy_(Zl[v], non_blocking=True)
 
-            for i in range(2):
+            for i in range(len(lanes)):
                 e2e_step(i)
             torch.cuda.synchronize()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(lanes[0][0])
-            lanes[1][0].wait_event(e0)
+            for s_, _, _, _, _ in lanes[1:]:
+                s_.wait_event(e0)
             for i in range(args.steps):
                 e2e_step(i)
             for s_, _, _, _, cs_ in lanes:
@@ -410,7 +411,7 @@ def main():
                 lanes[0][0].wait_stream(cs_)
             e1.record(lanes[0][0])
             torch.cuda.synchronize()
-            mode = "pipelined: 2 contexts/streams, step k's H2D/D2H overlap step k+1's kernels"
+            mode = "pipelined: 3 contexts/streams (+ a D2H stream each); step k's copies overlap other steps' kernels"
         else:
             out_host = {v: torch.empty((rows, dims[-1]), dtype=torch.float32).pin_memory() for v in variants}
             step(src_h, dst_h, out_host)
