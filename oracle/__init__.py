@@ -39,7 +39,8 @@ def _L():
         build()
         _lib = ctypes.CDLL(_SO)
         for name in ("oracle_gaussian", "oracle_build_csr", "oracle_apply", "oracle_project", "oracle_gcn",
-                     "oracle_embed_rows", "oracle_modularity", "oracle_ncut", "oracle_local_modularity"):
+                     "oracle_embed_rows", "oracle_modularity", "oracle_ncut", "oracle_local_modularity",
+                     "oracle_kmeans2", "oracle_model_select", "oracle_split_stops"):
             getattr(_lib, name).restype = ctypes.c_int
     return _lib
 
@@ -207,3 +208,39 @@ def local_modularity(g: CSR, nodes, block_of_node, k: int) -> float:
     _check(_L().oracle_local_modularity(ctypes.c_int64(g.n), _p(g.row_ptr), _p(g.col), _p(nd), ctypes.c_int64(nd.size),
                                         _p(b), ctypes.c_int32(k), ctypes.byref(out)))
     return out.value
+
+
+# ------------------------------------------------------------------ Alg. 1 model selection (NEXT-1)
+def kmeans2(Z: np.ndarray, members, max_iter: int = 100):
+    """SELECT_SPEC §3: deterministic 2-means on the rows Z[members]. Returns (side uint8[len], iterations)."""
+    Z = np.ascontiguousarray(Z, np.float32)
+    U = np.ascontiguousarray(members, np.int32)
+    side = np.zeros(max(1, U.size), np.uint8)
+    it = _L().oracle_kmeans2(_p(Z), ctypes.c_int32(Z.shape[1]), _p(U), ctypes.c_int64(U.size),
+                             ctypes.c_int32(max_iter), _p(side))
+    return side[: U.size], int(it)
+
+
+def model_select(g: CSR, Z: np.ndarray, eps: int = 5, max_iter: int = 100, rule=0):
+    """Alg. 1 from U = V on the fp32 embedding Z. Returns (labels int32[n], K, stats)
+    with canonical labels (SELECT_SPEC §5) and stats = dict(blocks, splits, kmeans_iters, depth).
+    rule: 0 = "global" e = |E| (SELECT_SPEC §4 default), 1 = "local" 2e = degree sum of U."""
+    rule = {"global": 0, "local": 1}.get(rule, rule)
+    Z = np.ascontiguousarray(Z, np.float32)
+    labels = np.zeros(max(1, g.n), np.int32)
+    k = ctypes.c_int32(0)
+    st = np.zeros(4, np.int64)
+    _check(_L().oracle_model_select(ctypes.c_int64(g.n), _p(g.row_ptr), _p(g.col), _p(Z), ctypes.c_int32(Z.shape[1]),
+                                    ctypes.c_int32(eps), ctypes.c_int32(max_iter), ctypes.c_int32(rule), _p(labels), ctypes.byref(k), _p(st)))
+    return labels[: g.n], int(k.value), dict(zip(("blocks", "splits", "kmeans_iters", "depth"), (int(x) for x in st)))
+
+
+def split_stops(g: CSR, members, side, eps: int = 5, rule=0) -> bool:
+    """Alg. 1 lines 2+4 (SELECT_SPEC §4): True iff U = members, split by `side`, becomes a block."""
+    rule = {"global": 0, "local": 1}.get(rule, rule)
+    U = np.ascontiguousarray(members, np.int32)
+    sd = np.ascontiguousarray(side, np.uint8)
+    where = np.zeros(g.n + 1, np.int32)
+    return bool(_L().oracle_split_stops(_p(g.row_ptr), _p(g.col), ctypes.c_int64(int(g.row_ptr[-1])), _p(U),
+                                        ctypes.c_int64(U.size), _p(sd), ctypes.c_int32(eps), ctypes.c_int32(rule),
+                                        _p(where)))

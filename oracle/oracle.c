@@ -23,6 +23,8 @@
  *   oracle_modularity      Eq. 3
  *   oracle_ncut            Eq. 1
  *   oracle_local_modularity Eq. 7
+ *   oracle_kmeans2,
+ *   oracle_model_select    Alg. 1 with the 2-means of docs/SELECT_SPEC.md (NEXT-1)
  *
  * Status codes: 0 ok, 2 parameter error, 3 data error (same numbering as include/raftgp.h, which
  * is NOT included here).
@@ -485,4 +487,185 @@ int oracle_local_modularity(int64_t n, const int64_t *row_ptr, const int32_t *co
     free(m2);
     free(mbar);
     return rc;
+}
+
+/* ---------------------------------------------------------------- Alg. 1: hierarchical model selection
+ * (§III-C) with the deterministic 2-means of docs/SELECT_SPEC.md. Plain recursion in the
+ * paper's (depth-first) order; every step cites the spec section it follows. */
+
+/* SELECT_SPEC §2: q(z) = round_half_even(double(z) * 2^32) */
+static int64_t sel_fixq(float z) { return (int64_t)llrint((double)z * 4294967296.0); }
+
+/* SELECT_SPEC §2: centroid of the members U[t] with (side == NULL or side[t] == want); returns the count */
+static int64_t sel_centroid(const float *Z, int32_t L, const int32_t *U, int64_t cnt, const uint8_t *side, int want,
+                            double *mu) {
+    int64_t *S = (int64_t *)calloc((size_t)L, sizeof(int64_t));
+    int64_t c = 0;
+    for (int64_t t = 0; t < cnt; ++t) {
+        if (side && side[t] != want) continue;
+        const float *z = Z + (int64_t)U[t] * L;
+        for (int32_t l = 0; l < L; ++l) S[l] += sel_fixq(z[l]);
+        c++;
+    }
+    if (c > 0)
+        for (int32_t l = 0; l < L; ++l) mu[l] = ((double)S[l] * 0x1p-32) / (double)c;
+    free(S);
+    return c;
+}
+
+/* SELECT_SPEC §2: d = sum_l (double(x_l) - mu_l)^2, sequential in l, no contraction (-ffp-contract=off) */
+static double sel_sqdist(const float *x, const double *mu, int32_t L) {
+    double d = 0.0;
+    for (int32_t l = 0; l < L; ++l) {
+        double t = (double)x[l] - mu[l];
+        d = d + t * t;
+    }
+    return d;
+}
+
+/* SELECT_SPEC §3.1: the member farthest from ref (ties: smallest node id) */
+static int32_t sel_farthest(const float *Z, int32_t L, const int32_t *U, int64_t cnt, const double *ref) {
+    int32_t best = -1;
+    double bd = -1.0;
+    for (int64_t t = 0; t < cnt; ++t) {
+        double d = sel_sqdist(Z + (int64_t)U[t] * L, ref, L);
+        if (d > bd || (d == bd && U[t] < best)) { bd = d; best = U[t]; }
+    }
+    return best;
+}
+
+/* SELECT_SPEC §3: KMeans with K = 2 on U (Alg. 1 line 3). side[t] in {0,1} for member U[t]; returns the
+ * number of Lloyd iterations t. */
+int32_t oracle_kmeans2(const float *Z, int32_t L, const int32_t *U, int64_t cnt, int32_t max_iter, uint8_t *side) {
+    double *mu0 = (double *)malloc(sizeof(double) * (size_t)L), *mu1 = (double *)malloc(sizeof(double) * (size_t)L);
+    double *mbar = (double *)malloc(sizeof(double) * (size_t)L);
+    uint8_t *prev = (uint8_t *)malloc((size_t)cnt + 1);
+    int32_t it = 0;
+    if (cnt > 0) {
+        /* §3.1 seeding */
+        sel_centroid(Z, L, U, cnt, NULL, 0, mbar);
+        int32_t a = sel_farthest(Z, L, U, cnt, mbar);
+        for (int32_t l = 0; l < L; ++l) mu0[l] = (double)Z[(int64_t)a * L + l];
+        int32_t b = sel_farthest(Z, L, U, cnt, mu0);
+        for (int32_t l = 0; l < L; ++l) mu1[l] = (double)Z[(int64_t)b * L + l];
+        /* §3.2 Lloyd */
+        for (int32_t t = 1; t <= max_iter; ++t) {
+            it = t;
+            int changed = 0;
+            for (int64_t s = 0; s < cnt; ++s) {
+                const float *z = Z + (int64_t)U[s] * L;
+                uint8_t c = sel_sqdist(z, mu1, L) < sel_sqdist(z, mu0, L) ? 1 : 0;
+                if (t > 1 && c != prev[s]) changed = 1;
+                side[s] = c;
+            }
+            if (t > 1 && !changed) break;
+            sel_centroid(Z, L, U, cnt, side, 0, mu0);   /* an empty side keeps its centre */
+            sel_centroid(Z, L, U, cnt, side, 1, mu1);
+            memcpy(prev, side, (size_t)cnt);
+        }
+    }
+    free(mu0);
+    free(mu1);
+    free(mbar);
+    free(prev);
+    return it;
+}
+
+/* Alg. 1 lines 2 and 4 via SELECT_SPEC §4: returns 1 iff U (members U[t], KMeans sides side[t]) becomes a
+ * block. two_E = 2|E| (degree sum of G); rule 0 = global 2e = two_E, 1 = local 2e = T.
+ * where: scratch int32[n], all zero on entry and on return. */
+int oracle_split_stops(const int64_t *row_ptr, const int32_t *col, int64_t two_E, const int32_t *U, int64_t cnt,
+                       const uint8_t *side, int32_t eps, int32_t rule, int32_t *where) {
+    int64_t n1 = 0, n2 = 0, mb1 = 0, mb2 = 0, cut = 0;
+    for (int64_t t = 0; t < cnt; ++t) where[U[t]] = side[t] ? 2 : 1;
+    for (int64_t t = 0; t < cnt; ++t) {
+        int32_t i = U[t];
+        int64_t d = row_ptr[i + 1] - row_ptr[i];
+        if (side[t]) { n2++; mb2 += d; }
+        else {
+            n1++;
+            mb1 += d;
+            for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p)
+                if (where[col[p]] == 2) cut++;   /* each U_1-U_2 edge is seen once, from its U_1 end */
+        }
+    }
+    for (int64_t t = 0; t < cnt; ++t) where[U[t]] = 0;
+    int64_t T = mb1 + mb2;
+    __int128 two_e = rule == 1 ? (__int128)T : (__int128)two_E;
+    /* m_1 > m_2  <=>  2e * c > mbar_1 * mbar_2 */
+    return n1 <= eps || n2 <= eps || T == 0 || two_e * (__int128)cut > (__int128)mb1 * (__int128)mb2;
+}
+
+typedef struct {
+    const int64_t *row_ptr;
+    const int32_t *col;
+    const float *Z;
+    int32_t L, eps, max_iter, rule;   /* rule: 0 = global e (reading #28), 1 = local e (PAPER.md:167 literal) */
+    int64_t two_E;       /* global degree sum 2|E| */
+    int32_t *block_of;   /* discovery-order block id per node */
+    int32_t nblocks;
+    int32_t *where;      /* scratch: 1 = in U_1, 2 = in U_2, 0 = elsewhere */
+    int64_t splits, kmeans_iters;
+    int32_t depth;
+} sel_state;
+
+/* PARTITION(U, G) of Alg. 1 on the members U[0..cnt) (reordered in place: U_1 first, then U_2). */
+static void sel_partition(sel_state *st, int32_t *U, int64_t cnt, int32_t depth) {
+    if (depth + 1 > st->depth) st->depth = depth + 1;
+    uint8_t *side = (uint8_t *)malloc((size_t)cnt + 1);
+    st->kmeans_iters += oracle_kmeans2(st->Z, st->L, U, cnt, st->max_iter, side);      /* line 3 */
+    /* lines 2 and 4 (m_1, m_2 and their comparison, SELECT_SPEC §4) */
+    int stop = oracle_split_stops(st->row_ptr, st->col, st->two_E, U, cnt, side, st->eps, st->rule, st->where);
+    int64_t n1 = 0, n2 = 0;
+    for (int64_t t = 0; t < cnt; ++t) { if (side[t]) n2++; else n1++; }
+    if (stop) {                                                                           /* line 5 */
+        for (int64_t t = 0; t < cnt; ++t) st->block_of[U[t]] = st->nblocks;
+        st->nblocks++;
+        free(side);
+        return;
+    }
+    st->splits++;
+    int32_t *tmp = (int32_t *)malloc(sizeof(int32_t) * (size_t)cnt);
+    int64_t a = 0, b = n1;
+    for (int64_t t = 0; t < cnt; ++t) tmp[side[t] ? b++ : a++] = U[t];
+    memcpy(U, tmp, sizeof(int32_t) * (size_t)cnt);
+    free(tmp);
+    free(side);
+    sel_partition(st, U, n1, depth + 1);                                                  /* line 7 */
+    sel_partition(st, U + n1, n2, depth + 1);                                             /* line 8 */
+}
+
+/* Alg. 1 from U = V. labels[i] = canonical block label (SELECT_SPEC §5: blocks numbered by smallest member);
+ * rule: 0 = e = |E| of G (SELECT_SPEC §4 default), 1 = 2e = total degree of U (PAPER.md:167 literal).
+ * stats (optional, int64[4]): blocks, splits, total Lloyd iterations, tree depth.
+ * Errors: 2 (L <= 0, eps < 0, max_iter < 1, rule not 0/1), 3 (|z| > 1). */
+int oracle_model_select(int64_t n, const int64_t *row_ptr, const int32_t *col, const float *Z, int32_t L,
+                        int32_t eps, int32_t max_iter, int32_t rule, int32_t *labels, int32_t *num_blocks,
+                        int64_t *stats) {
+    if (L <= 0 || eps < 0 || max_iter < 1 || n < 0 || rule < 0 || rule > 1) return 2;
+    for (int64_t i = 0; i < n * (int64_t)L; ++i)
+        if (!(Z[i] >= -1.0f && Z[i] <= 1.0f)) return 3;
+    sel_state st;
+    memset(&st, 0, sizeof st);
+    st.row_ptr = row_ptr; st.col = col; st.Z = Z; st.L = L; st.eps = eps; st.max_iter = max_iter; st.rule = rule; st.two_E = row_ptr[n];
+    st.block_of = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n + 1));
+    st.where = (int32_t *)calloc((size_t)(n + 1), sizeof(int32_t));
+    int32_t *U = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n + 1));
+    for (int64_t i = 0; i < n; ++i) U[i] = (int32_t)i;
+    if (n > 0) sel_partition(&st, U, n, 0);
+    /* canonical labels: first appearance in increasing node id */
+    int32_t *canon = (int32_t *)malloc(sizeof(int32_t) * (size_t)(st.nblocks + 1));
+    for (int32_t b = 0; b < st.nblocks; ++b) canon[b] = -1;
+    int32_t next = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (canon[st.block_of[i]] < 0) canon[st.block_of[i]] = next++;
+        labels[i] = canon[st.block_of[i]];
+    }
+    *num_blocks = st.nblocks;
+    if (stats) { stats[0] = st.nblocks; stats[1] = st.splits; stats[2] = st.kmeans_iters; stats[3] = st.depth; }
+    free(canon);
+    free(U);
+    free(st.where);
+    free(st.block_of);
+    return 0;
 }
