@@ -209,6 +209,27 @@ RAFTGP_API raftgp_status raftgp_ncut(raftgp_graph g, const int32_t *assign, int3
 RAFTGP_API raftgp_status raftgp_local_modularity(raftgp_graph g, const int64_t *nodes, int64_t count,
                                       const int32_t *block_of_node, int32_t k, double *out);
 
+/* ---------------------------------------------------------------- NEXT-1: hierarchical model selection
+ * Alg. 1 (§III-C) from U = V on the embedding Z, with KMeans(K = 2) and the split test of
+ * docs/SELECT_SPEC.md (deterministic farthest-first seeding, Lloyd iterations with exact fixed-point centroid
+ * sums, exact integer form of "m_1 > m_2" for the local modularity of Eq. 7). The tree is processed level by
+ * level on the GPU; the partition equals the depth-first recursion's.
+ *   Z_dev: device fp32 n x L, row-major, 16-byte aligned, every |z| <= 1 (rows of the l2-normalised
+ *          embedding). L in {8, 16, 32, 64, 128}.
+ *   eps: the size threshold epsilon (PAPER.md:200 uses 5), >= 0. max_iter: Lloyd cap (>= 1; 100 suggested).
+ *   rule: RAFTGP_LMOD_GLOBAL (2e = 2|E|: m_1 > m_2 iff splitting U lowers the modularity of G, PAPER.md:203;
+ *         DESIGN.md reading #28) or RAFTGP_LMOD_LOCAL (2e = total degree of U, PAPER.md:167 as printed).
+ *   labels_dev: device int32[n] out: block of every node, blocks numbered 0..K-1 by their smallest member.
+ *   num_blocks: host out, K.  stats: host int64[4] out or NULL: {blocks, splits, Lloyd iterations summed
+ *          over levels (lock-step), levels}.
+ * Whole-graph handle only. Synchronous (the host drives the levels). Workspace from the context pool.
+ * Errors: PARAM (L, eps, max_iter, rule, null/misaligned pointers, partial graph), DATA (|z| > 1 or NaN),
+ * STATE, NOMEM, CUDA. */
+typedef enum { RAFTGP_LMOD_GLOBAL = 0, RAFTGP_LMOD_LOCAL = 1 } raftgp_lmod_rule;
+RAFTGP_API raftgp_status raftgp_model_select(raftgp_graph g, const float *Z_dev, int32_t L, int32_t eps,
+                                             int32_t max_iter, int32_t rule, int32_t *labels_dev, int32_t *num_blocks,
+                                             int64_t *stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,7 +18,7 @@ namespace raftgp {
 
 const char *const kKernelNames[K_NUM] = {
     "csr_count", "scan", "csr_scatter", "csr_sort_warp", "csr_sort_block", "csr_compact", "degree_scalars",
-    "sketch", "g_partials", "g_final", "feature_hop", "transform", "gcn_hop", "hop_generic", "misc", "csr_partition", "csr_bucket_sort", "row_order"};
+    "sketch", "g_partials", "g_final", "feature_hop", "transform", "gcn_hop", "hop_generic", "misc", "csr_partition", "csr_bucket_sort", "row_order", "model_select"};
 
 static thread_local std::string g_last_error;
 
@@ -794,6 +794,27 @@ raftgp_status raftgp_local_modularity(raftgp_graph g, const int64_t *nodes, int6
     }
     *out = q;
     return RAFTGP_OK;
+    RG_GUARD_END
+}
+
+// ---------------------------------------------------------------- NEXT-1: Alg. 1 model selection
+raftgp_status raftgp_model_select(raftgp_graph g, const float *Z_dev, int32_t L, int32_t eps, int32_t max_iter,
+                                  int32_t rule, int32_t *labels_dev, int32_t *num_blocks, int64_t *stats) {
+    RG_GUARD_BEGIN
+    RG_TRY(need_ready(g));
+    RG_TRY(whole_graph(g));
+    if (!num_blocks) return fail(RAFTGP_ERR_PARAM, "null num_blocks");
+    if (eps < 0 || max_iter < 1) return fail(RAFTGP_ERR_PARAM, "eps must be >= 0 and max_iter >= 1");
+    if (rule != RAFTGP_LMOD_GLOBAL && rule != RAFTGP_LMOD_LOCAL) return fail(RAFTGP_ERR_PARAM, "bad LMod rule");
+    if (g->n > 0 && (!Z_dev || !labels_dev)) return fail(RAFTGP_ERR_PARAM, "null Z or labels");
+    if (g->n > 0 && !aligned16(Z_dev)) return fail(RAFTGP_ERR_PARAM, "Z must be 16-byte aligned");
+    RG_TRY(set_device(g->ctx));
+    if (g->n == 0) {
+        *num_blocks = 0;
+        if (stats) stats[0] = stats[1] = stats[2] = stats[3] = 0;
+        return RAFTGP_OK;
+    }
+    return model_select(g, Z_dev, L, eps, max_iter, rule, labels_dev, num_blocks, stats);
     RG_GUARD_END
 }
 

@@ -34,6 +34,7 @@ enum KernelId : int {
     K_CSR_PARTITION,
     K_CSR_BUCKET,
     K_ORDER,
+    K_SELECT,
     K_NUM
 };
 extern const char *const kKernelNames[K_NUM];
@@ -167,5 +168,8 @@ raftgp_status gcn_hop(raftgp_graph g, const float *Tfull, int32_t w, float *Zout
 // last GCN hop of two variants over the interleaved operand [T_a | T_b] (n x 2d); d in {32, 64}
 bool gcn_pair_supported(int32_t d);
 raftgp_status gcn_final_pair(raftgp_graph g, const float *Tboth, int32_t d, float *Za, float *Zb);
+// NEXT-1: Alg. 1 hierarchical model selection (select.cu)
+raftgp_status model_select(raftgp_graph g, const float *Z, int32_t L, int32_t eps, int32_t max_iter, int32_t rule,
+                           int32_t *labels, int32_t *num_blocks, int64_t *stats);
 
 }  // namespace raftgp

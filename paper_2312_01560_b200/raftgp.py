@@ -23,6 +23,8 @@ RAFTGP_OK, RAFTGP_ERR_PARAM, RAFTGP_ERR_DATA = 0, 2, 3
 RAFTGP_ERR_INTERNAL, RAFTGP_ERR_CUDA, RAFTGP_ERR_NOMEM, RAFTGP_ERR_STATE = 4, 5, 6, 7
 RAFTGP_NCUT, RAFTGP_MOD, RAFTGP_MOD_REDUCED = 0, 1, 2
 VARIANTS = {"ncut": RAFTGP_NCUT, "mod": RAFTGP_MOD, "mod_reduced": RAFTGP_MOD_REDUCED}
+RAFTGP_LMOD_GLOBAL, RAFTGP_LMOD_LOCAL = 0, 1
+LMOD_RULES = {"global": RAFTGP_LMOD_GLOBAL, "local": RAFTGP_LMOD_LOCAL}
 RAFTGP_HOST_PTRS, RAFTGP_DEVICE_PTRS = 0, 1
 
 # every symbol declared in include/raftgp.h
@@ -33,6 +35,7 @@ EXPORTS = (
     "raftgp_graph_local_degrees", "raftgp_graph_set_degrees", "raftgp_graph_set_order", "raftgp_graph_destroy", "raftgp_sketch",
     "raftgp_weights", "raftgp_project", "raftgp_gcn_transform", "raftgp_gcn_hop", "raftgp_gnn_embed",
     "raftgp_embed", "raftgp_embed_multi", "raftgp_feature_transform", "raftgp_modularity", "raftgp_ncut", "raftgp_local_modularity",
+    "raftgp_model_select",
 )
 
 _lib = None
@@ -82,6 +85,7 @@ _SIGS = {
     "raftgp_modularity": (ctypes.c_int, [c_vp, c_vp, c_i32, P(c_dbl)]),
     "raftgp_ncut": (ctypes.c_int, [c_vp, c_vp, c_i32, P(c_dbl)]),
     "raftgp_local_modularity": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_i32, P(c_dbl)]),
+    "raftgp_model_select": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, P(c_i32), c_vp]),
 }
 
 
@@ -396,3 +400,20 @@ def raftgp_local_modularity(g: Graph, nodes, block_of_node, k: int) -> float:
     _ck(load_library().raftgp_local_modularity(g.h, c_vp(nd.ctypes.data), nd.size, c_vp(b.ctypes.data), k,
                                                ctypes.byref(out)))
     return out.value
+
+
+# ------------------------------------------------------------------ NEXT-1: Alg. 1 model selection
+def raftgp_model_select(g: Graph, Z: torch.Tensor, eps: int = 5, max_iter: int = 100, rule="global",
+                        labels: Optional[torch.Tensor] = None):
+    """Alg. 1 on the device embedding Z (n x L fp32). Returns (labels int32 CUDA tensor, K, stats dict)."""
+    if Z.dtype != torch.float32 or Z.dim() != 2:
+        raise ValueError("Z must be a 2-D float32 tensor")
+    _dev(Z, "Z")
+    r = LMOD_RULES[rule] if isinstance(rule, str) else int(rule)
+    if labels is None:
+        labels = torch.empty(max(1, g.rows), dtype=torch.int32, device=g.ctx.device)[: g.rows]
+    k = c_i32(0)
+    st = np.zeros(4, np.int64)
+    _ck(load_library().raftgp_model_select(g.h, _ptr(Z.contiguous()), Z.shape[1], eps, max_iter, r, _ptr(labels),
+                                           ctypes.byref(k), c_vp(st.ctypes.data)))
+    return labels, int(k.value), dict(zip(("blocks", "splits", "lloyd_iters", "levels"), (int(x) for x in st)))
