@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-select", action="store_true", help="skip the NEXT-1 model-selection measurement")
+    ap.add_argument("--select-reps", type=int, default=3)
     ap.add_argument("--clock-period-ms", type=int, default=200)
     ap.add_argument("--clock-query", default=None)
     ap.add_argument("--no-clocks", action="store_true")
@@ -221,6 +223,51 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ GPU arm
+def measure_select(args, rg, ctx, gr, src_d, dst_d, variants, dims, Zbuf, barrier, peak, peak_src):
+    """NEXT-1 (Alg. 1): time raftgp_model_select on the embeddings of one step. The call is
+    synchronous (the host drives the tree levels), so the events bracket what a caller waits for. The Lloyd
+    pass is HBM-bound: per visited row it reads segment id, side and bounds and writes the bounds (24 B); a row
+    that fails the bound test also reads its node id and Z row (4L + 4 B)."""
+    import torch
+    from sklearn.metrics import adjusted_rand_score, normalized_mutual_info_score
+    g = rg.raftgp_build_csr(ctx, gr.n, src_d, dst_d)
+    rg.raftgp_embed_multi(g, variants, dims, args.seed, Z=Zbuf)
+    L = dims[-1]
+    out = {"call": "raftgp_model_select(eps=5, max_iter=100, rule=global)", "unit": "nodes/s", "L": L}
+    for v in variants:
+        lab, K, st = rg.raftgp_model_select(g, Zbuf[v])        # warm-up (allocates the workspace)
+        ctx.prof_reset()
+        ctx.set_profiling(True)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(ctx.stream)
+        for _ in range(args.select_reps):
+            lab, K, st = rg.raftgp_model_select(g, Zbuf[v])
+        e1.record(ctx.stream)
+        barrier()
+        ms = e0.elapsed_time(e1) / args.select_reps
+        prof = {k: (t / args.select_reps, c // args.select_reps) for k, (t, c) in ctx.prof_read().items()}
+        ctx.set_profiling(False)
+        labels = lab.cpu().numpy()
+        lloyd_ms = prof.get("select_lloyd", (0.0, 0))[0]
+        lloyd_bytes = st["lloyd_rows"] * 24 + st["rows_read"] * (4 * L + 4)
+        ach = lloyd_bytes / (lloyd_ms * 1e-3) / 1e9 if lloyd_ms else None
+        out[v] = {
+            "ms": ms, "value": gr.n / (ms * 1e-3), "blocks": K, "planted_blocks": int(gr.info["k"]),
+            "ari_vs_planted": float(adjusted_rand_score(gr.labels, labels)),
+            "nmi_vs_planted": float(normalized_mutual_info_score(gr.labels, labels)),
+            "stats": st, "kernel_ms": {k: round(t, 4) for k, (t, _) in sorted(prof.items(), key=lambda x: -x[1][0])},
+            "kernel_launches": sum(c for _, c in prof.values()),
+            "lloyd_roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                               "frac": (ach / peak) if ach else None, "peak_source": peak_src,
+                               "bytes": lloyd_bytes,
+                               "bytes_rule": "visited rows * 24 (segment, side, bounds r/w) + read rows * (4L + 4)"},
+        }
+    g.close()
+    return out
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -365,6 +412,11 @@ def main():
                 "peak_source": peak_src, "frac_of_8TBs_nominal": ach / 8000.0, "traffic": traffic,
                 "bytes_per_launch": hop_stats[dom]["bytes_per_launch"]}
 
+    # ---------------- NEXT-1: Alg. 1 model selection on this step's embeddings (whole graph, N = 1)
+    select = None
+    if world == 1 and not args.no_select:
+        select = measure_select(args, rg, ctx, gr, src_d, dst_d, variants, dims, Zbuf, barrier, peak, peak_src)
+
     # ---------------- e2e through the C-ABI with host buffers (H2D of edges, D2H of Z inside the timed region)
     # N = 1: three contexts on three streams, steps rotate over them, so a step's copies overlap other
     # steps' kernels (multi-buffering with the public API); every step still copies its own edges in and
@@ -454,6 +506,7 @@ def main():
             "clocks": clocks.summary(),
             "kernels_ms_per_step": {k: round(v, 4) for k, v in sorted(kernel_times.items(), key=lambda x: -x[1])},
             "hops": hop_stats,
+            "model_selection": select,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

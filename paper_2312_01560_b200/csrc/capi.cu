@@ -18,7 +18,7 @@ namespace raftgp {
 
 const char *const kKernelNames[K_NUM] = {
     "csr_count", "scan", "csr_scatter", "csr_sort_warp", "csr_sort_block", "csr_compact", "degree_scalars",
-    "sketch", "g_partials", "g_final", "feature_hop", "transform", "gcn_hop", "hop_generic", "misc", "csr_partition", "csr_bucket_sort", "row_order", "model_select"};
+    "sketch", "g_partials", "g_final", "feature_hop", "transform", "gcn_hop", "hop_generic", "misc", "csr_partition", "csr_bucket_sort", "row_order", "model_select", "select_seed", "select_lloyd", "select_split"};
 
 static thread_local std::string g_last_error;
 
@@ -811,7 +811,7 @@ raftgp_status raftgp_model_select(raftgp_graph g, const float *Z_dev, int32_t L,
     RG_TRY(set_device(g->ctx));
     if (g->n == 0) {
         *num_blocks = 0;
-        if (stats) stats[0] = stats[1] = stats[2] = stats[3] = 0;
+        if (stats) for (int i = 0; i < 7; ++i) stats[i] = 0;
         return RAFTGP_OK;
     }
     return model_select(g, Z_dev, L, eps, max_iter, rule, labels_dev, num_blocks, stats);

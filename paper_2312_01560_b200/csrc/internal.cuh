@@ -35,6 +35,9 @@ enum KernelId : int {
     K_CSR_BUCKET,
     K_ORDER,
     K_SELECT,
+    K_SEL_SEED,
+    K_SEL_LLOYD,
+    K_SEL_SPLIT,
     K_NUM
 };
 extern const char *const kKernelNames[K_NUM];

@@ -28,7 +28,6 @@
 namespace raftgp {
 namespace {
 
-constexpr int kSelRange = 128;   // positions per warp in the fused Lloyd / mean passes
 constexpr int kEdgeRange = 16;   // rows per warp in the split-test pass
 
 __device__ __forceinline__ long long fixq(float z) { return __double2ll_rn(__dmul_rn((double)z, 4294967296.0)); }
@@ -37,13 +36,13 @@ __device__ __forceinline__ double centre(long long S, unsigned long long cnt) {
     return __ddiv_rn(__dmul_rn(__ll2double_rn(S), 0x1p-32), __ull2double_rn(cnt));
 }
 
-// SELECT_SPEC §2 squared distance of a row held in shared memory (float4-aligned) to mu (global, fp64)
+// SELECT_SPEC §2 squared distance of a row (global memory, float4-aligned) to mu (fp64)
 template <int L>
 __device__ __forceinline__ double sqdist_smem(const float *row, const double *mu) {
     double d = 0.0;
 #pragma unroll 4
     for (int k = 0; k < L / 4; ++k) {
-        const float4 v = *reinterpret_cast<const float4 *>(row + 4 * k);
+        const float4 v = reinterpret_cast<const float4 *>(row)[k];
         const double2 m01 = __ldg(reinterpret_cast<const double2 *>(mu + 4 * k));
         const double2 m23 = __ldg(reinterpret_cast<const double2 *>(mu + 4 * k + 2));
         double t;
@@ -55,21 +54,41 @@ __device__ __forceinline__ double sqdist_smem(const float *row, const double *mu
     return d;
 }
 
-template <int L>
-__device__ __forceinline__ double sqdist_global(const float *row, const double *mu) {
-    double d = 0.0;
-#pragma unroll 4
-    for (int k = 0; k < L / 4; ++k) {
-        const float4 v = __ldg(reinterpret_cast<const float4 *>(row + 4 * k));
-        const double2 m01 = __ldg(reinterpret_cast<const double2 *>(mu + 4 * k));
-        const double2 m23 = __ldg(reinterpret_cast<const double2 *>(mu + 4 * k + 2));
-        double t;
-        t = __dsub_rn((double)v.x, m01.x); d = __dadd_rn(d, __dmul_rn(t, t));
-        t = __dsub_rn((double)v.y, m01.y); d = __dadd_rn(d, __dmul_rn(t, t));
-        t = __dsub_rn((double)v.z, m23.x); d = __dadd_rn(d, __dmul_rn(t, t));
-        t = __dsub_rn((double)v.w, m23.y); d = __dadd_rn(d, __dmul_rn(t, t));
+// Both squared distances of one row to the two centres mu[0..L), mu[L..2L): each element is converted once
+// and feeds the two sequential sums (the op sequence of each sum is exactly SELECT_SPEC §2's). Global rows
+// are loaded in chunks of up to 64 floats with every load issued before the arithmetic (one memory latency
+// per chunk instead of one per float4).
+template <int L, bool GLOBAL>
+__device__ __forceinline__ void sqdist2(const float *row, const double *mu, double &d0, double &d1) {
+    d0 = 0.0;
+    d1 = 0.0;
+    constexpr int CH = L / 4 < 16 ? L / 4 : 16;   // float4 per chunk
+#pragma unroll
+    for (int c = 0; c < L / 4; c += CH) {
+        float4 v[CH];
+#pragma unroll
+        for (int k = 0; k < CH; ++k)
+            v[k] = GLOBAL ? __ldg(reinterpret_cast<const float4 *>(row) + c + k)
+                          : reinterpret_cast<const float4 *>(row)[c + k];
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+            const double *m = mu + 4 * (c + k);
+            const double2 a01 = __ldg(reinterpret_cast<const double2 *>(m));
+            const double2 a23 = __ldg(reinterpret_cast<const double2 *>(m + 2));
+            const double2 b01 = __ldg(reinterpret_cast<const double2 *>(m + L));
+            const double2 b23 = __ldg(reinterpret_cast<const double2 *>(m + L + 2));
+            const double x0 = (double)v[k].x, x1 = (double)v[k].y, x2 = (double)v[k].z, x3 = (double)v[k].w;
+            double t;
+            t = __dsub_rn(x0, a01.x); d0 = __dadd_rn(d0, __dmul_rn(t, t));
+            t = __dsub_rn(x0, b01.x); d1 = __dadd_rn(d1, __dmul_rn(t, t));
+            t = __dsub_rn(x1, a01.y); d0 = __dadd_rn(d0, __dmul_rn(t, t));
+            t = __dsub_rn(x1, b01.y); d1 = __dadd_rn(d1, __dmul_rn(t, t));
+            t = __dsub_rn(x2, a23.x); d0 = __dadd_rn(d0, __dmul_rn(t, t));
+            t = __dsub_rn(x2, b23.x); d1 = __dadd_rn(d1, __dmul_rn(t, t));
+            t = __dsub_rn(x3, a23.y); d0 = __dadd_rn(d0, __dmul_rn(t, t));
+            t = __dsub_rn(x3, b23.y); d1 = __dadd_rn(d1, __dmul_rn(t, t));
+        }
     }
-    return d;
 }
 
 // Per-segment state of one level (S segments; all device arrays).
@@ -81,37 +100,80 @@ struct SegState {
     int32_t *amin;             // [S] smallest node id attaining dmax
     int32_t *changed;          // [S]
     int32_t *done;             // [S]
+    float *delta;              // [S][2] upper bounds of the last centre moves (pruning, see bound_up)
 };
 
-// Fused pass over the positions of a level. MODE 0: mean pass (every member into slot 0, |z| <= 1 check).
-// MODE 1: Lloyd iteration t: assign side by distance to mu[s][0], mu[s][1], then accumulate q(z) per side.
-// Each warp handles kSelRange consecutive positions; rows are staged 32 at a time in shared memory, then
-// lane-per-column integer sums run along the staged rows and are flushed with one atomic per (segment,
-// side, column) whenever the segment changes.
-template <int L, int MODE>
-__global__ void __launch_bounds__(L >= 128 ? 128 : 256) sel_pass(const float *__restrict__ Z, const int32_t *__restrict__ perm,
-                                                          const int32_t *__restrict__ pseg, int32_t *__restrict__ side,
-                                                          int64_t n_act, int t, SegState st, int32_t *err) {
-    constexpr int LD = L + 4;
-    constexpr int CPL = (L + 31) / 32;   // columns per lane
-    extern __shared__ __align__(16) float sel_smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float *stage = sel_smem + (size_t)warp * 32 * LD;
-    __shared__ int2 meta_all[8][32];
-    int2 *meta = meta_all[warp];
-    const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-    const int64_t beg = w * kSelRange;
-    if (beg >= n_act) return;
-    const int64_t end = min(beg + (int64_t)kSelRange, n_act);
+// Exact-pruning bounds (Hamerly's algorithm for K = 2, made exact): per row an upper bound u on the TRUE
+// Euclidean distance to its own centre and a lower bound l on the distance to the other centre, kept as
+// floats with directed rounding and a 2^-40 relative slack over the fp64 distances (whose rounding error is
+// < L * 2^-53). After the centres move by at most delta (rounded up), u += delta_own and l -= delta_other.
+// A row with u (1 + 2^-20) < l provably keeps its side: the true distances are ordered with a gap of at
+// least 2^-20 relative, far above the fp64 error of the spec's sequential squared distances, so the plain
+// recomputation (and the oracle) would take the same decision. Only rows that fail the test are read and
+// recomputed, and the centroid sums are updated incrementally (exact integers) for the rows that switched.
+__device__ __forceinline__ float bound_up(double d2) {
+    return __double2float_ru(__dmul_ru(__dsqrt_ru(d2), 1.0 + 0x1p-40));
+}
+__device__ __forceinline__ float bound_dn(double d2) {
+    return __double2float_rd(__dmul_rd(__dsqrt_rd(d2), 1.0 - 0x1p-40));
+}
 
+// ---------------------------------------------------------------- row staging by bulk copy (TMA engine)
+// Every row a pass needs is brought into shared memory by cp.async.bulk (one 4L-byte copy per row, issued by
+// the lane that owns the row, completion counted on a per-warp mbarrier). The rows never pass through
+// registers or the L1 data pipe on their way in; lanes then read their own row (distances, a lane per row,
+// conflict-free float4 loads thanks to the 16-byte row padding) or one row across the warp (column sums).
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init1(uint64_t *bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void bulk_row(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    for (uint32_t it = 0; it < (1u << 28); ++it) {
+        uint32_t done;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(phase)
+            : "memory");
+        if (done) return;
+    }
+    __trap();   // a copy never landed: fail loudly instead of hanging
+}
+
+// generic-proxy reads of a stage buffer are ordered before the next bulk copy into it
+__device__ __forceinline__ void stage_release() {
+    __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+constexpr int kRowWarps = 4;    // warps per CTA of sel_rows (two 32-row stages each)
+constexpr int kRowRange = 256;  // positions per warp of sel_rows
+
+template <int L>
+struct RowAcc {   // per-lane column sums (lane owns columns lane + 32 k) for two sides, run-aggregated
+    static constexpr int CPL = (L + 31) / 32;
     long long a0[CPL], a1[CPL];
-#pragma unroll
-    for (int k = 0; k < CPL; ++k) a0[k] = a1[k] = 0;
-    unsigned long long c0 = 0, c1 = 0;
+    long long c0 = 0, c1 = 0;
     int cur = -1;
-    bool bad = false;
-
-    auto flush = [&]() {
+    __device__ RowAcc() {
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) a0[k] = a1[k] = 0;
+    }
+    __device__ __forceinline__ void flush(const SegState &st, int lane) {
         if (cur >= 0) {
 #pragma unroll
             for (int k = 0; k < CPL; ++k) {
@@ -123,69 +185,275 @@ __global__ void __launch_bounds__(L >= 128 ? 128 : 256) sel_pass(const float *__
                 a0[k] = a1[k] = 0;
             }
             if (lane == 0) {
-                if (c0) atomicAdd(&st.cnt[cur * 2 + 0], c0);
-                if (c1) atomicAdd(&st.cnt[cur * 2 + 1], c1);
+                if (c0) atomicAdd(&st.cnt[cur * 2 + 0], (unsigned long long)c0);
+                if (c1) atomicAdd(&st.cnt[cur * 2 + 1], (unsigned long long)c1);
             }
         }
         c0 = c1 = 0;
-    };
-
-    for (int64_t b = beg; b < end; b += 32) {
-        const int64_t pos = b + lane;
-        int s = -1, c = 0;
-        if (pos < end) {
-            s = pseg[pos];
-            if (MODE == 1 && st.done[s]) s = -1;
+    }
+    // add (w = +1) or move (w = 0: side 0 -> 1 when dir > 0, side 1 -> 0 when dir < 0) one row's fixed-point
+    // values; s, dir are warp-uniform, the row is in shared memory
+    __device__ __forceinline__ void add(const SegState &st, int lane, int s, const float *row, int side, int dir) {
+        if (s != cur) {
+            flush(st, lane);
+            cur = s;
         }
-        if (s >= 0) {
-            const float4 *src = reinterpret_cast<const float4 *>(Z + (size_t)perm[pos] * L);
-            float4 *dst = reinterpret_cast<float4 *>(stage + lane * LD);
-#pragma unroll 4
-            for (int k = 0; k < L / 4; ++k) {
-                const float4 v = __ldg(src + k);
-                if (MODE == 0)
-                    bad |= !(fabsf(v.x) <= 1.f && fabsf(v.y) <= 1.f && fabsf(v.z) <= 1.f && fabsf(v.w) <= 1.f);
-                dst[k] = v;
-            }
-            if (MODE == 1) {
-                const double *m0 = st.mu + (size_t)s * 2 * L;
-                const double d0 = sqdist_smem<L>(stage + lane * LD, m0);
-                const double d1 = sqdist_smem<L>(stage + lane * LD, m0 + L);
-                c = d1 < d0 ? 1 : 0;
-                if (t > 1 && side[pos] != c) st.changed[s] = 1;
-                side[pos] = c;
-            }
-        }
-        meta[lane] = make_int2(s, c);
-        __syncwarp();
-        const int rows = (int)min((int64_t)32, end - b);
-        for (int r = 0; r < rows; ++r) {
-            const int2 mr = meta[r];
-            if (mr.x != cur) {
-                flush();
-                cur = mr.x;
-            }
-            if (mr.x < 0) continue;
-            const float *row = stage + r * LD;
 #pragma unroll
-            for (int k = 0; k < CPL; ++k) {
-                const int col = lane + 32 * k;
-                if (col < L) {
-                    const long long q = fixq(row[col]);
-                    if (mr.y) a1[k] += q;
+        for (int k = 0; k < CPL; ++k) {
+            const int col = lane + 32 * k;
+            if (col < L) {
+                const long long q = fixq(row[col]);
+                if (dir == 0) {
+                    if (side) a1[k] += q;
                     else a0[k] += q;
+                } else if (dir > 0) {
+                    a0[k] -= q;
+                    a1[k] += q;
+                } else {
+                    a0[k] += q;
+                    a1[k] -= q;
                 }
             }
-            if (mr.y) ++c1;
-            else ++c0;
         }
-        __syncwarp();
+        if (dir == 0) {
+            if (side) ++c1;
+            else ++c0;
+        } else {
+            c0 -= dir;
+            c1 += dir;
+        }
     }
-    flush();
+};
+
+// A pass over every row of the level (the positions are contiguous per segment). Each warp streams
+// kRowRange positions through two 32-row shared-memory stages (bulk copies of batch k+1 in flight while
+// batch k is processed).
+//   MODE 0: mean pass (level 1 only; deeper levels inherit their totals from the parent's final sums):
+//           every row added to slot 0 (|z| <= 1 checked).
+//   MODE 1: Lloyd iteration t = 1: d(z, mu_0) is the one the second seeding pass stored (mu_0 = z_a, same
+//           op sequence), so only d(z, mu_1) is computed; bounds initialised; only side-1 rows are summed
+//           (slot 1) and sel_update turns the slot-0 total into the side-0 sum (exact integers).
+//   MODE 2: seeding: distance to mu[s][0] per row (dpos) and the per-segment maximum (SELECT_SPEC §3.1).
+template <int L, int MODE>
+__global__ void __launch_bounds__(kRowWarps * 32) sel_rows(const float *__restrict__ Z, const int32_t *__restrict__ perm,
+                                                           const int32_t *__restrict__ pseg, int32_t *__restrict__ side,
+                                                           float2 *bnd, double *dpos,   // the same buffer (aliased)
+                                                           int64_t n_act, SegState st, int32_t *err,
+                                                           unsigned long long *rows_read) {
+    constexpr int LD = L + 4;
+    constexpr uint32_t RB = 4u * L;
+    extern __shared__ __align__(16) float sel_smem[];
+    __shared__ uint64_t bars[kRowWarps][2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float *stage = sel_smem + (size_t)warp * 2 * 32 * LD;
+    uint64_t *bar = bars[warp];
+    const int64_t beg = ((int64_t)blockIdx.x * kRowWarps + warp) * kRowRange;
+    if (beg >= n_act) return;
+    const int64_t end = min(beg + (int64_t)kRowRange, n_act);
+    if (lane == 0) {
+        mbar_init1(&bar[0]);
+        mbar_init1(&bar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+
+    RowAcc<L> acc;
+    bool bad = false;
+    int sb[2] = {-1, -1};
+    uint32_t ph = 0;   // bit k: phase of bar[k]
+
+    auto issue = [&](int64_t b, int buf) {
+        const int rows = (int)min((int64_t)32, end - b);
+        int s = -1;
+        if (lane == 0) mbar_expect(&bar[buf], (uint32_t)rows * RB);
+        __syncwarp();
+        if (lane < rows) {
+            s = pseg[b + lane];
+            bulk_row(stage + ((size_t)buf * 32 + lane) * LD, Z + (size_t)perm[b + lane] * L, RB, &bar[buf]);
+        }
+        sb[buf] = s;
+    };
+
+    issue(beg, 0);
+    int buf = 0;
+    for (int64_t b = beg; b < end; b += 32, buf ^= 1) {
+        if (b + 32 < end) issue(b + 32, buf ^ 1);
+        mbar_wait(&bar[buf], (ph >> buf) & 1u);
+        ph ^= 1u << buf;
+        const int64_t pos = b + lane;
+        const int s = sb[buf];
+        const float *srow = stage + (size_t)buf * 32 * LD;
+        const float *row = srow + lane * LD;
+        int add = 0;
+        constexpr int sd = MODE == 1 ? 1 : 0;   // slot the pass sums into (warp-uniform)
+        if (s >= 0) {
+            if (MODE == 0) {
+#pragma unroll 4
+                for (int k = 0; k < L / 4; ++k) {
+                    const float4 v = reinterpret_cast<const float4 *>(row)[k];
+                    bad |= !(fabsf(v.x) <= 1.f && fabsf(v.y) <= 1.f && fabsf(v.z) <= 1.f && fabsf(v.w) <= 1.f);
+                }
+                add = 1;
+            } else if (MODE == 1) {
+                const double d0 = dpos[pos];
+                const double d1 = sqdist_smem<L>(row, st.mu + ((size_t)s * 2 + 1) * L);
+                const int c = d1 < d0 ? 1 : 0;
+                bnd[pos] = c ? make_float2(bound_up(d1), bound_dn(d0)) : make_float2(bound_up(d0), bound_dn(d1));
+                side[pos] = c;
+                add = c;
+            }
+        }
+        if (MODE == 2) {
+            double d = 0.0;
+            if (s >= 0) {
+                d = sqdist_smem<L>(row, st.mu + (size_t)s * 2 * L);
+                dpos[pos] = d;
+            }
+            const int s0 = __shfl_sync(0xffffffffu, s, 0);
+            if (__all_sync(0xffffffffu, s == s0) && s0 >= 0) {
+                double m = d;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+                if (lane == 0) atomicMax(&st.dmax[s0], (unsigned long long)__double_as_longlong(m));
+            } else if (s >= 0) {
+                atomicMax(&st.dmax[s], (unsigned long long)__double_as_longlong(d));
+            }
+        } else {
+            // column sums over the staged rows, in position order (segments are contiguous runs)
+            for (unsigned m = __ballot_sync(0xffffffffu, add != 0); m; m &= m - 1) {
+                const int r = __ffs(m) - 1;
+                acc.add(st, lane, __shfl_sync(0xffffffffu, s, r), srow + r * LD, sd, 0);
+            }
+        }
+        stage_release();
+    }
+    if (MODE != 2) acc.flush(st, lane);
     if (MODE == 0 && __any_sync(0xffffffffu, bad) && lane == 0) atomicExch(err, 1);
+    if (MODE == 1 && lane == 0) atomicAdd(&rows_read[blockIdx.x & 63], (unsigned long long)(end - beg));
 }
 
-// Warp per segment: slot-0 mean from the mean pass, reset the accumulators and the argmax state.
+// Lloyd iteration t > 1 with exact pruning. Each warp scans kPruneRange consecutive positions: the bound test
+// runs on every position (segment, side and bounds only: 24 B per row); positions that fail it are queued in
+// shared memory and recomputed 32 at a time with all lanes busy (a lane per row, rows bulk-copied into a
+// shared-memory stage). Rows that switch side then move their fixed-point values between the two sums
+// (exact integers), run-aggregated per segment.
+constexpr int kPruneWarps = 8;
+constexpr int kPruneRange = 1024;
+
+template <int L>
+__global__ void __launch_bounds__(kPruneWarps * 32, 2) sel_lloyd_pruned(const float *__restrict__ Z,
+                                                                      const int32_t *__restrict__ perm,
+                                                                      const int32_t *__restrict__ pseg,
+                                                                      int32_t *__restrict__ side,
+                                                                      float2 *__restrict__ bnd, int64_t n_act,
+                                                                      SegState st, unsigned long long *rows_read) {
+    constexpr int LD = L + 4;
+    constexpr uint32_t RB = 4u * L;
+    extern __shared__ __align__(16) float sel_smem[];
+    __shared__ int qbuf[kPruneWarps][160];
+    __shared__ uint64_t bars[kPruneWarps];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float *stage = sel_smem + (size_t)warp * 32 * LD;
+    uint64_t *bar = &bars[warp];
+    int *q = qbuf[warp];
+    const int64_t beg = ((int64_t)blockIdx.x * kPruneWarps + warp) * kPruneRange;
+    if (beg >= n_act) return;
+    const int64_t end = min(beg + (int64_t)kPruneRange, n_act);
+    const unsigned lt = (1u << lane) - 1u;
+    if (lane == 0) {
+        mbar_init1(bar);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+
+    RowAcc<L> acc;
+    int qn = 0;
+    uint32_t ph = 0;
+    unsigned nread = 0;
+
+    // recompute the first k queued positions (k <= 32), lane j takes q[j]
+    auto round = [&](int k) {
+        nread += k;
+        int s = -1;
+        int64_t pos = 0;
+        if (lane == 0) mbar_expect(bar, (uint32_t)k * RB);
+        __syncwarp();
+        if (lane < k) {
+            pos = beg + q[lane];
+            s = pseg[pos];
+            bulk_row(stage + lane * LD, Z + (size_t)perm[pos] * L, RB, bar);
+        }
+        mbar_wait(bar, ph);
+        ph ^= 1u;
+        int w0 = 0;
+        if (lane < k) {
+            double d0, d1;
+            sqdist2<L, false>(stage + lane * LD, st.mu + (size_t)s * 2 * L, d0, d1);
+            const int c = d1 < d0 ? 1 : 0;
+            bnd[pos] = c ? make_float2(bound_up(d1), bound_dn(d0)) : make_float2(bound_up(d0), bound_dn(d1));
+            if (side[pos] != c) {
+                side[pos] = c;
+                st.changed[s] = 1;
+                w0 = c ? -1 : 1;   // moved 0 -> 1: (-1, +1); moved 1 -> 0: (+1, -1)
+            }
+        }
+        for (unsigned m = __ballot_sync(0xffffffffu, w0 != 0); m; m &= m - 1) {
+            const int r = __ffs(m) - 1;
+            acc.add(st, lane, __shfl_sync(0xffffffffu, s, r), stage + r * LD, 0, -__shfl_sync(0xffffffffu, w0, r));
+        }
+        stage_release();
+    };
+
+    for (int64_t b = beg; b < end; b += 128) {
+        // bound test of 128 positions: lane owns b + 32 j + lane, all loads issued up front
+        int sj[4], cj[4];
+        float2 ulj[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t pos = b + 32 * j + lane;
+            sj[j] = pos < end ? pseg[pos] : -1;
+            cj[j] = pos < end ? side[pos] : 0;
+            ulj[j] = pos < end ? bnd[pos] : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t pos = b + 32 * j + lane;
+            bool need = false;
+            const int s = sj[j];
+            if (s >= 0 && !st.done[s]) {
+                const int c = cj[j];
+                const float2 dl = reinterpret_cast<const float2 *>(st.delta)[s];
+                const float u = __fadd_ru(ulj[j].x, c ? dl.y : dl.x);
+                const float l = fmaxf(0.f, __fsub_rd(ulj[j].y, c ? dl.x : dl.y));
+                if (__fmul_ru(u, 1.0f + 0x1p-20f) < l) bnd[pos] = make_float2(u, l);
+                else need = true;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, need);
+            if (need) q[qn + __popc(m & lt)] = (int)(pos - beg);
+            qn += __popc(m);
+        }
+        __syncwarp();
+        while (qn >= 32) {
+            round(32);
+            const int rest = qn - 32;
+            int v[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[i] = lane + 32 * i < rest ? q[32 + lane + 32 * i] : 0;
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (lane + 32 * i < rest) q[lane + 32 * i] = v[i];
+            qn = rest;
+            __syncwarp();
+        }
+    }
+    if (qn > 0) round(qn);
+    acc.flush(st, lane);
+    if (lane == 0 && nread) atomicAdd(&rows_read[blockIdx.x & 63], (unsigned long long)nread);
+}
+
+// Warp per segment: the mean of U from the slot-0 totals (mean pass at level 1, inherited from the parent's
+// final side sums below it); slot 0 keeps the totals, slot 1 and the argmax / Lloyd state are reset.
 template <int L>
 __global__ void sel_mean(SegState st, int S) {
     const int s = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
@@ -194,40 +462,14 @@ __global__ void sel_mean(SegState st, int S) {
     for (int l = lane; l < L; l += 32) {
         const size_t i = (size_t)s * 2 * L + l;
         st.mu[i] = n ? centre((long long)st.acc[i], n) : 0.0;
-        st.acc[i] = 0;
         st.acc[i + L] = 0;
     }
     if (lane == 0) {
-        st.cnt[s * 2] = st.cnt[s * 2 + 1] = 0;
+        st.cnt[s * 2 + 1] = 0;
         st.dmax[s] = 0;
         st.amin[s] = INT_MAX;
         st.changed[s] = 0;
         st.done[s] = 0;
-    }
-}
-
-// Farthest member from the reference point mu[s][slot] (SELECT_SPEC §3.1): distances kept per position,
-// maximum bits per segment.
-template <int L>
-__global__ void sel_far(const float *__restrict__ Z, const int32_t *__restrict__ perm, const int32_t *__restrict__ pseg,
-                        int64_t n_act, int slot, SegState st, double *__restrict__ dpos) {
-    const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int lane = threadIdx.x & 31;
-    int s = -1;
-    double d = 0.0;
-    if (pos < n_act) {
-        s = pseg[pos];
-        d = sqdist_global<L>(Z + (size_t)perm[pos] * L, st.mu + ((size_t)s * 2 + slot) * L);
-        dpos[pos] = d;
-    }
-    const int s0 = __shfl_sync(0xffffffffu, s, 0);
-    if (__all_sync(0xffffffffu, s == s0) && s0 >= 0) {
-        double m = d;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (lane == 0) atomicMax(&st.dmax[s0], (unsigned long long)__double_as_longlong(m));
-    } else if (s >= 0) {
-        atomicMax(&st.dmax[s], (unsigned long long)__double_as_longlong(d));
     }
 }
 
@@ -254,28 +496,53 @@ __global__ void sel_seed(const float *__restrict__ Z, SegState st, int S, int sl
 }
 
 // Warp per segment after Lloyd iteration t (SELECT_SPEC §3.2): converged segments are frozen; the others
-// get their new centres (an empty side keeps its centre) and count as active.
+// get their new centres (an empty side keeps its centre), an upper bound on how far each centre moved
+// (for the pruning bounds), and count as active. The sums and counts are absolute (never reset): MODE 2
+// passes update them incrementally.
 template <int L>
-__global__ void sel_update(SegState st, int S, int t, int max_iter, int32_t *active) {
+__global__ void sel_update(SegState st, int S, int t, int max_iter, const int32_t *__restrict__ seg_off,
+                           unsigned long long *active) {
     const int s = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
     if (s >= S || st.done[s]) return;
+    if (t == 1) {   // slot 0 held the total over U; the t = 1 pass summed side 1 only
+        for (int l = lane; l < L; l += 32) {
+            const size_t i0 = (size_t)s * 2 * L + l;
+            st.acc[i0] -= st.acc[i0 + L];
+        }
+        if (lane == 0) st.cnt[s * 2] -= st.cnt[s * 2 + 1];
+        __syncwarp();
+    }
     if ((t > 1 && st.changed[s] == 0) || t >= max_iter) {
         if (lane == 0) st.done[s] = 1;
         return;
     }
     const unsigned long long n0 = st.cnt[s * 2], n1 = st.cnt[s * 2 + 1];
+    double m0 = 0.0, m1 = 0.0;
     for (int l = lane; l < L; l += 32) {
         const size_t i0 = (size_t)s * 2 * L + l, i1 = i0 + L;
-        if (n0) st.mu[i0] = centre((long long)st.acc[i0], n0);
-        if (n1) st.mu[i1] = centre((long long)st.acc[i1], n1);
-        st.acc[i0] = 0;
-        st.acc[i1] = 0;
+        if (n0) {
+            const double v = centre((long long)st.acc[i0], n0), dv = v - st.mu[i0];
+            m0 += dv * dv;
+            st.mu[i0] = v;
+        }
+        if (n1) {
+            const double v = centre((long long)st.acc[i1], n1), dv = v - st.mu[i1];
+            m1 += dv * dv;
+            st.mu[i1] = v;
+        }
     }
-    __syncwarp();
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        m0 += __shfl_xor_sync(0xffffffffu, m0, o);
+        m1 += __shfl_xor_sync(0xffffffffu, m1, o);
+    }
     if (lane == 0) {
-        st.cnt[s * 2] = st.cnt[s * 2 + 1] = 0;
+        // generous slack (2^-30 relative + an absolute floor) over the rounding of this fp64 sum
+        st.delta[2 * s] = __double2float_ru(__dmul_ru(__dsqrt_ru(m0), 1.0 + 0x1p-30) + 0x1p-60);
+        st.delta[2 * s + 1] = __double2float_ru(__dmul_ru(__dsqrt_ru(m1), 1.0 + 0x1p-30) + 0x1p-60);
         st.changed[s] = 0;
-        atomicAdd(active, 1);
+        atomicAdd(active, 1ull);                                                     // active segments
+        atomicAdd(active + 1, (unsigned long long)(seg_off[s + 1] - seg_off[s]));   // and their rows
     }
 }
 
@@ -366,6 +633,20 @@ __global__ void sel_children(const int32_t *__restrict__ keep, const int64_t *__
     new_off[2 * k + 1] = (int32_t)(base[s] + (int64_t)nsz[2 * s]);
 }
 
+// Warp per parent segment: the two children of a kept segment inherit its final side sums and counts as their
+// slot-0 totals (so no mean pass is needed below level 1).
+template <int L>
+__global__ void sel_inherit(const int32_t *__restrict__ keep, const int64_t *__restrict__ krank, SegState st, int S,
+                            unsigned long long *__restrict__ nacc, unsigned long long *__restrict__ ncnt) {
+    const int s = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    if (s >= S || !keep[s]) return;
+    const int64_t k = krank[s];
+    for (int c = 0; c < 2; ++c) {
+        for (int l = lane; l < L; l += 32) nacc[((size_t)(2 * k + c) * 2) * L + l] = st.acc[((size_t)s * 2 + c) * L + l];
+        if (lane == 0) ncnt[(2 * k + c) * 2] = st.cnt[s * 2 + c];
+    }
+}
+
 // Thread per position: stable partition of kept segments into their children; members of stopped
 // segments get their (discovery-order) block id and leave the active set.
 __global__ void sel_scatter(const int32_t *__restrict__ perm, const int32_t *__restrict__ pseg,
@@ -432,17 +713,21 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
     raftgp_ctx ctx = g->ctx;
     cudaStream_t st = ctx->stream;
     const int64_t n = g->n;
-    constexpr int kWarps = L >= 128 ? 4 : 8;
-    constexpr size_t kSmem = (size_t)kWarps * 32 * (L + 4) * sizeof(float);
+    constexpr size_t kRowSmem = (size_t)kRowWarps * 2 * 32 * (L + 4) * sizeof(float);
+    constexpr size_t kPruneSmem = (size_t)kPruneWarps * 32 * (L + 4) * sizeof(float);
     static bool attrs = false;
     if (!attrs) {
-        RG_CUDA(cudaFuncSetAttribute(sel_pass<L, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
-        RG_CUDA(cudaFuncSetAttribute(sel_pass<L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
+        RG_CUDA(cudaFuncSetAttribute(sel_rows<L, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem));
+        RG_CUDA(cudaFuncSetAttribute(sel_rows<L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem));
+        RG_CUDA(cudaFuncSetAttribute(sel_rows<L, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem));
+        RG_CUDA(cudaFuncSetAttribute(sel_lloyd_pruned<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kPruneSmem));
         attrs = true;
     }
 
     int32_t *perm = nullptr, *pseg = nullptr, *side = nullptr, *nperm = nullptr, *npseg = nullptr;
-    int32_t *node_key = nullptr, *label_tmp = nullptr, *err = nullptr, *active = nullptr;
+    int32_t *node_key = nullptr, *label_tmp = nullptr, *err = nullptr;
+    unsigned long long *active = nullptr;
     int64_t *ones = nullptr;
     double *dpos = nullptr;
     RG_TRY(dalloc_t(ctx, &perm, n));
@@ -454,9 +739,11 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
     RG_TRY(dalloc_t(ctx, &label_tmp, n));
     RG_TRY(dalloc_t(ctx, &ones, n + 1));
     RG_TRY(dalloc_t(ctx, &dpos, n));
-    RG_TRY(dalloc_t(ctx, &err, 2));
-    active = err + 1;
-    RG_CUDA(cudaMemsetAsync(err, 0, 2 * sizeof(int32_t), st));
+    float2 *bnd = reinterpret_cast<float2 *>(dpos);   // seeding distances, then the Lloyd pruning bounds
+    RG_TRY(dalloc_t(ctx, &err, 1));
+    RG_TRY(dalloc_t(ctx, &active, 2 + 64));   // [0] active segments, [1] their rows, [2..65] rows read
+    RG_CUDA(cudaMemsetAsync(active, 0, sizeof(unsigned long long) * 66, st));
+    RG_CUDA(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
     {
         LaunchScope LS(ctx, K_SELECT);
         sel_init<<<grid_for(n, 256), 256, 0, st>>>(perm, pseg, node_key, n);
@@ -471,10 +758,18 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
     RG_CUDA(cudaMemcpyAsync(seg_off, off0.data(), 2 * sizeof(int32_t), cudaMemcpyHostToDevice, st));
 
     int32_t blocks = 0;
-    int64_t splits = 0, lloyd_iters = 0, levels = 0;
+    int64_t splits = 0, lloyd_iters = 0, levels = 0, lloyd_rows = 0, seed_rows = 0, act_rows = 0;
     int32_t h_small[2] = {0, 0};
+    unsigned long long h_act[2] = {0, 0};
     int64_t h_two[2] = {0, 0};
     raftgp_status rc = RAFTGP_OK;
+    // per-level [S][2][L] side sums and [S][2] counts; level 1 fills slot 0 with a mean pass, deeper levels
+    // inherit the parent's final side sums (sel_inherit)
+    unsigned long long *lvl_acc = nullptr, *lvl_cnt = nullptr;
+    RG_TRY(dalloc_t(ctx, &lvl_acc, (size_t)2 * L));
+    RG_TRY(dalloc_t(ctx, &lvl_cnt, (size_t)2));
+    RG_CUDA(cudaMemsetAsync(lvl_acc, 0, sizeof(unsigned long long) * 2 * L, st));
+    RG_CUDA(cudaMemsetAsync(lvl_cnt, 0, sizeof(unsigned long long) * 2, st));
 
     while (S > 0 && rc == RAFTGP_OK) {
         ++levels;
@@ -483,13 +778,14 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
         unsigned long long *nsz = nullptr, *mbar = nullptr, *cut = nullptr;
         int32_t *keep = nullptr, *ksize = nullptr, *new_off = nullptr;
         int64_t *krank = nullptr, *base = nullptr;
-        RG_TRY(dalloc_t(ctx, &ss.acc, (size_t)S * 2 * L));
-        RG_TRY(dalloc_t(ctx, &ss.cnt, (size_t)S * 2));
+        ss.acc = lvl_acc;
+        ss.cnt = lvl_cnt;
         RG_TRY(dalloc_t(ctx, &ss.mu, (size_t)S * 2 * L));
         RG_TRY(dalloc_t(ctx, &ss.dmax, (size_t)S));
         RG_TRY(dalloc_t(ctx, &ss.amin, (size_t)S));
         RG_TRY(dalloc_t(ctx, &ss.changed, (size_t)S));
         RG_TRY(dalloc_t(ctx, &ss.done, (size_t)S));
+        RG_TRY(dalloc_t(ctx, &ss.delta, (size_t)S * 2));
         RG_TRY(dalloc_t(ctx, &nsz, (size_t)S * 5));
         mbar = nsz + 2 * (size_t)S;
         cut = nsz + 4 * (size_t)S;
@@ -498,21 +794,22 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
         RG_TRY(dalloc_t(ctx, &krank, (size_t)S + 1));
         RG_TRY(dalloc_t(ctx, &base, (size_t)S + 1));
         RG_TRY(dalloc_t(ctx, &new_off, (size_t)2 * S + 1));
-        RG_CUDA(cudaMemsetAsync(ss.acc, 0, sizeof(unsigned long long) * (size_t)S * 2 * L, st));
-        RG_CUDA(cudaMemsetAsync(ss.cnt, 0, sizeof(unsigned long long) * (size_t)S * 2, st));
         RG_CUDA(cudaMemsetAsync(nsz, 0, sizeof(unsigned long long) * (size_t)S * 5, st));
 
-        const int64_t nwarps = ceil_div(n_act, kSelRange);
-        const unsigned pgrid = grid_for(nwarps, kWarps);
+        const unsigned rgrid = grid_for(ceil_div(n_act, kRowRange), kRowWarps);
+        const unsigned qgrid = grid_for(ceil_div(n_act, kPruneRange), kPruneWarps);
+        act_rows = n_act;
+        seed_rows += n_act;
         const unsigned sgrid = grid_for((int64_t)S * 32, 256);
         // seeding: mean, farthest from the mean, farthest from that
-        {
-            LaunchScope LS(ctx, K_SELECT);
-            sel_pass<L, 0><<<pgrid, kWarps * 32, kSmem, st>>>(Z, perm, pseg, side, n_act, 0, ss, err);
+        if (levels == 1) {
+            LaunchScope LS(ctx, K_SEL_SEED);
+            sel_rows<L, 0><<<rgrid, kRowWarps * 32, kRowSmem, st>>>(Z, perm, pseg, side, bnd, dpos, n_act, ss, err,
+                                                                    active + 2);
         }
         RG_CHECK_LAUNCH(ctx);
         {
-            LaunchScope LS(ctx, K_SELECT);
+            LaunchScope LS(ctx, K_SEL_SEED);
             sel_mean<L><<<sgrid, 256, 0, st>>>(ss, S);
         }
         RG_CHECK_LAUNCH(ctx);
@@ -525,17 +822,18 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
         }
         for (int slot = 0; slot < 2 && rc == RAFTGP_OK; ++slot) {
             {
-                LaunchScope LS(ctx, K_SELECT);
-                sel_far<L><<<grid_for(n_act, 256), 256, 0, st>>>(Z, perm, pseg, n_act, 0, ss, dpos);
+                LaunchScope LS(ctx, K_SEL_SEED);
+                sel_rows<L, 2><<<rgrid, kRowWarps * 32, kRowSmem, st>>>(Z, perm, pseg, side, bnd, dpos, n_act, ss,
+                                                                        err, active + 2);
             }
             RG_CHECK_LAUNCH(ctx);
             {
-                LaunchScope LS(ctx, K_SELECT);
+                LaunchScope LS(ctx, K_SEL_SEED);
                 sel_argmin<<<grid_for(n_act, 256), 256, 0, st>>>(perm, pseg, n_act, dpos, ss);
             }
             RG_CHECK_LAUNCH(ctx);
             {
-                LaunchScope LS(ctx, K_SELECT);
+                LaunchScope LS(ctx, K_SEL_SEED);
                 // first seed a overwrites the mean in slot 0; the second seed b goes to slot 1
                 sel_seed<L><<<sgrid, 256, 0, st>>>(Z, ss, S, slot);
             }
@@ -544,36 +842,48 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
         // Lloyd iterations, all segments in lock step (converged ones frozen)
         for (int t = 1; t <= max_iter && rc == RAFTGP_OK; ++t) {
             ++lloyd_iters;
+            lloyd_rows += act_rows;
             {
-                LaunchScope LS(ctx, K_SELECT);
-                sel_pass<L, 1><<<pgrid, kWarps * 32, kSmem, st>>>(Z, perm, pseg, side, n_act, t, ss, err);
+                LaunchScope LS(ctx, K_SEL_LLOYD);
+                if (t == 1)
+                    sel_rows<L, 1><<<rgrid, kRowWarps * 32, kRowSmem, st>>>(Z, perm, pseg, side, bnd, dpos, n_act, ss,
+                                                                            err, active + 2);
+                else
+                    sel_lloyd_pruned<L><<<qgrid, kPruneWarps * 32, kPruneSmem, st>>>(Z, perm, pseg, side, bnd, n_act,
+                                                                                   ss, active + 2);
             }
             RG_CHECK_LAUNCH(ctx);
-            RG_CUDA(cudaMemsetAsync(active, 0, sizeof(int32_t), st));
+            RG_CUDA(cudaMemsetAsync(active, 0, 2 * sizeof(unsigned long long), st));
             {
-                LaunchScope LS(ctx, K_SELECT);
-                sel_update<L><<<sgrid, 256, 0, st>>>(ss, S, t, max_iter, active);
+                LaunchScope LS(ctx, K_SEL_LLOYD);
+                sel_update<L><<<sgrid, 256, 0, st>>>(ss, S, t, max_iter, seg_off, active);
             }
             RG_CHECK_LAUNCH(ctx);
-            RG_CUDA(cudaMemcpyAsync(h_small + 1, active, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+            RG_CUDA(cudaMemcpyAsync(h_act, active, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
             RG_CUDA(cudaStreamSynchronize(st));
-            if (h_small[1] == 0) break;
+            act_rows = (int64_t)h_act[1];
+            if (h_act[0] == 0) break;
         }
-        if (rc != RAFTGP_OK) break;
+        if (rc != RAFTGP_OK) {
+            dfree(ctx, ss.mu); dfree(ctx, ss.dmax); dfree(ctx, ss.amin); dfree(ctx, ss.changed); dfree(ctx, ss.done);
+            dfree(ctx, ss.delta); dfree(ctx, nsz); dfree(ctx, keep); dfree(ctx, krank); dfree(ctx, base);
+            dfree(ctx, new_off);
+            break;
+        }
         // split test
         {
-            LaunchScope LS(ctx, K_SELECT);
+            LaunchScope LS(ctx, K_SEL_SPLIT);
             sel_mark<<<grid_for(n_act, 256), 256, 0, st>>>(perm, pseg, side, n_act, node_key);
         }
         RG_CHECK_LAUNCH(ctx);
         {
-            LaunchScope LS(ctx, K_SELECT);
+            LaunchScope LS(ctx, K_SEL_SPLIT);
             sel_edges<<<grid_for(ceil_div(n_act, kEdgeRange) * 32, 256), 256, 0, st>>>(
                 g->row_ptr, g->col, perm, pseg, side, n_act, node_key, nsz, mbar, cut);
         }
         RG_CHECK_LAUNCH(ctx);
         {
-            LaunchScope LS(ctx, K_SELECT);
+            LaunchScope LS(ctx, K_SEL_SPLIT);
             sel_decide<<<grid_for(S, 256), 256, 0, st>>>(nsz, mbar, cut, S, eps, rule,
                                                          (unsigned long long)g->two_e, keep, ksize);
         }
@@ -582,12 +892,22 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
         RG_TRY(scan_i32_to_i64(ctx, ksize, base, S));
         RG_TRY(scan_i32_to_i64(ctx, side, ones, n_act));
         {
-            LaunchScope LS(ctx, K_SELECT);
+            LaunchScope LS(ctx, K_SEL_SPLIT);
             sel_children<<<grid_for((int64_t)S + 1, 256), 256, 0, st>>>(keep, krank, base, nsz, S, new_off);
         }
         RG_CHECK_LAUNCH(ctx);
+        unsigned long long *nacc = nullptr, *ncnt = nullptr;
+        RG_TRY(dalloc_t(ctx, &nacc, (size_t)S * 4 * L));
+        RG_TRY(dalloc_t(ctx, &ncnt, (size_t)S * 4));
+        RG_CUDA(cudaMemsetAsync(nacc, 0, sizeof(unsigned long long) * (size_t)S * 4 * L, st));
+        RG_CUDA(cudaMemsetAsync(ncnt, 0, sizeof(unsigned long long) * (size_t)S * 4, st));
         {
-            LaunchScope LS(ctx, K_SELECT);
+            LaunchScope LS(ctx, K_SEL_SPLIT);
+            sel_inherit<L><<<sgrid, 256, 0, st>>>(keep, krank, ss, S, nacc, ncnt);
+        }
+        RG_CHECK_LAUNCH(ctx);
+        {
+            LaunchScope LS(ctx, K_SEL_SPLIT);
             sel_scatter<<<grid_for(n_act, 256), 256, 0, st>>>(perm, pseg, side, n_act, seg_off, ones, keep, krank,
                                                               new_off, blocks, nperm, npseg, label_tmp, node_key);
         }
@@ -598,8 +918,11 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
         const int64_t kept = h_two[0];
         blocks += (int32_t)(S - kept);
         splits += kept;
-        dfree(ctx, ss.acc); dfree(ctx, ss.cnt); dfree(ctx, ss.mu); dfree(ctx, ss.dmax); dfree(ctx, ss.amin);
-        dfree(ctx, ss.changed); dfree(ctx, ss.done); dfree(ctx, nsz); dfree(ctx, keep); dfree(ctx, krank);
+        dfree(ctx, ss.acc); dfree(ctx, ss.cnt);
+        lvl_acc = nacc;
+        lvl_cnt = ncnt;
+        dfree(ctx, ss.mu); dfree(ctx, ss.dmax); dfree(ctx, ss.amin);
+        dfree(ctx, ss.changed); dfree(ctx, ss.done); dfree(ctx, ss.delta); dfree(ctx, nsz); dfree(ctx, keep); dfree(ctx, krank);
         dfree(ctx, base);
         dfree(ctx, seg_off);
         seg_off = new_off;
@@ -637,15 +960,28 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
         dfree(ctx, first);
     }
     dfree(ctx, seg_off);
+    dfree(ctx, lvl_acc);
+    dfree(ctx, lvl_cnt);
     dfree(ctx, perm); dfree(ctx, pseg); dfree(ctx, side); dfree(ctx, nperm); dfree(ctx, npseg);
     dfree(ctx, node_key); dfree(ctx, label_tmp); dfree(ctx, ones); dfree(ctx, dpos); dfree(ctx, err);
+    unsigned long long h_read[64] = {0};
+    if (rc == RAFTGP_OK) {
+        RG_CUDA(cudaMemcpyAsync(h_read, active + 2, sizeof(h_read), cudaMemcpyDeviceToHost, st));
+        RG_CUDA(cudaStreamSynchronize(st));
+    }
+    dfree(ctx, active);
     if (rc != RAFTGP_OK) return rc;
+    int64_t rows_read = 0;
+    for (int i = 0; i < 64; ++i) rows_read += (int64_t)h_read[i];
     *num_blocks = blocks;
     if (stats) {
         stats[0] = blocks;
         stats[1] = splits;
         stats[2] = lloyd_iters;
         stats[3] = levels;
+        stats[4] = lloyd_rows;   // rows of not-yet-converged segments visited by the Lloyd passes
+        stats[5] = seed_rows;    // rows visited per seeding pass (3 passes: mean, 2 x farthest)
+        stats[6] = rows_read;    // Z rows actually read by the Lloyd passes (the rest were pruned by bounds)
     }
     return RAFTGP_OK;
 }

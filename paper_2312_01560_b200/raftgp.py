@@ -413,7 +413,8 @@ def raftgp_model_select(g: Graph, Z: torch.Tensor, eps: int = 5, max_iter: int =
     if labels is None:
         labels = torch.empty(max(1, g.rows), dtype=torch.int32, device=g.ctx.device)[: g.rows]
     k = c_i32(0)
-    st = np.zeros(4, np.int64)
+    st = np.zeros(7, np.int64)
     _ck(load_library().raftgp_model_select(g.h, _ptr(Z.contiguous()), Z.shape[1], eps, max_iter, r, _ptr(labels),
                                            ctypes.byref(k), c_vp(st.ctypes.data)))
-    return labels, int(k.value), dict(zip(("blocks", "splits", "lloyd_iters", "levels"), (int(x) for x in st)))
+    return labels, int(k.value), dict(zip(("blocks", "splits", "lloyd_iters", "levels", "lloyd_rows", "seed_rows", "rows_read"),
+                                 (int(x) for x in st)))

@@ -175,3 +175,14 @@ def test_end_to_end_quality(rg, ctx):
         lab, K, _ = rg.raftgp_model_select(g, Z)
         aris.append(adjusted_rand_score(gr.labels, lab.cpu().numpy()))
     assert np.mean(aris) >= 0.75
+
+
+@pytest.mark.parametrize("max_iter", [1, 2, 3, 100])
+def test_parity_small_sweep(rg, ctx, max_iter):
+    """Many small graphs with ragged sizes (partial 32-row batches in every pass) and early Lloyd caps."""
+    for seed in range(24):
+        rng = np.random.default_rng(1000 + seed)
+        n = int(rng.integers(30, 400))
+        src, dst = synth.random_edges(n, 6 * n, seed=seed)
+        Z = _blob_Z(rng, n, 8, k=4, spread=0.7)
+        _check(*_both(rg, ctx, n, src, dst, Z, max_iter=max_iter))
