@@ -28,7 +28,7 @@
 namespace raftgp {
 namespace {
 
-constexpr int kEdgeRange = 16;   // rows per warp in the split-test pass
+constexpr int kIterChunk = 12;   // Lloyd iterations enqueued per host check
 
 __device__ __forceinline__ long long fixq(float z) { return __double2ll_rn(__dmul_rn((double)z, 4294967296.0)); }
 
@@ -332,13 +332,14 @@ __global__ void __launch_bounds__(kRowWarps * 32) sel_rows(const float *__restri
     if (MODE == 1 && lane == 0) atomicAdd(&rows_read[blockIdx.x & 63], (unsigned long long)(end - beg));
 }
 
-// Lloyd iteration t > 1 with exact pruning. Each warp scans kPruneRange consecutive positions: the bound test
+// Lloyd iteration t > 1 with exact pruning. Each warp scans `range` consecutive positions (a multiple of 128,
+// sized by the host so that the grid is one balanced wave of resident CTAs): the bound test
 // runs on every position (segment, side and bounds only: 24 B per row); positions that fail it are queued in
 // shared memory and recomputed 32 at a time with all lanes busy (a lane per row, rows bulk-copied into a
 // shared-memory stage). Rows that switch side then move their fixed-point values between the two sums
 // (exact integers), run-aggregated per segment.
 constexpr int kPruneWarps = 8;
-constexpr int kPruneRange = 1024;
+constexpr int kPruneMinRange = 512;
 
 template <int L>
 __global__ void __launch_bounds__(kPruneWarps * 32, 2) sel_lloyd_pruned(const float *__restrict__ Z,
@@ -346,7 +347,9 @@ __global__ void __launch_bounds__(kPruneWarps * 32, 2) sel_lloyd_pruned(const fl
                                                                       const int32_t *__restrict__ pseg,
                                                                       int32_t *__restrict__ side,
                                                                       float2 *__restrict__ bnd, int64_t n_act,
-                                                                      SegState st, unsigned long long *rows_read) {
+                                                                      SegState st, unsigned long long *rows_read,
+                                                                      const unsigned long long *__restrict__ prev_active,
+                                                                      int64_t range) {
     constexpr int LD = L + 4;
     constexpr uint32_t RB = 4u * L;
     extern __shared__ __align__(16) float sel_smem[];
@@ -356,9 +359,9 @@ __global__ void __launch_bounds__(kPruneWarps * 32, 2) sel_lloyd_pruned(const fl
     float *stage = sel_smem + (size_t)warp * 32 * LD;
     uint64_t *bar = &bars[warp];
     int *q = qbuf[warp];
-    const int64_t beg = ((int64_t)blockIdx.x * kPruneWarps + warp) * kPruneRange;
-    if (beg >= n_act) return;
-    const int64_t end = min(beg + (int64_t)kPruneRange, n_act);
+    const int64_t beg = ((int64_t)blockIdx.x * kPruneWarps + warp) * range;
+    if (beg >= n_act || prev_active[0] == 0) return;   // out of range, or every segment already converged
+    const int64_t end = min(beg + range, n_act);
     const unsigned lt = (1u << lane) - 1u;
     if (lane == 0) {
         mbar_init1(bar);
@@ -501,8 +504,9 @@ __global__ void sel_seed(const float *__restrict__ Z, SegState st, int S, int sl
 // passes update them incrementally.
 template <int L>
 __global__ void sel_update(SegState st, int S, int t, int max_iter, const int32_t *__restrict__ seg_off,
-                           unsigned long long *active) {
+                           const unsigned long long *__restrict__ prev_active, unsigned long long *active) {
     const int s = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    if (prev_active && prev_active[0] == 0) return;   // every segment converged at an earlier iteration
     if (s >= S || st.done[s]) return;
     if (t == 1) {   // slot 0 held the total over U; the t = 1 pass summed side 1 only
         for (int l = lane; l < L; l += 32) {
@@ -554,52 +558,78 @@ __global__ void sel_mark(const int32_t *__restrict__ perm, const int32_t *__rest
 }
 
 // Split-test statistics (SELECT_SPEC §4): per segment and side |U_r| and mbar_r; cut = edges from U_1
-// (side 0) rows into U_2 (side 1), counted once from the U_1 end. Warp per row, kEdgeRange rows per warp,
-// run-aggregated atomics.
-__global__ void sel_edges(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                          const int32_t *__restrict__ perm, const int32_t *__restrict__ pseg,
-                          const int32_t *__restrict__ side, int64_t n_act, const int32_t *__restrict__ node_key,
-                          unsigned long long *__restrict__ nsz, unsigned long long *__restrict__ mbar,
-                          unsigned long long *__restrict__ cut) {
-    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// (side 0) rows into U_2 (side 1), counted once from the U_1 end. A warp takes 32 consecutive positions, a
+// lane per row: rows of degree <= kLaneDeg are scanned by their own lane (32 rows' neighbour loads in flight
+// at once), longer rows by the whole warp (coalesced). Per-warp sums are reduced in registers and flushed
+// with one atomic per (segment, quantity) when the 32 rows share a segment, per lane otherwise.
+constexpr int kLaneDeg = 96;
+
+__global__ void __launch_bounds__(256) sel_edges(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                                                 const int32_t *__restrict__ perm, const int32_t *__restrict__ pseg,
+                                                 const int32_t *__restrict__ side, int64_t n_act,
+                                                 const int32_t *__restrict__ node_key,
+                                                 unsigned long long *__restrict__ nsz,
+                                                 unsigned long long *__restrict__ mbar,
+                                                 unsigned long long *__restrict__ cut) {
+    const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
-    const int64_t beg = w * kEdgeRange;
-    if (beg >= n_act) return;
-    const int64_t end = min(beg + (int64_t)kEdgeRange, n_act);
-    int cur = -1;
-    unsigned long long n0 = 0, n1 = 0, m0 = 0, m1 = 0, cu = 0;
-    auto flush = [&]() {
-        if (cur >= 0 && lane == 0) {
-            if (n0) atomicAdd(&nsz[cur * 2], n0);
-            if (n1) atomicAdd(&nsz[cur * 2 + 1], n1);
-            if (m0) atomicAdd(&mbar[cur * 2], m0);
-            if (m1) atomicAdd(&mbar[cur * 2 + 1], m1);
-            if (cu) atomicAdd(&cut[cur], cu);
-        }
-        n0 = n1 = m0 = m1 = cu = 0;
-    };
-    for (int64_t pos = beg; pos < end; ++pos) {
-        const int s = pseg[pos], c = side[pos], i = perm[pos];
-        if (s != cur) {
-            flush();
-            cur = s;
-        }
-        const int64_t rb = row_ptr[i], re = row_ptr[i + 1];
-        if (c) {
-            ++n1;
-            m1 += (unsigned long long)(re - rb);
-            continue;
-        }
-        ++n0;
-        m0 += (unsigned long long)(re - rb);
-        const int want = 2 * s + 1;
-        unsigned cnt = 0;
-        for (int64_t p = rb + lane; p < re; p += 32) cnt += (__ldg(node_key + __ldg(col + p)) == want);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        cu += cnt;
+    const bool valid = pos < n_act;
+    int s = -1, c = 0;
+    int64_t rb = 0, re = 0;
+    if (valid) {
+        s = pseg[pos];
+        c = side[pos];
+        const int i = perm[pos];
+        rb = row_ptr[i];
+        re = row_ptr[i + 1];
     }
-    flush();
+    const int64_t deg = re - rb;
+    const int want = 2 * s + 1;
+    unsigned cnt = 0;
+    const bool scan = valid && c == 0;
+    if (scan && deg <= kLaneDeg) {
+        int64_t p = rb;
+        for (; p + 4 <= re; p += 4) {
+            const int j0 = __ldg(col + p), j1 = __ldg(col + p + 1), j2 = __ldg(col + p + 2), j3 = __ldg(col + p + 3);
+            cnt += (__ldg(node_key + j0) == want) + (__ldg(node_key + j1) == want) + (__ldg(node_key + j2) == want) +
+                   (__ldg(node_key + j3) == want);
+        }
+        for (; p < re; ++p) cnt += (__ldg(node_key + __ldg(col + p)) == want);
+    }
+    for (unsigned m = __ballot_sync(0xffffffffu, scan && deg > kLaneDeg); m; m &= m - 1) {
+        const int r = __ffs(m) - 1;
+        const int64_t b0 = __shfl_sync(0xffffffffu, rb, r), e0 = __shfl_sync(0xffffffffu, re, r);
+        const int wr = __shfl_sync(0xffffffffu, want, r);
+        unsigned k = 0;
+        for (int64_t p = b0 + lane; p < e0; p += 32) k += (__ldg(node_key + __ldg(col + p)) == wr);
+        k = __reduce_add_sync(0xffffffffu, k);
+        if (lane == r) cnt += k;
+    }
+    const unsigned long long n0 = valid && c == 0, n1 = valid && c == 1;
+    const unsigned long long m0 = n0 ? (unsigned long long)deg : 0, m1 = n1 ? (unsigned long long)deg : 0;
+    const int s0 = __shfl_sync(0xffffffffu, s, 0);
+    if (__all_sync(0xffffffffu, s == s0) && s0 >= 0) {
+        const unsigned tn0 = __reduce_add_sync(0xffffffffu, (unsigned)n0);
+        const unsigned tn1 = __reduce_add_sync(0xffffffffu, (unsigned)n1);
+        unsigned long long tm0 = m0, tm1 = m1, tc = cnt;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            tm0 += __shfl_xor_sync(0xffffffffu, tm0, o);
+            tm1 += __shfl_xor_sync(0xffffffffu, tm1, o);
+            tc += __shfl_xor_sync(0xffffffffu, tc, o);
+        }
+        if (lane == 0) {
+            if (tn0) atomicAdd(&nsz[2 * s0], (unsigned long long)tn0);
+            if (tn1) atomicAdd(&nsz[2 * s0 + 1], (unsigned long long)tn1);
+            if (tm0) atomicAdd(&mbar[2 * s0], tm0);
+            if (tm1) atomicAdd(&mbar[2 * s0 + 1], tm1);
+            if (tc) atomicAdd(&cut[s0], tc);
+        }
+    } else if (valid) {
+        atomicAdd(&nsz[2 * s + c], 1ull);
+        if (deg) atomicAdd(&mbar[2 * s + c], (unsigned long long)deg);
+        if (cnt) atomicAdd(&cut[s], (unsigned long long)cnt);
+    }
 }
 
 // Thread per segment: exact split test, keep flag and kept size.
@@ -654,22 +684,37 @@ __global__ void sel_scatter(const int32_t *__restrict__ perm, const int32_t *__r
                             const int64_t *__restrict__ ones, const int32_t *__restrict__ keep,
                             const int64_t *__restrict__ krank, const int32_t *__restrict__ new_off, int32_t block_base,
                             int32_t *__restrict__ new_perm, int32_t *__restrict__ new_pseg,
-                            int32_t *__restrict__ label_tmp, int32_t *__restrict__ node_key) {
+                            int32_t *__restrict__ label_tmp, int32_t *__restrict__ node_key, int32_t *__restrict__ bmin) {
     const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (pos >= n_act) return;
-    const int s = pseg[pos], i = perm[pos];
-    if (!keep[s]) {
-        label_tmp[i] = block_base + (int32_t)(s - krank[s]);
-        node_key[i] = -1;
-        return;
+    const int lane = threadIdx.x & 31;
+    int blk = -1, i = INT_MAX;
+    if (pos < n_act) {
+        const int s = pseg[pos];
+        i = perm[pos];
+        if (!keep[s]) {
+            blk = block_base + (int32_t)(s - krank[s]);
+            label_tmp[i] = blk;
+            node_key[i] = -1;
+        } else {
+            const int64_t k = krank[s];
+            const int64_t o = ones[pos] - ones[seg_off[s]];
+            int64_t np;
+            if (side[pos]) np = new_off[2 * k + 1] + o;
+            else np = new_off[2 * k] + (pos - seg_off[s]) - o;
+            new_perm[np] = i;
+            new_pseg[np] = (int32_t)(2 * k + side[pos]);
+        }
     }
-    const int64_t k = krank[s];
-    const int64_t o = ones[pos] - ones[seg_off[s]];
-    int64_t np;
-    if (side[pos]) np = new_off[2 * k + 1] + o;
-    else np = new_off[2 * k] + (pos - seg_off[s]) - o;
-    new_perm[np] = i;
-    new_pseg[np] = (int32_t)(2 * k + side[pos]);
+    // smallest member of every finished block (canonical labels): one atomic per block run of the warp
+    const int b0 = __shfl_sync(0xffffffffu, blk, 0);
+    if (__all_sync(0xffffffffu, blk == b0)) {
+        if (b0 >= 0) {
+            const int mn = __reduce_min_sync(0xffffffffu, i);
+            if (lane == 0) atomicMin(&bmin[b0], mn);
+        }
+    } else if (blk >= 0) {
+        atomicMin(&bmin[blk], i);
+    }
 }
 
 __global__ void sel_init(int32_t *__restrict__ perm, int32_t *__restrict__ pseg, int32_t *__restrict__ node_key,
@@ -680,11 +725,6 @@ __global__ void sel_init(int32_t *__restrict__ perm, int32_t *__restrict__ pseg,
         pseg[i] = 0;
         node_key[i] = 0;
     }
-}
-
-__global__ void sel_block_min(const int32_t *__restrict__ label_tmp, int64_t n, int32_t *__restrict__ bmin) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) atomicMin(&bmin[label_tmp[i]], (int32_t)i);
 }
 
 __global__ void sel_first_flags(const int32_t *__restrict__ label_tmp, const int32_t *__restrict__ bmin, int64_t n,
@@ -716,12 +756,16 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
     constexpr size_t kRowSmem = (size_t)kRowWarps * 2 * 32 * (L + 4) * sizeof(float);
     constexpr size_t kPruneSmem = (size_t)kPruneWarps * 32 * (L + 4) * sizeof(float);
     static bool attrs = false;
+    static int prune_ctas = 1;
     if (!attrs) {
         RG_CUDA(cudaFuncSetAttribute(sel_rows<L, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem));
         RG_CUDA(cudaFuncSetAttribute(sel_rows<L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem));
         RG_CUDA(cudaFuncSetAttribute(sel_rows<L, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem));
         RG_CUDA(cudaFuncSetAttribute(sel_lloyd_pruned<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)kPruneSmem));
+        RG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&prune_ctas, sel_lloyd_pruned<L>, kPruneWarps * 32,
+                                                              kPruneSmem));
+        prune_ctas = std::max(1, prune_ctas);
         attrs = true;
     }
 
@@ -737,6 +781,8 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
     RG_TRY(dalloc_t(ctx, &npseg, n));
     RG_TRY(dalloc_t(ctx, &node_key, n));
     RG_TRY(dalloc_t(ctx, &label_tmp, n));
+    int32_t *bmin = nullptr;   // smallest member of each finished block (at most n blocks)
+    RG_TRY(dalloc_t(ctx, &bmin, n));
     RG_TRY(dalloc_t(ctx, &ones, n + 1));
     RG_TRY(dalloc_t(ctx, &dpos, n));
     float2 *bnd = reinterpret_cast<float2 *>(dpos);   // seeding distances, then the Lloyd pruning bounds
@@ -747,6 +793,10 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
     {
         LaunchScope LS(ctx, K_SELECT);
         sel_init<<<grid_for(n, 256), 256, 0, st>>>(perm, pseg, node_key, n);
+    }
+    {
+        LaunchScope LS(ctx, K_SELECT);
+        fill_i32<<<grid_for(n, 256), 256, 0, st>>>(bmin, n, INT_MAX);
     }
     RG_CHECK_LAUNCH(ctx);
 
@@ -760,7 +810,9 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
     int32_t blocks = 0;
     int64_t splits = 0, lloyd_iters = 0, levels = 0, lloyd_rows = 0, seed_rows = 0, act_rows = 0;
     int32_t h_small[2] = {0, 0};
-    unsigned long long h_act[2] = {0, 0};
+    std::vector<unsigned long long> h_iter(2 * ((size_t)max_iter + 1), 0);
+    unsigned long long *iter_act = nullptr;   // [t][2]: active segments / rows after update t
+    RG_TRY(dalloc_t(ctx, &iter_act, 2 * ((size_t)max_iter + 1)));
     int64_t h_two[2] = {0, 0};
     raftgp_status rc = RAFTGP_OK;
     // per-level [S][2][L] side sums and [S][2] counts; level 1 fills slot 0 with a mean pass, deeper levels
@@ -797,7 +849,10 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
         RG_CUDA(cudaMemsetAsync(nsz, 0, sizeof(unsigned long long) * (size_t)S * 5, st));
 
         const unsigned rgrid = grid_for(ceil_div(n_act, kRowRange), kRowWarps);
-        const unsigned qgrid = grid_for(ceil_div(n_act, kPruneRange), kPruneWarps);
+        // pruned passes: one balanced wave of resident CTAs, each warp a contiguous range (multiple of 128)
+        const int64_t q_warps = (int64_t)ctx->sm_count * prune_ctas * kPruneWarps;
+        const int64_t q_range = std::max<int64_t>(kPruneMinRange, ceil_div(ceil_div(n_act, q_warps), 128) * 128);
+        const unsigned qgrid = grid_for(ceil_div(n_act, q_range), kPruneWarps);
         act_rows = n_act;
         seed_rows += n_act;
         const unsigned sgrid = grid_for((int64_t)S * 32, 256);
@@ -839,30 +894,43 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
             }
             RG_CHECK_LAUNCH(ctx);
         }
-        // Lloyd iterations, all segments in lock step (converged ones frozen)
-        for (int t = 1; t <= max_iter && rc == RAFTGP_OK; ++t) {
-            ++lloyd_iters;
-            lloyd_rows += act_rows;
-            {
-                LaunchScope LS(ctx, K_SEL_LLOYD);
-                if (t == 1)
-                    sel_rows<L, 1><<<rgrid, kRowWarps * 32, kRowSmem, st>>>(Z, perm, pseg, side, bnd, dpos, n_act, ss,
-                                                                            err, active + 2);
-                else
-                    sel_lloyd_pruned<L><<<qgrid, kPruneWarps * 32, kPruneSmem, st>>>(Z, perm, pseg, side, bnd, n_act,
-                                                                                   ss, active + 2);
+        // Lloyd iterations, all segments in lock step (converged ones frozen). Iterations are enqueued in chunks
+        // of kIterChunk without host round trips: update t counts the still-active segments (and their rows)
+        // into iter_act[t], and the kernels of iteration t + 1 exit at once when that count is 0. The host
+        // reads the counters once per chunk.
+        RG_CUDA(cudaMemsetAsync(iter_act, 0, sizeof(unsigned long long) * 2 * ((size_t)max_iter + 1), st));
+        for (int t0 = 1; t0 <= max_iter && rc == RAFTGP_OK; t0 += kIterChunk) {
+            const int t1 = std::min(max_iter, t0 + kIterChunk - 1);
+            for (int t = t0; t <= t1; ++t) {
+                const unsigned long long *prev = t > 1 ? iter_act + 2 * (t - 1) : nullptr;
+                {
+                    LaunchScope LS(ctx, K_SEL_LLOYD);
+                    if (t == 1)
+                        sel_rows<L, 1><<<rgrid, kRowWarps * 32, kRowSmem, st>>>(Z, perm, pseg, side, bnd, dpos, n_act,
+                                                                                ss, err, active + 2);
+                    else
+                        sel_lloyd_pruned<L><<<qgrid, kPruneWarps * 32, kPruneSmem, st>>>(Z, perm, pseg, side, bnd,
+                                                                                       n_act, ss, active + 2, prev,
+                                                                                       q_range);
+                }
+                RG_CHECK_LAUNCH(ctx);
+                {
+                    LaunchScope LS(ctx, K_SEL_LLOYD);
+                    sel_update<L><<<sgrid, 256, 0, st>>>(ss, S, t, max_iter, seg_off, prev, iter_act + 2 * t);
+                }
+                RG_CHECK_LAUNCH(ctx);
             }
-            RG_CHECK_LAUNCH(ctx);
-            RG_CUDA(cudaMemsetAsync(active, 0, 2 * sizeof(unsigned long long), st));
-            {
-                LaunchScope LS(ctx, K_SEL_LLOYD);
-                sel_update<L><<<sgrid, 256, 0, st>>>(ss, S, t, max_iter, seg_off, active);
-            }
-            RG_CHECK_LAUNCH(ctx);
-            RG_CUDA(cudaMemcpyAsync(h_act, active, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+            RG_CUDA(cudaMemcpyAsync(h_iter.data() + 2 * t0, iter_act + 2 * t0,
+                                    sizeof(unsigned long long) * 2 * (size_t)(t1 - t0 + 1), cudaMemcpyDeviceToHost, st));
             RG_CUDA(cudaStreamSynchronize(st));
-            act_rows = (int64_t)h_act[1];
-            if (h_act[0] == 0) break;
+            bool stop = false;
+            for (int t = t0; t <= t1 && !stop; ++t) {
+                ++lloyd_iters;
+                lloyd_rows += act_rows;
+                act_rows = (int64_t)h_iter[2 * t + 1];
+                stop = h_iter[2 * t] == 0;
+            }
+            if (stop) break;
         }
         if (rc != RAFTGP_OK) {
             dfree(ctx, ss.mu); dfree(ctx, ss.dmax); dfree(ctx, ss.amin); dfree(ctx, ss.changed); dfree(ctx, ss.done);
@@ -878,7 +946,7 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
         RG_CHECK_LAUNCH(ctx);
         {
             LaunchScope LS(ctx, K_SEL_SPLIT);
-            sel_edges<<<grid_for(ceil_div(n_act, kEdgeRange) * 32, 256), 256, 0, st>>>(
+            sel_edges<<<grid_for(n_act, 256), 256, 0, st>>>(
                 g->row_ptr, g->col, perm, pseg, side, n_act, node_key, nsz, mbar, cut);
         }
         RG_CHECK_LAUNCH(ctx);
@@ -909,7 +977,8 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
         {
             LaunchScope LS(ctx, K_SEL_SPLIT);
             sel_scatter<<<grid_for(n_act, 256), 256, 0, st>>>(perm, pseg, side, n_act, seg_off, ones, keep, krank,
-                                                              new_off, blocks, nperm, npseg, label_tmp, node_key);
+                                                              new_off, blocks, nperm, npseg, label_tmp, node_key,
+                                                              bmin);
         }
         RG_CHECK_LAUNCH(ctx);
         RG_CUDA(cudaMemcpyAsync(&h_two[0], krank + S, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -933,17 +1002,8 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
     }
     if (rc == RAFTGP_OK && n > 0) {
         // canonical labels: blocks ordered by their smallest member (SELECT_SPEC §5)
-        int32_t *bmin = nullptr, *first = nullptr;
-        RG_TRY(dalloc_t(ctx, &bmin, std::max<int32_t>(1, blocks)));
+        int32_t *first = nullptr;
         RG_TRY(dalloc_t(ctx, &first, n));
-        {
-            LaunchScope LS(ctx, K_SELECT);
-            fill_i32<<<grid_for(blocks, 256), 256, 0, st>>>(bmin, blocks, INT_MAX);
-        }
-        {
-            LaunchScope LS(ctx, K_SELECT);
-            sel_block_min<<<grid_for(n, 256), 256, 0, st>>>(label_tmp, n, bmin);
-        }
         {
             LaunchScope LS(ctx, K_SELECT);
             sel_first_flags<<<grid_for(n, 256), 256, 0, st>>>(label_tmp, bmin, n, first);
@@ -956,14 +1016,14 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
         }
         RG_CHECK_LAUNCH(ctx);
         RG_CUDA(cudaStreamSynchronize(st));
-        dfree(ctx, bmin);
         dfree(ctx, first);
     }
     dfree(ctx, seg_off);
     dfree(ctx, lvl_acc);
     dfree(ctx, lvl_cnt);
+    dfree(ctx, iter_act);
     dfree(ctx, perm); dfree(ctx, pseg); dfree(ctx, side); dfree(ctx, nperm); dfree(ctx, npseg);
-    dfree(ctx, node_key); dfree(ctx, label_tmp); dfree(ctx, ones); dfree(ctx, dpos); dfree(ctx, err);
+    dfree(ctx, node_key); dfree(ctx, label_tmp); dfree(ctx, bmin); dfree(ctx, ones); dfree(ctx, dpos); dfree(ctx, err);
     unsigned long long h_read[64] = {0};
     if (rc == RAFTGP_OK) {
         RG_CUDA(cudaMemcpyAsync(h_read, active + 2, sizeof(h_read), cudaMemcpyDeviceToHost, st));
