@@ -342,7 +342,7 @@ constexpr int kPruneWarps = 8;
 constexpr int kPruneMinRange = 512;
 
 template <int L>
-__global__ void __launch_bounds__(kPruneWarps * 32, 2) sel_lloyd_pruned(const float *__restrict__ Z,
+__global__ void __launch_bounds__(kPruneWarps * 32, 3) sel_lloyd_pruned(const float *__restrict__ Z,
                                                                       const int32_t *__restrict__ perm,
                                                                       const int32_t *__restrict__ pseg,
                                                                       int32_t *__restrict__ side,
