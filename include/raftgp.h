@@ -232,6 +232,15 @@ RAFTGP_API raftgp_status raftgp_model_select(raftgp_graph g, const float *Z_dev,
                                              int32_t max_iter, int32_t rule, int32_t *labels_dev, int32_t *num_blocks,
                                              int64_t *stats);
 
+/* ---------------------------------------------------------------- NEXT-2: tensor-core GEMM
+ * C = diag(row_scale) A B on the tcgen05 tensor cores, fp32-accurate by the 3xTF32 split (error ~2^-20
+ * relative): the dense transforms of Eq. 6 at the paper's Table I widths and Theta W^(1).
+ *   A_dev: device fp32 M x K row-major; B_dev: device fp32 K x N row-major; row_scale_dev: device fp32[M] or
+ *   NULL (= 1); C_dev: device fp32 M x N row-major (rows 16-byte aligned for the vectorised epilogue).
+ * Workspace (hi / lo tiles of A and B) from the context pool. Errors: PARAM (sizes, null pointers). */
+RAFTGP_API raftgp_status raftgp_gemm_tf32x3(raftgp_ctx ctx, int64_t M, int32_t K, int32_t N, const float *A_dev,
+                                            const float *B_dev, const float *row_scale_dev, float *C_dev);
+
 #ifdef __cplusplus
 }
 #endif

@@ -244,3 +244,20 @@ def split_stops(g: CSR, members, side, eps: int = 5, rule=0) -> bool:
     return bool(_L().oracle_split_stops(_p(g.row_ptr), _p(g.col), ctypes.c_int64(int(g.row_ptr[-1])), _p(U),
                                         ctypes.c_int64(U.size), _p(sd), ctypes.c_int32(eps), ctypes.c_int32(rule),
                                         _p(where)))
+
+
+# ------------------------------------------------------------------ NEXT-2: Table I widths
+def gcn_np(g: CSR, dims, seed: int, Y: np.ndarray):
+    """Eq. 6 + row l2 normalisation for wide layers (Table I), the same
+    steps as oracle_gcn but with numpy's fp64 matmul as the dense product (a library primitive) so that
+    4096-wide stacks finish in seconds: Z^(k) = rownorm(tanh((P Z^(k-1)) W^(k))), P applied by oracle_apply.
+    Pinned against the C oracle_gcn at small widths (tests/test_oracle_graph_ops.py)."""
+    Z = np.ascontiguousarray(Y, np.float64)
+    out = []
+    for k in range(1, len(dims)):
+        W = weights(k, int(dims[k - 1]), int(dims[k]), seed).astype(np.float64)
+        H = np.tanh(apply(g, PROP, Z) @ W)
+        nrm = np.sqrt((H * H).sum(axis=1))
+        Z = np.where(nrm[:, None] > 0, H / np.where(nrm > 0, nrm, 1.0)[:, None], 0.0)
+        out.append(Z)
+    return out

@@ -18,7 +18,7 @@ namespace raftgp {
 
 const char *const kKernelNames[K_NUM] = {
     "csr_count", "scan", "csr_scatter", "csr_sort_warp", "csr_sort_block", "csr_compact", "degree_scalars",
-    "sketch", "g_partials", "g_final", "feature_hop", "transform", "gcn_hop", "hop_generic", "misc", "csr_partition", "csr_bucket_sort", "row_order", "model_select", "select_seed", "select_lloyd", "select_split"};
+    "sketch", "g_partials", "g_final", "feature_hop", "transform", "gcn_hop", "hop_generic", "misc", "csr_partition", "csr_bucket_sort", "row_order", "model_select", "select_seed", "select_lloyd", "select_split", "gemm_tf32x3", "gemm_tile", "wide_hop"};
 
 static thread_local std::string g_last_error;
 
@@ -627,6 +627,8 @@ raftgp_status raftgp_embed_multi(raftgp_graph g, int32_t nvariants, const int32_
     RG_TRY(set_device(g->ctx));
     raftgp_ctx ctx = g->ctx;
     const int32_t r = dims[0];
+    if (Y_dev == nullptr && wide_supported(layers, dims))
+        return embed_wide(g, nvariants, variants, layers, dims, seed, Z_dev, where);
     if (Y_dev == nullptr && sketch_w_supported(r, dims[1]))
         return embed_pre(g, nvariants, variants, layers, dims, seed, Z_dev, where);
     float *theta = nullptr, *W1 = nullptr;
@@ -815,6 +817,18 @@ raftgp_status raftgp_model_select(raftgp_graph g, const float *Z_dev, int32_t L,
         return RAFTGP_OK;
     }
     return model_select(g, Z_dev, L, eps, max_iter, rule, labels_dev, num_blocks, stats);
+    RG_GUARD_END
+}
+
+// ---------------------------------------------------------------- NEXT-2: tensor-core GEMM
+raftgp_status raftgp_gemm_tf32x3(raftgp_ctx ctx, int64_t M, int32_t K, int32_t N, const float *A_dev, const float *B_dev,
+                                 const float *row_scale_dev, float *C_dev) {
+    RG_GUARD_BEGIN
+    if (!ctx) return fail(RAFTGP_ERR_PARAM, "null context");
+    if (M < 0 || K <= 0 || N <= 0) return fail(RAFTGP_ERR_PARAM, "M must be >= 0, K and N > 0");
+    if (M > 0 && (!A_dev || !B_dev || !C_dev)) return fail(RAFTGP_ERR_PARAM, "null A, B or C");
+    RG_TRY(set_device(ctx));
+    return gemm_rowmajor(ctx, A_dev, M, K, B_dev, N, row_scale_dev, C_dev);
     RG_GUARD_END
 }
 

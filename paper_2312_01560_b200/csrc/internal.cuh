@@ -38,6 +38,9 @@ enum KernelId : int {
     K_SEL_SEED,
     K_SEL_LLOYD,
     K_SEL_SPLIT,
+    K_GEMM,
+    K_GEMM_TILE,
+    K_WIDE_HOP,
     K_NUM
 };
 extern const char *const kKernelNames[K_NUM];
@@ -171,6 +174,21 @@ raftgp_status gcn_hop(raftgp_graph g, const float *Tfull, int32_t w, float *Zout
 // last GCN hop of two variants over the interleaved operand [T_a | T_b] (n x 2d); d in {32, 64}
 bool gcn_pair_supported(int32_t d);
 raftgp_status gcn_final_pair(raftgp_graph g, const float *Tboth, int32_t d, float *Za, float *Zb);
+// NEXT-2: tensor-core 3xTF32 GEMM on pre-split, pre-tiled operands (wide.cu)
+int gemm_nt(int N);
+int64_t gemm_pad_rows(int64_t M);
+int gemm_pad_k(int K);
+raftgp_status gemm_tile_a(raftgp_ctx ctx, const float *X, int64_t M, int K, int64_t ldx, float *hi, float *lo);
+raftgp_status gemm_tile_b(raftgp_ctx ctx, const float *W, int K, int N, float *hi, float *lo);
+raftgp_status gemm_theta_tiles(raftgp_ctx ctx, uint64_t seed, int64_t n, int32_t r, float *hi, float *lo);
+raftgp_status gemm_tiled(raftgp_ctx ctx, const float *Ahi, const float *Alo, const float *Bhi, const float *Blo,
+                         int64_t M, int K, int N, const float *row_scale, float *C, int64_t ldc);
+raftgp_status gemm_rowmajor(raftgp_ctx ctx, const float *A, int64_t M, int K, const float *B, int N,
+                            const float *row_scale, float *C);
+// Table I widths: the whole embedding with tensor-core transforms and wide hops (Y not materialised)
+bool wide_supported(int32_t layers, const int32_t *dims);
+raftgp_status embed_wide(raftgp_graph g, int32_t nvariants, const int32_t *variants, int32_t layers,
+                         const int32_t *dims, uint64_t seed, float *const *Z_dev, const int where[3]);
 // NEXT-1: Alg. 1 hierarchical model selection (select.cu)
 raftgp_status model_select(raftgp_graph g, const float *Z, int32_t L, int32_t eps, int32_t max_iter, int32_t rule,
                            int32_t *labels, int32_t *num_blocks, int64_t *stats);

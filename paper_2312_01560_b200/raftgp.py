@@ -35,7 +35,7 @@ EXPORTS = (
     "raftgp_graph_local_degrees", "raftgp_graph_set_degrees", "raftgp_graph_set_order", "raftgp_graph_destroy", "raftgp_sketch",
     "raftgp_weights", "raftgp_project", "raftgp_gcn_transform", "raftgp_gcn_hop", "raftgp_gnn_embed",
     "raftgp_embed", "raftgp_embed_multi", "raftgp_feature_transform", "raftgp_modularity", "raftgp_ncut", "raftgp_local_modularity",
-    "raftgp_model_select",
+    "raftgp_model_select", "raftgp_gemm_tf32x3",
 )
 
 _lib = None
@@ -86,6 +86,7 @@ _SIGS = {
     "raftgp_ncut": (ctypes.c_int, [c_vp, c_vp, c_i32, P(c_dbl)]),
     "raftgp_local_modularity": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_i32, P(c_dbl)]),
     "raftgp_model_select": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, P(c_i32), c_vp]),
+    "raftgp_gemm_tf32x3": (ctypes.c_int, [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
 }
 
 
@@ -418,3 +419,18 @@ def raftgp_model_select(g: Graph, Z: torch.Tensor, eps: int = 5, max_iter: int =
                                            ctypes.byref(k), c_vp(st.ctypes.data)))
     return labels, int(k.value), dict(zip(("blocks", "splits", "lloyd_iters", "levels", "lloyd_rows", "seed_rows", "rows_read"),
                                  (int(x) for x in st)))
+
+
+# ------------------------------------------------------------------ NEXT-2: tensor-core GEMM
+def raftgp_gemm_tf32x3(ctx: Context, A: torch.Tensor, B: torch.Tensor, row_scale: Optional[torch.Tensor] = None,
+                       C: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """C = diag(row_scale) A B (fp32-accurate 3xTF32 on the tcgen05 tensor cores)."""
+    M, K = A.shape
+    K2, N = B.shape
+    if K != K2:
+        raise ValueError("inner dimensions differ")
+    if C is None:
+        C = torch.empty((M, N), dtype=torch.float32, device=ctx.device)
+    _ck(load_library().raftgp_gemm_tf32x3(ctx.h, M, K, N, _ptr(A.contiguous()), _ptr(B.contiguous()),
+                                          _ptr(row_scale), _ptr(C)))
+    return C

@@ -357,3 +357,15 @@ def test_local_modularity(seed):
     e = mbar.sum() / 2
     ref = float(np.sum(m / e - (mbar / (2 * e)) ** 2))
     assert abs(oracle.local_modularity(g, U, b, 2) - ref) < 1e-12
+
+
+@pytest.mark.parametrize("dims", [(64, 64, 32), (32, 48, 16, 8)])
+def test_gcn_np_matches_c_oracle(dims):
+    """The numpy-matmul GCN used for Table I widths equals the C oracle's loops (same steps, fp64)."""
+    gr = synth.generate("C1", 2)
+    g = oracle.build_csr(gr.n, gr.src, gr.dst)
+    Y = oracle.project(g, "mod", dims[0], 0)
+    ref = oracle.gcn(g, dims, 0, Y)
+    got = oracle.gcn_np(g, dims, 0, Y)
+    for a, b in zip(got, ref):
+        assert np.max(np.abs(a - b)) <= 1e-12
