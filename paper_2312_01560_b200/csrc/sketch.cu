@@ -52,7 +52,8 @@ __global__ void __launch_bounds__(128) g_partials(const float *__restrict__ thet
                                                   int64_t n, int32_t r, double *__restrict__ partial) {
     const int64_t chunk = blockIdx.x;
     const int64_t j0 = chunk * kGChunk, j1 = min(n, j0 + (int64_t)kGChunk);
-    for (int c = threadIdx.x; c < r; c += blockDim.x) {
+    // blockIdx.y picks a 128-column slice (wide operands); each (chunk, column) sum stays sequential in j
+    for (int c = blockIdx.y * blockDim.x + threadIdx.x; c < r; c += gridDim.y * blockDim.x) {
         double acc = 0.0;
         for (int64_t j = j0; j < j1; ++j) acc += static_cast<double>(deg[j]) * static_cast<double>(theta[j * r + c]);
         partial[chunk * r + c] = acc;
@@ -220,7 +221,8 @@ raftgp_status g_reduce(raftgp_graph g, const float *theta, int32_t r, double *g_
     RG_TRY(dalloc_t(ctx, &partial, (size_t)nchunks * r));
     {
         LaunchScope L(ctx, K_SKETCH_G);
-        g_partials<<<(unsigned)nchunks, 128, 0, ctx->stream>>>(theta, g->deg_all, g->n, r, partial);
+        g_partials<<<dim3((unsigned)nchunks, (unsigned)ceil_div(r, 128)), 128, 0, ctx->stream>>>(theta, g->deg_all, g->n,
+                                                                                                r, partial);
     }
     RG_CHECK_LAUNCH(ctx);
     {

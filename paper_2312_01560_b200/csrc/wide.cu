@@ -254,6 +254,7 @@ struct WideArgs {
     float *out;              // feature kinds: T = s^ (.) y (n x W); GCN: Z row-major (may be null)
     float *out2;             // W_DUAL: the MOD variant's T
     float *zhi, *zlo;        // GCN: Z split and tiled as the next GEMM's A operand (may be null)
+    float *ssq;              // GCN, deferred normalisation: per-row, per-slice sums of squares (n x NW) or null
 };
 
 template <int KIND, int V, int U>
@@ -326,17 +327,22 @@ __global__ void __launch_bounds__(128) hop_wide(WideArgs a) {
             }
 #pragma unroll
             for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-            if (NW > 1) {
-                if (lane == 0) ssq[wib] = ss;
-                __syncthreads();
-                ss = 0.f;
-                for (int q = 0; q < NW; ++q) ss += ssq[rsub * NW + q];
-                __syncthreads();
-            }
-            if (ss > 0.f) {
-                const float nrm = sqrtf(ss);
+            if (a.ssq) {
+                // deferred: the row's 1/||y|| is folded into the next GEMM's row scale (no CTA barrier here)
+                if (valid && lane == 0) a.ssq[i * NW + slice] = ss;
+            } else {
+                if (NW > 1) {
+                    if (lane == 0) ssq[wib] = ss;
+                    __syncthreads();
+                    ss = 0.f;
+                    for (int q = 0; q < NW; ++q) ss += ssq[rsub * NW + q];
+                    __syncthreads();
+                }
+                if (ss > 0.f) {
+                    const float nrm = sqrtf(ss);
 #pragma unroll
-                for (int v = 0; v < V; ++v) y[v] = make_float4(y[v].x / nrm, y[v].y / nrm, y[v].z / nrm, y[v].w / nrm);
+                    for (int v = 0; v < V; ++v) y[v] = make_float4(y[v].x / nrm, y[v].y / nrm, y[v].z / nrm, y[v].w / nrm);
+                }
             }
         } else if (valid) {
             const float shi = __ldg(a.sh_all + i);
@@ -391,6 +397,23 @@ __global__ void __launch_bounds__(128) hop_wide(WideArgs a) {
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, ceil_div(n, t)); }
 
+// Row scale of the GEMM after a deferred-normalisation hop: s^_i / ||y_i|| (y_i = 0 rows keep s^_i).
+__global__ void wide_row_scale(const float *__restrict__ ssq, int nw, int64_t n, const float *__restrict__ sh,
+                               float *__restrict__ scale) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float ss = 0.f;
+    for (int q = 0; q < nw; ++q) ss += ssq[i * nw + q];
+    scale[i] = ss > 0.f ? sh[i] / sqrtf(ss) : sh[i];
+}
+
+#ifndef RG_WIDE_U
+#define RG_WIDE_U 4
+#endif
+#ifndef RG_WIDE_U_DUAL
+#define RG_WIDE_U_DUAL 2
+#endif
+
 bool wide_width(int32_t w) { return w == 256 || w == 512 || w == 1024 || w == 2048; }
 
 template <int KIND>
@@ -402,8 +425,10 @@ raftgp_status launch_wide(raftgp_ctx ctx, const WideArgs &a) {
     const int64_t per_sm = 16;   // 128-thread CTAs per SM in the grid (grid-stride over rows)
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.n, rpc), ctx->sm_count * per_sm));
     LaunchScope LS(ctx, K_WIDE_HOP);
-    if (V == 2) hop_wide<KIND, 2, 4><<<grid, 128, 0, ctx->stream>>>(a);
-    else hop_wide<KIND, 4, 2><<<grid, 128, 0, ctx->stream>>>(a);
+    // neighbours in flight per lane: U x V float4 (DUAL keeps two accumulator sets, so a smaller U)
+    constexpr int U4 = KIND == W_DUAL ? RG_WIDE_U_DUAL : RG_WIDE_U;
+    if (V == 2) hop_wide<KIND, 2, 2 * U4><<<grid, 128, 0, ctx->stream>>>(a);
+    else hop_wide<KIND, 4, U4><<<grid, 128, 0, ctx->stream>>>(a);
     return RAFTGP_OK;
 }
 
@@ -637,7 +662,7 @@ raftgp_status embed_wide(raftgp_graph g, int32_t nvariants, const int32_t *varia
             if (w <= 128 && (last || wn <= 128)) {
                 st = gcn_hop(g, T, w, last ? Z_dev[v] : nullptr, last ? nullptr : Wrm[k + 1], wn, Tn);
             } else {
-                float *zhi = nullptr, *zlo = nullptr;
+                float *zhi = nullptr, *zlo = nullptr, *rscale = nullptr;
                 if (!last) {
                     st = take(reinterpret_cast<void **>(&zhi), (size_t)Mp * w * 4);
                     if (st == RAFTGP_OK) st = take(reinterpret_cast<void **>(&zlo), (size_t)Mp * w * 4);
@@ -660,11 +685,25 @@ raftgp_status embed_wide(raftgp_graph g, int32_t nvariants, const int32_t *varia
                     WideArgs a{};
                     a.n = n; a.row_ptr = g->row_ptr; a.col = g->col; a.X = T; a.s_all = g->s_all; a.sh_all = g->sh_all;
                     a.deg_all = g->deg_all; a.W = w; a.out = last ? Z_dev[v] : nullptr; a.zhi = zhi; a.zlo = zlo;
-                    st = launch_wide<W_GCN>(ctx, a);
+                    const int nw = w / (128 * (w == 256 ? 2 : 4));
+                    if (!last) {   // deferred row normalisation: y = tanh(.) tiled, 1/||y|| goes to the GEMM row scale
+                        st = take(reinterpret_cast<void **>(&a.ssq), (size_t)n * nw * 4);
+                        if (st == RAFTGP_OK) st = take(reinterpret_cast<void **>(&rscale), (size_t)n * 4);
+                    }
+                    if (st == RAFTGP_OK) st = launch_wide<W_GCN>(ctx, a);
                     if (st == RAFTGP_OK) { RG_CHECK_LAUNCH(ctx); }
+                    if (st == RAFTGP_OK && !last) {
+                        {
+                            LaunchScope LS(ctx, K_WIDE_HOP);
+                            wide_row_scale<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(a.ssq, nw, n, g->sh_all, rscale);
+                        }
+                        RG_CHECK_LAUNCH(ctx);
+                    }
+                    if (a.ssq) release(a.ssq);
                 }
                 if (st == RAFTGP_OK && !last)
-                    st = gemm_tiled(ctx, zhi, zlo, Bhi[k + 1], Blo[k + 1], n, w, wn, g->sh_all, Tn, wn);
+                    st = gemm_tiled(ctx, zhi, zlo, Bhi[k + 1], Blo[k + 1], n, w, wn, rscale ? rscale : g->sh_all, Tn, wn);
+                if (rscale) release(rscale);
                 if (zhi) release(zhi);
                 if (zlo) release(zlo);
             }
