@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-select", action="store_true", help="skip the NEXT-1 model-selection measurement")
     ap.add_argument("--select-reps", type=int, default=3)
+    ap.add_argument("--no-table1", action="store_true", help="skip the NEXT-2 Table I widths measurement")
+    ap.add_argument("--table1-steps", type=int, default=3)
     ap.add_argument("--clock-period-ms", type=int, default=200)
     ap.add_argument("--clock-query", default=None)
     ap.add_argument("--no-clocks", action="store_true")
@@ -268,6 +270,81 @@ def measure_select(args, rg, ctx, gr, src_d, dst_d, variants, dims, Zbuf, barrie
     return out
 
 
+TABLE1_DIMS = (4096, 2048, 1024, 512, 256)   # PAPER.md:268-273, Table I row 2E5 (and 1E4-1E5)
+
+
+def measure_table1(args, rg, dev, barrier, peak, peak_src):
+    """NEXT-2: the embedding at the paper's Table I widths on the C3 DC-SBM graph (N = 2E5, the largest Table I
+    size): one step = CSR build + raftgp_embed_multi(ncut, mod, dims 4096-2048-1024-512-256), inputs resident.
+    Reports nnz*w/s over the gathered widths actually used (Theta W1 is formed before aggregation, so the
+    feature hop gathers dims[1]), the wide-hop HBM roofline (gather-model bytes) and the tensor-core GEMM rate
+    (fp32-accurate flops; each is 3 TF32 MMA flops) against the TF32 dense peak."""
+    import torch
+    import synth
+    cfg = synth.CONFIGS["C3"]
+    gr = synth.generate(cfg, args.seed, rule=args.rule)
+    dims = TABLE1_DIMS
+    variants = ["ncut", "mod"]
+    src, dst = torch.from_numpy(gr.src).to(dev), torch.from_numpy(gr.dst).to(dev)
+    ctx = rg.Context(dev.index)
+    Z = {v: torch.empty((gr.n, dims[-1]), dtype=torch.float32, device=dev) for v in variants}
+
+    def step():
+        g = rg.raftgp_build_csr(ctx, gr.n, src, dst)
+        rg.raftgp_embed_multi(g, variants, dims, args.seed, Z=Z)
+        nnz = g.info()["nnz_local"]
+        g.close()
+        return nnz
+
+    for _ in range(2):
+        nnz = step()
+    ctx.prof_reset()
+    ctx.set_profiling(True)
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(ctx.stream)
+    for _ in range(args.table1_steps):
+        step()
+    e1.record(ctx.stream)
+    barrier()
+    ms = e0.elapsed_time(e1) / args.table1_steps
+    prof = {k: (t / args.table1_steps, c / args.table1_steps) for k, (t, c) in ctx.prof_read().items()}
+    ctx.set_profiling(False)
+    n, L = gr.n, len(dims) - 1
+    units = nnz * dims[1] + len(variants) * sum((nnz + n) * dims[k] for k in range(1, L + 1))
+    # wide-hop gather-model bytes per step: the dual feature hop + every GCN hop wider than 128
+    hop_b = 8 * (n + 1) + 4 * nnz + 4 * dims[1] * nnz + 2 * 4 * dims[1] * n + 4 * n
+    for k in range(1, L + 1):
+        w = dims[k]
+        if w > 128:
+            out_b = 4 * w * n if k == L else 2 * 4 * w * n + 4 * n * max(1, w // 512)
+            hop_b += len(variants) * (8 * (n + 1) + 4 * nnz + 4 * w * (nnz + n) + out_b + 4 * n)
+    flops = 2.0 * n * dims[0] * dims[1] + len(variants) * sum(2.0 * n * dims[k] * dims[k + 1] for k in range(1, L))
+    hop_ms = prof.get("wide_hop", (0.0, 0))[0]
+    gemm_ms = prof.get("gemm_tf32x3", (0.0, 0))[0]
+    try:
+        bf16 = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])
+        tf32_peak, tf32_src = 0.5 * bf16, "MEASURED_PEAKS.json bf16_tflops x 0.5 (nominal TF32:BF16 ratio)"
+    except Exception:
+        tf32_peak, tf32_src = 1125.0, "nominal 2.25 PFLOP/s bf16 x 0.5"
+    hop_gbs = hop_b / (hop_ms * 1e-3) / 1e9 if hop_ms else None
+    mma_tflops = 3 * flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None
+    return {
+        "workload": f"T1-2E5: C3 DC-SBM graph (N={n:,}, nnz={nnz:,}) with Table I widths {list(dims)} "
+                    f"(PAPER.md:268-273), variants ncut+mod",
+        "steps": args.table1_steps, "ms_per_step": ms, "value": units / (ms * 1e-3), "unit": UNIT,
+        "kernel_ms": {k: round(t, 3) for k, (t, _) in sorted(prof.items(), key=lambda x: -x[1][0])},
+        "wide_hop_roofline": {"bound": "hbm", "achieved": hop_gbs, "peak": peak, "unit": "GB/s",
+                              "frac": hop_gbs / peak if hop_gbs else None, "peak_source": peak_src,
+                              "bytes_per_step": hop_b},
+        "gemm_roofline": {"bound": "tensor", "fp32_tflops": flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None,
+                          "achieved": mma_tflops, "peak": tf32_peak, "unit": "TFLOP/s (TF32 MMA, 3 per fp32 flop)",
+                          "frac": mma_tflops / tf32_peak if mma_tflops else None, "peak_source": tf32_src,
+                          "fp32_flops_per_step": flops},
+    }
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -417,6 +494,11 @@ def main():
     if world == 1 and not args.no_select:
         select = measure_select(args, rg, ctx, gr, src_d, dst_d, variants, dims, Zbuf, barrier, peak, peak_src)
 
+    # ---------------- NEXT-2: Table I widths (N = 1 only)
+    table1 = None
+    if world == 1 and not args.no_table1:
+        table1 = measure_table1(args, rg, dev, barrier, peak, peak_src)
+
     # ---------------- e2e through the C-ABI with host buffers (H2D of edges, D2H of Z inside the timed region)
     # N = 1: three contexts on three streams, steps rotate over them, so a step's copies overlap other
     # steps' kernels (multi-buffering with the public API); every step still copies its own edges in and
@@ -507,6 +589,7 @@ def main():
             "kernels_ms_per_step": {k: round(v, 4) for k, v in sorted(kernel_times.items(), key=lambda x: -x[1])},
             "hops": hop_stats,
             "model_selection": select,
+            "table1_widths": table1,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
