@@ -18,6 +18,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "gauss.cuh"
@@ -397,6 +399,179 @@ __global__ void __launch_bounds__(128) hop_wide(WideArgs a) {
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, ceil_div(n, t)); }
 
+// Wide hop with the neighbour rows streamed by the TMA engine (W in {512, 1024, 2048}). CTA = 4 consumer
+// warps (warp c owns columns [c W/4, (c+1) W/4): V = W/512 float4 per lane) + 1 producer warp. The producer
+// walks the CTA's rows (grid-stride) and their neighbours in CSR order (the GCN self row last), reads col_idx
+// 32 at a time (coalesced), and for every item bulk-copies the whole W-float row into the next slot of an
+// S-slot shared-memory ring (full/empty mbarriers; the item's weight s_j / d_j travels in a slot array). The
+// consumers accumulate straight from shared memory. Memory parallelism is the ring depth (S x 4W bytes per
+// CTA), not registers: no per-lane load staging at all. Same per-column summation order as hop_wide.
+constexpr int kRingThreads = 160;
+#ifndef RG_RING_BYTES
+#define RG_RING_BYTES (96 * 1024)
+#endif
+
+template <int W>
+struct RingCfg {
+    static constexpr int S = RG_RING_BYTES / (4 * W);   // ring slots (one W-float row each)
+    static constexpr int V = W / 512;
+    static constexpr size_t SMEM = (size_t)S * W * 4 + 128;
+};
+
+template <int KIND, int W>
+__global__ void __launch_bounds__(kRingThreads) hop_wide_ring(WideArgs a) {
+    using R = RingCfg<W>;
+    constexpr int S = R::S, V = R::V;
+    extern __shared__ __align__(128) float ring[];
+    __shared__ __align__(8) uint64_t full[S], empty[S];
+    __shared__ float item_w[S];
+    __shared__ float ssq_sh[4];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < S; ++q) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const bool gcn = KIND == W_GCN;
+    if (warp == 4) {
+        // ---------------- producer
+        uint32_t it = 0;
+        for (int64_t i = blockIdx.x; i < a.n; i += gridDim.x) {
+            const int64_t beg = a.row_ptr[i], end = a.row_ptr[i + 1];
+            const int64_t total = (end - beg) + (gcn ? 1 : 0);
+            for (int64_t base = 0; base < total; base += 32) {
+                const int cnt = (int)min((int64_t)32, total - base);
+                int32_t myj = 0;
+                float myw = 1.f;
+                if (lane < cnt) {
+                    const int64_t p = beg + base + lane;
+                    myj = p < end ? __ldg(a.col + p) : (int32_t)i;   // the GCN self row comes last
+                    if (KIND == W_NCUT || KIND == W_DUAL) myw = __ldg(a.s_all + myj);
+                    if (KIND == W_MOD_REDUCED) myw = (float)__ldg(a.deg_all + myj);
+                }
+                for (int k = 0; k < cnt; ++k, ++it) {
+                    const int32_t j = __shfl_sync(0xffffffffu, myj, k);
+                    const float w = __shfl_sync(0xffffffffu, myw, k);
+                    if (lane == 0) {
+                        const int q = (int)(it % S);
+                        if (it >= (uint32_t)S) mbar_wait(&empty[q], ((it / S) - 1) & 1);
+                        item_w[q] = w;
+                        mbar_expect_tx(&full[q], W * 4);
+                        bulk_g2s(ring + (size_t)q * W, a.X + (int64_t)j * W, W * 4, &full[q]);
+                    }
+                }
+            }
+        }
+        return;
+    }
+    // ---------------- consumers: warp c, columns c * W/4 + (v * 32 + lane) * 4
+    uint32_t it = 0;
+    const int cbase4 = warp * (W / 16);   // first float4 column of this warp's slice
+    for (int64_t i = blockIdx.x; i < a.n; i += gridDim.x) {
+        const int64_t total = (a.row_ptr[i + 1] - a.row_ptr[i]) + (gcn ? 1 : 0);
+        float4 acc[V], acc2[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[v] = acc2[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int64_t k = 0; k < total; ++k, ++it) {
+            const int q = (int)(it % S);
+            mbar_wait(&full[q], (it / S) & 1);
+            const float w = item_w[q];
+            const float4 *row = reinterpret_cast<const float4 *>(ring + (size_t)q * W) + cbase4;
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const float4 x = row[v * 32 + lane];
+                if (KIND == W_NCUT) {
+                    acc[v].x = fmaf(w, x.x, acc[v].x); acc[v].y = fmaf(w, x.y, acc[v].y);
+                    acc[v].z = fmaf(w, x.z, acc[v].z); acc[v].w = fmaf(w, x.w, acc[v].w);
+                } else {
+                    acc[v].x += x.x; acc[v].y += x.y; acc[v].z += x.z; acc[v].w += x.w;
+                    if (KIND == W_DUAL || KIND == W_MOD_REDUCED) {
+                        acc2[v].x = fmaf(w, x.x, acc2[v].x); acc2[v].y = fmaf(w, x.y, acc2[v].y);
+                        acc2[v].z = fmaf(w, x.z, acc2[v].z); acc2[v].w = fmaf(w, x.w, acc2[v].w);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[q]);
+        }
+        // epilogue (same arithmetic as hop_wide)
+        float4 y[V], y2[V];
+        if (KIND == W_GCN) {
+            float ss = 0.f;
+            const float shi = __ldg(a.sh_all + i);
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                y[v] = make_float4(tanhf(shi * acc[v].x), tanhf(shi * acc[v].y), tanhf(shi * acc[v].z),
+                                   tanhf(shi * acc[v].w));
+                ss += y[v].x * y[v].x + y[v].y * y[v].y + y[v].z * y[v].z + y[v].w * y[v].w;
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+            if (a.ssq) {
+                if (lane == 0) a.ssq[i * 4 + warp] = ss;
+            } else {
+                if (lane == 0) ssq_sh[warp] = ss;
+                asm volatile("bar.sync 1, 128;" ::: "memory");   // the 4 consumer warps only
+                ss = ssq_sh[0] + ssq_sh[1] + ssq_sh[2] + ssq_sh[3];
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (ss > 0.f) {
+                    const float nrm = sqrtf(ss);
+#pragma unroll
+                    for (int v = 0; v < V; ++v) y[v] = make_float4(y[v].x / nrm, y[v].y / nrm, y[v].z / nrm, y[v].w / nrm);
+                }
+            }
+        } else {
+            const float shi = __ldg(a.sh_all + i);
+            const float si = __ldg(a.s_all + i);
+            const double c = (double)__ldg(a.deg_all + i) * a.inv2e;
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                float4 t;
+                if (KIND == W_NCUT) {
+                    t = make_float4(si * acc[v].x, si * acc[v].y, si * acc[v].z, si * acc[v].w);
+                } else if (KIND == W_MOD_REDUCED) {
+                    t = make_float4((float)(acc[v].x - c * acc2[v].x), (float)(acc[v].y - c * acc2[v].y),
+                                    (float)(acc[v].z - c * acc2[v].z), (float)(acc[v].w - c * acc2[v].w));
+                } else {
+                    const int64_t c4 = cbase4 + v * 32 + lane;
+                    const double2 ga = __ldg(reinterpret_cast<const double2 *>(a.gvec) + 2 * c4);
+                    const double2 gb = __ldg(reinterpret_cast<const double2 *>(a.gvec) + 2 * c4 + 1);
+                    t = make_float4((float)(acc[v].x - c * ga.x), (float)(acc[v].y - c * ga.y),
+                                    (float)(acc[v].z - c * gb.x), (float)(acc[v].w - c * gb.y));
+                }
+                y[v] = make_float4(shi * t.x, shi * t.y, shi * t.z, shi * t.w);
+                if (KIND == W_DUAL) {
+                    const float4 t2 = make_float4(si * acc2[v].x, si * acc2[v].y, si * acc2[v].z, si * acc2[v].w);
+                    y2[v] = make_float4(shi * t2.x, shi * t2.y, shi * t2.z, shi * t2.w);
+                }
+            }
+        }
+        const int64_t W4 = W / 4;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const int64_t c4 = cbase4 + v * 32 + lane;
+            if (KIND == W_DUAL) {
+                if (a.out) reinterpret_cast<float4 *>(a.out)[i * W4 + c4] = y2[v];
+                if (a.out2) reinterpret_cast<float4 *>(a.out2)[i * W4 + c4] = y[v];
+            } else if (a.out) {
+                reinterpret_cast<float4 *>(a.out)[i * W4 + c4] = y[v];
+            }
+            if (KIND == W_GCN && a.zhi) {
+                const int kk = (int)(c4 * 4);
+                const int64_t chunk = (i / kGM) * (W / kKB) + kk / kKB;
+                const size_t off = (size_t)chunk * chunk_bytes(kGM) + kmajor_off((int)(i % kGM), kk % kKB, kGM);
+                const float4 h = make_float4(tf32_hi(y[v].x), tf32_hi(y[v].y), tf32_hi(y[v].z), tf32_hi(y[v].w));
+                *reinterpret_cast<float4 *>(reinterpret_cast<char *>(a.zhi) + off) = h;
+                *reinterpret_cast<float4 *>(reinterpret_cast<char *>(a.zlo) + off) =
+                    make_float4(y[v].x - h.x, y[v].y - h.y, y[v].z - h.z, y[v].w - h.w);
+            }
+        }
+    }
+}
+
 // Row scale of the GEMM after a deferred-normalisation hop: s^_i / ||y_i|| (y_i = 0 rows keep s^_i).
 __global__ void wide_row_scale(const float *__restrict__ ssq, int nw, int64_t n, const float *__restrict__ sh,
                                float *__restrict__ scale) {
@@ -414,10 +589,54 @@ __global__ void wide_row_scale(const float *__restrict__ ssq, int nw, int64_t n,
 #define RG_WIDE_U_DUAL 2
 #endif
 
+int wide_ssq_slices(int32_t w);
+
 bool wide_width(int32_t w) { return w == 256 || w == 512 || w == 1024 || w == 2048; }
+
+// The bulk-copy ring is off by default (RAFTGP_WIDE_RING=1 selects it): measured at 2E5 with Table I widths
+// it is slower than the register-staged hop_wide (wide hops 85 ms with a 96-KB ring, 120 ms with 192 KB,
+// vs 66-69 ms), see DESIGN.md "tried and rejected".
+bool wide_ring_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("RAFTGP_WIDE_RING");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+// slices (partial sums of squares) per row written by a deferred-normalisation GCN hop of width w
+int wide_ssq_slices(int32_t w) { return (wide_ring_enabled() && w >= 512) ? 4 : w / (128 * (w == 256 ? 2 : 4)); }
 
 template <int KIND>
 raftgp_status launch_wide(raftgp_ctx ctx, const WideArgs &a) {
+    const bool use_ring = wide_ring_enabled();
+    if (use_ring && a.W >= 512) {
+        auto go = [&](auto wtag) -> raftgp_status {
+            constexpr int W = decltype(wtag)::value;
+            using R = RingCfg<W>;
+            static bool attr = false;
+            static int per_sm = 1;
+            if (!attr) {
+                RG_CUDA(cudaFuncSetAttribute(hop_wide_ring<KIND, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)R::SMEM));
+                RG_CUDA(cudaFuncSetAttribute(hop_wide_ring<KIND, W>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                             100));
+                RG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hop_wide_ring<KIND, W>, kRingThreads,
+                                                                      R::SMEM));
+                per_sm = std::max(1, per_sm);
+                attr = true;
+            }
+            const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.n, (int64_t)ctx->sm_count * per_sm));
+            LaunchScope LS(ctx, K_WIDE_HOP);
+            hop_wide_ring<KIND, W><<<grid, kRingThreads, R::SMEM, ctx->stream>>>(a);
+            return RAFTGP_OK;
+        };
+        switch (a.W) {
+            case 512: return go(std::integral_constant<int, 512>());
+            case 1024: return go(std::integral_constant<int, 1024>());
+            default: return go(std::integral_constant<int, 2048>());
+        }
+    }
     // V float4 per lane per slice: 256 -> V 2 (one warp per row); 512 -> 4 (1 warp); 1024 -> 4 (2); 2048 -> 4 (4)
     const int V = a.W == 256 ? 2 : 4;
     const int NW = a.W / (128 * V);
@@ -685,7 +904,7 @@ raftgp_status embed_wide(raftgp_graph g, int32_t nvariants, const int32_t *varia
                     WideArgs a{};
                     a.n = n; a.row_ptr = g->row_ptr; a.col = g->col; a.X = T; a.s_all = g->s_all; a.sh_all = g->sh_all;
                     a.deg_all = g->deg_all; a.W = w; a.out = last ? Z_dev[v] : nullptr; a.zhi = zhi; a.zlo = zlo;
-                    const int nw = w / (128 * (w == 256 ? 2 : 4));
+                    const int nw = wide_ssq_slices(w);
                     if (!last) {   // deferred row normalisation: y = tanh(.) tiled, 1/||y|| goes to the GEMM row scale
                         st = take(reinterpret_cast<void **>(&a.ssq), (size_t)n * nw * 4);
                         if (st == RAFTGP_OK) st = take(reinterpret_cast<void **>(&rscale), (size_t)n * 4);
