@@ -40,7 +40,7 @@ def _L():
         _lib = ctypes.CDLL(_SO)
         for name in ("oracle_gaussian", "oracle_build_csr", "oracle_apply", "oracle_project", "oracle_gcn",
                      "oracle_embed_rows", "oracle_modularity", "oracle_ncut", "oracle_local_modularity",
-                     "oracle_kmeans2", "oracle_model_select", "oracle_split_stops"):
+                     "oracle_kmeans2", "oracle_model_select", "oracle_split_stops", "oracle_sbm_sample"):
             getattr(_lib, name).restype = ctypes.c_int
     return _lib
 
@@ -261,3 +261,55 @@ def gcn_np(g: CSR, dims, seed: int, Y: np.ndarray):
         Z = np.where(nrm[:, None] > 0, H / np.where(nrm > 0, nrm, 1.0)[:, None], 0.0)
         out.append(Z)
     return out
+
+
+# ------------------------------------------------------------------ NEXT-3: Alg. 2 SBM sampler
+def _L_f64():
+    lib = _L()
+    lib.oracle_ln_spec64.restype = ctypes.c_double
+    lib.oracle_ln_spec64.argtypes = [ctypes.c_double]
+    lib.oracle_sbm_uniform.restype = ctypes.c_double
+    lib.oracle_sbm_uniform.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32]
+    lib.oracle_sbm_range_sum_hook.restype = ctypes.c_double
+    lib.oracle_sbm_range_sum_hook.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
+                                              ctypes.c_void_p, ctypes.c_double, ctypes.c_int64, ctypes.c_int64]
+    return lib
+
+
+def sbm_range_sum(theta_r, theta_s, omega: float, x: int, y: int) -> float:
+    """SBM_SPEC §3 RangeSum over cells x..y of one block pair (theta_s=None: the diagonal pair of theta_r)."""
+    tr = np.ascontiguousarray(theta_r, np.float64)
+    ts = np.ascontiguousarray(theta_s if theta_s is not None else [0.0], np.float64)
+    return _L_f64().oracle_sbm_range_sum_hook(int(theta_s is None), tr.size, tr.ctypes.data, ts.size if theta_s is not None else 0,
+                                              ts.ctypes.data, float(omega), int(x), int(y))
+
+
+def ln_spec64(u: float) -> float:
+    """SBM_SPEC §6."""
+    return _L_f64().oracle_ln_spec64(float(u))
+
+
+def sbm_uniform(seed: int, p: int, k: int, d: int) -> float:
+    """SBM_SPEC §5."""
+    return _L_f64().oracle_sbm_uniform(seed, p, k, d)
+
+
+def sbm_sample(c, theta, omega, seed: int, q: int = 20, cap=None):
+    """Alg. 2 per docs/SBM_SPEC.md: returns (src, dst) int32 edge arrays in (pair, chunk,
+    cell) order."""
+    c = np.ascontiguousarray(c, np.int32)
+    theta = np.ascontiguousarray(theta, np.float64)
+    omega = np.ascontiguousarray(omega, np.float64)
+    K = omega.shape[0]
+    n = c.size
+    m = ctypes.c_int64(0)
+    cap = int(cap) if cap is not None else max(1024, int(4 * (theta.sum() ** 2) * omega.max() + 10 * n))
+    while True:
+        src = np.zeros(max(1, cap), np.int32)
+        dst = np.zeros(max(1, cap), np.int32)
+        _check(_L().oracle_sbm_sample(ctypes.c_int64(n), ctypes.c_int32(K), _p(c), _p(theta), _p(omega),
+                                      ctypes.c_uint64(seed), ctypes.c_int32(q), _p(src), _p(dst),
+                                      ctypes.c_int64(cap), ctypes.byref(m)))
+        if m.value <= cap:
+            return src[: m.value].copy(), dst[: m.value].copy()
+        cap = m.value

@@ -25,6 +25,7 @@
  *   oracle_local_modularity Eq. 7
  *   oracle_kmeans2,
  *   oracle_model_select    Alg. 1 with the 2-means of docs/SELECT_SPEC.md (NEXT-1)
+ *   oracle_sbm_sample      Alg. 2 per docs/SBM_SPEC.md (NEXT-3)
  *
  * Status codes: 0 ok, 2 parameter error, 3 data error (same numbering as include/raftgp.h, which
  * is NOT included here).
@@ -668,4 +669,172 @@ int oracle_model_select(int64_t n, const int64_t *row_ptr, const int32_t *col, c
     free(st.where);
     free(st.block_of);
     return 0;
+}
+
+/* ---------------------------------------------------------------- Alg. 2: exact SBM sampler (NEXT-3)
+ * docs/SBM_SPEC.md (Def. 5). Plain loops in the spec's order. */
+
+/* SBM_SPEC §6 */
+double oracle_ln_spec64(double u) {
+    uint64_t bits;
+    memcpy(&bits, &u, 8);
+    int e = (int)((bits >> 52) & 0x7FF) - 1023;
+    uint64_t mb = (bits & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull;
+    double m;
+    memcpy(&m, &mb, 8);
+    if (m > 0x1.6a09e667f3bcdp+0) { m = m * 0.5; e = e + 1; }
+    double t = (m - 1.0) / (m + 1.0);
+    double t2 = t * t;
+    double s = 2.0 / 25.0;
+    for (int k = 11; k >= 0; --k) s = fma(t2, s, 2.0 / (double)(2 * k + 1));
+    double lnm = t * s;
+    return fma((double)e, 0x1.62e42fefa39efp-1, fma((double)e, 0x1.abc9e3b39803fp-56, lnm));
+}
+
+/* SBM_SPEC §5 */
+double oracle_sbm_uniform(uint64_t seed, uint32_t p, uint32_t k, uint32_t d) {
+    uint32_t ctr[4] = {p, k, d, 0x53424D31u}, key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)}, x[4];
+    oracle_philox4x32_10(ctr, key, x);
+    uint64_t v = ((uint64_t)(x[0] >> 5) << 26) + (uint64_t)(x[1] >> 6) + 1u;
+    return (double)v * 0x1p-53;
+}
+
+typedef struct {
+    int diag;                 /* r == s */
+    int64_t nr, ns;
+    const int32_t *Cr, *Cs;   /* members (ascending ids) */
+    const double *th;         /* theta of all nodes */
+    const double *Pr, *Ps, *Q;
+    double omega;
+} sbm_pair;
+
+static int64_t tri_row_start(int64_t n, int64_t a) { return a * n - a * (a + 1) / 2; }
+
+/* SBM_SPEC §3: cell -> (a, b) */
+static void sbm_cell(const sbm_pair *P, int64_t x, int64_t *a, int64_t *b) {
+    if (!P->diag) { *a = x / P->ns; *b = x % P->ns; return; }
+    int64_t n = P->nr, lo = 0, hi = n - 2;
+    while (lo < hi) {
+        int64_t mid = (lo + hi + 1) / 2;
+        if (tri_row_start(n, mid) <= x) lo = mid; else hi = mid - 1;
+    }
+    *a = lo;
+    *b = lo + 1 + (x - tri_row_start(n, lo));
+}
+
+/* SBM_SPEC §3: RangeSum(x, y), cells inclusive */
+double oracle_sbm_range_sum(const sbm_pair *P, int64_t x, int64_t y) {
+    int64_t a1, b1, a2, b2;
+    sbm_cell(P, x, &a1, &b1);
+    sbm_cell(P, y, &a2, &b2);
+    double t1 = P->th[P->Cr[a1]], t2 = P->th[P->Cr[a2]];
+    if (!P->diag) {
+        if (a1 == a2) return P->omega * (t1 * (P->Ps[b2 + 1] - P->Ps[b1]));
+        return P->omega * ((t1 * (P->Ps[P->ns] - P->Ps[b1]) + (P->Pr[a2] - P->Pr[a1 + 1]) * P->Ps[P->ns]) +
+                           t2 * P->Ps[b2 + 1]);
+    }
+    const double *Pp = P->Pr;
+    int64_t n = P->nr;
+    if (a1 == a2) return P->omega * (t1 * (Pp[b2 + 1] - Pp[b1]));
+    return P->omega * ((t1 * (Pp[n] - Pp[b1]) + (P->Q[a2] - P->Q[a1 + 1])) + t2 * (Pp[b2 + 1] - Pp[a2 + 1]));
+}
+
+/* Alg. 2 (SBM_SPEC §4) for all pairs. Edges (src < dst not implied: src from the row block) are appended in
+ * (pair, chunk, cell) order to out_src/out_dst (capacity cap; the total count is returned in *m_out even when
+ * it exceeds cap). Errors: 2 (bad arguments: K <= 0, a label outside [0,K), theta <= 0, omega < 0 or not
+ * symmetric, q outside [4, 30]). */
+int oracle_sbm_sample(int64_t n, int32_t K, const int32_t *c, const double *theta, const double *omega,
+                      uint64_t seed, int32_t q, int32_t *out_src, int32_t *out_dst, int64_t cap, int64_t *m_out) {
+    if (n < 0 || K <= 0 || q < 4 || q > 30) return 2;
+    for (int64_t i = 0; i < n; ++i) if (c[i] < 0 || c[i] >= K || !(theta[i] > 0.0)) return 2;
+    for (int32_t r = 0; r < K; ++r)
+        for (int32_t s = 0; s < K; ++s)
+            if (!(omega[r * K + s] >= 0.0) || omega[r * K + s] != omega[s * K + r]) return 2;
+    /* members per block in ascending id */
+    int64_t *cnt = (int64_t *)calloc((size_t)K + 1, sizeof(int64_t));
+    for (int64_t i = 0; i < n; ++i) cnt[c[i] + 1]++;
+    for (int32_t r = 0; r < K; ++r) cnt[r + 1] += cnt[r];
+    int32_t *mem = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n + 1));
+    int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * (size_t)(K + 1));
+    memcpy(fill, cnt, sizeof(int64_t) * (size_t)(K + 1));
+    for (int64_t i = 0; i < n; ++i) mem[fill[c[i]]++] = (int32_t)i;
+    /* SBM_SPEC §2 tables, per block */
+    double *P = (double *)malloc(sizeof(double) * (size_t)(n + K + 1));
+    double *Qt = (double *)malloc(sizeof(double) * (size_t)(n + K + 1));
+    for (int32_t r = 0; r < K; ++r) {
+        int64_t nr = cnt[r + 1] - cnt[r], o = cnt[r] + r;
+        P[o] = 0.0;
+        for (int64_t a = 0; a < nr; ++a) P[o + a + 1] = P[o + a] + theta[mem[cnt[r] + a]];
+        Qt[o] = 0.0;
+        for (int64_t a = 0; a < nr; ++a) Qt[o + a + 1] = Qt[o + a] + theta[mem[cnt[r] + a]] * (P[o + nr] - P[o + a + 1]);
+    }
+    int64_t m = 0;
+    const int64_t chunk = (int64_t)1 << q;
+    uint32_t pidx = 0;
+    for (int32_t r = 0; r < K; ++r) {
+        for (int32_t s = r; s < K; ++s, ++pidx) {
+            sbm_pair pr;
+            pr.diag = r == s;
+            pr.nr = cnt[r + 1] - cnt[r];
+            pr.ns = cnt[s + 1] - cnt[s];
+            pr.Cr = mem + cnt[r];
+            pr.Cs = mem + cnt[s];
+            pr.th = theta;
+            pr.Pr = P + cnt[r] + r;
+            pr.Ps = P + cnt[s] + s;
+            pr.Q = Qt + cnt[r] + r;
+            pr.omega = omega[r * K + s];
+            int64_t T = pr.diag ? pr.nr * (pr.nr - 1) / 2 : pr.nr * pr.ns;
+            if (pr.omega == 0.0 || T <= 0) continue;
+            for (int64_t k = 0; k * chunk < T; ++k) {
+                int64_t x0 = k * chunk, x1 = x0 + chunk < T ? x0 + chunk : T, mm = x0;
+                uint32_t d = 0;
+                for (;;) {
+                    double u = oracle_sbm_uniform(seed, pidx, (uint32_t)k, d++);
+                    double E = -oracle_ln_spec64(u);
+                    if (!(oracle_sbm_range_sum(&pr, mm, x1 - 1) > E)) break;
+                    int64_t lo = mm, hi = x1 - 1;
+                    while (lo < hi) {
+                        int64_t mid = lo + (hi - lo) / 2;
+                        if (oracle_sbm_range_sum(&pr, mm, mid) > E) hi = mid; else lo = mid + 1;
+                    }
+                    int64_t a, b;
+                    sbm_cell(&pr, lo, &a, &b);
+                    if (m < cap) { out_src[m] = pr.Cr[a]; out_dst[m] = pr.diag ? pr.Cr[b] : pr.Cs[b]; }
+                    m++;
+                    mm = lo + 1;
+                    if (mm == x1) break;
+                }
+            }
+        }
+    }
+    *m_out = m;
+    free(cnt); free(mem); free(fill); free(P); free(Qt);
+    return 0;
+}
+
+/* Test hook: RangeSum(x, y) of one block pair given the member thetas (rows theta_r[n_r], cols theta_s[n_s];
+ * diag: the upper triangle of one block, theta_s ignored). Builds the §2 tables like oracle_sbm_sample. */
+double oracle_sbm_range_sum_hook(int diag, int64_t nr, const double *theta_r, int64_t ns, const double *theta_s,
+                                 double omega, int64_t x, int64_t y) {
+    int64_t nt = nr + (diag ? 0 : ns);
+    double *th = (double *)malloc(sizeof(double) * (size_t)(nt + 1));
+    int32_t *Cr = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nr + 1));
+    int32_t *Cs = (int32_t *)malloc(sizeof(int32_t) * (size_t)(ns + 1));
+    for (int64_t a = 0; a < nr; ++a) { th[a] = theta_r[a]; Cr[a] = (int32_t)a; }
+    if (!diag) for (int64_t b = 0; b < ns; ++b) { th[nr + b] = theta_s[b]; Cs[b] = (int32_t)(nr + b); }
+    double *Pr = (double *)malloc(sizeof(double) * (size_t)(nr + 1)), *Ps = (double *)malloc(sizeof(double) * (size_t)(ns + 1));
+    double *Q = (double *)malloc(sizeof(double) * (size_t)(nr + 1));
+    Pr[0] = 0.0;
+    for (int64_t a = 0; a < nr; ++a) Pr[a + 1] = Pr[a] + th[Cr[a]];
+    Q[0] = 0.0;
+    for (int64_t a = 0; a < nr; ++a) Q[a + 1] = Q[a] + th[Cr[a]] * (Pr[nr] - Pr[a + 1]);
+    Ps[0] = 0.0;
+    if (!diag) for (int64_t b = 0; b < ns; ++b) Ps[b + 1] = Ps[b] + th[Cs[b]];
+    sbm_pair P;
+    P.diag = diag; P.nr = nr; P.ns = diag ? nr : ns; P.Cr = Cr; P.Cs = diag ? Cr : Cs; P.th = th;
+    P.Pr = Pr; P.Ps = diag ? Pr : Ps; P.Q = Q; P.omega = omega;
+    double v = oracle_sbm_range_sum(&P, x, y);
+    free(th); free(Cr); free(Cs); free(Pr); free(Ps); free(Q);
+    return v;
 }
