@@ -241,6 +241,20 @@ RAFTGP_API raftgp_status raftgp_model_select(raftgp_graph g, const float *Z_dev,
 RAFTGP_API raftgp_status raftgp_gemm_tf32x3(raftgp_ctx ctx, int64_t M, int32_t K, int32_t N, const float *A_dev,
                                             const float *B_dev, const float *row_scale_dev, float *C_dev);
 
+/* ---------------------------------------------------------------- NEXT-3: exact SBM sampler
+ * Alg. 2 for the degree-corrected SBM of Def. 5: every node pair
+ * (i, j), i != j, is an edge with probability 1 - exp(-theta_i theta_j Omega[c_i][c_j]), independently; the
+ * walk over each block pair's virtual table jumps to the next cell with a Poisson event by binary search over
+ * prefix sums. Stream, fp64 evaluation and the chunking of the walk are fixed by docs/SBM_SPEC.md, so the edge
+ * list is identical to the oracle's, in (block pair, chunk, cell) order; src is the member of the lower block.
+ *   c_dev: device int32[n] block labels in [0, K); theta_dev: device fp64[n] > 0; omega_dev: device fp64[K*K]
+ *   symmetric, >= 0; q: chunks of 2^q cells (4..30; 20 suggested); src_dev/dst_dev: device int32[cap].
+ *   m_out: host, the number of edges. If it exceeds cap nothing is written: call again with cap >= *m_out.
+ * Synchronous. Errors: PARAM (sizes, null pointers, invalid labels / theta / Omega). */
+RAFTGP_API raftgp_status raftgp_sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c_dev,
+                                           const double *theta_dev, const double *omega_dev, uint64_t seed, int32_t q,
+                                           int32_t *src_dev, int32_t *dst_dev, int64_t cap, int64_t *m_out);
+
 #ifdef __cplusplus
 }
 #endif

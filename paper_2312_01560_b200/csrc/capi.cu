@@ -18,7 +18,7 @@ namespace raftgp {
 
 const char *const kKernelNames[K_NUM] = {
     "csr_count", "scan", "csr_scatter", "csr_sort_warp", "csr_sort_block", "csr_compact", "degree_scalars",
-    "sketch", "g_partials", "g_final", "feature_hop", "transform", "gcn_hop", "hop_generic", "misc", "csr_partition", "csr_bucket_sort", "row_order", "model_select", "select_seed", "select_lloyd", "select_split", "gemm_tf32x3", "gemm_tile", "wide_hop"};
+    "sketch", "g_partials", "g_final", "feature_hop", "transform", "gcn_hop", "hop_generic", "misc", "csr_partition", "csr_bucket_sort", "row_order", "model_select", "select_seed", "select_lloyd", "select_split", "gemm_tf32x3", "gemm_tile", "wide_hop", "sbm_setup", "sbm_walk"};
 
 static thread_local std::string g_last_error;
 
@@ -829,6 +829,22 @@ raftgp_status raftgp_gemm_tf32x3(raftgp_ctx ctx, int64_t M, int32_t K, int32_t N
     if (M > 0 && (!A_dev || !B_dev || !C_dev)) return fail(RAFTGP_ERR_PARAM, "null A, B or C");
     RG_TRY(set_device(ctx));
     return gemm_rowmajor(ctx, A_dev, M, K, B_dev, N, row_scale_dev, C_dev);
+    RG_GUARD_END
+}
+
+// ---------------------------------------------------------------- NEXT-3: Alg. 2 SBM sampler
+raftgp_status raftgp_sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c_dev, const double *theta_dev,
+                                const double *omega_dev, uint64_t seed, int32_t q, int32_t *src_dev, int32_t *dst_dev,
+                                int64_t cap, int64_t *m_out) {
+    RG_GUARD_BEGIN
+    if (!ctx || !m_out) return fail(RAFTGP_ERR_PARAM, "null argument");
+    if (n < 0 || n + K >= (int64_t)INT32_MAX || K <= 0 || q < 4 || q > 30 || cap < 0)
+        return fail(RAFTGP_ERR_PARAM, "need 0 <= n, n + K < 2^31 - 1, K > 0, 4 <= q <= 30, cap >= 0");
+    if (n > 0 && (!c_dev || !theta_dev)) return fail(RAFTGP_ERR_PARAM, "null c or theta");
+    if (!omega_dev) return fail(RAFTGP_ERR_PARAM, "null omega");
+    if (cap > 0 && (!src_dev || !dst_dev)) return fail(RAFTGP_ERR_PARAM, "null edge outputs");
+    RG_TRY(set_device(ctx));
+    return sbm_sample(ctx, n, K, c_dev, theta_dev, omega_dev, seed, q, src_dev, dst_dev, cap, m_out);
     RG_GUARD_END
 }
 

@@ -41,6 +41,8 @@ enum KernelId : int {
     K_GEMM,
     K_GEMM_TILE,
     K_WIDE_HOP,
+    K_SBM,
+    K_SBM_WALK,
     K_NUM
 };
 extern const char *const kKernelNames[K_NUM];
@@ -189,6 +191,10 @@ raftgp_status gemm_rowmajor(raftgp_ctx ctx, const float *A, int64_t M, int K, co
 bool wide_supported(int32_t layers, const int32_t *dims);
 raftgp_status embed_wide(raftgp_graph g, int32_t nvariants, const int32_t *variants, int32_t layers,
                          const int32_t *dims, uint64_t seed, float *const *Z_dev, const int where[3]);
+// NEXT-3: Alg. 2 exact SBM sampler (sbm.cu)
+raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c, const double *theta,
+                         const double *omega, uint64_t seed, int32_t q, int32_t *src, int32_t *dst, int64_t cap,
+                         int64_t *m_out);
 // NEXT-1: Alg. 1 hierarchical model selection (select.cu)
 raftgp_status model_select(raftgp_graph g, const float *Z, int32_t L, int32_t eps, int32_t max_iter, int32_t rule,
                            int32_t *labels, int32_t *num_blocks, int64_t *stats);

@@ -35,7 +35,7 @@ EXPORTS = (
     "raftgp_graph_local_degrees", "raftgp_graph_set_degrees", "raftgp_graph_set_order", "raftgp_graph_destroy", "raftgp_sketch",
     "raftgp_weights", "raftgp_project", "raftgp_gcn_transform", "raftgp_gcn_hop", "raftgp_gnn_embed",
     "raftgp_embed", "raftgp_embed_multi", "raftgp_feature_transform", "raftgp_modularity", "raftgp_ncut", "raftgp_local_modularity",
-    "raftgp_model_select", "raftgp_gemm_tf32x3",
+    "raftgp_model_select", "raftgp_gemm_tf32x3", "raftgp_sbm_sample",
 )
 
 _lib = None
@@ -87,6 +87,7 @@ _SIGS = {
     "raftgp_local_modularity": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_i32, P(c_dbl)]),
     "raftgp_model_select": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, P(c_i32), c_vp]),
     "raftgp_gemm_tf32x3": (ctypes.c_int, [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
+    "raftgp_sbm_sample": (ctypes.c_int, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_u64, c_i32, c_vp, c_vp, c_i64, P(c_i64)]),
 }
 
 
@@ -434,3 +435,34 @@ def raftgp_gemm_tf32x3(ctx: Context, A: torch.Tensor, B: torch.Tensor, row_scale
     _ck(load_library().raftgp_gemm_tf32x3(ctx.h, M, K, N, _ptr(A.contiguous()), _ptr(B.contiguous()),
                                           _ptr(row_scale), _ptr(C)))
     return C
+
+
+# ------------------------------------------------------------------ NEXT-3: exact SBM sampler
+def raftgp_sbm_sample(ctx: Context, c: torch.Tensor, theta: torch.Tensor, omega: torch.Tensor, seed: int,
+                      q: int = 20, cap: Optional[int] = None):
+    """Alg. 2 (docs/SBM_SPEC.md) on the device: returns (src, dst) int32 CUDA tensors."""
+    c = _dev(c.to(torch.int32).contiguous(), "c")
+    theta = _dev(theta.to(torch.float64).contiguous(), "theta")
+    omega = _dev(omega.to(torch.float64).contiguous(), "omega")
+    K = omega.shape[0]
+    n = c.numel()
+    if cap is None:   # expected edges + slack (a second call fixes an underestimate)
+        cap = int(1.2 * _expected_edges(c, theta, omega)) + 1024
+    m = c_i64(0)
+    while True:
+        src = torch.empty(max(1, cap), dtype=torch.int32, device=ctx.device)
+        dst = torch.empty(max(1, cap), dtype=torch.int32, device=ctx.device)
+        _ck(load_library().raftgp_sbm_sample(ctx.h, n, K, _ptr(c), _ptr(theta), _ptr(omega), seed, q, _ptr(src),
+                                             _ptr(dst), cap, ctypes.byref(m)))
+        if m.value <= cap:
+            return src[: m.value], dst[: m.value]
+        cap = m.value
+
+
+def _expected_edges(c, theta, omega) -> float:
+    """sum_{i<j} lambda_ij (upper bound of the expected simple-graph edge count), from block theta sums."""
+    K = omega.shape[0]
+    ts = torch.zeros(K, dtype=torch.float64, device=theta.device).index_add_(0, c.long(), theta)
+    t2 = torch.zeros(K, dtype=torch.float64, device=theta.device).index_add_(0, c.long(), theta * theta)
+    tot = (ts[:, None] * ts[None, :] * omega).sum() - (t2 * torch.diagonal(omega)).sum()
+    return float(tot.item()) / 2

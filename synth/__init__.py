@@ -164,3 +164,33 @@ def sample_rows(n: int, count: int, seed: int) -> np.ndarray:
     rng = np.random.Generator(np.random.PCG64(seed + 7919))
     count = min(count, n)
     return np.sort(rng.choice(n, size=count, replace=False)).astype(np.int64)
+
+
+def sbm_params(cfg: DCSBMConfig | str, seed: int = 0, rule: str = "stated", n: int | None = None):
+    """Parameters (c, theta, Omega) of the same degree-corrected SBM that `generate` draws from (Def. 5,
+    PAPER.md:106-109): lambda_ij = theta_i theta_j Omega[c_i][c_j] with the mixture Omega_rs =
+    f_in delta_rs / kappa_r + (1 - f_in) / 2m, node ids randomly permuted. Input for the Alg. 2 sampler."""
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    N = int(n if n is not None else cfg.n)
+    m_target = cfg.m_stated * (N / cfg.n)
+    K = min(cfg.k, max(1, N // 2))
+    rng = np.random.Generator(np.random.PCG64(seed))
+    sizes = _block_sizes(rng, N, K, cfg.alpha, cfg.min_size)
+    theta = _powerlaw(rng, N, cfg.gamma, cfg.dmin, cfg.dmax)
+    if rule == "stated":
+        theta *= (2.0 * m_target) / theta.sum()
+    block = np.repeat(np.arange(K, dtype=np.int32), sizes)
+    two_m = float(theta.sum())
+    kappa = np.bincount(block, weights=theta, minlength=K)
+    s = float((kappa ** 2).sum() / two_m)
+    f_in = (cfg.rho * (two_m - s) - s) / ((1.0 + cfg.rho) * (two_m - s)) if two_m > s else 1.0
+    f_in = float(np.clip(f_in, 0.0, 1.0))
+    omega = np.full((K, K), (1.0 - f_in) / two_m)
+    omega[np.arange(K), np.arange(K)] += f_in / kappa
+    perm = rng.permutation(N)
+    c = np.empty(N, np.int32)
+    th = np.empty(N, np.float64)
+    c[perm] = block
+    th[perm] = theta
+    return c, th, omega
