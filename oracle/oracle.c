@@ -769,7 +769,6 @@ int oracle_sbm_sample(int64_t n, int32_t K, const int32_t *c, const double *thet
         for (int64_t a = 0; a < nr; ++a) Qt[o + a + 1] = Qt[o + a] + theta[mem[cnt[r] + a]] * (P[o + nr] - P[o + a + 1]);
     }
     int64_t m = 0;
-    const int64_t chunk = (int64_t)1 << q;
     uint32_t pidx = 0;
     for (int32_t r = 0; r < K; ++r) {
         for (int32_t s = r; s < K; ++s, ++pidx) {
@@ -786,6 +785,12 @@ int oracle_sbm_sample(int64_t n, int32_t K, const int32_t *c, const double *thet
             pr.omega = omega[r * K + s];
             int64_t T = pr.diag ? pr.nr * (pr.nr - 1) / 2 : pr.nr * pr.ns;
             if (pr.omega == 0.0 || T <= 0) continue;
+            /* SBM_SPEC §4: q_p, the largest q' in [4, q] with R_p 2^q' <= 8 T (else 4) */
+            double Rp = oracle_sbm_range_sum(&pr, 0, T - 1);
+            int qp = 4;
+            for (int qq = q; qq >= 4; --qq)
+                if (ldexp(Rp, qq) <= 8.0 * (double)T) { qp = qq; break; }
+            const int64_t chunk = (int64_t)1 << qp;
             for (int64_t k = 0; k * chunk < T; ++k) {
                 int64_t x0 = k * chunk, x1 = x0 + chunk < T ? x0 + chunk : T, mm = x0;
                 uint32_t d = 0;

@@ -53,10 +53,11 @@ struct SbmArgs {
     int32_t K;
     const int64_t *boff;     // [K+1] member offsets
     const int32_t *mem;      // members, ascending id per block
-    const double *theta;     // [N]
+    const double *thm;       // theta of the members, in member order (thm[boff[r] + a] = theta[C_r[a]])
     const double *omega;     // [K*K]
     const double *P, *Q;     // tables: block r at boff[r] + r, length n_r + 1
     const int64_t *choff;    // [npairs+1] chunk offsets per pair
+    const int8_t *qp;        // [npairs] log2 chunk size of each pair (SBM_SPEC §4)
     int64_t npairs, nchunks;
     uint64_t seed;
     int q;
@@ -66,6 +67,7 @@ struct PairView {
     bool diag;
     int64_t nr, ns;
     const int32_t *Cr, *Cs;
+    const double *Tr;        // theta of the row block's members
     const double *Pr, *Ps, *Qr;
     double omega;
 };
@@ -107,10 +109,10 @@ __device__ __forceinline__ void cell_ab(const PairView &v, int64_t x, int64_t &a
 __device__ __forceinline__ double range_sum(const SbmArgs &A, const PairView &v, int64_t a1, int64_t b1, int64_t y) {
     int64_t a2, b2;
     cell_ab(v, y, a2, b2);
-    const double t1 = A.theta[v.Cr[a1]];
+    const double t1 = v.Tr[a1];
     if (!v.diag) {
         if (a1 == a2) return __dmul_rn(v.omega, __dmul_rn(t1, __dsub_rn(v.Ps[b2 + 1], v.Ps[b1])));
-        const double t2 = A.theta[v.Cr[a2]];
+        const double t2 = v.Tr[a2];
         const double u1 = __dmul_rn(t1, __dsub_rn(v.Ps[v.ns], v.Ps[b1]));
         const double u2 = __dmul_rn(__dsub_rn(v.Pr[a2], v.Pr[a1 + 1]), v.Ps[v.ns]);
         const double u3 = __dmul_rn(t2, v.Ps[b2 + 1]);
@@ -118,7 +120,7 @@ __device__ __forceinline__ double range_sum(const SbmArgs &A, const PairView &v,
     }
     const int64_t n = v.nr;
     if (a1 == a2) return __dmul_rn(v.omega, __dmul_rn(t1, __dsub_rn(v.Pr[b2 + 1], v.Pr[b1])));
-    const double t2 = A.theta[v.Cr[a2]];
+    const double t2 = v.Tr[a2];
     const double u1 = __dmul_rn(t1, __dsub_rn(v.Pr[n], v.Pr[b1]));
     const double u2 = __dsub_rn(v.Qr[a2], v.Qr[a1 + 1]);
     const double u3 = __dmul_rn(t2, __dsub_rn(v.Pr[b2 + 1], v.Pr[a2 + 1]));
@@ -144,12 +146,14 @@ __device__ int64_t walk_chunk(const SbmArgs &A, int64_t chunk, int32_t *src, int
     v.ns = A.boff[s + 1] - A.boff[s];
     v.Cr = A.mem + A.boff[r];
     v.Cs = A.mem + A.boff[s];
+    v.Tr = A.thm + A.boff[r];
     v.Pr = A.P + A.boff[r] + r;
     v.Ps = A.P + A.boff[s] + s;
     v.Qr = A.Q + A.boff[r] + r;
     v.omega = A.omega[(int64_t)r * A.K + s];
     const int64_t T = v.diag ? v.nr * (v.nr - 1) / 2 : v.nr * v.ns;
-    const int64_t x0 = k << A.q, x1 = min(T, (k + 1) << A.q);
+    const int q = A.qp[p];
+    const int64_t x0 = k << q, x1 = min(T, (k + 1) << q);
     int64_t mm = x0, cnt = 0;
     uint32_t d = 0;
     int64_t a1, b1;
@@ -188,38 +192,84 @@ __global__ void sbm_write(SbmArgs A, const int64_t *off, int32_t *src, int32_t *
         walk_chunk<true>(A, c, src, dst, off[c]);
 }
 
-// SBM_SPEC §2: one thread per block, sequential fp64 sums in member order
-__global__ void sbm_tables(int32_t K, const int64_t *boff, const int32_t *mem, const double *theta, double *P,
-                           double *Q) {
+__global__ void sbm_gather_theta(const int32_t *mem, const double *theta, int64_t n, double *thm) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) thm[t] = theta[mem[t]];
+}
+
+// SBM_SPEC §2: one thread per block, sequential fp64 sums in member order (over the contiguous member thetas)
+__global__ void sbm_tables(int32_t K, const int64_t *boff, const double *thm, double *P, double *Q) {
     const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= K) return;
     const int64_t b0 = boff[r], nr = boff[r + 1] - b0, o = b0 + r;
+    // sequential in a (the spec's order); operands are loaded 8 ahead so the add chain is the only dependency
     double acc = 0.0;
     P[o] = 0.0;
-    for (int64_t a = 0; a < nr; ++a) {
-        acc = __dadd_rn(acc, theta[mem[b0 + a]]);
-        P[o + a + 1] = acc;
+    for (int64_t a0 = 0; a0 < nr; a0 += 8) {
+        double t[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) t[j] = a0 + j < nr ? thm[b0 + a0 + j] : 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (a0 + j < nr) {
+                acc = __dadd_rn(acc, t[j]);
+                P[o + a0 + j + 1] = acc;
+            }
     }
     const double tot = acc;
     double q = 0.0;
     Q[o] = 0.0;
-    for (int64_t a = 0; a < nr; ++a) {
-        q = __dadd_rn(q, __dmul_rn(theta[mem[b0 + a]], __dsub_rn(tot, P[o + a + 1])));
-        Q[o + a + 1] = q;
+    for (int64_t a0 = 0; a0 < nr; a0 += 8) {
+        double t[8], pp[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            t[j] = a0 + j < nr ? thm[b0 + a0 + j] : 0.0;
+            pp[j] = a0 + j < nr ? P[o + a0 + j + 1] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (a0 + j < nr) {
+                q = __dadd_rn(q, __dmul_rn(t[j], __dsub_rn(tot, pp[j])));
+                Q[o + a0 + j + 1] = q;
+            }
     }
 }
 
-// chunks per pair (0 when omega_rs = 0 or the pair has no cells)
-__global__ void sbm_pair_chunks(int32_t K, int64_t npairs, const int64_t *boff, const double *omega, int q,
-                                int32_t *nch) {
+// chunks per pair (0 when omega_rs = 0 or the pair has no cells) and the pair's chunk size 2^q_p:
+// the largest q_p in [4, q] with R_p 2^q_p <= 8 T, R_p = RangeSum(0, T - 1) (SBM_SPEC §4)
+__global__ void sbm_pair_chunks(SbmArgs A, int q, int32_t *nch, int8_t *qp) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= npairs) return;
+    if (p >= A.npairs) return;
     int32_t r, s;
-    pair_of(p, K, r, s);
-    const int64_t nr = boff[r + 1] - boff[r], ns = boff[s + 1] - boff[s];
-    const int64_t T = r == s ? nr * (nr - 1) / 2 : nr * ns;
-    const double w = omega[(int64_t)r * K + s];
-    nch[p] = (w == 0.0 || T <= 0) ? 0 : (int32_t)((T + ((int64_t)1 << q) - 1) >> q);
+    pair_of(p, A.K, r, s);
+    PairView v;
+    v.diag = r == s;
+    v.nr = A.boff[r + 1] - A.boff[r];
+    v.ns = A.boff[s + 1] - A.boff[s];
+    v.Cr = A.mem + A.boff[r];
+    v.Cs = A.mem + A.boff[s];
+    v.Tr = A.thm + A.boff[r];
+    v.Pr = A.P + A.boff[r] + r;
+    v.Ps = A.P + A.boff[s] + s;
+    v.Qr = A.Q + A.boff[r] + r;
+    v.omega = A.omega[(int64_t)r * A.K + s];
+    const int64_t T = v.diag ? v.nr * (v.nr - 1) / 2 : v.nr * v.ns;
+    if (v.omega == 0.0 || T <= 0) {
+        nch[p] = 0;
+        qp[p] = 4;
+        return;
+    }
+    int64_t a0, b0;
+    cell_ab(v, 0, a0, b0);   // the first cell: (0, 0), or (0, 1) on the diagonal
+    const double Rp = range_sum(A, v, a0, b0, T - 1);
+    int qq = 4;
+    for (int t = q; t >= 4; --t)
+        if (scalbn(Rp, t) <= 8.0 * (double)T) {
+            qq = t;
+            break;
+        }
+    qp[p] = (int8_t)qq;
+    nch[p] = (int32_t)((T + ((int64_t)1 << qq) - 1) >> qq);
 }
 
 __global__ void sbm_bip_edges(const int32_t *c, int64_t n, int32_t *src, int32_t *dst) {
@@ -287,26 +337,36 @@ raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c,
     A.K = K;
     A.boff = members.row_ptr;
     A.mem = members.col;
-    A.theta = theta;
     A.omega = omega;
     A.seed = seed;
     A.q = q;
     A.npairs = (int64_t)K * (K + 1) / 2;
-    double *P = nullptr, *Q = nullptr;
+    double *P = nullptr, *Q = nullptr, *thm = nullptr;
     int32_t *nch = nullptr, *cnt = nullptr;
+    int8_t *qp = nullptr;
     int64_t *choff = nullptr, *off = nullptr;
     raftgp_status s2 = dalloc_t(ctx, &P, (size_t)(n + K + 1));
     if (s2 == RAFTGP_OK) s2 = dalloc_t(ctx, &Q, (size_t)(n + K + 1));
+    if (s2 == RAFTGP_OK) s2 = dalloc_t(ctx, &thm, (size_t)std::max<int64_t>(n, 1));
     if (s2 == RAFTGP_OK) s2 = dalloc_t(ctx, &nch, (size_t)A.npairs);
     if (s2 == RAFTGP_OK) s2 = dalloc_t(ctx, &choff, (size_t)A.npairs + 1);
+    if (s2 == RAFTGP_OK) s2 = dalloc_t(ctx, &qp, (size_t)A.npairs);
+    A.P = P;
+    A.Q = Q;
+    A.thm = thm;
+    A.qp = qp;
     if (s2 == RAFTGP_OK) {
         {
             LaunchScope LS(ctx, K_SBM);
-            sbm_tables<<<grid1(K, 128), 128, 0, st>>>(K, A.boff, A.mem, theta, P, Q);
+            sbm_gather_theta<<<grid1(n, 256), 256, 0, st>>>(A.mem, theta, n, thm);
         }
         {
             LaunchScope LS(ctx, K_SBM);
-            sbm_pair_chunks<<<grid1(A.npairs, 256), 256, 0, st>>>(K, A.npairs, A.boff, omega, q, nch);
+            sbm_tables<<<grid1(K, 32), 32, 0, st>>>(K, A.boff, thm, P, Q);
+        }
+        {
+            LaunchScope LS(ctx, K_SBM);
+            sbm_pair_chunks<<<grid1(A.npairs, 128), 128, 0, st>>>(A, q, nch, qp);
         }
         s2 = scan_i32_to_i64(ctx, nch, choff, A.npairs);
     }
@@ -315,8 +375,6 @@ raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c,
         RG_CUDA(cudaMemcpyAsync(&nchunks, choff + A.npairs, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
         RG_CUDA(cudaStreamSynchronize(st));
     }
-    A.P = P;
-    A.Q = Q;
     A.choff = choff;
     A.nchunks = nchunks;
     int64_t total = 0;
@@ -342,7 +400,7 @@ raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c,
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) s2 = cuda_fail(e, "sbm kernels");
     }
-    dfree(ctx, P); dfree(ctx, Q); dfree(ctx, nch); dfree(ctx, choff); dfree(ctx, cnt); dfree(ctx, off);
+    dfree(ctx, P); dfree(ctx, Q); dfree(ctx, thm); dfree(ctx, qp); dfree(ctx, nch); dfree(ctx, choff); dfree(ctx, cnt); dfree(ctx, off);
     drop_members();
     if (s2 == RAFTGP_OK) *m_out = total;
     return s2;

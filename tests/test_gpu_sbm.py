@@ -82,3 +82,15 @@ def test_capacity_protocol_and_errors(rg, ctx):
         rg.raftgp_sbm_sample(ctx, ct, -tt, ot, 5)
     with pytest.raises(rg.RaftGPError):
         rg.raftgp_sbm_sample(ctx, ct, tt, ot, 5, q=3)
+
+
+def test_parity_diagonal_heavy(rg, ctx):
+    """One dense block plus sparse ones: per-pair chunk sizes hit the 2^4 floor on the diagonal pair."""
+    rng = np.random.default_rng(11)
+    n, K = 600, 4
+    c = np.where(rng.random(n) < 0.5, 0, rng.integers(1, K, n)).astype(np.int32)
+    th = rng.uniform(0.5, 2.0, n)
+    om = np.full((K, K), 0.002)
+    om[0, 0] = 0.05
+    for q in (4, 8, 20):
+        _check(*_both(rg, ctx, c, th, om, 3, q))
