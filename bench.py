@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--select-reps", type=int, default=3)
     ap.add_argument("--no-table1", action="store_true", help="skip the NEXT-2 Table I widths measurement")
     ap.add_argument("--table1-steps", type=int, default=3)
+    ap.add_argument("--no-sbm", action="store_true", help="skip the NEXT-3 SBM sampler measurement")
     ap.add_argument("--clock-period-ms", type=int, default=200)
     ap.add_argument("--clock-query", default=None)
     ap.add_argument("--no-clocks", action="store_true")
@@ -267,6 +268,50 @@ def measure_select(args, rg, ctx, gr, src_d, dst_d, variants, dims, Zbuf, barrie
                                "bytes_rule": "visited rows * 24 (segment, side, bounds r/w) + read rows * (4L + 4)"},
         }
     g.close()
+    return out
+
+
+def measure_sbm(args, rg, dev, barrier):
+    """NEXT-3: Alg. 2 sampling the C4 DC-SBM (N = 5e6, K = 500, ~1e8 expected edges) with
+    raftgp_sbm_sample (parameters resident on the device; the call is synchronous: count pass, scan, write
+    pass). Reports edges/s, per-kernel times and the oracle's rate on C2's parameters (same algorithm, one core)."""
+    import time
+    import torch
+    import synth
+    c, th, om = synth.sbm_params("C4", args.seed, rule=args.rule)
+    ct, tt, ot = (torch.from_numpy(x).to(dev) for x in (c, th, om))
+    ctx = rg.Context(dev.index)
+    src, dst = rg.raftgp_sbm_sample(ctx, ct, tt, ot, 0)              # warm-up, sizes the output
+    cap = int(src.numel() * 1.05) + 1024
+    ctx.prof_reset()
+    ctx.set_profiling(True)
+    barrier()
+    reps = 3
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(ctx.stream)
+    edges = 0
+    for i in range(reps):
+        s_, d_ = rg.raftgp_sbm_sample(ctx, ct, tt, ot, 1 + i, cap=cap)
+        edges += s_.numel()
+    e1.record(ctx.stream)
+    barrier()
+    ms = e0.elapsed_time(e1) / reps
+    prof = {k: round(t / reps, 3) for k, (t, c_) in sorted(ctx.prof_read().items(), key=lambda x: -x[1][0])}
+    ctx.set_profiling(False)
+    out = {"workload": f"C4 DC-SBM parameters (N={c.size:,}, K={om.shape[0]}), q = 20", "ms": ms,
+           "edges_per_call": edges / reps, "value": edges / reps / (ms * 1e-3), "unit": "edges/s",
+           "kernel_ms": prof}
+    if not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        c2, th2, om2 = synth.sbm_params("C2", args.seed)
+        t0 = time.perf_counter()
+        s2, _ = oracle.sbm_sample(c2, th2, om2, 1)
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": s2.size / dt, "unit": "edges/s", "cores": 1, "kind": "oracle",
+                               "sample": f"oracle.sbm_sample on C2's parameters (N={c2.size:,}, {s2.size:,} edges), "
+                                         f"{dt:.2f} s, single thread"}
     return out
 
 
@@ -499,6 +544,11 @@ def main():
     if world == 1 and not args.no_table1:
         table1 = measure_table1(args, rg, dev, barrier, peak, peak_src)
 
+    # ---------------- NEXT-3: Alg. 2 SBM sampler (N = 1 only)
+    sbm = None
+    if world == 1 and not args.no_sbm:
+        sbm = measure_sbm(args, rg, dev, barrier)
+
     # ---------------- e2e through the C-ABI with host buffers (H2D of edges, D2H of Z inside the timed region)
     # N = 1: three contexts on three streams, steps rotate over them, so a step's copies overlap other
     # steps' kernels (multi-buffering with the public API); every step still copies its own edges in and
@@ -590,6 +640,7 @@ def main():
             "hops": hop_stats,
             "model_selection": select,
             "table1_widths": table1,
+            "sbm_sampler": sbm,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
