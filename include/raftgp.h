@@ -39,6 +39,7 @@ extern "C" {
 
 typedef struct raftgp_ctx_s *raftgp_ctx;     /* device + stream + profiling state; library-owned */
 typedef struct raftgp_graph_s *raftgp_graph; /* device CSR (local rows) + degree scalars; library-owned */
+typedef struct raftgp_stream_s *raftgp_stream; /* a graph + its NCut embedding state, updated by edge additions */
 
 typedef enum {
     RAFTGP_OK = 0,
@@ -254,6 +255,29 @@ RAFTGP_API raftgp_status raftgp_gemm_tf32x3(raftgp_ctx ctx, int64_t M, int32_t K
 RAFTGP_API raftgp_status raftgp_sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c_dev,
                                            const double *theta_dev, const double *omega_dev, uint64_t seed, int32_t q,
                                            int32_t *src_dev, int32_t *dst_dev, int64_t cap, int64_t *m_out);
+
+/* ---------------------------------------------------------------- NEXT-4: streaming updates
+ * PAPER.md:207-214 (§III-D): after edges E' are added only the multi-hop neighbourhood of the nodes V' whose
+ * degree changed is re-embedded. A stream holds the graph and the state of the X = M (NCut) embedding of
+ * raftgp_embed (Theta' = Theta W^(1), the GCN operands T_1..T_L and Z). raftgp_stream_add_edges merges E' into
+ * the CSR (duplicates and self-loops drop out), recomputes the feature-hop rows of R_1 = V' u N(V') and the
+ * GCN hop-k rows of R_{k+1} = R_k u N(R_k) (new graph) with the same kernels as raftgp_embed, so Z is
+ * bit-identical to raftgp_embed(NCUT) on the whole new graph. (Q and Q~ depend on 2e, which changes every row
+ * when an edge is added: their exact update is the full recompute, so streams are NCut only.)
+ *   raftgp_stream_create: g = whole-graph handle, ownership passes to the stream (do not destroy it);
+ *     dims[0] = r and every width in {32, 64, 128}. Synchronous state build.
+ *   raftgp_stream_add_edges: m pairs (host or device per flags). stats: host int64[layers + 3] or NULL:
+ *     {|V'|, |R_1|, ..., |R_{layers+1}|, nnz of the new graph}. Synchronous.
+ *   raftgp_stream_embedding: copies Z (n x dims[layers], device) out (async on the context stream).
+ *   raftgp_stream_graph: borrowed handle of the current graph (export / scoring), valid until the next add.
+ * Errors: PARAM (widths, arguments), DATA (node id outside [0, n)), STATE, NOMEM, CUDA. */
+RAFTGP_API raftgp_status raftgp_stream_create(raftgp_graph g, int32_t layers, const int32_t *dims, uint64_t seed,
+                                              raftgp_stream *out);
+RAFTGP_API raftgp_status raftgp_stream_add_edges(raftgp_stream s, int64_t m, const int32_t *src, const int32_t *dst,
+                                                 uint32_t flags, int64_t *stats);
+RAFTGP_API raftgp_status raftgp_stream_embedding(raftgp_stream s, float *Z_dev);
+RAFTGP_API raftgp_status raftgp_stream_graph(raftgp_stream s, raftgp_graph *g_out);
+RAFTGP_API raftgp_status raftgp_stream_destroy(raftgp_stream s);
 
 #ifdef __cplusplus
 }

@@ -18,7 +18,7 @@ namespace raftgp {
 
 const char *const kKernelNames[K_NUM] = {
     "csr_count", "scan", "csr_scatter", "csr_sort_warp", "csr_sort_block", "csr_compact", "degree_scalars",
-    "sketch", "g_partials", "g_final", "feature_hop", "transform", "gcn_hop", "hop_generic", "misc", "csr_partition", "csr_bucket_sort", "row_order", "model_select", "select_seed", "select_lloyd", "select_split", "gemm_tf32x3", "gemm_tile", "wide_hop", "sbm_setup", "sbm_walk"};
+    "sketch", "g_partials", "g_final", "feature_hop", "transform", "gcn_hop", "hop_generic", "misc", "csr_partition", "csr_bucket_sort", "row_order", "model_select", "select_seed", "select_lloyd", "select_split", "gemm_tf32x3", "gemm_tile", "wide_hop", "sbm_setup", "sbm_walk", "stream_update"};
 
 static thread_local std::string g_last_error;
 
@@ -846,6 +846,64 @@ raftgp_status raftgp_sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int3
     RG_TRY(set_device(ctx));
     return sbm_sample(ctx, n, K, c_dev, theta_dev, omega_dev, seed, q, src_dev, dst_dev, cap, m_out);
     RG_GUARD_END
+}
+
+// ---------------------------------------------------------------- NEXT-4: streaming updates
+raftgp_status raftgp_stream_create(raftgp_graph g, int32_t layers, const int32_t *dims, uint64_t seed,
+                                   raftgp_stream *out) {
+    RG_GUARD_BEGIN
+    if (!out) return fail(RAFTGP_ERR_PARAM, "null out");
+    *out = nullptr;
+    RG_TRY(need_ready(g));
+    RG_TRY(whole_graph(g));
+    RG_TRY(check_dims(layers, dims));
+    RG_TRY(set_device(g->ctx));
+    return stream_create(g, layers, dims, seed, out);
+    RG_GUARD_END
+}
+
+raftgp_status raftgp_stream_add_edges(raftgp_stream s, int64_t m, const int32_t *src, const int32_t *dst,
+                                      uint32_t flags, int64_t *stats) {
+    RG_GUARD_BEGIN
+    if (!s) return fail(RAFTGP_ERR_PARAM, "null stream");
+    if (m < 0 || (m > 0 && (!src || !dst)) || flags > 1u) return fail(RAFTGP_ERR_PARAM, "bad edge arguments");
+    raftgp_ctx ctx = s->ctx;
+    RG_TRY(set_device(ctx));
+    const int32_t *dsrc = src, *ddst = dst;
+    int32_t *tmp = nullptr;
+    if (flags == RAFTGP_HOST_PTRS && m > 0) {
+        RG_TRY(dalloc_t(ctx, &tmp, 2 * (size_t)m));
+        RG_CUDA(cudaMemcpyAsync(tmp, src, sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
+        RG_CUDA(cudaMemcpyAsync(tmp + m, dst, sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
+        dsrc = tmp;
+        ddst = tmp + m;
+    }
+    raftgp_status st = stream_add(s, m, dsrc, ddst, stats);
+    dfree(ctx, tmp);
+    return st;
+    RG_GUARD_END
+}
+
+raftgp_status raftgp_stream_embedding(raftgp_stream s, float *Z_dev) {
+    if (!s || (!Z_dev && s->g->n > 0)) return fail(RAFTGP_ERR_PARAM, "null argument");
+    RG_TRY(set_device(s->ctx));
+    if (s->g->n > 0)
+        RG_CUDA(cudaMemcpyAsync(Z_dev, s->Z, sizeof(float) * (size_t)s->g->n * s->dims[s->layers],
+                                cudaMemcpyDeviceToDevice, s->ctx->stream));
+    return RAFTGP_OK;
+}
+
+raftgp_status raftgp_stream_graph(raftgp_stream s, raftgp_graph *g_out) {
+    if (!s || !g_out) return fail(RAFTGP_ERR_PARAM, "null argument");
+    *g_out = s->g;
+    return RAFTGP_OK;
+}
+
+raftgp_status raftgp_stream_destroy(raftgp_stream s) {
+    if (!s) return RAFTGP_OK;
+    cudaSetDevice(s->ctx->device);
+    stream_destroy(s);
+    return RAFTGP_OK;
 }
 
 }  // extern "C"

@@ -43,6 +43,7 @@ enum KernelId : int {
     K_WIDE_HOP,
     K_SBM,
     K_SBM_WALK,
+    K_STREAM,
     K_NUM
 };
 extern const char *const kKernelNames[K_NUM];
@@ -87,6 +88,19 @@ struct raftgp_graph_s {
     bool host_valid = false;
     std::vector<int64_t> h_row_ptr;
     std::vector<int32_t> h_col;
+};
+
+// NEXT-4 (stream.cu): a graph + the state of its NCut embedding
+struct raftgp_stream_s {
+    raftgp_ctx ctx = nullptr;
+    raftgp_graph g = nullptr;
+    int32_t layers = 0;
+    std::vector<int32_t> dims;
+    uint64_t seed = 0;
+    float *thw = nullptr;               // Theta' (n x dims[1])
+    std::vector<float *> T;             // T[k], k = 1..layers (n x dims[k])
+    std::vector<float *> W;             // W[k], k = 2..layers (dims[k-1] x dims[k])
+    float *Z = nullptr;                 // n x dims[layers]
 };
 
 namespace raftgp {
@@ -173,6 +187,11 @@ raftgp_status feature_hop_pre(raftgp_graph g, int variant_or_dual, int32_t l1, c
 raftgp_status gcn_transform(raftgp_graph g, const float *Z, int32_t lin, const float *W, int32_t lout, float *T);
 raftgp_status gcn_hop(raftgp_graph g, const float *Tfull, int32_t w, float *Zout, const float *Wn, int32_t wn,
                       float *Tnext, int32_t tn_ld = 0);
+// the same hops over a list of local rows (NEXT-4 streaming)
+raftgp_status feature_hop_pre_rows(raftgp_graph g, int variant, int32_t l1, const float *theta_w, const double *gvec_w,
+                                   float *T, const int32_t *rows, int64_t count);
+raftgp_status gcn_hop_rows(raftgp_graph g, const float *Tfull, int32_t w, float *Zout, const float *Wn, int32_t wn,
+                           float *Tnext, const int32_t *rows, int64_t count);
 // last GCN hop of two variants over the interleaved operand [T_a | T_b] (n x 2d); d in {32, 64}
 bool gcn_pair_supported(int32_t d);
 raftgp_status gcn_final_pair(raftgp_graph g, const float *Tboth, int32_t d, float *Za, float *Zb);
@@ -191,6 +210,10 @@ raftgp_status gemm_rowmajor(raftgp_ctx ctx, const float *A, int64_t M, int K, co
 bool wide_supported(int32_t layers, const int32_t *dims);
 raftgp_status embed_wide(raftgp_graph g, int32_t nvariants, const int32_t *variants, int32_t layers,
                          const int32_t *dims, uint64_t seed, float *const *Z_dev, const int where[3]);
+// NEXT-4: streaming updates (stream.cu)
+raftgp_status stream_create(raftgp_graph g, int32_t layers, const int32_t *dims, uint64_t seed, raftgp_stream *out);
+raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const int32_t *dst, int64_t *stats);
+void stream_destroy(raftgp_stream s);
 // NEXT-3: Alg. 2 exact SBM sampler (sbm.cu)
 raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c, const double *theta,
                          const double *omega, uint64_t seed, int32_t q, int32_t *src, int32_t *dst, int64_t cap,

@@ -556,6 +556,50 @@ raftgp_status feature_hop_pre(raftgp_graph g, int variant_or_dual, int32_t l1, c
     }
 }
 
+// Row-list variants (NEXT-4 streaming): the same kernels over `count` local rows listed in `rows` (the
+// kernels' visiting-order hook; every row's arithmetic is unchanged, so the rows come out bit-identical).
+raftgp_status feature_hop_pre_rows(raftgp_graph g, int variant, int32_t l1, const float *theta_w, const double *gvec_w,
+                                   float *T, const int32_t *rows, int64_t count) {
+    if (count == 0) return RAFTGP_OK;
+    HopArgs a = base_args(g, l1);
+    a.nl = count;
+    a.order = rows;
+    a.X = theta_w;
+    a.gvec = gvec_w;
+    a.out = T;
+    a.scale_sh = true;
+    if (!((l1 == 32 || l1 == 64 || l1 == 128) && aligned16(theta_w) && aligned16(T)))
+        return fail(RAFTGP_ERR_INTERNAL, "feature_hop_pre_rows: unsupported width/alignment");
+    auto go = [&](auto kind_tag) -> raftgp_status {
+        constexpr int K = decltype(kind_tag)::value;
+        switch (l1) {
+            case 32: return launch_fast<K, 32, 0>(g->ctx, a);
+            case 64: return launch_fast<K, 64, 0>(g->ctx, a);
+            default: return launch_fast<K, 128, 0>(g->ctx, a);
+        }
+    };
+    switch (variant) {
+        case RAFTGP_NCUT: return go(std::integral_constant<int, KIND_NCUT>());
+        case RAFTGP_MOD: return go(std::integral_constant<int, KIND_MOD>());
+        default: return go(std::integral_constant<int, KIND_MOD_REDUCED>());
+    }
+}
+
+raftgp_status gcn_hop_rows(raftgp_graph g, const float *Tfull, int32_t w, float *Zout, const float *Wn, int32_t wn,
+                           float *Tnext, const int32_t *rows, int64_t count) {
+    if (count == 0) return RAFTGP_OK;
+    HopArgs a = base_args(g, w);
+    a.nl = count;
+    a.order = rows;
+    a.X = Tfull;
+    a.out = Zout;
+    a.Wn = Wn;
+    a.Tn = Tnext;
+    if (!((w == 32 || w == 64 || w == 128) && (wn == 0 || wn == 32 || wn == 64 || wn == 128)))
+        return fail(RAFTGP_ERR_INTERNAL, "gcn_hop_rows: unsupported width");
+    return dispatch<KIND_GCN>(g->ctx, a, w, Wn ? wn : 0);
+}
+
 raftgp_status gcn_transform(raftgp_graph g, const float *Z, int32_t lin, const float *W, int32_t lout, float *T) {
     HopArgs a = base_args(g, lin);
     a.X = Z;

@@ -35,7 +35,8 @@ EXPORTS = (
     "raftgp_graph_local_degrees", "raftgp_graph_set_degrees", "raftgp_graph_set_order", "raftgp_graph_destroy", "raftgp_sketch",
     "raftgp_weights", "raftgp_project", "raftgp_gcn_transform", "raftgp_gcn_hop", "raftgp_gnn_embed",
     "raftgp_embed", "raftgp_embed_multi", "raftgp_feature_transform", "raftgp_modularity", "raftgp_ncut", "raftgp_local_modularity",
-    "raftgp_model_select", "raftgp_gemm_tf32x3", "raftgp_sbm_sample",
+    "raftgp_model_select", "raftgp_gemm_tf32x3", "raftgp_sbm_sample", "raftgp_stream_create",
+    "raftgp_stream_add_edges", "raftgp_stream_embedding", "raftgp_stream_graph", "raftgp_stream_destroy",
 )
 
 _lib = None
@@ -88,6 +89,11 @@ _SIGS = {
     "raftgp_model_select": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, P(c_i32), c_vp]),
     "raftgp_gemm_tf32x3": (ctypes.c_int, [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "raftgp_sbm_sample": (ctypes.c_int, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_u64, c_i32, c_vp, c_vp, c_i64, P(c_i64)]),
+    "raftgp_stream_create": (ctypes.c_int, [c_vp, c_i32, c_vp, c_u64, P(c_vp)]),
+    "raftgp_stream_add_edges": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_u32, c_vp]),
+    "raftgp_stream_embedding": (ctypes.c_int, [c_vp, c_vp]),
+    "raftgp_stream_graph": (ctypes.c_int, [c_vp, P(c_vp)]),
+    "raftgp_stream_destroy": (ctypes.c_int, [c_vp]),
 }
 
 
@@ -466,3 +472,55 @@ def _expected_edges(c, theta, omega) -> float:
     t2 = torch.zeros(K, dtype=torch.float64, device=theta.device).index_add_(0, c.long(), theta * theta)
     tot = (ts[:, None] * ts[None, :] * omega).sum() - (t2 * torch.diagonal(omega)).sum()
     return float(tot.item()) / 2
+
+
+# ------------------------------------------------------------------ NEXT-4: streaming updates
+class Stream:
+    """raftgp_stream: a graph (ownership taken from `graph`) and its NCut embedding, updated by edge additions."""
+
+    def __init__(self, graph: Graph, dims: Sequence[int], seed: int):
+        self.ctx = graph.ctx
+        self.dims = [int(d) for d in dims]
+        h = c_vp()
+        d = (c_i32 * len(self.dims))(*self.dims)
+        _ck(load_library().raftgp_stream_create(graph.h, len(self.dims) - 1, d, seed, ctypes.byref(h)))
+        graph.h = None          # owned by the stream now
+        self.h = h
+
+    def add_edges(self, src: torch.Tensor, dst: torch.Tensor) -> dict:
+        """Merge the pairs (src, dst) into the graph and re-embed the affected rows; returns the set sizes."""
+        if src.dtype != torch.int32 or dst.dtype != torch.int32 or src.numel() != dst.numel():
+            raise ValueError("src/dst must be int32 tensors of equal length")
+        L = len(self.dims) - 1
+        st = np.zeros(L + 3, np.int64)
+        flags = RAFTGP_DEVICE_PTRS if src.is_cuda else RAFTGP_HOST_PTRS
+        s, d = src.contiguous(), dst.contiguous()
+        _ck(load_library().raftgp_stream_add_edges(self.h, s.numel(), _ptr(s), _ptr(d), flags, c_vp(st.ctypes.data)))
+        return {"changed": int(st[0]), "affected": [int(x) for x in st[1:L + 2]], "nnz": int(st[L + 2])}
+
+    def embedding(self) -> torch.Tensor:
+        n = self.graph().n
+        Z = torch.empty((max(1, n), self.dims[-1]), dtype=torch.float32, device=self.ctx.device)[:n]
+        _ck(load_library().raftgp_stream_embedding(self.h, _ptr(Z)))
+        return Z
+
+    def graph(self) -> Graph:
+        """Borrowed handle of the current graph (valid until the next add_edges; never destroyed by Python)."""
+        h = c_vp()
+        _ck(load_library().raftgp_stream_graph(self.h, ctypes.byref(h)))
+        g = Graph.__new__(Graph)
+        g.ctx = self.ctx
+        g.h = h
+        g.close = lambda: None   # borrowed
+        return g
+
+    def close(self):
+        if getattr(self, "h", None) is not None and _lib is not None and not _exiting:
+            _lib.raftgp_stream_destroy(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,118 @@
+"""GPU checks of NEXT-4 — streaming updates — through the C-ABI (raftgp_stream_*).
+
+The streamed NCut embedding after adding edges must be BIT-IDENTICAL to raftgp_embed(NCUT) on a graph built
+from scratch with all the edges (every row's arithmetic depends only on its neighbour list and inputs), the
+recomputed sets must be exactly the (k)-hop closures of the changed nodes (checked with scipy on the host), and
+the result must match the oracle within 1e-4. Edge cases: duplicates of existing edges and self-loops (no
+change at all), edges to isolated nodes, empty batches, errors."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rg(cuda_required):
+    from paper_2312_01560_b200 import raftgp
+    raftgp.load_library()
+    return raftgp
+
+
+@pytest.fixture(scope="module")
+def ctx(rg):
+    return rg.Context(0)
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.int32))
+
+
+def _fresh_ncut(rg, ctx, n, src, dst, dims, seed):
+    g = rg.raftgp_build_csr(ctx, n, _t(src), _t(dst))
+    _, Z = rg.raftgp_embed_multi(g, ["ncut"], dims, seed)
+    return Z["ncut"]
+
+
+def _closures(n, src, dst, changed, L):
+    a = sp.coo_matrix((np.ones(src.size), (src, dst)), shape=(n, n)).tocsr()
+    a = ((a + a.T) > 0).astype(np.int8)
+    a.setdiag(0)
+    a.eliminate_zeros()
+    cur = changed.copy()
+    sizes = []
+    for _ in range(L + 1):
+        cur = cur | (a @ cur.astype(np.int8) > 0)
+        sizes.append(int(cur.sum()))
+    return sizes
+
+
+@pytest.mark.parametrize("cfg,n,dims,batches", [("C1", None, (64, 64, 32), 3), ("C2", 20000, (64, 64, 32), 2),
+                                                ("C1", None, (128, 64, 32, 32), 2)])
+def test_stream_equals_full_recompute(rg, ctx, cfg, n, dims, batches):
+    gr = synth.generate(cfg, 4, n=n)
+    rng = np.random.default_rng(9)
+    m = gr.src.size
+    held = rng.choice(m, size=min(m // 50, 400), replace=False)
+    keep = np.setdiff1d(np.arange(m), held)
+    src0, dst0 = gr.src[keep], gr.dst[keep]
+    # extra new edges between random nodes (some to nodes that were isolated in the base graph)
+    extra_s = rng.integers(0, gr.n, 40).astype(np.int32)
+    extra_d = rng.integers(0, gr.n, 40).astype(np.int32)
+    add_s = np.concatenate([gr.src[held], extra_s])
+    add_d = np.concatenate([gr.dst[held], extra_d])
+    g = rg.raftgp_build_csr(ctx, gr.n, _t(src0), _t(dst0))
+    stream = rg.Stream(g, dims, 5)
+    Z0 = stream.embedding().clone()
+    assert torch.equal(Z0, _fresh_ncut(rg, ctx, gr.n, src0, dst0, dims, 5))
+    cur_s, cur_d = src0, dst0
+    for part_s, part_d in zip(np.array_split(add_s, batches), np.array_split(add_d, batches)):
+        deg_before = np.bincount(np.concatenate([cur_s, cur_d])[np.concatenate([cur_s != cur_d] * 2)], minlength=gr.n)
+        st = stream.add_edges(_t(part_s), _t(part_d))
+        cur_s = np.concatenate([cur_s, part_s])
+        cur_d = np.concatenate([cur_d, part_d])
+        Zs = stream.embedding()
+        assert torch.equal(Zs, _fresh_ncut(rg, ctx, gr.n, cur_s, cur_d, dims, 5))
+        # recomputed sets = closures of the nodes whose (simple-graph) degree changed
+        go = oracle.build_csr(gr.n, cur_s, cur_d)
+        gb = oracle.build_csr(gr.n, cur_s[:-part_s.size] if part_s.size else cur_s,
+                              cur_d[:-part_d.size] if part_d.size else cur_d)
+        changed = go.deg != gb.deg
+        assert st["changed"] == int(changed.sum())
+        assert st["affected"] == _closures(gr.n, cur_s, cur_d, changed, len(dims) - 1)
+        assert st["nnz"] == go.nnz
+    Zo = oracle.gcn(go, list(dims), 5, oracle.project(go, "ncut", dims[0], 5))[-1]
+    e = np.linalg.norm(Zs.cpu().numpy() - Zo) / np.linalg.norm(Zo)
+    assert e <= 1e-4
+
+
+def test_stream_no_change_and_empty(rg, ctx):
+    gr = synth.generate("C1", 0)
+    g = rg.raftgp_build_csr(ctx, gr.n, _t(gr.src), _t(gr.dst))
+    stream = rg.Stream(g, (64, 64, 32), 1)
+    Z0 = stream.embedding().clone()
+    st = stream.add_edges(_t(gr.src[:25]), _t(gr.dst[:25]))          # all already present
+    assert st["changed"] == 0 and st["affected"] == [0, 0, 0]
+    st = stream.add_edges(_t(np.arange(10)), _t(np.arange(10)))        # self-loops only
+    assert st["changed"] == 0
+    st = stream.add_edges(_t(np.zeros(0)), _t(np.zeros(0)))            # empty batch
+    assert st["changed"] == 0
+    assert torch.equal(stream.embedding(), Z0)
+    host = stream.add_edges(torch.tensor([0], dtype=torch.int32), torch.tensor([999], dtype=torch.int32))
+    assert host["changed"] in (0, 2)
+
+
+def test_stream_errors(rg, ctx):
+    gr = synth.generate("C1", 0)
+    g = rg.raftgp_build_csr(ctx, gr.n, _t(gr.src), _t(gr.dst))
+    with pytest.raises(rg.RaftGPError) as e:
+        rg.Stream(g, (64, 48, 32), 1)
+    assert e.value.code == rg.RAFTGP_ERR_PARAM
+    stream = rg.Stream(g, (64, 64, 32), 1)
+    with pytest.raises(rg.RaftGPError) as e:
+        stream.add_edges(_t([0]), _t([gr.n + 5]))
+    assert e.value.code == rg.RAFTGP_ERR_DATA
