@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-table1", action="store_true", help="skip the NEXT-2 Table I widths measurement")
     ap.add_argument("--table1-steps", type=int, default=3)
     ap.add_argument("--no-sbm", action="store_true", help="skip the NEXT-3 SBM sampler measurement")
+    ap.add_argument("--no-stream", action="store_true", help="skip the NEXT-4 streaming-update measurement")
     ap.add_argument("--clock-period-ms", type=int, default=200)
     ap.add_argument("--clock-query", default=None)
     ap.add_argument("--no-clocks", action="store_true")
@@ -315,6 +316,45 @@ def measure_sbm(args, rg, dev, barrier):
     return out
 
 
+def measure_stream(args, rg, dev, barrier, gr, src_d, dst_d, dims):
+    """NEXT-4: streaming updates on the C4 graph, NCut embedding with the bench dims: the
+    time of raftgp_stream_add_edges for batches of B new random edges against a full rebuild + embed of the
+    same final graph (raftgp_build_csr + raftgp_embed_multi(ncut)), with the recomputed set sizes."""
+    import numpy as np
+    import torch
+    rng = np.random.default_rng(args.seed + 17)
+    out = {"workload": f"C4 graph (N={gr.n:,}), NCut, dims {list(dims)}", "batches": []}
+    ctx = rg.Context(dev.index)
+    for B in (10, 1000):
+        g = rg.raftgp_build_csr(ctx, gr.n, src_d, dst_d)
+        stream = rg.Stream(g, dims, args.seed)
+        es = torch.from_numpy(rng.integers(0, gr.n, B).astype(np.int32)).to(dev)
+        ed = torch.from_numpy(rng.integers(0, gr.n, B).astype(np.int32)).to(dev)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(ctx.stream)
+        st = stream.add_edges(es, ed)
+        e1.record(ctx.stream)
+        barrier()
+        t_stream = e0.elapsed_time(e1)
+        stream.close()
+        s_all, d_all = torch.cat([src_d, es]), torch.cat([dst_d, ed])
+        Z = {"ncut": torch.empty((gr.n, dims[-1]), dtype=torch.float32, device=dev)}
+        barrier()
+        e0.record(ctx.stream)
+        g2 = rg.raftgp_build_csr(ctx, gr.n, s_all, d_all)
+        rg.raftgp_embed_multi(g2, ["ncut"], dims, args.seed, Z=Z)
+        e1.record(ctx.stream)
+        barrier()
+        t_full = e0.elapsed_time(e1)
+        g2.close()
+        out["batches"].append({"new_edges": B, "stream_ms": t_stream, "full_rebuild_ms": t_full,
+                               "speedup": t_full / t_stream, "changed_nodes": st["changed"],
+                               "recomputed_rows": st["affected"]})
+    return out
+
+
 TABLE1_DIMS = (4096, 2048, 1024, 512, 256)   # PAPER.md:268-273, Table I row 2E5 (and 1E4-1E5)
 
 
@@ -549,6 +589,11 @@ def main():
     if world == 1 and not args.no_sbm:
         sbm = measure_sbm(args, rg, dev, barrier)
 
+    # ---------------- NEXT-4: streaming updates (N = 1 only)
+    stream = None
+    if world == 1 and not args.no_stream:
+        stream = measure_stream(args, rg, dev, barrier, gr, src_d, dst_d, dims)
+
     # ---------------- e2e through the C-ABI with host buffers (H2D of edges, D2H of Z inside the timed region)
     # N = 1: three contexts on three streams, steps rotate over them, so a step's copies overlap other
     # steps' kernels (multi-buffering with the public API); every step still copies its own edges in and
@@ -641,6 +686,7 @@ def main():
             "model_selection": select,
             "table1_widths": table1,
             "sbm_sampler": sbm,
+            "streaming": stream,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
