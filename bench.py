@@ -473,12 +473,12 @@ def main():
     fused_pair = (not args.no_fuse_variants) and "ncut" in variants and "mod" in variants
 
     def step_single(src, dst, out_host=None):
-        g = rg.raftgp_build_csr(ctx, gr.n, src, dst)
         if args.no_fuse_variants:
+            g = rg.raftgp_build_csr(ctx, gr.n, src, dst)
             for v in variants:
                 rg.raftgp_embed(g, v, dims, args.seed, Z=Zbuf[v], want_Y=False)
-        else:
-            rg.raftgp_embed_multi(g, variants, dims, args.seed, Z=Zbuf)
+        else:   # build + embed in one call: Theta' generated on a side stream during the CSR build
+            _, g = rg.raftgp_build_embed(ctx, gr.n, src, dst, variants, dims, args.seed, Z=Zbuf, keep_graph=True)
         if out_host is not None:
             for v in variants:
                 out_host[v].copy_(Zbuf[v], non_blocking=True)

@@ -190,6 +190,16 @@ RAFTGP_API raftgp_status raftgp_embed_multi(raftgp_graph g, int32_t nvariants, c
                                             const int32_t *dims, uint64_t seed, float *const *Y_dev,
                                             float *const *Z_dev);
 
+/* raftgp_build_csr (whole graph) + raftgp_embed_multi (Y not written) in one call: Theta' = Theta W^(1)
+ * depends only on the seed, so it is generated on a library-owned side stream while the CSR build runs on the
+ * context stream (tensor cores / ALUs against atomics / HBM); outputs are those of the two calls. Edge arrays
+ * host or device per flags. g_out: NULL, or receives the graph handle (caller destroys it). Synchronous like
+ * raftgp_build_csr; the embedding is enqueued on the context stream. Errors: those of the two calls. */
+RAFTGP_API raftgp_status raftgp_build_embed(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src, const int32_t *dst,
+                                            uint32_t flags, int32_t nvariants, const int32_t *variants, int32_t layers,
+                                            const int32_t *dims, uint64_t seed, float *const *Z_dev,
+                                            raftgp_graph *g_out);
+
 /* First GCN operand of every listed variant for the LOCAL rows (works on row-partitioned graphs):
  * T1 = s^ (.) (X Theta W^(1)) = s^ (.) (Y W^(1)), X the variant's feature operator, Theta and W^(1) as in
  * raftgp_embed. Theta' = Theta W^(1) is generated on chip (Theta never written) and NCUT + MOD share one

@@ -182,6 +182,10 @@ raftgp_status raftgp_ctx_destroy(raftgp_ctx ctx) {
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
     release_cache(ctx);
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->side) {
+        cudaStreamSynchronize(ctx->side);
+        cudaStreamDestroy(ctx->side);
+    }
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return RAFTGP_OK;
@@ -565,22 +569,29 @@ raftgp_status raftgp_embed(raftgp_graph g, raftgp_variant variant, int32_t layer
 // one gather), then the GCN stacks. Same results as the Y path up to fp32 rounding order (reading #13).
 // T1 = s^ (.) (X Theta W1) of the local rows for every listed variant (Theta' = Theta W1 on chip, one
 // shared gather for NCUT + MOD). T1[v]: local_rows x l1 device buffers.
+// T1 of every variant from Theta' = Theta W1 (thw_pre: already computed, e.g. on a side stream; else here)
 static raftgp_status first_transform_pre(raftgp_graph g, int32_t nvariants, const int32_t *variants, int32_t r,
-                                         int32_t l1, uint64_t seed, float *const *T1, const int where[3]) {
+                                         int32_t l1, uint64_t seed, float *const *T1, const int where[3],
+                                         const float *thw_pre = nullptr) {
     raftgp_ctx ctx = g->ctx;
     float *W1 = nullptr, *thw = nullptr;
     double *gw = nullptr;
-    raftgp_status st = dalloc_t(ctx, &W1, (size_t)r * l1);
-    if (st == RAFTGP_OK) st = sketch_fill(ctx, seed, 1u, 0, r, l1, r, W1);
-    if (st == RAFTGP_OK) st = dalloc_t(ctx, &thw, (size_t)g->n * l1);
+    raftgp_status st = RAFTGP_OK;
+    if (!thw_pre) {
+        st = dalloc_t(ctx, &W1, (size_t)r * l1);
+        if (st == RAFTGP_OK) st = sketch_fill(ctx, seed, 1u, 0, r, l1, r, W1);
+        if (st == RAFTGP_OK) st = dalloc_t(ctx, &thw, (size_t)g->n * l1);
+        if (st == RAFTGP_OK) st = sketch_w_any(ctx, seed, g->n, r, W1, l1, thw);
+    }
+    const float *tw = thw_pre ? thw_pre : thw;
     if (st == RAFTGP_OK && where[RAFTGP_MOD] >= 0) st = dalloc_t(ctx, &gw, (size_t)l1);
-    if (st == RAFTGP_OK) st = sketch_theta_w(g, seed, r, W1, l1, thw, gw);
+    if (st == RAFTGP_OK && gw) st = g_reduce(g, tw, l1, gw);
     const bool dual = where[RAFTGP_NCUT] >= 0 && where[RAFTGP_MOD] >= 0;
     if (st == RAFTGP_OK && dual)
-        st = feature_hop_pre(g, -1, l1, thw, gw, T1[where[RAFTGP_NCUT]], T1[where[RAFTGP_MOD]]);
+        st = feature_hop_pre(g, -1, l1, tw, gw, T1[where[RAFTGP_NCUT]], T1[where[RAFTGP_MOD]]);
     for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v) {
         if (dual && (variants[v] == RAFTGP_NCUT || variants[v] == RAFTGP_MOD)) continue;
-        st = feature_hop_pre(g, variants[v], l1, thw, gw, T1[v], nullptr);
+        st = feature_hop_pre(g, variants[v], l1, tw, gw, T1[v], nullptr);
     }
     dfree(ctx, thw);
     dfree(ctx, gw);
@@ -589,13 +600,14 @@ static raftgp_status first_transform_pre(raftgp_graph g, int32_t nvariants, cons
 }
 
 static raftgp_status embed_pre(raftgp_graph g, int32_t nvariants, const int32_t *variants, int32_t layers,
-                               const int32_t *dims, uint64_t seed, float *const *Z_dev, const int where[3]) {
+                               const int32_t *dims, uint64_t seed, float *const *Z_dev, const int where[3],
+                               const float *thw_pre = nullptr) {
     raftgp_ctx ctx = g->ctx;
     const int32_t r = dims[0], l1 = dims[1];
     std::vector<float *> T1(nvariants, nullptr);
     raftgp_status st = RAFTGP_OK;
     for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v) st = dalloc_t(ctx, &T1[v], (size_t)g->n * l1);
-    if (st == RAFTGP_OK) st = first_transform_pre(g, nvariants, variants, r, l1, seed, T1.data(), where);
+    if (st == RAFTGP_OK) st = first_transform_pre(g, nvariants, variants, r, l1, seed, T1.data(), where, thw_pre);
     const bool dual = where[RAFTGP_NCUT] >= 0 && where[RAFTGP_MOD] >= 0;
     for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v) {
         if (dual && variants[v] == RAFTGP_MOD) continue;    // computed with its NCUT partner below
@@ -904,6 +916,69 @@ raftgp_status raftgp_stream_destroy(raftgp_stream s) {
     cudaSetDevice(s->ctx->device);
     stream_destroy(s);
     return RAFTGP_OK;
+}
+
+// ---------------------------------------------------------------- build + embed with overlap
+// raftgp_build_csr + raftgp_embed_multi in one call. Theta' = Theta W^(1) depends only on the seed, so it is
+// generated on a side stream (tensor cores / ALUs) while the CSR build (atomics / HBM) runs on the context
+// stream; the results are those of the two separate calls.
+raftgp_status raftgp_build_embed(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src, const int32_t *dst,
+                                 uint32_t flags, int32_t nvariants, const int32_t *variants, int32_t layers,
+                                 const int32_t *dims, uint64_t seed, float *const *Z_dev, raftgp_graph *g_out) {
+    RG_GUARD_BEGIN
+    if (!ctx) return fail(RAFTGP_ERR_PARAM, "null ctx");
+    if (g_out) *g_out = nullptr;
+    RG_TRY(check_dims(layers, dims));
+    if (nvariants < 1 || !variants || !Z_dev) return fail(RAFTGP_ERR_PARAM, "need >= 1 variant and Z outputs");
+    if (n < 0 || n >= (int64_t)INT32_MAX || m < 0 || flags > 1u || (m > 0 && (!src || !dst)))
+        return fail(RAFTGP_ERR_PARAM, "bad graph arguments");
+    RG_TRY(set_device(ctx));
+    const int32_t r = dims[0], l1 = dims[1];
+    const bool overlap = sketch_w_supported(r, l1) && !wide_supported(layers, dims) && n > 0;
+    float *W1 = nullptr, *thw = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    raftgp_status st = RAFTGP_OK;
+    if (overlap) {
+        if (!ctx->side) RG_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+        RG_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+        RG_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+        st = dalloc_t(ctx, &W1, (size_t)r * l1);
+        if (st == RAFTGP_OK) st = dalloc_t(ctx, &thw, (size_t)n * l1);
+        if (st == RAFTGP_OK) {
+            RG_CUDA(cudaEventRecord(ev_fork, ctx->stream));
+            RG_CUDA(cudaStreamWaitEvent(ctx->side, ev_fork, 0));
+            cudaStream_t main = ctx->stream;
+            ctx->stream = ctx->side;   // the sketch kernels enqueue on the side stream
+            st = sketch_fill(ctx, seed, 1u, 0, r, l1, r, W1);
+            if (st == RAFTGP_OK) st = sketch_w_any(ctx, seed, n, r, W1, l1, thw);
+            ctx->stream = main;
+            RG_CUDA(cudaEventRecord(ev_join, ctx->side));
+        }
+    }
+    raftgp_graph g = nullptr;
+    if (st == RAFTGP_OK) st = raftgp_build_csr(ctx, n, m, src, dst, 0, n, flags, &g);
+    if (overlap && ev_join) cudaStreamWaitEvent(ctx->stream, ev_join, 0);   // Theta' ready (also on failure)
+    if (st == RAFTGP_OK) {
+        int where[3] = {-1, -1, -1};
+        for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v) {
+            st = check_variant(g, variants[v], r);
+            if (st == RAFTGP_OK && where[variants[v]] >= 0) st = fail(RAFTGP_ERR_PARAM, "variant listed twice");
+            if (st == RAFTGP_OK) where[variants[v]] = v;
+            if (st == RAFTGP_OK && !Z_dev[v]) st = fail(RAFTGP_ERR_PARAM, "null Z");
+        }
+        if (st == RAFTGP_OK) {
+            if (overlap) st = embed_pre(g, nvariants, variants, layers, dims, seed, Z_dev, where, thw);
+            else st = raftgp_embed_multi(g, nvariants, variants, layers, dims, seed, nullptr, Z_dev);
+        }
+    }
+    dfree(ctx, W1);
+    dfree(ctx, thw);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (st == RAFTGP_OK && g_out) *g_out = g;
+    else if (g) raftgp_graph_destroy(g);
+    return st;
+    RG_GUARD_END
 }
 
 }  // extern "C"

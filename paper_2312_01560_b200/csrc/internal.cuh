@@ -58,6 +58,7 @@ struct ProfRec {
 struct raftgp_ctx_s {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;   // library-owned side stream (overlapped work inside one call)
     bool own_stream = false;
     int sm_count = 148;
     int64_t launches = 0;

@@ -60,10 +60,20 @@ __global__ void __launch_bounds__(128) g_partials(const float *__restrict__ thet
     }
 }
 
+// g[c] = sum over chunks in chunk order (sequential per column; operands loaded 8 ahead so the fp64 add chain,
+// not the load latency, sets the pace)
 __global__ void g_final(const double *__restrict__ partial, int64_t nchunks, int32_t r, double *__restrict__ g) {
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < r; c += gridDim.x * blockDim.x) {
         double acc = 0.0;
-        for (int64_t k = 0; k < nchunks; ++k) acc += partial[k * r + c];
+        int64_t k = 0;
+        for (; k + 8 <= nchunks; k += 8) {
+            double v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = __ldg(partial + (k + j) * r + c);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc += v[j];
+        }
+        for (; k < nchunks; ++k) acc += partial[k * r + c];
         g[c] = acc;
     }
 }
@@ -227,7 +237,7 @@ raftgp_status g_reduce(raftgp_graph g, const float *theta, int32_t r, double *g_
     RG_CHECK_LAUNCH(ctx);
     {
         LaunchScope L(ctx, K_G_FINAL);
-        g_final<<<(unsigned)ceil_div(r, 128), 128, 0, ctx->stream>>>(partial, nchunks, r, g_out);
+        g_final<<<(unsigned)ceil_div(r, 32), 32, 0, ctx->stream>>>(partial, nchunks, r, g_out);
     }
     RG_CHECK_LAUNCH(ctx);
     dfree(ctx, partial);

@@ -37,6 +37,7 @@ EXPORTS = (
     "raftgp_embed", "raftgp_embed_multi", "raftgp_feature_transform", "raftgp_modularity", "raftgp_ncut", "raftgp_local_modularity",
     "raftgp_model_select", "raftgp_gemm_tf32x3", "raftgp_sbm_sample", "raftgp_stream_create",
     "raftgp_stream_add_edges", "raftgp_stream_embedding", "raftgp_stream_graph", "raftgp_stream_destroy",
+    "raftgp_build_embed",
 )
 
 _lib = None
@@ -94,6 +95,8 @@ _SIGS = {
     "raftgp_stream_embedding": (ctypes.c_int, [c_vp, c_vp]),
     "raftgp_stream_graph": (ctypes.c_int, [c_vp, P(c_vp)]),
     "raftgp_stream_destroy": (ctypes.c_int, [c_vp]),
+    "raftgp_build_embed": (ctypes.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_u32, c_i32, c_vp, c_i32, c_vp, c_u64, c_vp,
+                                          P(c_vp)]),
 }
 
 
@@ -370,6 +373,27 @@ def raftgp_embed_multi(g: Graph, variants: Sequence, dims: Sequence[int], seed: 
                                           _zk_array([Y[nm] for nm in names]) if want_Y else None,
                                           _zk_array([Z[nm] for nm in names])))
     return Y, Z
+
+
+def raftgp_build_embed(ctx: Context, n: int, src: torch.Tensor, dst: torch.Tensor, variants: Sequence,
+                       dims: Sequence[int], seed: int, Z=None, keep_graph: bool = False):
+    """raftgp_build_csr + raftgp_embed_multi in one call (Theta' overlapped with the CSR build on a side stream).
+    Returns ({variant: Z}, Graph or None)."""
+    if src.dtype != torch.int32 or dst.dtype != torch.int32 or src.numel() != dst.numel():
+        raise ValueError("src/dst must be int32 tensors of equal length")
+    dims = [int(d) for d in dims]
+    vs = [_variant(v) for v in variants]
+    names = [v if isinstance(v, str) else {0: "ncut", 1: "mod", 2: "mod_reduced"}[int(v)] for v in variants]
+    Z = Z or {nm: torch.empty((n, dims[-1]), dtype=torch.float32, device=ctx.device) for nm in names}
+    flags = RAFTGP_DEVICE_PTRS if src.is_cuda else RAFTGP_HOST_PTRS
+    s, d = src.contiguous(), dst.contiguous()
+    va = (c_i32 * len(vs))(*vs)
+    dd = (c_i32 * len(dims))(*dims)
+    h = c_vp()
+    _ck(load_library().raftgp_build_embed(ctx.h, n, s.numel(), _ptr(s), _ptr(d), flags, len(vs), va, len(dims) - 1, dd,
+                                          seed, _zk_array([Z[nm] for nm in names]),
+                                          ctypes.byref(h) if keep_graph else None))
+    return Z, (Graph(ctx, h) if keep_graph else None)
 
 
 def raftgp_feature_transform(g: Graph, variants: Sequence, r: int, l1: int, seed: int) -> dict:

@@ -330,3 +330,20 @@ def test_sketch_transform_tcgen05(rg, ctx, n, r, l1):
     ref = oracle.theta(n, r, 9).astype(np.float64) @ W.astype(np.float64)
     assert rel_fro(got, ref) < 5e-6
     assert np.max(np.abs(got - ref)) < 1e-5 * max(1.0, np.abs(ref).max())
+
+
+@pytest.mark.parametrize("variants", [["ncut", "mod"], ["mod_reduced"], ["ncut", "mod", "mod_reduced"]])
+def test_build_embed_equals_separate_calls(rg, ctx, variants):
+    """raftgp_build_embed (Theta' on a side stream during the CSR build) gives exactly the two-call results."""
+    gr = synth.generate("C2", 2)
+    src, dst = torch.from_numpy(gr.src).cuda(), torch.from_numpy(gr.dst).cuda()
+    dims = (64, 64, 32)
+    Z1, g1 = rg.raftgp_build_embed(ctx, gr.n, src, dst, variants, dims, 3, keep_graph=True)
+    g2 = rg.raftgp_build_csr(ctx, gr.n, src, dst)
+    _, Z2 = rg.raftgp_embed_multi(g2, variants, dims, 3)
+    for v in variants:
+        assert torch.equal(Z1[v], Z2[v])
+    assert np.array_equal(g1.export()[1], g2.export()[1])
+    Z3, _ = rg.raftgp_build_embed(ctx, gr.n, torch.from_numpy(gr.src), torch.from_numpy(gr.dst), variants, dims, 3)
+    for v in variants:
+        assert torch.equal(Z3[v], Z2[v])
