@@ -260,13 +260,13 @@ struct WideArgs {
 };
 
 template <int KIND, int V, int U>
-__global__ void __launch_bounds__(128) hop_wide(WideArgs a) {
+__global__ void __launch_bounds__(512) hop_wide(WideArgs a) {
     constexpr int CW = 128 * V;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int NW = a.W / CW;                 // warps (slices) per row: 1, 2 or 4
-    const int rpc = 4 / NW;                  // rows per CTA iteration
+    const int NW = a.W / CW;                 // warps (slices) per row
+    const int rpc = (int)(blockDim.x >> 5) / NW;   // rows per CTA iteration
     const int rsub = wib / NW, slice = wib % NW;
-    __shared__ float ssq[4];
+    __shared__ float ssq[16];
     const float4 *X4 = reinterpret_cast<const float4 *>(a.X);
     const int64_t W4 = a.W / 4;
     const int64_t cbase = (int64_t)slice * (CW / 4);   // first float4 column of this slice
@@ -605,7 +605,12 @@ bool wide_ring_enabled() {
 }
 
 // slices (partial sums of squares) per row written by a deferred-normalisation GCN hop of width w
-int wide_ssq_slices(int32_t w) { return (wide_ring_enabled() && w >= 512) ? 4 : w / (128 * (w == 256 ? 2 : 4)); }
+int wide_ssq_slices(int32_t w) {
+    if (wide_ring_enabled() && w >= 512) return 4;
+    const char *e = getenv("RAFTGP_WIDE_V");
+    const int v = (e && e[0] == '1') ? 1 : (w == 256 ? 2 : 4);
+    return w / (128 * v);
+}
 
 template <int KIND>
 raftgp_status launch_wide(raftgp_ctx ctx, const WideArgs &a) {
@@ -637,17 +642,24 @@ raftgp_status launch_wide(raftgp_ctx ctx, const WideArgs &a) {
             default: return go(std::integral_constant<int, 2048>());
         }
     }
-    // V float4 per lane per slice: 256 -> V 2 (one warp per row); 512 -> 4 (1 warp); 1024 -> 4 (2); 2048 -> 4 (4)
-    const int V = a.W == 256 ? 2 : 4;
+    // V float4 per lane per slice: 4 = 512-column slices (default; 256-wide rows use V = 2); RAFTGP_WIDE_V=1 =
+    // 128-column slices, W/128 warps per row at 64 registers (measured slower at 2E5: 77 vs 69 ms of wide hops)
+    static const int Vsel = [] {
+        const char *e = getenv("RAFTGP_WIDE_V");
+        return (e && e[0] == '1') ? 1 : 4;
+    }();
+    const int V = a.W == 256 ? (Vsel == 4 ? 2 : 1) : Vsel;
     const int NW = a.W / (128 * V);
-    const int rpc = 4 / NW;
-    const int64_t per_sm = 16;   // 128-thread CTAs per SM in the grid (grid-stride over rows)
+    const int warps = std::max(4, NW);
+    const int rpc = warps / NW;
+    const int64_t per_sm = 2048 / (32 * warps);   // CTAs per SM in the grid (grid-stride over rows)
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.n, rpc), ctx->sm_count * per_sm));
     LaunchScope LS(ctx, K_WIDE_HOP);
     // neighbours in flight per lane: U x V float4 (DUAL keeps two accumulator sets, so a smaller U)
     constexpr int U4 = KIND == W_DUAL ? RG_WIDE_U_DUAL : RG_WIDE_U;
-    if (V == 2) hop_wide<KIND, 2, 2 * U4><<<grid, 128, 0, ctx->stream>>>(a);
-    else hop_wide<KIND, 4, U4><<<grid, 128, 0, ctx->stream>>>(a);
+    if (V == 1) hop_wide<KIND, 1, 2 * U4><<<grid, 32 * warps, 0, ctx->stream>>>(a);
+    else if (V == 2) hop_wide<KIND, 2, 2 * U4><<<grid, 32 * warps, 0, ctx->stream>>>(a);
+    else hop_wide<KIND, 4, U4><<<grid, 32 * warps, 0, ctx->stream>>>(a);
     return RAFTGP_OK;
 }
 
