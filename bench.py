@@ -573,6 +573,12 @@ def main():
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "peak_source": peak_src, "frac_of_8TBs_nominal": ach / 8000.0, "traffic": traffic,
                 "bytes_per_launch": hop_stats[dom]["bytes_per_launch"]}
+        if traffic:
+            # the DRAM view: ncu's measured bytes per launch over this run's event-timed launch duration (the
+            # gather-model bytes above count L2 hits as traffic, so frac can exceed the DRAM-side fraction)
+            t_launch = hop_stats[dom]["ms_per_step"] * 1e-3 / hop_stats[dom]["launches_per_step"]
+            roof["dram_gb_s"] = traffic / t_launch / 1e9
+            roof["dram_frac"] = roof["dram_gb_s"] / peak
 
     # ---------------- NEXT-1: Alg. 1 model selection on this step's embeddings (whole graph, N = 1)
     select = None

@@ -1,6 +1,6 @@
 """Per-launch DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) of the hop kernels from an ncu
 --set full report, averaged per kernel family as bench.py's roofline uses them:
-  feature_hop = hop_kernel<0|1|2|5,...> (feature kinds), gcn_hop = hop_kernel<3,...>.
+  feature_hop = hop_kernel<0|1|2|5,...> (feature kinds), gcn_hop = hop_kernel<3|6,...> (GCN, paired GCN).
 Usage: python tools/traffic_from_ncu.py <report.ncu-rep> <config> [out.json]"""
 import csv
 import json
@@ -19,7 +19,7 @@ for d in data:
     if "hop_kernel<" not in name:
         continue
     kind = int(name.split("hop_kernel<")[1].split(",")[0])
-    key = "gcn_hop" if kind == 3 else ("transform" if kind == 4 else "feature_hop")
+    key = "gcn_hop" if kind in (3, 6) else ("transform" if kind == 4 else "feature_hop")
     b = 0.0
     for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
         b += float(d[hdr.index(m)].replace(",", "")) * mul[units[hdr.index(m)]]
