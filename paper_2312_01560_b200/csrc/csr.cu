@@ -315,7 +315,14 @@ __global__ void __launch_bounds__(1024) csr_sort_block(const int64_t *__restrict
 // places the entries into their rows in shared memory, sorts and dedups every row (one warp per row) and
 // writes the unique prefix of each row to col_raw. Buckets that do not fit shared memory are placed into
 // col_raw in global memory and their rows handed to the warp / block sort kernels above.
-constexpr int kPartTile = 262144;       // raw pairs per partition tile
+#ifndef RG_PART_TILE
+#define RG_PART_TILE 65536
+#endif
+constexpr int kPartTile = RG_PART_TILE;   // raw pairs per partition tile
+#ifndef RG_PART_UNROLL
+#define RG_PART_UNROLL 8
+#endif
+constexpr int kPartUnroll = RG_PART_UNROLL;   // edge loads in flight per thread
 constexpr int kMaxBuckets = 12288;      // partition smem: 12 B per bucket
 constexpr int kMaxBucketRows = 4096;    // bucket_sort smem for row cursors/offsets
 constexpr int kBucketCap = 44032;       // entries of one bucket held in shared memory (172 KB)
@@ -365,11 +372,22 @@ __global__ void __launch_bounds__(1024) csr_partition(const int32_t *__restrict_
         const int64_t e1 = min(m, e0 + (int64_t)kPartTile);
         for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
         __syncthreads();
-        for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-            const int32_t u = __ldg(src + e), v = __ldg(dst + e);
-            if (u < 0 || v < 0 || u >= n || v >= n || u == v) continue;
-            if (u >= rb && u < re) atomicAdd(&hist[(u - rb) >> shift], 1u);
-            if (v >= rb && v < re) atomicAdd(&hist[(v - rb) >> shift], 1u);
+        // loads issued kPartUnroll at a time (the histogram pass is otherwise bound by their latency)
+        for (int64_t eb = e0 + threadIdx.x; eb < e1; eb += kPartUnroll * (int64_t)blockDim.x) {
+            int32_t us[kPartUnroll], vs[kPartUnroll];
+#pragma unroll
+            for (int k = 0; k < kPartUnroll; ++k) {
+                const int64_t e = eb + (int64_t)k * blockDim.x;
+                us[k] = e < e1 ? __ldg(src + e) : -1;
+                vs[k] = e < e1 ? __ldg(dst + e) : -1;
+            }
+#pragma unroll
+            for (int k = 0; k < kPartUnroll; ++k) {
+                const int32_t u = us[k], v = vs[k];
+                if (u < 0 || v < 0 || u >= n || v >= n || u == v) continue;
+                if (u >= rb && u < re) atomicAdd(&hist[(u - rb) >> shift], 1u);
+                if (v >= rb && v < re) atomicAdd(&hist[(v - rb) >> shift], 1u);
+            }
         }
         __syncthreads();
         for (int b = threadIdx.x; b < nb; b += blockDim.x) {
@@ -378,16 +396,16 @@ __global__ void __launch_bounds__(1024) csr_partition(const int32_t *__restrict_
             hist[b] = 0u;
         }
         __syncthreads();
-        for (int64_t eb = e0 + threadIdx.x; eb < e1; eb += 4 * (int64_t)blockDim.x) {
-            int32_t us[4], vs[4];
+        for (int64_t eb = e0 + threadIdx.x; eb < e1; eb += kPartUnroll * (int64_t)blockDim.x) {
+            int32_t us[kPartUnroll], vs[kPartUnroll];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < kPartUnroll; ++k) {
                 const int64_t e = eb + (int64_t)k * blockDim.x;
                 us[k] = e < e1 ? __ldg(src + e) : -1;
                 vs[k] = e < e1 ? __ldg(dst + e) : -1;
             }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < kPartUnroll; ++k) {
                 const int32_t u = us[k], v = vs[k];
                 if (u < 0 || v < 0 || u >= n || v >= n || u == v) continue;
                 if (u >= rb && u < re) {
