@@ -72,6 +72,9 @@ RAFTGP_API raftgp_status raftgp_ctx_create(int device, void *cuda_stream, raftgp
 RAFTGP_API raftgp_status raftgp_ctx_destroy(raftgp_ctx ctx);
 RAFTGP_API raftgp_status raftgp_ctx_sync(raftgp_ctx ctx);                     /* synchronous */
 RAFTGP_API raftgp_status raftgp_ctx_stream(raftgp_ctx ctx, void **cuda_stream_out);
+/* Return the context's cached workspace blocks to the device (steady-state calls reuse them; a caller about to
+ * allocate a lot itself can trim first). Synchronous. bytes_released: host out or NULL. */
+RAFTGP_API raftgp_status raftgp_ctx_trim(raftgp_ctx ctx, int64_t *bytes_released);
 
 /* Per-kernel device timing with CUDA events recorded around every launch on the ctx stream.
  * raftgp_prof_read is synchronous; kernel ids are 0..raftgp_prof_kernels()-1. */

@@ -191,6 +191,16 @@ raftgp_status raftgp_ctx_destroy(raftgp_ctx ctx) {
     return RAFTGP_OK;
 }
 
+raftgp_status raftgp_ctx_trim(raftgp_ctx ctx, int64_t *bytes_released) {
+    if (!ctx) return fail(RAFTGP_ERR_PARAM, "null ctx");
+    RG_TRY(set_device(ctx));
+    const int64_t b = (int64_t)ctx->cached_bytes;
+    release_cache(ctx);
+    RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (bytes_released) *bytes_released = b;
+    return RAFTGP_OK;
+}
+
 raftgp_status raftgp_ctx_sync(raftgp_ctx ctx) {
     if (!ctx) return fail(RAFTGP_ERR_PARAM, "null ctx");
     RG_CUDA(cudaStreamSynchronize(ctx->stream));

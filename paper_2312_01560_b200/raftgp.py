@@ -37,7 +37,7 @@ EXPORTS = (
     "raftgp_embed", "raftgp_embed_multi", "raftgp_feature_transform", "raftgp_modularity", "raftgp_ncut", "raftgp_local_modularity",
     "raftgp_model_select", "raftgp_gemm_tf32x3", "raftgp_sbm_sample", "raftgp_stream_create",
     "raftgp_stream_add_edges", "raftgp_stream_embedding", "raftgp_stream_graph", "raftgp_stream_destroy",
-    "raftgp_build_embed",
+    "raftgp_build_embed", "raftgp_ctx_trim",
 )
 
 _lib = None
@@ -61,6 +61,7 @@ _SIGS = {
     "raftgp_ctx_destroy": (ctypes.c_int, [c_vp]),
     "raftgp_ctx_sync": (ctypes.c_int, [c_vp]),
     "raftgp_ctx_stream": (ctypes.c_int, [c_vp, P(c_vp)]),
+    "raftgp_ctx_trim": (ctypes.c_int, [c_vp, P(c_i64)]),
     "raftgp_ctx_set_profiling": (ctypes.c_int, [c_vp, ctypes.c_int]),
     "raftgp_prof_kernels": (ctypes.c_int, []),
     "raftgp_prof_name": (ctypes.c_char_p, [ctypes.c_int]),
@@ -155,6 +156,12 @@ class Context:
 
     def sync(self):
         _ck(load_library().raftgp_ctx_sync(self.h))
+
+    def trim(self) -> int:
+        """Release the cached workspace blocks to the device; returns the bytes released."""
+        b = c_i64(0)
+        _ck(load_library().raftgp_ctx_trim(self.h, ctypes.byref(b)))
+        return b.value
 
     def set_profiling(self, on: bool = True):
         _ck(load_library().raftgp_ctx_set_profiling(self.h, int(on)))

@@ -1,0 +1,51 @@
+"""One-off C5 probe (N = 5e7, ~2e9 CSR entries, int64 offsets): build + embed on one B200, then check the CSR
+against the raw edges on sampled rows and the embedding for unit rows / finiteness."""
+import sys, time, json
+import numpy as np, torch
+sys.path.insert(0, '.')
+import synth
+from paper_2312_01560_b200 import raftgp as rg
+t = time.time()
+gr = synth.generate("C5", 0)
+print("synth", gr.n, gr.src.size, "%.1f s" % (time.time() - t), flush=True)
+ctx = rg.Context(0)
+src, dst = torch.from_numpy(gr.src).cuda(), torch.from_numpy(gr.dst).cuda()
+dims = (128, 128, 64)
+Z = {v: torch.empty((gr.n, dims[-1]), dtype=torch.float32, device='cuda') for v in ("ncut", "mod")}
+for rep in range(3):
+    torch.cuda.synchronize(); t = time.perf_counter()
+    Z, g = rg.raftgp_build_embed(ctx, gr.n, src, dst, ["ncut", "mod"], dims, 0, Z=Z, keep_graph=True)
+    torch.cuda.synchronize(); dt = time.perf_counter() - t
+    info = g.info()
+    print("rep", rep, "build+embed %.1f ms" % (dt * 1e3), info, flush=True)
+    if rep < 2:
+        g.close()
+print("cached workspace released:", ctx.trim() / 1e9, "GB", flush=True)
+nnz = info["nnz_local"]
+print("nnz", nnz, "> 2^31:", nnz > 2**31, flush=True)
+for v in ("ncut", "mod"):
+    z = Z[v]
+    nrm = torch.linalg.norm(z, dim=1)
+    print(v, "finite", bool(torch.isfinite(z).all()), "unit rows", float(((nrm - 1).abs() < 1e-5).float().mean()),
+          "zero rows", int((nrm == 0).sum()), flush=True)
+# sampled rows of the CSR vs the raw edges
+rp, col, deg = None, None, None
+rp = np.zeros(gr.n + 1, np.int64)
+import ctypes
+lib = rg.load_library()
+col = np.zeros(nnz, np.int32)
+rc = lib.raftgp_graph_export(g.h, ctypes.c_void_p(rp.ctypes.data), ctypes.c_void_p(col.ctypes.data), None, 0)
+print("export rc", rc, "row_ptr[-1]", rp[-1], flush=True)
+rng = np.random.default_rng(0)
+sample = np.sort(rng.choice(gr.n, 200, replace=False)).astype(np.int32)
+ins = np.isin(gr.src, sample)
+ind = np.isin(gr.dst, sample)
+pairs = np.concatenate([np.stack([gr.src[ins], gr.dst[ins]], 1), np.stack([gr.dst[ind], gr.src[ind]], 1)])
+pairs = pairs[pairs[:, 0] != pairs[:, 1]]
+ok = 0
+for i in sample:
+    ref = np.unique(pairs[pairs[:, 0] == i, 1])
+    got = col[rp[i]:rp[i + 1]]
+    ok += int(np.array_equal(ref, got))
+print("sampled rows matching the raw edges:", ok, "/", sample.size, flush=True)
+print("row_ptr monotone", bool(np.all(np.diff(rp) >= 0)), "sum deg = nnz", int(np.diff(rp).sum()) == nnz)
