@@ -2,7 +2,7 @@
 against the raw edges on sampled rows and the embedding for unit rows / finiteness."""
 import sys, time, json
 import numpy as np, torch
-sys.path.insert(0, '.')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 import synth
 from paper_2312_01560_b200 import raftgp as rg
 t = time.time()
