@@ -269,6 +269,21 @@ def measure_select(args, rg, ctx, gr, src_d, dst_d, variants, dims, Zbuf, barrie
                                "bytes_rule": "visited rows * 24 (segment, side, bounds r/w) + read rows * (4L + 4)"},
         }
     g.close()
+    # end-to-end quality where the BASELINE embeddings separate the blocks (C1, C2: 11 / 44 planted blocks)
+    import synth
+    out["quality"] = {}
+    for qcfg in ("C1", "C2"):
+        c = synth.CONFIGS[qcfg]
+        qg = synth.generate(c, args.seed, rule=args.rule)
+        qgr = rg.raftgp_build_csr(ctx, qg.n, torch.from_numpy(qg.src).to(ctx.device),
+                                  torch.from_numpy(qg.dst).to(ctx.device))
+        _, qZ = rg.raftgp_embed_multi(qgr, ["mod"], c.dims, args.seed)
+        qlab, qK, _ = rg.raftgp_model_select(qgr, qZ["mod"])
+        qlab = qlab.cpu().numpy()
+        out["quality"][qcfg] = {"variant": "mod", "blocks": qK, "planted_blocks": int(qg.info["k"]),
+                                "ari_vs_planted": float(adjusted_rand_score(qg.labels, qlab)),
+                                "nmi_vs_planted": float(normalized_mutual_info_score(qg.labels, qlab))}
+        qgr.close()
     return out
 
 
