@@ -1,0 +1,69 @@
+"""Degenerate sizes through the NEXT entry points: empty and one-node graphs at Table I widths, model selection
+on one node, the SBM sampler with no nodes / one block, a stream over a one-node graph."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rg(cuda_required):
+    from paper_2312_01560_b200 import raftgp
+    raftgp.load_library()
+    return raftgp
+
+
+@pytest.fixture(scope="module")
+def ctx(rg):
+    return rg.Context(0)
+
+
+def _g(rg, ctx, n, src, dst):
+    return rg.raftgp_build_csr(ctx, n, torch.tensor(src, dtype=torch.int32), torch.tensor(dst, dtype=torch.int32))
+
+
+@pytest.mark.parametrize("n", [0, 1, 2])
+def test_wide_tiny(rg, ctx, n):
+    src, dst = ([0], [1]) if n == 2 else ([], [])
+    g = _g(rg, ctx, n, src, dst)
+    dims = (256, 512, 128)
+    variants = ["ncut"] if n < 2 else ["ncut", "mod"]
+    _, Z = rg.raftgp_embed_multi(g, variants, dims, 1)
+    for v in variants:
+        assert Z[v].shape == (n, 128)
+        if n:
+            go = oracle.build_csr(n, np.array(src, np.int32), np.array(dst, np.int32))
+            Zo = oracle.gcn_np(go, dims, 1, oracle.project(go, v, dims[0], 1))[-1]
+            assert np.allclose(Z[v].cpu().numpy(), Zo, atol=1e-5)
+
+
+def test_select_one_node(rg, ctx):
+    g = _g(rg, ctx, 1, [], [])
+    lab, K, st = rg.raftgp_model_select(g, torch.zeros((1, 8), dtype=torch.float32, device="cuda"))
+    assert K == 1 and lab.cpu().tolist() == [0]
+
+
+def test_sbm_degenerate(rg, ctx):
+    s, d = rg.raftgp_sbm_sample(ctx, torch.zeros(0, dtype=torch.int32, device="cuda"),
+                                torch.zeros(0, dtype=torch.float64, device="cuda"),
+                                torch.ones((1, 1), dtype=torch.float64, device="cuda"), 0)
+    assert s.numel() == 0
+    c = torch.zeros(5, dtype=torch.int32, device="cuda")
+    s, d = rg.raftgp_sbm_sample(ctx, c, torch.ones(5, dtype=torch.float64, device="cuda"),
+                                torch.full((1, 1), 1e4, dtype=torch.float64, device="cuda"), 0)
+    assert s.numel() == 10                                         # complete graph on one block
+    rs, rd = oracle.sbm_sample(np.zeros(5, np.int32), np.ones(5), np.full((1, 1), 1e4), 0)
+    assert np.array_equal(s.cpu().numpy(), rs) and np.array_equal(d.cpu().numpy(), rd)
+
+
+def test_stream_one_node(rg, ctx):
+    g = _g(rg, ctx, 2, [], [])
+    st = rg.Stream(g, (32, 32, 32), 0)
+    info = st.add_edges(torch.tensor([0], dtype=torch.int32), torch.tensor([1], dtype=torch.int32))
+    assert info["changed"] == 2 and info["nnz"] == 2
+    g2 = _g(rg, ctx, 2, [0], [1])
+    _, Z = rg.raftgp_embed_multi(g2, ["ncut"], (32, 32, 32), 0)
+    assert torch.equal(st.embedding(), Z["ncut"])
