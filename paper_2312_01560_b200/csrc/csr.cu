@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(1024) csr_sort_block(const int64_t *__restrict
 // writes the unique prefix of each row to col_raw. Buckets that do not fit shared memory are placed into
 // col_raw in global memory and their rows handed to the warp / block sort kernels above.
 #ifndef RG_PART_TILE
-#define RG_PART_TILE 65536
+#define RG_PART_TILE 16384
 #endif
 constexpr int kPartTile = RG_PART_TILE;   // raw pairs per partition tile
 #ifndef RG_PART_UNROLL
@@ -355,24 +355,78 @@ struct Entry<false> {
     __device__ __forceinline__ static bool valid(T e) { return e.x >= 0; }
 };
 
+// Radix-style bucket partition of the raw entries (both orientations of every valid pair, local rows only)
+// into buckets of 2^shift consecutive local rows. csr_bucket_count: CTA c histograms its contiguous edge range
+// into shared memory and writes the counts bucket-major (cnt[b * G + c], no global atomics); an exclusive scan
+// gives the bucket starts base[b * G] (and the bucket sizes the bucket sort needs). The order of the entries
+// inside a bucket is irrelevant: the bucket sort sorts every row. The count pass also checks the node ids.
+__device__ __forceinline__ void cta_range(int64_t m, int64_t &e0, int64_t &e1) {
+    const int64_t chunk = (m + gridDim.x - 1) / gridDim.x;
+    e0 = min(m, (int64_t)blockIdx.x * chunk);
+    e1 = min(m, e0 + chunk);
+}
+
+__global__ void __launch_bounds__(1024) csr_bucket_count(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
+                                                         int64_t m, int64_t n, int64_t rb, int64_t re, int shift,
+                                                         int nb, int32_t *__restrict__ cnt, int *__restrict__ err) {
+    extern __shared__ unsigned int hsm[];
+    int64_t e0, e1;
+    cta_range(m, e0, e1);
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) hsm[b] = 0u;
+    __syncthreads();
+    bool bad = false;
+    for (int64_t eb = e0 + threadIdx.x; eb < e1; eb += kPartUnroll * (int64_t)blockDim.x) {
+        int32_t us[kPartUnroll], vs[kPartUnroll];
+#pragma unroll
+        for (int k = 0; k < kPartUnroll; ++k) {
+            const int64_t e = eb + (int64_t)k * blockDim.x;
+            us[k] = e < e1 ? __ldg(src + e) : 0;
+            vs[k] = e < e1 ? __ldg(dst + e) : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < kPartUnroll; ++k) {
+            const int32_t u = us[k], v = vs[k];
+            if (u < 0 || v < 0 || u >= n || v >= n) {
+                bad = true;
+                continue;
+            }
+            if (u == v) continue;
+            if (u >= rb && u < re) atomicAdd(&hsm[(u - rb) >> shift], 1u);
+            if (v >= rb && v < re) atomicAdd(&hsm[(v - rb) >> shift], 1u);
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) cnt[(int64_t)b * gridDim.x + blockIdx.x] = (int32_t)hsm[b];
+    if (bad) atomicOr(err, 1);
+}
+
+// The scatter pass runs over tiles of kPartTile edges claimed round robin: each tile histograms its entries
+// in shared memory, claims one contiguous slot range per bucket with a global atomic on the bucket cursor
+// (initialised to the bucket start), then writes. Concurrent tiles thus fill neighbouring slots of every
+// bucket, which keeps the scattered writes sector-local in L2 (per-CTA fixed offsets, i.e. an atomic-free
+// scatter, measured 2x slower: DESIGN.md "tried and rejected").
+__global__ void csr_bucket_cursor(const int64_t *__restrict__ base, int pgrid, int nb,
+                                  unsigned long long *__restrict__ bcur) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < nb) bcur[b] = (unsigned long long)base[(int64_t)b * pgrid];
+}
+
 template <bool PACKED>
 __global__ void __launch_bounds__(1024) csr_partition(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
                                                       int64_t m, int64_t n, int64_t rb, int64_t re, int shift, int nb,
-                                                      int vbits, const int64_t *__restrict__ raw_ptr,
-                                                      unsigned long long *__restrict__ bcur,
+                                                      int vbits, int64_t ptile, unsigned long long *__restrict__ bcur,
                                                       typename Entry<PACKED>::T *__restrict__ pairs) {
     using E = Entry<PACKED>;
     extern __shared__ long long psm[];
     long long *base = psm;                                              // nb
     unsigned int *hist = reinterpret_cast<unsigned int *>(psm + nb);    // nb
     const int bmask = (1 << shift) - 1;
-    const int64_t ntiles = (m + kPartTile - 1) / kPartTile;
+    const int64_t ntiles = (m + ptile - 1) / ptile;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t e0 = tile * kPartTile;
-        const int64_t e1 = min(m, e0 + (int64_t)kPartTile);
+        const int64_t e0 = tile * ptile;
+        const int64_t e1 = min(m, e0 + ptile);
         for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
         __syncthreads();
-        // loads issued kPartUnroll at a time (the histogram pass is otherwise bound by their latency)
         for (int64_t eb = e0 + threadIdx.x; eb < e1; eb += kPartUnroll * (int64_t)blockDim.x) {
             int32_t us[kPartUnroll], vs[kPartUnroll];
 #pragma unroll
@@ -392,7 +446,7 @@ __global__ void __launch_bounds__(1024) csr_partition(const int32_t *__restrict_
         __syncthreads();
         for (int b = threadIdx.x; b < nb; b += blockDim.x) {
             const unsigned int h = hist[b];
-            if (h) base[b] = raw_ptr[(int64_t)b << shift] + (long long)atomicAdd(&bcur[b], (unsigned long long)h);
+            if (h) base[b] = (long long)atomicAdd(&bcur[b], (unsigned long long)h);
             hist[b] = 0u;
         }
         __syncthreads();
@@ -499,34 +553,69 @@ __device__ __forceinline__ int warp_sort_dedup(int32_t *a, int len, int32_t *out
 
 template <bool PACKED>
 __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PACKED>::T *__restrict__ pairs,
-                                                        const int64_t *__restrict__ raw_ptr, int64_t nl, int shift,
-                                                        int nb, int vbits, int32_t *__restrict__ col_raw,
-                                                        int32_t *__restrict__ deg, int64_t *__restrict__ fb_rows,
-                                                        int32_t *__restrict__ fb_count) {
+                                                        const int64_t *__restrict__ base, int pgrid,
+                                                        int64_t *__restrict__ raw_ptr,
+                                                        int64_t nl, int shift, int nb, int vbits,
+                                                        int32_t *__restrict__ col_raw, int32_t *__restrict__ deg,
+                                                        int64_t *__restrict__ fb_rows, int32_t *__restrict__ fb_count) {
     extern __shared__ int32_t bsm[];
     int32_t *s = bsm;                                   // kBucketCap values
-    int32_t *cur = bsm + kBucketCap;                    // B cursors
+    int32_t *cur = bsm + kBucketCap;                    // B cursors (first: the row counts)
     int32_t *off = cur + kMaxBucketRows;                // B + 1 offsets (relative to the bucket start)
     int32_t *big = off + kMaxBucketRows + 1;            // rows longer than 32, longest work first
     __shared__ int fb_base, nbig, qnext;
+    __shared__ int64_t scan_sh[32];
     const int lane = threadIdx.x & 31;
     constexpr int kLoadBatch = 8;
+    constexpr int kRowsPerThread = kMaxBucketRows / 1024;
     for (int b = blockIdx.x; b < nb; b += gridDim.x) {
         const int64_t r0 = (int64_t)b << shift;
         const int nr = static_cast<int>(min(nl, r0 + ((int64_t)1 << shift)) - r0);
-        const int64_t e0 = raw_ptr[r0];
-        const int64_t E = raw_ptr[r0 + nr] - e0;
+        const int64_t e0 = base[(int64_t)b * pgrid];            // bucket b starts at its first CTA's offset
+        const int64_t E = base[(int64_t)(b + 1) * pgrid] - e0;
         const bool fits = E <= kBucketCap;
         if (threadIdx.x == 0) {
             nbig = 0;
             qnext = 0;
         }
+        for (int t = threadIdx.x; t < nr; t += blockDim.x) cur[t] = 0;
+        __syncthreads();
+        // row lengths of this bucket (the bucket is its own count pass: no global per-row counters)
+        for (int64_t i0 = (int64_t)threadIdx.x * kLoadBatch; i0 < E; i0 += (int64_t)blockDim.x * kLoadBatch) {
+            typename Entry<PACKED>::T p[kLoadBatch];
+#pragma unroll
+            for (int k = 0; k < kLoadBatch; ++k)
+                p[k] = (i0 + k < E) ? pairs[e0 + i0 + k] : Entry<PACKED>::invalid();
+#pragma unroll
+            for (int k = 0; k < kLoadBatch; ++k)
+                if (Entry<PACKED>::valid(p[k])) atomicAdd(&cur[Entry<PACKED>::row(p[k], vbits)], 1);
+        }
+        __syncthreads();
+        {   // exclusive scan of the row lengths: thread t owns rows [kRowsPerThread t, +kRowsPerThread)
+            int32_t v[kRowsPerThread];
+            int64_t sum = 0;
+#pragma unroll
+            for (int j = 0; j < kRowsPerThread; ++j) {
+                const int t = threadIdx.x * kRowsPerThread + j;
+                v[j] = t < nr ? cur[t] : 0;
+                sum += v[j];
+            }
+            int64_t total;
+            int64_t run = block_incl_scan(sum, scan_sh, total) - sum;
+#pragma unroll
+            for (int j = 0; j < kRowsPerThread; ++j) {
+                const int t = threadIdx.x * kRowsPerThread + j;
+                if (t < nr) off[t] = static_cast<int32_t>(run);
+                run += v[j];
+            }
+            if (threadIdx.x == 0) off[nr] = static_cast<int32_t>(total);
+        }
         __syncthreads();
         for (int t = threadIdx.x; t <= nr; t += blockDim.x) {
-            off[t] = static_cast<int32_t>(fits ? raw_ptr[r0 + t] - e0 : 0);
+            if (t < nr || r0 + nr == nl) raw_ptr[r0 + t] = e0 + off[t];
             if (t < nr) {
                 cur[t] = 0;
-                if (fits && raw_ptr[r0 + t + 1] - raw_ptr[r0 + t] > kGroupRow) big[atomicAdd(&nbig, 1)] = t;
+                if (fits && off[t + 1] - off[t] > kGroupRow) big[atomicAdd(&nbig, 1)] = t;
             }
         }
         __syncthreads();
@@ -594,7 +683,7 @@ __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PAC
                 const typename Entry<PACKED>::T p = pairs[e0 + idx];
                 const int lr = Entry<PACKED>::row(p, vbits);
                 const int64_t k = atomicAdd(&cur[lr], 1);
-                col_raw[raw_ptr[r0 + lr] + k] = Entry<PACKED>::col(p, vbits);
+                col_raw[e0 + off[lr] + k] = Entry<PACKED>::col(p, vbits);
             }
             if (threadIdx.x == 0) fb_base = atomicAdd(fb_count, nr);
             __syncthreads();
@@ -712,18 +801,20 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
     RG_TRY(dalloc_t(ctx, &g->deg_all, n));
     RG_TRY(dalloc_t(ctx, &g->s_all, n));
     RG_TRY(dalloc_t(ctx, &g->sh_all, n));
-    RG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nl ? nl : 1), st));
     RG_CUDA(cudaMemsetAsync(big_count, 0, sizeof(int32_t) * 2, st));
     const int egrid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 256), (int64_t)ctx->sm_count * 16)));
-    if (m > 0) {
-        LaunchScope L(ctx, K_CSR_COUNT);
-        csr_count<<<egrid, 256, 0, st>>>(src, dst, m, n, rb, re, cnt, err);
-    }
-    RG_CHECK_LAUNCH(ctx);
-    RG_TRY(scan_i32_to_i64(ctx, cnt, raw_ptr, nl));
     int shift = 0;
     while (shift < 31 && ceil_div(nl, (int64_t)1 << shift) > kMaxBuckets) ++shift;
     const bool bucketed = nl > 0 && ((int64_t)1 << shift) <= kMaxBucketRows;
+    if (!bucketed) {   // per-row counts (the bucketed path lets every bucket count its own rows)
+        RG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nl ? nl : 1), st));
+        if (m > 0) {
+            LaunchScope L(ctx, K_CSR_COUNT);
+            csr_count<<<egrid, 256, 0, st>>>(src, dst, m, n, rb, re, cnt, err);
+        }
+        RG_CHECK_LAUNCH(ctx);
+        RG_TRY(scan_i32_to_i64(ctx, cnt, raw_ptr, nl));
+    }
     const int rgrid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nl, 8), (int64_t)ctx->sm_count * 8)));
     int64_t *fb_rows = nullptr;
     int32_t *fb_count = nullptr;
@@ -732,43 +823,61 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
         int vbits = 1;
         while (vbits < 31 && ((int64_t)1 << vbits) < n) ++vbits;
         const bool packed = shift + vbits <= 32;
-        unsigned long long *bcur = nullptr;
+        const int pgrid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 65536), ctx->sm_count)));
         void *pairs = nullptr;
+        int32_t *bcnt = nullptr;
+        int64_t *bstart = nullptr;
+        unsigned long long *bcur = nullptr;
         RG_TRY(dalloc_t(ctx, &bcur, (size_t)nb));
+        RG_TRY(dalloc_t(ctx, &bcnt, (size_t)nb * pgrid));
+        RG_TRY(dalloc_t(ctx, &bstart, (size_t)nb * pgrid + 1));
         RG_TRY(dalloc(ctx, &pairs, (size_t)cap * (packed ? 4 : 8)));
         RG_TRY(dalloc_t(ctx, &fb_rows, (size_t)nl));
         RG_TRY(dalloc_t(ctx, &fb_count, 1));
-        RG_CUDA(cudaMemsetAsync(bcur, 0, sizeof(unsigned long long) * nb, st));
         RG_CUDA(cudaMemsetAsync(fb_count, 0, sizeof(int32_t), st));
         const size_t bsmem = (size_t)(kBucketCap + 3 * kMaxBucketRows + 1) * 4;
         static bool attrs = false;
         if (!attrs) {
+            RG_CUDA(cudaFuncSetAttribute(csr_bucket_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 4));
             RG_CUDA(cudaFuncSetAttribute(csr_partition<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 12));
             RG_CUDA(cudaFuncSetAttribute(csr_partition<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 12));
             RG_CUDA(cudaFuncSetAttribute(csr_bucket_sort<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
             RG_CUDA(cudaFuncSetAttribute(csr_bucket_sort<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
             attrs = true;
         }
+        {
+            LaunchScope L(ctx, K_CSR_COUNT);
+            csr_bucket_count<<<pgrid, 1024, (size_t)nb * 4, st>>>(src, dst, m, n, rb, re, shift, nb, bcnt, err);
+        }
+        RG_CHECK_LAUNCH(ctx);
+        RG_TRY(scan_i32_to_i64(ctx, bcnt, bstart, (int64_t)nb * pgrid));
         if (m > 0) {
-            const int pgrid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, kPartTile), ctx->sm_count)));
             LaunchScope L(ctx, K_CSR_PARTITION);
+            csr_bucket_cursor<<<(nb + 255) / 256, 256, 0, st>>>(bstart, pgrid, nb, bcur);
+            static const int64_t ptile = [] {
+                const char *e = getenv("RAFTGP_PART_TILE");
+                return e ? std::max<int64_t>(1024, atoll(e)) : (int64_t)kPartTile;
+            }();
+            const int tgrid = static_cast<int>(std::min<int64_t>(ceil_div(m, ptile), ctx->sm_count));
             if (packed)
-                csr_partition<true><<<pgrid, 1024, (size_t)nb * 12, st>>>(src, dst, m, n, rb, re, shift, nb, vbits, raw_ptr,
-                                                                          bcur, static_cast<uint32_t *>(pairs));
+                csr_partition<true><<<tgrid, 1024, (size_t)nb * 12, st>>>(src, dst, m, n, rb, re, shift, nb, vbits, ptile, bcur,
+                                                                          static_cast<uint32_t *>(pairs));
             else
-                csr_partition<false><<<pgrid, 1024, (size_t)nb * 12, st>>>(src, dst, m, n, rb, re, shift, nb, vbits, raw_ptr,
-                                                                           bcur, static_cast<int2 *>(pairs));
+                csr_partition<false><<<tgrid, 1024, (size_t)nb * 12, st>>>(src, dst, m, n, rb, re, shift, nb, vbits, ptile, bcur,
+                                                                           static_cast<int2 *>(pairs));
         }
         RG_CHECK_LAUNCH(ctx);
         {
             LaunchScope L(ctx, K_CSR_BUCKET);
             const int bgrid = std::min(nb, ctx->sm_count);
             if (packed)
-                csr_bucket_sort<true><<<bgrid, 1024, bsmem, st>>>(static_cast<const uint32_t *>(pairs), raw_ptr, nl, shift, nb,
-                                                                  vbits, col_raw, g->deg_local, fb_rows, fb_count);
+                csr_bucket_sort<true><<<bgrid, 1024, bsmem, st>>>(static_cast<const uint32_t *>(pairs), bstart, pgrid, raw_ptr,
+                                                                  nl, shift, nb, vbits, col_raw, g->deg_local, fb_rows,
+                                                                  fb_count);
             else
-                csr_bucket_sort<false><<<bgrid, 1024, bsmem, st>>>(static_cast<const int2 *>(pairs), raw_ptr, nl, shift, nb,
-                                                                   vbits, col_raw, g->deg_local, fb_rows, fb_count);
+                csr_bucket_sort<false><<<bgrid, 1024, bsmem, st>>>(static_cast<const int2 *>(pairs), bstart, pgrid, raw_ptr,
+                                                                   nl, shift, nb, vbits, col_raw, g->deg_local, fb_rows,
+                                                                   fb_count);
         }
         RG_CHECK_LAUNCH(ctx);
         {
@@ -776,6 +885,8 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
             csr_sort_warp<<<rgrid, 256, 0, st>>>(nl, fb_rows, fb_count, raw_ptr, col_raw, g->deg_local, big_rows, big_count);
         }
         RG_CHECK_LAUNCH(ctx);
+        dfree(ctx, bcnt);
+        dfree(ctx, bstart);
         dfree(ctx, bcur);
         dfree(ctx, pairs);
     } else {
