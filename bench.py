@@ -130,7 +130,8 @@ def work_units(nnz, n, r, dims, nvar):
 def algorithmic_bytes(nnz, n, r, dims, nvar, kernel, fused_pair=False):
     """SURVEY.md §8(d) gather model per launch, summed over one step's launches of that kernel:
     B_h = 8(N+1) + 4 nnz + 4 w_h G_h + 4 w'_h N + 4 N. With fused_pair the NCUT and MOD feature hops share
-    one launch (one gather of Theta, two written T1 blocks)."""
+    one launch (one gather of Theta, two written T1 blocks), and so do their last GCN hops (one read of the
+    CSR and of s_hat, both 64-wide operands gathered side by side)."""
     L = len(dims) - 1
     if kernel == "feature_hop":
         if fused_pair:
@@ -143,6 +144,9 @@ def algorithmic_bytes(nnz, n, r, dims, nvar, kernel, fused_pair=False):
         for k in range(1, L + 1):
             w_out = dims[k + 1] if k < L else dims[L]
             b += 8 * (n + 1) + 4 * nnz + 4 * dims[k] * (nnz + n) + 4 * w_out * n + 4 * n
+        if fused_pair and nvar >= 2 and L >= 2 and dims[L] in (32, 64):   # gcn_pair_supported (spmm.cu)
+            shared = 8 * (n + 1) + 4 * nnz + 4 * n
+            return nvar * b - shared, nvar * L - 1
         return nvar * b, nvar * L
     return None, None
 

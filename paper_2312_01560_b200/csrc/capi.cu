@@ -141,6 +141,35 @@ static raftgp_status need_ready(raftgp_graph g) {
     return RAFTGP_OK;
 }
 
+namespace raftgp {
+
+static void ctx_teardown(raftgp_ctx ctx) {
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto &r : ctx->recs) {
+        cudaEventDestroy(r.start);
+        cudaEventDestroy(r.stop);
+    }
+    for (auto e : ctx->event_pool) cudaEventDestroy(e);
+    release_cache(ctx);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->side) {
+        cudaStreamSynchronize(ctx->side);
+        cudaStreamDestroy(ctx->side);
+    }
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+
+void ctx_retain(raftgp_ctx ctx) { ctx->refs.fetch_add(1); }
+
+void ctx_release(raftgp_ctx ctx) {
+    if (ctx->refs.fetch_sub(1) == 1) ctx_teardown(ctx);
+}
+
+}  // namespace raftgp
+
 extern "C" {
 
 const char *raftgp_last_error(void) { return g_last_error.c_str(); }
@@ -172,22 +201,7 @@ raftgp_status raftgp_ctx_create(int device, void *cuda_stream, raftgp_ctx *out) 
 }
 
 raftgp_status raftgp_ctx_destroy(raftgp_ctx ctx) {
-    if (!ctx) return RAFTGP_OK;
-    cudaSetDevice(ctx->device);
-    cudaStreamSynchronize(ctx->stream);
-    for (auto &r : ctx->recs) {
-        cudaEventDestroy(r.start);
-        cudaEventDestroy(r.stop);
-    }
-    for (auto e : ctx->event_pool) cudaEventDestroy(e);
-    release_cache(ctx);
-    cudaStreamSynchronize(ctx->stream);
-    if (ctx->side) {
-        cudaStreamSynchronize(ctx->side);
-        cudaStreamDestroy(ctx->side);
-    }
-    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
-    delete ctx;
+    if (ctx) ctx_release(ctx);
     return RAFTGP_OK;
 }
 
@@ -280,6 +294,7 @@ raftgp_status raftgp_build_csr(raftgp_ctx ctx, int64_t n, int64_t m, const int32
     }
     raftgp_graph g = new raftgp_graph_s();
     g->ctx = ctx;
+    ctx_retain(ctx);
     raftgp_status st = csr_build(ctx, n, m, dsrc, ddst, row_begin, row_end, g);
     dfree(ctx, tmp);
     if (st != RAFTGP_OK) {
@@ -361,6 +376,7 @@ raftgp_status raftgp_graph_destroy(raftgp_graph g) {
     dfree(ctx, g->s_all);
     dfree(ctx, g->sh_all);
     delete g;
+    ctx_release(ctx);
     return RAFTGP_OK;
 }
 

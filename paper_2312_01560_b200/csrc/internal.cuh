@@ -8,6 +8,7 @@
 #include <map>
 #include <string>
 #include <unordered_map>
+#include <atomic>
 #include <vector>
 
 #include "../../include/raftgp.h"
@@ -56,6 +57,9 @@ struct ProfRec {
 }  // namespace raftgp
 
 struct raftgp_ctx_s {
+    // references: the caller's (dropped by raftgp_ctx_destroy) + one per live graph / stream, so a graph or
+    // stream destroyed after its context (e.g. by a garbage collector) still finds the context alive
+    std::atomic<int> refs{1};
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;   // library-owned side stream (overlapped work inside one call)
@@ -105,6 +109,10 @@ struct raftgp_stream_s {
 };
 
 namespace raftgp {
+
+// ---------------------------------------------------------------- context lifetime (capi.cu)
+void ctx_retain(raftgp_ctx ctx);
+void ctx_release(raftgp_ctx ctx);   // tears the context down when the last reference goes
 
 // ---------------------------------------------------------------- errors
 void set_error(const std::string &msg);

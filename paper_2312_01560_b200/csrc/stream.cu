@@ -112,6 +112,7 @@ raftgp_status stream_create(raftgp_graph g, int32_t layers, const int32_t *dims,
         if (!fast_width(dims[k])) return fail(RAFTGP_ERR_PARAM, "stream: layer widths must be 32, 64 or 128");
     raftgp_stream s = new raftgp_stream_s();
     s->ctx = ctx;
+    ctx_retain(ctx);
     s->g = g;
     s->layers = layers;
     s->dims.assign(dims, dims + layers + 1);
@@ -272,8 +273,10 @@ void stream_destroy(raftgp_stream s) {
         dfree(ctx, x.row_ptr); dfree(ctx, x.col); dfree(ctx, x.deg_local); dfree(ctx, x.order); dfree(ctx, x.deg_all);
         dfree(ctx, x.s_all); dfree(ctx, x.sh_all);
         delete s->g;
+        ctx_release(ctx);
     }
     delete s;
+    ctx_release(ctx);
 }
 
 }  // namespace raftgp

@@ -67,3 +67,22 @@ def test_stream_one_node(rg, ctx):
     g2 = _g(rg, ctx, 2, [0], [1])
     _, Z = rg.raftgp_embed_multi(g2, ["ncut"], (32, 32, 32), 0)
     assert torch.equal(st.embedding(), Z["ncut"])
+
+
+def test_handles_outlive_context(rg):
+    """A graph or stream destroyed after its context (as a garbage collector may order it) must still find the
+    context alive: the library reference-counts it (raftgp_ctx_destroy drops only the caller's reference)."""
+    c = rg.Context(0)
+    src = torch.tensor([0, 1, 2, 3], dtype=torch.int32)
+    dst = torch.tensor([1, 2, 3, 0], dtype=torch.int32)
+    g1 = rg.raftgp_build_csr(c, 4, src, dst)
+    g2 = rg.raftgp_build_csr(c, 4, src, dst)
+    s = rg.Stream(g2, (32, 32, 32), 7)
+    s.add_edges(torch.tensor([0], dtype=torch.int32), torch.tensor([2], dtype=torch.int32))
+    c.close()
+    rp, col, deg = g1.export()          # the graph is still usable: its context is alive
+    assert list(deg) == [2, 2, 2, 2]
+    assert s.embedding().shape == (4, 32)
+    g1.close()
+    s.close()
+    torch.cuda.synchronize()
