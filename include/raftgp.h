@@ -69,6 +69,9 @@ RAFTGP_API const char *raftgp_version(void);
 /* device: CUDA ordinal. cuda_stream: the cudaStream_t every call of this context enqueues on (NULL =
  * the legacy default stream). The stream stays owned by the caller and must outlive the context. */
 RAFTGP_API raftgp_status raftgp_ctx_create(int device, void *cuda_stream, raftgp_ctx *out);
+/* Drops the caller's reference. Graphs and streams hold their own reference, so they may be destroyed
+ * before or after their context; the context (its side stream, events and cached workspace) is torn down
+ * when the last of them goes. NULL is a no-op. Always RAFTGP_OK. */
 RAFTGP_API raftgp_status raftgp_ctx_destroy(raftgp_ctx ctx);
 RAFTGP_API raftgp_status raftgp_ctx_sync(raftgp_ctx ctx);                     /* synchronous */
 RAFTGP_API raftgp_status raftgp_ctx_stream(raftgp_ctx ctx, void **cuda_stream_out);
