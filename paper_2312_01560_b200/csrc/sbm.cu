@@ -6,9 +6,11 @@
 //   tables    P_r (theta prefix sums) and Q_r (upper-triangle row-sum prefixes), one thread per block,
 //             sequential fp64 in the spec's order
 //   chunks    per pair (r <= s): T_rs cells -> ceil(T / 2^q) chunks; exclusive scan -> chunk ids
-//   count     thread per chunk: the spec's walk (draw u, E = -ln_spec64(u), binary search of the first cell
-//             whose RangeSum exceeds E), counting edges
-//   write     scan of the counts, then the same walk writing (src, dst) at its offset
+//   count     persistent walk, one chunk per lane at a time (draw u, E = -ln_spec64(u), binary search of the
+//             first cell whose RangeSum exceeds E), counting edges and recording the first kSlots event
+//             cells of every chunk
+//   write     scan of the counts, then the recorded cells are emitted as (src, dst) at the chunk's offset;
+//             only chunks with more than kSlots events are walked again
 // Every floating-point value that decides an integer (RangeSum bits, E) is computed with the spec's operation
 // sequence (explicit round-to-nearest intrinsics, no contraction), so the edge list is bit-identical to the
 // oracle's, in (pair, chunk, cell) order.
@@ -17,6 +19,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "gauss.cuh"
 #include "internal.cuh"
@@ -61,6 +64,7 @@ struct SbmArgs {
     int64_t npairs, nchunks;
     uint64_t seed;
     int q;
+    int nslot;               // event cells recorded per chunk by the count walk (0: the write pass walks again)
 };
 
 struct PairView {
@@ -127,9 +131,9 @@ __device__ __forceinline__ double range_sum(const SbmArgs &A, const PairView &v,
     return __dmul_rn(v.omega, __dadd_rn(__dadd_rn(u1, u2), u3));
 }
 
-// One chunk's walk (SBM_SPEC §4). WRITE = false counts, true writes at out offset.
-template <bool WRITE>
-__device__ int64_t walk_chunk(const SbmArgs &A, int64_t chunk, int32_t *src, int32_t *dst, int64_t off) {
+// Chunk set-up: pair of the chunk, its cell range [x0, x1) and the row/column of x0 (SBM_SPEC §3, §4)
+__device__ __forceinline__ void chunk_setup(const SbmArgs &A, int64_t chunk, int64_t &p, int64_t &k, PairView &v,
+                                            int64_t &x1, int64_t &mm) {
     // pair of this chunk: largest p with choff[p] <= chunk
     int64_t lo = 0, hi = A.npairs - 1;
     while (lo < hi) {
@@ -137,10 +141,10 @@ __device__ int64_t walk_chunk(const SbmArgs &A, int64_t chunk, int32_t *src, int
         if (A.choff[mid] <= chunk) lo = mid;
         else hi = mid - 1;
     }
-    const int64_t p = lo, k = chunk - A.choff[p];
+    p = lo;
+    k = chunk - A.choff[p];
     int32_t r, s;
     pair_of(p, A.K, r, s);
-    PairView v;
     v.diag = r == s;
     v.nr = A.boff[r + 1] - A.boff[r];
     v.ns = A.boff[s + 1] - A.boff[s];
@@ -153,43 +157,105 @@ __device__ int64_t walk_chunk(const SbmArgs &A, int64_t chunk, int32_t *src, int
     v.omega = A.omega[(int64_t)r * A.K + s];
     const int64_t T = v.diag ? v.nr * (v.nr - 1) / 2 : v.nr * v.ns;
     const int q = A.qp[p];
-    const int64_t x0 = k << q, x1 = min(T, (k + 1) << q);
-    int64_t mm = x0, cnt = 0;
+    mm = k << q;
+    x1 = min(T, (k + 1) << q);
+}
+
+// The walks (SBM_SPEC §4) as a persistent kernel: every lane owns one chunk at a time and performs ONE event
+// attempt per loop iteration (draw, test, binary search, emit); a lane whose chunk ends takes the next
+// unclaimed chunk (warp-aggregated claim on a global counter). The per-chunk event counts are Poisson, so a
+// thread-per-chunk walk leaves most lanes of a warp idle behind the longest chunk; here they stay busy. A
+// chunk's events depend only on the chunk, so the output (in (pair, chunk, cell) order via the count scan) is
+// the same for any assignment of chunks to lanes. WRITE = false counts (cnt[chunk]), true writes at off[chunk].
+constexpr int kSlots = 16;   // default event cells recorded per chunk by the count walk (expected <= 8 per chunk)
+
+template <bool WRITE>
+__global__ void __launch_bounds__(128) sbm_walk(SbmArgs A, unsigned long long *next, int32_t *cnt,
+                                                const int64_t *off, int32_t *src, int32_t *dst,
+                                                uint32_t *slots, int64_t *ovf, unsigned long long *novf,
+                                                const int64_t *list, int64_t nlist) {
+    const int lane = threadIdx.x & 31;
+    int64_t chunk = -1, p = 0, k = 0, x0 = 0, x1 = 0, mm = 0, a1 = 0, b1 = 0, c = 0, o = 0;
     uint32_t d = 0;
-    int64_t a1, b1;
-    cell_ab(v, mm, a1, b1);
+    PairView v{};
+    bool exhausted = false;
     for (;;) {
+        const bool need = chunk < 0 && !exhausted;
+        const unsigned nm = __ballot_sync(0xffffffffu, need);
+        if (nm) {
+            const int leader = __ffs(nm) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(next, (unsigned long long)__popc(nm));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (need) {
+                const int64_t cid = (int64_t)base + __popc(nm & ((1u << lane) - 1u));
+                if (cid >= nlist) {
+                    exhausted = true;
+                } else {
+                    chunk = list ? list[cid] : cid;
+                    chunk_setup(A, chunk, p, k, v, x1, mm);
+                    cell_ab(v, mm, a1, b1);
+                    d = 0;
+                    c = 0;
+                    x0 = mm;
+                    if (WRITE) o = off[chunk];
+                }
+            }
+        }
+        if (__all_sync(0xffffffffu, exhausted)) break;
+        if (chunk < 0) continue;
         const double u = sbm_uniform(A.seed, (uint32_t)p, (uint32_t)k, d++);
         const double E = -ln_spec64(u);
-        if (!(range_sum(A, v, a1, b1, x1 - 1) > E)) break;
-        int64_t l = mm, h = x1 - 1;
-        while (l < h) {
-            const int64_t mid = l + (h - l) / 2;
-            if (range_sum(A, v, a1, b1, mid) > E) h = mid;
-            else l = mid + 1;
+        bool end = !(range_sum(A, v, a1, b1, x1 - 1) > E);
+        if (!end) {
+            int64_t l = mm, h = x1 - 1;
+            while (l < h) {
+                const int64_t mid = l + (h - l) / 2;
+                if (range_sum(A, v, a1, b1, mid) > E) h = mid;
+                else l = mid + 1;
+            }
+            if (WRITE) {
+                int64_t a, b;
+                cell_ab(v, l, a, b);
+                src[o + c] = v.Cr[a];
+                dst[o + c] = v.diag ? v.Cr[b] : v.Cs[b];
+            } else if (slots && c < A.nslot) {
+                slots[chunk * A.nslot + c] = (uint32_t)(l - x0);   // < 2^q <= 2^30
+            }
+            ++c;
+            mm = l + 1;
+            end = mm >= x1;
+            if (!end) cell_ab(v, mm, a1, b1);
         }
-        if (WRITE) {
-            int64_t a, b;
-            cell_ab(v, l, a, b);
-            src[off + cnt] = v.Cr[a];
-            dst[off + cnt] = v.diag ? v.Cr[b] : v.Cs[b];
+        if (end) {
+            if (!WRITE) {
+                cnt[chunk] = (int32_t)c;
+                if (slots && c > A.nslot) ovf[atomicAdd(novf, 1ull)] = chunk;
+            }
+            chunk = -1;
         }
-        ++cnt;
-        mm = l + 1;
-        if (mm >= x1) break;
-        cell_ab(v, mm, a1, b1);
     }
-    return cnt;
 }
 
-__global__ void sbm_count(SbmArgs A, int32_t *cnt) {
-    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < A.nchunks; c += (int64_t)gridDim.x * blockDim.x)
-        cnt[c] = (int32_t)walk_chunk<false>(A, c, nullptr, nullptr, 0);
-}
-
-__global__ void sbm_write(SbmArgs A, const int64_t *off, int32_t *src, int32_t *dst) {
-    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < A.nchunks; c += (int64_t)gridDim.x * blockDim.x)
-        walk_chunk<true>(A, c, src, dst, off[c]);
+// Emit the recorded cells of every chunk with at most kSlots events as (src, dst) at the chunk's offset
+// (thread per chunk; a chunk's cells are in increasing order, as the walk found them).
+__global__ void __launch_bounds__(128) sbm_emit(SbmArgs A, const int32_t *cnt, const int64_t *off,
+                                                const uint32_t *slots, int32_t *src, int32_t *dst) {
+    for (int64_t chunk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; chunk < A.nchunks;
+         chunk += (int64_t)gridDim.x * blockDim.x) {
+        const int c = cnt[chunk];
+        if (c == 0 || c > A.nslot) continue;
+        int64_t p, k, x1, x0;
+        PairView v;
+        chunk_setup(A, chunk, p, k, v, x1, x0);
+        const int64_t o = off[chunk];
+        for (int i = 0; i < c; ++i) {
+            int64_t a, b;
+            cell_ab(v, x0 + slots[chunk * A.nslot + i], a, b);
+            src[o + i] = v.Cr[a];
+            dst[o + i] = v.diag ? v.Cr[b] : v.Cs[b];
+        }
+    }
 }
 
 __global__ void sbm_gather_theta(const int32_t *mem, const double *theta, int64_t n, double *thm) {
@@ -198,41 +264,80 @@ __global__ void sbm_gather_theta(const int32_t *mem, const double *theta, int64_
 }
 
 // SBM_SPEC §2: one thread per block, sequential fp64 sums in member order (over the contiguous member thetas)
-__global__ void sbm_tables(int32_t K, const int64_t *boff, const double *thm, double *P, double *Q) {
-    const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+// P_r and Q_r (SBM_SPEC §2): one warp per block. The sums are sequential in a (the spec's order), so one lane
+// runs the add chain; the warp streams the operands through shared memory 256 at a time, loading the next
+// tile into registers while the chain consumes the current one, and writes the results back coalesced.
+constexpr int kTabTile = 256;
+
+template <bool QPASS>
+__device__ __forceinline__ void tables_pass(const double *__restrict__ thm, const double *__restrict__ Pin,
+                                            int64_t b0, int64_t nr, int64_t o, double tot, double *__restrict__ out,
+                                            double *sth, double *spp, double *sout, double &acc) {
+    const int lane = threadIdx.x;
+    double rt[kTabTile / 32], rp[kTabTile / 32];
+    auto load = [&](int64_t a0) {
+#pragma unroll
+        for (int j = 0; j < kTabTile / 32; ++j) {
+            const int64_t a = a0 + j * 32 + lane;
+            rt[j] = a < nr ? thm[b0 + a] : 0.0;
+            if (QPASS) rp[j] = a < nr ? Pin[o + a + 1] : 0.0;
+        }
+    };
+    load(0);
+    for (int64_t a0 = 0; a0 < nr; a0 += kTabTile) {
+#pragma unroll
+        for (int j = 0; j < kTabTile / 32; ++j) {
+            sth[j * 32 + lane] = rt[j];
+            if (QPASS) spp[j * 32 + lane] = rp[j];
+        }
+        __syncwarp();
+        if (a0 + kTabTile < nr) load(a0 + kTabTile);   // in flight while the chain runs
+        if (lane == 0) {
+            const int cnt = (int)min((int64_t)kTabTile, nr - a0);
+            for (int i0 = 0; i0 < cnt; i0 += 8) {
+                double t[8], pp[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    t[j] = sth[i0 + j];
+                    if (QPASS) pp[j] = spp[i0 + j];
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (i0 + j < cnt) {
+                        if (QPASS) acc = __dadd_rn(acc, __dmul_rn(t[j], __dsub_rn(tot, pp[j])));
+                        else acc = __dadd_rn(acc, t[j]);
+                        sout[i0 + j] = acc;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < kTabTile / 32; ++j) {
+            const int64_t a = a0 + j * 32 + lane;
+            if (a < nr) out[o + a + 1] = sout[j * 32 + lane];
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(32) sbm_tables(int32_t K, const int64_t *boff, const double *thm, double *P,
+                                                 double *Q) {
+    __shared__ double sth[kTabTile], spp[kTabTile], sout[kTabTile];
+    const int32_t r = blockIdx.x;
     if (r >= K) return;
     const int64_t b0 = boff[r], nr = boff[r + 1] - b0, o = b0 + r;
-    // sequential in a (the spec's order); operands are loaded 8 ahead so the add chain is the only dependency
+    if (threadIdx.x == 0) {
+        P[o] = 0.0;
+        Q[o] = 0.0;
+    }
     double acc = 0.0;
-    P[o] = 0.0;
-    for (int64_t a0 = 0; a0 < nr; a0 += 8) {
-        double t[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) t[j] = a0 + j < nr ? thm[b0 + a0 + j] : 0.0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (a0 + j < nr) {
-                acc = __dadd_rn(acc, t[j]);
-                P[o + a0 + j + 1] = acc;
-            }
-    }
-    const double tot = acc;
+    tables_pass<false>(thm, nullptr, b0, nr, o, 0.0, P, sth, spp, sout, acc);
+    __syncwarp();
+    const double tot = __shfl_sync(0xffffffffu, acc, 0);
+    __threadfence_block();
     double q = 0.0;
-    Q[o] = 0.0;
-    for (int64_t a0 = 0; a0 < nr; a0 += 8) {
-        double t[8], pp[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            t[j] = a0 + j < nr ? thm[b0 + a0 + j] : 0.0;
-            pp[j] = a0 + j < nr ? P[o + a0 + j + 1] : 0.0;
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (a0 + j < nr) {
-                q = __dadd_rn(q, __dmul_rn(t[j], __dsub_rn(tot, pp[j])));
-                Q[o + a0 + j + 1] = q;
-            }
-    }
+    tables_pass<true>(thm, P, b0, nr, o, tot, Q, sth, spp, sout, q);
 }
 
 // chunks per pair (0 when omega_rs = 0 or the pair has no cells) and the pair's chunk size 2^q_p:
@@ -345,6 +450,9 @@ raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c,
     int32_t *nch = nullptr, *cnt = nullptr;
     int8_t *qp = nullptr;
     int64_t *choff = nullptr, *off = nullptr;
+    unsigned long long *next = nullptr;
+    uint32_t *slots = nullptr;
+    int64_t *ovf = nullptr;
     raftgp_status s2 = dalloc_t(ctx, &P, (size_t)(n + K + 1));
     if (s2 == RAFTGP_OK) s2 = dalloc_t(ctx, &Q, (size_t)(n + K + 1));
     if (s2 == RAFTGP_OK) s2 = dalloc_t(ctx, &thm, (size_t)std::max<int64_t>(n, 1));
@@ -362,7 +470,7 @@ raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c,
         }
         {
             LaunchScope LS(ctx, K_SBM);
-            sbm_tables<<<grid1(K, 32), 32, 0, st>>>(K, A.boff, thm, P, Q);
+            sbm_tables<<<std::max<int32_t>(K, 1), 32, 0, st>>>(K, A.boff, thm, P, Q);
         }
         {
             LaunchScope LS(ctx, K_SBM);
@@ -381,26 +489,61 @@ raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c,
     if (s2 == RAFTGP_OK && nchunks > 0) {
         s2 = dalloc_t(ctx, &cnt, (size_t)nchunks);
         if (s2 == RAFTGP_OK) s2 = dalloc_t(ctx, &off, (size_t)nchunks + 1);
-        const unsigned g = (unsigned)std::min<int64_t>(ceil_div(nchunks, 128), (int64_t)ctx->sm_count * 64);
+        if (s2 == RAFTGP_OK) s2 = dalloc_t(ctx, &next, 3);
+        if (s2 == RAFTGP_OK) RG_CUDA(cudaMemsetAsync(next, 0, 3 * sizeof(unsigned long long), st));
+        // recorded event cells (nslot per chunk; RAFTGP_SBM_SLOTS overrides, 0 = none); without room for them
+        // both passes walk
+        static const int nslot_env = [] {
+            const char *e = getenv("RAFTGP_SBM_SLOTS");
+            return e ? std::max(0, std::min(64, atoi(e))) : kSlots;
+        }();
+        A.nslot = nslot_env;
+        if (s2 == RAFTGP_OK && A.nslot > 0 && dalloc_t(ctx, &slots, (size_t)nchunks * A.nslot) != RAFTGP_OK)
+            slots = nullptr;
+        if (s2 == RAFTGP_OK && slots && dalloc_t(ctx, &ovf, (size_t)nchunks) != RAFTGP_OK) {
+            dfree(ctx, slots);
+            slots = nullptr;
+        }
+        if (!slots) A.nslot = 0;
+        static int walk_blocks = [] {
+            int b = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sbm_walk<true>, 128, 0);
+            return std::max(1, b);
+        }();
+        auto wgrid = [&](int64_t items) {
+            return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, 128), (int64_t)ctx->sm_count * walk_blocks));
+        };
         if (s2 == RAFTGP_OK) {
             LaunchScope LS(ctx, K_SBM_WALK);
-            sbm_count<<<g, 128, 0, st>>>(A, cnt);
+            sbm_walk<false><<<wgrid(nchunks), 128, 0, st>>>(A, next, cnt, nullptr, nullptr, nullptr, slots, ovf, next + 2,
+                                                           nullptr, nchunks);
         }
         if (s2 == RAFTGP_OK) s2 = scan_i32_to_i64(ctx, cnt, off, nchunks);
+        int64_t novf = 0;
         if (s2 == RAFTGP_OK) {
             RG_CUDA(cudaMemcpyAsync(&total, off + nchunks, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+            RG_CUDA(cudaMemcpyAsync(&novf, next + 2, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
             RG_CUDA(cudaStreamSynchronize(st));
         }
         if (s2 == RAFTGP_OK && total <= cap && total > 0) {
             LaunchScope LS(ctx, K_SBM_WALK);
-            sbm_write<<<g, 128, 0, st>>>(A, off, src, dst);
+            if (slots) {
+                sbm_emit<<<wgrid(nchunks), 128, 0, st>>>(A, cnt, off, slots, src, dst);
+                if (novf > 0)
+                    sbm_walk<true><<<wgrid(novf), 128, 0, st>>>(A, next + 1, nullptr, off, src, dst, nullptr, nullptr,
+                                                                nullptr, ovf, novf);
+            } else {
+                sbm_walk<true><<<wgrid(nchunks), 128, 0, st>>>(A, next + 1, nullptr, off, src, dst, nullptr, nullptr,
+                                                               nullptr, nullptr, nchunks);
+            }
         }
     }
     if (s2 == RAFTGP_OK) {
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) s2 = cuda_fail(e, "sbm kernels");
     }
-    dfree(ctx, P); dfree(ctx, Q); dfree(ctx, thm); dfree(ctx, qp); dfree(ctx, nch); dfree(ctx, choff); dfree(ctx, cnt); dfree(ctx, off);
+    dfree(ctx, P); dfree(ctx, Q); dfree(ctx, thm); dfree(ctx, qp); dfree(ctx, nch); dfree(ctx, choff); dfree(ctx, cnt); dfree(ctx, off); dfree(ctx, next);
+    dfree(ctx, slots); dfree(ctx, ovf);
     drop_members();
     if (s2 == RAFTGP_OK) *m_out = total;
     return s2;

@@ -94,3 +94,34 @@ def test_parity_diagonal_heavy(rg, ctx):
     om[0, 0] = 0.05
     for q in (4, 8, 20):
         _check(*_both(rg, ctx, c, th, om, 3, q))
+
+
+_SLOT_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, '.')
+import oracle, synth
+from paper_2312_01560_b200 import raftgp as rg
+ctx = rg.Context(0)
+c, th, om = synth.sbm_params('C2', 2, n=20000)
+for q in (6, 20):
+    rs, rd = oracle.sbm_sample(c, th, om, 11, q=q)
+    gs, gd = rg.raftgp_sbm_sample(ctx, torch.from_numpy(c).cuda(), torch.from_numpy(th).cuda(),
+                                  torch.from_numpy(om).cuda(), 11, q=q)
+    assert np.array_equal(gs.cpu().numpy(), rs) and np.array_equal(gd.cpu().numpy(), rd), q
+print('ok', rs.size)
+"""
+
+
+@pytest.mark.parametrize("slots", ["0", "1", "3"])
+def test_parity_slot_paths(rg, slots):
+    """The write pass emits the event cells recorded by the count walk (RAFTGP_SBM_SLOTS per chunk) and walks
+    again only the chunks with more events: slots = 0 (every chunk walked twice), 1 and 3 (most chunks
+    overflow) must give the oracle's edge list as the default does."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, RAFTGP_SBM_SLOTS=slots)
+    r = subprocess.run([sys.executable, "-c", _SLOT_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
