@@ -1,16 +1,17 @@
 // sbm.cu — NEXT-3: Alg. 2 (§IV), the exact degree-corrected SBM sampler, per
 // docs/SBM_SPEC.md. The walk of every block pair is cut into fixed chunks of 2^q cells (independent Poisson
 // events, so the distribution is the exact SBM one), and every chunk is one GPU thread:
-//   members   block member lists in ascending id: the CSR build (csr.cu) of the bipartite edge list
-//             (i, N + c_i), keeping only the block rows N..N+K-1
+//   members   block member lists in ascending id: a stable counting sort by block (K <= 4096), else the CSR
+//             build (csr.cu) of the bipartite edge list (i, N + c_i), keeping only the block rows N..N+K-1
 //   tables    P_r (theta prefix sums) and Q_r (upper-triangle row-sum prefixes), one thread per block,
 //             sequential fp64 in the spec's order
 //   chunks    per pair (r <= s): T_rs cells -> ceil(T / 2^q) chunks; exclusive scan -> chunk ids
 //   count     persistent walk, one chunk per lane at a time (draw u, E = -ln_spec64(u), binary search of the
 //             first cell whose RangeSum exceeds E), counting edges and recording the first kSlots event
 //             cells of every chunk
-//   write     scan of the counts, then the recorded cells are emitted as (src, dst) at the chunk's offset;
-//             only chunks with more than kSlots events are walked again
+//   write     scan of the counts, then the recorded cells (and the logged events past them) are emitted as
+//             (src, dst) at the chunk's offset; without room for the log, the chunks with more than nslot
+//             events are walked again
 // Every floating-point value that decides an integer (RangeSum bits, E) is computed with the spec's operation
 // sequence (explicit round-to-nearest intrinsics, no contraction), so the edge list is bit-identical to the
 // oracle's, in (pair, chunk, cell) order.
@@ -169,16 +170,38 @@ __device__ __forceinline__ void chunk_setup(const SbmArgs &A, int64_t chunk, int
 // the same for any assignment of chunks to lanes. WRITE = false counts (cnt[chunk]), true writes at off[chunk].
 constexpr int kSlots = 16;   // default event cells recorded per chunk by the count walk (expected <= 8 per chunk)
 
+// Events past a chunk's nslot recorded cells (the hub rows of dense diagonal pairs hold hundreds per chunk)
+// go to an append-only log, staged per warp in shared memory and flushed with one atomic per kWarpLog entries.
+struct LogEnt {
+    int64_t chunk;
+    uint32_t c;      // event index within the chunk
+    uint32_t cell;   // cell offset from the chunk start
+};
+constexpr int kWarpLog = 64;
+
 template <bool WRITE>
 __global__ void __launch_bounds__(128) sbm_walk(SbmArgs A, unsigned long long *next, int32_t *cnt,
                                                 const int64_t *off, int32_t *src, int32_t *dst,
                                                 uint32_t *slots, int64_t *ovf, unsigned long long *novf,
+                                                LogEnt *log, unsigned long long *nlog, int64_t log_cap,
                                                 const int64_t *list, int64_t nlist) {
-    const int lane = threadIdx.x & 31;
+    __shared__ LogEnt wbuf[WRITE ? 1 : 4][WRITE ? 1 : kWarpLog];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int64_t chunk = -1, p = 0, k = 0, x0 = 0, x1 = 0, mm = 0, a1 = 0, b1 = 0, c = 0, o = 0;
     uint32_t d = 0;
     PairView v{};
     bool exhausted = false;
+    int wc = 0;   // staged log entries of this warp (warp-uniform)
+    auto flush = [&]() {
+        __syncwarp();
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(nlog, (unsigned long long)wc);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        for (int i = lane; i < wc; i += 32)
+            if ((int64_t)(base + i) < log_cap) log[base + i] = wbuf[w][i];
+        __syncwarp();
+        wc = 0;
+    };
     for (;;) {
         const bool need = chunk < 0 && !exhausted;
         const unsigned nm = __ballot_sync(0xffffffffu, need);
@@ -203,48 +226,70 @@ __global__ void __launch_bounds__(128) sbm_walk(SbmArgs A, unsigned long long *n
             }
         }
         if (__all_sync(0xffffffffu, exhausted)) break;
-        if (chunk < 0) continue;
-        const double u = sbm_uniform(A.seed, (uint32_t)p, (uint32_t)k, d++);
-        const double E = -ln_spec64(u);
-        bool end = !(range_sum(A, v, a1, b1, x1 - 1) > E);
-        if (!end) {
-            int64_t l = mm, h = x1 - 1;
-            while (l < h) {
-                const int64_t mid = l + (h - l) / 2;
-                if (range_sum(A, v, a1, b1, mid) > E) h = mid;
-                else l = mid + 1;
+        bool lg = false;
+        LogEnt ent;
+        if (chunk >= 0) {
+            const double u = sbm_uniform(A.seed, (uint32_t)p, (uint32_t)k, d++);
+            const double E = -ln_spec64(u);
+            bool end = !(range_sum(A, v, a1, b1, x1 - 1) > E);
+            if (!end) {
+                int64_t l = mm, h = x1 - 1;
+                while (l < h) {
+                    const int64_t mid = l + (h - l) / 2;
+                    if (range_sum(A, v, a1, b1, mid) > E) h = mid;
+                    else l = mid + 1;
+                }
+                if (WRITE) {
+                    int64_t a, b;
+                    cell_ab(v, l, a, b);
+                    src[o + c] = v.Cr[a];
+                    dst[o + c] = v.diag ? v.Cr[b] : v.Cs[b];
+                } else if (slots) {
+                    if (c < A.nslot) {
+                        slots[chunk * A.nslot + c] = (uint32_t)(l - x0);   // < 2^q <= 2^30
+                    } else if (log) {
+                        lg = true;
+                        ent.chunk = chunk;
+                        ent.c = (uint32_t)c;
+                        ent.cell = (uint32_t)(l - x0);
+                    }
+                }
+                ++c;
+                mm = l + 1;
+                end = mm >= x1;
+                if (!end) cell_ab(v, mm, a1, b1);
             }
-            if (WRITE) {
-                int64_t a, b;
-                cell_ab(v, l, a, b);
-                src[o + c] = v.Cr[a];
-                dst[o + c] = v.diag ? v.Cr[b] : v.Cs[b];
-            } else if (slots && c < A.nslot) {
-                slots[chunk * A.nslot + c] = (uint32_t)(l - x0);   // < 2^q <= 2^30
+            if (end) {
+                if (!WRITE) {
+                    cnt[chunk] = (int32_t)c;
+                    if (slots && c > A.nslot) ovf[atomicAdd(novf, 1ull)] = chunk;
+                }
+                chunk = -1;
             }
-            ++c;
-            mm = l + 1;
-            end = mm >= x1;
-            if (!end) cell_ab(v, mm, a1, b1);
         }
-        if (end) {
-            if (!WRITE) {
-                cnt[chunk] = (int32_t)c;
-                if (slots && c > A.nslot) ovf[atomicAdd(novf, 1ull)] = chunk;
+        if (!WRITE && log) {   // converged: stage this iteration's log entries
+            const unsigned lm = __ballot_sync(0xffffffffu, lg);
+            if (lm) {
+                const int nn = __popc(lm);
+                if (wc + nn > kWarpLog) flush();
+                if (lg) wbuf[w][wc + __popc(lm & ((1u << lane) - 1u))] = ent;
+                wc += nn;
             }
-            chunk = -1;
         }
     }
+    if (!WRITE && log && wc > 0) flush();
 }
 
-// Emit the recorded cells of every chunk with at most kSlots events as (src, dst) at the chunk's offset
-// (thread per chunk; a chunk's cells are in increasing order, as the walk found them).
+// Emit the recorded cells of every chunk as (src, dst) at the chunk's offset (thread per chunk; a chunk's
+// cells are in increasing order, as the walk found them): all of them for chunks with at most nslot events,
+// the first nslot of the others when the log holds the rest (with_log), none of those otherwise.
 __global__ void __launch_bounds__(128) sbm_emit(SbmArgs A, const int32_t *cnt, const int64_t *off,
-                                                const uint32_t *slots, int32_t *src, int32_t *dst) {
+                                                const uint32_t *slots, bool with_log, int32_t *src, int32_t *dst) {
     for (int64_t chunk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; chunk < A.nchunks;
          chunk += (int64_t)gridDim.x * blockDim.x) {
-        const int c = cnt[chunk];
-        if (c == 0 || c > A.nslot) continue;
+        const int call = cnt[chunk];
+        if (call == 0 || (call > A.nslot && !with_log)) continue;
+        const int c = min(call, A.nslot);
         int64_t p, k, x1, x0;
         PairView v;
         chunk_setup(A, chunk, p, k, v, x1, x0);
@@ -255,6 +300,22 @@ __global__ void __launch_bounds__(128) sbm_emit(SbmArgs A, const int32_t *cnt, c
             src[o + i] = v.Cr[a];
             dst[o + i] = v.diag ? v.Cr[b] : v.Cs[b];
         }
+    }
+}
+
+// Emit the logged events (thread per entry) at off[chunk] + c.
+__global__ void __launch_bounds__(128) sbm_emit_log(SbmArgs A, const LogEnt *log, int64_t nlog, const int64_t *off,
+                                                    int32_t *src, int32_t *dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nlog; i += (int64_t)gridDim.x * blockDim.x) {
+        const LogEnt e = log[i];
+        int64_t p, k, x1, x0;
+        PairView v;
+        chunk_setup(A, e.chunk, p, k, v, x1, x0);
+        int64_t a, b;
+        cell_ab(v, x0 + e.cell, a, b);
+        const int64_t o = off[e.chunk] + e.c;
+        src[o] = v.Cr[a];
+        dst[o] = v.diag ? v.Cr[b] : v.Cs[b];
     }
 }
 
@@ -396,6 +457,67 @@ __global__ void sbm_validate(const int32_t *c, const double *theta, int64_t n, c
     }
 }
 
+// Member lists (block r's nodes in ascending id) by a stable counting sort, for K <= kMemMaxK: one warp per tile
+// of kMemTile consecutive nodes counts its blocks in shared memory (bucket-major counts, no global atomics); a
+// scan gives every (block, tile) its offset; the same warp then places its nodes in id order, ranking equal
+// blocks within each 32-node round with __match_any_sync (stable). Larger K: the CSR build of (i, N + c_i).
+constexpr int kMemTile = 2048;
+constexpr int kMemWarps = 4;
+constexpr int kMemMaxK = 4096;
+
+__global__ void __launch_bounds__(kMemWarps * 32) sbm_member_count(const int32_t *__restrict__ c, int64_t n, int K,
+                                                                  int64_t ntiles, int32_t *__restrict__ cnt) {
+    extern __shared__ int32_t mcs[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int32_t *h = mcs + (size_t)w * K;
+    for (int64_t tile = (int64_t)blockIdx.x * kMemWarps + w; tile < ntiles; tile += (int64_t)gridDim.x * kMemWarps) {
+        for (int b = lane; b < K; b += 32) h[b] = 0;
+        __syncwarp();
+        const int64_t t0 = tile * kMemTile, t1 = min(n, t0 + kMemTile);
+        for (int64_t i = t0 + lane; i < t1; i += 32) atomicAdd(&h[__ldg(c + i)], 1);
+        __syncwarp();
+        for (int b = lane; b < K; b += 32) cnt[(int64_t)b * ntiles + tile] = h[b];
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(kMemWarps * 32) sbm_member_scatter(const int32_t *__restrict__ c, int64_t n, int K,
+                                                                    int64_t ntiles, const int64_t *__restrict__ base,
+                                                                    int32_t *__restrict__ mem) {
+    extern __shared__ long long mss[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    long long *h = mss + (size_t)w * K;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t tile = (int64_t)blockIdx.x * kMemWarps + w; tile < ntiles; tile += (int64_t)gridDim.x * kMemWarps) {
+        for (int b = lane; b < K; b += 32) h[b] = base[(int64_t)b * ntiles + tile];
+        __syncwarp();
+        const int64_t t0 = tile * kMemTile, t1 = min(n, t0 + kMemTile);
+        for (int64_t r0 = t0; r0 < t1; r0 += 8 * 32) {
+            int32_t bb[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int64_t i = r0 + j * 32 + lane;
+                bb[j] = i < t1 ? __ldg(c + i) : -1;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int64_t i = r0 + j * 32 + lane;
+                const int32_t b = bb[j];
+                const unsigned peers = __match_any_sync(0xffffffffu, b);
+                if (b >= 0) mem[h[b] + __popc(peers & lt)] = (int32_t)i;
+                __syncwarp();
+                if (b >= 0 && lane == __ffs(peers) - 1) h[b] += __popc(peers);
+                __syncwarp();
+            }
+        }
+    }
+}
+
+__global__ void sbm_member_boff(const int64_t *base, int K, int64_t ntiles, int64_t n, int64_t *boff) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b <= K) boff[b] = b < K ? base[(int64_t)b * ntiles] : n;
+}
+
 inline unsigned grid1(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, ceil_div(n, t)); }
 
 }  // namespace
@@ -418,30 +540,70 @@ raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c,
     dfree(ctx, err);
     if (herr) return fail(RAFTGP_ERR_PARAM, "raftgp_sbm_sample: label outside [0,K), theta <= 0, or Omega negative / "
                                             "not symmetric");
-    // members per block (ascending id): CSR rows N..N+K-1 of the bipartite edges (i, N + c_i)
-    int32_t *bsrc = nullptr;
-    RG_TRY(dalloc_t(ctx, &bsrc, 2 * (size_t)std::max<int64_t>(n, 1)));
-    {
-        LaunchScope LS(ctx, K_SBM);
-        sbm_bip_edges<<<grid1(n, 256), 256, 0, st>>>(c, n, bsrc, bsrc + n);
-    }
-    RG_CHECK_LAUNCH(ctx);
+    // members per block (ascending id)
     raftgp_graph_s members;
     members.ctx = ctx;
-    raftgp_status rs = csr_build(ctx, n + K, n, bsrc, bsrc + n, n, n + K, &members);
-    dfree(ctx, bsrc);
+    int64_t *mboff = nullptr;
+    int32_t *mmem = nullptr;
     auto drop_members = [&]() {
         dfree(ctx, members.row_ptr); dfree(ctx, members.col); dfree(ctx, members.deg_local); dfree(ctx, members.order);
         dfree(ctx, members.deg_all); dfree(ctx, members.s_all); dfree(ctx, members.sh_all);
+        dfree(ctx, mboff); dfree(ctx, mmem);
     };
-    if (rs != RAFTGP_OK) {
-        drop_members();
-        return rs;
+    if (K <= kMemMaxK) {   // stable counting sort
+        const int64_t ntiles = std::max<int64_t>(1, ceil_div(n, kMemTile));
+        int32_t *mcnt = nullptr;
+        int64_t *mbase = nullptr;
+        raftgp_status rs = dalloc_t(ctx, &mcnt, (size_t)K * ntiles);
+        if (rs == RAFTGP_OK) rs = dalloc_t(ctx, &mbase, (size_t)K * ntiles + 1);
+        if (rs == RAFTGP_OK) rs = dalloc_t(ctx, &mboff, (size_t)K + 1);
+        if (rs == RAFTGP_OK) rs = dalloc_t(ctx, &mmem, (size_t)std::max<int64_t>(n, 1));
+        static bool attrs = false;
+        if (rs == RAFTGP_OK && !attrs) {
+            cudaFuncSetAttribute(sbm_member_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kMemWarps * kMemMaxK * 4);
+            cudaFuncSetAttribute(sbm_member_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kMemWarps * kMemMaxK * 8);
+            attrs = true;
+        }
+        const unsigned mg = (unsigned)ceil_div(ntiles, kMemWarps);
+        if (rs == RAFTGP_OK) {
+            LaunchScope LS(ctx, K_SBM);
+            sbm_member_count<<<mg, kMemWarps * 32, (size_t)kMemWarps * K * 4, st>>>(c, n, K, ntiles, mcnt);
+        }
+        if (rs == RAFTGP_OK) rs = scan_i32_to_i64(ctx, mcnt, mbase, (int64_t)K * ntiles);
+        if (rs == RAFTGP_OK) {
+            LaunchScope LS(ctx, K_SBM);
+            sbm_member_scatter<<<mg, kMemWarps * 32, (size_t)kMemWarps * K * 8, st>>>(c, n, K, ntiles, mbase, mmem);
+            sbm_member_boff<<<grid1(K + 1, 256), 256, 0, st>>>(mbase, K, ntiles, n, mboff);
+        }
+        if (rs == RAFTGP_OK) {
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) rs = cuda_fail(e, "sbm member lists");
+        }
+        dfree(ctx, mcnt);
+        dfree(ctx, mbase);
+        if (rs != RAFTGP_OK) {
+            drop_members();
+            return rs;
+        }
+    } else {   // CSR rows N..N+K-1 of the bipartite edges (i, N + c_i)
+        int32_t *bsrc = nullptr;
+        RG_TRY(dalloc_t(ctx, &bsrc, 2 * (size_t)std::max<int64_t>(n, 1)));
+        {
+            LaunchScope LS(ctx, K_SBM);
+            sbm_bip_edges<<<grid1(n, 256), 256, 0, st>>>(c, n, bsrc, bsrc + n);
+        }
+        RG_CHECK_LAUNCH(ctx);
+        raftgp_status rs = csr_build(ctx, n + K, n, bsrc, bsrc + n, n, n + K, &members);
+        dfree(ctx, bsrc);
+        if (rs != RAFTGP_OK) {
+            drop_members();
+            return rs;
+        }
     }
     SbmArgs A{};
     A.K = K;
-    A.boff = members.row_ptr;
-    A.mem = members.col;
+    A.boff = mboff ? mboff : members.row_ptr;
+    A.mem = mmem ? mmem : members.col;
     A.omega = omega;
     A.seed = seed;
     A.q = q;
@@ -453,6 +615,7 @@ raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c,
     unsigned long long *next = nullptr;
     uint32_t *slots = nullptr;
     int64_t *ovf = nullptr;
+    LogEnt *logb = nullptr;
     raftgp_status s2 = dalloc_t(ctx, &P, (size_t)(n + K + 1));
     if (s2 == RAFTGP_OK) s2 = dalloc_t(ctx, &Q, (size_t)(n + K + 1));
     if (s2 == RAFTGP_OK) s2 = dalloc_t(ctx, &thm, (size_t)std::max<int64_t>(n, 1));
@@ -489,10 +652,11 @@ raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c,
     if (s2 == RAFTGP_OK && nchunks > 0) {
         s2 = dalloc_t(ctx, &cnt, (size_t)nchunks);
         if (s2 == RAFTGP_OK) s2 = dalloc_t(ctx, &off, (size_t)nchunks + 1);
-        if (s2 == RAFTGP_OK) s2 = dalloc_t(ctx, &next, 3);
-        if (s2 == RAFTGP_OK) RG_CUDA(cudaMemsetAsync(next, 0, 3 * sizeof(unsigned long long), st));
-        // recorded event cells (nslot per chunk; RAFTGP_SBM_SLOTS overrides, 0 = none); without room for them
-        // both passes walk
+        if (s2 == RAFTGP_OK) s2 = dalloc_t(ctx, &next, 4);
+        if (s2 == RAFTGP_OK) RG_CUDA(cudaMemsetAsync(next, 0, 4 * sizeof(unsigned long long), st));
+        // recorded event cells (nslot per chunk; RAFTGP_SBM_SLOTS overrides, 0 = none) and the log of the
+        // events past them; without room for the cells both passes walk, without room for the log the write
+        // pass re-walks the chunks with more than nslot events
         static const int nslot_env = [] {
             const char *e = getenv("RAFTGP_SBM_SLOTS");
             return e ? std::max(0, std::min(64, atoi(e))) : kSlots;
@@ -505,9 +669,16 @@ raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c,
             slots = nullptr;
         }
         if (!slots) A.nslot = 0;
+        static const int64_t log_env = [] {   // RAFTGP_SBM_LOG: log capacity override (0 = no log)
+            const char *e = getenv("RAFTGP_SBM_LOG");
+            return e ? std::max<int64_t>(0, atoll(e)) : (int64_t)-1;
+        }();
+        const int64_t log_cap = !slots ? 0 : log_env >= 0 ? log_env : std::max<int64_t>(1 << 20, nchunks);
+        if (s2 == RAFTGP_OK && log_cap > 0 && dalloc(ctx, reinterpret_cast<void **>(&logb), (size_t)log_cap * sizeof(LogEnt)) != RAFTGP_OK)
+            logb = nullptr;
         static int walk_blocks = [] {
             int b = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sbm_walk<true>, 128, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sbm_walk<false>, 128, 0);
             return std::max(1, b);
         }();
         auto wgrid = [&](int64_t items) {
@@ -516,25 +687,29 @@ raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c,
         if (s2 == RAFTGP_OK) {
             LaunchScope LS(ctx, K_SBM_WALK);
             sbm_walk<false><<<wgrid(nchunks), 128, 0, st>>>(A, next, cnt, nullptr, nullptr, nullptr, slots, ovf, next + 2,
-                                                           nullptr, nchunks);
+                                                           logb, next + 3, log_cap, nullptr, nchunks);
         }
         if (s2 == RAFTGP_OK) s2 = scan_i32_to_i64(ctx, cnt, off, nchunks);
-        int64_t novf = 0;
+        int64_t novf = 0, nlogged = 0;
         if (s2 == RAFTGP_OK) {
             RG_CUDA(cudaMemcpyAsync(&total, off + nchunks, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
             RG_CUDA(cudaMemcpyAsync(&novf, next + 2, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+            RG_CUDA(cudaMemcpyAsync(&nlogged, next + 3, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
             RG_CUDA(cudaStreamSynchronize(st));
         }
         if (s2 == RAFTGP_OK && total <= cap && total > 0) {
             LaunchScope LS(ctx, K_SBM_WALK);
             if (slots) {
-                sbm_emit<<<wgrid(nchunks), 128, 0, st>>>(A, cnt, off, slots, src, dst);
-                if (novf > 0)
+                const bool with_log = logb && nlogged <= log_cap;
+                sbm_emit<<<wgrid(nchunks), 128, 0, st>>>(A, cnt, off, slots, with_log, src, dst);
+                if (with_log && nlogged > 0)
+                    sbm_emit_log<<<grid1(nlogged, 128), 128, 0, st>>>(A, logb, nlogged, off, src, dst);
+                if (!with_log && novf > 0)
                     sbm_walk<true><<<wgrid(novf), 128, 0, st>>>(A, next + 1, nullptr, off, src, dst, nullptr, nullptr,
-                                                                nullptr, ovf, novf);
+                                                                nullptr, nullptr, nullptr, 0, ovf, novf);
             } else {
                 sbm_walk<true><<<wgrid(nchunks), 128, 0, st>>>(A, next + 1, nullptr, off, src, dst, nullptr, nullptr,
-                                                               nullptr, nullptr, nchunks);
+                                                               nullptr, nullptr, nullptr, 0, nullptr, nchunks);
             }
         }
     }
@@ -543,7 +718,7 @@ raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c,
         if (e != cudaSuccess) s2 = cuda_fail(e, "sbm kernels");
     }
     dfree(ctx, P); dfree(ctx, Q); dfree(ctx, thm); dfree(ctx, qp); dfree(ctx, nch); dfree(ctx, choff); dfree(ctx, cnt); dfree(ctx, off); dfree(ctx, next);
-    dfree(ctx, slots); dfree(ctx, ovf);
+    dfree(ctx, slots); dfree(ctx, ovf); dfree(ctx, logb);
     drop_members();
     if (s2 == RAFTGP_OK) *m_out = total;
     return s2;

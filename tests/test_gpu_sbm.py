@@ -112,16 +112,30 @@ print('ok', rs.size)
 """
 
 
-@pytest.mark.parametrize("slots", ["0", "1", "3"])
-def test_parity_slot_paths(rg, slots):
-    """The write pass emits the event cells recorded by the count walk (RAFTGP_SBM_SLOTS per chunk) and walks
-    again only the chunks with more events: slots = 0 (every chunk walked twice), 1 and 3 (most chunks
-    overflow) must give the oracle's edge list as the default does."""
+@pytest.mark.parametrize("slots,log", [("0", None), ("1", None), ("3", None), ("1", "0"), ("2", "100")])
+def test_parity_slot_paths(rg, slots, log):
+    """The write pass emits the event cells recorded by the count walk (RAFTGP_SBM_SLOTS per chunk) and the
+    events logged past them (RAFTGP_SBM_LOG entries); chunks whose events do not all fit are walked again.
+    slots = 0 (every chunk walked twice), 1 and 3 (most events logged), no log (overflow chunks re-walked) and
+    a log too small for the events (falls back to the re-walk) must all give the oracle's edge list."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, RAFTGP_SBM_SLOTS=slots)
+    if log is not None:
+        env["RAFTGP_SBM_LOG"] = log
     r = subprocess.run([sys.executable, "-c", _SLOT_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_parity_many_blocks(rg, ctx):
+    """K above the counting-sort limit (4096): member lists come from the CSR build path instead."""
+    rng = np.random.default_rng(5)
+    n, K = 6000, 4200
+    c = rng.integers(0, K, n).astype(np.int32)
+    th = rng.uniform(0.5, 3.0, n)
+    om = np.full((K, K), 2e-3)
+    np.fill_diagonal(om, 0.5)
+    _check(*_both(rg, ctx, c, th, om, 3, 20))
