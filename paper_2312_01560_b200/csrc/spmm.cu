@@ -56,7 +56,11 @@ struct HopArgs {
     float *Tn2;                // KIND_DUAL: second variant's T
     bool scale_sh;             // multiply the stored rows by s^_i (feature hop on Theta' = Theta W1)
     int32_t tn_ld;             // row stride of Tn in floats (0 = WN)
+    unsigned long long *ctr;   // zeroed group counter: warps claim kClaim row groups at a time (degree skew), or
+                               // null: static grid-stride
 };
+
+constexpr int kClaim = 8;      // row groups per dynamic claim
 
 __device__ __forceinline__ float4 ldg4(const float4 *p) { return __ldg(p); }
 
@@ -193,7 +197,15 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
     const int sub = lane / LPN, cl = lane % LPN;
     const int64_t ngroups = (a.nl + RB - 1) / RB;
     const int64_t gw = (int64_t)gridDim.x * wpb;
-    for (int64_t grp = (int64_t)blockIdx.x * wpb + wib; grp < ngroups; grp += gw) {
+    int64_t grp = (int64_t)blockIdx.x * wpb + wib, glim = 0;
+    for (;; grp += a.ctr ? 1 : gw) {
+        if (a.ctr && grp >= glim) {   // dynamic: the warp's next kClaim groups
+            unsigned long long g0 = 0;
+            if (lane == 0) g0 = atomicAdd(a.ctr, (unsigned long long)kClaim);
+            grp = (int64_t)__shfl_sync(FULL, g0, 0);
+            glim = grp + kClaim;
+        }
+        if (grp >= ngroups) break;
         const int64_t row0 = grp * RB;
         const int rows_here = (a.nl - row0 < RB) ? static_cast<int>(a.nl - row0) : RB;
         // first col chunk of the group's first row; each row prefetches the next row's first chunk
@@ -422,10 +434,21 @@ raftgp_status launch_fast(raftgp_ctx ctx, const HopArgs &a) {
     const int64_t want = ceil_div(groups, WPB);
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count * blocks_per_sm)));
     const int kid = (KIND == KIND_GCN || KIND == KIND_GCN2) ? K_GCN_HOP : (KIND == KIND_LOAD ? K_TRANSFORM : K_FEATURE_HOP);
+    HopArgs b = a;
+    b.ctr = nullptr;
+    static const bool dyn = [] {   // RAFTGP_HOP_DYN=0: static grid-stride groups
+        const char *e = getenv("RAFTGP_HOP_DYN");
+        return !(e && e[0] == '0');
+    }();
+    if (dyn && KIND != KIND_LOAD) {
+        RG_TRY(dalloc_t(ctx, &b.ctr, 1));
+        RG_CUDA(cudaMemsetAsync(b.ctr, 0, sizeof(unsigned long long), ctx->stream));
+    }
     {
         LaunchScope L(ctx, kid);
-        kern<<<grid, THREADS, smem, ctx->stream>>>(a);
+        kern<<<grid, THREADS, smem, ctx->stream>>>(b);
     }
+    dfree(ctx, b.ctr);
     RG_CHECK_LAUNCH(ctx);
     return RAFTGP_OK;
 }

@@ -257,6 +257,7 @@ struct WideArgs {
     float *out2;             // W_DUAL: the MOD variant's T
     float *zhi, *zlo;        // GCN: Z split and tiled as the next GEMM's A operand (may be null)
     float *ssq;              // GCN, deferred normalisation: per-row, per-slice sums of squares (n x NW) or null
+    unsigned long long *ctr; // zeroed row counter: CTAs claim rows dynamically (degree skew), or null (grid-stride)
 };
 
 template <int KIND, int V, int U>
@@ -270,7 +271,14 @@ __global__ void __launch_bounds__(512) hop_wide(WideArgs a) {
     const float4 *X4 = reinterpret_cast<const float4 *>(a.X);
     const int64_t W4 = a.W / 4;
     const int64_t cbase = (int64_t)slice * (CW / 4);   // first float4 column of this slice
-    for (int64_t r0 = (int64_t)blockIdx.x * rpc; r0 < a.n; r0 += (int64_t)gridDim.x * rpc) {
+    __shared__ long long claim;
+    for (int64_t r0 = (int64_t)blockIdx.x * rpc;; r0 += (int64_t)gridDim.x * rpc) {
+        if (a.ctr) {   // dynamic: the CTA's next rpc rows (a hub row no longer delays a statically assigned range)
+            if (threadIdx.x == 0) claim = (long long)atomicAdd(a.ctr, (unsigned long long)rpc);
+            __syncthreads();
+            r0 = claim;
+        }
+        if (r0 >= a.n) break;
         const int64_t i = r0 + rsub;
         const bool valid = i < a.n;
         float4 acc[V], acc2[V];
@@ -394,6 +402,7 @@ __global__ void __launch_bounds__(512) hop_wide(WideArgs a) {
                 }
             }
         }
+        if (a.ctr) __syncthreads();   // every warp has read `claim` before thread 0 overwrites it
     }
 }
 
@@ -654,12 +663,25 @@ raftgp_status launch_wide(raftgp_ctx ctx, const WideArgs &a) {
     const int rpc = warps / NW;
     const int64_t per_sm = 2048 / (32 * warps);   // CTAs per SM in the grid (grid-stride over rows)
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.n, rpc), ctx->sm_count * per_sm));
-    LaunchScope LS(ctx, K_WIDE_HOP);
-    // neighbours in flight per lane: U x V float4 (DUAL keeps two accumulator sets, so a smaller U)
-    constexpr int U4 = KIND == W_DUAL ? RG_WIDE_U_DUAL : RG_WIDE_U;
-    if (V == 1) hop_wide<KIND, 1, 2 * U4><<<grid, 32 * warps, 0, ctx->stream>>>(a);
-    else if (V == 2) hop_wide<KIND, 2, 2 * U4><<<grid, 32 * warps, 0, ctx->stream>>>(a);
-    else hop_wide<KIND, 4, U4><<<grid, 32 * warps, 0, ctx->stream>>>(a);
+    WideArgs b = a;
+    b.ctr = nullptr;
+    static const bool dyn = [] {   // RAFTGP_WIDE_DYN=0: static grid-stride rows
+        const char *e = getenv("RAFTGP_WIDE_DYN");
+        return !(e && e[0] == '0');
+    }();
+    if (dyn) {
+        RG_TRY(dalloc_t(ctx, &b.ctr, 1));
+        RG_CUDA(cudaMemsetAsync(b.ctr, 0, sizeof(unsigned long long), ctx->stream));
+    }
+    {
+        LaunchScope LS(ctx, K_WIDE_HOP);
+        // neighbours in flight per lane: U x V float4 (DUAL keeps two accumulator sets, so a smaller U)
+        constexpr int U4 = KIND == W_DUAL ? RG_WIDE_U_DUAL : RG_WIDE_U;
+        if (V == 1) hop_wide<KIND, 1, 2 * U4><<<grid, 32 * warps, 0, ctx->stream>>>(b);
+        else if (V == 2) hop_wide<KIND, 2, 2 * U4><<<grid, 32 * warps, 0, ctx->stream>>>(b);
+        else hop_wide<KIND, 4, U4><<<grid, 32 * warps, 0, ctx->stream>>>(b);
+    }
+    dfree(ctx, b.ctr);
     return RAFTGP_OK;
 }
 
