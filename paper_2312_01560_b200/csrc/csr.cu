@@ -557,7 +557,8 @@ __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PAC
                                                         int64_t *__restrict__ raw_ptr,
                                                         int64_t nl, int shift, int nb, int vbits,
                                                         int32_t *__restrict__ col_raw, int32_t *__restrict__ deg,
-                                                        int64_t *__restrict__ fb_rows, int32_t *__restrict__ fb_count) {
+                                                        int64_t *__restrict__ fb_rows, int32_t *__restrict__ fb_count,
+                                                        unsigned int *__restrict__ bnext) {
     extern __shared__ int32_t bsm[];
     int32_t *s = bsm;                                   // kBucketCap values
     int32_t *cur = bsm + kBucketCap;                    // B cursors (first: the row counts)
@@ -568,7 +569,12 @@ __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PAC
     const int lane = threadIdx.x & 31;
     constexpr int kLoadBatch = 8;
     constexpr int kRowsPerThread = kMaxBucketRows / 1024;
-    for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+    __shared__ int bclaim;
+    for (;;) {   // buckets claimed dynamically (their sizes and hub rows vary)
+        if (threadIdx.x == 0) bclaim = (int)atomicAdd(bnext, 1u);
+        __syncthreads();
+        const int b = bclaim;
+        if (b >= nb) break;
         const int64_t r0 = (int64_t)b << shift;
         const int nr = static_cast<int>(min(nl, r0 + ((int64_t)1 << shift)) - r0);
         const int64_t e0 = base[(int64_t)b * pgrid];            // bucket b starts at its first CTA's offset
@@ -828,7 +834,10 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
         int32_t *bcnt = nullptr;
         int64_t *bstart = nullptr;
         unsigned long long *bcur = nullptr;
+        unsigned int *bnext = nullptr;
         RG_TRY(dalloc_t(ctx, &bcur, (size_t)nb));
+        RG_TRY(dalloc_t(ctx, &bnext, 1));
+        RG_CUDA(cudaMemsetAsync(bnext, 0, sizeof(unsigned int), st));
         RG_TRY(dalloc_t(ctx, &bcnt, (size_t)nb * pgrid));
         RG_TRY(dalloc_t(ctx, &bstart, (size_t)nb * pgrid + 1));
         RG_TRY(dalloc(ctx, &pairs, (size_t)cap * (packed ? 4 : 8)));
@@ -873,11 +882,11 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
             if (packed)
                 csr_bucket_sort<true><<<bgrid, 1024, bsmem, st>>>(static_cast<const uint32_t *>(pairs), bstart, pgrid, raw_ptr,
                                                                   nl, shift, nb, vbits, col_raw, g->deg_local, fb_rows,
-                                                                  fb_count);
+                                                                  fb_count, bnext);
             else
                 csr_bucket_sort<false><<<bgrid, 1024, bsmem, st>>>(static_cast<const int2 *>(pairs), bstart, pgrid, raw_ptr,
                                                                    nl, shift, nb, vbits, col_raw, g->deg_local, fb_rows,
-                                                                   fb_count);
+                                                                   fb_count, bnext);
         }
         RG_CHECK_LAUNCH(ctx);
         {
@@ -888,6 +897,7 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
         dfree(ctx, bcnt);
         dfree(ctx, bstart);
         dfree(ctx, bcur);
+        dfree(ctx, bnext);
         dfree(ctx, pairs);
     } else {
         if (m > 0) {
