@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-table1", action="store_true", help="skip the NEXT-2 Table I widths measurement")
     ap.add_argument("--table1-steps", type=int, default=3)
     ap.add_argument("--no-sbm", action="store_true", help="skip the NEXT-3 SBM sampler measurement")
+    ap.add_argument("--e2e-lanes", type=int, default=3, help="contexts/streams the e2e steps rotate over (N = 1)")
+    ap.add_argument("--e2e-api", default="separate", choices=["separate", "build_embed"],
+                    help="e2e step: raftgp_build_csr + raftgp_embed_multi, or raftgp_build_embed")
     ap.add_argument("--no-stream", action="store_true", help="skip the NEXT-4 streaming-update measurement")
     ap.add_argument("--clock-period-ms", type=int, default=200)
     ap.add_argument("--clock-query", default=None)
@@ -628,27 +631,38 @@ def main():
         d2h = int(sum(rows * dims[-1] * 4 for _ in variants))
         if world == 1 and not args.no_fuse_variants:
             lanes = []
-            for _ in range(3):
+            for _ in range(args.e2e_lanes):
                 s_ = torch.cuda.Stream(dev)
                 cs_ = torch.cuda.Stream(dev)          # D2H of this lane's Z, off the compute stream
                 c_ = rg.Context(dev.index, stream=s_)
-                Zl = {v: torch.empty((rows, dims[-1]), dtype=torch.float32, device=dev) for v in variants}
-                Hl = {v: torch.empty((rows, dims[-1]), dtype=torch.float32).pin_memory() for v in variants}
-                lanes.append((s_, c_, Zl, Hl, cs_))
+                # two Z buffers per lane: a step waits only for the D2H of its buffer's previous use (two
+                # rounds back), recorded as an event, not for the lane's latest copy
+                Zl = [{v: torch.empty((rows, dims[-1]), dtype=torch.float32, device=dev) for v in variants}
+                      for _ in range(2)]
+                Hl = [{v: torch.empty((rows, dims[-1]), dtype=torch.float32).pin_memory() for v in variants}
+                      for _ in range(2)]
+                ev = [torch.cuda.Event() for _ in range(2)]
+                lanes.append((s_, c_, Zl, Hl, cs_, ev))
 
             def e2e_step(i):
-                s_, c_, Zl, Hl, cs_ = lanes[i % len(lanes)]
+                s_, c_, Zl, Hl, cs_, ev = lanes[i % len(lanes)]
+                b = (i // len(lanes)) % 2
                 with torch.cuda.stream(s_):
                     sd = src_h.to(dev, non_blocking=True)
                     dd = dst_h.to(dev, non_blocking=True)
-                    g = rg.raftgp_build_csr(c_, gr.n, sd, dd)
-                    s_.wait_stream(cs_)                # Zl is free again once its previous D2H is done
-                    rg.raftgp_embed_multi(g, variants, dims, args.seed, Z=Zl)
-                    g.close()
+                    if args.e2e_api == "build_embed":
+                        s_.wait_event(ev[b])           # Zl[b] is free once its previous D2H is done
+                        rg.raftgp_build_embed(c_, gr.n, sd, dd, variants, dims, args.seed, Z=Zl[b])
+                    else:
+                        g = rg.raftgp_build_csr(c_, gr.n, sd, dd)
+                        s_.wait_event(ev[b])
+                        rg.raftgp_embed_multi(g, variants, dims, args.seed, Z=Zl[b])
+                        g.close()
                 cs_.wait_stream(s_)
                 with torch.cuda.stream(cs_):
                     for v in variants:
-                        Hl[v].copy_(Zl[v], non_blocking=True)
+                        Hl[b][v].copy_(Zl[b][v], non_blocking=True)
+                    ev[b].record(cs_)
 
             for i in range(len(lanes)):
                 e2e_step(i)
@@ -656,16 +670,17 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(lanes[0][0])
-            for s_, _, _, _, _ in lanes[1:]:
+            for s_, *_ in lanes[1:]:
                 s_.wait_event(e0)
             for i in range(args.steps):
                 e2e_step(i)
-            for s_, _, _, _, cs_ in lanes:
+            for s_, _, _, _, cs_, _ in lanes:
                 lanes[0][0].wait_stream(s_)
                 lanes[0][0].wait_stream(cs_)
             e1.record(lanes[0][0])
             torch.cuda.synchronize()
-            mode = "pipelined: 3 contexts/streams (+ a D2H stream each); step k's copies overlap other steps' kernels"
+            mode = (f"pipelined: {args.e2e_lanes} contexts/streams (+ a D2H stream each), {args.e2e_api} per step; "
+                    "step k's copies overlap other steps' kernels")
         else:
             out_host = {v: torch.empty((rows, dims[-1]), dtype=torch.float32).pin_memory() for v in variants}
             step(src_h, dst_h, out_host)

@@ -70,6 +70,83 @@ static size_t round_block(size_t bytes) {
 
 // Stream-ordered workspace: every user of a block runs on ctx->stream, so a block released by dfree may
 // be handed out again immediately — the next user is ordered after the previous one on the stream.
+namespace {
+__global__ void zero_bytes(uint4 *p16, size_t n16, unsigned char *tail, size_t ntail) {
+    const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (size_t i = t; i < n16; i += (size_t)gridDim.x * blockDim.x) p16[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (t < ntail) tail[t] = 0;
+}
+}  // namespace
+
+raftgp_status dzero(raftgp_ctx ctx, void *p, size_t bytes, cudaStream_t st) {
+    if (!p || bytes == 0) return RAFTGP_OK;
+    if (!st) st = ctx->stream;
+    unsigned char *b = static_cast<unsigned char *>(p);
+    const size_t head = (16 - (reinterpret_cast<uintptr_t>(b) & 15)) & 15;   // bytes before 16-B alignment
+    const size_t pre = std::min(head, bytes);
+    const size_t n16 = (bytes - pre) / 16;
+    const size_t ntail = bytes - pre - n16 * 16;
+    if (pre) zero_bytes<<<1, 32, 0, st>>>(nullptr, 0, b, pre);
+    if (n16 || ntail) {
+        const size_t blocks = std::min<size_t>(std::max<size_t>(1, (n16 + 255) / 256), (size_t)ctx->sm_count * 8);
+        zero_bytes<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<uint4 *>(b + pre), n16, b + pre + n16 * 16, ntail);
+    }
+    RG_CUDA(cudaGetLastError());
+    return RAFTGP_OK;
+}
+
+namespace {
+__global__ void copy_16(const uint4 *s, uint4 *d, size_t n16) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
+        d[i] = s[i];
+}
+__global__ void copy_u8(const unsigned char *s, unsigned char *d, size_t n) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        d[i] = s[i];
+}
+constexpr size_t kMbox = 64 << 10;
+}  // namespace
+
+raftgp_status dcopy(raftgp_ctx ctx, void *dst, const void *src, size_t bytes, cudaStream_t st) {
+    if (bytes == 0) return RAFTGP_OK;
+    if (!st) st = ctx->stream;
+    const unsigned char *s = static_cast<const unsigned char *>(src);
+    unsigned char *d = static_cast<unsigned char *>(dst);
+    const bool al = ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d)) & 15) == 0;
+    const size_t n16 = al ? bytes / 16 : 0;
+    const size_t rest = bytes - n16 * 16;
+    const size_t cap = (size_t)ctx->sm_count * 8;
+    if (n16)
+        copy_16<<<(unsigned)std::min<size_t>((n16 + 255) / 256, cap), 256, 0, st>>>(
+            reinterpret_cast<const uint4 *>(s), reinterpret_cast<uint4 *>(d), n16);
+    if (rest)
+        copy_u8<<<(unsigned)std::min<size_t>((rest + 255) / 256, cap), 256, 0, st>>>(s + n16 * 16, d + n16 * 16, rest);
+    RG_CUDA(cudaGetLastError());
+    return RAFTGP_OK;
+}
+
+raftgp_status dread(raftgp_ctx ctx, void *host, const void *dev, size_t bytes, cudaStream_t st) {
+    if (bytes == 0) return RAFTGP_OK;
+    if (!st) st = ctx->stream;
+    if (!ctx->mbox_h && bytes <= kMbox) {
+        if (cudaHostAlloc(&ctx->mbox_h, kMbox, cudaHostAllocMapped) != cudaSuccess ||
+            cudaHostGetDevicePointer(&ctx->mbox_d, ctx->mbox_h, 0) != cudaSuccess) {
+            cudaGetLastError();
+            if (ctx->mbox_h) cudaFreeHost(ctx->mbox_h);
+            ctx->mbox_h = ctx->mbox_d = nullptr;
+        }
+    }
+    if (ctx->mbox_d && bytes <= kMbox) {
+        RG_TRY(dcopy(ctx, ctx->mbox_d, dev, bytes, st));
+        RG_CUDA(cudaStreamSynchronize(st));
+        std::memcpy(host, ctx->mbox_h, bytes);
+        return RAFTGP_OK;
+    }
+    RG_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, st));
+    RG_CUDA(cudaStreamSynchronize(st));
+    return RAFTGP_OK;
+}
+
 raftgp_status dalloc(raftgp_ctx ctx, void **p, size_t bytes) {
     const size_t want = round_block(bytes ? bytes : 16);
     auto it = ctx->free_blocks.lower_bound(want);
@@ -158,6 +235,7 @@ static void ctx_teardown(raftgp_ctx ctx) {
         cudaStreamDestroy(ctx->side);
     }
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->mbox_h) cudaFreeHost(ctx->mbox_h);
     delete ctx;
 }
 

@@ -741,7 +741,7 @@ raftgp_status scan_i32_to_i64(raftgp_ctx ctx, const int32_t *in, int64_t *out, i
     const int64_t per_tile = (int64_t)kScanBlock * kScanItems;
     const int64_t ntiles = n > 0 ? ceil_div(n, per_tile) : 0;
     if (ntiles == 0) {
-        RG_CUDA(cudaMemsetAsync(out, 0, sizeof(int64_t), ctx->stream));
+        RG_TRY(dzero(ctx, out, sizeof(int64_t), ctx->stream));
         return RAFTGP_OK;
     }
     int64_t *tiles = nullptr;
@@ -769,7 +769,7 @@ raftgp_status degrees_finalize(raftgp_graph g) {
     raftgp_ctx ctx = g->ctx;
     unsigned long long *d_buf = nullptr;   // [0] = 2e, [1..] = degree histogram
     RG_TRY(dalloc_t(ctx, &d_buf, 1 + kDegHistBins));
-    RG_CUDA(cudaMemsetAsync(d_buf, 0, sizeof(unsigned long long) * (1 + kDegHistBins), ctx->stream));
+    RG_TRY(dzero(ctx, d_buf, sizeof(unsigned long long) * (1 + kDegHistBins), ctx->stream));
     if (g->n > 0) {
         const int grid = static_cast<int>(std::min<int64_t>(ceil_div(g->n, 256), (int64_t)ctx->sm_count * 4));
         LaunchScope L(ctx, K_DEGREES);
@@ -777,8 +777,7 @@ raftgp_status degrees_finalize(raftgp_graph g) {
     }
     RG_CHECK_LAUNCH(ctx);
     std::vector<unsigned long long> h(1 + kDegHistBins, 0);
-    RG_CUDA(cudaMemcpyAsync(h.data(), d_buf, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, ctx->stream));
-    RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    RG_TRY(dread(ctx, h.data(), d_buf, sizeof(unsigned long long) * h.size()));
     dfree(ctx, d_buf);
     g->two_e = static_cast<int64_t>(h[0]);
     g->deg_hist.assign(h.begin() + 1, h.end());
@@ -807,13 +806,13 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
     RG_TRY(dalloc_t(ctx, &g->deg_all, n));
     RG_TRY(dalloc_t(ctx, &g->s_all, n));
     RG_TRY(dalloc_t(ctx, &g->sh_all, n));
-    RG_CUDA(cudaMemsetAsync(big_count, 0, sizeof(int32_t) * 2, st));
+    RG_TRY(dzero(ctx, big_count, sizeof(int32_t) * 2, st));
     const int egrid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 256), (int64_t)ctx->sm_count * 16)));
     int shift = 0;
     while (shift < 31 && ceil_div(nl, (int64_t)1 << shift) > kMaxBuckets) ++shift;
     const bool bucketed = nl > 0 && ((int64_t)1 << shift) <= kMaxBucketRows;
     if (!bucketed) {   // per-row counts (the bucketed path lets every bucket count its own rows)
-        RG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nl ? nl : 1), st));
+        RG_TRY(dzero(ctx, cnt, sizeof(int32_t) * (nl ? nl : 1), st));
         if (m > 0) {
             LaunchScope L(ctx, K_CSR_COUNT);
             csr_count<<<egrid, 256, 0, st>>>(src, dst, m, n, rb, re, cnt, err);
@@ -837,13 +836,13 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
         unsigned int *bnext = nullptr;
         RG_TRY(dalloc_t(ctx, &bcur, (size_t)nb));
         RG_TRY(dalloc_t(ctx, &bnext, 1));
-        RG_CUDA(cudaMemsetAsync(bnext, 0, sizeof(unsigned int), st));
+        RG_TRY(dzero(ctx, bnext, sizeof(unsigned int), st));
         RG_TRY(dalloc_t(ctx, &bcnt, (size_t)nb * pgrid));
         RG_TRY(dalloc_t(ctx, &bstart, (size_t)nb * pgrid + 1));
         RG_TRY(dalloc(ctx, &pairs, (size_t)cap * (packed ? 4 : 8)));
         RG_TRY(dalloc_t(ctx, &fb_rows, (size_t)nl));
         RG_TRY(dalloc_t(ctx, &fb_count, 1));
-        RG_CUDA(cudaMemsetAsync(fb_count, 0, sizeof(int32_t), st));
+        RG_TRY(dzero(ctx, fb_count, sizeof(int32_t), st));
         const size_t bsmem = (size_t)(kBucketCap + 3 * kMaxBucketRows + 1) * 4;
         static bool attrs = false;
         if (!attrs) {
@@ -928,9 +927,8 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
     RG_TRY(scan_i32_to_i64(ctx, g->deg_local, g->row_ptr, nl));
     int64_t nnz = 0;
     int herr = 0;
-    RG_CUDA(cudaMemcpyAsync(&nnz, g->row_ptr + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    RG_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
-    RG_CUDA(cudaStreamSynchronize(st));
+    RG_TRY(dread(ctx, &nnz, g->row_ptr + nl, sizeof(int64_t), st));
+    RG_TRY(dread(ctx, &herr, err, sizeof(int), st));
     if (herr) {
         dfree(ctx, cnt); dfree(ctx, raw_ptr); dfree(ctx, col_raw); dfree(ctx, big_rows); dfree(ctx, big_count);
         return fail(RAFTGP_ERR_DATA, "build_csr: node id outside [0, n)");
@@ -950,7 +948,7 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
     dfree(ctx, big_count);
     RG_TRY(compute_order(g));
     if (rb == 0 && re == n) {
-        if (n > 0) RG_CUDA(cudaMemcpyAsync(g->deg_all, g->deg_local, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
+        if (n > 0) RG_TRY(dcopy(ctx, g->deg_all, g->deg_local, sizeof(int32_t) * n, st));
         RG_TRY(degrees_finalize(g));
     }
     return RAFTGP_OK;

@@ -61,6 +61,8 @@ struct raftgp_ctx_s {
     // stream destroyed after its context (e.g. by a garbage collector) still finds the context alive
     std::atomic<int> refs{1};
     int device = 0;
+    void *mbox_h = nullptr;        // mapped pinned host mailbox for scalar readbacks (dread), and its device alias
+    void *mbox_d = nullptr;
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;   // library-owned side stream (overlapped work inside one call)
     bool own_stream = false;
@@ -150,6 +152,16 @@ struct LaunchScope {
 
 // ---------------------------------------------------------------- memory (stream-ordered pool)
 raftgp_status dalloc(raftgp_ctx ctx, void **p, size_t bytes);
+// Zero `bytes` of device memory with a kernel on `st` (default: the context stream). cudaMemsetAsync is not
+// used on the hot paths: it can queue behind host<->device copies in flight on other streams, which
+// serialised the pipelined end-to-end steps.
+raftgp_status dzero(raftgp_ctx ctx, void *p, size_t bytes, cudaStream_t st = nullptr);
+// Device-to-device copy with a kernel (same reason as dzero).
+raftgp_status dcopy(raftgp_ctx ctx, void *dst, const void *src, size_t bytes, cudaStream_t st = nullptr);
+// Synchronous device-to-host read of a few bytes: a kernel stores them into a mapped pinned mailbox, then the
+// stream is synchronised. Keeps the library's readbacks off the copy engines, where they would wait behind
+// large transfers of other streams. Falls back to cudaMemcpyAsync above the mailbox size.
+raftgp_status dread(raftgp_ctx ctx, void *host, const void *dev, size_t bytes, cudaStream_t st = nullptr);
 void dfree(raftgp_ctx ctx, void *p);
 void release_cache(raftgp_ctx ctx);
 

@@ -129,14 +129,14 @@ raftgp_status compute_order(raftgp_graph g) {
         label_prop<<<wgrid, 256, 0, st>>>(g->row_ptr, g->col, nl, g->row_begin, label);
     }
     RG_CHECK_LAUNCH(ctx);
-    RG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * n, st));
+    RG_TRY(dzero(ctx, cnt, sizeof(int32_t) * n, st));
     {
         LaunchScope L(ctx, K_ORDER);
         label_hist<<<grid, 256, 0, st>>>(label, nl, g->row_begin, n, cnt);
     }
     RG_CHECK_LAUNCH(ctx);
     RG_TRY(scan_i32_to_i64(ctx, cnt, start, n));
-    RG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * n, st));
+    RG_TRY(dzero(ctx, cnt, sizeof(int32_t) * n, st));
     {
         LaunchScope L(ctx, K_ORDER);
         label_scatter<<<grid, 256, 0, st>>>(label, nl, n, start, cnt, g->order);

@@ -528,7 +528,7 @@ raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c,
     cudaStream_t st = ctx->stream;
     int32_t *err = nullptr;
     RG_TRY(dalloc_t(ctx, &err, 1));
-    RG_CUDA(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
+    RG_TRY(dzero(ctx, err, sizeof(int32_t), st));
     {
         LaunchScope LS(ctx, K_SBM);
         sbm_validate<<<grid1(std::max<int64_t>(n, (int64_t)K * K), 256), 256, 0, st>>>(c, theta, n, omega, K, err);
@@ -653,7 +653,7 @@ raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c,
         s2 = dalloc_t(ctx, &cnt, (size_t)nchunks);
         if (s2 == RAFTGP_OK) s2 = dalloc_t(ctx, &off, (size_t)nchunks + 1);
         if (s2 == RAFTGP_OK) s2 = dalloc_t(ctx, &next, 4);
-        if (s2 == RAFTGP_OK) RG_CUDA(cudaMemsetAsync(next, 0, 4 * sizeof(unsigned long long), st));
+        if (s2 == RAFTGP_OK) RG_TRY(dzero(ctx, next, 4 * sizeof(unsigned long long), st));
         // recorded event cells (nslot per chunk; RAFTGP_SBM_SLOTS overrides, 0 = none) and the log of the
         // events past them; without room for the cells both passes walk, without room for the log the write
         // pass re-walks the chunks with more than nslot events

@@ -788,8 +788,8 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
     float2 *bnd = reinterpret_cast<float2 *>(dpos);   // seeding distances, then the Lloyd pruning bounds
     RG_TRY(dalloc_t(ctx, &err, 1));
     RG_TRY(dalloc_t(ctx, &active, 2 + 64));   // [0] active segments, [1] their rows, [2..65] rows read
-    RG_CUDA(cudaMemsetAsync(active, 0, sizeof(unsigned long long) * 66, st));
-    RG_CUDA(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
+    RG_TRY(dzero(ctx, active, sizeof(unsigned long long) * 66, st));
+    RG_TRY(dzero(ctx, err, sizeof(int32_t), st));
     {
         LaunchScope LS(ctx, K_SELECT);
         sel_init<<<grid_for(n, 256), 256, 0, st>>>(perm, pseg, node_key, n);
@@ -820,8 +820,8 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
     unsigned long long *lvl_acc = nullptr, *lvl_cnt = nullptr;
     RG_TRY(dalloc_t(ctx, &lvl_acc, (size_t)2 * L));
     RG_TRY(dalloc_t(ctx, &lvl_cnt, (size_t)2));
-    RG_CUDA(cudaMemsetAsync(lvl_acc, 0, sizeof(unsigned long long) * 2 * L, st));
-    RG_CUDA(cudaMemsetAsync(lvl_cnt, 0, sizeof(unsigned long long) * 2, st));
+    RG_TRY(dzero(ctx, lvl_acc, sizeof(unsigned long long) * 2 * L, st));
+    RG_TRY(dzero(ctx, lvl_cnt, sizeof(unsigned long long) * 2, st));
 
     while (S > 0 && rc == RAFTGP_OK) {
         ++levels;
@@ -846,7 +846,7 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
         RG_TRY(dalloc_t(ctx, &krank, (size_t)S + 1));
         RG_TRY(dalloc_t(ctx, &base, (size_t)S + 1));
         RG_TRY(dalloc_t(ctx, &new_off, (size_t)2 * S + 1));
-        RG_CUDA(cudaMemsetAsync(nsz, 0, sizeof(unsigned long long) * (size_t)S * 5, st));
+        RG_TRY(dzero(ctx, nsz, sizeof(unsigned long long) * (size_t)S * 5, st));
 
         const unsigned rgrid = grid_for(ceil_div(n_act, kRowRange), kRowWarps);
         // pruned passes: one balanced wave of resident CTAs, each warp a contiguous range (multiple of 128)
@@ -898,7 +898,7 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
         // of kIterChunk without host round trips: update t counts the still-active segments (and their rows)
         // into iter_act[t], and the kernels of iteration t + 1 exit at once when that count is 0. The host
         // reads the counters once per chunk.
-        RG_CUDA(cudaMemsetAsync(iter_act, 0, sizeof(unsigned long long) * 2 * ((size_t)max_iter + 1), st));
+        RG_TRY(dzero(ctx, iter_act, sizeof(unsigned long long) * 2 * ((size_t)max_iter + 1), st));
         for (int t0 = 1; t0 <= max_iter && rc == RAFTGP_OK; t0 += kIterChunk) {
             const int t1 = std::min(max_iter, t0 + kIterChunk - 1);
             for (int t = t0; t <= t1; ++t) {
@@ -967,8 +967,8 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
         unsigned long long *nacc = nullptr, *ncnt = nullptr;
         RG_TRY(dalloc_t(ctx, &nacc, (size_t)S * 4 * L));
         RG_TRY(dalloc_t(ctx, &ncnt, (size_t)S * 4));
-        RG_CUDA(cudaMemsetAsync(nacc, 0, sizeof(unsigned long long) * (size_t)S * 4 * L, st));
-        RG_CUDA(cudaMemsetAsync(ncnt, 0, sizeof(unsigned long long) * (size_t)S * 4, st));
+        RG_TRY(dzero(ctx, nacc, sizeof(unsigned long long) * (size_t)S * 4 * L, st));
+        RG_TRY(dzero(ctx, ncnt, sizeof(unsigned long long) * (size_t)S * 4, st));
         {
             LaunchScope LS(ctx, K_SEL_SPLIT);
             sel_inherit<L><<<sgrid, 256, 0, st>>>(keep, krank, ss, S, nacc, ncnt);

@@ -224,7 +224,7 @@ raftgp_status g_reduce(raftgp_graph g, const float *theta, int32_t r, double *g_
     if (g_out == nullptr) return RAFTGP_OK;
     const int64_t nchunks = ceil_div(g->n, kGChunk);
     if (nchunks == 0) {
-        RG_CUDA(cudaMemsetAsync(g_out, 0, sizeof(double) * r, ctx->stream));
+        RG_TRY(dzero(ctx, g_out, sizeof(double) * r, ctx->stream));
         return RAFTGP_OK;
     }
     double *partial = nullptr;

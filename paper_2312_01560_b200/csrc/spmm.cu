@@ -442,7 +442,7 @@ raftgp_status launch_fast(raftgp_ctx ctx, const HopArgs &a) {
     }();
     if (dyn && KIND != KIND_LOAD) {
         RG_TRY(dalloc_t(ctx, &b.ctr, 1));
-        RG_CUDA(cudaMemsetAsync(b.ctr, 0, sizeof(unsigned long long), ctx->stream));
+        RG_TRY(dzero(ctx, b.ctr, sizeof(unsigned long long), ctx->stream));
     }
     {
         LaunchScope L(ctx, kid);

@@ -671,7 +671,7 @@ raftgp_status launch_wide(raftgp_ctx ctx, const WideArgs &a) {
     }();
     if (dyn) {
         RG_TRY(dalloc_t(ctx, &b.ctr, 1));
-        RG_CUDA(cudaMemsetAsync(b.ctr, 0, sizeof(unsigned long long), ctx->stream));
+        RG_TRY(dzero(ctx, b.ctr, sizeof(unsigned long long), ctx->stream));
     }
     {
         LaunchScope LS(ctx, K_WIDE_HOP);
@@ -930,10 +930,8 @@ raftgp_status embed_wide(raftgp_graph g, int32_t nvariants, const int32_t *varia
                 } else if (st == RAFTGP_OK) {
                     if (!last && Mp > n) {   // padding rows of the last row tile are zero
                         const size_t tile = (size_t)(w / kKB) * chunk_bytes(kGM);
-                        RG_CUDA(cudaMemsetAsync(reinterpret_cast<char *>(zhi) + (size_t)(Mp / kGM - 1) * tile, 0, tile,
-                                                ctx->stream));
-                        RG_CUDA(cudaMemsetAsync(reinterpret_cast<char *>(zlo) + (size_t)(Mp / kGM - 1) * tile, 0, tile,
-                                                ctx->stream));
+                        RG_TRY(dzero(ctx, reinterpret_cast<char *>(zhi) + (size_t)(Mp / kGM - 1) * tile, tile));
+                        RG_TRY(dzero(ctx, reinterpret_cast<char *>(zlo) + (size_t)(Mp / kGM - 1) * tile, tile));
                     }
                     WideArgs a{};
                     a.n = n; a.row_ptr = g->row_ptr; a.col = g->col; a.X = T; a.s_all = g->s_all; a.sh_all = g->sh_all;
