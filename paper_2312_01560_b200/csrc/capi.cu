@@ -414,7 +414,7 @@ raftgp_status raftgp_graph_local_degrees(raftgp_graph g, int32_t *deg_dev) {
     if (!g || (!deg_dev && g->nl)) return fail(RAFTGP_ERR_PARAM, "null argument");
     RG_TRY(set_device(g->ctx));
     if (g->nl)
-        RG_CUDA(cudaMemcpyAsync(deg_dev, g->deg_local, sizeof(int32_t) * g->nl, cudaMemcpyDeviceToDevice, g->ctx->stream));
+        RG_TRY(dcopy(g->ctx, deg_dev, g->deg_local, sizeof(int32_t) * g->nl));
     return RAFTGP_OK;
 }
 
@@ -423,7 +423,7 @@ raftgp_status raftgp_graph_set_degrees(raftgp_graph g, const int32_t *deg_all_de
     if (!g || (!deg_all_dev && g->n)) return fail(RAFTGP_ERR_PARAM, "null argument");
     RG_TRY(set_device(g->ctx));
     if (g->n)
-        RG_CUDA(cudaMemcpyAsync(g->deg_all, deg_all_dev, sizeof(int32_t) * g->n, cudaMemcpyDeviceToDevice, g->ctx->stream));
+        RG_TRY(dcopy(g->ctx, g->deg_all, deg_all_dev, sizeof(int32_t) * g->n));
     return degrees_finalize(g);
     RG_GUARD_END
 }
@@ -438,7 +438,7 @@ raftgp_status raftgp_graph_set_order(raftgp_graph g, const int32_t *order_dev) {
     }
     if (g->order == nullptr && g->nl > 0) RG_TRY(dalloc_t(g->ctx, &g->order, (size_t)g->nl));
     if (g->nl > 0)
-        RG_CUDA(cudaMemcpyAsync(g->order, order_dev, sizeof(int32_t) * g->nl, cudaMemcpyDeviceToDevice, g->ctx->stream));
+        RG_TRY(dcopy(g->ctx, g->order, order_dev, sizeof(int32_t) * g->nl));
     return RAFTGP_OK;
 }
 
@@ -1003,9 +1003,7 @@ raftgp_status raftgp_stream_add_edges(raftgp_stream s, int64_t m, const int32_t 
 raftgp_status raftgp_stream_embedding(raftgp_stream s, float *Z_dev) {
     if (!s || (!Z_dev && s->g->n > 0)) return fail(RAFTGP_ERR_PARAM, "null argument");
     RG_TRY(set_device(s->ctx));
-    if (s->g->n > 0)
-        RG_CUDA(cudaMemcpyAsync(Z_dev, s->Z, sizeof(float) * (size_t)s->g->n * s->dims[s->layers],
-                                cudaMemcpyDeviceToDevice, s->ctx->stream));
+    if (s->g->n > 0) RG_TRY(dcopy(s->ctx, Z_dev, s->Z, sizeof(float) * (size_t)s->g->n * s->dims[s->layers]));
     return RAFTGP_OK;
 }
 

@@ -535,8 +535,7 @@ raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c,
     }
     RG_CHECK_LAUNCH(ctx);
     int32_t herr = 0;
-    RG_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    RG_CUDA(cudaStreamSynchronize(st));
+    RG_TRY(dread(ctx, &herr, err, sizeof(int32_t), st));
     dfree(ctx, err);
     if (herr) return fail(RAFTGP_ERR_PARAM, "raftgp_sbm_sample: label outside [0,K), theta <= 0, or Omega negative / "
                                             "not symmetric");
@@ -643,8 +642,7 @@ raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c,
     }
     int64_t nchunks = 0;
     if (s2 == RAFTGP_OK) {
-        RG_CUDA(cudaMemcpyAsync(&nchunks, choff + A.npairs, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        RG_CUDA(cudaStreamSynchronize(st));
+        s2 = dread(ctx, &nchunks, choff + A.npairs, sizeof(int64_t), st);
     }
     A.choff = choff;
     A.nchunks = nchunks;
@@ -692,10 +690,9 @@ raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c,
         if (s2 == RAFTGP_OK) s2 = scan_i32_to_i64(ctx, cnt, off, nchunks);
         int64_t novf = 0, nlogged = 0;
         if (s2 == RAFTGP_OK) {
-            RG_CUDA(cudaMemcpyAsync(&total, off + nchunks, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-            RG_CUDA(cudaMemcpyAsync(&novf, next + 2, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-            RG_CUDA(cudaMemcpyAsync(&nlogged, next + 3, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-            RG_CUDA(cudaStreamSynchronize(st));
+            s2 = dread(ctx, &total, off + nchunks, sizeof(int64_t), st);
+            if (s2 == RAFTGP_OK) s2 = dread(ctx, &novf, next + 2, sizeof(int64_t), st);
+            if (s2 == RAFTGP_OK) s2 = dread(ctx, &nlogged, next + 3, sizeof(int64_t), st);
         }
         if (s2 == RAFTGP_OK && total <= cap && total > 0) {
             LaunchScope LS(ctx, K_SBM_WALK);

@@ -332,14 +332,15 @@ __global__ void __launch_bounds__(kRowWarps * 32) sel_rows(const float *__restri
     if (MODE == 1 && lane == 0) atomicAdd(&rows_read[blockIdx.x & 63], (unsigned long long)(end - beg));
 }
 
-// Lloyd iteration t > 1 with exact pruning. Each warp scans `range` consecutive positions (a multiple of 128,
-// sized by the host so that the grid is one balanced wave of resident CTAs): the bound test
+// Lloyd iteration t > 1 with exact pruning. Warps claim kLloydChunk consecutive positions at a time from a
+// per-iteration counter (one resident wave of CTAs; the rows failing the bound test cluster, so a static split
+// left warps idle behind the busiest range): the bound test
 // runs on every position (segment, side and bounds only: 24 B per row); positions that fail it are queued in
 // shared memory and recomputed 32 at a time with all lanes busy (a lane per row, rows bulk-copied into a
 // shared-memory stage). Rows that switch side then move their fixed-point values between the two sums
 // (exact integers), run-aggregated per segment.
 constexpr int kPruneWarps = 8;
-constexpr int kPruneMinRange = 512;
+constexpr int kLloydChunk = 1024;   // positions per dynamic claim (a multiple of 128)
 
 template <int L>
 __global__ void __launch_bounds__(kPruneWarps * 32, 3) sel_lloyd_pruned(const float *__restrict__ Z,
@@ -349,7 +350,7 @@ __global__ void __launch_bounds__(kPruneWarps * 32, 3) sel_lloyd_pruned(const fl
                                                                       float2 *__restrict__ bnd, int64_t n_act,
                                                                       SegState st, unsigned long long *rows_read,
                                                                       const unsigned long long *__restrict__ prev_active,
-                                                                      int64_t range) {
+                                                                      unsigned long long *__restrict__ claim) {
     constexpr int LD = L + 4;
     constexpr uint32_t RB = 4u * L;
     extern __shared__ __align__(16) float sel_smem[];
@@ -359,9 +360,7 @@ __global__ void __launch_bounds__(kPruneWarps * 32, 3) sel_lloyd_pruned(const fl
     float *stage = sel_smem + (size_t)warp * 32 * LD;
     uint64_t *bar = &bars[warp];
     int *q = qbuf[warp];
-    const int64_t beg = ((int64_t)blockIdx.x * kPruneWarps + warp) * range;
-    if (beg >= n_act || prev_active[0] == 0) return;   // out of range, or every segment already converged
-    const int64_t end = min(beg + range, n_act);
+    if (prev_active[0] == 0) return;   // every segment already converged
     const unsigned lt = (1u << lane) - 1u;
     if (lane == 0) {
         mbar_init1(bar);
@@ -382,7 +381,7 @@ __global__ void __launch_bounds__(kPruneWarps * 32, 3) sel_lloyd_pruned(const fl
         if (lane == 0) mbar_expect(bar, (uint32_t)k * RB);
         __syncwarp();
         if (lane < k) {
-            pos = beg + q[lane];
+            pos = q[lane];
             s = pseg[pos];
             bulk_row(stage + lane * LD, Z + (size_t)perm[pos] * L, RB, bar);
         }
@@ -407,6 +406,13 @@ __global__ void __launch_bounds__(kPruneWarps * 32, 3) sel_lloyd_pruned(const fl
         stage_release();
     };
 
+    for (;;) {
+        // the warp's next kLloydChunk positions (dynamic: the rows that fail the bound test are not uniform)
+        unsigned long long c0 = 0;
+        if (lane == 0) c0 = atomicAdd(claim, (unsigned long long)kLloydChunk);
+        const int64_t beg = (int64_t)__shfl_sync(0xffffffffu, c0, 0);
+        if (beg >= n_act) break;
+        const int64_t end = min(beg + (int64_t)kLloydChunk, n_act);
     for (int64_t b = beg; b < end; b += 128) {
         // bound test of 128 positions: lane owns b + 32 j + lane, all loads issued up front
         int sj[4], cj[4];
@@ -432,7 +438,7 @@ __global__ void __launch_bounds__(kPruneWarps * 32, 3) sel_lloyd_pruned(const fl
                 else need = true;
             }
             const unsigned m = __ballot_sync(0xffffffffu, need);
-            if (need) q[qn + __popc(m & lt)] = (int)(pos - beg);
+            if (need) q[qn + __popc(m & lt)] = (int)pos;
             qn += __popc(m);
         }
         __syncwarp();
@@ -449,6 +455,7 @@ __global__ void __launch_bounds__(kPruneWarps * 32, 3) sel_lloyd_pruned(const fl
             qn = rest;
             __syncwarp();
         }
+    }
     }
     if (qn > 0) round(qn);
     acc.flush(st, lane);
@@ -805,7 +812,11 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
     std::vector<int32_t> off0 = {0, (int32_t)n};
     int32_t *seg_off = nullptr;
     RG_TRY(dalloc_t(ctx, &seg_off, 2));
-    RG_CUDA(cudaMemcpyAsync(seg_off, off0.data(), 2 * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    {
+        LaunchScope LS(ctx, K_SELECT);
+        fill_i32<<<1, 32, 0, st>>>(seg_off, 1, 0);
+        fill_i32<<<1, 32, 0, st>>>(seg_off + 1, 1, (int32_t)n);
+    }
 
     int32_t blocks = 0;
     int64_t splits = 0, lloyd_iters = 0, levels = 0, lloyd_rows = 0, seed_rows = 0, act_rows = 0;
@@ -813,6 +824,8 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
     std::vector<unsigned long long> h_iter(2 * ((size_t)max_iter + 1), 0);
     unsigned long long *iter_act = nullptr;   // [t][2]: active segments / rows after update t
     RG_TRY(dalloc_t(ctx, &iter_act, 2 * ((size_t)max_iter + 1)));
+    unsigned long long *claims = nullptr;     // [t]: position counter of Lloyd iteration t (zeroed per level)
+    RG_TRY(dalloc_t(ctx, &claims, (size_t)max_iter + 1));
     int64_t h_two[2] = {0, 0};
     raftgp_status rc = RAFTGP_OK;
     // per-level [S][2][L] side sums and [S][2] counts; level 1 fills slot 0 with a mean pass, deeper levels
@@ -849,10 +862,9 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
         RG_TRY(dzero(ctx, nsz, sizeof(unsigned long long) * (size_t)S * 5, st));
 
         const unsigned rgrid = grid_for(ceil_div(n_act, kRowRange), kRowWarps);
-        // pruned passes: one balanced wave of resident CTAs, each warp a contiguous range (multiple of 128)
-        const int64_t q_warps = (int64_t)ctx->sm_count * prune_ctas * kPruneWarps;
-        const int64_t q_range = std::max<int64_t>(kPruneMinRange, ceil_div(ceil_div(n_act, q_warps), 128) * 128);
-        const unsigned qgrid = grid_for(ceil_div(n_act, q_range), kPruneWarps);
+        // pruned passes: one wave of resident CTAs claiming kLloydChunk positions per warp at a time
+        const unsigned qgrid = (unsigned)std::max<int64_t>(
+            1, std::min<int64_t>((int64_t)ctx->sm_count * prune_ctas, ceil_div(ceil_div(n_act, kLloydChunk), kPruneWarps)));
         act_rows = n_act;
         seed_rows += n_act;
         const unsigned sgrid = grid_for((int64_t)S * 32, 256);
@@ -869,8 +881,7 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
         }
         RG_CHECK_LAUNCH(ctx);
         if (levels == 1) {
-            RG_CUDA(cudaMemcpyAsync(h_small, err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-            RG_CUDA(cudaStreamSynchronize(st));
+            RG_TRY(dread(ctx, h_small, err, sizeof(int32_t), st));
             if (h_small[0]) {
                 rc = fail(RAFTGP_ERR_DATA, "raftgp_model_select: Z has an entry with |z| > 1 or NaN (SELECT_SPEC §1)");
             }
@@ -899,6 +910,7 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
         // into iter_act[t], and the kernels of iteration t + 1 exit at once when that count is 0. The host
         // reads the counters once per chunk.
         RG_TRY(dzero(ctx, iter_act, sizeof(unsigned long long) * 2 * ((size_t)max_iter + 1), st));
+        RG_TRY(dzero(ctx, claims, sizeof(unsigned long long) * ((size_t)max_iter + 1), st));
         for (int t0 = 1; t0 <= max_iter && rc == RAFTGP_OK; t0 += kIterChunk) {
             const int t1 = std::min(max_iter, t0 + kIterChunk - 1);
             for (int t = t0; t <= t1; ++t) {
@@ -911,7 +923,7 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
                     else
                         sel_lloyd_pruned<L><<<qgrid, kPruneWarps * 32, kPruneSmem, st>>>(Z, perm, pseg, side, bnd,
                                                                                        n_act, ss, active + 2, prev,
-                                                                                       q_range);
+                                                                                       claims + t);
                 }
                 RG_CHECK_LAUNCH(ctx);
                 {
@@ -920,9 +932,8 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
                 }
                 RG_CHECK_LAUNCH(ctx);
             }
-            RG_CUDA(cudaMemcpyAsync(h_iter.data() + 2 * t0, iter_act + 2 * t0,
-                                    sizeof(unsigned long long) * 2 * (size_t)(t1 - t0 + 1), cudaMemcpyDeviceToHost, st));
-            RG_CUDA(cudaStreamSynchronize(st));
+            RG_TRY(dread(ctx, h_iter.data() + 2 * t0, iter_act + 2 * t0,
+                         sizeof(unsigned long long) * 2 * (size_t)(t1 - t0 + 1), st));
             bool stop = false;
             for (int t = t0; t <= t1 && !stop; ++t) {
                 ++lloyd_iters;
@@ -981,9 +992,8 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
                                                               bmin);
         }
         RG_CHECK_LAUNCH(ctx);
-        RG_CUDA(cudaMemcpyAsync(&h_two[0], krank + S, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        RG_CUDA(cudaMemcpyAsync(&h_two[1], base + S, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        RG_CUDA(cudaStreamSynchronize(st));
+        RG_TRY(dread(ctx, &h_two[0], krank + S, sizeof(int64_t), st));
+        RG_TRY(dread(ctx, &h_two[1], base + S, sizeof(int64_t), st));
         const int64_t kept = h_two[0];
         blocks += (int32_t)(S - kept);
         splits += kept;
@@ -1022,12 +1032,12 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
     dfree(ctx, lvl_acc);
     dfree(ctx, lvl_cnt);
     dfree(ctx, iter_act);
+    dfree(ctx, claims);
     dfree(ctx, perm); dfree(ctx, pseg); dfree(ctx, side); dfree(ctx, nperm); dfree(ctx, npseg);
     dfree(ctx, node_key); dfree(ctx, label_tmp); dfree(ctx, bmin); dfree(ctx, ones); dfree(ctx, dpos); dfree(ctx, err);
     unsigned long long h_read[64] = {0};
     if (rc == RAFTGP_OK) {
-        RG_CUDA(cudaMemcpyAsync(h_read, active + 2, sizeof(h_read), cudaMemcpyDeviceToHost, st));
-        RG_CUDA(cudaStreamSynchronize(st));
+        RG_TRY(dread(ctx, h_read, active + 2, sizeof(h_read), st));
     }
     dfree(ctx, active);
     if (rc != RAFTGP_OK) return rc;

@@ -183,8 +183,7 @@ raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const i
         rc = scan_i32_to_i64(ctx, ng->deg_local, ng->row_ptr, n);
     }
     if (rc == RAFTGP_OK) {
-        RG_CUDA(cudaMemcpyAsync(&ng->nnz_local, ng->row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        RG_CUDA(cudaStreamSynchronize(st));
+        RG_TRY(dread(ctx, &ng->nnz_local, ng->row_ptr + n, sizeof(int64_t), st));
         rc = dalloc_t(ctx, &ng->col, (size_t)std::max<int64_t>(1, ng->nnz_local));
     }
     if (rc == RAFTGP_OK) {
@@ -199,7 +198,7 @@ raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const i
         if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &ng->sh_all, (size_t)n);
     }
     if (rc == RAFTGP_OK) {
-        if (n > 0) RG_CUDA(cudaMemcpyAsync(ng->deg_all, ng->deg_local, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
+        if (n > 0) RG_TRY(dcopy(ctx, ng->deg_all, ng->deg_local, sizeof(int32_t) * n, st));
         rc = degrees_finalize(ng);
     }
     drop(delta);
@@ -225,8 +224,7 @@ raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const i
         }
         rc = scan_i32_to_i64(ctx, flag, pos, n);
         if (rc == RAFTGP_OK) {
-            RG_CUDA(cudaMemcpyAsync(&counts[k], pos + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-            RG_CUDA(cudaStreamSynchronize(st));
+            RG_TRY(dread(ctx, &counts[k], pos + n, sizeof(int64_t), st));
         }
         if (rc != RAFTGP_OK || k == 0) continue;
         // ---- 3. recompute the rows of R_k: the feature hop for k = 1, GCN hop k - 1 for k >= 2
