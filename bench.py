@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--table1-steps", type=int, default=3)
     ap.add_argument("--no-sbm", action="store_true", help="skip the NEXT-3 SBM sampler measurement")
     ap.add_argument("--e2e-lanes", type=int, default=3, help="contexts/streams the e2e steps rotate over (N = 1)")
+    ap.add_argument("--exchange", default="push", choices=["push", "allgather"],
+                    help="N > 1: per-hop exchange fused into the producing kernels (peer stores through CUDA IPC) "
+                         "or NCCL all-gathers pipelined across variants")
     ap.add_argument("--e2e-api", default="separate", choices=["separate", "build_embed"],
                     help="e2e step: raftgp_build_csr + raftgp_embed_multi, or raftgp_build_embed")
     ap.add_argument("--no-stream", action="store_true", help="skip the NEXT-4 streaming-update measurement")
@@ -465,8 +468,16 @@ def main():
     world, rank, local = dist_env()
     if world > 1:
         import torch.distributed as tdist
+        # RAFTGP_BENCH_BACKEND=gloo + RAFTGP_BENCH_ONE_GPU=1: functional check of the N > 1 code path with all
+        # ranks on one GPU (host barriers; not a measurement)
+        backend = os.environ.get("RAFTGP_BENCH_BACKEND", "nccl")
+        if os.environ.get("RAFTGP_BENCH_ONE_GPU") == "1":
+            local = 0
         torch.cuda.set_device(local)
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            tdist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     if rank == 0:
@@ -508,10 +519,13 @@ def main():
         g.close()
         return nnz
 
+    push_bufs = rdist.PushBuffers(ctx) if (world > 1 and args.exchange == "push") else None
+
     def step_multi(src, dst, out_host=None):
         keep = {}
-        gen = rdist.rank_pipeline(rdist.CudaEngine(ctx), gr.n, src, dst, rank, world, variants, dims, args.seed, keep)
-        Z = rdist.run_distributed(gen)
+        pipe = rdist.rank_pipeline_push if push_bufs is not None else rdist.rank_pipeline
+        gen = pipe(rdist.CudaEngine(ctx), gr.n, src, dst, rank, world, variants, dims, args.seed, keep)
+        Z = rdist.run_distributed(gen, push=push_bufs)
         for v in variants:
             Zbuf[v].copy_(Z[v])
             if out_host is not None:
@@ -718,6 +732,7 @@ def main():
                        "n": gr.n, "nnz": nnz, "m_raw_pairs": m, "r": cfg.r, "dims": list(dims), "variants": variants,
                        "rule": args.rule, "fused_variant_pair": fused_pair and world == 1,
                        "parallelism": f"rowpart{world}" if world > 1 else "single",
+                       "exchange": (args.exchange if world > 1 else None),
                        "l2": "inputs larger than L2 (gathered operands >= 1.28 GB vs 126 MB L2); no flush"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks.summary(),
@@ -729,6 +744,8 @@ def main():
             "streaming": stream,
         }
         print(json.dumps(line), flush=True)
+    if push_bufs is not None:
+        push_bufs.close()
     if world > 1:
         tdist.barrier()
         tdist.destroy_process_group()

@@ -295,6 +295,35 @@ RAFTGP_API raftgp_status raftgp_stream_embedding(raftgp_stream s, float *Z_dev);
 RAFTGP_API raftgp_status raftgp_stream_graph(raftgp_stream s, raftgp_graph *g_out);
 RAFTGP_API raftgp_status raftgp_stream_destroy(raftgp_stream s);
 
+/* ---------------------------------------------------------------- a6 fused: exchange inside the producing hop
+ * SURVEY §8(e) / north_star "per-hop all-gather": on P ranks every GCN hop needs the next operand T for ALL n
+ * rows. Instead of computing local rows and then all-gathering them, the producing kernel's epilogue stores
+ * each finished row of T straight into every rank's full n-row copy (peer memory over NVLink, opened with the
+ * IPC calls below), so the transfer overlaps the hop's gathers row by row. After the producing calls of all
+ * ranks, the caller runs one stream-ordered barrier (e.g. a 1-element NCCL all-reduce) before the next hop
+ * reads its copy. Results are bit-identical to raftgp_feature_transform / raftgp_gcn_hop + all-gather.
+ *   raftgp_feature_transform_push: as raftgp_feature_transform; rep = host array [nvariants][nrep] of device
+ *     pointers, rep[v][q] = rank q's n x l1 copy of variant v's T1 (this rank's rows land at rows
+ *     [row_begin, row_end)). nrep in [1, 8].
+ *   raftgp_gcn_hop_push: as raftgp_gcn_hop with W_next (required); T_next goes to rep[0..nrep) (n x w_next each)
+ *     instead of a local buffer. Z_out_dev may be NULL.
+ *   Widths in {32, 64, 128} and 16-B aligned pointers fuse the stores into the hop kernels; other shapes compute
+ *   locally and then copy into the replicas (same result).
+ *   raftgp_ipc_alloc: cudaMalloc'd buffer (library-owned until raftgp_ipc_free) and its 64-byte IPC handle.
+ *   raftgp_ipc_open / raftgp_ipc_close: map / unmap another process's buffer on this context's device (peer
+ *     access enabled lazily). raftgp_copy: device-to-device copy by a kernel on the context stream.
+ * Errors: PARAM (replica count / null pointers / widths), CUDA (IPC failures), NOMEM. */
+RAFTGP_API raftgp_status raftgp_feature_transform_push(raftgp_graph g, int32_t nvariants, const int32_t *variants,
+                                                       int32_t r, int32_t l1, uint64_t seed, float *const *rep,
+                                                       int32_t nrep);
+RAFTGP_API raftgp_status raftgp_gcn_hop_push(raftgp_graph g, const float *T_full_dev, int32_t w, float *Z_out_dev,
+                                             const float *W_next_dev, int32_t w_next, float *const *rep, int32_t nrep);
+RAFTGP_API raftgp_status raftgp_ipc_alloc(raftgp_ctx ctx, size_t bytes, void **dev_ptr, void *handle64);
+RAFTGP_API raftgp_status raftgp_ipc_free(raftgp_ctx ctx, void *dev_ptr);
+RAFTGP_API raftgp_status raftgp_ipc_open(raftgp_ctx ctx, const void *handle64, void **dev_ptr);
+RAFTGP_API raftgp_status raftgp_ipc_close(raftgp_ctx ctx, void *dev_ptr);
+RAFTGP_API raftgp_status raftgp_copy(raftgp_ctx ctx, void *dst_dev, const void *src_dev, size_t bytes);
+
 #ifdef __cplusplus
 }
 #endif

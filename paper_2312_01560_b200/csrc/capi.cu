@@ -676,7 +676,8 @@ raftgp_status raftgp_embed(raftgp_graph g, raftgp_variant variant, int32_t layer
 // T1 of every variant from Theta' = Theta W1 (thw_pre: already computed, e.g. on a side stream; else here)
 static raftgp_status first_transform_pre(raftgp_graph g, int32_t nvariants, const int32_t *variants, int32_t r,
                                          int32_t l1, uint64_t seed, float *const *T1, const int where[3],
-                                         const float *thw_pre = nullptr) {
+                                         const float *thw_pre = nullptr, float *const *rep = nullptr,
+                                         int32_t nrep = 0) {
     raftgp_ctx ctx = g->ctx;
     float *W1 = nullptr, *thw = nullptr;
     double *gw = nullptr;
@@ -691,11 +692,26 @@ static raftgp_status first_transform_pre(raftgp_graph g, int32_t nvariants, cons
     if (st == RAFTGP_OK && where[RAFTGP_MOD] >= 0) st = dalloc_t(ctx, &gw, (size_t)l1);
     if (st == RAFTGP_OK && gw) st = g_reduce(g, tw, l1, gw);
     const bool dual = where[RAFTGP_NCUT] >= 0 && where[RAFTGP_MOD] >= 0;
-    if (st == RAFTGP_OK && dual)
-        st = feature_hop_pre(g, -1, l1, tw, gw, T1[where[RAFTGP_NCUT]], T1[where[RAFTGP_MOD]]);
+    // rep (push mode): variant v's replicas are rep[v * nrep .. v * nrep + nrep)
+    auto spec = [&](int va, int vb) {
+        PushSpec p{};
+        p.nrep = nrep;
+        p.row0 = g->row_begin;
+        for (int q = 0; q < nrep; ++q) {
+            p.rep[q] = rep[(size_t)va * nrep + q];
+            p.rep2[q] = vb >= 0 ? rep[(size_t)vb * nrep + q] : nullptr;
+        }
+        return p;
+    };
+    if (st == RAFTGP_OK && dual) {
+        const int a = where[RAFTGP_NCUT], b = where[RAFTGP_MOD];
+        const PushSpec p = rep ? spec(a, b) : PushSpec{};
+        st = feature_hop_pre(g, -1, l1, tw, gw, T1 ? T1[a] : nullptr, T1 ? T1[b] : p.rep2[0], rep ? &p : nullptr);
+    }
     for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v) {
         if (dual && (variants[v] == RAFTGP_NCUT || variants[v] == RAFTGP_MOD)) continue;
-        st = feature_hop_pre(g, variants[v], l1, tw, gw, T1[v], nullptr);
+        const PushSpec p = rep ? spec(v, -1) : PushSpec{};
+        st = feature_hop_pre(g, variants[v], l1, tw, gw, T1 ? T1[v] : nullptr, nullptr, rep ? &p : nullptr);
     }
     dfree(ctx, thw);
     dfree(ctx, gw);
@@ -1081,6 +1097,131 @@ raftgp_status raftgp_build_embed(raftgp_ctx ctx, int64_t n, int64_t m, const int
     else if (g) raftgp_graph_destroy(g);
     return st;
     RG_GUARD_END
+}
+
+// ---------------------------------------------------------------- fused exchange (a6): push replicas + CUDA IPC
+static raftgp_status check_reps(float *const *rep, int32_t nrep, int32_t nvariants) {
+    if (!rep || nrep < 1 || nrep > kMaxPush) return fail(RAFTGP_ERR_PARAM, "push: need 1..8 replicas");
+    for (int64_t i = 0; i < (int64_t)nrep * nvariants; ++i)
+        if (!rep[i]) return fail(RAFTGP_ERR_PARAM, "push: null replica");
+    return RAFTGP_OK;
+}
+
+raftgp_status raftgp_feature_transform_push(raftgp_graph g, int32_t nvariants, const int32_t *variants, int32_t r,
+                                            int32_t l1, uint64_t seed, float *const *rep, int32_t nrep) {
+    RG_GUARD_BEGIN
+    RG_TRY(need_ready(g));
+    if (nvariants < 1 || !variants) return fail(RAFTGP_ERR_PARAM, "need >= 1 variant");
+    if (l1 <= 0) return fail(RAFTGP_ERR_PARAM, "l1 must be > 0");
+    RG_TRY(check_reps(rep, nrep, nvariants));
+    int where[3] = {-1, -1, -1};
+    for (int v = 0; v < nvariants; ++v) {
+        RG_TRY(check_variant(g, variants[v], r));
+        if (where[variants[v]] >= 0) return fail(RAFTGP_ERR_PARAM, "variant listed twice");
+        where[variants[v]] = v;
+    }
+    RG_TRY(set_device(g->ctx));
+    if (g->nl == 0) return RAFTGP_OK;
+    bool al = sketch_w_supported(r, l1) && push_fusable(l1, 0);
+    for (int64_t i = 0; i < (int64_t)nrep * nvariants; ++i) al = al && aligned16(rep[i]);
+    if (al) return first_transform_pre(g, nvariants, variants, r, l1, seed, nullptr, where, nullptr, rep, nrep);
+    // other shapes: local T1, then copied into every replica (not overlapped)
+    raftgp_ctx ctx = g->ctx;
+    std::vector<float *> T(nvariants, nullptr);
+    raftgp_status st = RAFTGP_OK;
+    for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v) st = dalloc_t(ctx, &T[v], (size_t)g->nl * l1);
+    if (st == RAFTGP_OK) st = raftgp_feature_transform(g, nvariants, variants, r, l1, seed, T.data());
+    for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v)
+        for (int q = 0; q < nrep && st == RAFTGP_OK; ++q)
+            st = dcopy(ctx, rep[(size_t)v * nrep + q] + (size_t)g->row_begin * l1, T[v], sizeof(float) * g->nl * l1);
+    for (auto t : T) dfree(ctx, t);
+    return st;
+    RG_GUARD_END
+}
+
+raftgp_status raftgp_gcn_hop_push(raftgp_graph g, const float *T_full_dev, int32_t w, float *Z_out_dev,
+                                  const float *W_next_dev, int32_t w_next, float *const *rep, int32_t nrep) {
+    RG_GUARD_BEGIN
+    RG_TRY(need_ready(g));
+    if (w <= 0 || w_next <= 0 || !W_next_dev) return fail(RAFTGP_ERR_PARAM, "push hop needs w > 0 and W_next");
+    if (g->nl > 0 && !T_full_dev) return fail(RAFTGP_ERR_PARAM, "null T_full");
+    RG_TRY(check_reps(rep, nrep, 1));
+    RG_TRY(set_device(g->ctx));
+    if (g->nl == 0) return RAFTGP_OK;
+    PushSpec p{};
+    p.nrep = nrep;
+    p.row0 = g->row_begin;
+    for (int q = 0; q < nrep; ++q) p.rep[q] = rep[q];
+    bool al = push_fusable(w, w_next) && aligned16(T_full_dev) && aligned16(W_next_dev) &&
+              (!Z_out_dev || aligned16(Z_out_dev));
+    for (int q = 0; q < nrep; ++q) al = al && aligned16(rep[q]);
+    if (al) return gcn_hop(g, T_full_dev, w, Z_out_dev, W_next_dev, w_next, nullptr, 0, &p);
+    raftgp_ctx ctx = g->ctx;
+    float *T = nullptr;
+    raftgp_status st = dalloc_t(ctx, &T, (size_t)g->nl * w_next);
+    if (st == RAFTGP_OK) st = gcn_hop(g, T_full_dev, w, Z_out_dev, W_next_dev, w_next, T);
+    for (int q = 0; q < nrep && st == RAFTGP_OK; ++q)
+        st = dcopy(ctx, rep[q] + (size_t)g->row_begin * w_next, T, sizeof(float) * g->nl * w_next);
+    dfree(ctx, T);
+    return st;
+    RG_GUARD_END
+}
+
+raftgp_status raftgp_ipc_alloc(raftgp_ctx ctx, size_t bytes, void **dev_ptr, void *handle64) {
+    if (!ctx || !dev_ptr || !handle64) return fail(RAFTGP_ERR_PARAM, "null argument");
+    *dev_ptr = nullptr;
+    RG_TRY(set_device(ctx));
+    cudaError_t e = cudaMalloc(dev_ptr, bytes ? bytes : 16);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *dev_ptr = nullptr;
+        return cuda_fail(e, "raftgp_ipc_alloc");
+    }
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    e = cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t *>(handle64), *dev_ptr);
+    if (e != cudaSuccess) {
+        cudaFree(*dev_ptr);
+        *dev_ptr = nullptr;
+        cudaGetLastError();
+        return cuda_fail(e, "cudaIpcGetMemHandle");
+    }
+    return RAFTGP_OK;
+}
+
+raftgp_status raftgp_ipc_free(raftgp_ctx ctx, void *dev_ptr) {
+    if (!ctx || !dev_ptr) return RAFTGP_OK;
+    RG_TRY(set_device(ctx));
+    RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    RG_CUDA(cudaFree(dev_ptr));
+    return RAFTGP_OK;
+}
+
+raftgp_status raftgp_ipc_open(raftgp_ctx ctx, const void *handle64, void **dev_ptr) {
+    if (!ctx || !handle64 || !dev_ptr) return fail(RAFTGP_ERR_PARAM, "null argument");
+    *dev_ptr = nullptr;
+    RG_TRY(set_device(ctx));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof(h));
+    cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *dev_ptr = nullptr;
+        return cuda_fail(e, "cudaIpcOpenMemHandle");
+    }
+    return RAFTGP_OK;
+}
+
+raftgp_status raftgp_ipc_close(raftgp_ctx ctx, void *dev_ptr) {
+    if (!ctx || !dev_ptr) return RAFTGP_OK;
+    RG_TRY(set_device(ctx));
+    RG_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+    return RAFTGP_OK;
+}
+
+raftgp_status raftgp_copy(raftgp_ctx ctx, void *dst_dev, const void *src_dev, size_t bytes) {
+    if (!ctx || (bytes && (!dst_dev || !src_dev))) return fail(RAFTGP_ERR_PARAM, "null argument");
+    RG_TRY(set_device(ctx));
+    return dcopy(ctx, dst_dev, src_dev, bytes);
 }
 
 }  // extern "C"

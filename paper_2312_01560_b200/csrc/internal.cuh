@@ -201,13 +201,27 @@ raftgp_status feature_hop(raftgp_graph g, int variant, int32_t r, const float *t
 // NCut and full-modularity feature hops from ONE gather of Theta (+ both first transforms).
 raftgp_status feature_hop_dual(raftgp_graph g, int32_t r, const float *theta, const double *gvec, float *Y_ncut,
                                float *Y_mod, const float *W1, int32_t l1, float *T_ncut, float *T_mod);
+// Fused exchange (a6 without a separate all-gather): a producing hop's epilogue stores each of its rows of
+// the next operand T straight into every rank's full n-row copy of T (`rep`: the ranks' buffers, peer
+// pointers opened through CUDA IPC over NVLink; `rep2`: the second variant's, for the dual kernels), at
+// global row row0 + local row. The kernel ends with a system-scope fence so the peers see the rows once the
+// producing kernels of all ranks have completed (the caller then runs a stream-ordered barrier).
+constexpr int kMaxPush = 8;
+struct PushSpec {
+    float *rep[kMaxPush];
+    float *rep2[kMaxPush];
+    int nrep;
+    int64_t row0;
+};
 // Feature hop on a pre-transformed operand Theta' = Theta W1 (no epilogue GEMM): writes
 // T1 = s^ (.) (X Theta') for NCUT (T_ncut) and/or MOD (T_mod), or MOD_REDUCED (T_ncut slot, variant 2).
 raftgp_status feature_hop_pre(raftgp_graph g, int variant_or_dual, int32_t l1, const float *theta_w,
-                              const double *gvec_w, float *T_a, float *T_b);
+                              const double *gvec_w, float *T_a, float *T_b, const PushSpec *push = nullptr);
 raftgp_status gcn_transform(raftgp_graph g, const float *Z, int32_t lin, const float *W, int32_t lout, float *T);
 raftgp_status gcn_hop(raftgp_graph g, const float *Tfull, int32_t w, float *Zout, const float *Wn, int32_t wn,
-                      float *Tnext, int32_t tn_ld = 0);
+                      float *Tnext, int32_t tn_ld = 0, const PushSpec *push = nullptr);
+// whether gcn_hop / feature_hop_pre can fuse the push into their epilogue for these widths
+bool push_fusable(int32_t w, int32_t wn);
 // the same hops over a list of local rows (NEXT-4 streaming)
 raftgp_status feature_hop_pre_rows(raftgp_graph g, int variant, int32_t l1, const float *theta_w, const double *gvec_w,
                                    float *T, const int32_t *rows, int64_t count);

@@ -58,6 +58,8 @@ struct HopArgs {
     int32_t tn_ld;             // row stride of Tn in floats (0 = WN)
     unsigned long long *ctr;   // zeroed group counter: warps claim kClaim row groups at a time (degree skew), or
                                // null: static grid-stride
+    PushSpec push;             // push.nrep > 0: the T output (out/out2 when WN == 0, Tn/Tn2 when WN > 0) goes to
+                               // the replicas at global rows instead of the local buffers
 };
 
 constexpr int kClaim = 8;      // row groups per dynamic claim
@@ -287,9 +289,17 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
                 float *o = cl < HL ? a.out : a.out2;
                 if (sub == 0 && o != nullptr) reinterpret_cast<float4 *>(o)[row * HL + (cl % HL)] = y;
             } else if (sub == 0) {
-                if (a.out != nullptr) reinterpret_cast<float4 *>(a.out)[row * LPN + cl] = y;
-                if constexpr (NV == 2) {
-                    if (a.out2 != nullptr) reinterpret_cast<float4 *>(a.out2)[row * LPN + cl] = y2;
+                if (WN == 0 && a.push.nrep > 0) {   // fused exchange: this row into every rank's copy of T
+                    const int64_t grow = a.push.row0 + row;
+                    for (int r = 0; r < a.push.nrep; ++r) {
+                        reinterpret_cast<float4 *>(a.push.rep[r])[grow * LPN + cl] = y;
+                        if constexpr (NV == 2) reinterpret_cast<float4 *>(a.push.rep2[r])[grow * LPN + cl] = y2;
+                    }
+                } else {
+                    if (a.out != nullptr) reinterpret_cast<float4 *>(a.out)[row * LPN + cl] = y;
+                    if constexpr (NV == 2) {
+                        if (a.out2 != nullptr) reinterpret_cast<float4 *>(a.out2)[row * LPN + cl] = y2;
+                    }
                 }
                 if constexpr (WN > 0) {
                     reinterpret_cast<float4 *>(stage)[rr * LPN + cl] = y;
@@ -337,15 +347,23 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
                     if (r_in < rows_here) {
                         const int64_t row = a.order ? static_cast<int64_t>(__ldg(a.order + row0 + r_in)) : row0 + r_in;
                         const float shi = __ldg(a.sh_all + a.rb + row);
-                        float4 *T4 = reinterpret_cast<float4 *>(v == 0 ? a.Tn : a.Tn2);
-                        const int64_t ld4 = a.tn_ld > 0 ? a.tn_ld / 4 : OL;
-                        T4[row * ld4 + oc] = make_float4(shi * o[q].x, shi * o[q].y, shi * o[q].z, shi * o[q].w);
+                        const float4 t4 = make_float4(shi * o[q].x, shi * o[q].y, shi * o[q].z, shi * o[q].w);
+                        if (a.push.nrep > 0) {   // fused exchange (see PushSpec)
+                            const int64_t grow = a.push.row0 + row;
+                            for (int r = 0; r < a.push.nrep; ++r)
+                                reinterpret_cast<float4 *>(v == 0 ? a.push.rep[r] : a.push.rep2[r])[grow * OL + oc] = t4;
+                        } else {
+                            float4 *T4 = reinterpret_cast<float4 *>(v == 0 ? a.Tn : a.Tn2);
+                            const int64_t ld4 = a.tn_ld > 0 ? a.tn_ld / 4 : OL;
+                            T4[row * ld4 + oc] = t4;
+                        }
                     }
                 }
             }
             __syncwarp();
         }
     }
+    if (a.push.nrep > 1) __threadfence_system();   // the pushed rows are visible to the peers
 }
 
 // ---------------------------------------------------------------- generic (any width / alignment)
@@ -553,7 +571,7 @@ raftgp_status feature_hop_dual(raftgp_graph g, int32_t r, const float *theta, co
 }
 
 raftgp_status feature_hop_pre(raftgp_graph g, int variant_or_dual, int32_t l1, const float *theta_w,
-                              const double *gvec_w, float *T_a, float *T_b) {
+                              const double *gvec_w, float *T_a, float *T_b, const PushSpec *push) {
     if (g->nl == 0) return RAFTGP_OK;
     HopArgs a = base_args(g, l1);
     a.X = theta_w;
@@ -561,7 +579,10 @@ raftgp_status feature_hop_pre(raftgp_graph g, int variant_or_dual, int32_t l1, c
     a.out = T_a;
     a.out2 = T_b;
     a.scale_sh = true;
-    if (!((l1 == 32 || l1 == 64 || l1 == 128) && aligned16(theta_w) && aligned16(T_a) && (!T_b || aligned16(T_b))))
+    if (push) a.push = *push;
+    bool al = aligned16(theta_w) && (push || aligned16(T_a)) && (push || !T_b || aligned16(T_b));
+    for (int r = 0; push && r < push->nrep; ++r) al = al && aligned16(push->rep[r]) && (!T_b || aligned16(push->rep2[r]));
+    if (!((l1 == 32 || l1 == 64 || l1 == 128) && al))
         return fail(RAFTGP_ERR_INTERNAL, "feature_hop_pre: unsupported width/alignment");
     auto go = [&](auto kind_tag) -> raftgp_status {
         constexpr int K = decltype(kind_tag)::value;
@@ -632,14 +653,25 @@ raftgp_status gcn_transform(raftgp_graph g, const float *Z, int32_t lin, const f
     return dispatch<KIND_LOAD>(g->ctx, a, lin, lout);
 }
 
+bool push_fusable(int32_t w, int32_t wn) {
+    return (w == 32 || w == 64 || w == 128) && (wn == 0 || wn == 32 || wn == 64 || wn == 128);
+}
+
 raftgp_status gcn_hop(raftgp_graph g, const float *Tfull, int32_t w, float *Zout, const float *Wn, int32_t wn,
-                      float *Tnext, int32_t tn_ld) {
+                      float *Tnext, int32_t tn_ld, const PushSpec *push) {
     HopArgs a = base_args(g, w);
     a.X = Tfull;
     a.out = Zout;
     a.Wn = Wn;
     a.Tn = Tnext;
     a.tn_ld = tn_ld;
+    if (push) {
+        bool al = aligned16(Tfull) && aligned16(Wn) && (!Zout || aligned16(Zout));
+        for (int r = 0; r < push->nrep; ++r) al = al && aligned16(push->rep[r]);
+        if (!(Wn && push_fusable(w, wn) && al)) return fail(RAFTGP_ERR_INTERNAL, "gcn_hop: push needs the fast kernel");
+        a.push = *push;
+        a.Tn = push->rep[0];   // non-null for the dispatcher's alignment checks; the kernel writes the replicas
+    }
     if (tn_ld > 0 && tn_ld != wn && !((w == 32 || w == 64 || w == 128) && (wn == 32 || wn == 64 || wn == 128) &&
                                       aligned16(Tfull) && aligned16(Tnext) && aligned16(Wn) && tn_ld % 4 == 0))
         return fail(RAFTGP_ERR_INTERNAL, "gcn_hop: strided T_next needs the fast kernel");

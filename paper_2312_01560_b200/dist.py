@@ -14,6 +14,12 @@ The per-rank pipeline is a generator that yields ("gather", tensor) at each exch
 receives the gathered block; drivers run it over torch.distributed (NCCL on B200, gloo on CPU tests)
 or, for single-GPU testing, over P shards in lockstep ("loopback"). The compute steps go through an
 `engine`: `CudaEngine` calls libraftgp (the product path); tests may plug a CPU engine.
+
+Push mode (`rank_pipeline_push`, the default on GPUs): the per-hop all-gather is fused into the producing
+kernels. Every rank holds a full n-row copy of each operand T_k; the feature transform and each GCN hop
+store their finished rows straight into ALL ranks' copies (peer memory over NVLink, mapped with CUDA IPC:
+raftgp_feature_transform_push / raftgp_gcn_hop_push), so the exchange overlaps the hop's gathers row by
+row, and one stream-ordered barrier (a 1-element all-reduce) separates producing and consuming hops.
 """
 from __future__ import annotations
 
@@ -65,6 +71,18 @@ class CudaEngine:
         _, T_next = rg.raftgp_gcn_hop(h, T_full, Z, W_next)
         return Z, T_next
 
+    # push mode: `reps` are device pointers (IPC-mapped peers) or tensors, one per rank copy
+    def feature_transform_push(self, h, variants, dims, seed, reps):
+        rg.raftgp_feature_transform_push(h, variants, dims[0], dims[1], seed, reps)
+
+    def hop_push(self, h, T_own, w, W_next, reps_next):
+        rg.raftgp_gcn_hop_push(h, T_own, w, W_next, reps_next)
+
+    def hop_last(self, h, T_own, w):
+        Z = torch.empty((max(1, h.rows), w), dtype=torch.float32, device=self.ctx.device)[: h.rows]
+        rg.raftgp_gcn_hop(h, T_own, Z, w=w)
+        return Z
+
 
 def rank_pipeline(engine, n: int, src, dst, rank: int, world: int, variants, dims: Sequence[int], seed: int,
                   keep: Optional[dict] = None) -> Generator:
@@ -102,6 +120,49 @@ def rank_pipeline(engine, n: int, src, dst, rank: int, world: int, variants, dim
     return out[vlist[0]] if single else out
 
 
+def rank_pipeline_push(engine, n: int, src, dst, rank: int, world: int, variants, dims: Sequence[int], seed: int,
+                       keep: Optional[dict] = None) -> Generator:
+    """One rank's share of the path with the exchange fused into the producing hops (module docstring).
+    Yields to its driver:
+        ("gather", block)   -> the all-gathered degree block (as in rank_pipeline)
+        ("buffers", info)   -> {(variant, k): [copy of rank 0, ..., rank P-1]} full n x dims[k] copies of T_k
+                               (a driver may hand out only this rank's copy: a list of length 1)
+        ("barrier", [(variant, k), ...]) -> the listed copies are complete on every rank
+    Same arithmetic as rank_pipeline, so the result is bit-identical to it and to P = 1."""
+    single = isinstance(variants, (str, int))
+    vlist = [variants] if single else list(variants)
+    ranges, R = row_partition(n, world)
+    rb, re = ranges[rank]
+    h = engine.build(n, src, dst, rb, re)
+    deg_all = yield ("gather", _pad(engine.local_degrees(h), R))
+    engine.set_degrees(h, deg_all[:n].contiguous())
+    L = len(dims) - 1
+    spec = [(v, k, int(dims[k])) for v in vlist for k in range(1, L + 1)]
+    reps = yield ("buffers", {"n": n, "spec": spec, "ranges": ranges, "R": R})
+
+    def own(v, k):
+        lst = reps[(v, k)]
+        return lst[rank] if len(lst) > 1 else lst[0]
+
+    W = {k: engine.weights(seed, k, dims[k - 1], dims[k]) for k in range(2, L + 1)}
+    engine.feature_transform_push(h, vlist, dims, seed, {v: reps[(v, 1)] for v in vlist})
+    yield ("barrier", [(v, 1) for v in vlist])
+    out = {}
+    for k in range(1, L + 1):
+        produced = []
+        for v in vlist:
+            if k < L:
+                engine.hop_push(h, own(v, k), int(dims[k]), W[k + 1], reps[(v, k + 1)])
+                produced.append((v, k + 1))
+            else:
+                out[v] = engine.hop_last(h, own(v, k), int(dims[k]))
+        if produced:
+            yield ("barrier", produced)
+    if keep is not None:
+        keep["graph"] = h
+    return out[vlist[0]] if single else out
+
+
 class _Done:
     """A completed exchange (loopback / blocking drivers)."""
 
@@ -109,8 +170,9 @@ class _Done:
         self.value = value
 
 
-def run_loopback(gens: List[Generator]):
-    """Advance P rank pipelines in lockstep; a gather concatenates the P blocks in rank order."""
+def run_loopback(gens: List[Generator], device=None, dtype=torch.float32):
+    """Advance P rank pipelines in lockstep; a gather concatenates the P blocks in rank order; push-mode
+    buffers are P full copies on `device` (one per logical rank)."""
     msgs = [next(g) for g in gens]
     results: List[Optional[torch.Tensor]] = [None] * len(gens)
     while True:
@@ -119,6 +181,13 @@ def run_loopback(gens: List[Generator]):
             raise RuntimeError("rank pipelines went out of step")
         if kind == "wait":
             replies = [m[1].value for m in msgs]
+        elif kind == "buffers":   # one full copy per logical rank, shared by all (push mode)
+            info = msgs[0][1]
+            bufs = {(v, k): [torch.zeros((info["n"], w), dtype=dtype, device=device) for _ in msgs]
+                    for v, k, w in info["spec"]}
+            replies = [bufs for _ in msgs]
+        elif kind == "barrier":   # one stream, ranks in lockstep: nothing to wait for
+            replies = [None for _ in msgs]
         else:
             full = torch.cat([m[1] for m in msgs], 0)
             replies = [full if kind == "gather" else _Done(full) for _ in msgs]
@@ -146,8 +215,56 @@ class _Pending:
         return torch.cat(self.parts, 0) if self.parts is not None else self.out
 
 
-def run_distributed(gen: Generator, group=None):
-    """Drive one rank's pipeline over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+class PushBuffers:
+    """Per-process cache of the push-mode copies: for every (variant, k) a library-allocated n x w buffer on
+    this GPU (raftgp_ipc_alloc) plus the peers' buffers mapped through CUDA IPC (raftgp_ipc_open), so steps
+    after the first reuse them. Rank q's copy is at list index q."""
+
+    def __init__(self, ctx: rg.Context, group=None):
+        self.ctx, self.group, self.key, self.own, self.maps = ctx, group, None, {}, {}
+
+    def get(self, info) -> dict:
+        import torch.distributed as dist
+        key = (info["n"], tuple(info["spec"]))
+        if key == self.key:
+            return self.maps
+        self.close()
+        world, rank = dist.get_world_size(self.group), dist.get_rank(self.group)
+        handles = {}
+        for v, k, w in info["spec"]:
+            buf = rg.IpcBuffer(self.ctx, max(16, info["n"] * w * 4))
+            self.own[(v, k)] = buf
+            handles[(v, k)] = buf.handle_bytes()
+        allh = [None] * world
+        dist.all_gather_object(allh, handles, group=self.group)
+        for vk in handles:
+            self.maps[vk] = [self.own[vk].ptr if q == rank else rg.raftgp_ipc_open(self.ctx, allh[q][vk])
+                             for q in range(world)]
+        self.key = key
+        dist.barrier(group=self.group)
+        return self.maps
+
+    def close(self):
+        """Unmap the peers' copies, wait until every rank has done so, then free this rank's copies."""
+        import torch.distributed as dist
+        if self.maps:
+            rank = dist.get_rank(self.group)
+            for ptrs in self.maps.values():
+                for q, p in enumerate(ptrs):
+                    if q != rank:
+                        rg.raftgp_ipc_close(self.ctx, p)
+        if self.own and dist.is_initialized():
+            torch.cuda.synchronize(self.ctx.device)
+            dist.barrier(group=self.group)
+        for b in self.own.values():
+            b.close()
+        self.key, self.own, self.maps = None, {}, {}
+
+
+def run_distributed(gen: Generator, group=None, push: Optional[PushBuffers] = None):
+    """Drive one rank's pipeline over torch.distributed (NCCL on GPUs, gloo on CPU). Push-mode buffers come
+    from `push` (GPU: IPC-mapped copies) or, without it, are this rank's own CPU copy only, completed at each
+    barrier by an all-gather of the row blocks (the CPU stand-in for the peer stores)."""
     import torch.distributed as dist
 
     def _start(t: torch.Tensor) -> _Pending:
@@ -159,6 +276,7 @@ def run_distributed(gen: Generator, group=None):
         parts = [torch.empty_like(t) for _ in range(world)]
         return _Pending(dist.all_gather(parts, t, group=group, async_op=True), None, parts)
 
+    cpu_copies, info = {}, None
     msg = next(gen)
     while True:
         kind, payload = msg
@@ -166,6 +284,30 @@ def run_distributed(gen: Generator, group=None):
             reply = _start(payload).result()
         elif kind == "start":
             reply = _start(payload)
+        elif kind == "buffers":
+            info = payload
+            if push is not None:
+                reply = push.get(payload)
+            else:
+                cpu_copies = {(v, k): [torch.zeros((payload["n"], w), dtype=torch.float64)]
+                              for v, k, w in payload["spec"]}
+                reply = cpu_copies
+        elif kind == "barrier":
+            if push is not None:
+                if dist.get_backend(group) == "nccl":
+                    flag = torch.zeros(1, dtype=torch.float32, device=push.ctx.device)
+                    dist.all_reduce(flag, group=group)   # stream-ordered: every rank's producing kernels are done
+                else:                                    # host barrier (tests: several processes on one GPU)
+                    torch.cuda.synchronize(push.ctx.device)
+                    dist.barrier(group=group)
+            else:
+                rank = dist.get_rank(group)
+                rb, re = info["ranges"][rank]
+                for vk in payload:
+                    full = cpu_copies[vk][0]
+                    blocks = _start(_pad(full[rb:re], info["R"])).result()
+                    full.copy_(blocks[: info["n"]])
+            reply = None
         else:
             reply = payload.result()
         try:
@@ -174,8 +316,10 @@ def run_distributed(gen: Generator, group=None):
             return stop.value
 
 
-def loopback_embed(ctx: rg.Context, n: int, src, dst, world: int, variant, dims, seed: int):
-    """P logical ranks on ONE GPU (sequential per stage, no concurrent waiting kernels)."""
+def loopback_embed(ctx: rg.Context, n: int, src, dst, world: int, variant, dims, seed: int, push: bool = False):
+    """P logical ranks on ONE GPU (sequential per stage, no concurrent waiting kernels). push=True runs the
+    fused-exchange pipeline: each logical rank's kernels store their rows into all P full copies."""
     eng = CudaEngine(ctx)
-    gens = [rank_pipeline(eng, n, src, dst, p, world, variant, dims, seed) for p in range(world)]
-    return run_loopback(gens)
+    pipe = rank_pipeline_push if push else rank_pipeline
+    gens = [pipe(eng, n, src, dst, p, world, variant, dims, seed) for p in range(world)]
+    return run_loopback(gens, device=ctx.device)

@@ -37,7 +37,8 @@ EXPORTS = (
     "raftgp_embed", "raftgp_embed_multi", "raftgp_feature_transform", "raftgp_modularity", "raftgp_ncut", "raftgp_local_modularity",
     "raftgp_model_select", "raftgp_gemm_tf32x3", "raftgp_sbm_sample", "raftgp_stream_create",
     "raftgp_stream_add_edges", "raftgp_stream_embedding", "raftgp_stream_graph", "raftgp_stream_destroy",
-    "raftgp_build_embed", "raftgp_ctx_trim",
+    "raftgp_build_embed", "raftgp_ctx_trim", "raftgp_feature_transform_push", "raftgp_gcn_hop_push",
+    "raftgp_ipc_alloc", "raftgp_ipc_free", "raftgp_ipc_open", "raftgp_ipc_close", "raftgp_copy",
 )
 
 _lib = None
@@ -81,6 +82,13 @@ _SIGS = {
     "raftgp_project": (ctypes.c_int, [c_vp, ctypes.c_int, c_i32, c_u64, c_vp]),
     "raftgp_gcn_transform": (ctypes.c_int, [c_vp, c_vp, c_i32, c_vp, c_i32, c_vp]),
     "raftgp_gcn_hop": (ctypes.c_int, [c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp]),
+    "raftgp_feature_transform_push": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i32, c_i32, c_u64, c_vp, c_i32]),
+    "raftgp_gcn_hop_push": (ctypes.c_int, [c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_i32]),
+    "raftgp_ipc_alloc": (ctypes.c_int, [c_vp, ctypes.c_size_t, P(c_vp), c_vp]),
+    "raftgp_ipc_free": (ctypes.c_int, [c_vp, c_vp]),
+    "raftgp_ipc_open": (ctypes.c_int, [c_vp, c_vp, P(c_vp)]),
+    "raftgp_ipc_close": (ctypes.c_int, [c_vp, c_vp]),
+    "raftgp_copy": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_size_t]),
     "raftgp_gnn_embed": (ctypes.c_int, [c_vp, c_i32, c_vp, c_u64, c_vp, c_vp, c_vp]),
     "raftgp_embed": (ctypes.c_int, [c_vp, ctypes.c_int, c_i32, c_vp, c_u64, c_vp, c_vp, c_vp]),
     "raftgp_embed_multi": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i32, c_vp, c_u64, c_vp, c_vp]),
@@ -316,13 +324,16 @@ def raftgp_gcn_transform(g: Graph, Z: torch.Tensor, W: torch.Tensor, T: Optional
     return T
 
 
-def raftgp_gcn_hop(g: Graph, T_full: torch.Tensor, Z_out: Optional[torch.Tensor] = None,
-                   W_next: Optional[torch.Tensor] = None, T_next: Optional[torch.Tensor] = None):
-    w = T_full.shape[1]
+def raftgp_gcn_hop(g: Graph, T_full, Z_out: Optional[torch.Tensor] = None,
+                   W_next: Optional[torch.Tensor] = None, T_next: Optional[torch.Tensor] = None,
+                   w: Optional[int] = None):
+    """T_full: n x w tensor, or a raw device pointer with its width w."""
+    w = T_full.shape[1] if isinstance(T_full, torch.Tensor) else int(w)
     wn = 0 if W_next is None else W_next.shape[1]
     if W_next is not None and T_next is None:
         T_next = torch.empty((g.rows, wn), dtype=torch.float32, device=g.ctx.device)
-    _ck(load_library().raftgp_gcn_hop(g.h, _ptr(T_full), w, _ptr(Z_out), _ptr(W_next), wn, _ptr(T_next)))
+    _ck(load_library().raftgp_gcn_hop(g.h, _dptr(T_full) if T_full is not None else None, w, _ptr(Z_out),
+                                      _ptr(W_next), wn, _ptr(T_next)))
     return Z_out, T_next
 
 
@@ -401,6 +412,79 @@ def raftgp_build_embed(ctx: Context, n: int, src: torch.Tensor, dst: torch.Tenso
                                           seed, _zk_array([Z[nm] for nm in names]),
                                           ctypes.byref(h) if keep_graph else None))
     return Z, (Graph(ctx, h) if keep_graph else None)
+
+
+def _dptr(x) -> int:
+    """Device pointer of a CUDA tensor or a raw pointer (int)."""
+    if isinstance(x, torch.Tensor):
+        return _ptr(_dev(x, "buffer"))
+    return int(x)
+
+
+def raftgp_feature_transform_push(g: Graph, variants: Sequence, r: int, l1: int, seed: int, reps: dict):
+    """a6 fused: T1 of every variant pushed into all ranks' full n x l1 copies. reps = {variant: [ptr or tensor
+    per rank]} (same length for every variant)."""
+    vs = [_variant(v) for v in variants]
+    names = [v if isinstance(v, str) else {0: "ncut", 1: "mod", 2: "mod_reduced"}[int(v)] for v in variants]
+    nrep = len(reps[names[0]])
+    flat = [_dptr(p) for nm in names for p in reps[nm]]
+    arr = (c_vp * len(flat))(*flat)
+    va = (c_i32 * len(vs))(*vs)
+    _ck(load_library().raftgp_feature_transform_push(g.h, len(vs), va, r, l1, seed, arr, nrep))
+
+
+def raftgp_gcn_hop_push(g: Graph, T_full, w: int, W_next: torch.Tensor, reps: Sequence, want_Z: bool = False):
+    """a6 fused: one GCN hop whose T_next rows go straight into every rank's full copy (reps: ptrs/tensors).
+    Returns Z (local rows x w) when want_Z, else None."""
+    Z = torch.empty((max(1, g.rows), w), dtype=torch.float32, device=g.ctx.device)[: g.rows] if want_Z else None
+    flat = [_dptr(p) for p in reps]
+    arr = (c_vp * len(flat))(*flat)
+    _ck(load_library().raftgp_gcn_hop_push(g.h, _dptr(T_full), w, None if Z is None else _ptr(Z),
+                                           _ptr(W_next.contiguous()), W_next.shape[1], arr, len(flat)))
+    return Z
+
+
+class IpcBuffer:
+    """A library-allocated device buffer that other processes can map (raftgp_ipc_alloc)."""
+
+    def __init__(self, ctx: Context, nbytes: int):
+        self.ctx = ctx
+        p = c_vp()
+        self.handle = (ctypes.c_char * 64)()
+        _ck(load_library().raftgp_ipc_alloc(ctx.h, nbytes, ctypes.byref(p), self.handle))
+        self.ptr = p.value
+        self.nbytes = nbytes
+
+    def handle_bytes(self) -> bytes:
+        return bytes(self.handle)
+
+    def close(self):
+        if getattr(self, "ptr", None) and _lib is not None and not _exiting:
+            _lib.raftgp_ipc_free(self.ctx.h, c_vp(self.ptr))
+        self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def raftgp_ipc_open(ctx: Context, handle: bytes) -> int:
+    """Map another process's IpcBuffer on this context's device; returns the device pointer."""
+    h = (ctypes.c_char * 64).from_buffer_copy(handle)
+    p = c_vp()
+    _ck(load_library().raftgp_ipc_open(ctx.h, h, ctypes.byref(p)))
+    return p.value
+
+
+def raftgp_ipc_close(ctx: Context, ptr: int):
+    _ck(load_library().raftgp_ipc_close(ctx.h, c_vp(ptr)))
+
+
+def raftgp_copy(ctx: Context, dst, src, nbytes: int):
+    """Device-to-device copy by a library kernel (tensors or raw pointers)."""
+    _ck(load_library().raftgp_copy(ctx.h, c_vp(_dptr(dst)), c_vp(_dptr(src)), nbytes))
 
 
 def raftgp_feature_transform(g: Graph, variants: Sequence, r: int, l1: int, seed: int) -> dict:

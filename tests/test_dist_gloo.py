@@ -76,6 +76,21 @@ class NumpyEngine:
             Tn = torch.from_numpy(h["sh"][h["rb"]:h["re"], None] * (Z @ W_next.numpy()))
         return (torch.from_numpy(Z) if want_Z else None), Tn
 
+    # push mode: write this rank's rows [rb, re) into every given full copy
+    def feature_transform_push(self, h, variants, dims, seed, reps):
+        T = self.feature_transform(h, variants, dims, seed)
+        for v in variants:
+            for buf in reps[v]:
+                buf[h["rb"]:h["re"]] = T[v]
+
+    def hop_push(self, h, T_own, w, W_next, reps_next):
+        _, Tn = self.hop(h, T_own, W_next, want_Z=False)
+        for buf in reps_next:
+            buf[h["rb"]:h["re"]] = Tn
+
+    def hop_last(self, h, T_own, w):
+        return self.hop(h, T_own, None, want_Z=True)[0]
+
 
 def _free_port():
     s = socket.socket()
@@ -85,23 +100,24 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n, src, dst, variants, dims, seed, out):
+def _worker(rank, world, port, n, src, dst, variants, dims, seed, out, push=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        gen = rdist.rank_pipeline(NumpyEngine(), n, torch.from_numpy(src), torch.from_numpy(dst), rank, world,
-                                  variants, dims, seed)
+        pipe = rdist.rank_pipeline_push if push else rdist.rank_pipeline
+        gen = pipe(NumpyEngine(), n, torch.from_numpy(src), torch.from_numpy(dst), rank, world, variants, dims, seed)
         Z = rdist.run_distributed(gen)
         out[rank] = {v: Z[v].numpy() for v in Z}
     finally:
         dist.destroy_process_group()
 
 
-def _run(world, n, src, dst, variants, dims, seed):
+def _run(world, n, src, dst, variants, dims, seed, push=False):
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), n, src, dst, variants, dims, seed, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), n, src, dst, variants, dims, seed, out, push), nprocs=world,
+             join=True)
     return {v: np.concatenate([out[r][v] for r in range(world)], 0) for v in variants}
 
 
@@ -114,12 +130,15 @@ def test_row_partition():
     assert ranges == [(0, 0), (0, 0)] and R == 1
 
 
+@pytest.mark.parametrize("push", [False, True])
 @pytest.mark.parametrize("world", [2, 3])
-def test_gloo_row_partitioned_pipeline_matches_oracle(world):
+def test_gloo_row_partitioned_pipeline_matches_oracle(world, push):
+    """push=True: the fused-exchange pipeline (rank_pipeline_push); on CPU the peer stores are stood in for
+    by an all-gather of the row blocks at each barrier."""
     gr = synth.generate("C1", 2, n=301)               # 301 rows: ragged partition (101/101/99, 151/150)
     dims = (16, 12, 8)
     variants = ["ncut", "mod"]
-    Zd = _run(world, gr.n, gr.src, gr.dst, variants, dims, 7)
+    Zd = _run(world, gr.n, gr.src, gr.dst, variants, dims, 7, push)
     ref = oracle.build_csr(gr.n, gr.src, gr.dst)
     for v in variants:
         Yo = oracle.project(ref, v, dims[0], 7)
@@ -135,6 +154,23 @@ def test_loopback_equals_single_rank_numpy(variants):
     one = rdist.run_loopback([rdist.rank_pipeline(NumpyEngine(), gr.n, src, dst, 0, 1, variants, dims, 3)])[0]
     three = rdist.run_loopback([rdist.rank_pipeline(NumpyEngine(), gr.n, src, dst, p, 3, variants, dims, 3)
                                 for p in range(3)])
+    if isinstance(variants, str):
+        np.testing.assert_allclose(torch.cat(three, 0).numpy(), one.numpy(), atol=1e-12)
+    else:
+        for v in variants:
+            np.testing.assert_allclose(torch.cat([t[v] for t in three], 0).numpy(), one[v].numpy(), atol=1e-12)
+
+
+@pytest.mark.parametrize("variants", ["ncut", ["ncut", "mod"], ["mod", "mod_reduced", "ncut"]])
+def test_loopback_push_equals_single_rank_numpy(variants):
+    """Push mode in lockstep: every logical rank writes its rows into all P copies; the copies each rank
+    reads must be complete, so the result equals the one-rank pipeline."""
+    gr = synth.generate("C1", 4, n=120)
+    dims = (8, 8, 6, 4)
+    src, dst = torch.from_numpy(gr.src), torch.from_numpy(gr.dst)
+    one = rdist.run_loopback([rdist.rank_pipeline(NumpyEngine(), gr.n, src, dst, 0, 1, variants, dims, 3)])[0]
+    three = rdist.run_loopback([rdist.rank_pipeline_push(NumpyEngine(), gr.n, src, dst, p, 3, variants, dims, 3)
+                                for p in range(3)], dtype=torch.float64)
     if isinstance(variants, str):
         np.testing.assert_allclose(torch.cat(three, 0).numpy(), one.numpy(), atol=1e-12)
     else:

@@ -235,6 +235,43 @@ def test_partitioned_equals_whole(rg, ctx, P, variants):
         assert rel_fro(one[v].cpu().numpy(), Zo) <= TOL
 
 
+@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("variants,dims", [(["ncut", "mod"], (64, 64, 32)), (["mod_reduced"], (64, 64, 32)),
+                                           (["ncut", "mod"], (128, 128, 64, 32)), (["ncut"], (48, 40, 24))])
+def test_partitioned_push_equals_whole(rg, ctx, P, variants, dims):
+    """Fused exchange (rank_pipeline_push): every logical rank's feature transform and GCN hops store their
+    rows straight into all P full copies of the next operand (raftgp_feature_transform_push /
+    raftgp_gcn_hop_push, the epilogue pushes of the hop kernels; odd widths take the compute-then-copy
+    path). The result is bit-identical to the whole-graph pipeline."""
+    from paper_2312_01560_b200 import dist
+    n, src, dst, ref = graph_case("c1_s3")
+    eng = dist.CudaEngine(ctx)
+    gens = [dist.rank_pipeline_push(eng, n, _t(src), _t(dst), p, P, variants, dims, 4) for p in range(P)]
+    Zs = dist.run_loopback(gens, device=ctx.device)
+    one = dist.run_loopback([dist.rank_pipeline(eng, n, _t(src), _t(dst), 0, 1, variants, dims, 4)])[0]
+    for v in variants:
+        assert torch.equal(torch.cat([z[v] for z in Zs], 0), one[v]), v
+        Zo = oracle.gcn(ref, dims, 4, oracle.project(ref, v, dims[0], 4))[-1]
+        assert rel_fro(one[v].cpu().numpy(), Zo) <= TOL
+
+
+def test_push_replicas_hold_all_rows(rg, ctx):
+    """raftgp_gcn_hop_push writes rows [row_begin, row_end) of T_next into every replica, nothing else."""
+    from paper_2312_01560_b200 import dist
+    n, src, dst, ref = graph_case("c1_s3")
+    w, wn = 64, 32
+    g = rg.raftgp_build_csr(ctx, n, _t(src), _t(dst), 100, 400)
+    g.set_degrees(torch.from_numpy(np.diff(ref.row_ptr).astype(np.int32)).cuda())
+    T = torch.randn(n, w, device="cuda")
+    W = torch.randn(w, wn, device="cuda")
+    reps = [torch.full((n, wn), 7.0, device="cuda") for _ in range(3)]
+    rg.raftgp_gcn_hop_push(g, T, w, W, reps)
+    _, Tn = rg.raftgp_gcn_hop(g, T, None, W)
+    for r in reps:
+        assert torch.equal(r[100:400], Tn)
+        assert bool((r[:100] == 7.0).all()) and bool((r[400:] == 7.0).all())
+
+
 # ------------------------------------------------------------------ a7: scoring
 def test_scoring_matches_oracle(rg, ctx):
     n, src, dst, ref = graph_case("c1_s0")
