@@ -452,6 +452,12 @@ def measure_table1(args, rg, dev, barrier, peak, peak_src):
                           "achieved": mma_tflops, "peak": tf32_peak, "unit": "TFLOP/s (TF32 MMA, 3 per fp32 flop)",
                           "frac": mma_tflops / tf32_peak if mma_tflops else None, "peak_source": tf32_src,
                           "fp32_flops_per_step": flops},
+        # context only (other hardware, the authors' own graphs, one variant per run, CSR build not included):
+        # Table III's per-stage wall times at 2E5
+        "paper_context": {"source": "PAPER.md:353-354 (Table III, N = 2E5)", "hardware": "2x Xeon 6130 + RTX 3090",
+                          "raftgp_c_feat_s": 62.105, "raftgp_c_emb_s": 1.3236,
+                          "raftgp_m_feat_s": 57.6826, "raftgp_m_emb_s": 1.5124,
+                          "this_step_s_both_variants_incl_csr": ms * 1e-3},
     }
 
 
