@@ -48,6 +48,14 @@ def main():
                 acc += int(((zz @ cen.T).argmax(1) == lab[b0:b0 + (1 << 20)]).sum())
             res[v] = {"cos_same_block_mean": float(cos_same.mean()), "cos_random_pair_mean": float(cos[~same].mean()),
                       "nearest_block_centroid_accuracy": acc / gr.n, "chance": 1.0 / K}
+            # Alg. 1 on this embedding: how whole are the planted blocks inside its clusters?
+            labs, Kf, _ = rg.raftgp_model_select(g, z)
+            lf = torch.as_tensor(labs).cuda().long()
+            tab = torch.zeros(K, Kf, device="cuda").index_put_((lab, lf), torch.ones_like(lab, dtype=torch.float32),
+                                                               accumulate=True)
+            purity = float(tab.max(1).values.sum() / gr.n)   # share of nodes in their block's majority cluster
+            res[v]["alg1_blocks_found"] = int(Kf)
+            res[v]["alg1_block_wholeness"] = purity
         out[name] = res
         print(name, json.dumps(res), flush=True)
         g.close()
