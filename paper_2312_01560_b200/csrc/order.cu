@@ -102,13 +102,71 @@ __global__ void label_scatter(const int32_t *__restrict__ label, int64_t nl, int
 
 }  // namespace
 
+// Default visiting order: the heavy rows (degree > kHeavyDeg) spread one per 32 positions at the front —
+// one per dynamic claim of the hop kernels (8 groups of 4 rows) — and the light rows in natural order around
+// them. A warp that claims a hub gets 31 light rows with it, and no hub is left for the end of a launch
+// (the tail a power-law degree sequence otherwise leaves). Pure scheduling: every row's arithmetic and
+// output are unchanged (bit-identical for any order).
+constexpr int kHeavyDeg = 256;
+
+__global__ void heavy_flags(const int32_t *__restrict__ deg, int64_t nl, int32_t *__restrict__ flag) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nl) flag[i] = deg[i] > kHeavyDeg ? 1 : 0;
+}
+
+__global__ void heavy_place(const int32_t *__restrict__ flag, const int64_t *__restrict__ hrank, int64_t nl,
+                            int64_t H, int32_t *__restrict__ order) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nl) return;
+    const int64_t h = hrank[i];   // heavy rows before row i
+    int64_t pos;
+    if (flag[i]) {
+        pos = 32 * h;
+    } else {
+        const int64_t j = i - h;   // light index
+        pos = j < 31 * H ? j + j / 31 + 1 : j + H;
+    }
+    order[pos] = (int32_t)i;
+}
+
 raftgp_status compute_order(raftgp_graph g) {
     static const int rounds = [] {
         const char *e = getenv("RAFTGP_ORDER_ROUNDS");
         return e ? atoi(e) : 0;   // off by default: measured gain < cost at C4
     }();
     raftgp_ctx ctx = g->ctx;
-    if (rounds <= 0 || g->nl == 0) return RAFTGP_OK;
+    if (g->nl == 0) return RAFTGP_OK;
+    if (rounds <= 0) {
+        static const bool spread = [] {   // RAFTGP_HEAVY_SPREAD=0: natural order
+            const char *e = getenv("RAFTGP_HEAVY_SPREAD");
+            return !(e && e[0] == '0');
+        }();
+        if (!spread) return RAFTGP_OK;
+        cudaStream_t st = ctx->stream;
+        const int64_t nl = g->nl;
+        int32_t *flag = nullptr;
+        int64_t *hrank = nullptr;
+        RG_TRY(dalloc_t(ctx, &flag, (size_t)nl));
+        RG_TRY(dalloc_t(ctx, &hrank, (size_t)nl + 1));
+        const unsigned grid = (unsigned)ceil_div(nl, 256);
+        {
+            LaunchScope L(ctx, K_ORDER);
+            heavy_flags<<<grid, 256, 0, st>>>(g->deg_local, nl, flag);
+        }
+        RG_CHECK_LAUNCH(ctx);
+        RG_TRY(scan_i32_to_i64(ctx, flag, hrank, nl));
+        int64_t H = 0;
+        RG_TRY(dread(ctx, &H, hrank + nl, sizeof(int64_t), st));
+        if (H > 0) {
+            if (g->order == nullptr) RG_TRY(dalloc_t(ctx, &g->order, (size_t)nl));
+            LaunchScope L(ctx, K_ORDER);
+            heavy_place<<<grid, 256, 0, st>>>(flag, hrank, nl, H, g->order);
+        }
+        RG_CHECK_LAUNCH(ctx);
+        dfree(ctx, flag);
+        dfree(ctx, hrank);
+        return RAFTGP_OK;
+    }
     cudaStream_t st = ctx->stream;
     const int64_t nl = g->nl, n = g->n;
     int32_t *label = nullptr, *cnt = nullptr;
