@@ -551,6 +551,64 @@ __device__ __forceinline__ int warp_sort_dedup(int32_t *a, int len, int32_t *out
     return written;
 }
 
+// in-place ascending warp sort of a[0..len) (registers up to 128 values, shared-memory bitonic beyond)
+template <int E>
+__device__ __forceinline__ void warp_sort_reg_inplace(int32_t *a, int len, int lane) {
+    int32_t v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = (e * 32 + lane < len) ? a[e * 32 + lane] : INT_MAX;
+#pragma unroll
+    for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j >= 1; j >>= 1) {
+            if (j >= 32) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int e2 = e ^ (j >> 5);
+                    if (e2 > e) {
+                        const bool up = (((e * 32 + lane) & k) == 0);
+                        const int32_t lo = min(v[e], v[e2]), hi = max(v[e], v[e2]);
+                        v[e] = up ? lo : hi;
+                        v[e2] = up ? hi : lo;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int32_t o = __shfl_xor_sync(0xffffffffu, v[e], j);
+                    const bool up = (((e * 32 + lane) & k) == 0);
+                    const bool lower = ((lane & j) == 0);
+                    v[e] = (lower == up) ? min(v[e], o) : max(v[e], o);
+                }
+            }
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+        if (e * 32 + lane < len) a[e * 32 + lane] = v[e];
+    __syncwarp();
+}
+
+__device__ __forceinline__ void warp_sort_inplace(int32_t *a, int len, int lane) {
+    if (len <= 1) return;
+    if (len <= 32) {
+        int32_t v = lane < len ? a[lane] : INT_MAX;
+        v = warp_sort32(v, lane);
+        __syncwarp();
+        if (lane < len) a[lane] = v;
+        __syncwarp();
+    } else if (len <= 64) {
+        warp_sort_reg_inplace<2>(a, len, lane);
+    } else if (len <= 128) {
+        warp_sort_reg_inplace<4>(a, len, lane);
+    } else {
+        bitonic_any(a, len, lane, 32, WarpSync());
+    }
+}
+
+constexpr int kSubAvg = 48;   // mean entries per value sub-range when a long row is split for sorting
+
 template <bool PACKED>
 __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PACKED>::T *__restrict__ pairs,
                                                         const int64_t *__restrict__ base, int pgrid,
@@ -564,7 +622,8 @@ __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PAC
     int32_t *cur = bsm + kBucketCap;                    // B cursors (first: the row counts)
     int32_t *off = cur + kMaxBucketRows;                // B + 1 offsets (relative to the bucket start)
     int32_t *big = off + kMaxBucketRows + 1;            // rows longer than 32, longest work first
-    __shared__ int fb_base, nbig, qnext;
+    __shared__ int fb_base, nbig, qnext, tail;
+    __shared__ int gtmp[8];
     __shared__ int64_t scan_sh[32];
     const int lane = threadIdx.x & 31;
     constexpr int kLoadBatch = 8;
@@ -583,6 +642,7 @@ __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PAC
         if (threadIdx.x == 0) {
             nbig = 0;
             qnext = 0;
+            tail = (int)min(E, (int64_t)kBucketCap);   // free shared memory after the bucket's entries
         }
         for (int t = threadIdx.x; t < nr; t += blockDim.x) cur[t] = 0;
         __syncthreads();
@@ -649,7 +709,54 @@ __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PAC
                 const int t = big[q];
                 int32_t *a = s + off[t];
                 const int len = off[t + 1] - off[t];
-                bitonic_any(a, len, gt, 128, gsync);
+                // split by value into ~len/48 sub-ranges (ids are spread over [0, 2^vbits)), then one warp sorts
+                // each sub-range in registers; the bucket's free shared memory holds the counts and a copy.
+                // Equal values share a sub-range, so the row ends up fully sorted. No room: plain bitonic.
+                const int nsub = (len + kSubAvg - 1) / kSubAvg;
+                if (gt == 0) gtmp[grp] = atomicAdd(&tail, nsub + len);
+                gsync();
+                const int tb = gtmp[grp];
+                if (tb + nsub + len <= kBucketCap) {
+                    int32_t *cnt = s + tb, *tmp = cnt + nsub;
+                    const int gw = gt >> 5;
+                    auto sub_of = [&](int32_t v) {
+                        return (int)(((uint64_t)(uint32_t)v * (uint64_t)nsub) >> vbits);
+                    };
+                    for (int k = gt; k < nsub; k += 128) cnt[k] = 0;
+                    gsync();
+                    for (int i = gt; i < len; i += 128) atomicAdd(&cnt[sub_of(a[i])], 1);
+                    gsync();
+                    if (gw == 0) {   // exclusive scan of the counts (one warp)
+                        int run = 0;
+                        for (int k0 = 0; k0 < nsub; k0 += 32) {
+                            const int k = k0 + lane;
+                            const int c = k < nsub ? cnt[k] : 0;
+                            int x = c;
+#pragma unroll
+                            for (int o = 1; o < 32; o <<= 1) {
+                                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                                if (lane >= o) x += y;
+                            }
+                            if (k < nsub) cnt[k] = run + x - c;
+                            run += __shfl_sync(0xffffffffu, x, 31);
+                        }
+                    }
+                    gsync();
+                    for (int i = gt; i < len; i += 128) {
+                        const int32_t v = a[i];
+                        tmp[atomicAdd(&cnt[sub_of(v)], 1)] = v;
+                    }
+                    gsync();
+                    // cnt[k] now ends sub-range k; sort each range into place
+                    for (int k = gw; k < nsub; k += 4) {
+                        const int b0 = k ? cnt[k - 1] : 0, b1 = cnt[k];
+                        warp_sort_inplace(tmp + b0, b1 - b0, lane);
+                        for (int i = b0 + lane; i < b1; i += 32) a[i] = tmp[i];
+                    }
+                    gsync();
+                } else {
+                    bitonic_any(a, len, gt, 128, gsync);
+                }
                 // dedup: running count over 128-wide chunks (group-shared partial counts in `cur`)
                 int written = 0;
                 for (int base = 0; base < len; base += 128) {
