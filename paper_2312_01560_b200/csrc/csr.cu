@@ -326,7 +326,10 @@ constexpr int kPartUnroll = RG_PART_UNROLL;   // edge loads in flight per thread
 constexpr int kMaxBuckets = 12288;      // partition smem: 12 B per bucket
 constexpr int kMaxBucketRows = 4096;    // bucket_sort smem for row cursors/offsets
 constexpr int kBucketCap = 44032;       // entries of one bucket held in shared memory (172 KB)
-constexpr int kGroupRow = 256;          // rows longer than this are sorted by a group of 4 warps
+#ifndef RG_GROUP_ROW
+#define RG_GROUP_ROW 128
+#endif
+constexpr int kGroupRow = RG_GROUP_ROW;   // rows longer than this are sorted by a group of 4 warps
 
 // Bucket entries: (row within the bucket, neighbour id). PACKED = one 32-bit word (row << vbits | id) when
 // log2(B) + vbits <= 32 (C4: 9 + 23 bits), else an int2.
@@ -607,7 +610,10 @@ __device__ __forceinline__ void warp_sort_inplace(int32_t *a, int len, int lane)
     }
 }
 
-constexpr int kSubAvg = 48;   // mean entries per value sub-range when a long row is split for sorting
+#ifndef RG_SUB_AVG
+#define RG_SUB_AVG 32
+#endif
+constexpr int kSubAvg = RG_SUB_AVG;   // mean entries per value sub-range when a long row is split for sorting
 
 template <bool PACKED>
 __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PACKED>::T *__restrict__ pairs,
