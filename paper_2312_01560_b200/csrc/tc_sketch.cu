@@ -7,7 +7,7 @@
 // mantissa bits cleared, lo = x - hi exactly): A B ~ A_hi B_hi + A_hi B_lo + A_lo B_hi, accumulated in fp32
 // in TMEM (error ~2^-20 relative, far inside the 1e-4 parity bar).
 //
-// Per CTA (512 threads, one per SM): a persistent loop over 128-row tiles. For each tile and each
+// Per CTA (1024 threads, one per SM): a persistent loop over 128-row tiles. For each tile and each
 // K-half of at most 64 columns: all threads generate Theta (one Philox call -> 4 normals -> one 16-byte
 // K-chunk) and store hi/lo in the canonical no-swizzle K-major layout (8-row x 16-byte core matrices);
 // one thread issues tcgen05.mma (M = 128, N = L1, K = 8) x 3 products per K-step into the TMEM
@@ -30,7 +30,7 @@ namespace {
 using namespace tc;
 
 #ifndef RG_TC_THREADS
-#define RG_TC_THREADS 512
+#define RG_TC_THREADS 1024
 #endif
 constexpr int kTM = 128;       // rows per tile (MMA M)
 constexpr int kKH = 64;        // K columns per half (A buffer)
