@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--exchange", default="push", choices=["push", "allgather"],
                     help="N > 1: per-hop exchange fused into the producing kernels (peer stores through CUDA IPC) "
                          "or NCCL all-gathers pipelined across variants")
-    ap.add_argument("--e2e-api", default="separate", choices=["separate", "build_embed"],
+    ap.add_argument("--e2e-api", default="build_embed", choices=["separate", "build_embed"],
                     help="e2e step: raftgp_build_csr + raftgp_embed_multi, or raftgp_build_embed")
     ap.add_argument("--no-stream", action="store_true", help="skip the NEXT-4 streaming-update measurement")
     ap.add_argument("--clock-period-ms", type=int, default=200)
