@@ -46,6 +46,23 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     return out
 
 
+DEMO_SRC = os.path.join(os.path.dirname(HERE), "examples", "raftgp_demo.c")
+DEMO = os.path.join(os.path.dirname(HERE), "examples", "raftgp_demo")
+
+
+def build_demo(force: bool = False) -> str:
+    """gcc the plain-C example of the C-ABI (examples/raftgp_demo.c) against the in-tree library."""
+    if not force and os.path.exists(DEMO) and os.path.getmtime(DEMO) > max(os.path.getmtime(DEMO_SRC),
+                                                                             os.path.getmtime(LIB)):
+        return DEMO
+    cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    cmd = [os.environ.get("CC", "gcc"), "-O2", "-std=c99", "-Wall", DEMO_SRC, "-I", INCLUDE,
+           "-I", os.path.join(cuda, "include"), "-L", HERE, "-lraftgp", "-L", os.path.join(cuda, "lib64"), "-lcudart",
+           "-lm", "-Wl,-rpath,$ORIGIN/../paper_2312_01560_b200", f"-Wl,-rpath,{os.path.join(cuda, 'lib64')}", "-o", DEMO]
+    subprocess.check_call(cmd)
+    return DEMO
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose="-v" in sys.argv)
     print(LIB)
