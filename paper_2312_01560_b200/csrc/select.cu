@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) sel_rows(const float *__restri
         __syncwarp();
         if (lane < rows) {
             s = pseg[b + lane];
-            bulk_row(stage + ((size_t)buf * 32 + lane) * LD, Z + (size_t)perm[b + lane] * L, RB, &bar[buf]);
+            bulk_row(stage + ((size_t)buf * 32 + lane) * LD, Z + (size_t)(b + lane) * L, RB, &bar[buf]);   // Z in position order
         }
         sb[buf] = s;
     };
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(kPruneWarps * 32, 3) sel_lloyd_pruned(const fl
         if (lane < k) {
             pos = q[lane];
             s = pseg[pos];
-            bulk_row(stage + lane * LD, Z + (size_t)perm[pos] * L, RB, bar);
+            bulk_row(stage + lane * LD, Z + (size_t)pos * L, RB, bar);   // Z in position order
         }
         mbar_wait(bar, ph);
         ph ^= 1u;
@@ -746,6 +746,20 @@ __global__ void sel_canon(const int32_t *__restrict__ label_tmp, const int32_t *
     if (i < n) labels[i] = (int32_t)frank[bmin[label_tmp[i]]];
 }
 
+// Z in the level's position order (Zp[pos] = Z[perm[pos]]), so the row passes read rows by position: no
+// perm indirection in their dependent load chains, and the rows a pruned pass recomputes (clustered near the
+// split) are close together. One coalesced copy per level.
+template <int L>
+__global__ void sel_gather_rows(const float *__restrict__ Z, const int32_t *__restrict__ perm, int64_t n_act,
+                                float *__restrict__ Zp) {
+    constexpr int Q = L / 4;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_act * Q) return;
+    const int64_t pos = t / Q;
+    const int c = (int)(t % Q);
+    reinterpret_cast<float4 *>(Zp)[t] = __ldg(reinterpret_cast<const float4 *>(Z + (size_t)perm[pos] * L) + c);
+}
+
 __global__ void fill_i32(int32_t *p, int64_t n, int32_t v) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
@@ -792,6 +806,8 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
     RG_TRY(dalloc_t(ctx, &bmin, n));
     RG_TRY(dalloc_t(ctx, &ones, n + 1));
     RG_TRY(dalloc_t(ctx, &dpos, n));
+    float *Zp = nullptr;   // Z in position order (rebuilt per level)
+    RG_TRY(dalloc_t(ctx, &Zp, (size_t)std::max<int64_t>(n, 1) * L));
     float2 *bnd = reinterpret_cast<float2 *>(dpos);   // seeding distances, then the Lloyd pruning bounds
     RG_TRY(dalloc_t(ctx, &err, 1));
     RG_TRY(dalloc_t(ctx, &active, 2 + 64));   // [0] active segments, [1] their rows, [2..65] rows read
@@ -838,6 +854,10 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
 
     while (S > 0 && rc == RAFTGP_OK) {
         ++levels;
+        if (n_act > 0) {
+            LaunchScope LS(ctx, K_SEL_SEED);
+            sel_gather_rows<L><<<grid_for(n_act * (L / 4), 256), 256, 0, st>>>(Z, perm, n_act, Zp);
+        }
         // per-segment state of this level
         SegState ss{};
         unsigned long long *nsz = nullptr, *mbar = nullptr, *cut = nullptr;
@@ -871,7 +891,7 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
         // seeding: mean, farthest from the mean, farthest from that
         if (levels == 1) {
             LaunchScope LS(ctx, K_SEL_SEED);
-            sel_rows<L, 0><<<rgrid, kRowWarps * 32, kRowSmem, st>>>(Z, perm, pseg, side, bnd, dpos, n_act, ss, err,
+            sel_rows<L, 0><<<rgrid, kRowWarps * 32, kRowSmem, st>>>(Zp, perm, pseg, side, bnd, dpos, n_act, ss, err,
                                                                     active + 2);
         }
         RG_CHECK_LAUNCH(ctx);
@@ -889,7 +909,7 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
         for (int slot = 0; slot < 2 && rc == RAFTGP_OK; ++slot) {
             {
                 LaunchScope LS(ctx, K_SEL_SEED);
-                sel_rows<L, 2><<<rgrid, kRowWarps * 32, kRowSmem, st>>>(Z, perm, pseg, side, bnd, dpos, n_act, ss,
+                sel_rows<L, 2><<<rgrid, kRowWarps * 32, kRowSmem, st>>>(Zp, perm, pseg, side, bnd, dpos, n_act, ss,
                                                                         err, active + 2);
             }
             RG_CHECK_LAUNCH(ctx);
@@ -918,10 +938,10 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
                 {
                     LaunchScope LS(ctx, K_SEL_LLOYD);
                     if (t == 1)
-                        sel_rows<L, 1><<<rgrid, kRowWarps * 32, kRowSmem, st>>>(Z, perm, pseg, side, bnd, dpos, n_act,
+                        sel_rows<L, 1><<<rgrid, kRowWarps * 32, kRowSmem, st>>>(Zp, perm, pseg, side, bnd, dpos, n_act,
                                                                                 ss, err, active + 2);
                     else
-                        sel_lloyd_pruned<L><<<qgrid, kPruneWarps * 32, kPruneSmem, st>>>(Z, perm, pseg, side, bnd,
+                        sel_lloyd_pruned<L><<<qgrid, kPruneWarps * 32, kPruneSmem, st>>>(Zp, perm, pseg, side, bnd,
                                                                                        n_act, ss, active + 2, prev,
                                                                                        claims + t);
                 }
@@ -1033,6 +1053,7 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
     dfree(ctx, lvl_cnt);
     dfree(ctx, iter_act);
     dfree(ctx, claims);
+    dfree(ctx, Zp);
     dfree(ctx, perm); dfree(ctx, pseg); dfree(ctx, side); dfree(ctx, nperm); dfree(ctx, npseg);
     dfree(ctx, node_key); dfree(ctx, label_tmp); dfree(ctx, bmin); dfree(ctx, ones); dfree(ctx, dpos); dfree(ctx, err);
     unsigned long long h_read[64] = {0};
