@@ -23,6 +23,7 @@ row, and one stream-ordered barrier (a 1-element all-reduce) separates producing
 """
 from __future__ import annotations
 
+import os
 from typing import Generator, List, Optional, Sequence
 
 import torch
@@ -222,6 +223,8 @@ class PushBuffers:
 
     def __init__(self, ctx: rg.Context, group=None):
         self.ctx, self.group, self.key, self.own, self.maps = ctx, group, None, {}, {}
+        self.mapped = True   # False: some rank could not map a peer; copies are completed by all-gathers
+        self.tensors = {}
 
     def get(self, info) -> dict:
         import torch.distributed as dist
@@ -237,9 +240,31 @@ class PushBuffers:
             handles[(v, k)] = buf.handle_bytes()
         allh = [None] * world
         dist.all_gather_object(allh, handles, group=self.group)
-        for vk in handles:
-            self.maps[vk] = [self.own[vk].ptr if q == rank else rg.raftgp_ipc_open(self.ctx, allh[q][vk])
-                             for q in range(world)]
+        opened, ok = {}, os.environ.get("RAFTGP_PUSH_NOIPC") != "1"   # test hook: force the fallback
+        try:
+            for vk in (handles if ok else []):
+                opened[vk] = [self.own[vk].ptr if q == rank else rg.raftgp_ipc_open(self.ctx, allh[q][vk])
+                              for q in range(world)]
+        except rg.RaftGPError:
+            ok = False
+        oks = [None] * world
+        dist.all_gather_object(oks, ok, group=self.group)
+        self.mapped = all(oks)
+        if self.mapped:
+            self.maps = opened
+        else:   # no peer mapping on this box: every rank keeps only its own copy (all-gathered at barriers)
+            for vk, ptrs in opened.items():
+                for q, p in enumerate(ptrs):
+                    if q != rank and p:
+                        rg.raftgp_ipc_close(self.ctx, p)
+            torch.cuda.synchronize(self.ctx.device)
+            dist.barrier(group=self.group)   # every mapping is gone before any rank frees its buffers
+            for b in self.own.values():
+                b.close()
+            self.own = {}
+            self.tensors = {(v, k): torch.zeros((max(1, info["n"]), w), dtype=torch.float32, device=self.ctx.device)
+                            for v, k, w in info["spec"]}
+            self.maps = {vk: [t.data_ptr()] for vk, t in self.tensors.items()}
         self.key = key
         dist.barrier(group=self.group)
         return self.maps
@@ -247,7 +272,7 @@ class PushBuffers:
     def close(self):
         """Unmap the peers' copies, wait until every rank has done so, then free this rank's copies."""
         import torch.distributed as dist
-        if self.maps:
+        if self.maps and self.mapped:
             rank = dist.get_rank(self.group)
             for ptrs in self.maps.values():
                 for q, p in enumerate(ptrs):
@@ -258,7 +283,7 @@ class PushBuffers:
             dist.barrier(group=self.group)
         for b in self.own.values():
             b.close()
-        self.key, self.own, self.maps = None, {}, {}
+        self.key, self.own, self.maps, self.tensors, self.mapped = None, {}, {}, {}, True
 
 
 def run_distributed(gen: Generator, group=None, push: Optional[PushBuffers] = None):
@@ -293,7 +318,17 @@ def run_distributed(gen: Generator, group=None, push: Optional[PushBuffers] = No
                               for v, k, w in payload["spec"]}
                 reply = cpu_copies
         elif kind == "barrier":
-            if push is not None:
+            if push is not None and not push.mapped:
+                # fallback without peer mappings: complete this rank's copies with all-gathers of the row blocks
+                rank = dist.get_rank(group)
+                rb, re = info["ranges"][rank]
+                nccl = dist.get_backend(group) == "nccl"
+                for vk in payload:
+                    full = push.tensors[vk][: info["n"]]
+                    mine = _pad(full[rb:re], info["R"])
+                    blocks = _start(mine if nccl else mine.cpu()).result()   # gloo: host all-gather
+                    full.copy_(blocks[: info["n"]])
+            elif push is not None:
                 if dist.get_backend(group) == "nccl":
                     flag = torch.zeros(1, dtype=torch.float32, device=push.ctx.device)
                     dist.all_reduce(flag, group=group)   # stream-ordered: every rank's producing kernels are done

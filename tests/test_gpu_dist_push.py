@@ -23,7 +23,9 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n, src, dst, variants, dims, seed, out):
+def _worker(rank, world, port, n, src, dst, variants, dims, seed, out, noipc=False):
+    if noipc:
+        os.environ["RAFTGP_PUSH_NOIPC"] = "1"
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -38,13 +40,16 @@ def _worker(rank, world, port, n, src, dst, variants, dims, seed, out):
             Z = rdist.run_distributed(gen, push=push)
             torch.cuda.synchronize()
             out[(rank, rep)] = {v: Z[v].cpu().numpy() for v in Z}
+            out[("mapped", rank)] = push.mapped
         push.close()
     finally:
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("noipc", [False, True])
 @pytest.mark.parametrize("world", [2])
-def test_ipc_push_two_processes(cuda_required, world):
+def test_ipc_push_two_processes(cuda_required, world, noipc):
+    """noipc: peer mapping made to fail on every rank -> the copies are completed by all-gathers instead."""
     import synth
     from paper_2312_01560_b200 import raftgp as rg
     gr = synth.generate("C2", 1, n=20000)
@@ -52,12 +57,13 @@ def test_ipc_push_two_processes(cuda_required, world):
     variants = ["ncut", "mod"]
     mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
-    mp.start_processes(_worker, args=(world, _free_port(), gr.n, gr.src, gr.dst, variants, dims, 5, out),
+    mp.start_processes(_worker, args=(world, _free_port(), gr.n, gr.src, gr.dst, variants, dims, 5, out, noipc),
                        nprocs=world, join=True, start_method="spawn")
     from paper_2312_01560_b200 import dist as rdist
     ctx = rg.Context(0)
     Z = rdist.run_loopback([rdist.rank_pipeline(rdist.CudaEngine(ctx), gr.n, torch.from_numpy(gr.src).cuda(),
                                                 torch.from_numpy(gr.dst).cuda(), 0, 1, variants, dims, 5)])[0]
+    assert all(out[("mapped", r)] == (not noipc) for r in range(world))
     for rep in range(2):
         for v in variants:
             got = np.concatenate([out[(r, rep)][v] for r in range(world)], 0)
