@@ -258,6 +258,7 @@ struct WideArgs {
     float *zhi, *zlo;        // GCN: Z split and tiled as the next GEMM's A operand (may be null)
     float *ssq;              // GCN, deferred normalisation: per-row, per-slice sums of squares (n x NW) or null
     unsigned long long *ctr; // zeroed row counter: CTAs claim rows dynamically (degree skew), or null (grid-stride)
+    const int32_t *order;    // visiting order of the rows (heavy rows spread, order.cu), or null
 };
 
 template <int KIND, int V, int U>
@@ -279,8 +280,9 @@ __global__ void __launch_bounds__(512) hop_wide(WideArgs a) {
             r0 = claim;
         }
         if (r0 >= a.n) break;
-        const int64_t i = r0 + rsub;
-        const bool valid = i < a.n;
+        const int64_t ii = r0 + rsub;
+        const bool valid = ii < a.n;
+        const int64_t i = (valid && a.order) ? (int64_t)__ldg(a.order + ii) : ii;
         float4 acc[V], acc2[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) acc[v] = acc2[v] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -874,6 +876,7 @@ raftgp_status embed_wide(raftgp_graph g, int32_t nvariants, const int32_t *varia
             WideArgs a{};
             a.n = n; a.row_ptr = g->row_ptr; a.col = g->col; a.X = thw; a.s_all = g->s_all; a.sh_all = g->sh_all;
             a.deg_all = g->deg_all; a.gvec = gw; a.inv2e = g->two_e > 0 ? 1.0 / (double)g->two_e : 0.0; a.W = l1;
+            a.order = g->order;
             if (dual) {
                 a.out = T1[where[RAFTGP_NCUT]];
                 a.out2 = T1[where[RAFTGP_MOD]];
@@ -936,6 +939,7 @@ raftgp_status embed_wide(raftgp_graph g, int32_t nvariants, const int32_t *varia
                     WideArgs a{};
                     a.n = n; a.row_ptr = g->row_ptr; a.col = g->col; a.X = T; a.s_all = g->s_all; a.sh_all = g->sh_all;
                     a.deg_all = g->deg_all; a.W = w; a.out = last ? Z_dev[v] : nullptr; a.zhi = zhi; a.zlo = zlo;
+                    a.order = g->order;
                     const int nw = wide_ssq_slices(w);
                     if (!last) {   // deferred row normalisation: y = tanh(.) tiled, 1/||y|| goes to the GEMM row scale
                         st = take(reinterpret_cast<void **>(&a.ssq), (size_t)n * nw * 4);
