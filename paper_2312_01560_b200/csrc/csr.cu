@@ -1047,13 +1047,22 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
         return fail(RAFTGP_ERR_DATA, "build_csr: node id outside [0, n)");
     }
     g->nnz_local = nnz;
-    RG_TRY(dalloc_t(ctx, &g->col, nnz));
-    if (nl > 0 && nnz > 0) {
-        LaunchScope L(ctx, K_CSR_COMPACT);
-        const int cgrid = static_cast<int>(std::min<int64_t>(ceil_div(nl, 8), (int64_t)ctx->sm_count * 16));
-        csr_compact<<<cgrid, 256, 0, st>>>(nl, raw_ptr, col_raw, g->row_ptr, g->col);
+    // without duplicate pairs every row kept all its raw entries: the raw layout IS the CSR (no compaction)
+    int64_t raw_total = 0;
+    if (nl > 0) RG_TRY(dread(ctx, &raw_total, raw_ptr + nl, sizeof(int64_t), st));
+    const bool no_dups = raw_total == nnz;
+    if (no_dups) {
+        g->col = col_raw;
+        col_raw = nullptr;
+    } else {
+        RG_TRY(dalloc_t(ctx, &g->col, nnz));
+        if (nl > 0 && nnz > 0) {
+            LaunchScope L(ctx, K_CSR_COMPACT);
+            const int cgrid = static_cast<int>(std::min<int64_t>(ceil_div(nl, 8), (int64_t)ctx->sm_count * 16));
+            csr_compact<<<cgrid, 256, 0, st>>>(nl, raw_ptr, col_raw, g->row_ptr, g->col);
+        }
+        RG_CHECK_LAUNCH(ctx);
     }
-    RG_CHECK_LAUNCH(ctx);
     dfree(ctx, cnt);
     dfree(ctx, raw_ptr);
     dfree(ctx, col_raw);
