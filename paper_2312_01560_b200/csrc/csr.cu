@@ -814,12 +814,31 @@ __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PAC
 
 __global__ void csr_compact(int64_t nl, const int64_t *__restrict__ raw_ptr, const int32_t *__restrict__ col_raw,
                             const int64_t *__restrict__ row_ptr, int32_t *__restrict__ col) {
+    // a warp takes 32 consecutive rows: their offsets are loaded once, coalesced (lane = row), then the rows
+    // are copied one after the other with the offsets broadcast by shuffle, two rows' loads in flight
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < nl; row += warps) {
-        const int64_t src = raw_ptr[row], dst = row_ptr[row];
-        const int len = static_cast<int>(row_ptr[row + 1] - dst);
-        for (int x = lane; x < len; x += 32) col[dst + x] = col_raw[src + x];
+    for (int64_t r0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; r0 < nl; r0 += warps * 32) {
+        const int64_t row = r0 + lane;
+        int64_t src = 0, dst = 0;
+        int len = 0;
+        if (row < nl) {
+            src = raw_ptr[row];
+            dst = row_ptr[row];
+            len = static_cast<int>(row_ptr[row + 1] - dst);
+        }
+        for (int j = 0; j < 32; j += 2) {
+            const int64_t s0 = __shfl_sync(0xffffffffu, src, j), d0 = __shfl_sync(0xffffffffu, dst, j);
+            const int64_t s1 = __shfl_sync(0xffffffffu, src, j + 1), d1 = __shfl_sync(0xffffffffu, dst, j + 1);
+            const int l0 = __shfl_sync(0xffffffffu, len, j), l1 = __shfl_sync(0xffffffffu, len, j + 1);
+            const int lm = max(l0, l1);
+            for (int x = lane; x < lm; x += 32) {
+                const int32_t a = x < l0 ? col_raw[s0 + x] : 0;
+                const int32_t b = x < l1 ? col_raw[s1 + x] : 0;
+                if (x < l0) col[d0 + x] = a;
+                if (x < l1) col[d1 + x] = b;
+            }
+        }
     }
 }
 
@@ -1058,7 +1077,7 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
         RG_TRY(dalloc_t(ctx, &g->col, nnz));
         if (nl > 0 && nnz > 0) {
             LaunchScope L(ctx, K_CSR_COMPACT);
-            const int cgrid = static_cast<int>(std::min<int64_t>(ceil_div(nl, 8), (int64_t)ctx->sm_count * 16));
+            const int cgrid = static_cast<int>(std::min<int64_t>(ceil_div(nl, 256), (int64_t)ctx->sm_count * 16));
             csr_compact<<<cgrid, 256, 0, st>>>(nl, raw_ptr, col_raw, g->row_ptr, g->col);
         }
         RG_CHECK_LAUNCH(ctx);
