@@ -603,18 +603,22 @@ def main():
         ach = b_step / t_step / 1e9
         hop_stats[k] = {"gb_s": ach, "ms_per_step": t_step * 1e3, "launches_per_step": prof[k][1] / args.steps,
                         "bytes_per_launch": b_step / l_step}
-    traffic = None
+    traffic, ncu_counters = None, None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if dom and os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get(args.config, {}).get(dom)
+            tj = json.load(open(tfile)).get(args.config, {})
+            traffic, ncu_counters = tj.get(dom), tj.get(dom + "_ncu")
+            if ncu_counters is not None:
+                ncu_counters = dict(ncu_counters, source=tj.get("_source"))
         except Exception:
             traffic = None
     if dom:
         ach = hop_stats[dom]["gb_s"]
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "peak_source": peak_src, "frac_of_8TBs_nominal": ach / 8000.0, "traffic": traffic,
-                "bytes_per_launch": hop_stats[dom]["bytes_per_launch"]}
+                "bytes_per_launch": hop_stats[dom]["bytes_per_launch"],
+                "ncu": ncu_counters}   # L2 hit rate, sectors per request, DRAM % of nominal (one ncu --set full)
         if traffic:
             # the DRAM view: ncu's measured bytes per launch over this run's event-timed launch duration (the
             # gather-model bytes above count L2 hits as traffic, so frac can exceed the DRAM-side fraction)

@@ -13,7 +13,7 @@ raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_outpu
 rows = list(csv.reader(raw.splitlines()))
 hdr, units, data = rows[0], rows[1], rows[2:]
 mul = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
-fam = {}
+fam, extra = {}, {}
 for d in data:
     name = d[hdr.index("Kernel Name")]
     if "hop_kernel<" not in name:
@@ -24,11 +24,21 @@ for d in data:
     for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
         b += float(d[hdr.index(m)].replace(",", "")) * mul[units[hdr.index(m)]]
     fam.setdefault(key, []).append(b)
+
+    def val(m):
+        return float(d[hdr.index(m)].replace(",", "")) if m in hdr and d[hdr.index(m)] else None
+    sec, req = val("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum"), val("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum")
+    extra.setdefault(key, []).append({"l2_hit_rate_pct": val("lts__t_sector_hit_rate.pct"),
+                                      "sectors_per_request": (sec / req) if sec and req else None,
+                                      "dram_pct_of_nominal_peak": val("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")})
 try:
     js = json.load(open(out))
 except Exception:
     js = {}
 js[cfg] = {k: sum(v) / len(v) for k, v in fam.items()}
+for k, lst in extra.items():   # per-launch counters averaged per family
+    js[cfg][k + "_ncu"] = {m: (sum(e[m] for e in lst if e[m] is not None) / max(1, sum(e[m] is not None for e in lst)))
+                           for m in lst[0]}
 js[cfg]["_source"] = rep
 json.dump(js, open(out, "w"), indent=1)
 print(js[cfg])
