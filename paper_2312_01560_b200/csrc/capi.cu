@@ -1082,7 +1082,7 @@ raftgp_status raftgp_build_embed(raftgp_ctx ctx, int64_t n, int64_t m, const int
             st = check_variant(g, variants[v], r);
             if (st == RAFTGP_OK && where[variants[v]] >= 0) st = fail(RAFTGP_ERR_PARAM, "variant listed twice");
             if (st == RAFTGP_OK) where[variants[v]] = v;
-            if (st == RAFTGP_OK && !Z_dev[v]) st = fail(RAFTGP_ERR_PARAM, "null Z");
+            if (st == RAFTGP_OK && !Z_dev[v] && g->nl > 0) st = fail(RAFTGP_ERR_PARAM, "null Z");
         }
         if (st == RAFTGP_OK) {
             if (overlap) st = embed_pre(g, nvariants, variants, layers, dims, seed, Z_dev, where, thw);

@@ -86,3 +86,35 @@ def test_handles_outlive_context(rg):
     g1.close()
     s.close()
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("n,src,dst", [(0, [], []), (1, [], []), (3, [0, 1], [1, 1]), (5, [0, 0, 3], [1, 1, 4])])
+@pytest.mark.parametrize("dims", [(64, 64, 32), (48, 40, 24), (256, 128, 64)])
+def test_build_embed_degenerate(rg, ctx, n, src, dst, dims):
+    """raftgp_build_embed on empty / one-node / self-loop / duplicate-edge graphs, at fused (tcgen05 side-stream),
+    generic and Table I-style widths: same result as the separate calls, and within 1e-4 of the oracle."""
+    s, d = torch.tensor(src, dtype=torch.int32), torch.tensor(dst, dtype=torch.int32)
+    Z1, _ = rg.raftgp_build_embed(ctx, n, s, d, ["ncut", "mod"] if n > 1 else ["ncut"], dims, 2)
+    g = _g(rg, ctx, n, src, dst)
+    variants = ["ncut", "mod"] if n > 1 else ["ncut"]
+    _, Z2 = rg.raftgp_embed_multi(g, variants, dims, 2)
+    for v in variants:
+        assert torch.equal(Z1[v], Z2[v])
+        assert Z1[v].shape == (n, dims[-1])
+        if n:
+            go = oracle.build_csr(n, np.array(src, np.int32), np.array(dst, np.int32))
+            if v == "mod" and go.row_ptr[-1] == 0:
+                continue
+            Zo = oracle.gcn_np(go, dims, 2, oracle.project(go, v, dims[0], 2))[-1]
+            assert np.allclose(Z1[v].cpu().numpy(), Zo, atol=1e-5)
+
+
+def test_build_embed_bad_ids(rg, ctx):
+    s = torch.tensor([0, 7], dtype=torch.int32)
+    d = torch.tensor([1, 2], dtype=torch.int32)
+    with pytest.raises(rg.RaftGPError):
+        rg.raftgp_build_embed(ctx, 5, s, d, ["ncut"], (64, 64, 32), 1)
+    # the context stays usable after the error
+    Z, _ = rg.raftgp_build_embed(ctx, 3, torch.tensor([0], dtype=torch.int32), torch.tensor([1], dtype=torch.int32),
+                                 ["ncut"], (64, 64, 32), 1)
+    assert Z["ncut"].shape == (3, 32)
