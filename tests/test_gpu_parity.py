@@ -384,3 +384,20 @@ def test_build_embed_equals_separate_calls(rg, ctx, variants):
     Z3, _ = rg.raftgp_build_embed(ctx, gr.n, torch.from_numpy(gr.src), torch.from_numpy(gr.dst), variants, dims, 3)
     for v in variants:
         assert torch.equal(Z3[v], Z2[v])
+
+
+@pytest.mark.parametrize("n,P", [(5, 3), (2, 3), (7, 4)])
+def test_partitioned_push_tiny(rg, ctx, n, P):
+    """Push mode with ragged and EMPTY rank partitions (n < P): the empty ranks still take part in every
+    exchange and the result equals the one-rank pipeline."""
+    from paper_2312_01560_b200 import dist
+    rng = np.random.default_rng(n * 10 + P)
+    src = rng.integers(0, n, 3 * n).astype(np.int32)
+    dst = rng.integers(0, n, 3 * n).astype(np.int32)
+    dims = (64, 64, 32)
+    eng = dist.CudaEngine(ctx)
+    gens = [dist.rank_pipeline_push(eng, n, _t(src), _t(dst), p, P, ["ncut", "mod"], dims, 4) for p in range(P)]
+    Zs = dist.run_loopback(gens, device=ctx.device)
+    one = dist.run_loopback([dist.rank_pipeline(eng, n, _t(src), _t(dst), 0, 1, ["ncut", "mod"], dims, 4)])[0]
+    for v in ("ncut", "mod"):
+        assert torch.equal(torch.cat([z[v] for z in Zs], 0), one[v]), v
