@@ -653,7 +653,66 @@ def main():
     e2e = None
     if not args.no_e2e:
         d2h = int(sum(rows * dims[-1] * 4 for _ in variants))
-        if world == 1 and not args.no_fuse_variants:
+        if world == 1 and not args.no_fuse_variants and args.e2e_lanes == 1:
+            # one compute stream (steps back to back, no kernel interleaving across steps) with the copies on
+            # their own streams: H2D of step k+1 and D2H of step k-1 run under step k's kernels; inputs and
+            # outputs double-buffered, ordered by events
+            cs = torch.cuda.Stream(dev)
+            hs, ds = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+            c1 = rg.Context(dev.index, stream=cs)
+            Din = [(torch.empty(m, dtype=torch.int32, device=dev), torch.empty(m, dtype=torch.int32, device=dev))
+                   for _ in range(2)]
+            Zb = [{v: torch.empty((rows, dims[-1]), dtype=torch.float32, device=dev) for v in variants}
+                  for _ in range(2)]
+            Hb = [{v: torch.empty((rows, dims[-1]), dtype=torch.float32).pin_memory() for v in variants}
+                  for _ in range(2)]
+            in_ready = [torch.cuda.Event() for _ in range(2)]
+            in_free = [torch.cuda.Event() for _ in range(2)]
+            out_free = [torch.cuda.Event() for _ in range(2)]
+            for b in range(2):
+                in_free[b].record(cs)
+                out_free[b].record(cs)
+
+            def h2d(k):
+                b = k % 2
+                hs.wait_event(in_free[b])
+                with torch.cuda.stream(hs):
+                    Din[b][0].copy_(src_h, non_blocking=True)
+                    Din[b][1].copy_(dst_h, non_blocking=True)
+                    in_ready[b].record(hs)
+
+            def run(nsteps):
+                h2d(0)
+                for k in range(nsteps):
+                    b = k % 2
+                    if k + 1 < nsteps:
+                        h2d(k + 1)
+                    cs.wait_event(in_ready[b])
+                    cs.wait_event(out_free[b])
+                    with torch.cuda.stream(cs):
+                        rg.raftgp_build_embed(c1, gr.n, Din[b][0], Din[b][1], variants, dims, args.seed, Z=Zb[b])
+                        in_free[b].record(cs)
+                    ds.wait_stream(cs)
+                    with torch.cuda.stream(ds):
+                        for v in variants:
+                            Hb[b][v].copy_(Zb[b][v], non_blocking=True)
+                        out_free[b].record(ds)
+
+            run(2)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(cs)
+            hs.wait_event(e0)
+            ds.wait_event(e0)
+            run(args.steps)
+            cs.wait_stream(hs)
+            cs.wait_stream(ds)
+            e1.record(cs)
+            torch.cuda.synchronize()
+            mode = ("one compute stream (raftgp_build_embed per step) + H2D and D2H streams: step k+1's inputs and "
+                    "step k-1's outputs cross PCIe under step k's kernels")
+        elif world == 1 and not args.no_fuse_variants:
             lanes = []
             for _ in range(args.e2e_lanes):
                 s_ = torch.cuda.Stream(dev)
