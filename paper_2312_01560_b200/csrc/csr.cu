@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(1024) csr_sort_block(const int64_t *__restrict
 #endif
 constexpr int kPartTile = RG_PART_TILE;   // raw pairs per partition tile
 #ifndef RG_PART_UNROLL
-#define RG_PART_UNROLL 8
+#define RG_PART_UNROLL 16
 #endif
 constexpr int kPartUnroll = RG_PART_UNROLL;   // edge loads in flight per thread
 constexpr int kMaxBuckets = 12288;      // partition smem: 12 B per bucket
