@@ -615,6 +615,17 @@ __device__ __forceinline__ void warp_sort_inplace(int32_t *a, int len, int lane)
 #endif
 constexpr int kSubAvg = RG_SUB_AVG;   // mean entries per value sub-range when a long row is split for sorting
 
+// 4 group-shared counters per 4-warp group for the dedup of long rows. The row cursors `cur` of the rows
+// being sorted are still needed when a bucket is processed window by window, so the counters live at the
+// top of the cursor array (kMaxBucketRows slots; a bucket has at most kMaxBucketRows rows, and the window
+// path only runs for buckets of that size... so they use a separate small shared array instead).
+__device__ __forceinline__ int32_t *gtmp_cnt(int32_t *cur, int nr, int grp) {
+    __shared__ int32_t wcnt[8][4];
+    (void)cur;
+    (void)nr;
+    return wcnt[grp];
+}
+
 template <bool PACKED>
 __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PACKED>::T *__restrict__ pairs,
                                                         const int64_t *__restrict__ base, int pgrid,
@@ -622,13 +633,13 @@ __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PAC
                                                         int64_t nl, int shift, int nb, int vbits,
                                                         int32_t *__restrict__ col_raw, int32_t *__restrict__ deg,
                                                         int64_t *__restrict__ fb_rows, int32_t *__restrict__ fb_count,
-                                                        unsigned int *__restrict__ bnext) {
+                                                        unsigned int *__restrict__ bnext, int cap) {
     extern __shared__ int32_t bsm[];
-    int32_t *s = bsm;                                   // kBucketCap values
+    int32_t *s = bsm;                                   // cap (<= kBucketCap) values
     int32_t *cur = bsm + kBucketCap;                    // B cursors (first: the row counts)
     int32_t *off = cur + kMaxBucketRows;                // B + 1 offsets (relative to the bucket start)
-    int32_t *big = off + kMaxBucketRows + 1;            // rows longer than 32, longest work first
-    __shared__ int fb_base, nbig, qnext, tail;
+    int32_t *big = off + kMaxBucketRows + 1;            // rows longer than kGroupRow
+    __shared__ int fb_base, nbig, qnext, tail, wend;
     __shared__ int gtmp[8];
     __shared__ int64_t scan_sh[32];
     const int lane = threadIdx.x & 31;
@@ -644,12 +655,6 @@ __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PAC
         const int nr = static_cast<int>(min(nl, r0 + ((int64_t)1 << shift)) - r0);
         const int64_t e0 = base[(int64_t)b * pgrid];            // bucket b starts at its first CTA's offset
         const int64_t E = base[(int64_t)(b + 1) * pgrid] - e0;
-        const bool fits = E <= kBucketCap;
-        if (threadIdx.x == 0) {
-            nbig = 0;
-            qnext = 0;
-            tail = (int)min(E, (int64_t)kBucketCap);   // free shared memory after the bucket's entries
-        }
         for (int t = threadIdx.x; t < nr; t += blockDim.x) cur[t] = 0;
         __syncthreads();
         // row lengths of this bucket (the bucket is its own count pass: no global per-row counters)
@@ -685,14 +690,45 @@ __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PAC
         __syncthreads();
         for (int t = threadIdx.x; t <= nr; t += blockDim.x) {
             if (t < nr || r0 + nr == nl) raw_ptr[r0 + t] = e0 + off[t];
-            if (t < nr) {
-                cur[t] = 0;
-                if (fits && off[t + 1] - off[t] > kGroupRow) big[atomicAdd(&nbig, 1)] = t;
-            }
+            if (t < nr) cur[t] = 0;
         }
         __syncthreads();
-        if (fits) {
-            // placement: batched loads for memory-level parallelism, warp-aggregated slot claims per row
+        // windows of consecutive rows [ws, we) whose entries fit shared memory (the whole bucket when it
+        // fits; a bucket too large is sorted window by window, each window re-reading the bucket's entries).
+        // A single row longer than `cap` goes to the global fallback (warp / block sort kernels).
+        for (int ws = 0; ws < nr;) {
+            if (threadIdx.x == 0) {
+                int lo = ws, hi = nr;   // largest we with off[we] - off[ws] <= cap
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) / 2;
+                    if (off[mid] - off[ws] <= cap) lo = mid;
+                    else hi = mid - 1;
+                }
+                wend = lo;
+                nbig = 0;
+                qnext = ws;
+            }
+            __syncthreads();
+            const int we = wend;
+            if (we == ws) {   // one oversized row: place it in col_raw (global) for the fallback kernels
+                const int t = ws;
+                for (int64_t idx = threadIdx.x; idx < E; idx += blockDim.x) {
+                    const typename Entry<PACKED>::T p = pairs[e0 + idx];
+                    if (Entry<PACKED>::valid(p) && Entry<PACKED>::row(p, vbits) == t) {
+                        const int64_t k = atomicAdd(&cur[t], 1);
+                        col_raw[e0 + off[t] + k] = Entry<PACKED>::col(p, vbits);
+                    }
+                }
+                if (threadIdx.x == 0) fb_rows[atomicAdd(fb_count, 1)] = r0 + t;
+                __syncthreads();
+                ws = we + 1;
+                continue;
+            }
+            const int wbase = off[ws];
+            if (threadIdx.x == 0) tail = off[we] - wbase;   // free shared memory after the window's entries
+            for (int t = ws + threadIdx.x; t < we; t += blockDim.x)
+                if (off[t + 1] - off[t] > kGroupRow) big[atomicAdd(&nbig, 1)] = t;
+            // placement: batched loads for memory-level parallelism
             for (int64_t i0 = (int64_t)threadIdx.x * kLoadBatch; i0 < E; i0 += (int64_t)blockDim.x * kLoadBatch) {
                 typename Entry<PACKED>::T p[kLoadBatch];
 #pragma unroll
@@ -702,7 +738,8 @@ __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PAC
                 for (int k = 0; k < kLoadBatch; ++k) {
                     if (Entry<PACKED>::valid(p[k])) {
                         const int lr = Entry<PACKED>::row(p[k], vbits);
-                        s[off[lr] + atomicAdd(&cur[lr], 1)] = Entry<PACKED>::col(p[k], vbits);
+                        if (lr >= ws && lr < we)
+                            s[off[lr] - wbase + atomicAdd(&cur[lr], 1)] = Entry<PACKED>::col(p[k], vbits);
                     }
                 }
             }
@@ -713,10 +750,10 @@ __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PAC
             const GroupSync gsync{1 + grp, 128};
             for (int q = grp; q < nbr; q += 8) {
                 const int t = big[q];
-                int32_t *a = s + off[t];
+                int32_t *a = s + off[t] - wbase;
                 const int len = off[t + 1] - off[t];
-                // split by value into ~len/48 sub-ranges (ids are spread over [0, 2^vbits)), then one warp sorts
-                // each sub-range in registers; the bucket's free shared memory holds the counts and a copy.
+                // split by value into ~len/kSubAvg sub-ranges (ids are spread over [0, 2^vbits)), then one warp
+                // sorts each sub-range in registers; the free shared memory holds the counts and a copy.
                 // Equal values share a sub-range, so the row ends up fully sorted. No room: plain bitonic.
                 const int nsub = (len + kSubAvg - 1) / kSubAvg;
                 if (gt == 0) gtmp[grp] = atomicAdd(&tail, nsub + len);
@@ -765,13 +802,13 @@ __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PAC
                 }
                 // dedup: running count over 128-wide chunks (group-shared partial counts in `cur`)
                 int written = 0;
-                for (int base = 0; base < len; base += 128) {
-                    const int x = base + gt;
+                for (int base0 = 0; base0 < len; base0 += 128) {
+                    const int x = base0 + gt;
                     const int32_t v = x < len ? a[x] : INT_MAX;
                     const bool keep = x < len && (x == 0 || v != a[x - 1]);
                     const unsigned bal = __ballot_sync(0xffffffffu, keep);
                     const int lw = gt >> 5;
-                    int32_t *wc = cur + grp * 4;        // cursors are free after placement
+                    int32_t *wc = gtmp_cnt(cur, nr, grp);
                     if (lane == 0) wc[lw] = __popc(bal);
                     gsync();
                     int before = 0, total = 0;
@@ -785,28 +822,19 @@ __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PAC
                 }
                 if (gt == 0) deg[r0 + t] = written;
             }
-            // all other rows: one warp per row, fetched dynamically
+            // all other rows of the window: one warp per row, fetched dynamically
             for (;;) {
                 int t = 0;
                 if (lane == 0) t = atomicAdd(&qnext, 1);
                 t = __shfl_sync(0xffffffffu, t, 0);
-                if (t >= nr) break;
+                if (t >= we) break;
                 const int len = off[t + 1] - off[t];
                 if (len > kGroupRow) continue;
-                const int w = warp_sort_dedup(s + off[t], len, col_raw + e0 + off[t], lane);
+                const int w = warp_sort_dedup(s + off[t] - wbase, len, col_raw + e0 + off[t], lane);
                 if (lane == 0) deg[r0 + t] = w;
             }
-        } else {
-            // too large for shared memory: place into col_raw (global), rows go to the warp/block sort kernels
-            for (int64_t idx = threadIdx.x; idx < E; idx += blockDim.x) {
-                const typename Entry<PACKED>::T p = pairs[e0 + idx];
-                const int lr = Entry<PACKED>::row(p, vbits);
-                const int64_t k = atomicAdd(&cur[lr], 1);
-                col_raw[e0 + off[lr] + k] = Entry<PACKED>::col(p, vbits);
-            }
-            if (threadIdx.x == 0) fb_base = atomicAdd(fb_count, nr);
             __syncthreads();
-            for (int t = threadIdx.x; t < nr; t += blockDim.x) fb_rows[fb_base + t] = r0 + t;
+            ws = we;
         }
         __syncthreads();
     }
@@ -1007,17 +1035,21 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
                                                                            static_cast<int2 *>(pairs));
         }
         RG_CHECK_LAUNCH(ctx);
+        static const int bcap = [] {   // RAFTGP_BUCKET_CAP: smaller shared-memory windows (tests)
+            const char *e = getenv("RAFTGP_BUCKET_CAP");
+            return e ? std::max(256, std::min(kBucketCap, atoi(e))) : kBucketCap;
+        }();
         {
             LaunchScope L(ctx, K_CSR_BUCKET);
             const int bgrid = std::min(nb, ctx->sm_count);
             if (packed)
                 csr_bucket_sort<true><<<bgrid, 1024, bsmem, st>>>(static_cast<const uint32_t *>(pairs), bstart, pgrid, raw_ptr,
                                                                   nl, shift, nb, vbits, col_raw, g->deg_local, fb_rows,
-                                                                  fb_count, bnext);
+                                                                  fb_count, bnext, bcap);
             else
                 csr_bucket_sort<false><<<bgrid, 1024, bsmem, st>>>(static_cast<const int2 *>(pairs), bstart, pgrid, raw_ptr,
                                                                    nl, shift, nb, vbits, col_raw, g->deg_local, fb_rows,
-                                                                   fb_count, bnext);
+                                                                   fb_count, bnext, bcap);
         }
         RG_CHECK_LAUNCH(ctx);
         {

@@ -118,3 +118,35 @@ def test_build_embed_bad_ids(rg, ctx):
     Z, _ = rg.raftgp_build_embed(ctx, 3, torch.tensor([0], dtype=torch.int32), torch.tensor([1], dtype=torch.int32),
                                  ["ncut"], (64, 64, 32), 1)
     assert Z["ncut"].shape == (3, 32)
+
+
+_WINDOW_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, '.')
+import oracle, synth
+from paper_2312_01560_b200 import raftgp as rg
+ctx = rg.Context(0)
+cases = [synth.generate('C2', 3, n=30000), synth.generate('C1', 1)]
+rng = np.random.default_rng(3)
+hub_src = np.concatenate([np.zeros(5000, np.int32), rng.integers(0, 20000, 40000).astype(np.int32)])
+hub_dst = np.concatenate([rng.integers(1, 20000, 5000).astype(np.int32), rng.integers(0, 20000, 40000).astype(np.int32)])
+for n, src, dst in [(c.n, c.src, c.dst) for c in cases] + [(20000, hub_src, hub_dst)]:
+    g = rg.raftgp_build_csr(ctx, n, torch.from_numpy(src), torch.from_numpy(dst))
+    rp, col, deg = g.export()
+    ref = oracle.build_csr(n, src, dst)
+    assert np.array_equal(rp, ref.row_ptr) and np.array_equal(col, ref.col), n
+print('ok')
+"""
+
+
+@pytest.mark.parametrize("cap", ["300", "2048"])
+def test_bucket_windows(rg, cap):
+    """Buckets larger than the shared-memory window (RAFTGP_BUCKET_CAP shrinks it) are sorted window by
+    window; rows longer than a window go to the fallback kernels. The CSR must stay bit-exact."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _WINDOW_SCRIPT], cwd=root, env=dict(os.environ, RAFTGP_BUCKET_CAP=cap),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
