@@ -177,7 +177,8 @@ struct KindTraits {
                                 : KIND == KIND_DUAL ? M_SUM_S : M_SUM;
 };
 
-// One hop for groups of RB consecutive local rows per warp (grid-stride over groups).
+// One hop for groups of RB consecutive visiting positions per warp; warps claim kClaim groups at a time from a
+// per-launch counter (dynamic, a.ctr) or walk them grid-stride (a.ctr == null).
 template <int KIND, int W, int WN, int RB, int U, int THREADS>
 __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREADS) > 0 ? KindTraits<KIND>::WARPS * 32 / THREADS : 1)
     hop_kernel(HopArgs a) {
