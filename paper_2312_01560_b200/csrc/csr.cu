@@ -323,7 +323,8 @@ constexpr int kPartTile = RG_PART_TILE;   // raw pairs per partition tile
 #define RG_PART_UNROLL 16
 #endif
 constexpr int kPartUnroll = RG_PART_UNROLL;   // edge loads in flight per thread
-constexpr int kMaxBuckets = 12288;      // partition smem: 12 B per bucket
+constexpr int kMaxBuckets = 12288;      // partition smem with 64-bit bucket cursors: 12 B per bucket
+constexpr int kMaxBuckets32 = 24576;    // with 32-bit cursors (raw entry count < 2^32): 8 B per bucket
 constexpr int kMaxBucketRows = 4096;    // bucket_sort smem for row cursors/offsets
 constexpr int kBucketCap = 44032;       // entries of one bucket held in shared memory (172 KB)
 #ifndef RG_GROUP_ROW
@@ -414,15 +415,15 @@ __global__ void csr_bucket_cursor(const int64_t *__restrict__ base, int pgrid, i
     if (b < nb) bcur[b] = (unsigned long long)base[(int64_t)b * pgrid];
 }
 
-template <bool PACKED>
+template <bool PACKED, typename BT>
 __global__ void __launch_bounds__(1024) csr_partition(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
                                                       int64_t m, int64_t n, int64_t rb, int64_t re, int shift, int nb,
                                                       int vbits, int64_t ptile, unsigned long long *__restrict__ bcur,
                                                       typename Entry<PACKED>::T *__restrict__ pairs) {
     using E = Entry<PACKED>;
-    extern __shared__ long long psm[];
-    long long *base = psm;                                              // nb
-    unsigned int *hist = reinterpret_cast<unsigned int *>(psm + nb);    // nb
+    extern __shared__ __align__(8) unsigned char psm_raw[];
+    BT *base = reinterpret_cast<BT *>(psm_raw);                                       // nb slot bases
+    unsigned int *hist = reinterpret_cast<unsigned int *>(psm_raw + sizeof(BT) * nb);  // nb
     const int bmask = (1 << shift) - 1;
     const int64_t ntiles = (m + ptile - 1) / ptile;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -449,7 +450,7 @@ __global__ void __launch_bounds__(1024) csr_partition(const int32_t *__restrict_
         __syncthreads();
         for (int b = threadIdx.x; b < nb; b += blockDim.x) {
             const unsigned int h = hist[b];
-            if (h) base[b] = (long long)atomicAdd(&bcur[b], (unsigned long long)h);
+            if (h) base[b] = (BT)atomicAdd(&bcur[b], (unsigned long long)h);
             hist[b] = 0u;
         }
         __syncthreads();
@@ -968,8 +969,15 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
     RG_TRY(dalloc_t(ctx, &g->sh_all, n));
     RG_TRY(dzero(ctx, big_count, sizeof(int32_t) * 2, st));
     const int egrid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 256), (int64_t)ctx->sm_count * 16)));
+    // 32-bit partition cursors when every raw entry position fits: twice the buckets in the same shared memory,
+    // so huge graphs (C5) get buckets half as large; then buckets grow while a typical one still fits a window
+    const bool b32 = cap < ((int64_t)1 << 32);
+    const int kMaxB = b32 ? kMaxBuckets32 : kMaxBuckets;
     int shift = 0;
-    while (shift < 31 && ceil_div(nl, (int64_t)1 << shift) > kMaxBuckets) ++shift;
+    while (shift < 31 && ceil_div(nl, (int64_t)1 << shift) > kMaxB) ++shift;
+    while (nl > 0 && shift < 12 && (cap / nl + 1) * ((int64_t)2 << shift) <= kBucketCap / 2 &&
+           ceil_div(nl, (int64_t)2 << shift) >= 4 * (int64_t)ctx->sm_count)
+        ++shift;
     const bool bucketed = nl > 0 && ((int64_t)1 << shift) <= kMaxBucketRows;
     if (!bucketed) {   // per-row counts (the bucketed path lets every bucket count its own rows)
         RG_TRY(dzero(ctx, cnt, sizeof(int32_t) * (nl ? nl : 1), st));
@@ -1006,9 +1014,11 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
         const size_t bsmem = (size_t)(kBucketCap + 3 * kMaxBucketRows + 1) * 4;
         static bool attrs = false;
         if (!attrs) {
-            RG_CUDA(cudaFuncSetAttribute(csr_bucket_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 4));
-            RG_CUDA(cudaFuncSetAttribute(csr_partition<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 12));
-            RG_CUDA(cudaFuncSetAttribute(csr_partition<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 12));
+            RG_CUDA(cudaFuncSetAttribute(csr_bucket_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets32 * 4));
+            RG_CUDA(cudaFuncSetAttribute(csr_partition<true, long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 12));
+            RG_CUDA(cudaFuncSetAttribute(csr_partition<false, long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 12));
+            RG_CUDA(cudaFuncSetAttribute(csr_partition<true, unsigned int>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets32 * 8));
+            RG_CUDA(cudaFuncSetAttribute(csr_partition<false, unsigned int>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets32 * 8));
             RG_CUDA(cudaFuncSetAttribute(csr_bucket_sort<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
             RG_CUDA(cudaFuncSetAttribute(csr_bucket_sort<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
             attrs = true;
@@ -1027,12 +1037,19 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
                 return e ? std::max<int64_t>(1024, atoll(e)) : (int64_t)kPartTile;
             }();
             const int tgrid = static_cast<int>(std::min<int64_t>(ceil_div(m, ptile), ctx->sm_count));
-            if (packed)
-                csr_partition<true><<<tgrid, 1024, (size_t)nb * 12, st>>>(src, dst, m, n, rb, re, shift, nb, vbits, ptile, bcur,
-                                                                          static_cast<uint32_t *>(pairs));
+            const size_t psmem = (size_t)nb * (b32 ? 8 : 12);
+            if (packed && b32)
+                csr_partition<true, unsigned int><<<tgrid, 1024, psmem, st>>>(src, dst, m, n, rb, re, shift, nb, vbits, ptile,
+                                                                               bcur, static_cast<uint32_t *>(pairs));
+            else if (packed)
+                csr_partition<true, long long><<<tgrid, 1024, psmem, st>>>(src, dst, m, n, rb, re, shift, nb, vbits, ptile,
+                                                                            bcur, static_cast<uint32_t *>(pairs));
+            else if (b32)
+                csr_partition<false, unsigned int><<<tgrid, 1024, psmem, st>>>(src, dst, m, n, rb, re, shift, nb, vbits, ptile,
+                                                                                bcur, static_cast<int2 *>(pairs));
             else
-                csr_partition<false><<<tgrid, 1024, (size_t)nb * 12, st>>>(src, dst, m, n, rb, re, shift, nb, vbits, ptile, bcur,
-                                                                           static_cast<int2 *>(pairs));
+                csr_partition<false, long long><<<tgrid, 1024, psmem, st>>>(src, dst, m, n, rb, re, shift, nb, vbits, ptile,
+                                                                             bcur, static_cast<int2 *>(pairs));
         }
         RG_CHECK_LAUNCH(ctx);
         static const int bcap = [] {   // RAFTGP_BUCKET_CAP: smaller shared-memory windows (tests)
