@@ -658,7 +658,21 @@ def main():
     # steps' kernels (multi-buffering with the public API); every step still copies its own edges in and
     # its own Z out. N > 1: one stream, sequential.
     e2e = None
+    e2e_skip = None
     if not args.no_e2e:
+        # each pipelined lane holds its own context (workspace) and two Z buffer sets; at C5 sizes that does
+        # not fit next to the main context, so the lane count drops, and the leg is skipped (with the reason)
+        # when even one lane would not fit
+        ctx.trim()
+        torch.cuda.empty_cache()
+        free_b, _ = torch.cuda.mem_get_info(dev)
+        lane_b = 2 * int(sum(rows * dims[-1] * 4 for _ in variants)) + 2 * 8 * m + 40 * m   # Z x2, edges x2, workspace
+        lanes_fit = int(free_b // max(1, lane_b))
+        if lanes_fit < args.e2e_lanes:
+            args.e2e_lanes = max(1, min(args.e2e_lanes, lanes_fit))
+        if lanes_fit < 1:
+            e2e_skip = f"needs ~{lane_b / 2**30:.0f} GiB per pipeline lane, {free_b / 2**30:.0f} GiB free"
+    if not args.no_e2e and e2e_skip is None:
         d2h = int(sum(rows * dims[-1] * 4 for _ in variants))
         if world == 1 and not args.no_fuse_variants and args.e2e_lanes == 1:
             # one compute stream (steps back to back, no kernel interleaving across steps) with the copies on
@@ -810,7 +824,8 @@ def main():
                        "parallelism": f"rowpart{world}" if world > 1 else "single",
                        "exchange": (args.exchange if world > 1 else None),
                        "l2": "inputs larger than L2 (gathered operands >= 1.28 GB vs 126 MB L2); no flush"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e if e2e_skip is None else {"skipped": e2e_skip},
+            "gpu_launches": launches,
             "clocks": clocks.summary(),
             "kernels_ms_per_step": {k: round(v, 4) for k, v in sorted(kernel_times.items(), key=lambda x: -x[1])},
             "hops": hop_stats,
