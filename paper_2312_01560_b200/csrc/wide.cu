@@ -33,7 +33,13 @@ namespace {
 using namespace tc;
 
 constexpr int kGM = 128;   // MMA M (rows per output tile)
-constexpr int kKB = 32;    // K columns per k-block (one bulk-copied chunk)
+#ifndef RG_KB
+#define RG_KB 32
+#endif
+#ifndef RG_GEMM_NS
+#define RG_GEMM_NS 4
+#endif
+constexpr int kKB = RG_KB;    // K columns per k-block (one bulk-copied chunk)
 constexpr int kGemmThreads = 128;
 
 __host__ __device__ constexpr uint32_t chunk_bytes(int rows) { return (uint32_t)rows * kKB * 4u; }
@@ -112,7 +118,7 @@ struct GemmCfg {
     static constexpr uint32_t A_CH = chunk_bytes(kGM);
     static constexpr uint32_t B_CH = chunk_bytes(NT);
     static constexpr uint32_t STAGE = 2 * A_CH + 2 * B_CH;
-    static constexpr int NS = (int)((220u * 1024u) / STAGE) > 4 ? 4 : (int)((220u * 1024u) / STAGE);
+    static constexpr int NS = (int)((220u * 1024u) / STAGE) > RG_GEMM_NS ? RG_GEMM_NS : (int)((220u * 1024u) / STAGE);
     static constexpr size_t SMEM = (size_t)NS * STAGE + 1024;   // + alignment slack
     // NACC accumulators in TMEM (512 columns in all), k-block kb accumulating into kb % NACC: the tensor
     // cores' fp32 accumulation error grows with the number of accumulated terms (measured: relative error
