@@ -28,8 +28,9 @@ VARIANTS = {"ncut": NCUT, "mod": MOD, "mod_reduced": MOD_REDUCED}
 def build() -> str:
     src = os.path.join(_HERE, "oracle.c")
     if (not os.path.exists(_SO)) or os.path.getmtime(_SO) < os.path.getmtime(src):
-        subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-ffp-contract=off", "-fno-fast-math",
-                               "-o", _SO, src, "-lm"])
+        subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
+                               "-o", _SO + ".tmp", src, "-lm"])
+        os.replace(_SO + ".tmp", _SO)
     return _SO
 
 
@@ -43,6 +44,16 @@ def _L():
                      "oracle_kmeans2", "oracle_model_select", "oracle_split_stops", "oracle_sbm_sample"):
             getattr(_lib, name).restype = ctypes.c_int
     return _lib
+
+
+def set_threads(k: int) -> None:
+    """Threads of the oracle's row loops (0 = OpenMP default = all cores). Results are bit-identical for any k
+    (each output row is computed sequentially by one thread; cross-row sums stay sequential)."""
+    _L().oracle_set_threads(ctypes.c_int(int(k)))
+
+
+def get_threads() -> int:
+    return int(_L().oracle_get_threads())
 
 
 def _p(a: np.ndarray):

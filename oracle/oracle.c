@@ -9,6 +9,12 @@
  * defined bit-exactly by docs/SKETCH_SPEC.md (the paper fixes no generator).
  * Compile with -ffp-contract=off (no silent FMA contraction); fmaf() is the C99 fused multiply-add.
  *
+ * Threads ("OpenMP over rows allowed because per-row sums are sequential"): the loops
+ * over OUTPUT ROWS (operator rows, GEMM rows, generator rows, per-row CSR sorts) run under OpenMP. Every
+ * row is still computed by one thread, sequentially, in the order written below, so every output bit is
+ * independent of the thread count (pinned: tests/test_oracle_graph_ops.py::test_thread_count_invariance).
+ * Reductions across rows (g = d^T Theta, scores) stay sequential. oracle_set_threads(k) fixes the count.
+ *
  * What each function follows:
  *   oracle_philox4x32_10   SKETCH_SPEC §1 (pinned against curand's host Philox)
  *   oracle_ln_spec_batch,
@@ -34,6 +40,21 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* thread count of the row loops (0 = the OpenMP default); results never depend on it (see header) */
+static int g_threads = 0;
+void oracle_set_threads(int k) { g_threads = k > 0 ? k : 0; }
+int oracle_get_threads(void) {
+#ifdef _OPENMP
+    return g_threads > 0 ? g_threads : omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+#define ORACLE_ROWS_PARALLEL _Pragma("omp parallel for schedule(dynamic, 256) num_threads(oracle_get_threads())")
 
 /* ---------------------------------------------------------------- Philox4x32-10 (SKETCH_SPEC §1) */
 void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
@@ -131,6 +152,7 @@ int oracle_gaussian(uint64_t seed, uint32_t tag, int64_t row_begin, int64_t rows
                     float *out) {
     if (rows < 0 || cols <= 0 || den <= 0 || row_begin < 0) return 2;
     float sigma = sigma_of(den);
+    ORACLE_ROWS_PARALLEL
     for (int64_t i = 0; i < rows; ++i)
         for (int32_t q = 0; 4 * q < cols; ++q) {
             float v[4];
@@ -141,40 +163,63 @@ int oracle_gaussian(uint64_t seed, uint32_t tag, int64_t row_begin, int64_t rows
 }
 
 /* ---------------------------------------------------------------- CSR build */
-static int cmp_u64(const void *a, const void *b) {
-    uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
+static int cmp_i32(const void *a, const void *b) {
+    int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
     return (x > y) - (x < y);
 }
 
 /*
- * Canonical CSR of the simple undirected graph of the raw pairs (src[e], dst[e]):
+ * Canonical CSR of the simple undirected graph of the raw pairs (src[e], dst[e]) (PAPER.md:56; SPEC.md:57-59):
  * drop u == v, add (u,v) and (v,u), sort lexicographically, drop duplicates.
- * row_ptr: int64[n+1]; col: int32[capacity >= 2m]; *nnz_out = row_ptr[n] = 2e.
+ * The lexicographic sort of (row, col) keys is done as "group by row, then sort each row by col":
+ *   1. count the entries of every row (both orientations, self pairs dropped);
+ *   2. place each entry's col into its row's segment of col[] (raw offsets = prefix sum of the counts);
+ *   3. sort every row segment ascending and drop consecutive duplicates;
+ *   4. row_ptr = prefix sum of the deduplicated lengths; move the rows left into place (in row order,
+ *      never overwriting a row not yet moved, since every destination is at or before its source).
+ * row_ptr: int64[n+1]; col: int32[capacity >= 2m] (also the workspace); *nnz_out = row_ptr[n] = 2e.
  */
 int oracle_build_csr(int64_t n, int64_t m, const int32_t *src, const int32_t *dst, int64_t *row_ptr, int32_t *col,
                      int64_t *nnz_out) {
     if (n < 0 || m < 0) return 2;
     for (int64_t e = 0; e < m; ++e)
         if (src[e] < 0 || src[e] >= n || dst[e] < 0 || dst[e] >= n) return 3;
-    uint64_t *key = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(2 * m + 1));
-    if (!key) return 4;
-    int64_t cnt = 0;
+    int64_t *raw = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));   /* raw row offsets, then cursors */
+    int64_t *len = (int64_t *)malloc(sizeof(int64_t) * ((size_t)n + 1));
+    if (!raw || !len) { free(raw); free(len); return 4; }
+    /* 1. */
     for (int64_t e = 0; e < m; ++e) {
-        uint64_t u = (uint64_t)src[e], v = (uint64_t)dst[e];
-        if (u == v) continue;
-        key[cnt++] = (u << 32) | v;
-        key[cnt++] = (v << 32) | u;
+        if (src[e] == dst[e]) continue;
+        raw[src[e] + 1] += 1;
+        raw[dst[e] + 1] += 1;
     }
-    qsort(key, (size_t)cnt, sizeof(uint64_t), cmp_u64);
-    int64_t nnz = 0;
-    for (int64_t k = 0; k < cnt; ++k)
-        if (k == 0 || key[k] != key[k - 1]) key[nnz++] = key[k];
-    for (int64_t i = 0; i <= n; ++i) row_ptr[i] = 0;
-    for (int64_t k = 0; k < nnz; ++k) row_ptr[(key[k] >> 32) + 1] += 1;
-    for (int64_t i = 0; i < n; ++i) row_ptr[i + 1] += row_ptr[i];
-    for (int64_t k = 0; k < nnz; ++k) col[k] = (int32_t)(key[k] & 0xFFFFFFFFu);
-    *nnz_out = nnz;
-    free(key);
+    for (int64_t i = 0; i < n; ++i) raw[i + 1] += raw[i];
+    /* 2. (len[] doubles as the fill cursor) */
+    for (int64_t i = 0; i < n; ++i) len[i] = raw[i];
+    for (int64_t e = 0; e < m; ++e) {
+        int32_t u = src[e], v = dst[e];
+        if (u == v) continue;
+        col[len[u]++] = v;
+        col[len[v]++] = u;
+    }
+    /* 3. */
+    ORACLE_ROWS_PARALLEL
+    for (int64_t i = 0; i < n; ++i) {
+        int32_t *r = col + raw[i];
+        int64_t cnt = raw[i + 1] - raw[i], k = 0;
+        qsort(r, (size_t)cnt, sizeof(int32_t), cmp_i32);
+        for (int64_t t = 0; t < cnt; ++t)
+            if (t == 0 || r[t] != r[t - 1]) r[k++] = r[t];
+        len[i] = k;
+    }
+    /* 4. */
+    row_ptr[0] = 0;
+    for (int64_t i = 0; i < n; ++i) row_ptr[i + 1] = row_ptr[i] + len[i];
+    for (int64_t i = 0; i < n; ++i)
+        if (row_ptr[i] != raw[i]) memmove(col + row_ptr[i], col + raw[i], sizeof(int32_t) * (size_t)len[i]);
+    *nnz_out = row_ptr[n];
+    free(raw);
+    free(len);
     return 0;
 }
 
@@ -193,6 +238,7 @@ static int64_t deg_of(const int64_t *row_ptr, int64_t i) { return row_ptr[i + 1]
 static void apply_rows(int64_t n, const int64_t *row_ptr, const int32_t *col, int op, int32_t w, const double *X,
                        const int32_t *xslot, const double *dTX, double two_e, const int64_t *rows, int64_t S,
                        double *out) {
+    ORACLE_ROWS_PARALLEL
     for (int64_t s = 0; s < S; ++s) {
         int64_t i = rows ? rows[s] : s;
         double *o = out + s * (int64_t)w;
@@ -248,6 +294,7 @@ int oracle_project(int64_t n, const int64_t *row_ptr, const int32_t *col, int va
     float *th = (float *)malloc(sizeof(float) * (size_t)(n * (int64_t)r + 1));
     double *X = (double *)malloc(sizeof(double) * (size_t)(n * (int64_t)r + 1));
     oracle_gaussian(seed, 0u, 0, n, r, r, th);
+    ORACLE_ROWS_PARALLEL
     for (int64_t k = 0; k < n * (int64_t)r; ++k) X[k] = (double)th[k];
     int rc = oracle_apply(n, row_ptr, col, variant, r, X, Y);
     free(th);
@@ -262,6 +309,17 @@ static void act_normalize(double *h, int32_t w) {
     if (ss > 0.0) {
         double nrm = sqrt(ss);
         for (int32_t c = 0; c < w; ++c) h[c] = h[c] / nrm;
+    }
+}
+
+/* h[c] = sum_{t = 0..a-1} z[t] W[t][c], each h[c] summed sequentially in t starting from 0.0 (the loops are
+ * nested t-outer so W is read row by row; the sequence of additions into every h[c] is unchanged). */
+static void row_times_w(const double *z, const double *W, int32_t a, int32_t b, double *h) {
+    for (int32_t c = 0; c < b; ++c) h[c] = 0.0;
+    for (int32_t t = 0; t < a; ++t) {
+        const double zt = z[t];
+        const double *w = W + (int64_t)t * b;
+        for (int32_t c = 0; c < b; ++c) h[c] += zt * w[c];
     }
 }
 
@@ -287,13 +345,10 @@ int oracle_gcn(int64_t n, const int64_t *row_ptr, const int32_t *col, int32_t la
         double *Wk = weights_f64(seed, k, a, b);
         double *AZ = (double *)malloc(sizeof(double) * (size_t)(n * (int64_t)a + 1));
         oracle_apply(n, row_ptr, col, OP_PROP, a, Zin, AZ);
+        ORACLE_ROWS_PARALLEL
         for (int64_t i = 0; i < n; ++i) {
             double *h = Zout + i * (int64_t)b;
-            for (int32_t c = 0; c < b; ++c) {
-                double acc = 0.0;
-                for (int32_t t = 0; t < a; ++t) acc += AZ[i * (int64_t)a + t] * Wk[(int64_t)t * b + c];
-                h[c] = acc;
-            }
+            row_times_w(AZ + i * (int64_t)a, Wk, a, b, h);
             act_normalize(h, b);
         }
         free(AZ);
@@ -357,21 +412,34 @@ int oracle_embed_rows(int64_t n, const int64_t *row_ptr, const int32_t *col, int
     /* chain[L - k] holds the rows of Z^(k) needed (Z^(0) = Y); chain[L + 1] the Theta rows. */
     const vec64 *thr = &chain[L + 1];
     double *TH = (double *)malloc(sizeof(double) * (size_t)(thr->len * (int64_t)r + 1));
-    float *tmp = (float *)malloc(sizeof(float) * (size_t)r);
+    ORACLE_ROWS_PARALLEL
     for (int64_t q = 0; q < thr->len; ++q) {
-        oracle_gaussian(seed, 0u, thr->v[q], 1, r, r, tmp);
-        for (int32_t c = 0; c < r; ++c) TH[q * r + c] = (double)tmp[c];
+        float tmp[4];
+        for (int32_t c0 = 0; c0 < r; c0 += 4) {
+            int32_t w4 = r - c0 < 4 ? r - c0 : 4;
+            /* columns c0..c0+3 of row thr->v[q]: the generator's quad q = c0/4 */
+            float sigma = sigma_of(r);
+            gaussian_quad(seed, 0u, (uint64_t)thr->v[q], (uint32_t)(c0 / 4), sigma, tmp);
+            for (int32_t c = 0; c < w4; ++c) TH[q * r + c0 + c] = (double)tmp[c];
+        }
     }
     double *dTX = NULL;
     if (variant == OP_MOD) {
+        /* g = d^T Theta over ALL n rows, summed sequentially in j (Theta regenerated chunk by chunk; the chunk
+         * generation is parallel over rows, the accumulation is not) */
         dTX = (double *)calloc((size_t)r, sizeof(double));
-        for (int64_t j = 0; j < n; ++j) {
-            double dj = (double)deg_of(row_ptr, j);
-            oracle_gaussian(seed, 0u, j, 1, r, r, tmp);
-            for (int32_t c = 0; c < r; ++c) dTX[c] += dj * (double)tmp[c];
+        const int64_t CH = 1 << 16;
+        float *buf = (float *)malloc(sizeof(float) * (size_t)(CH * (int64_t)r));
+        for (int64_t j0 = 0; j0 < n; j0 += CH) {
+            int64_t cnt = n - j0 < CH ? n - j0 : CH;
+            oracle_gaussian(seed, 0u, j0, cnt, r, r, buf);
+            for (int64_t j = j0; j < j0 + cnt; ++j) {
+                double dj = (double)deg_of(row_ptr, j);
+                for (int32_t c = 0; c < r; ++c) dTX[c] += dj * (double)buf[(j - j0) * (int64_t)r + c];
+            }
         }
+        free(buf);
     }
-    free(tmp);
     /* Y on chain[L] */
     const vec64 *yr = &chain[L];
     double *Zprev = (double *)malloc(sizeof(double) * (size_t)(yr->len * (int64_t)r + 1));
@@ -388,13 +456,10 @@ int oracle_embed_rows(int64_t n, const int64_t *row_ptr, const int32_t *col, int
         double *AZ = (double *)malloc(sizeof(double) * (size_t)(zr->len * (int64_t)a + 1));
         apply_rows(n, row_ptr, col, OP_PROP, a, Zprev, cslot[L - k + 1], NULL, two_e, zr->v, zr->len, AZ);
         double *Zk = (double *)malloc(sizeof(double) * (size_t)(zr->len * (int64_t)b + 1));
+        ORACLE_ROWS_PARALLEL
         for (int64_t q = 0; q < zr->len; ++q) {
             double *h = Zk + q * (int64_t)b;
-            for (int32_t c = 0; c < b; ++c) {
-                double acc = 0.0;
-                for (int32_t t = 0; t < a; ++t) acc += AZ[q * (int64_t)a + t] * Wk[(int64_t)t * b + c];
-                h[c] = acc;
-            }
+            row_times_w(AZ + q * (int64_t)a, Wk, a, b, h);
             act_normalize(h, b);
         }
         for (int64_t s = 0; s < S; ++s)

@@ -247,6 +247,46 @@ def test_embed_rows_identical_to_full(variant):
         np.testing.assert_array_equal(Zr[k], Zs[k][rows])
 
 
+def test_embed_rows_identical_to_full_ragged_and_chunked():
+    """Odd sketch width (generator quads cut at r) and n > 65536 (MOD's g streamed over several chunks)."""
+    n = 70_001
+    src, dst = synth.random_edges(n, 150_000, seed=9)
+    g = oracle.build_csr(n, src, dst)
+    dims = [10, 6]
+    rows = np.concatenate([synth.sample_rows(n, 20, seed=1), [n - 1, 65_535, 65_536]])
+    for variant in ("ncut", "mod"):
+        Y = oracle.project(g, variant, 10, seed=2)
+        Z = oracle.gcn(g, dims, seed=2, Y=Y)
+        Yr, Zr = oracle.embed_rows(g, variant, 10, dims, 2, rows)
+        np.testing.assert_array_equal(Yr, Y[rows])
+        np.testing.assert_array_equal(Zr[0], Z[0][rows])
+
+
+def test_thread_count_invariance():
+    """the row loops may run under OpenMP because each output row is summed sequentially by one
+    thread. Pin: one thread and all threads give bit-identical CSR, projections, GCN layers and sampled rows."""
+    gr = synth.generate("C2", 0)
+    dims = [16, 12, 8]
+    rows = synth.sample_rows(gr.n, 30, seed=3)
+    out = []
+    try:
+        for k in (1, 0):
+            oracle.set_threads(k)
+            g = oracle.build_csr(gr.n, gr.src, gr.dst)
+            res = [g.row_ptr, g.col]
+            for v in ("ncut", "mod", "mod_reduced"):
+                Y = oracle.project(g, v, 16, seed=1)
+                res += [Y] + oracle.gcn(g, dims, seed=1, Y=Y)
+            Yr, Zr = oracle.embed_rows(g, "mod", 16, dims, 1, rows)
+            res += [Yr] + Zr
+            out.append(res)
+    finally:
+        oracle.set_threads(0)
+    assert oracle.get_threads() >= 1
+    for a, b in zip(*out):
+        assert a.dtype == b.dtype and np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
 def test_planted_partition_recovery():
     """The pipeline recovers the planted blocks of C1-shaped DC-SBM graphs, and the GNN stage is what
     makes it work (paper Table II: ARI 0.9994 at N=1E3 with its own Alg. 1 and wider layers; Table IV:
