@@ -3,11 +3,15 @@
  * 2-layer untrained GCN, score a labelling, and print checksums. Built by __graft_entry__.build();
  * tests/test_gpu_c_api.py runs it and compares with the Python binding on the same inputs.
  *
- * usage: raftgp_demo [n] [seed]   (graph: ring i -- i+1 plus chords i -- (7 i + 3) mod n) */
+ * usage: raftgp_demo [n] [seed]   (graph: ring i -- i+1 plus chords i -- (7 i + 3) mod n)
+ *        raftgp_demo n seed rank world idfile   (row-partitioned: `world` processes, one per GPU; rank 0 writes the
+ *        NCCL unique id to idfile, the others read it; each process prints the checksums of ITS rows of Z) */
+#define _DEFAULT_SOURCE   /* usleep */
 #include <cuda_runtime_api.h>
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <unistd.h>
 
 #include "raftgp.h"
 
@@ -20,6 +24,55 @@
         }                                                                                             \
     } while (0)
 
+/* the row-partitioned step through raftgp_ctx_create_dist + raftgp_build_embed */
+static int run_dist(int64_t n, uint64_t seed, int rank, int world, const char *idfile, const int32_t *src,
+                    const int32_t *dst, int64_t m) {
+    unsigned char id[128];
+    if (rank == 0) {
+        char tmp[4096];
+        snprintf(tmp, sizeof tmp, "%s.tmp", idfile);
+        CHECK(raftgp_nccl_unique_id(id));
+        FILE *f = fopen(tmp, "wb");
+        if (!f || fwrite(id, 1, 128, f) != 128) return 1;
+        fclose(f);
+        if (rename(tmp, idfile) != 0) return 1;
+    } else {
+        FILE *f = NULL;
+        for (int t = 0; t < 6000 && !(f = fopen(idfile, "rb")); ++t) usleep(10000);
+        if (!f || fread(id, 1, 128, f) != 128) return 1;
+        fclose(f);
+    }
+    int ndev = 1;
+    cudaGetDeviceCount(&ndev);
+    raftgp_ctx ctx = NULL;
+    CHECK(raftgp_ctx_create_dist(rank % ndev, NULL, rank, world, id, &ctx));
+    const int64_t R = (n + world - 1) / world;
+    const int64_t rb = rank * R < n ? rank * R : n, re = (rank + 1) * R < n ? (rank + 1) * R : n;
+    const int32_t dims[3] = {64, 64, 32};
+    const int32_t variants[2] = {RAFTGP_NCUT, RAFTGP_MOD};
+    float *Zd[2] = {NULL, NULL};
+    const size_t bytes = sizeof(float) * (size_t)(re - rb > 0 ? re - rb : 1) * dims[2];
+    for (int v = 0; v < 2; ++v)
+        if (cudaMalloc((void **)&Zd[v], bytes) != cudaSuccess) return 1;
+    CHECK(raftgp_build_embed(ctx, n, m, src, dst, RAFTGP_HOST_PTRS, 2, variants, 2, dims, seed, Zd, NULL));
+    CHECK(raftgp_ctx_sync(ctx));
+    float *Z = (float *)malloc(bytes);
+    printf("rank %d world %d rows %lld %lld\n", rank, world, (long long)rb, (long long)re);
+    for (int v = 0; v < 2; ++v) {
+        if (cudaMemcpy(Z, Zd[v], bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return 1;
+        double sum = 0.0, sq = 0.0;
+        for (int64_t i = 0; i < (re - rb) * dims[2]; ++i) {
+            sum += Z[i];
+            sq += (double)Z[i] * Z[i];
+        }
+        printf("%s sum %.9e sumsq %.9e z00 %.9e\n", v == 0 ? "ncut" : "mod", sum, sq, re > rb ? Z[0] : 0.0f);
+        cudaFree(Zd[v]);
+    }
+    free(Z);
+    CHECK(raftgp_ctx_destroy(ctx));   /* collective on a distributed context */
+    return 0;
+}
+
 int main(int argc, char **argv) {
     const int64_t n = argc > 1 ? atoll(argv[1]) : 1000;
     const uint64_t seed = argc > 2 ? strtoull(argv[2], NULL, 10) : 1;
@@ -30,6 +83,11 @@ int main(int argc, char **argv) {
         dst[2 * i] = (int32_t)((i + 1) % n);
         src[2 * i + 1] = (int32_t)i;
         dst[2 * i + 1] = (int32_t)((7 * i + 3) % n);
+    }
+    if (argc > 5) {
+        const int rc = run_dist(n, seed, atoi(argv[3]), atoi(argv[4]), argv[5], src, dst, m);
+        free(src); free(dst);
+        return rc;
     }
     raftgp_ctx ctx = NULL;
     raftgp_graph g = NULL;

@@ -17,10 +17,14 @@
  *    caller owns every array passed in. Device inputs must stay valid until the stream work completes.
  *  - Errors: every function returns raftgp_status; on non-OK, raftgp_last_error() holds a message for
  *    the calling thread. No C++ exception crosses this ABI. Handles are not thread-safe.
- *  - Multi-GPU: one process and one context per GPU. A graph may hold only the rows [row_begin,
- *    row_end) of the global CSR (1-D row partition); column ids are always global. Row-indexed
- *    outputs (Y, Z, T) hold the local rows only. The exchange between hops (all-gather of the next
- *    operand) is done by the caller (paper_2312_01560_b200/dist.py, torch.distributed/NCCL).
+ *  - Multi-GPU: one process and one context per GPU. raftgp_ctx_create_dist gives the
+ *    contexts of a job an NCCL communicator (the unique id comes from raftgp_nccl_unique_id on rank 0 and
+ *    reaches the other ranks by any out-of-band means). On such a context raftgp_build_embed runs the whole
+ *    row-partitioned step inside the library (rank p owns rows [p R, min((p+1) R, n)), R = ceil(n / P);
+ *    exchanges fused into the producing kernels, see "a6" below) and returns the local rows of Z. The
+ *    building blocks stay public too: a graph may hold only the rows [row_begin, row_end) of the global CSR
+ *    (column ids always global; row-indexed outputs hold the local rows), and raftgp_barrier /
+ *    raftgp_allgather run the job's collectives on the context stream.
  */
 #ifndef RAFTGP_H
 #define RAFTGP_H
@@ -48,7 +52,8 @@ typedef enum {
     RAFTGP_ERR_INTERNAL = 4,
     RAFTGP_ERR_CUDA = 5,     /* a CUDA runtime call or kernel launch failed */
     RAFTGP_ERR_NOMEM = 6,    /* device allocation failed */
-    RAFTGP_ERR_STATE = 7     /* handle not ready (e.g. partial graph without raftgp_graph_set_degrees) */
+    RAFTGP_ERR_COMM = 7,     /* an NCCL call of a distributed context failed (raftgp_ctx_create_dist) */
+    RAFTGP_ERR_STATE = 8     /* handle not ready (e.g. partial graph without raftgp_graph_set_degrees) */
 } raftgp_status;
 
 /* The feature operator X of Eq. 5 ("X in {M, Q~}"; PAPER.md:289 RaftGP-C / RaftGP-M). */
@@ -75,8 +80,10 @@ RAFTGP_API raftgp_status raftgp_ctx_create(int device, void *cuda_stream, raftgp
 RAFTGP_API raftgp_status raftgp_ctx_destroy(raftgp_ctx ctx);
 RAFTGP_API raftgp_status raftgp_ctx_sync(raftgp_ctx ctx);                     /* synchronous */
 RAFTGP_API raftgp_status raftgp_ctx_stream(raftgp_ctx ctx, void **cuda_stream_out);
-/* Return the context's cached workspace blocks to the device (steady-state calls reuse them; a caller about to
- * allocate a lot itself can trim first). Synchronous. bytes_released: host out or NULL. */
+/* Workspace: every context allocates from its OWN stream-ordered memory pool (the device's default pool and its
+ * release threshold are left untouched) and keeps freed blocks cached for reuse. raftgp_ctx_trim returns the
+ * cached blocks to the pool and the pool's unused memory to the device (cudaMemPoolTrimTo), so it is visible to
+ * other allocators (e.g. PyTorch's) afterwards. Synchronous. bytes_released: host out or NULL. */
 RAFTGP_API raftgp_status raftgp_ctx_trim(raftgp_ctx ctx, int64_t *bytes_released);
 
 /* Per-kernel device timing with CUDA events recorded around every launch on the ctx stream.
@@ -88,6 +95,25 @@ RAFTGP_API raftgp_status raftgp_prof_read(raftgp_ctx ctx, int kernel_id, double 
 RAFTGP_API raftgp_status raftgp_prof_reset(raftgp_ctx ctx);
 /* number of kernels this context has launched since creation (or since the last reset) */
 RAFTGP_API raftgp_status raftgp_launch_count(raftgp_ctx ctx, int64_t *out, int reset);
+
+/* ---------------------------------------------------------------- multi-GPU contexts
+ * raftgp_nccl_unique_id: a new NCCL unique id (128 bytes, host out), created by ONE rank (rank 0) and passed to all.
+ * raftgp_ctx_create_dist: like raftgp_ctx_create, plus membership `rank` of a `world`-rank NCCL communicator
+ *   (1 <= world <= 8, one rank per GPU of one node; collective: every rank calls it with the same id).
+ *   raftgp_ctx_destroy of such a context is collective too (the cached operand copies are unmapped and freed
+ *   behind a barrier, then the communicator is destroyed).
+ * raftgp_ctx_rank: rank and world of a context (0 and 1 for raftgp_ctx_create).
+ * raftgp_barrier: stream-ordered barrier (a 1-element ncclAllReduce on the context stream): work enqueued after it
+ *   on any rank runs after the work every rank enqueued before it. No-op on a one-rank context.
+ * raftgp_allgather: ncclAllGather of bytes_per_rank bytes per rank on the context stream (device buffers; recv
+ *   holds world * bytes_per_rank; send may alias recv + rank * bytes_per_rank). A copy on non-dist contexts.
+ * Errors: PARAM, COMM (NCCL failure; raftgp_last_error has NCCL's message), CUDA, NOMEM. */
+RAFTGP_API raftgp_status raftgp_nccl_unique_id(void *out128);
+RAFTGP_API raftgp_status raftgp_ctx_create_dist(int device, void *cuda_stream, int rank, int world, const void *id128,
+                                                raftgp_ctx *out);
+RAFTGP_API raftgp_status raftgp_ctx_rank(raftgp_ctx ctx, int *rank, int *world);
+RAFTGP_API raftgp_status raftgp_barrier(raftgp_ctx ctx);
+RAFTGP_API raftgp_status raftgp_allgather(raftgp_ctx ctx, const void *send_dev, void *recv_dev, size_t bytes_per_rank);
 
 /* ---------------------------------------------------------------- a1 + a2: CSR build, degrees
  * Canonical CSR of the simple undirected graph given by m raw pairs (src[e], dst[e]) over n nodes
@@ -124,7 +150,9 @@ RAFTGP_API raftgp_status raftgp_graph_set_degrees(raftgp_graph g, const int32_t 
 /* Visiting order of the local rows used by the hop kernels (a permutation of 0..rows-1, device int32;
  * NULL = natural order). Performance only: every row's arithmetic, and so every output bit, is the same
  * for any order. With RAFTGP_ORDER_ROUNDS=k > 0 in the environment build_csr installs an order from k rounds
- * of label propagation (paper_2312_01560_b200/csrc/order.cu); the default is the natural order. */
+ * of label propagation (paper_2312_01560_b200/csrc/order.cu); by default build_csr installs the degree-aware
+ * order (hub rows spread one per claim). Synchronous: the array is checked on the device and rejected with
+ * RAFTGP_ERR_PARAM unless it is a permutation of 0..rows-1 (out-of-range or repeated entries). */
 RAFTGP_API raftgp_status raftgp_graph_set_order(raftgp_graph g, const int32_t *order_dev);
 
 RAFTGP_API raftgp_status raftgp_graph_destroy(raftgp_graph g);
@@ -200,11 +228,27 @@ RAFTGP_API raftgp_status raftgp_embed_multi(raftgp_graph g, int32_t nvariants, c
  * depends only on the seed, so it is generated on a library-owned side stream while the CSR build runs on the
  * context stream (tensor cores / ALUs against atomics / HBM); outputs are those of the two calls. Edge arrays
  * host or device per flags. g_out: NULL, or receives the graph handle (caller destroys it). Synchronous like
- * raftgp_build_csr; the embedding is enqueued on the context stream. Errors: those of the two calls. */
+ * raftgp_build_csr; the embedding is enqueued on the context stream. Errors: those of the two calls.
+ * On a distributed context (raftgp_ctx_create_dist; collective: every rank calls it with the same graph, all m
+ * pairs, and the same arguments) this is the row-partitioned step: rank p builds the CSR of its
+ * rows, degrees are all-gathered, Theta' rows are generated by their owner and pushed into every rank's copy
+ * during the CSR build, and every feature / GCN hop stores its output rows into all ranks' copies of the next
+ * operand (NVLink peer stores, CUDA IPC mappings cached in the context across calls; a stream-ordered barrier
+ * between producing and consuming hops). Z_dev[v] then receives the LOCAL rows (row_end - row_begin) x dims[L];
+ * the results are bit-identical to one GPU. Needs r and every width in {32, 64, 128}; g_out must be NULL. */
 RAFTGP_API raftgp_status raftgp_build_embed(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src, const int32_t *dst,
                                             uint32_t flags, int32_t nvariants, const int32_t *variants, int32_t layers,
                                             const int32_t *dims, uint64_t seed, float *const *Z_dev,
                                             raftgp_graph *g_out);
+
+/* The row-partitioned step of raftgp_build_embed with P logical ranks simulated on this context's GPU (P CSR shards,
+ * P full copies of every operand, each shard's hops storing into all P copies, lockstep stages on one stream): the
+ * single-GPU double of a P-GPU job, used to check that the partitioned schedule is bit-identical to one GPU.
+ * Z_dev[v]: n x dims[L] (all rows, shard p's rows at [p R, ...)). 1 <= P <= 8. Errors: those of raftgp_build_embed. */
+RAFTGP_API raftgp_status raftgp_build_embed_loopback(raftgp_ctx ctx, int32_t P, int64_t n, int64_t m, const int32_t *src,
+                                                     const int32_t *dst, uint32_t flags, int32_t nvariants,
+                                                     const int32_t *variants, int32_t layers, const int32_t *dims,
+                                                     uint64_t seed, float *const *Z_dev);
 
 /* First GCN operand of every listed variant for the LOCAL rows (works on row-partitioned graphs):
  * T1 = s^ (.) (X Theta W^(1)) = s^ (.) (Y W^(1)), X the variant's feature operator, Theta and W^(1) as in

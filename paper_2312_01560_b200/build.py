@@ -20,6 +20,24 @@ NVCC_FLAGS = [
 ]
 
 
+def nccl_home() -> str:
+    """NCCL the library links against: the torch wheel's (nvidia-nccl, 2.28.x), so a process that also imports torch
+    loads ONE libnccl.so.2 (same soname, same file); RAFTGP_NCCL_HOME overrides (needs include/nccl.h and
+    lib/libnccl.so.2)."""
+    cands = [os.environ.get("RAFTGP_NCCL_HOME", "")]
+    try:
+        import nvidia.nccl as _n   # the wheel torch's libtorch_cuda resolves libnccl.so.2 from
+        cands += list(_n.__path__)
+    except Exception:
+        pass
+    cands.append("/usr")
+    for c in cands:
+        if c and os.path.exists(os.path.join(c, "include", "nccl.h")) and \
+                os.path.exists(os.path.join(c, "lib", "libnccl.so.2")):
+            return c
+    raise RuntimeError("NCCL (include/nccl.h + lib/libnccl.so.2) not found; set RAFTGP_NCCL_HOME")
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
@@ -37,7 +55,10 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
     tmp = out + ".tmp"
-    cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-o", tmp, *sources()]
+    nh = nccl_home()
+    nlib = os.path.join(nh, "lib")
+    cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-I", os.path.join(nh, "include"),
+           "-o", tmp, *sources(), "-Xlinker", os.path.join(nlib, "libnccl.so.2"), "-Xlinker", f"-rpath,{nlib}"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

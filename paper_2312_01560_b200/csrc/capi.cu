@@ -6,6 +6,9 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <cstring>
 #include <new>
 #include <string>
@@ -18,7 +21,7 @@ namespace raftgp {
 
 const char *const kKernelNames[K_NUM] = {
     "csr_count", "scan", "csr_scatter", "csr_sort_warp", "csr_sort_block", "csr_compact", "degree_scalars",
-    "sketch", "g_partials", "g_final", "feature_hop", "transform", "gcn_hop", "hop_generic", "misc", "csr_partition", "csr_bucket_sort", "row_order", "model_select", "select_seed", "select_lloyd", "select_split", "gemm_tf32x3", "gemm_tile", "wide_hop", "sbm_setup", "sbm_walk", "stream_update"};
+    "sketch", "g_partials", "g_final", "feature_hop", "transform", "gcn_hop", "hop_generic", "misc", "csr_partition", "csr_bucket_sort", "row_order", "model_select", "select_seed", "select_lloyd", "select_split", "gemm_tf32x3", "gemm_tile", "wide_hop", "sbm_setup", "sbm_walk", "stream_update", "exchange", "push_copy"};
 
 static thread_local std::string g_last_error;
 
@@ -46,8 +49,8 @@ static cudaEvent_t take_event(raftgp_ctx ctx) {
     return e;
 }
 
-LaunchScope::LaunchScope(raftgp_ctx c, int k) : ctx(c), kid(k) {
-    ctx->launches += 1;
+LaunchScope::LaunchScope(raftgp_ctx c, int k, bool count) : ctx(c), kid(k) {
+    if (count) ctx->launches += 1;
     if (ctx->prof) {
         a = take_event(ctx);
         b = take_event(ctx);
@@ -157,14 +160,15 @@ raftgp_status dalloc(raftgp_ctx ctx, void **p, size_t bytes) {
         ctx->free_blocks.erase(it);
         return RAFTGP_OK;
     }
-    cudaError_t e = cudaMallocAsync(p, want, ctx->stream);
+    cudaError_t e = cudaMallocFromPoolAsync(p, want, ctx->pool, ctx->stream);
     if (e == cudaErrorMemoryAllocation && !ctx->free_blocks.empty()) {   // give the cache back, retry once
         cudaGetLastError();
         for (auto &kv : ctx->free_blocks) cudaFreeAsync(kv.second, ctx->stream);
         ctx->free_blocks.clear();
         ctx->cached_bytes = 0;
         cudaStreamSynchronize(ctx->stream);
-        e = cudaMallocAsync(p, want, ctx->stream);
+        cudaMemPoolTrimTo(ctx->pool, 0);
+        e = cudaMallocFromPoolAsync(p, want, ctx->pool, ctx->stream);
     }
     if (e != cudaSuccess) {
         *p = nullptr;
@@ -191,6 +195,21 @@ void release_cache(raftgp_ctx ctx) {
     for (auto &kv : ctx->free_blocks) cudaFreeAsync(kv.second, ctx->stream);
     ctx->free_blocks.clear();
     ctx->cached_bytes = 0;
+}
+
+raftgp_status per_device(int device, const void *key, int *value, const std::function<raftgp_status(int *)> &init) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void *>, int> done;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = done.find({device, key});
+    if (it == done.end()) {
+        int v = 0;
+        const raftgp_status st = init(&v);
+        if (st != RAFTGP_OK) return st;
+        it = done.emplace(std::make_pair(device, key), v).first;
+    }
+    if (value) *value = it->second;
+    return RAFTGP_OK;
 }
 
 }  // namespace raftgp
@@ -220,9 +239,12 @@ static raftgp_status need_ready(raftgp_graph g) {
 
 namespace raftgp {
 
+void dist_comm_destroy(raftgp_ctx ctx);   // dist.cu
+
 static void ctx_teardown(raftgp_ctx ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    dist_comm_destroy(ctx);
     for (auto &r : ctx->recs) {
         cudaEventDestroy(r.start);
         cudaEventDestroy(r.stop);
@@ -230,6 +252,7 @@ static void ctx_teardown(raftgp_ctx ctx) {
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
     release_cache(ctx);
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->pool) cudaMemPoolDestroy(ctx->pool);   // blocks still live (caller never freed them) are released too
     if (ctx->side) {
         cudaStreamSynchronize(ctx->side);
         cudaStreamDestroy(ctx->side);
@@ -267,12 +290,19 @@ raftgp_status raftgp_ctx_create(int device, void *cuda_stream, raftgp_ctx *out) 
     c->stream = static_cast<cudaStream_t>(cuda_stream);   // NULL = the legacy default stream
     c->own_stream = false;
     cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
-    // keep freed blocks in the stream-ordered pool (hot calls then never hit the driver allocator)
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    // the context's own stream-ordered pool: freed blocks stay reserved in it (hot calls never reach the driver
+    // allocator) without changing the device's default pool, which other cudaMallocAsync users share
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaError_t pe = cudaMemPoolCreate(&c->pool, &props);
+    if (pe != cudaSuccess) {
+        delete c;
+        return cuda_fail(pe, "cudaMemPoolCreate");
     }
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr);
     *out = c;
     return RAFTGP_OK;
     RG_GUARD_END
@@ -289,6 +319,7 @@ raftgp_status raftgp_ctx_trim(raftgp_ctx ctx, int64_t *bytes_released) {
     const int64_t b = (int64_t)ctx->cached_bytes;
     release_cache(ctx);
     RG_CUDA(cudaStreamSynchronize(ctx->stream));
+    RG_CUDA(cudaMemPoolTrimTo(ctx->pool, 0));   // the pool's unused memory goes back to the device
     if (bytes_released) *bytes_released = b;
     return RAFTGP_OK;
 }
@@ -436,6 +467,9 @@ raftgp_status raftgp_graph_set_order(raftgp_graph g, const int32_t *order_dev) {
         g->order = nullptr;
         return RAFTGP_OK;
     }
+    bool ok = true;
+    RG_TRY(order_is_permutation(g->ctx, order_dev, g->nl, &ok));
+    if (!ok) return fail(RAFTGP_ERR_PARAM, "order is not a permutation of the local rows 0..rows-1");
     if (g->order == nullptr && g->nl > 0) RG_TRY(dalloc_t(g->ctx, &g->order, (size_t)g->nl));
     if (g->nl > 0)
         RG_TRY(dcopy(g->ctx, g->order, order_dev, sizeof(int32_t) * g->nl));
@@ -1036,6 +1070,32 @@ raftgp_status raftgp_stream_destroy(raftgp_stream s) {
     return RAFTGP_OK;
 }
 
+// ---------------------------------------------------------------- row-partitioned build + embed (dist.cu)
+static raftgp_status build_embed_partitioned(raftgp_ctx ctx, int32_t P, bool loopback, int64_t n, int64_t m,
+                                             const int32_t *src, const int32_t *dst, uint32_t flags, int32_t nvariants,
+                                             const int32_t *variants, int32_t layers, const int32_t *dims, uint64_t seed,
+                                             float *const *Z_dev) {
+    int seen[3] = {0, 0, 0};
+    for (int v = 0; v < nvariants; ++v) {
+        if (variants[v] < 0 || variants[v] > 2) return fail(RAFTGP_ERR_PARAM, "bad variant");
+        if (seen[variants[v]]++) return fail(RAFTGP_ERR_PARAM, "variant listed twice");
+        if (n > 0 && !Z_dev[v]) return fail(RAFTGP_ERR_PARAM, "null Z");
+        if (Z_dev[v] && !aligned16(Z_dev[v])) return fail(RAFTGP_ERR_PARAM, "Z must be 16-byte aligned");
+    }
+    const int32_t *dsrc = src, *ddst = dst;
+    int32_t *tmp = nullptr;
+    if (flags == RAFTGP_HOST_PTRS && m > 0) {
+        RG_TRY(dalloc_t(ctx, &tmp, 2 * (size_t)m));
+        RG_CUDA(cudaMemcpyAsync(tmp, src, sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
+        RG_CUDA(cudaMemcpyAsync(tmp + m, dst, sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
+        dsrc = tmp;
+        ddst = tmp + m;
+    }
+    raftgp_status st = dist_build_embed(ctx, P, loopback, n, m, dsrc, ddst, nvariants, variants, layers, dims, seed, Z_dev);
+    dfree(ctx, tmp);
+    return st;
+}
+
 // ---------------------------------------------------------------- build + embed with overlap
 // raftgp_build_csr + raftgp_embed_multi in one call. Theta' = Theta W^(1) depends only on the seed, so it is
 // generated on a side stream (tensor cores / ALUs) while the CSR build (atomics / HBM) runs on the context
@@ -1051,6 +1111,11 @@ raftgp_status raftgp_build_embed(raftgp_ctx ctx, int64_t n, int64_t m, const int
     if (n < 0 || n >= (int64_t)INT32_MAX || m < 0 || flags > 1u || (m > 0 && (!src || !dst)))
         return fail(RAFTGP_ERR_PARAM, "bad graph arguments");
     RG_TRY(set_device(ctx));
+    if (ctx->nccl) {   // distributed context: the row-partitioned step (dist.cu)
+        if (g_out) return fail(RAFTGP_ERR_PARAM, "distributed build_embed returns no graph handle (g_out must be NULL)");
+        return build_embed_partitioned(ctx, ctx->world, false, n, m, src, dst, flags, nvariants, variants, layers, dims,
+                                       seed, Z_dev);
+    }
     const int32_t r = dims[0], l1 = dims[1];
     const bool overlap = sketch_w_supported(r, l1) && !wide_supported(layers, dims) && n > 0;
     float *W1 = nullptr, *thw = nullptr;
@@ -1096,6 +1161,21 @@ raftgp_status raftgp_build_embed(raftgp_ctx ctx, int64_t n, int64_t m, const int
     if (st == RAFTGP_OK && g_out) *g_out = g;
     else if (g) raftgp_graph_destroy(g);
     return st;
+    RG_GUARD_END
+}
+
+raftgp_status raftgp_build_embed_loopback(raftgp_ctx ctx, int32_t P, int64_t n, int64_t m, const int32_t *src,
+                                          const int32_t *dst, uint32_t flags, int32_t nvariants, const int32_t *variants,
+                                          int32_t layers, const int32_t *dims, uint64_t seed, float *const *Z_dev) {
+    RG_GUARD_BEGIN
+    if (!ctx) return fail(RAFTGP_ERR_PARAM, "null ctx");
+    RG_TRY(check_dims(layers, dims));
+    if (P < 1 || P > kMaxPush) return fail(RAFTGP_ERR_PARAM, "P must be in [1, 8]");
+    if (nvariants < 1 || !variants || !Z_dev) return fail(RAFTGP_ERR_PARAM, "need >= 1 variant and Z outputs");
+    if (n < 0 || n >= (int64_t)INT32_MAX || m < 0 || flags > 1u || (m > 0 && (!src || !dst)))
+        return fail(RAFTGP_ERR_PARAM, "bad graph arguments");
+    RG_TRY(set_device(ctx));
+    return build_embed_partitioned(ctx, P, true, n, m, src, dst, flags, nvariants, variants, layers, dims, seed, Z_dev);
     RG_GUARD_END
 }
 

@@ -1012,8 +1012,8 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
         RG_TRY(dalloc_t(ctx, &fb_count, 1));
         RG_TRY(dzero(ctx, fb_count, sizeof(int32_t), st));
         const size_t bsmem = (size_t)(kBucketCap + 3 * kMaxBucketRows + 1) * 4;
-        static bool attrs = false;
-        if (!attrs) {
+        static const char attrs_key = 0;   // per-(device, instantiation) key
+        RG_TRY(per_device(ctx->device, &attrs_key, nullptr, [&](int *) -> raftgp_status {
             RG_CUDA(cudaFuncSetAttribute(csr_bucket_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets32 * 4));
             RG_CUDA(cudaFuncSetAttribute(csr_partition<true, long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 12));
             RG_CUDA(cudaFuncSetAttribute(csr_partition<false, long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 12));
@@ -1021,8 +1021,8 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
             RG_CUDA(cudaFuncSetAttribute(csr_partition<false, unsigned int>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets32 * 8));
             RG_CUDA(cudaFuncSetAttribute(csr_bucket_sort<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
             RG_CUDA(cudaFuncSetAttribute(csr_bucket_sort<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
-            attrs = true;
-        }
+            return RAFTGP_OK;
+        }));
         {
             LaunchScope L(ctx, K_CSR_COUNT);
             csr_bucket_count<<<pgrid, 1024, (size_t)nb * 4, st>>>(src, dst, m, n, rb, re, shift, nb, bcnt, err);
@@ -1092,12 +1092,12 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
         RG_CHECK_LAUNCH(ctx);
     }
     if (nl > 0) {
-        static bool attr_set = false;
-        if (!attr_set) {
+        static const char attr_set_key = 0;   // per-(device, instantiation) key
+        RG_TRY(per_device(ctx->device, &attr_set_key, nullptr, [&](int *) -> raftgp_status {
             RG_CUDA(cudaFuncSetAttribute(csr_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kBlockSortSmemCap * (int)sizeof(int32_t)));
-            attr_set = true;
-        }
+            return RAFTGP_OK;
+        }));
         LaunchScope L(ctx, K_CSR_SORT_BLOCK);
         csr_sort_block<<<ctx->sm_count, 1024, kBlockSortSmemCap * sizeof(int32_t), st>>>(big_rows, big_count, raw_ptr,
                                                                                          col_raw, g->deg_local);

@@ -9,6 +9,7 @@
 #include <string>
 #include <unordered_map>
 #include <atomic>
+#include <functional>
 #include <vector>
 
 #include "../../include/raftgp.h"
@@ -45,6 +46,8 @@ enum KernelId : int {
     K_SBM,
     K_SBM_WALK,
     K_STREAM,
+    K_EXCHANGE,     // NCCL collectives of the row-partitioned path (barrier, all-gathers; not counted as our launches)
+    K_PUSH_COPY,    // deferred push of a finished operand block into the peers' copies (dist.cu)
     K_NUM
 };
 extern const char *const kKernelNames[K_NUM];
@@ -52,6 +55,17 @@ extern const char *const kKernelNames[K_NUM];
 struct ProfRec {
     int kid;
     cudaEvent_t start, stop;
+};
+
+// Operand copies of the row-partitioned path (dist.cu), cached in the context across steps: for every slot (Theta'
+// and the GCN operands T_k) an n_pad x width buffer on this GPU plus the peers' buffers mapped through CUDA IPC.
+struct DistBufs {
+    int64_t rows = 0;                       // P * R (padded: ncclAllGather in place needs equal blocks)
+    std::vector<int32_t> widths;            // per slot
+    std::vector<float *> own;               // per slot: this rank's copy (cudaMalloc: IPC-exportable)
+    std::vector<std::vector<float *>> rep;  // per slot: [q] = rank q's copy (rep[s][rank] == own[s])
+    bool mapped = false;                    // peers' copies mapped: pushes fused into the producing kernels;
+                                            // else every rank holds its own copy only, completed by all-gathers
 };
 
 }  // namespace raftgp
@@ -65,6 +79,7 @@ struct raftgp_ctx_s {
     void *mbox_d = nullptr;
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;   // library-owned side stream (overlapped work inside one call)
+    cudaMemPool_t pool = nullptr;  // this context's own stream-ordered pool (release threshold: keep everything)
     bool own_stream = false;
     int sm_count = 148;
     int64_t launches = 0;
@@ -76,6 +91,11 @@ struct raftgp_ctx_s {
     std::multimap<size_t, void *> free_blocks;
     std::unordered_map<void *, size_t> live_blocks;
     size_t cached_bytes = 0;
+    // row-partitioned contexts (raftgp_ctx_create_dist): NCCL communicator over `world` ranks, one per GPU
+    void *nccl = nullptr;          // ncclComm_t
+    int rank = 0, world = 1;
+    float *dist_flag = nullptr;    // 1-element operand of the stream-ordered barrier (all-reduce)
+    raftgp::DistBufs dist;         // cached operand copies (dist.cu)
 };
 
 struct raftgp_graph_s {
@@ -139,6 +159,13 @@ raftgp_status cuda_fail(cudaError_t e, const char *what);
         if (_s != RAFTGP_OK) return _s;          \
     } while (0)
 
+// ---------------------------------------------------------------- per-device one-time setup
+// Kernel attributes (dynamic shared-memory limits) and occupancy results belong to a device context, so they are
+// set / computed once per (device, kernel): a process with contexts on several GPUs gets them on each device.
+// Thread-safe. `init` runs at most once per (device, key) (again if it failed) and may store an int (e.g. CTAs
+// per SM) that later calls receive in *value.
+raftgp_status per_device(int device, const void *key, int *value, const std::function<raftgp_status(int *)> &init);
+
 // ---------------------------------------------------------------- launch accounting
 // Scope object placed around ONE kernel launch: counts it, and when profiling is on records CUDA
 // events before/after it on the context stream.
@@ -146,7 +173,8 @@ struct LaunchScope {
     raftgp_ctx ctx;
     int kid;
     cudaEvent_t a = nullptr, b = nullptr;
-    LaunchScope(raftgp_ctx c, int k);
+    // count = false: a library call that is not one of our kernels (NCCL), timed but not counted as a launch
+    LaunchScope(raftgp_ctx c, int k, bool count = true);
     ~LaunchScope();
 };
 
@@ -180,7 +208,9 @@ raftgp_status scan_i32_to_i64(raftgp_ctx ctx, const int32_t *in, int64_t *out, i
 raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src, const int32_t *dst, int64_t rb,
                         int64_t re, raftgp_graph g);
 raftgp_status degrees_finalize(raftgp_graph g);
-raftgp_status compute_order(raftgp_graph g);      // g->order (label propagation + counting sort)   // deg_all -> two_e, s_all, sh_all, deg_hist
+raftgp_status compute_order(raftgp_graph g);
+// whether order[0..nl) is a permutation of 0..nl-1 (device check, synchronous)
+raftgp_status order_is_permutation(raftgp_ctx ctx, const int32_t *order, int64_t nl, bool *ok);      // g->order (label propagation + counting sort)   // deg_all -> two_e, s_all, sh_all, deg_hist
 
 raftgp_status sketch_fill(raftgp_ctx ctx, uint64_t seed, uint32_t tag, int64_t row_begin, int64_t rows, int32_t cols,
                           int32_t den, float *out);
@@ -188,10 +218,19 @@ raftgp_status sketch_fill(raftgp_ctx ctx, uint64_t seed, uint32_t tag, int64_t r
 raftgp_status sketch_theta(raftgp_graph g, uint64_t seed, int32_t r, float *theta, double *g_out);
 // g = d^T X over all n rows (fp64, fixed chunk order); X is n x r
 raftgp_status g_reduce(raftgp_graph g, const float *X, int32_t r, double *g_out);
+// the same in two steps (row-partitioned path): per-chunk partial sums of the global chunks chunk0 .. chunk0+count-1
+// (partial[chunk * r + c]; X holds all n rows), then the sum over all chunks in chunk order
+int64_t g_chunks(int64_t n);
+int64_t g_chunk_rows();
+raftgp_status g_partials_range(raftgp_graph g, const float *X, int32_t r, int64_t chunk0, int64_t count, double *partial);
+raftgp_status g_final_chunks(raftgp_ctx ctx, const double *partial, int64_t nchunks, int32_t r, double *g_out);
 // Theta' = Theta W1 (Theta generated on chip, n x l1 written) and optionally g' = d^T Theta'
 bool sketch_w_supported(int32_t r, int32_t l1);
 // Theta' = Theta W1 on tcgen05 tensor cores (3xTF32, fp32-accurate), Theta generated on chip
 raftgp_status sketch_w_tc(raftgp_ctx ctx, uint64_t seed, int64_t n, int32_t r, const float *W1, int32_t l1, float *out);
+// rows row0 .. row0 + rows - 1 of Theta', each stored at its global row into all nout copies (row-partitioned path)
+raftgp_status sketch_w_tc_rows(raftgp_ctx ctx, uint64_t seed, int64_t row0, int64_t rows, int32_t r, const float *W1,
+                               int32_t l1, float *const *outs, int nout);
 raftgp_status sketch_w_any(raftgp_ctx ctx, uint64_t seed, int64_t n, int32_t r, const float *W1, int32_t l1, float *out);
 raftgp_status sketch_theta_w(raftgp_graph g, uint64_t seed, int32_t r, const float *W1, int32_t l1, float *out,
                              double *g_out);
@@ -211,7 +250,10 @@ struct PushSpec {
     float *rep[kMaxPush];
     float *rep2[kMaxPush];
     int nrep;
+    int nrep2;      // replicas of the second variant's rows (dual kernels); 0 = nrep. 1 = this rank's copy only (its
+                    // push to the peers is deferred to a copy kernel on another stream, dist.cu)
     int64_t row0;
+    int32_t ld;     // row stride of the replicas in floats (0 = the row width); > width for interleaved operands
 };
 // Feature hop on a pre-transformed operand Theta' = Theta W1 (no epilogue GEMM): writes
 // T1 = s^ (.) (X Theta') for NCUT (T_ncut) and/or MOD (T_mod), or MOD_REDUCED (T_ncut slot, variant 2).
@@ -253,6 +295,12 @@ void stream_destroy(raftgp_stream s);
 raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c, const double *theta,
                          const double *omega, uint64_t seed, int32_t q, int32_t *src, int32_t *dst, int64_t cap,
                          int64_t *m_out);
+// Row-partitioned path (dist.cu). P ranks; `loopback`: all P ranks are simulated in this process on this ctx's GPU
+// (one stream, lockstep stages; tests), else this ctx is rank ctx->rank of an NCCL communicator.
+raftgp_status dist_build_embed(raftgp_ctx ctx, int P, bool loopback, int64_t n, int64_t m, const int32_t *src,
+                               const int32_t *dst, int32_t nvariants, const int32_t *variants, int32_t layers,
+                               const int32_t *dims, uint64_t seed, float *const *Z_dev);
+void dist_release(raftgp_ctx ctx);   // drop the cached operand copies (collective on NCCL contexts)
 // NEXT-1: Alg. 1 hierarchical model selection (select.cu)
 raftgp_status model_select(raftgp_graph g, const float *Z, int32_t L, int32_t eps, int32_t max_iter, int32_t rule,
                            int32_t *labels, int32_t *num_blocks, int64_t *stats);

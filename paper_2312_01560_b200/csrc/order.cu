@@ -129,6 +129,45 @@ __global__ void heavy_place(const int32_t *__restrict__ flag, const int64_t *__r
     order[pos] = (int32_t)i;
 }
 
+namespace {
+// order validation: cnt[v] += 1 for every listed row (err if out of range), then err if any cnt != 1
+__global__ void order_count(const int32_t *__restrict__ order, int64_t nl, int32_t *cnt, int32_t *err) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nl; t += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = order[t];
+        if (v < 0 || (int64_t)v >= nl) atomicOr(err, 1);
+        else atomicAdd(cnt + v, 1);
+    }
+}
+__global__ void order_check(const int32_t *__restrict__ cnt, int64_t nl, int32_t *err) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nl; t += (int64_t)gridDim.x * blockDim.x)
+        if (cnt[t] != 1) atomicOr(err, 2);
+}
+}  // namespace
+
+raftgp_status order_is_permutation(raftgp_ctx ctx, const int32_t *order, int64_t nl, bool *ok) {
+    *ok = true;
+    if (nl == 0) return RAFTGP_OK;
+    int32_t *cnt = nullptr;
+    RG_TRY(dalloc_t(ctx, &cnt, (size_t)nl + 1));
+    RG_TRY(dzero(ctx, cnt, sizeof(int32_t) * ((size_t)nl + 1)));
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(nl, 256), (int64_t)ctx->sm_count * 8);
+    {
+        LaunchScope L(ctx, K_MISC);
+        order_count<<<grid, 256, 0, ctx->stream>>>(order, nl, cnt, cnt + nl);
+    }
+    RG_CHECK_LAUNCH(ctx);
+    {
+        LaunchScope L(ctx, K_MISC);
+        order_check<<<grid, 256, 0, ctx->stream>>>(cnt, nl, cnt + nl);
+    }
+    RG_CHECK_LAUNCH(ctx);
+    int32_t err = 0;
+    RG_TRY(dread(ctx, &err, cnt + nl, sizeof(int32_t)));
+    dfree(ctx, cnt);
+    *ok = err == 0;
+    return RAFTGP_OK;
+}
+
 raftgp_status compute_order(raftgp_graph g) {
     static const int rounds = [] {
         const char *e = getenv("RAFTGP_ORDER_ROUNDS");

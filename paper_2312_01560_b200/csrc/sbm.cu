@@ -557,12 +557,15 @@ raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c,
         if (rs == RAFTGP_OK) rs = dalloc_t(ctx, &mbase, (size_t)K * ntiles + 1);
         if (rs == RAFTGP_OK) rs = dalloc_t(ctx, &mboff, (size_t)K + 1);
         if (rs == RAFTGP_OK) rs = dalloc_t(ctx, &mmem, (size_t)std::max<int64_t>(n, 1));
-        static bool attrs = false;
-        if (rs == RAFTGP_OK && !attrs) {
-            cudaFuncSetAttribute(sbm_member_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kMemWarps * kMemMaxK * 4);
-            cudaFuncSetAttribute(sbm_member_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kMemWarps * kMemMaxK * 8);
-            attrs = true;
-        }
+        static const char attrs_key = 0;
+        if (rs == RAFTGP_OK)
+            rs = per_device(ctx->device, &attrs_key, nullptr, [&](int *) -> raftgp_status {
+                RG_CUDA(cudaFuncSetAttribute(sbm_member_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kMemWarps * kMemMaxK * 4));
+                RG_CUDA(cudaFuncSetAttribute(sbm_member_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kMemWarps * kMemMaxK * 8));
+                return RAFTGP_OK;
+            });
         const unsigned mg = (unsigned)ceil_div(ntiles, kMemWarps);
         if (rs == RAFTGP_OK) {
             LaunchScope LS(ctx, K_SBM);
@@ -674,11 +677,15 @@ raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c,
         const int64_t log_cap = !slots ? 0 : log_env >= 0 ? log_env : std::max<int64_t>(1 << 20, nchunks);
         if (s2 == RAFTGP_OK && log_cap > 0 && dalloc(ctx, reinterpret_cast<void **>(&logb), (size_t)log_cap * sizeof(LogEnt)) != RAFTGP_OK)
             logb = nullptr;
-        static int walk_blocks = [] {
-            int b = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sbm_walk<false>, 128, 0);
-            return std::max(1, b);
-        }();
+        static const char walk_key = 0;
+        int walk_blocks = 1;
+        if (s2 == RAFTGP_OK)
+            s2 = per_device(ctx->device, &walk_key, &walk_blocks, [&](int *v) -> raftgp_status {
+                int b = 0;
+                RG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sbm_walk<false>, 128, 0));
+                *v = std::max(1, b);
+                return RAFTGP_OK;
+            });
         auto wgrid = [&](int64_t items) {
             return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, 128), (int64_t)ctx->sm_count * walk_blocks));
         };

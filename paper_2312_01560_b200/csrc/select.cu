@@ -776,19 +776,19 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
     const int64_t n = g->n;
     constexpr size_t kRowSmem = (size_t)kRowWarps * 2 * 32 * (L + 4) * sizeof(float);
     constexpr size_t kPruneSmem = (size_t)kPruneWarps * 32 * (L + 4) * sizeof(float);
-    static bool attrs = false;
-    static int prune_ctas = 1;
-    if (!attrs) {
+    static const char attrs_key = 0;   // per-(device, L) key
+    int prune_ctas = 1;
+    RG_TRY(per_device(ctx->device, &attrs_key, &prune_ctas, [&](int *v) -> raftgp_status {
         RG_CUDA(cudaFuncSetAttribute(sel_rows<L, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem));
         RG_CUDA(cudaFuncSetAttribute(sel_rows<L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem));
         RG_CUDA(cudaFuncSetAttribute(sel_rows<L, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem));
         RG_CUDA(cudaFuncSetAttribute(sel_lloyd_pruned<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)kPruneSmem));
-        RG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&prune_ctas, sel_lloyd_pruned<L>, kPruneWarps * 32,
-                                                              kPruneSmem));
-        prune_ctas = std::max(1, prune_ctas);
-        attrs = true;
-    }
+        int b = 0;
+        RG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sel_lloyd_pruned<L>, kPruneWarps * 32, kPruneSmem));
+        *v = std::max(1, b);
+        return RAFTGP_OK;
+    }));
 
     int32_t *perm = nullptr, *pseg = nullptr, *side = nullptr, *nperm = nullptr, *npseg = nullptr;
     int32_t *node_key = nullptr, *label_tmp = nullptr, *err = nullptr;

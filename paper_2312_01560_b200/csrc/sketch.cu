@@ -49,8 +49,8 @@ __global__ void __launch_bounds__(256) gauss_fill(uint64_t seed, uint32_t tag, i
 
 // partial[chunk][c] = sum_{j in chunk, sequential} d_j * theta[j][c]   (fp64)
 __global__ void __launch_bounds__(128) g_partials(const float *__restrict__ theta, const int32_t *__restrict__ deg,
-                                                  int64_t n, int32_t r, double *__restrict__ partial) {
-    const int64_t chunk = blockIdx.x;
+                                                  int64_t n, int32_t r, int64_t chunk0, double *__restrict__ partial) {
+    const int64_t chunk = chunk0 + blockIdx.x;
     const int64_t j0 = chunk * kGChunk, j1 = min(n, j0 + (int64_t)kGChunk);
     // blockIdx.y picks a 128-column slice (wide operands); each (chunk, column) sum stays sequential in j
     for (int c = blockIdx.y * blockDim.x + threadIdx.x; c < r; c += gridDim.y * blockDim.x) {
@@ -146,11 +146,11 @@ __global__ void __launch_bounds__(256, 2) sketch_w_kernel(uint64_t seed, int64_t
 template <int R, int L1>
 raftgp_status launch_sketch_w(raftgp_ctx ctx, uint64_t seed, int64_t n, float sigma, const float *W1, float *out) {
     const size_t smem = sizeof(float) * ((size_t)R * L1 + 128 * 36);
-    static bool attr = false;
-    if (!attr) {
+    static const char attr_key = 0;   // per-(device, instantiation) key
+    RG_TRY(per_device(ctx->device, &attr_key, nullptr, [&](int *) -> raftgp_status {
         RG_CUDA(cudaFuncSetAttribute(sketch_w_kernel<R, L1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+        return RAFTGP_OK;
+    }));
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 128), 2 * ctx->sm_count)));
     {
         LaunchScope L(ctx, K_SKETCH);
@@ -229,18 +229,35 @@ raftgp_status g_reduce(raftgp_graph g, const float *theta, int32_t r, double *g_
     }
     double *partial = nullptr;
     RG_TRY(dalloc_t(ctx, &partial, (size_t)nchunks * r));
+    RG_TRY(g_partials_range(g, theta, r, 0, nchunks, partial));
+    RG_TRY(g_final_chunks(ctx, partial, nchunks, r, g_out));
+    dfree(ctx, partial);
+    return RAFTGP_OK;
+}
+
+int64_t g_chunks(int64_t n) { return ceil_div(n, kGChunk); }
+int64_t g_chunk_rows() { return kGChunk; }
+
+raftgp_status g_partials_range(raftgp_graph g, const float *theta, int32_t r, int64_t chunk0, int64_t count,
+                               double *partial) {
+    raftgp_ctx ctx = g->ctx;
+    if (count <= 0) return RAFTGP_OK;
     {
         LaunchScope L(ctx, K_SKETCH_G);
-        g_partials<<<dim3((unsigned)nchunks, (unsigned)ceil_div(r, 128)), 128, 0, ctx->stream>>>(theta, g->deg_all, g->n,
-                                                                                                r, partial);
+        g_partials<<<dim3((unsigned)count, (unsigned)ceil_div(r, 128)), 128, 0, ctx->stream>>>(theta, g->deg_all, g->n,
+                                                                                               r, chunk0, partial);
     }
     RG_CHECK_LAUNCH(ctx);
+    return RAFTGP_OK;
+}
+
+raftgp_status g_final_chunks(raftgp_ctx ctx, const double *partial, int64_t nchunks, int32_t r, double *g_out) {
+    if (nchunks == 0) return dzero(ctx, g_out, sizeof(double) * r);
     {
         LaunchScope L(ctx, K_G_FINAL);
         g_final<<<(unsigned)ceil_div(r, 32), 32, 0, ctx->stream>>>(partial, nchunks, r, g_out);
     }
     RG_CHECK_LAUNCH(ctx);
-    dfree(ctx, partial);
     return RAFTGP_OK;
 }
 

@@ -292,9 +292,12 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
             } else if (sub == 0) {
                 if (WN == 0 && a.push.nrep > 0) {   // fused exchange: this row into every rank's copy of T
                     const int64_t grow = a.push.row0 + row;
-                    for (int r = 0; r < a.push.nrep; ++r) {
-                        reinterpret_cast<float4 *>(a.push.rep[r])[grow * LPN + cl] = y;
-                        if constexpr (NV == 2) reinterpret_cast<float4 *>(a.push.rep2[r])[grow * LPN + cl] = y2;
+                    const int64_t ld4 = a.push.ld > 0 ? a.push.ld / 4 : LPN;
+                    for (int r = 0; r < a.push.nrep; ++r)
+                        reinterpret_cast<float4 *>(a.push.rep[r])[grow * ld4 + cl] = y;
+                    if constexpr (NV == 2) {
+                        const int n2 = a.push.nrep2 > 0 ? a.push.nrep2 : a.push.nrep;
+                        for (int r = 0; r < n2; ++r) reinterpret_cast<float4 *>(a.push.rep2[r])[grow * ld4 + cl] = y2;
                     }
                 } else {
                     if (a.out != nullptr) reinterpret_cast<float4 *>(a.out)[row * LPN + cl] = y;
@@ -351,8 +354,10 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
                         const float4 t4 = make_float4(shi * o[q].x, shi * o[q].y, shi * o[q].z, shi * o[q].w);
                         if (a.push.nrep > 0) {   // fused exchange (see PushSpec)
                             const int64_t grow = a.push.row0 + row;
-                            for (int r = 0; r < a.push.nrep; ++r)
-                                reinterpret_cast<float4 *>(v == 0 ? a.push.rep[r] : a.push.rep2[r])[grow * OL + oc] = t4;
+                            const int64_t pl4 = a.push.ld > 0 ? a.push.ld / 4 : OL;
+                            const int nr = (v == 0 || a.push.nrep2 == 0) ? a.push.nrep : a.push.nrep2;
+                            for (int r = 0; r < nr; ++r)
+                                reinterpret_cast<float4 *>(v == 0 ? a.push.rep[r] : a.push.rep2[r])[grow * pl4 + oc] = t4;
                         } else {
                             float4 *T4 = reinterpret_cast<float4 *>(v == 0 ? a.Tn : a.Tn2);
                             const int64_t ld4 = a.tn_ld > 0 ? a.tn_ld / 4 : OL;
@@ -373,7 +378,8 @@ __global__ void __launch_bounds__(128) hop_generic(HopArgs a, int W, int WN) {
     extern __shared__ float gsm[];   // W floats (the finished row) + 32 scratch
     float *rowbuf = gsm;
     float *red = gsm + W;
-    for (int64_t row = blockIdx.x; row < a.nl; row += gridDim.x) {
+    for (int64_t t = blockIdx.x; t < a.nl; t += gridDim.x) {
+        const int64_t row = a.order ? a.order[t] : t;   // visiting order / row list (streaming), like the fast kernels
         const int64_t gi = a.rb + row;
         float part = 0.f;
         for (int c = threadIdx.x; c < W; c += blockDim.x) {
@@ -442,13 +448,16 @@ raftgp_status launch_fast(raftgp_ctx ctx, const HopArgs &a) {
     constexpr int WPB = THREADS / 32;
     constexpr int NV = KindTraits<KIND>::NV;
     const size_t smem = sizeof(float) * ((size_t)W * WN + (WN > 0 ? (size_t)WPB * NV * RB * W : 0));
-    static int blocks_per_sm = -1;
+    static const char occ_key = 0;   // per-(device, instantiation) key
+    int blocks_per_sm = 1;
     auto kern = hop_kernel<KIND, W, WN, RB, U, THREADS>;
-    if (blocks_per_sm < 0) {
+    RG_TRY(per_device(ctx->device, &occ_key, &blocks_per_sm, [&](int *v) -> raftgp_status {
         RG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        RG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, THREADS, smem));
-        if (blocks_per_sm < 1) blocks_per_sm = 1;
-    }
+        int b = 0;
+        RG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, THREADS, smem));
+        *v = b < 1 ? 1 : b;
+        return RAFTGP_OK;
+    }));
     const int64_t groups = ceil_div(a.nl, RB);
     const int64_t want = ceil_div(groups, WPB);
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count * blocks_per_sm)));
@@ -496,13 +505,17 @@ raftgp_status dispatch(raftgp_ctx ctx, const HopArgs &a, int w, int wn) {
             default: return dispatch_wn<KIND, 128>(ctx, a, wn);
         }
     }
+    // the generic kernel implements the plain hop only: the fused exchange, strided T_next and the s^ row scale
+    // of the pre-transformed feature hop exist only in the fast kernels (their callers check the fast path first)
+    if (a.push.nrep > 0 || a.scale_sh || (a.tn_ld > 0 && a.tn_ld != wn))
+        return fail(RAFTGP_ERR_INTERNAL, "hop: push / strided output / s^ scale need the fast kernel");
     const size_t smem = sizeof(float) * ((size_t)w + 32);
     if (smem > 48 * 1024) {
-        static bool set = false;
-        if (!set) {
+        static const char set_key = 0;   // per-(device, instantiation) key
+        RG_TRY(per_device(ctx->device, &set_key, nullptr, [&](int *) -> raftgp_status {
             RG_CUDA(cudaFuncSetAttribute(hop_generic<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            set = true;
-        }
+            return RAFTGP_OK;
+        }));
     }
     const int grid = static_cast<int>(std::min<int64_t>(a.nl, (int64_t)ctx->sm_count * 16));
     {
@@ -640,8 +653,9 @@ raftgp_status gcn_hop_rows(raftgp_graph g, const float *Tfull, int32_t w, float 
     a.out = Zout;
     a.Wn = Wn;
     a.Tn = Tnext;
-    if (!((w == 32 || w == 64 || w == 128) && (wn == 0 || wn == 32 || wn == 64 || wn == 128)))
-        return fail(RAFTGP_ERR_INTERNAL, "gcn_hop_rows: unsupported width");
+    if (!((w == 32 || w == 64 || w == 128) && (wn == 0 || wn == 32 || wn == 64 || wn == 128) && aligned16(Tfull) &&
+          (!Zout || aligned16(Zout)) && (!Wn || aligned16(Wn)) && (!Tnext || aligned16(Tnext))))
+        return fail(RAFTGP_ERR_INTERNAL, "gcn_hop_rows: unsupported width/alignment");
     return dispatch<KIND_GCN>(g->ctx, a, w, Wn ? wn : 0);
 }
 

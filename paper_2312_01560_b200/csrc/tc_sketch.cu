@@ -36,9 +36,17 @@ using namespace tc;
 constexpr int kTM = 128;       // rows per tile (MMA M)
 constexpr int kKQ = 32;        // K columns per quarter (one of two A buffers)
 
+// Global rows row0 .. row0 + n - 1 of Theta' (Theta's generator row = the global row); each finished row is stored at
+// its global row into every one of the nout output copies (nout > 1: the row-partitioned path pushes its share of
+// Theta' into every rank's copy over NVLink, dist.cu).
+struct SketchOut {
+    float *out[kMaxPush];
+    int nout;
+};
+
 template <int R, int L1>
-__global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t seed, int64_t n, float sigma,
-                                                             const float *__restrict__ W1, float *__restrict__ out) {
+__global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t seed, int64_t row0, int64_t n, float sigma,
+                                                             const float *__restrict__ W1, SketchOut outs) {
     constexpr int KQ = R < kKQ ? R : kKQ;              // K columns per quarter (one A buffer)
     constexpr int NQK = R / KQ;                         // quarters per tile
     constexpr int NCOL = L1 < 32 ? 32 : L1;             // TMEM columns of one accumulator (power of two >= 32)
@@ -96,9 +104,11 @@ __global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t 
             float v[32];
             tmem_ld32(tmem_d + (static_cast<uint32_t>(lq * 32) << 16) + (uint32_t)(acc * NCOL + c0), v);
             if (row < n) {
-                float4 *o = reinterpret_cast<float4 *>(out + row * L1 + c0);
+                for (int q = 0; q < outs.nout; ++q) {
+                    float4 *o = reinterpret_cast<float4 *>(outs.out[q] + (row0 + row) * L1 + c0);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                    for (int i = 0; i < 8; ++i) o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                }
             }
         }
     };
@@ -119,8 +129,8 @@ __global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t 
                 const int row = t % kTM, qq = t / kTM;      // consecutive threads: consecutive rows
                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (r0 + row < n)
-                    v = spec_quad(seed, 0u, static_cast<uint64_t>(r0 + row), static_cast<uint32_t>(q * (KQ / 4) + qq),
-                                  sigma);
+                    v = spec_quad(seed, 0u, static_cast<uint64_t>(row0 + r0 + row),
+                                  static_cast<uint32_t>(q * (KQ / 4) + qq), sigma);
                 const float4 hi = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
                 const float4 lo = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
                 const uint32_t o = kmajor_off(row, 4 * qq, kTM);
@@ -170,45 +180,57 @@ __global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t 
     __syncthreads();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(2 * NCOL));
+    if (outs.nout > 1) __threadfence_system();   // rows stored into the peers' copies are visible to them
 }
 
 template <int R, int L1>
-raftgp_status launch_tc(raftgp_ctx ctx, uint64_t seed, int64_t n, float sigma, const float *W1, float *out) {
+raftgp_status launch_tc(raftgp_ctx ctx, uint64_t seed, int64_t row0, int64_t n, float sigma, const float *W1,
+                        const SketchOut &outs) {
     constexpr int KQ = R < kKQ ? R : kKQ;
     const size_t smem = 2 * (size_t)L1 * R * 4 + 2 * 2 * (size_t)kTM * KQ * 4;
-    static bool attr = false;
-    if (!attr) {
+    static const char attr_key = 0;   // per-(device, instantiation) key
+    RG_TRY(per_device(ctx->device, &attr_key, nullptr, [&](int *) -> raftgp_status {
         RG_CUDA(cudaFuncSetAttribute(sketch_w_tc_kernel<R, L1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+        return RAFTGP_OK;
+    }));
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kTM), ctx->sm_count)));
     {
         LaunchScope L(ctx, K_SKETCH);
-        sketch_w_tc_kernel<R, L1><<<grid, RG_TC_THREADS, smem, ctx->stream>>>(seed, n, sigma, W1, out);
+        sketch_w_tc_kernel<R, L1><<<grid, RG_TC_THREADS, smem, ctx->stream>>>(seed, row0, n, sigma, W1, outs);
     }
     RG_CHECK_LAUNCH(ctx);
     return RAFTGP_OK;
 }
 
 template <int R>
-raftgp_status dispatch_tc(raftgp_ctx ctx, uint64_t seed, int64_t n, float sigma, const float *W1, int l1, float *out) {
+raftgp_status dispatch_tc(raftgp_ctx ctx, uint64_t seed, int64_t row0, int64_t n, float sigma, const float *W1, int l1,
+                          const SketchOut &outs) {
     switch (l1) {
-        case 32: return launch_tc<R, 32>(ctx, seed, n, sigma, W1, out);
-        case 64: return launch_tc<R, 64>(ctx, seed, n, sigma, W1, out);
-        default: return launch_tc<R, 128>(ctx, seed, n, sigma, W1, out);
+        case 32: return launch_tc<R, 32>(ctx, seed, row0, n, sigma, W1, outs);
+        case 64: return launch_tc<R, 64>(ctx, seed, row0, n, sigma, W1, outs);
+        default: return launch_tc<R, 128>(ctx, seed, row0, n, sigma, W1, outs);
     }
 }
 
 }  // namespace
 
-raftgp_status sketch_w_tc(raftgp_ctx ctx, uint64_t seed, int64_t n, int32_t r, const float *W1, int32_t l1, float *out) {
-    if (n == 0) return RAFTGP_OK;
+raftgp_status sketch_w_tc_rows(raftgp_ctx ctx, uint64_t seed, int64_t row0, int64_t rows, int32_t r, const float *W1,
+                               int32_t l1, float *const *outs, int nout) {
+    if (rows == 0) return RAFTGP_OK;
+    if (nout < 1 || nout > kMaxPush) return fail(RAFTGP_ERR_INTERNAL, "sketch_w_tc_rows: 1..8 outputs");
+    SketchOut so{};
+    so.nout = nout;
+    for (int q = 0; q < nout; ++q) so.out[q] = outs[q];
     const float sigma = spec_sigma(r);
     switch (r) {
-        case 32: return dispatch_tc<32>(ctx, seed, n, sigma, W1, l1, out);
-        case 64: return dispatch_tc<64>(ctx, seed, n, sigma, W1, l1, out);
-        default: return dispatch_tc<128>(ctx, seed, n, sigma, W1, l1, out);
+        case 32: return dispatch_tc<32>(ctx, seed, row0, rows, sigma, W1, l1, so);
+        case 64: return dispatch_tc<64>(ctx, seed, row0, rows, sigma, W1, l1, so);
+        default: return dispatch_tc<128>(ctx, seed, row0, rows, sigma, W1, l1, so);
     }
+}
+
+raftgp_status sketch_w_tc(raftgp_ctx ctx, uint64_t seed, int64_t n, int32_t r, const float *W1, int32_t l1, float *out) {
+    return sketch_w_tc_rows(ctx, seed, 0, n, r, W1, l1, &out, 1);
 }
 
 }  // namespace raftgp

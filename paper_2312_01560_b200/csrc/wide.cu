@@ -636,18 +636,19 @@ raftgp_status launch_wide(raftgp_ctx ctx, const WideArgs &a) {
         auto go = [&](auto wtag) -> raftgp_status {
             constexpr int W = decltype(wtag)::value;
             using R = RingCfg<W>;
-            static bool attr = false;
-            static int per_sm = 1;
-            if (!attr) {
+            static const char ring_key = 0;
+            int per_sm = 1;
+            RG_TRY(per_device(ctx->device, &ring_key, &per_sm, [&](int *v) -> raftgp_status {
                 RG_CUDA(cudaFuncSetAttribute(hop_wide_ring<KIND, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)R::SMEM));
                 RG_CUDA(cudaFuncSetAttribute(hop_wide_ring<KIND, W>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                              100));
-                RG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hop_wide_ring<KIND, W>, kRingThreads,
+                int b = 0;
+                RG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, hop_wide_ring<KIND, W>, kRingThreads,
                                                                       R::SMEM));
-                per_sm = std::max(1, per_sm);
-                attr = true;
-            }
+                *v = std::max(1, b);
+                return RAFTGP_OK;
+            }));
             const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.n, (int64_t)ctx->sm_count * per_sm));
             LaunchScope LS(ctx, K_WIDE_HOP);
             hop_wide_ring<KIND, W><<<grid, kRingThreads, R::SMEM, ctx->stream>>>(a);
@@ -697,11 +698,11 @@ template <int NT>
 raftgp_status launch_gemm(raftgp_ctx ctx, const float *Ahi, const float *Alo, const float *Bhi, const float *Blo,
                           int64_t M, int Kp, int N, const float *row_scale, float *C, int64_t ldc) {
     using G = GemmCfg<NT>;
-    static bool attr = false;
-    if (!attr) {
+    static const char attr_key = 0;   // per-(device, instantiation) key
+    RG_TRY(per_device(ctx->device, &attr_key, nullptr, [&](int *) -> raftgp_status {
         RG_CUDA(cudaFuncSetAttribute(gemm_tf32x3<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
-        attr = true;
-    }
+        return RAFTGP_OK;
+    }));
     const int ntn = (int)ceil_div(N, NT);
     const int64_t mtn = ceil_div(M, kGM);
     if (M == 0 || N == 0) return RAFTGP_OK;

@@ -20,7 +20,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("RAFTGP_LIB") or os.path.join(_HERE, "libraftgp.so")
 
 RAFTGP_OK, RAFTGP_ERR_PARAM, RAFTGP_ERR_DATA = 0, 2, 3
-RAFTGP_ERR_INTERNAL, RAFTGP_ERR_CUDA, RAFTGP_ERR_NOMEM, RAFTGP_ERR_STATE = 4, 5, 6, 7
+RAFTGP_ERR_INTERNAL, RAFTGP_ERR_CUDA, RAFTGP_ERR_NOMEM, RAFTGP_ERR_COMM, RAFTGP_ERR_STATE = 4, 5, 6, 7, 8
 RAFTGP_NCUT, RAFTGP_MOD, RAFTGP_MOD_REDUCED = 0, 1, 2
 VARIANTS = {"ncut": RAFTGP_NCUT, "mod": RAFTGP_MOD, "mod_reduced": RAFTGP_MOD_REDUCED}
 RAFTGP_LMOD_GLOBAL, RAFTGP_LMOD_LOCAL = 0, 1
@@ -39,6 +39,8 @@ EXPORTS = (
     "raftgp_stream_add_edges", "raftgp_stream_embedding", "raftgp_stream_graph", "raftgp_stream_destroy",
     "raftgp_build_embed", "raftgp_ctx_trim", "raftgp_feature_transform_push", "raftgp_gcn_hop_push",
     "raftgp_ipc_alloc", "raftgp_ipc_free", "raftgp_ipc_open", "raftgp_ipc_close", "raftgp_copy",
+    "raftgp_nccl_unique_id", "raftgp_ctx_create_dist", "raftgp_ctx_rank", "raftgp_barrier", "raftgp_allgather",
+    "raftgp_build_embed_loopback",
 )
 
 _lib = None
@@ -106,6 +108,13 @@ _SIGS = {
     "raftgp_stream_destroy": (ctypes.c_int, [c_vp]),
     "raftgp_build_embed": (ctypes.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_u32, c_i32, c_vp, c_i32, c_vp, c_u64, c_vp,
                                           P(c_vp)]),
+    "raftgp_build_embed_loopback": (ctypes.c_int, [c_vp, c_i32, c_i64, c_i64, c_vp, c_vp, c_u32, c_i32, c_vp, c_i32, c_vp,
+                                                   c_u64, c_vp]),
+    "raftgp_nccl_unique_id": (ctypes.c_int, [c_vp]),
+    "raftgp_ctx_create_dist": (ctypes.c_int, [ctypes.c_int, c_vp, ctypes.c_int, ctypes.c_int, c_vp, P(c_vp)]),
+    "raftgp_ctx_rank": (ctypes.c_int, [c_vp, P(ctypes.c_int), P(ctypes.c_int)]),
+    "raftgp_barrier": (ctypes.c_int, [c_vp]),
+    "raftgp_allgather": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_size_t]),
 }
 
 
@@ -144,6 +153,20 @@ def _ptr(t: Optional[torch.Tensor]):
     return ctypes.c_void_p(t.data_ptr())
 
 
+def _own(t: torch.Tensor, stream) -> torch.Tensor:
+    """t as a contiguous tensor for a library call that reads it on `stream` (the context's stream). The caller keeps
+    the returned tensor alive for the whole call. A copy made here runs on torch's current stream: when that is not
+    the context's stream, the context's stream waits for it, and record_stream keeps the caching allocator from
+    handing the copy's memory out again before the library's kernels have read it."""
+    c = t.contiguous()
+    if c is not t and c.is_cuda and stream is not None:
+        cur = torch.cuda.current_stream(c.device)
+        if stream.cuda_stream != cur.cuda_stream:
+            stream.wait_stream(cur)
+            c.record_stream(stream)
+    return c
+
+
 def _dev(t: torch.Tensor, what: str):
     if not t.is_cuda:
         raise ValueError(f"{what} must be a CUDA tensor")
@@ -152,15 +175,38 @@ def _dev(t: torch.Tensor, what: str):
 
 # ------------------------------------------------------------------ context
 class Context:
-    """raftgp_ctx on one device, enqueuing on a torch CUDA stream (the current one by default)."""
+    """raftgp_ctx on one device, enqueuing on a torch CUDA stream (the current one by default). With `dist=(rank,
+    world, uid)` the context joins a world-rank NCCL communicator (raftgp_ctx_create_dist; uid from
+    raftgp_nccl_unique_id() on rank 0, passed to the others out of band)."""
 
-    def __init__(self, device: int = 0, stream: Optional[torch.cuda.Stream] = None):
+    def __init__(self, device: int = 0, stream: Optional[torch.cuda.Stream] = None, dist=None):
         lib = load_library()
         self.device = torch.device("cuda", device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         h = c_vp()
-        _ck(lib.raftgp_ctx_create(device, c_vp(self.stream.cuda_stream), ctypes.byref(h)))
+        if dist is None:
+            _ck(lib.raftgp_ctx_create(device, c_vp(self.stream.cuda_stream), ctypes.byref(h)))
+        else:
+            rank, world, uid = dist
+            if len(uid) != 128:
+                raise ValueError("the NCCL unique id has 128 bytes")
+            ub = (ctypes.c_char * 128).from_buffer_copy(uid)
+            _ck(lib.raftgp_ctx_create_dist(device, c_vp(self.stream.cuda_stream), int(rank), int(world), ub,
+                                           ctypes.byref(h)))
         self.h = h
+
+    def rank_world(self):
+        r, w = ctypes.c_int(0), ctypes.c_int(1)
+        _ck(load_library().raftgp_ctx_rank(self.h, ctypes.byref(r), ctypes.byref(w)))
+        return r.value, w.value
+
+    def barrier(self):
+        """Stream-ordered barrier over the context's communicator (no-op on a one-rank context)."""
+        _ck(load_library().raftgp_barrier(self.h))
+
+    def allgather(self, send: torch.Tensor, recv: torch.Tensor):
+        """ncclAllGather on the context stream: recv (world x send bytes) receives every rank's send block."""
+        _ck(load_library().raftgp_allgather(self.h, _ptr(send), _ptr(recv), send.numel() * send.element_size()))
 
     def sync(self):
         _ck(load_library().raftgp_ctx_sync(self.h))
@@ -245,11 +291,13 @@ class Graph:
         return out[: self.rows]
 
     def set_degrees(self, deg_all: torch.Tensor):
-        _ck(load_library().raftgp_graph_set_degrees(self.h, _ptr(_dev(deg_all.contiguous(), "deg_all"))))
+        d = _own(_dev(deg_all, "deg_all"), self.ctx.stream)
+        _ck(load_library().raftgp_graph_set_degrees(self.h, _ptr(d)))
 
     def set_order(self, order: Optional[torch.Tensor]):
         """Row visiting order (int32 permutation of the local rows) or None for the natural order."""
-        _ck(load_library().raftgp_graph_set_order(self.h, None if order is None else _ptr(order.contiguous())))
+        o = None if order is None else _own(_dev(order, "order"), self.ctx.stream)
+        _ck(load_library().raftgp_graph_set_order(self.h, _ptr(o)))
 
     def close(self):
         if getattr(self, "h", None) is not None and _lib is not None and not _exiting:
@@ -271,7 +319,7 @@ def raftgp_build_csr(ctx: Context, n: int, src: torch.Tensor, dst: torch.Tensor,
     if src.is_cuda != dst.is_cuda:
         raise ValueError("src and dst must live on the same side")
     flags = RAFTGP_DEVICE_PTRS if src.is_cuda else RAFTGP_HOST_PTRS
-    src, dst = src.contiguous(), dst.contiguous()
+    src, dst = _own(src, ctx.stream), _own(dst, ctx.stream)
     h = c_vp()
     re = n if row_end is None else row_end
     _ck(load_library().raftgp_build_csr(ctx.h, n, src.numel(), _ptr(src), _ptr(dst), row_begin, re, flags,
@@ -300,7 +348,8 @@ def raftgp_sketch_transform(ctx: Context, seed: int, rows: int, W: torch.Tensor)
     """Theta' = Theta W (Theta generated on chip, tcgen05 3xTF32 GEMM)."""
     r, l1 = W.shape
     out = torch.empty((rows, l1), dtype=torch.float32, device=ctx.device)
-    _ck(load_library().raftgp_sketch_transform(ctx.h, seed, rows, r, _ptr(W.contiguous()), l1, _ptr(out)))
+    Wc = _own(W, ctx.stream)
+    _ck(load_library().raftgp_sketch_transform(ctx.h, seed, rows, r, _ptr(Wc), l1, _ptr(out)))
     return out
 
 
@@ -393,18 +442,35 @@ def raftgp_embed_multi(g: Graph, variants: Sequence, dims: Sequence[int], seed: 
     return Y, Z
 
 
+def raftgp_nccl_unique_id() -> bytes:
+    """A new NCCL unique id (128 bytes) for raftgp_ctx_create_dist (created on rank 0, sent to the others)."""
+    b = (ctypes.c_char * 128)()
+    _ck(load_library().raftgp_nccl_unique_id(b))
+    return bytes(b)
+
+
+def local_rows(n: int, rank: int, world: int):
+    """Rank `rank`'s rows [p R, min((p+1) R, n)), R = ceil(n / world) (the library's row partition)."""
+    R = max(1, -(-n // world))
+    return min(n, rank * R), min(n, (rank + 1) * R)
+
+
 def raftgp_build_embed(ctx: Context, n: int, src: torch.Tensor, dst: torch.Tensor, variants: Sequence,
                        dims: Sequence[int], seed: int, Z=None, keep_graph: bool = False):
     """raftgp_build_csr + raftgp_embed_multi in one call (Theta' overlapped with the CSR build on a side stream).
-    Returns ({variant: Z}, Graph or None)."""
+    On a distributed context: the row-partitioned step; Z holds this rank's rows. Returns ({variant: Z}, Graph or
+    None)."""
     if src.dtype != torch.int32 or dst.dtype != torch.int32 or src.numel() != dst.numel():
         raise ValueError("src/dst must be int32 tensors of equal length")
     dims = [int(d) for d in dims]
     vs = [_variant(v) for v in variants]
     names = [v if isinstance(v, str) else {0: "ncut", 1: "mod", 2: "mod_reduced"}[int(v)] for v in variants]
-    Z = Z or {nm: torch.empty((n, dims[-1]), dtype=torch.float32, device=ctx.device) for nm in names}
+    rank, world = ctx.rank_world()
+    rb, re = local_rows(n, rank, world)
+    Z = Z or {nm: torch.empty((max(1, re - rb), dims[-1]), dtype=torch.float32, device=ctx.device)[: re - rb]
+              for nm in names}
     flags = RAFTGP_DEVICE_PTRS if src.is_cuda else RAFTGP_HOST_PTRS
-    s, d = src.contiguous(), dst.contiguous()
+    s, d = _own(src, ctx.stream), _own(dst, ctx.stream)
     va = (c_i32 * len(vs))(*vs)
     dd = (c_i32 * len(dims))(*dims)
     h = c_vp()
@@ -412,6 +478,24 @@ def raftgp_build_embed(ctx: Context, n: int, src: torch.Tensor, dst: torch.Tenso
                                           seed, _zk_array([Z[nm] for nm in names]),
                                           ctypes.byref(h) if keep_graph else None))
     return Z, (Graph(ctx, h) if keep_graph else None)
+
+
+def raftgp_build_embed_loopback(ctx: Context, P: int, n: int, src: torch.Tensor, dst: torch.Tensor, variants: Sequence,
+                                dims: Sequence[int], seed: int, Z=None) -> dict:
+    """The row-partitioned step with P logical ranks on this context's GPU (all n rows of Z)."""
+    if src.dtype != torch.int32 or dst.dtype != torch.int32 or src.numel() != dst.numel():
+        raise ValueError("src/dst must be int32 tensors of equal length")
+    dims = [int(d) for d in dims]
+    vs = [_variant(v) for v in variants]
+    names = [v if isinstance(v, str) else {0: "ncut", 1: "mod", 2: "mod_reduced"}[int(v)] for v in variants]
+    Z = Z or {nm: torch.empty((max(1, n), dims[-1]), dtype=torch.float32, device=ctx.device)[:n] for nm in names}
+    flags = RAFTGP_DEVICE_PTRS if src.is_cuda else RAFTGP_HOST_PTRS
+    s, d = _own(src, ctx.stream), _own(dst, ctx.stream)
+    va = (c_i32 * len(vs))(*vs)
+    dd = (c_i32 * len(dims))(*dims)
+    _ck(load_library().raftgp_build_embed_loopback(ctx.h, P, n, s.numel(), _ptr(s), _ptr(d), flags, len(vs), va,
+                                                   len(dims) - 1, dd, seed, _zk_array([Z[nm] for nm in names])))
+    return Z
 
 
 def _dptr(x) -> int:
@@ -439,8 +523,9 @@ def raftgp_gcn_hop_push(g: Graph, T_full, w: int, W_next: torch.Tensor, reps: Se
     Z = torch.empty((max(1, g.rows), w), dtype=torch.float32, device=g.ctx.device)[: g.rows] if want_Z else None
     flat = [_dptr(p) for p in reps]
     arr = (c_vp * len(flat))(*flat)
+    Wn = _own(W_next, g.ctx.stream)
     _ck(load_library().raftgp_gcn_hop_push(g.h, _dptr(T_full), w, None if Z is None else _ptr(Z),
-                                           _ptr(W_next.contiguous()), W_next.shape[1], arr, len(flat)))
+                                           _ptr(Wn), W_next.shape[1], arr, len(flat)))
     return Z
 
 
@@ -537,7 +622,8 @@ def raftgp_model_select(g: Graph, Z: torch.Tensor, eps: int = 5, max_iter: int =
         labels = torch.empty(max(1, g.rows), dtype=torch.int32, device=g.ctx.device)[: g.rows]
     k = c_i32(0)
     st = np.zeros(7, np.int64)
-    _ck(load_library().raftgp_model_select(g.h, _ptr(Z.contiguous()), Z.shape[1], eps, max_iter, r, _ptr(labels),
+    Zc = _own(Z, g.ctx.stream)
+    _ck(load_library().raftgp_model_select(g.h, _ptr(Zc), Z.shape[1], eps, max_iter, r, _ptr(labels),
                                            ctypes.byref(k), c_vp(st.ctypes.data)))
     return labels, int(k.value), dict(zip(("blocks", "splits", "lloyd_iters", "levels", "lloyd_rows", "seed_rows", "rows_read"),
                                  (int(x) for x in st)))
@@ -553,7 +639,8 @@ def raftgp_gemm_tf32x3(ctx: Context, A: torch.Tensor, B: torch.Tensor, row_scale
         raise ValueError("inner dimensions differ")
     if C is None:
         C = torch.empty((M, N), dtype=torch.float32, device=ctx.device)
-    _ck(load_library().raftgp_gemm_tf32x3(ctx.h, M, K, N, _ptr(A.contiguous()), _ptr(B.contiguous()),
+    Ac, Bc = _own(A, ctx.stream), _own(B, ctx.stream)
+    _ck(load_library().raftgp_gemm_tf32x3(ctx.h, M, K, N, _ptr(Ac), _ptr(Bc),
                                           _ptr(row_scale), _ptr(C)))
     return C
 
@@ -562,9 +649,9 @@ def raftgp_gemm_tf32x3(ctx: Context, A: torch.Tensor, B: torch.Tensor, row_scale
 def raftgp_sbm_sample(ctx: Context, c: torch.Tensor, theta: torch.Tensor, omega: torch.Tensor, seed: int,
                       q: int = 20, cap: Optional[int] = None):
     """Alg. 2 (docs/SBM_SPEC.md) on the device: returns (src, dst) int32 CUDA tensors."""
-    c = _dev(c.to(torch.int32).contiguous(), "c")
-    theta = _dev(theta.to(torch.float64).contiguous(), "theta")
-    omega = _dev(omega.to(torch.float64).contiguous(), "omega")
+    c = _own(_dev(c.to(torch.int32), "c"), ctx.stream)
+    theta = _own(_dev(theta.to(torch.float64), "theta"), ctx.stream)
+    omega = _own(_dev(omega.to(torch.float64), "omega"), ctx.stream)
     K = omega.shape[0]
     n = c.numel()
     if cap is None:   # expected edges + slack (a second call fixes an underestimate)
@@ -609,7 +696,7 @@ class Stream:
         L = len(self.dims) - 1
         st = np.zeros(L + 3, np.int64)
         flags = RAFTGP_DEVICE_PTRS if src.is_cuda else RAFTGP_HOST_PTRS
-        s, d = src.contiguous(), dst.contiguous()
+        s, d = _own(src, self.ctx.stream), _own(dst, self.ctx.stream)
         _ck(load_library().raftgp_stream_add_edges(self.h, s.numel(), _ptr(s), _ptr(d), flags, c_vp(st.ctypes.data)))
         return {"changed": int(st[0]), "affected": [int(x) for x in st[1:L + 2]], "nnz": int(st[L + 2])}
 

@@ -150,3 +150,42 @@ def test_bucket_windows(rg, cap):
     r = subprocess.run([sys.executable, "-c", _WINDOW_SCRIPT], cwd=root, env=dict(os.environ, RAFTGP_BUCKET_CAP=cap),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_set_order_rejects_non_permutations(rg, ctx):
+    """raftgp_graph_set_order checks its array on the device: out-of-range or repeated rows are a PARAM error
+    (the hop kernels index with it), a true permutation is accepted and leaves the results unchanged."""
+    import synth
+    gr = synth.generate("C1", 0)
+    g = rg.raftgp_build_csr(ctx, gr.n, torch.from_numpy(gr.src).cuda(), torch.from_numpy(gr.dst).cuda())
+    _, Z0 = rg.raftgp_embed_multi(g, ["ncut"], (64, 64, 32), 0)
+    bad = [np.arange(gr.n, dtype=np.int32) + 1,                                      # out of range
+           np.concatenate([[0], np.arange(gr.n - 1, dtype=np.int32)]).astype(np.int32),   # repeated 0
+           -np.ones(gr.n, np.int32)]
+    for b in bad:
+        with pytest.raises(rg.RaftGPError) as ei:
+            g.set_order(torch.from_numpy(b).cuda())
+        assert ei.value.code == rg.RAFTGP_ERR_PARAM
+    perm = np.random.default_rng(1).permutation(gr.n).astype(np.int32)
+    g.set_order(torch.from_numpy(perm).cuda())
+    _, Z1 = rg.raftgp_embed_multi(g, ["ncut"], (64, 64, 32), 0)
+    assert torch.equal(Z0["ncut"], Z1["ncut"])
+
+
+def test_trim_returns_memory_to_the_device(rg):
+    """the context's workspace lives in its own pool; raftgp_ctx_trim hands it back to the device, so
+    the free memory other allocators see recovers (the device's default pool is not modified)."""
+    import synth
+    c = rg.Context(0)
+    gr = synth.generate("C3", 0)
+    src, dst = torch.from_numpy(gr.src).cuda(), torch.from_numpy(gr.dst).cuda()
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    Z, _ = rg.raftgp_build_embed(c, gr.n, src, dst, ["ncut", "mod"], (128, 128, 64), 0)
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    released = c.trim()
+    free2, _ = torch.cuda.mem_get_info()
+    assert released > 0 and free1 < free0
+    assert free2 >= free1 + 0.9 * released
+    c.close()
