@@ -47,9 +47,14 @@ def parse():
     ap.add_argument("--table1-steps", type=int, default=3)
     ap.add_argument("--no-sbm", action="store_true", help="skip the NEXT-3 SBM sampler measurement")
     ap.add_argument("--e2e-lanes", type=int, default=3, help="contexts/streams the e2e steps rotate over (N = 1)")
-    ap.add_argument("--exchange", default="push", choices=["push", "allgather"],
-                    help="N > 1: per-hop exchange fused into the producing kernels (peer stores through CUDA IPC) "
+    ap.add_argument("--exchange", default="lib", choices=["lib", "push", "allgather"],
+                    help="N > 1: lib = the row-partitioned step inside the library (raftgp_build_embed on a context "
+                         "created with raftgp_ctx_create_dist; exchanges fused into the producing kernels, NCCL "
+                         "barriers); push / allgather = the same step driven from Python (dist.py) with peer stores "
                          "or NCCL all-gathers pipelined across variants")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch check only (no GPU work): spawn/join the ranks, rendezvous, max-over-ranks, one JSON "
+                         "line with dry_run = true. Not a measurement.")
     ap.add_argument("--e2e-api", default="build_embed", choices=["separate", "build_embed"],
                     help="e2e step: raftgp_build_csr + raftgp_embed_multi, or raftgp_build_embed")
     ap.add_argument("--no-stream", action="store_true", help="skip the NEXT-4 streaming-update measurement")
@@ -155,6 +160,22 @@ def algorithmic_bytes(nnz, n, r, dims, nvar, kernel, fused_pair=False):
             return nvar * b - shared, nvar * L - 1
         return nvar * b, nvar * L
     return None, None
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def self_spawn(args) -> int:
+    """`python bench.py --gpus N` outside torchrun: start N ranks with torch.distributed.run on this node (one per
+    GPU, rendezvous on 127.0.0.1) running this same command line; rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ, RAFTGP_BENCH_SPAWNED="1")
+    return subprocess.call(cmd, env=env)
 
 
 def dist_env():
@@ -468,8 +489,31 @@ def measure_table1(args, rg, dev, barrier, peak, peak_src):
     }
 
 
+def dry_run(args):
+    """Launch check: every rank joins the process group (gloo), the ranks agree on a value by max-over-ranks, rank 0
+    prints one line. No kernels run, nothing is measured."""
+    import torch
+    import torch.distributed as tdist
+    world, rank, _ = dist_env()
+    if world > 1:
+        tdist.init_process_group("gloo")
+    t = torch.tensor([float(rank)])
+    if world > 1:
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "metric": METRIC, "n_gpus": world, "max_rank": int(t.item()),
+                          "steps": args.steps, "warmup": args.warmup, "gpus_flag": args.gpus}), flush=True)
+    if world > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_spawn(args))
+    if args.dry_run:
+        return dry_run(args)
     if args.impl == "reference":
         return run_reference(args)
     import torch
@@ -486,6 +530,8 @@ def main():
         backend = os.environ.get("RAFTGP_BENCH_BACKEND", "nccl")
         if os.environ.get("RAFTGP_BENCH_ONE_GPU") == "1":
             local = 0
+            if args.exchange == "lib":   # one NCCL communicator cannot hold two ranks of one GPU
+                args.exchange = "push"
         torch.cuda.set_device(local)
         if backend == "nccl":
             tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -510,11 +556,20 @@ def main():
     dst_h = torch.from_numpy(gr.dst).pin_memory()
     src_d, dst_d = src_h.to(dev), dst_h.to(dev)
     ctx = rg.Context(dev.index)
-    stream = ctx.stream
+    lib_dist = world > 1 and args.exchange == "lib"
+    dctx = None
+    if lib_dist:
+        # the library's own NCCL communicator (raftgp_ctx_create_dist); torch.distributed only carries the id
+        uid = [rg.raftgp_nccl_unique_id() if rank == 0 else None]
+        tdist.broadcast_object_list(uid, src=0)
+        dctx = rg.Context(dev.index, dist=(rank, world, uid[0]))
+    run_ctx = dctx if lib_dist else ctx       # the context whose stream / profile / launch count the step uses
+    stream = run_ctx.stream
     ranges, _ = rdist.row_partition(gr.n, world)
     rb, re = ranges[rank]
     rows = re - rb
-    Zbuf = {v: torch.empty((rows, dims[-1]), dtype=torch.float32, device=dev) for v in variants}
+    assert (rb, re) == rg.local_rows(gr.n, rank, world)
+    Zbuf = {v: torch.empty((max(1, rows), dims[-1]), dtype=torch.float32, device=dev)[:rows] for v in variants}
 
     fused_pair = (not args.no_fuse_variants) and "ncut" in variants and "mod" in variants
 
@@ -547,7 +602,15 @@ def main():
         keep["graph"].close()
         return nnz
 
-    step = step_single if world == 1 else step_multi
+    def step_lib(src, dst, out_host=None):
+        # the row-partitioned step inside the library: one C-ABI call per rank (exchanges fused, NCCL barriers)
+        rg.raftgp_build_embed(dctx, gr.n, src, dst, variants, dims, args.seed, Z=Zbuf)
+        if out_host is not None:
+            for v in variants:
+                out_host[v].copy_(Zbuf[v], non_blocking=True)
+        return None
+
+    step = step_single if world == 1 else (step_lib if lib_dist else step_multi)
 
     def barrier():
         torch.cuda.synchronize()
@@ -573,11 +636,16 @@ def main():
     nnz_local = 0
     for _ in range(max(3, args.warmup)):
         nnz_local = step(src_d, dst_d)
+    if lib_dist:   # this rank's entries (the library call returns no graph): one local CSR build, untimed
+        gl = rg.raftgp_build_csr(ctx, gr.n, src_d, dst_d, rb, re)
+        nnz_local = gl.info()["nnz_local"]
+        gl.close()
+        ctx.trim()
     nnz = int(sum_over_ranks(nnz_local))
     # ---------------- timed region (device-resident inputs)
-    ctx.prof_reset()
-    ctx.set_profiling(True)
-    ctx.launch_count(reset=True)
+    run_ctx.prof_reset()
+    run_ctx.set_profiling(True)
+    run_ctx.launch_count(reset=True)
     barrier()
     with ClockSampler(dev.index, args.clock_period_ms, not args.no_clocks, args.clock_query) as clocks:
         t0 = torch.cuda.Event(enable_timing=True)
@@ -588,9 +656,9 @@ def main():
         t1.record(stream)
         barrier()
     ms = t0.elapsed_time(t1) / args.steps
-    launches = ctx.launch_count()
-    prof = ctx.prof_read()
-    ctx.set_profiling(False)
+    launches = run_ctx.launch_count()
+    prof = run_ctx.prof_read()
+    run_ctx.set_profiling(False)
     ms_max = max_over_ranks(ms)
     units = work_units(nnz, gr.n, cfg.r, dims, len(variants))
     value = units / (ms_max * 1e-3)
@@ -605,7 +673,7 @@ def main():
         if k not in prof:
             continue
         b_step, l_step = algorithmic_bytes(nnz if world == 1 else nnz_local, rows if world > 1 else gr.n, cfg.r, dims,
-                                           len(variants), k, fused_pair and world == 1)
+                                           len(variants), k, fused_pair and (world == 1 or lib_dist))
         t_step = prof[k][0] / args.steps * 1e-3
         ach = b_step / t_step / 1e9
         hop_stats[k] = {"gb_s": ach, "ms_per_step": t_step * 1e3, "launches_per_step": prof[k][1] / args.steps,
@@ -632,6 +700,39 @@ def main():
             t_launch = hop_stats[dom]["ms_per_step"] * 1e-3 / hop_stats[dom]["launches_per_step"]
             roof["dram_gb_s"] = traffic / t_launch / 1e9
             roof["dram_frac"] = roof["dram_gb_s"] / peak
+
+    # ---------------- N > 1: the exchange and the partition
+    dist_info = None
+    if world > 1:
+        per_rank = [None] * world
+        tdist.all_gather_object(per_rank, {"nnz_local": int(nnz_local), "rows": rows,
+                                           "kernel_ms": {k: v for k, v in kernel_times.items()}})
+        nl = [x["nnz_local"] for x in per_rank]
+        kmax = {}
+        for x in per_rank:
+            for k, v in x["kernel_ms"].items():
+                kmax[k] = max(kmax.get(k, 0.0), v)
+        V = len(variants)
+        # every operand row is stored into the P - 1 peers' copies by the kernel that produces it: Theta' (l1 wide,
+        # lib path), T_1 .. T_L of every variant (dims[1..L] wide)
+        per_row = (dims[1] if lib_dist else 0) + V * sum(dims[1:])
+        egress = (world - 1) * rows * 4 * per_row
+        producing = sum(kmax.get(k, 0.0) for k in ("sketch", "feature_hop", "gcn_hop", "push_copy"))
+        dist_info = {
+            "communicator": (f"library NCCL communicator of {world} ranks (raftgp_ctx_create_dist)" if lib_dist
+                             else f"torch.distributed ({tdist.get_backend()}) of {world} ranks"),
+            "exchange": ("fused into the producing kernels (peer stores over NVLink, CUDA IPC mappings) + stream-"
+                         "ordered NCCL barriers" if args.exchange in ("lib", "push") else "NCCL all-gathers"),
+            "partition": "1-D rows [p R, (p+1) R), R = ceil(n / P)",
+            "nnz_local": nl, "nnz_imbalance_max_over_mean": max(nl) / (sum(nl) / len(nl)),
+            "kernel_ms_per_step_max_over_ranks": {k: round(v, 4) for k, v in sorted(kmax.items(), key=lambda x: -x[1])},
+            "exchange_wait_ms_per_step": kmax.get("exchange", 0.0),
+            "egress_bytes_per_rank_per_step": egress,
+            "egress_gb_s_during_producing_kernels": (egress / (producing * 1e-3) / 1e9) if producing else None,
+            "note": ("the exchange is overlapped by construction: its stores run inside the producing kernels, so their "
+                     "time is part of sketch / feature_hop / gcn_hop; exchange_wait is the time spent in NCCL barriers "
+                     "and all-gathers, including waiting for the slowest rank"),
+        }
 
     # ---------------- NEXT-1: Alg. 1 model selection on this step's embeddings (whole graph, N = 1)
     select = None
@@ -823,12 +924,15 @@ def main():
                        "rule": args.rule, "fused_variant_pair": fused_pair and world == 1,
                        "parallelism": f"rowpart{world}" if world > 1 else "single",
                        "exchange": (args.exchange if world > 1 else None),
+                       "launch": ("torch.distributed.run, one rank per GPU (bench.py self-spawns it for --gpus N > 1)"
+                                  if world > 1 else "single process"),
                        "l2": "inputs larger than L2 (gathered operands >= 1.28 GB vs 126 MB L2); no flush"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e if e2e_skip is None else {"skipped": e2e_skip},
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "kernels_ms_per_step": {k: round(v, 4) for k, v in sorted(kernel_times.items(), key=lambda x: -x[1])},
             "hops": hop_stats,
+            "dist": dist_info,
             "model_selection": select,
             "table1_widths": table1,
             "sbm_sampler": sbm,
@@ -837,6 +941,9 @@ def main():
         print(json.dumps(line), flush=True)
     if push_bufs is not None:
         push_bufs.close()
+    if dctx is not None:
+        torch.cuda.synchronize()
+        dctx.close()   # collective (the cached operand copies are unmapped behind a barrier)
     if world > 1:
         tdist.barrier()
         tdist.destroy_process_group()
