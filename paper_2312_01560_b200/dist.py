@@ -170,6 +170,9 @@ class _Done:
     def __init__(self, value):
         self.value = value
 
+    def result(self):
+        return self.value
+
 
 def run_loopback(gens: List[Generator], device=None, dtype=torch.float32):
     """Advance P rank pipelines in lockstep; a gather concatenates the P blocks in rank order; push-mode
@@ -286,15 +289,22 @@ class PushBuffers:
         self.key, self.own, self.maps, self.tensors, self.mapped = None, {}, {}, {}, True
 
 
-def run_distributed(gen: Generator, group=None, push: Optional[PushBuffers] = None):
+def run_distributed(gen: Generator, group=None, push: Optional[PushBuffers] = None, lib_ctx: Optional[rg.Context] = None):
     """Drive one rank's pipeline over torch.distributed (NCCL on GPUs, gloo on CPU). Push-mode buffers come
     from `push` (GPU: IPC-mapped copies) or, without it, are this rank's own CPU copy only, completed at each
-    barrier by an all-gather of the row blocks (the CPU stand-in for the peer stores)."""
+    barrier by an all-gather of the row blocks (the CPU stand-in for the peer stores).
+    lib_ctx: a context made by raftgp_ctx_create_dist -- the device all-gathers and the push barriers then run on the
+    LIBRARY's NCCL communicator, stream-ordered on lib_ctx's stream (raftgp_allgather / raftgp_barrier); torch's
+    process group only carries the host-side handle exchange of the push buffers."""
     import torch.distributed as dist
 
     def _start(t: torch.Tensor) -> _Pending:
         world = dist.get_world_size(group)
         t = t.contiguous()
+        if t.is_cuda and lib_ctx is not None:   # stream-ordered on the library's stream: usable at once
+            out = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+            lib_ctx.allgather(t, out)
+            return _Done(out)
         if t.is_cuda:
             out = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
             return _Pending(dist.all_gather_into_tensor(out, t, group=group, async_op=True), out)
@@ -329,7 +339,9 @@ def run_distributed(gen: Generator, group=None, push: Optional[PushBuffers] = No
                     blocks = _start(mine if nccl else mine.cpu()).result()   # gloo: host all-gather
                     full.copy_(blocks[: info["n"]])
             elif push is not None:
-                if dist.get_backend(group) == "nccl":
+                if lib_ctx is not None:
+                    lib_ctx.barrier()                    # 1-element ncclAllReduce on the library's communicator
+                elif dist.get_backend(group) == "nccl":
                     flag = torch.zeros(1, dtype=torch.float32, device=push.ctx.device)
                     dist.all_reduce(flag, group=group)   # stream-ordered: every rank's producing kernels are done
                 else:                                    # host barrier (tests: several processes on one GPU)

@@ -59,3 +59,30 @@ def test_rank_pipeline_over_nccl_matches_single_gpu(nccl_group):
         assert torch.equal(Z[v], ref[v]), v
         Zo = oracle.gcn(go, list(dims), 5, oracle.project(go, v, dims[0], 5))[-1]
         assert np.linalg.norm(Z[v].cpu().numpy() - Zo) / np.linalg.norm(Zo) <= 1e-4
+
+
+@pytest.mark.parametrize("push", [False, True])
+def test_rank_pipeline_over_library_comm(nccl_group, push):
+    """The Python-driven pipelines with the exchanges on the LIBRARY's communicator (raftgp_ctx_create_dist:
+    raftgp_allgather for the degree / operand all-gathers, raftgp_barrier for the push barriers)."""
+    from paper_2312_01560_b200 import dist as rdist
+    from paper_2312_01560_b200 import raftgp as rg
+    gr = synth.generate("C2", 3)
+    dims = (64, 64, 32)
+    variants = ["ncut", "mod"]
+    ctx = rg.Context(0)
+    lib = rg.Context(0, dist=(0, 1, rg.raftgp_nccl_unique_id()))
+    src, dst = torch.from_numpy(gr.src).cuda(), torch.from_numpy(gr.dst).cuda()
+    pipe = rdist.rank_pipeline_push if push else rdist.rank_pipeline
+    bufs = rdist.PushBuffers(lib) if push else None
+    gen = pipe(rdist.CudaEngine(lib), gr.n, src, dst, 0, 1, variants, dims, 5)
+    Z = rdist.run_distributed(gen, push=bufs, lib_ctx=lib)
+    torch.cuda.synchronize()
+    if bufs is not None:
+        bufs.close()
+    # reference: the same pipeline driven in loopback on a plain context (one rank)
+    ref = rdist.run_loopback([pipe(rdist.CudaEngine(ctx), gr.n, src, dst, 0, 1, variants, dims, 5)],
+                             device=ctx.device)[0]
+    for v in variants:
+        assert torch.equal(Z[v], ref[v]), v
+    lib.close()
