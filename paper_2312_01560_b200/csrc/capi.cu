@@ -1100,6 +1100,18 @@ static raftgp_status build_embed_partitioned(raftgp_ctx ctx, int32_t P, bool loo
 // raftgp_build_csr + raftgp_embed_multi in one call. Theta' = Theta W^(1) depends only on the seed, so it is
 // generated on a side stream (tensor cores / ALUs) while the CSR build (atomics / HBM) runs on the context
 // stream; the results are those of the two separate calls.
+// CTAs of the Theta' kernel while it overlaps the CSR build (RAFTGP_OVERLAP_CTAS; default measured)
+static int build_overlap_ctas(raftgp_ctx ctx) {
+    static const int env = [] {
+        const char *e = getenv("RAFTGP_OVERLAP_CTAS");
+        return e ? atoi(e) : -1;
+    }();
+    if (env >= 0) return env;
+    // half the SMs: C4 step 72.5 ms vs 73.9 with every SM (the CSR kernels then queue behind the 1-CTA-per-SM
+    // sketch) and 74.2 serial; 112 / 96 / 48 / 32 CTAs: 74.1 / 74.6 / 73.9 / 76.6 ms (profiles/r02/overlap_sweep.txt)
+    return std::max(1, ctx->sm_count / 2);
+}
+
 raftgp_status raftgp_build_embed(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src, const int32_t *dst,
                                  uint32_t flags, int32_t nvariants, const int32_t *variants, int32_t layers,
                                  const int32_t *dims, uint64_t seed, float *const *Z_dev, raftgp_graph *g_out) {
@@ -1130,10 +1142,16 @@ raftgp_status raftgp_build_embed(raftgp_ctx ctx, int64_t n, int64_t m, const int
         if (st == RAFTGP_OK) {
             RG_CUDA(cudaEventRecord(ev_fork, ctx->stream));
             RG_CUDA(cudaStreamWaitEvent(ctx->side, ev_fork, 0));
+            static const bool serial = [] {   // RAFTGP_BUILD_OVERLAP=0: Theta' before the CSR build, same stream
+                const char *e = getenv("RAFTGP_BUILD_OVERLAP");
+                return e && e[0] == '0';
+            }();
             cudaStream_t main = ctx->stream;
-            ctx->stream = ctx->side;   // the sketch kernels enqueue on the side stream
+            if (!serial) ctx->stream = ctx->side;   // the sketch kernels enqueue on the side stream
+            ctx->sketch_ctas = build_overlap_ctas(ctx);   // leave SMs to the CSR build that runs beside it
             st = sketch_fill(ctx, seed, 1u, 0, r, l1, r, W1);
             if (st == RAFTGP_OK) st = sketch_w_any(ctx, seed, n, r, W1, l1, thw);
+            ctx->sketch_ctas = 0;
             ctx->stream = main;
             RG_CUDA(cudaEventRecord(ev_join, ctx->side));
         }

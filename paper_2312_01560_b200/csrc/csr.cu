@@ -2,17 +2,27 @@
 // and the degree / normalisation pass (deg, 2e, s = D^-1/2 for M, s^ = (D+I)^-1/2 for
 // Eq. 6's propagation matrix).
 //
-// Build pipeline (all on the ctx stream, one host sync at the end):
-//   count     : one pass over the raw pairs; int atomics count both orientations of every u != v pair
-//               whose row falls in [rb, re); ids outside [0, n) raise a device data-error flag.
-//   scan      : exclusive int64 scan of the raw counts -> raw_ptr.
-//   scatter   : second pass; atomic slot claim per row, writes the neighbour into col_raw.
-//   sort+dedup: per-row ascending sort and duplicate removal, in place inside the raw segment.
-//               Rows <= 32 entries: one warp, register bitonic network; rows <= 512: one warp, bitonic
-//               in shared memory; longer rows are deferred to a block-per-row kernel (shared memory up to
-//               24K entries, global memory beyond). The unique count is the degree.
-//   scan      : exclusive int64 scan of the degrees -> row_ptr.
-//   compact   : copies each row's unique prefix into the final col array.
+// Build pipeline (all on the ctx stream; csr_build, the default path for every graph whose buckets fit):
+//   bucket count : one CTA per SM histograms its contiguous range of raw pairs into shared memory by BUCKET of
+//                  2^shift consecutive local rows (both orientations of every u != v pair whose row is local) and
+//                  writes per-(bucket, CTA) counts; ids outside [0, n) raise a device data-error flag.
+//   scan         : exclusive scan of the counts -> bucket starts.
+//   partition    : tiles of 16K pairs claimed round robin: shared-memory tile histogram, one global atomic per
+//                  (tile, bucket) on the bucket cursor, then the entries (row-in-bucket, neighbour) are written
+//                  into their bucket's slots (32-bit packed when log2(B) + id bits <= 32).
+//   bucket sort  : one CTA per bucket (persistent): counts its own rows, writes the raw row pointers, places the
+//                  entries into rows in shared memory, sorts each row (one warp in registers up to 128 entries,
+//                  groups of 4 warps by value sub-ranges beyond) and removes duplicates; the unique count is the
+//                  degree. Buckets larger than shared memory are processed window by window; single rows longer
+//                  than a window fall back to global placement + csr_sort_warp / csr_sort_block.
+//   scan         : exclusive int64 scan of the degrees -> row_ptr; one host read-back (nnz, raw entry count,
+//                  data-error flag).
+//   compact      : copies each row's unique prefix into the final col array (skipped when no duplicate was
+//                  dropped: the raw layout is then the CSR).
+//   order        : degree-aware visiting order of the rows for the hop kernels (order.cu; one read-back).
+//   degrees      : deg -> 2e, s, s^ and a degree histogram (whole-graph builds; one read-back).
+// Graphs whose rows cannot be bucketed (a bucket larger than kMaxBucketRows rows) take the older per-row path:
+// count (global atomics) -> scan -> scatter -> per-row warp / block sorts.
 // The result is canonical (sorted, unique), hence independent of atomic ordering: bit-exact.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -872,6 +882,16 @@ __global__ void csr_compact(int64_t nl, const int64_t *__restrict__ raw_ptr, con
 }
 
 // deg_all -> s, s^ ; two_e = sum deg (int64) via one atomic per block; degree histogram (capped bins)
+// out[0] = nnz (row_ptr[nl]), out[1] = raw entries (raw_ptr[nl], 0 without rows), out[2] = data-error flag
+__global__ void gather_scalars(const int64_t *nnz, const int64_t *raw_total, const int *err, bool has_rows,
+                               int64_t *out) {
+    if (threadIdx.x == 0) {
+        out[0] = *nnz;
+        out[1] = has_rows ? *raw_total : 0;
+        out[2] = *err;
+    }
+}
+
 __global__ void degree_scalars(const int32_t *__restrict__ deg, int64_t n, float *__restrict__ s,
                                float *__restrict__ sh, unsigned long long *__restrict__ two_e,
                                unsigned long long *__restrict__ hist) {
@@ -957,7 +977,7 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
     int32_t *cnt = nullptr, *col_raw = nullptr, *big_count = nullptr, *err = nullptr;
     int64_t *raw_ptr = nullptr, *big_rows = nullptr;
     RG_TRY(dalloc_t(ctx, &cnt, nl));
-    RG_TRY(dalloc_t(ctx, &raw_ptr, nl + 1));
+    RG_TRY(dalloc_t(ctx, &raw_ptr, nl + 4));
     RG_TRY(dalloc_t(ctx, &col_raw, cap));
     RG_TRY(dalloc_t(ctx, &big_rows, nl));
     RG_TRY(dalloc_t(ctx, &big_count, 2));
@@ -1106,18 +1126,24 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
     dfree(ctx, fb_rows);
     dfree(ctx, fb_count);
     RG_TRY(scan_i32_to_i64(ctx, g->deg_local, g->row_ptr, nl));
-    int64_t nnz = 0;
-    int herr = 0;
-    RG_TRY(dread(ctx, &nnz, g->row_ptr + nl, sizeof(int64_t), st));
-    RG_TRY(dread(ctx, &herr, err, sizeof(int), st));
+    // one host read-back for the three scalars (nnz, raw entry count, data-error flag): gather them into
+    // raw_ptr's spare slots [nl + 1 .. nl + 3] (allocated nl + 4 long) with one tiny kernel, then read them together
+    int64_t hv[3] = {0, 0, 0};
+    {
+        LaunchScope L(ctx, K_MISC);
+        gather_scalars<<<1, 32, 0, st>>>(g->row_ptr + nl, raw_ptr + nl, err, nl > 0, raw_ptr + nl + 1);
+    }
+    RG_CHECK_LAUNCH(ctx);
+    RG_TRY(dread(ctx, hv, raw_ptr + nl + 1, sizeof(hv), st));
+    const int64_t nnz = hv[0];
+    const int herr = (int)hv[2];
     if (herr) {
         dfree(ctx, cnt); dfree(ctx, raw_ptr); dfree(ctx, col_raw); dfree(ctx, big_rows); dfree(ctx, big_count);
         return fail(RAFTGP_ERR_DATA, "build_csr: node id outside [0, n)");
     }
     g->nnz_local = nnz;
     // without duplicate pairs every row kept all its raw entries: the raw layout IS the CSR (no compaction)
-    int64_t raw_total = 0;
-    if (nl > 0) RG_TRY(dread(ctx, &raw_total, raw_ptr + nl, sizeof(int64_t), st));
+    const int64_t raw_total = hv[1];
     const bool no_dups = raw_total == nnz;
     if (no_dups) {
         g->col = col_raw;

@@ -82,6 +82,7 @@ struct raftgp_ctx_s {
     cudaMemPool_t pool = nullptr;  // this context's own stream-ordered pool (release threshold: keep everything)
     bool own_stream = false;
     int sm_count = 148;
+    int sketch_ctas = 0;           // CTAs of the tcgen05 Theta' kernel (0 = every SM); set while it shares the GPU
     int64_t launches = 0;
     bool prof = false;
     std::vector<raftgp::ProfRec> recs;

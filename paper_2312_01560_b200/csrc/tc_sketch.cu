@@ -19,6 +19,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "gauss.cuh"
 #include "internal.cuh"
@@ -193,7 +194,14 @@ raftgp_status launch_tc(raftgp_ctx ctx, uint64_t seed, int64_t row0, int64_t n, 
         RG_CUDA(cudaFuncSetAttribute(sketch_w_tc_kernel<R, L1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         return RAFTGP_OK;
     }));
-    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kTM), ctx->sm_count)));
+    // CTAs (one per SM while resident): ctx->sketch_ctas if set (raftgp_build_embed leaves SMs to the concurrent CSR
+    // build), else every SM; RAFTGP_TC_GRID overrides (A/B runs)
+    static const int env_grid = [] {
+        const char *e = getenv("RAFTGP_TC_GRID");
+        return e ? atoi(e) : 0;
+    }();
+    const int want = env_grid > 0 ? env_grid : (ctx->sketch_ctas > 0 ? ctx->sketch_ctas : ctx->sm_count);
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kTM), want)));
     {
         LaunchScope L(ctx, K_SKETCH);
         sketch_w_tc_kernel<R, L1><<<grid, RG_TC_THREADS, smem, ctx->stream>>>(seed, row0, n, sigma, W1, outs);
