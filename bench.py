@@ -179,6 +179,10 @@ def self_spawn(args) -> int:
     return subprocess.call(cmd, env=env)
 
 
+def sketch_ok(cfg) -> bool:
+    return cfg.r in (32, 64, 128) and cfg.dims[1] in (32, 64, 128)
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -420,6 +424,45 @@ def measure_stream(args, rg, dev, barrier, gr, src_d, dst_d, dims):
 
 
 TABLE1_DIMS = (4096, 2048, 1024, 512, 256)   # PAPER.md:268-273, Table I row 2E5 (and 1E4-1E5)
+
+
+# SASS thread-instructions executed per generated normal by sketch_w_tc_kernel<128, 128> (Philox4x32-10, Box-Muller
+# with the spec's polynomials, hi/lo split, shared-memory stores, MMA issue and drain), from ncu's
+# smsp__inst_executed.sum x 32 / (n r) at C4 (profiles/r02/ncu_sketch_v3.md)
+SKETCH_THREAD_INST_PER_NORMAL = 81.7
+
+
+def measure_sketch(args, rg, ctx, n, r, l1, barrier, sm_mhz):
+    """a3 as an ALU-bound kernel (normals/s and the ALU fraction): Theta' = Theta W^(1) for the
+    bench's n rows on every SM (raftgp_sketch_transform), event-timed alone. peak = the issue-slot roofline: 148 SMs x
+    4 warp-instructions / clock x 32 lanes / (thread-instructions per normal), at the SM clock sampled under load."""
+    import torch
+    W = rg.raftgp_weights(ctx, args.seed, 1, r, l1)
+    out = torch.empty((n, l1), dtype=torch.float32, device=ctx.device)
+    lib = rg.load_library()
+    for _ in range(2):
+        rg._ck(lib.raftgp_sketch_transform(ctx.h, args.seed, n, r, rg._ptr(W), l1, rg._ptr(out)))
+    barrier()
+    reps = 5
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(ctx.stream)
+    for _ in range(reps):
+        rg._ck(lib.raftgp_sketch_transform(ctx.h, args.seed, n, r, rg._ptr(W), l1, rg._ptr(out)))
+    e1.record(ctx.stream)
+    barrier()
+    ms = e0.elapsed_time(e1) / reps
+    normals = n * r
+    ach = normals / (ms * 1e-3)
+    sms = torch.cuda.get_device_properties(ctx.device).multi_processor_count
+    clk = (sm_mhz or 1965.0) * 1e6
+    peak = sms * 4 * 32 * clk / SKETCH_THREAD_INST_PER_NORMAL
+    del out
+    return {"kernel": "sketch_w_tc_kernel (Theta generated on chip, tcgen05 3xTF32 Theta W1)", "ms": ms,
+            "normals": normals, "bound": "alu", "achieved": ach, "unit": "normals/s", "peak": peak, "frac": ach / peak,
+            "peak_rule": (f"{sms} SMs x 4 warp-instructions/clock x 32 lanes x {clk / 1e6:.0f} MHz / "
+                          f"{SKETCH_THREAD_INST_PER_NORMAL} thread-instructions per normal (ncu, this kernel)"),
+            "in_step": "runs on half the SMs on a side stream while the CSR build runs (DESIGN.md §6)"}
 
 
 def measure_table1(args, rg, dev, barrier, peak, peak_src):
@@ -745,6 +788,11 @@ def main():
                      "and all-gathers, including waiting for the slowest rank"),
         }
 
+    # ---------------- a3: the sketch as an ALU-bound kernel (N = 1)
+    sketch_roof = None
+    if world == 1 and sketch_ok(cfg):
+        sketch_roof = measure_sketch(args, rg, ctx, gr.n, cfg.r, dims[1], barrier, clocks.summary().get("sm_mhz"))
+
     # ---------------- NEXT-1: Alg. 1 model selection on this step's embeddings (whole graph, N = 1)
     select = None
     if world == 1 and not args.no_select:
@@ -950,6 +998,7 @@ def main():
             "clocks": clocks.summary(),
             "kernels_ms_per_step": {k: round(v, 4) for k, v in sorted(kernel_times.items(), key=lambda x: -x[1])},
             "hops": hop_stats,
+            "sketch_roofline": sketch_roof,
             "dist": dist_info,
             "model_selection": select,
             "table1_widths": table1,

@@ -7,13 +7,12 @@
 // mantissa bits cleared, lo = x - hi exactly): A B ~ A_hi B_hi + A_hi B_lo + A_lo B_hi, accumulated in fp32
 // in TMEM (error ~2^-20 relative, far inside the 1e-4 parity bar).
 //
-// Per CTA (1024 threads, one per SM): a persistent loop over 128-row tiles. For each tile and each
-// K-quarter of at most 32 columns: all threads generate Theta (one Philox call -> 4 normals -> one 16-byte
-// K-chunk) and store hi/lo in the canonical no-swizzle K-major layout (8-row x 16-byte core matrices) into
-// one of two A buffers; one thread issues tcgen05.mma (M = 128, N = L1, K = 8) x 3 products per K-step into
-// one of two TMEM accumulators and commits to that buffer's mbarrier, so generating quarter g overlaps the
-// MMAs of quarter g - 1. All warps read the previous tile's accumulator back with tcgen05.ld (warp w: lane
-// quarter w % 4, 32-column chunks) and store its rows of Theta' while the next tile's first MMAs run. Every mbarrier wait is bounded (trap on
+// Per CTA (1024 threads, one per SM): a persistent loop over 128-row tiles, each split into K-quarters of at most
+// 32 columns. Every thread generates one Philox quad (4 normals) per quarter and stores its hi / lo tf32 parts in
+// the canonical no-swizzle K-major layout (8-row x 16-byte core matrices) into a ring of NS quarter stages; one
+// thread issues tcgen05.mma (M = 128, N = L1, K = 8) x 3 products per K-step into one of two TMEM accumulators as
+// soon as a stage is complete; four warps drain the previous tile's accumulator with tcgen05.ld and store its rows
+// of Theta'. The warps meet only at the ring's mbarriers (see the kernel). Every mbarrier wait is bounded (trap on
 // timeout) so a descriptor mistake fails loudly instead of hanging the GPU.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -46,21 +45,46 @@ struct SketchOut {
 };
 
 template <int R, int L1>
+struct TcCfg {
+    static constexpr int KQ = R < kKQ ? R : kKQ;                 // K columns per quarter (one A stage)
+    static constexpr int NQK = R / KQ;                            // quarters per tile
+    static constexpr int NCOL = L1 < 32 ? 32 : L1;                // TMEM columns of one accumulator
+    static constexpr uint32_t A_BYTES = kTM * KQ * 4;             // one of hi / lo of one stage
+    static constexpr uint32_t B_BYTES = L1 * R * 4;
+    // A ring depth: as many stages as fit next to W1 (hi + lo), at most 4
+    static constexpr int NS0 = (int)((224u * 1024u - 2u * B_BYTES) / (2u * A_BYTES));
+    static constexpr int NS = NS0 > 4 ? 4 : NS0;
+    static constexpr size_t SMEM = 2 * (size_t)B_BYTES + (size_t)NS * 2 * A_BYTES;
+    static_assert(NS >= 2, "A ring needs two stages");
+};
+
+// Warp roles inside one CTA (RG_TC_THREADS = 1024, 32 warps):
+//   every warp generates: one Philox call -> 4 normals per thread per quarter (128 rows x KQ columns = 1024 quads),
+//     stored as hi / lo K-chunks into the quarter's ring stage, then the warp arrives on full[stage];
+//   warp 0, lane 0 also issues the MMAs of each quarter as soon as full[stage] completes (all 32 warps' stores are
+//     in), and commits them to empty[stage] (the stage may be rewritten) and, after a tile's last quarter, to
+//     accf[acc];
+//   warps 28..31 (lane quarters 0..3 of TMEM) also drain the previous tile's accumulator into Theta' after
+//     generating the first quarter of a tile (wait accf, tcgen05.ld, store, arrive on acce[acc]).
+// No block-wide barrier inside the loop: the warps only meet at the ring's mbarriers, so generation is never held
+// up by the MMA issue or the drain (the round-1 version's per-quarter __syncthreads was its largest stall).
+template <int R, int L1>
 __global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t seed, int64_t row0, int64_t n, float sigma,
                                                              const float *__restrict__ W1, SketchOut outs) {
-    constexpr int KQ = R < kKQ ? R : kKQ;              // K columns per quarter (one A buffer)
-    constexpr int NQK = R / KQ;                         // quarters per tile
-    constexpr int NCOL = L1 < 32 ? 32 : L1;             // TMEM columns of one accumulator (power of two >= 32)
-    constexpr uint32_t A_BYTES = kTM * KQ * 4;
-    constexpr uint32_t B_BYTES = L1 * R * 4;
+    using C = TcCfg<R, L1>;
+    constexpr int KQ = C::KQ, NQK = C::NQK, NCOL = C::NCOL, NS = C::NS;
+    constexpr uint32_t A_BYTES = C::A_BYTES, B_BYTES = C::B_BYTES;
+    constexpr int NW = RG_TC_THREADS / 32;
+    constexpr int EPI0 = NW - 4;                          // first drain warp (its index is 0 mod 4)
+    static_assert(NW % 4 == 0 && kTM * (KQ / 4) == RG_TC_THREADS, "one quad per thread per quarter");
     // instruction descriptor: D f32, A/B tf32, both K-major, N = L1, M = 128
     constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(L1 >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
 
     extern __shared__ __align__(1024) unsigned char tsm[];
     unsigned char *b_hi = tsm;
     unsigned char *b_lo = b_hi + B_BYTES;
-    unsigned char *a_base = b_lo + B_BYTES;             // two A buffers, each hi | lo
-    __shared__ __align__(8) uint64_t mma_bar[2];        // completion of the MMAs reading A buffer 0 / 1
+    unsigned char *a_base = b_lo + B_BYTES;             // NS stages, each hi | lo
+    __shared__ __align__(8) uint64_t full[NS], empty[NS], accf[2], acce[2];
     __shared__ uint32_t tmem_base_sh;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -75,11 +99,17 @@ __global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t 
         *reinterpret_cast<float *>(b_lo + o) = w - hi;
     }
     if (tid == 0) {
-        mbar_init(&mma_bar[0], 1);
-        mbar_init(&mma_bar[1], 1);
+        for (int q = 0; q < NS; ++q) {
+            mbar_init(&full[q], NW);
+            mbar_init(&empty[q], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&accf[a], 1);
+            mbar_init(&acce[a], 4);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 0) {   // two accumulators: tile t accumulates into t & 1 while tile t - 1 is read back
+    if (warp == 0) {   // two accumulators: tile t accumulates into t & 1 while tile t - 1 is drained
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                      ::"r"(smem_u32(&tmem_base_sh)), "r"(2 * NCOL));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -90,18 +120,15 @@ __global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t 
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem_d = tmem_base_sh;
 
-    // Pipeline over quarters g = (local tile) * NQK + q, A buffer g & 1: generating quarter g overlaps the
-    // MMAs of quarter g - 1, and tile t - 1 is read back from TMEM while the MMAs of tile t's first quarter
-    // run. Quarter g's commit is the (g >> 1)-th completion of mma_bar[g & 1] (parity (g >> 1) & 1); every
-    // wait happens before that barrier can complete again, so the parity test is unambiguous.
-    auto wait_quarter = [&](int64_t g) { mbar_wait(&mma_bar[g & 1], (uint32_t)((g >> 1) & 1)); };
-    auto epilogue = [&](int64_t tile_prev, int acc) {
-        // warp w reads TMEM lanes 32 (w % 4) .. + 31 (= tile rows; a warp may only touch the lane quarter of
-        // its index mod 4) and the column chunks c = w / 4, w / 4 + NW / 4, ...
-        constexpr int NW = RG_TC_THREADS / 32;
+    // drain the accumulator of local tile `it` (global tile index `tile`) into Theta' (drain warps only)
+    auto drain = [&](int64_t it, int64_t tile) {
+        const int acc = (int)(it & 1);
+        mbar_wait(&accf[acc], (uint32_t)((it >> 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int lq = warp & 3;
-        const int64_t row = tile_prev * kTM + lq * 32 + lane;
-        for (int c0 = (warp >> 2) * 32; c0 < L1; c0 += (NW / 4) * 32) {
+        const int64_t row = tile * kTM + lq * 32 + lane;
+#pragma unroll 1
+        for (int c0 = 0; c0 < L1; c0 += 32) {
             float v[32];
             tmem_ld32(tmem_d + (static_cast<uint32_t>(lq * 32) << 16) + (uint32_t)(acc * NCOL + c0), v);
             if (row < n) {
@@ -112,22 +139,24 @@ __global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t 
                 }
             }
         }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acce[acc]);
     };
 
     const int64_t ntiles = (n + kTM - 1) / kTM;
-    int64_t it = 0, prev_tile = -1;
+    int64_t it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int64_t r0 = tile * kTM;
         const int acc = (int)(it & 1);
         for (int q = 0; q < NQK; ++q) {
-            const int64_t g = it * NQK + q;
-            unsigned char *a_hi = a_base + (size_t)(g & 1) * 2 * A_BYTES;
+            const int64_t g = it * NQK + q;                    // this CTA's quarter counter
+            const int st = (int)(g % NS);
+            unsigned char *a_hi = a_base + (size_t)st * 2 * A_BYTES;
             unsigned char *a_lo = a_hi + A_BYTES;
-            if (g >= 2) wait_quarter(g - 2);   // the MMAs that read this buffer have retired
-            // generate Theta[r0 .. r0+127][q*KQ .. q*KQ+KQ-1] as hi/lo K-chunks (one Philox call per 4 columns)
-            constexpr int NQ = kTM * (KQ / 4);
-            for (int t = tid; t < NQ; t += RG_TC_THREADS) {
-                const int row = t % kTM, qq = t / kTM;      // consecutive threads: consecutive rows
+            if (g >= NS) mbar_wait(&empty[st], (uint32_t)(((g / NS) - 1) & 1));   // its previous MMAs retired
+            {   // Theta[r0 .. r0+127][q*KQ .. q*KQ+KQ-1]: thread t -> row t % 128, column quad t / 128
+                const int row = tid % kTM, qq = tid / kTM;
                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (r0 + row < n)
                     v = spec_quad(seed, 0u, static_cast<uint64_t>(row0 + r0 + row),
@@ -138,45 +167,38 @@ __global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t 
                 *reinterpret_cast<float4 *>(a_hi + o) = hi;
                 *reinterpret_cast<float4 *>(a_lo + o) = lo;
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncthreads();
-            if (tid == 0) {
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo);
-                const uint32_t bh = smem_u32(b_hi), bl = smem_u32(b_lo);
-                constexpr uint32_t A_LBO = (kTM / 8) * 128, B_LBO = (L1 / 8) * 128, SBO = 128;
-                const uint32_t dacc = tmem_d + (uint32_t)(acc * NCOL);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic stores -> async proxy (MMA)
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[st]);
+            if (warp == 0) {
+                if (lane == 0) {
+                    if (q == 0 && it >= 2) mbar_wait(&acce[acc], (uint32_t)(((it - 2) >> 1) & 1));   // drained
+                    mbar_wait(&full[st], (uint32_t)((g / NS) & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo);
+                    const uint32_t bh = smem_u32(b_hi), bl = smem_u32(b_lo);
+                    constexpr uint32_t A_LBO = (kTM / 8) * 128, B_LBO = (L1 / 8) * 128, SBO = 128;
+                    const uint32_t dacc = tmem_d + (uint32_t)(acc * NCOL);
 #pragma unroll
-                for (int s = 0; s < KQ / 8; ++s) {
-                    const uint32_t aoff = s * 2 * A_LBO;
-                    const uint32_t boff = (q * (KQ / 8) + s) * 2 * B_LBO;
-                    const uint64_t dah = smem_desc(ah + aoff, A_LBO, SBO), dal = smem_desc(al + aoff, A_LBO, SBO);
-                    const uint64_t dbh = smem_desc(bh + boff, B_LBO, SBO), dbl = smem_desc(bl + boff, B_LBO, SBO);
-                    const uint32_t acc0 = (q > 0 || s > 0) ? 1u : 0u;
-                    mma_tf32(dacc, dah, dbh, IDESC, acc0);
-                    mma_tf32(dacc, dah, dbl, IDESC, 1u);
-                    mma_tf32(dacc, dal, dbh, IDESC, 1u);
+                    for (int s8 = 0; s8 < KQ / 8; ++s8) {
+                        const uint32_t aoff = s8 * 2 * A_LBO;
+                        const uint32_t boff = (q * (KQ / 8) + s8) * 2 * B_LBO;
+                        const uint64_t dah = smem_desc(ah + aoff, A_LBO, SBO), dal = smem_desc(al + aoff, A_LBO, SBO);
+                        const uint64_t dbh = smem_desc(bh + boff, B_LBO, SBO), dbl = smem_desc(bl + boff, B_LBO, SBO);
+                        const uint32_t acc0 = (q > 0 || s8 > 0) ? 1u : 0u;
+                        mma_tf32(dacc, dah, dbh, IDESC, acc0);
+                        mma_tf32(dacc, dah, dbl, IDESC, 1u);
+                        mma_tf32(dacc, dal, dbh, IDESC, 1u);
+                    }
+                    mma_commit(&empty[st]);
+                    if (q == NQK - 1) mma_commit(&accf[acc]);
                 }
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-                             ::"r"(smem_u32(&mma_bar[g & 1])) : "memory");
+                __syncwarp();
             }
-            if (q == 0 && prev_tile >= 0) {
-                // the previous tile's accumulator is complete once its last quarter's MMAs retired (they
-                // were issued before this tile's first quarter, which now runs on the other accumulator)
-                wait_quarter(g - 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                epilogue(prev_tile, acc ^ 1);
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            }
+            if (q == 0 && warp >= EPI0 && it >= 1) drain(it - 1, tile - gridDim.x);
         }
-        prev_tile = tile;
     }
-    if (prev_tile >= 0) {
-        wait_quarter(it * NQK - 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        epilogue(prev_tile, (int)((it - 1) & 1));
-    }
+    if (warp >= EPI0 && it >= 1) drain(it - 1, (int64_t)blockIdx.x + (it - 1) * gridDim.x);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0)
@@ -187,8 +209,7 @@ __global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t 
 template <int R, int L1>
 raftgp_status launch_tc(raftgp_ctx ctx, uint64_t seed, int64_t row0, int64_t n, float sigma, const float *W1,
                         const SketchOut &outs) {
-    constexpr int KQ = R < kKQ ? R : kKQ;
-    const size_t smem = 2 * (size_t)L1 * R * 4 + 2 * 2 * (size_t)kTM * KQ * 4;
+    const size_t smem = TcCfg<R, L1>::SMEM;
     static const char attr_key = 0;   // per-(device, instantiation) key
     RG_TRY(per_device(ctx->device, &attr_key, nullptr, [&](int *) -> raftgp_status {
         RG_CUDA(cudaFuncSetAttribute(sketch_w_tc_kernel<R, L1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
