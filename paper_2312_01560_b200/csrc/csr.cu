@@ -650,7 +650,7 @@ __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PAC
     int32_t *cur = bsm + kBucketCap;                    // B cursors (first: the row counts)
     int32_t *off = cur + kMaxBucketRows;                // B + 1 offsets (relative to the bucket start)
     int32_t *big = off + kMaxBucketRows + 1;            // rows longer than kGroupRow
-    __shared__ int fb_base, nbig, qnext, tail, wend;
+    __shared__ int nbig, qnext, tail, wend;
     __shared__ int gtmp[8];
     __shared__ int64_t scan_sh[32];
     const int lane = threadIdx.x & 31;

@@ -72,31 +72,178 @@ __global__ void merge_write(int64_t n, const int64_t *__restrict__ orp, const in
     }
 }
 
-// frontier expansion: nodes at level k - 1 mark their unmarked neighbours with level k
-__global__ void expand_level(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ col, int8_t *level,
-                             int k) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n || level[i] != k - 1) return;
-    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
-        const int32_t j = col[p];
-        if (level[j] > k) level[j] = (int8_t)k;   // idempotent: every writer stores k
+// ---- affected sets as frontier lists. level[i] = hop distance from V' (127 = farther than L + 1). The rows of
+// level k are appended to one list right after those of level k - 1, so R_k = V' u ... u N^k(V') is a PREFIX of
+// the list and the hops of step 3 read prefixes. Only frontier rows are visited (the round-1 version scanned all n
+// rows per level with a thread per row, so a hub's neighbour loop ran serially in one thread).
+__global__ void fill_level(int64_t n, int32_t *level) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        level[i] = 127;
+}
+
+// V' from the changed flags (large-delta path): level 0 and the list head
+__global__ void seed_changed(int64_t n, const int32_t *__restrict__ changed, int32_t *level, int32_t *rows,
+                             int32_t *cnt) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (changed[i]) {
+            level[i] = 0;
+            rows[atomicAdd(cnt, 1)] = (int32_t)i;
+        }
+}
+
+// warp per frontier row (rows[f0 .. f0 + fc)): every neighbour j first reached at level k (atomicMin saw a larger
+// level) is appended exactly once at the end of the list
+__global__ void expand_frontier(const int64_t *__restrict__ rp, const int32_t *__restrict__ col, int32_t *level,
+                                int32_t *rows, int64_t f0, int64_t fc, int k, int32_t *cnt) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = w; t < fc; t += nw) {
+        const int32_t i = rows[f0 + t];
+        for (int64_t p = rp[i] + lane; p < rp[i + 1]; p += 32) {
+            const int32_t j = col[p];
+            if (atomicMin(&level[j], k) > k) rows[atomicAdd(cnt, 1)] = j;   // cnt = the list's length
+        }
     }
 }
 
-__global__ void init_level(int64_t n, const int32_t *__restrict__ changed, int8_t *level) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) level[i] = changed[i] ? 0 : 127;
+// ---- small deltas (m <= kSmallPairs pairs): ONE CTA sorts both orientations of the pairs by (row, col) in shared
+// memory and drops self-loops and duplicates, instead of the full-graph CSR build of the delta (which visits all
+// n rows: bucket sort, visiting order, degrees)
+constexpr int kSmallPairs = 2048;   // 4096 keys x 8 B in static shared memory
+constexpr int kSmallKeys = 2 * kSmallPairs;
+
+__global__ void __launch_bounds__(1024) delta_sort_small(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
+                                                         int64_t m, int64_t n, unsigned long long *__restrict__ keys,
+                                                         int32_t *__restrict__ nkeys, int *__restrict__ err) {
+    __shared__ unsigned long long k[kSmallKeys];
+    __shared__ int32_t wsum[32];
+    const int t = threadIdx.x;
+    int P = 2;
+    while (P < 2 * m) P <<= 1;
+    for (int e = t; e < P; e += blockDim.x) {
+        unsigned long long v = ~0ull;
+        if (e < 2 * m) {
+            const int64_t pi = e >> 1;
+            const int32_t u = src[pi], w = dst[pi];
+            if (u < 0 || w < 0 || u >= n || w >= n) atomicOr(err, 1);
+            else if (u != w) {
+                const uint32_t a = (e & 1) ? (uint32_t)w : (uint32_t)u, b = (e & 1) ? (uint32_t)u : (uint32_t)w;
+                v = ((unsigned long long)a << 32) | b;
+            }
+        }
+        k[e] = v;
+    }
+    __syncthreads();
+    for (int size = 2; size <= P; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int e = t; e < P; e += blockDim.x) {
+                const int o = e ^ stride;
+                if (o > e) {
+                    const bool up = (e & size) == 0;
+                    const unsigned long long a = k[e], b = k[o];
+                    if ((a > b) == up) {
+                        k[e] = b;
+                        k[o] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    // unique, valid keys keep their order: per-thread segment counts, block scan, write
+    const int per = (P + blockDim.x - 1) / blockDim.x;
+    const int e0 = t * per, e1 = min(P, e0 + per);
+    int c = 0;
+    for (int e = e0; e < e1; ++e) c += k[e] != ~0ull && (e == 0 || k[e] != k[e - 1]);
+    int incl = c;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((t & 31) >= o) incl += y;
+    }
+    if ((t & 31) == 31) wsum[t >> 5] = incl;
+    __syncthreads();
+    if (t < 32) {
+        int x = t < (int)(blockDim.x >> 5) ? wsum[t] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (t >= o) x += y;
+        }
+        wsum[t] = x;
+    }
+    __syncthreads();
+    int pos = incl - c + ((t >> 5) ? wsum[(t >> 5) - 1] : 0);
+    for (int e = e0; e < e1; ++e)
+        if (k[e] != ~0ull && (e == 0 || k[e] != k[e - 1])) keys[pos++] = k[e];
+    if (t == blockDim.x - 1) *nkeys = pos;
 }
 
-__global__ void level_flags(int64_t n, const int8_t *__restrict__ level, int k, int32_t *__restrict__ flag) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) flag[i] = level[i] <= k;
+// per sorted delta entry (row u, col v): is v new in u's old row? count per row; the first new entry of a row puts
+// the row on the list (V') at level 0
+__global__ void delta_new(const unsigned long long *__restrict__ keys, const int32_t *__restrict__ nkeys,
+                          const int64_t *__restrict__ orp, const int32_t *__restrict__ ocol, int32_t *__restrict__ add,
+                          uint8_t *__restrict__ isnew, int32_t *level, int32_t *rows, int32_t *cnt) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= *nkeys) return;
+    const int32_t u = (int32_t)(keys[e] >> 32), v = (int32_t)(keys[e] & 0xffffffffu);
+    int64_t lo = orp[u], hi = orp[u + 1];
+    const int64_t oe = hi;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (ocol[mid] < v) lo = mid + 1;
+        else hi = mid;
+    }
+    const bool nw = lo == oe || ocol[lo] != v;
+    isnew[e] = nw;
+    if (nw && atomicAdd(add + u, 1) == 0) {
+        level[u] = 0;
+        rows[atomicAdd(cnt, 1)] = u;
+    }
 }
 
-__global__ void compact_rows(int64_t n, const int32_t *__restrict__ flag, const int64_t *__restrict__ pos,
-                             int32_t *__restrict__ rows) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n && flag[i]) rows[pos[i]] = (int32_t)i;
+__global__ void new_degrees(int64_t n, const int32_t *__restrict__ odeg, const int32_t *__restrict__ add,
+                            int32_t *__restrict__ ndeg) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        ndeg[i] = odeg[i] + add[i];
+}
+
+// write the merged rows (small delta): warp per row; unchanged rows are copied, changed rows merge the old row
+// with the row's new delta entries (a contiguous run of the sorted keys, found by binary search)
+__global__ void merge_write_small(int64_t n, const int64_t *__restrict__ orp, const int32_t *__restrict__ ocol,
+                                  const unsigned long long *__restrict__ keys, const int32_t *__restrict__ nkeys,
+                                  const uint8_t *__restrict__ isnew, const int32_t *__restrict__ add,
+                                  const int64_t *__restrict__ nrp, int32_t *__restrict__ ncol) {
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    const int64_t ob = orp[i], oe = orp[i + 1], nb = nrp[i];
+    if (add[i] == 0) {
+        for (int64_t p = ob + lane; p < oe; p += 32) ncol[nb + (p - ob)] = ocol[p];
+        return;
+    }
+    if (lane != 0) return;
+    int lo = 0, hi = *nkeys;
+    const unsigned long long first = (unsigned long long)i << 32;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (keys[mid] < first) lo = mid + 1;
+        else hi = mid;
+    }
+    int b = lo;
+    const int be = *nkeys;
+    int64_t a = ob, o = nb;
+    auto next_new = [&]() {   // the next new entry of row i, or -1
+        while (b < be && (int64_t)(keys[b] >> 32) == i && !isnew[b]) ++b;
+        return (b < be && (int64_t)(keys[b] >> 32) == i) ? (int32_t)(keys[b] & 0xffffffffu) : -1;
+    };
+    int32_t d = next_new();
+    while (a < oe || d >= 0) {
+        if (d < 0 || (a < oe && ocol[a] < d)) ncol[o++] = ocol[a++];
+        else {
+            ncol[o++] = d;
+            ++b;
+            d = next_new();
+        }
+    }
 }
 
 inline unsigned g256(int64_t n) { return (unsigned)std::max<int64_t>(1, ceil_div(n, 256)); }
@@ -153,85 +300,126 @@ raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const i
     cudaStream_t st = ctx->stream;
     const int64_t n = g->n;
     const int L = s->layers;
-    // ---- 1. delta CSR of E' (canonical: both orientations, sorted, deduplicated, no self-loops)
-    raftgp_graph_s delta;
-    delta.ctx = ctx;
-    RG_TRY(csr_build(ctx, n, m, src, dst, 0, n, &delta));
-    auto drop = [&](raftgp_graph_s &x) {
-        dfree(ctx, x.row_ptr); dfree(ctx, x.col); dfree(ctx, x.deg_local); dfree(ctx, x.order); dfree(ctx, x.deg_all);
-        dfree(ctx, x.s_all); dfree(ctx, x.sh_all);
-    };
-    // ---- merged CSR
+    const bool small = m <= kSmallPairs;
     raftgp_graph ng = new raftgp_graph_s();
     ng->ctx = ctx;
     ng->n = n;
     ng->row_begin = 0;
     ng->row_end = n;
     ng->nl = n;
-    int32_t *changed = nullptr, *flag = nullptr, *rows = nullptr;
-    int64_t *pos = nullptr;
-    int8_t *level = nullptr;
-    raftgp_status rc = dalloc_t(ctx, &ng->deg_local, (size_t)n);
+    auto drop = [&](raftgp_graph_s &x) {
+        dfree(ctx, x.row_ptr); dfree(ctx, x.col); dfree(ctx, x.deg_local); dfree(ctx, x.order); dfree(ctx, x.deg_all);
+        dfree(ctx, x.s_all); dfree(ctx, x.sh_all);
+    };
+    int32_t *add = nullptr, *level = nullptr, *rows = nullptr, *cnt = nullptr, *nkeys = nullptr;
+    int *err = nullptr;
+    unsigned long long *keys = nullptr;
+    uint8_t *isnew = nullptr;
+    raftgp_graph_s delta;
+    delta.ctx = ctx;
+    bool have_delta = false;
+    raftgp_status rc = dalloc_t(ctx, &ng->deg_local, (size_t)std::max<int64_t>(1, n));
     if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &ng->row_ptr, (size_t)n + 1);
-    if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &changed, (size_t)n);
-    if (rc == RAFTGP_OK) {
-        {
-            LaunchScope LS(ctx, K_STREAM);
-            merge_count<<<g256(n), 256, 0, st>>>(n, g->row_ptr, g->col, delta.row_ptr, delta.col, g->deg_local,
-                                                 ng->deg_local, changed);
+    if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &add, (size_t)std::max<int64_t>(1, n));
+    if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &level, (size_t)std::max<int64_t>(1, n));
+    if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &rows, (size_t)std::max<int64_t>(1, n));
+    if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &cnt, 4);   // [0] list length, [1] nkeys, [2] data error
+    if (rc == RAFTGP_OK) rc = dzero(ctx, cnt, 4 * sizeof(int32_t));
+    if (rc == RAFTGP_OK && n > 0) {
+        LaunchScope LS(ctx, K_STREAM);
+        fill_level<<<(unsigned)std::min<int64_t>(g256(n), (int64_t)ctx->sm_count * 8), 256, 0, st>>>(n, level);
+    }
+    nkeys = cnt + 1;
+    err = cnt + 2;
+    // ---- 1. the new entries of every row, V' (rows with new entries) at level 0, new degrees
+    if (rc == RAFTGP_OK && small) {
+        rc = dalloc_t(ctx, &keys, (size_t)kSmallKeys);
+        if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &isnew, (size_t)kSmallKeys);
+        if (rc == RAFTGP_OK) rc = dzero(ctx, add, sizeof(int32_t) * (size_t)std::max<int64_t>(1, n));
+        if (rc == RAFTGP_OK && m > 0) {
+            {
+                LaunchScope LS(ctx, K_STREAM);
+                delta_sort_small<<<1, 1024, 0, st>>>(src, dst, m, n, keys, nkeys, err);
+            }
+            {
+                LaunchScope LS(ctx, K_STREAM);
+                delta_new<<<kSmallKeys / 256, 256, 0, st>>>(keys, nkeys, g->row_ptr, g->col, add, isnew, level, rows, cnt);
+            }
+            RG_CHECK_LAUNCH(ctx);
         }
-        rc = scan_i32_to_i64(ctx, ng->deg_local, ng->row_ptr, n);
+    } else if (rc == RAFTGP_OK) {   // large delta: canonical CSR of E' (both orientations, sorted, deduplicated)
+        rc = csr_build(ctx, n, m, src, dst, 0, n, &delta);
+        have_delta = rc == RAFTGP_OK || delta.row_ptr != nullptr;
+        int32_t *changed = nullptr;
+        if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &changed, (size_t)std::max<int64_t>(1, n));
+        if (rc == RAFTGP_OK && n > 0) {
+            {
+                LaunchScope LS(ctx, K_STREAM);
+                merge_count<<<g256(n), 256, 0, st>>>(n, g->row_ptr, g->col, delta.row_ptr, delta.col, g->deg_local,
+                                                     ng->deg_local, changed);
+            }
+            {
+                LaunchScope LS(ctx, K_STREAM);
+                seed_changed<<<(unsigned)std::min<int64_t>(g256(n), (int64_t)ctx->sm_count * 8), 256, 0, st>>>(
+                    n, changed, level, rows, cnt);
+            }
+            RG_CHECK_LAUNCH(ctx);
+        }
+        if (rc == RAFTGP_OK) rc = dcopy(ctx, add, changed, sizeof(int32_t) * (size_t)std::max<int64_t>(1, n));   // add > 0 <=> changed
+        dfree(ctx, changed);
+    }
+    int32_t head[3] = {0, 0, 0};
+    if (rc == RAFTGP_OK) rc = dread(ctx, head, cnt, sizeof(head), st);   // |V'|, delta keys, data error
+    if (rc == RAFTGP_OK && head[2]) rc = fail(RAFTGP_ERR_DATA, "stream: node id outside [0, n)");
+    // ---- merged CSR (new row pointers from the new degrees; changed rows merged, the others copied)
+    if (rc == RAFTGP_OK && small && n > 0) {
+        LaunchScope LS(ctx, K_STREAM);
+        new_degrees<<<(unsigned)std::min<int64_t>(g256(n), (int64_t)ctx->sm_count * 8), 256, 0, st>>>(n, g->deg_local, add,
+                                                                                                  ng->deg_local);
+    }
+    if (rc == RAFTGP_OK) rc = scan_i32_to_i64(ctx, ng->deg_local, ng->row_ptr, n);
+    if (rc == RAFTGP_OK) rc = dread(ctx, &ng->nnz_local, ng->row_ptr + n, sizeof(int64_t), st);
+    if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &ng->col, (size_t)std::max<int64_t>(1, ng->nnz_local));
+    if (rc == RAFTGP_OK && n > 0) {
+        LaunchScope LS(ctx, K_STREAM);
+        if (small)
+            merge_write_small<<<g256(n * 32), 256, 0, st>>>(n, g->row_ptr, g->col, keys, nkeys, isnew, add, ng->row_ptr,
+                                                             ng->col);
+        else
+            merge_write<<<g256(n * 32), 256, 0, st>>>(n, g->row_ptr, g->col, delta.row_ptr, delta.col, add, ng->row_ptr,
+                                                      ng->col);
     }
     if (rc == RAFTGP_OK) {
-        RG_TRY(dread(ctx, &ng->nnz_local, ng->row_ptr + n, sizeof(int64_t), st));
-        rc = dalloc_t(ctx, &ng->col, (size_t)std::max<int64_t>(1, ng->nnz_local));
+        RG_CHECK_LAUNCH(ctx);
+        rc = dalloc_t(ctx, &ng->deg_all, (size_t)std::max<int64_t>(1, n));
+        if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &ng->s_all, (size_t)std::max<int64_t>(1, n));
+        if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &ng->sh_all, (size_t)std::max<int64_t>(1, n));
     }
     if (rc == RAFTGP_OK) {
-        {
+        if (n > 0) rc = dcopy(ctx, ng->deg_all, ng->deg_local, sizeof(int32_t) * n, st);
+        if (rc == RAFTGP_OK) rc = degrees_finalize(ng);
+    }
+    if (have_delta) drop(delta);
+    dfree(ctx, keys);
+    dfree(ctx, isnew);
+    // ---- 2 + 3. level by level: the frontier of level k - 1 marks level k; then the rows of R_k (a prefix of the
+    // list) are recomputed: the feature hop for k = 1, GCN hop k - 1 for k >= 2
+    std::vector<int64_t> counts(L + 2, 0);
+    counts[0] = head[0];
+    int64_t f0 = 0, fc = head[0];
+    for (int k = 1; k <= L + 1 && rc == RAFTGP_OK; ++k) {
+        if (fc > 0) {
             LaunchScope LS(ctx, K_STREAM);
-            merge_write<<<g256(n * 32), 256, 0, st>>>(n, g->row_ptr, g->col, delta.row_ptr, delta.col, changed,
-                                                      ng->row_ptr, ng->col);
+            const unsigned eg = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(fc, 8), (int64_t)ctx->sm_count * 16));
+            expand_frontier<<<eg, 256, 0, st>>>(ng->row_ptr, ng->col, level, rows, f0, fc, k, cnt);
         }
         RG_CHECK_LAUNCH(ctx);
-        rc = dalloc_t(ctx, &ng->deg_all, (size_t)n);
-        if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &ng->s_all, (size_t)n);
-        if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &ng->sh_all, (size_t)n);
-    }
-    if (rc == RAFTGP_OK) {
-        if (n > 0) RG_TRY(dcopy(ctx, ng->deg_all, ng->deg_local, sizeof(int32_t) * n, st));
-        rc = degrees_finalize(ng);
-    }
-    drop(delta);
-    // ---- 2. affected sets R_1..R_{L+1} (levels 0..L+1 from V')
-    if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &level, (size_t)n);
-    if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &flag, (size_t)n);
-    if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &pos, (size_t)n + 1);
-    if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &rows, (size_t)std::max<int64_t>(1, n));
-    std::vector<int64_t> counts(L + 2, 0);
-    if (rc == RAFTGP_OK) {
-        LaunchScope LS(ctx, K_STREAM);
-        init_level<<<g256(n), 256, 0, st>>>(n, changed, level);
-    }
-    for (int k = 1; k <= L + 1 && rc == RAFTGP_OK; ++k) {
-        LaunchScope LS(ctx, K_STREAM);
-        expand_level<<<g256(n), 256, 0, st>>>(n, ng->row_ptr, ng->col, level, k);
-    }
-    // |V'| and the sizes of R_k (synchronous reads: the row lists are built per set below)
-    for (int k = 0; k <= L + 1 && rc == RAFTGP_OK; ++k) {
-        {
-            LaunchScope LS(ctx, K_STREAM);
-            level_flags<<<g256(n), 256, 0, st>>>(n, level, k, flag);
-        }
-        rc = scan_i32_to_i64(ctx, flag, pos, n);
-        if (rc == RAFTGP_OK) {
-            RG_TRY(dread(ctx, &counts[k], pos + n, sizeof(int64_t), st));
-        }
-        if (rc != RAFTGP_OK || k == 0) continue;
-        // ---- 3. recompute the rows of R_k: the feature hop for k = 1, GCN hop k - 1 for k >= 2
-        {
-            LaunchScope LS(ctx, K_STREAM);
-            compact_rows<<<g256(n), 256, 0, st>>>(n, flag, pos, rows);
-        }
+        int32_t total = 0;
+        rc = dread(ctx, &total, cnt, sizeof(int32_t), st);
+        if (rc != RAFTGP_OK) break;
+        f0 += fc;
+        fc = total - f0;
+        counts[k] = total;   // |R_k|: the list prefix
         const auto &d = s->dims;
         if (k == 1) {
             rc = feature_hop_pre_rows(ng, RAFTGP_NCUT, d[1], s->thw, nullptr, s->T[1], rows, counts[1]);
@@ -242,7 +430,7 @@ raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const i
                               last ? 0 : d[h + 1], last ? nullptr : s->T[h + 1], rows, counts[k]);
         }
     }
-    dfree(ctx, changed); dfree(ctx, flag); dfree(ctx, pos); dfree(ctx, rows); dfree(ctx, level);
+    dfree(ctx, add); dfree(ctx, level); dfree(ctx, rows); dfree(ctx, cnt);
     if (rc != RAFTGP_OK) {
         drop(*ng);
         delete ng;

@@ -211,8 +211,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tf32x3(const float *__re
     // epilogue: warp w reads TMEM lanes 32w..32w+31 (tile rows), 32 columns at a time
     const int64_t row = mt * kGM + warp * 32 + lane;
     const float sc = (row_scale && row < M) ? row_scale[row] : 1.0f;
-#pragma unroll 1
     const int nacc = KBn < G::NACC ? KBn : G::NACC;   // accumulators that received at least one k-block
+#pragma unroll 1
     for (int c0 = 0; c0 < NT; c0 += 32) {
         float v[32];
         tmem_ld32(tmem_d + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
@@ -599,11 +599,11 @@ __global__ void wide_row_scale(const float *__restrict__ ssq, int nw, int64_t n,
     scale[i] = ss > 0.f ? sh[i] / sqrtf(ss) : sh[i];
 }
 
-#ifndef RG_WIDE_U
-#define RG_WIDE_U 4
+#ifndef RG_WIDE_U   // neighbours in flight per lane; U = 6 / U_DUAL = 4: Table I wide hops 51.3 vs 54.1 ms with 4 / 2
+#define RG_WIDE_U 6
 #endif
 #ifndef RG_WIDE_U_DUAL
-#define RG_WIDE_U_DUAL 2
+#define RG_WIDE_U_DUAL 4
 #endif
 
 int wide_ssq_slices(int32_t w);
@@ -718,9 +718,12 @@ raftgp_status launch_gemm(raftgp_ctx ctx, const float *Ahi, const float *Alo, co
 }  // namespace
 
 // N-tile width used for an output of N columns (a power of two in [32, 128]: at least 4 accumulators)
+#ifndef RG_GEMM_NT_MAX   // 256-column output tiles: Table I GEMMs 22.3 vs 25.1 ms with 128 (fewer operand bytes per MAC)
+#define RG_GEMM_NT_MAX 256
+#endif
 int gemm_nt(int N) {
     int nt = 32;
-    while (nt < N && nt < 128) nt <<= 1;
+    while (nt < N && nt < RG_GEMM_NT_MAX) nt <<= 1;
     return nt;
 }
 
@@ -768,6 +771,9 @@ raftgp_status gemm_tiled(raftgp_ctx ctx, const float *Ahi, const float *Alo, con
     switch (gemm_nt(N)) {
         case 32: return launch_gemm<32>(ctx, Ahi, Alo, Bhi, Blo, M, Kp, N, row_scale, C, ldc);
         case 64: return launch_gemm<64>(ctx, Ahi, Alo, Bhi, Blo, M, Kp, N, row_scale, C, ldc);
+#if RG_GEMM_NT_MAX >= 256
+        case 256: return launch_gemm<256>(ctx, Ahi, Alo, Bhi, Blo, M, Kp, N, row_scale, C, ldc);
+#endif
         default: return launch_gemm<128>(ctx, Ahi, Alo, Bhi, Blo, M, Kp, N, row_scale, C, ldc);
     }
 }

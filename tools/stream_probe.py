@@ -24,7 +24,9 @@ ctx = rg.Context(0)
 g = rg.raftgp_build_csr(ctx, gr.n, torch.from_numpy(gr.src).cuda(), torch.from_numpy(gr.dst).cuda())
 s = rg.Stream(g, cfg.dims, 0)
 rng = np.random.default_rng(5)
+ctx.set_profiling(True)
 for i in range(a.reps):
+    ctx.prof_reset()
     src = torch.from_numpy(rng.integers(0, gr.n, a.batch).astype(np.int32)).cuda()
     dst = torch.from_numpy(rng.integers(0, gr.n, a.batch).astype(np.int32)).cuda()
     torch.cuda.synchronize()
@@ -32,3 +34,6 @@ for i in range(a.reps):
     st = s.add_edges(src, dst)
     torch.cuda.synchronize()
     print(f"batch {a.batch}: {1e3 * (time.perf_counter() - t):.2f} ms {st}", flush=True)
+    prof = ctx.prof_read()
+    print("   kernels (ms, launches):", {k: (round(v[0], 3), v[1]) for k, v in sorted(prof.items(), key=lambda x: -x[1][0])},
+          "sum %.2f ms" % sum(v[0] for v in prof.values()), flush=True)
