@@ -210,6 +210,8 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
                         int64_t re, raftgp_graph g);
 raftgp_status degrees_finalize(raftgp_graph g);
 raftgp_status compute_order(raftgp_graph g);
+// a row list reordered for the hop kernels: heavy rows spread from the front (order.cu)
+raftgp_status spread_heavy_list(raftgp_ctx ctx, const int32_t *rows, int64_t count, const int32_t *deg, int32_t *out);
 // whether order[0..nl) is a permutation of 0..nl-1 (device check, synchronous)
 raftgp_status order_is_permutation(raftgp_ctx ctx, const int32_t *order, int64_t nl, bool *ok);      // g->order (label propagation + counting sort)   // deg_all -> two_e, s_all, sh_all, deg_hist
 

@@ -129,6 +129,54 @@ __global__ void heavy_place(const int32_t *__restrict__ flag, const int64_t *__r
     order[pos] = (int32_t)i;
 }
 
+// The same spreading for a LIST of rows (the streamed hops, stream.cu): heavy rows every s positions from the front,
+// s = min(32, count / H) (>= 1), the light rows in list order around them. H is read on the device (no host sync).
+__global__ void heavy_flags_list(const int32_t *__restrict__ rows, int64_t count, const int32_t *__restrict__ deg,
+                                 int32_t *__restrict__ flag) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x)
+        flag[t] = deg[rows[t]] > kHeavyDeg ? 1 : 0;
+}
+
+__global__ void heavy_place_list(const int32_t *__restrict__ rows, const int32_t *__restrict__ flag,
+                                 const int64_t *__restrict__ hrank, int64_t count, int32_t *__restrict__ out) {
+    const int64_t H = hrank[count];
+    const int64_t sp = H > 0 ? (count / H < 32 ? count / H : 32) : 32;   // >= 1 since H <= count
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t h = hrank[t];
+        int64_t pos;
+        if (flag[t]) {
+            pos = sp * h;
+        } else {
+            const int64_t j = t - h;   // light index
+            pos = (sp > 1 && j < (sp - 1) * H) ? (j / (sp - 1)) * sp + j % (sp - 1) + 1 : j + H;
+        }
+        out[pos] = rows[t];
+    }
+}
+
+raftgp_status spread_heavy_list(raftgp_ctx ctx, const int32_t *rows, int64_t count, const int32_t *deg, int32_t *out) {
+    if (count <= 0) return RAFTGP_OK;
+    int32_t *flag = nullptr;
+    int64_t *hrank = nullptr;
+    RG_TRY(dalloc_t(ctx, &flag, (size_t)count));
+    RG_TRY(dalloc_t(ctx, &hrank, (size_t)count + 1));
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(count, 256), (int64_t)ctx->sm_count * 8);
+    {
+        LaunchScope L(ctx, K_ORDER);
+        heavy_flags_list<<<grid, 256, 0, ctx->stream>>>(rows, count, deg, flag);
+    }
+    RG_CHECK_LAUNCH(ctx);
+    RG_TRY(scan_i32_to_i64(ctx, flag, hrank, count));
+    {
+        LaunchScope L(ctx, K_ORDER);
+        heavy_place_list<<<grid, 256, 0, ctx->stream>>>(rows, flag, hrank, count, out);
+    }
+    RG_CHECK_LAUNCH(ctx);
+    dfree(ctx, flag);
+    dfree(ctx, hrank);
+    return RAFTGP_OK;
+}
+
 namespace {
 // order validation: cnt[v] += 1 for every listed row (err if out of range), then err if any cnt != 1
 __global__ void order_count(const int32_t *__restrict__ order, int64_t nl, int32_t *cnt, int32_t *err) {

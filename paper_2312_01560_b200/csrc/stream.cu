@@ -84,11 +84,18 @@ __global__ void fill_level(int64_t n, int32_t *level) {
 // V' from the changed flags (large-delta path): level 0 and the list head
 __global__ void seed_changed(int64_t n, const int32_t *__restrict__ changed, int32_t *level, int32_t *rows,
                              int32_t *cnt) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        if (changed[i]) {
-            level[i] = 0;
-            rows[atomicAdd(cnt, 1)] = (int32_t)i;
-        }
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {   // whole warps iterate together
+        const int64_t i = i0 + threadIdx.x;
+        const bool c = i < n && changed[i];
+        if (c) level[i] = 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, c);
+        int base = 0;
+        if (lane == 0 && bal) base = atomicAdd(cnt, __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (c) rows[base + __popc(bal & ((1u << lane) - 1u))] = (int32_t)i;
+    }
 }
 
 // warp per frontier row (rows[f0 .. f0 + fc)): every neighbour j first reached at level k (atomicMin saw a larger
@@ -100,9 +107,17 @@ __global__ void expand_frontier(const int64_t *__restrict__ rp, const int32_t *_
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t t = w; t < fc; t += nw) {
         const int32_t i = rows[f0 + t];
-        for (int64_t p = rp[i] + lane; p < rp[i + 1]; p += 32) {
-            const int32_t j = col[p];
-            if (atomicMin(&level[j], k) > k) rows[atomicAdd(cnt, 1)] = j;   // cnt = the list's length
+        const int64_t b = rp[i], e = rp[i + 1];
+        for (int64_t p0 = b; p0 < e; p0 += 32) {
+            const int64_t p = p0 + lane;
+            const int32_t j = p < e ? col[p] : 0;
+            const bool fresh = p < e && atomicMin(&level[j], k) > k;
+            // warp-aggregated append (one atomic per warp and chunk, not per row: the list counter is one address)
+            const unsigned bal = __ballot_sync(0xffffffffu, fresh);
+            int base = 0;
+            if (lane == 0 && bal) base = atomicAdd(cnt, __popc(bal));   // cnt = the list's length
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (fresh) rows[base + __popc(bal & ((1u << lane) - 1u))] = j;
         }
     }
 }
@@ -200,27 +215,74 @@ __global__ void delta_new(const unsigned long long *__restrict__ keys, const int
     }
 }
 
-__global__ void new_degrees(int64_t n, const int32_t *__restrict__ odeg, const int32_t *__restrict__ add,
-                            int32_t *__restrict__ ndeg) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        ndeg[i] = odeg[i] + add[i];
+// V' (rows[0 .. nc), any order, nc <= kSmallKeys) sorted ascending by one CTA; ends[t] = old end of the t-th changed
+// row, shift[t] = new entries of the changed rows before it (so an old entry p after t changed rows moves by shift[t])
+__global__ void __launch_bounds__(1024) changed_table(const int32_t *__restrict__ rows, int nc,
+                                                      const int64_t *__restrict__ orp, const int32_t *__restrict__ add,
+                                                      int32_t *__restrict__ sorted, int64_t *__restrict__ ends,
+                                                      int64_t *__restrict__ shift) {
+    __shared__ int32_t k[kSmallKeys];
+    const int t = threadIdx.x;
+    int P = 1;
+    while (P < nc) P <<= 1;
+    for (int e = t; e < P; e += blockDim.x) k[e] = e < nc ? rows[e] : 0x7fffffff;
+    __syncthreads();
+    for (int size = 2; size <= P; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int e = t; e < P; e += blockDim.x) {
+                const int o = e ^ stride;
+                if (o > e) {
+                    const bool up = (e & size) == 0;
+                    const int32_t a = k[e], b = k[o];
+                    if ((a > b) == up) {
+                        k[e] = b;
+                        k[o] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    if (t == 0) {   // serial prefix over <= 4096 entries
+        int64_t acc = 0;
+        for (int e = 0; e < nc; ++e) {
+            sorted[e] = k[e];
+            ends[e] = orp[k[e] + 1];
+            shift[e] = acc;
+            acc += add[k[e]];
+        }
+        shift[nc] = acc;
+    }
 }
 
-// write the merged rows (small delta): warp per row; unchanged rows are copied, changed rows merge the old row
-// with the row's new delta entries (a contiguous run of the sorted keys, found by binary search)
-__global__ void merge_write_small(int64_t n, const int64_t *__restrict__ orp, const int32_t *__restrict__ ocol,
-                                  const unsigned long long *__restrict__ keys, const int32_t *__restrict__ nkeys,
-                                  const uint8_t *__restrict__ isnew, const int32_t *__restrict__ add,
-                                  const int64_t *__restrict__ nrp, int32_t *__restrict__ ncol) {
-    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (i >= n) return;
-    const int64_t ob = orp[i], oe = orp[i + 1], nb = nrp[i];
-    if (add[i] == 0) {
-        for (int64_t p = ob + lane; p < oe; p += 32) ncol[nb + (p - ob)] = ocol[p];
-        return;
+// the unchanged rows of the merged CSR: every old entry p outside the changed rows moves by the new entries of the
+// changed rows before it (a streaming, coalesced copy; the changed rows are written by merge_changed)
+__global__ void merge_copy(int64_t nnz, const int32_t *__restrict__ ocol, const int32_t *__restrict__ sorted,
+                           const int64_t *__restrict__ orp, const int64_t *__restrict__ ends,
+                           const int64_t *__restrict__ shift, int nc, int32_t *__restrict__ ncol) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = nc;   // t = changed rows that end at or before p
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (ends[mid] <= p) lo = mid + 1;
+            else hi = mid;
+        }
+        if (lo < nc && orp[sorted[lo]] <= p) continue;   // inside a changed row
+        ncol[p + shift[lo]] = ocol[p];
     }
-    if (lane != 0) return;
+}
+
+// the changed rows: warp per row. The row's new entries d_0 < d_1 < ... are a contiguous run of the sorted keys
+// (flagged new); every old entry moves by the number of new entries below it and every new entry lands after the old
+// entries below it (binary searches, all lanes in parallel: a hub row is not merged by one lane)
+__global__ void merge_changed(const int32_t *__restrict__ sorted, int nc, const int64_t *__restrict__ orp,
+                              const int32_t *__restrict__ ocol, const unsigned long long *__restrict__ keys,
+                              const int32_t *__restrict__ nkeys, const uint8_t *__restrict__ isnew,
+                              const int64_t *__restrict__ nrp, int32_t *__restrict__ ncol) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= nc) return;
+    const int64_t i = sorted[w];
+    const int64_t ob = orp[i], oe = orp[i + 1], nb = nrp[i];
     int lo = 0, hi = *nkeys;
     const unsigned long long first = (unsigned long long)i << 32;
     while (lo < hi) {
@@ -228,22 +290,58 @@ __global__ void merge_write_small(int64_t n, const int64_t *__restrict__ orp, co
         if (keys[mid] < first) lo = mid + 1;
         else hi = mid;
     }
-    int b = lo;
-    const int be = *nkeys;
-    int64_t a = ob, o = nb;
-    auto next_new = [&]() {   // the next new entry of row i, or -1
-        while (b < be && (int64_t)(keys[b] >> 32) == i && !isnew[b]) ++b;
-        return (b < be && (int64_t)(keys[b] >> 32) == i) ? (int32_t)(keys[b] & 0xffffffffu) : -1;
-    };
-    int32_t d = next_new();
-    while (a < oe || d >= 0) {
-        if (d < 0 || (a < oe && ocol[a] < d)) ncol[o++] = ocol[a++];
-        else {
-            ncol[o++] = d;
-            ++b;
-            d = next_new();
+    int kb = lo, ke = lo;
+    while (ke < *nkeys && (int64_t)(keys[ke] >> 32) == i) ++ke;   // the row's delta run [kb, ke), few entries
+    // new entries: rank among the new ones (prefix count of isnew) + old entries below
+    for (int q = kb + lane; q < ke; q += 32) {
+        if (!isnew[q]) continue;
+        int r = 0;
+        for (int u = kb; u < q; ++u) r += isnew[u];
+        const int32_t d = (int32_t)(keys[q] & 0xffffffffu);
+        int64_t a = ob, b = oe;
+        while (a < b) {
+            const int64_t mid = (a + b) >> 1;
+            if (ocol[mid] < d) a = mid + 1;
+            else b = mid;
         }
+        ncol[nb + (a - ob) + r] = d;
     }
+    // old entries: index + new entries below
+    for (int64_t p = ob + lane; p < oe; p += 32) {
+        const int32_t v = ocol[p];
+        int r = 0;
+        for (int u = kb; u < ke; ++u) r += isnew[u] && (int32_t)(keys[u] & 0xffffffffu) < v;
+        ncol[nb + (p - ob) + r] = v;
+    }
+}
+
+// merged rows, warp per row (many changed rows): unchanged rows copied, changed rows left to merge_changed
+__global__ void merge_rows_copy(int64_t n, const int64_t *__restrict__ orp, const int32_t *__restrict__ ocol,
+                                const int32_t *__restrict__ add, const int64_t *__restrict__ nrp,
+                                int32_t *__restrict__ ncol) {
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= n || add[i] != 0) return;
+    const int64_t ob = orp[i], oe = orp[i + 1], nb = nrp[i];
+    for (int64_t p = ob + lane; p < oe; p += 32) ncol[nb + (p - ob)] = ocol[p];
+}
+
+__global__ void new_degrees(int64_t n, const int32_t *__restrict__ odeg, const int32_t *__restrict__ add,
+                            int32_t *__restrict__ ndeg) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        ndeg[i] = odeg[i] + add[i];
+}
+
+// R_k in natural row order (for large sets: the hop then streams row_ptr / col_idx like a full pass)
+__global__ void level_flags(int64_t n, const int32_t *__restrict__ level, int k, int32_t *__restrict__ flag) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = level[i] <= k;
+}
+
+__global__ void compact_rows(int64_t n, const int32_t *__restrict__ flag, const int64_t *__restrict__ pos,
+                             int32_t *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (flag[i]) out[pos[i]] = (int32_t)i;
 }
 
 inline unsigned g256(int64_t n) { return (unsigned)std::max<int64_t>(1, ceil_div(n, 256)); }
@@ -380,14 +478,40 @@ raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const i
     if (rc == RAFTGP_OK) rc = scan_i32_to_i64(ctx, ng->deg_local, ng->row_ptr, n);
     if (rc == RAFTGP_OK) rc = dread(ctx, &ng->nnz_local, ng->row_ptr + n, sizeof(int64_t), st);
     if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &ng->col, (size_t)std::max<int64_t>(1, ng->nnz_local));
-    if (rc == RAFTGP_OK && n > 0) {
+    if (rc == RAFTGP_OK && n > 0 && small) {   // coalesced copy of the unchanged rows + merge of the |V'| changed rows
+        const int nc = head[0];
+        int32_t *sorted = nullptr;
+        int64_t *ends = nullptr, *shift = nullptr;
+        rc = dalloc_t(ctx, &sorted, (size_t)nc + 1);
+        if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &ends, (size_t)nc + 1);
+        if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &shift, (size_t)nc + 1);
+        if (rc == RAFTGP_OK) {
+            {
+                LaunchScope LS(ctx, K_STREAM);
+                changed_table<<<1, 1024, 0, st>>>(rows, nc, g->row_ptr, add, sorted, ends, shift);
+            }
+            if (g->nnz_local > 0 && nc <= 64) {   // few changed rows: a streaming element-wise copy
+                LaunchScope LS(ctx, K_STREAM);
+                merge_copy<<<(unsigned)std::min<int64_t>(ceil_div(g->nnz_local, 256), (int64_t)ctx->sm_count * 16), 256, 0,
+                             st>>>(g->nnz_local, g->col, sorted, g->row_ptr, ends, shift, nc, ng->col);
+            } else if (g->nnz_local > 0) {        // many: warp per row (the element-wise search would cost more)
+                LaunchScope LS(ctx, K_STREAM);
+                merge_rows_copy<<<g256(n * 32), 256, 0, st>>>(n, g->row_ptr, g->col, add, ng->row_ptr, ng->col);
+            }
+            if (nc > 0) {
+                LaunchScope LS(ctx, K_STREAM);
+                merge_changed<<<(unsigned)ceil_div((int64_t)nc * 32, 256), 256, 0, st>>>(sorted, nc, g->row_ptr, g->col, keys,
+                                                                                      nkeys, isnew, ng->row_ptr, ng->col);
+            }
+            RG_CHECK_LAUNCH(ctx);
+        }
+        dfree(ctx, sorted);
+        dfree(ctx, ends);
+        dfree(ctx, shift);
+    } else if (rc == RAFTGP_OK && n > 0) {
         LaunchScope LS(ctx, K_STREAM);
-        if (small)
-            merge_write_small<<<g256(n * 32), 256, 0, st>>>(n, g->row_ptr, g->col, keys, nkeys, isnew, add, ng->row_ptr,
-                                                             ng->col);
-        else
-            merge_write<<<g256(n * 32), 256, 0, st>>>(n, g->row_ptr, g->col, delta.row_ptr, delta.col, add, ng->row_ptr,
-                                                      ng->col);
+        merge_write<<<g256(n * 32), 256, 0, st>>>(n, g->row_ptr, g->col, delta.row_ptr, delta.col, add, ng->row_ptr,
+                                                  ng->col);
     }
     if (rc == RAFTGP_OK) {
         RG_CHECK_LAUNCH(ctx);
@@ -406,6 +530,9 @@ raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const i
     // list) are recomputed: the feature hop for k = 1, GCN hop k - 1 for k >= 2
     std::vector<int64_t> counts(L + 2, 0);
     counts[0] = head[0];
+    int32_t *hop_rows = nullptr, *nat_rows = nullptr;
+    if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &hop_rows, (size_t)std::max<int64_t>(1, n));
+    if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &nat_rows, (size_t)std::max<int64_t>(1, n));
     int64_t f0 = 0, fc = head[0];
     for (int k = 1; k <= L + 1 && rc == RAFTGP_OK; ++k) {
         if (fc > 0) {
@@ -421,16 +548,43 @@ raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const i
         fc = total - f0;
         counts[k] = total;   // |R_k|: the list prefix
         const auto &d = s->dims;
+        // the hop visits R_k with its heavy rows spread from the front (one per dynamic claim where possible), so no
+        // hub is left for the end of the launch; a separate list: the frontier positions of `rows` stay intact
+        // (a set covering much of the graph is first put in natural row order: row_ptr / col_idx then stream)
+        const int32_t *list = rows;
+        if (counts[k] * 8 >= n) {
+            int32_t *flag = nullptr;
+            int64_t *pos = nullptr;
+            rc = dalloc_t(ctx, &flag, (size_t)n);
+            if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &pos, (size_t)n + 1);
+            if (rc == RAFTGP_OK) {
+                const unsigned gg = (unsigned)std::min<int64_t>(g256(n), (int64_t)ctx->sm_count * 8);
+                {
+                    LaunchScope LS(ctx, K_STREAM);
+                    level_flags<<<gg, 256, 0, st>>>(n, level, k, flag);
+                }
+                rc = scan_i32_to_i64(ctx, flag, pos, n);
+                if (rc == RAFTGP_OK) {
+                    LaunchScope LS(ctx, K_STREAM);
+                    compact_rows<<<gg, 256, 0, st>>>(n, flag, pos, nat_rows);
+                }
+                list = nat_rows;
+            }
+            dfree(ctx, flag);
+            dfree(ctx, pos);
+        }
+        if (rc == RAFTGP_OK) rc = spread_heavy_list(ctx, list, counts[k], ng->deg_local, hop_rows);
+        if (rc != RAFTGP_OK) break;
         if (k == 1) {
-            rc = feature_hop_pre_rows(ng, RAFTGP_NCUT, d[1], s->thw, nullptr, s->T[1], rows, counts[1]);
+            rc = feature_hop_pre_rows(ng, RAFTGP_NCUT, d[1], s->thw, nullptr, s->T[1], hop_rows, counts[1]);
         } else {
             const int h = k - 1;   // GCN hop h reads T_h, writes T_{h+1} (or Z after the last layer)
             const bool last = h == L;
             rc = gcn_hop_rows(ng, s->T[h], d[h], last ? s->Z : nullptr, last ? nullptr : s->W[h + 1],
-                              last ? 0 : d[h + 1], last ? nullptr : s->T[h + 1], rows, counts[k]);
+                              last ? 0 : d[h + 1], last ? nullptr : s->T[h + 1], hop_rows, counts[k]);
         }
     }
-    dfree(ctx, add); dfree(ctx, level); dfree(ctx, rows); dfree(ctx, cnt);
+    dfree(ctx, add); dfree(ctx, level); dfree(ctx, rows); dfree(ctx, cnt); dfree(ctx, hop_rows); dfree(ctx, nat_rows);
     if (rc != RAFTGP_OK) {
         drop(*ng);
         delete ng;
