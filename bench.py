@@ -912,13 +912,13 @@ def main():
                 s_, c_, Zl, Hl, cs_, ev = lanes[i % len(lanes)]
                 b = (i // len(lanes)) % 2
                 with torch.cuda.stream(s_):
-                    sd = src_h.to(dev, non_blocking=True)
-                    dd = dst_h.to(dev, non_blocking=True)
+                    # the C-ABI gets the HOST (pinned) edge arrays (RAFTGP_HOST_PTRS): the library copies them in on
+                    # its stream inside the call
                     if args.e2e_api == "build_embed":
                         s_.wait_event(ev[b])           # Zl[b] is free once its previous D2H is done
-                        rg.raftgp_build_embed(c_, gr.n, sd, dd, variants, dims, args.seed, Z=Zl[b])
+                        rg.raftgp_build_embed(c_, gr.n, src_h, dst_h, variants, dims, args.seed, Z=Zl[b])
                     else:
-                        g = rg.raftgp_build_csr(c_, gr.n, sd, dd)
+                        g = rg.raftgp_build_csr(c_, gr.n, src_h, dst_h)
                         s_.wait_event(ev[b])
                         rg.raftgp_embed_multi(g, variants, dims, args.seed, Z=Zl[b])
                         g.close()
@@ -943,8 +943,9 @@ def main():
                 lanes[0][0].wait_stream(cs_)
             e1.record(lanes[0][0])
             torch.cuda.synchronize()
-            mode = (f"pipelined: {args.e2e_lanes} contexts/streams (+ a D2H stream each), {args.e2e_api} per step; "
-                    "step k's copies overlap other steps' kernels")
+            mode = (f"pipelined: {args.e2e_lanes} contexts/streams (+ a D2H stream each), {args.e2e_api} per step with "
+                    "the host edge arrays (RAFTGP_HOST_PTRS: H2D inside the C-ABI call), Z copied to pinned host "
+                    "memory; step k's copies overlap other steps' kernels")
         else:
             out_host = {v: torch.empty((rows, dims[-1]), dtype=torch.float32).pin_memory() for v in variants}
             step(src_h, dst_h, out_host)
