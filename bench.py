@@ -791,7 +791,9 @@ def main():
     # ---------------- a3: the sketch as an ALU-bound kernel (N = 1)
     sketch_roof = None
     if world == 1 and sketch_ok(cfg):
-        sketch_roof = measure_sketch(args, rg, ctx, gr.n, cfg.r, dims[1], barrier, clocks.summary().get("sm_mhz"))
+        ctx.trim()   # the step's cached workspace back to the device (C5 holds ~128 GB of it)
+        sketch_roof = measure_sketch(args, rg, ctx, min(gr.n, 5_000_000), cfg.r, dims[1], barrier,
+                                     clocks.summary().get("sm_mhz"))
 
     # ---------------- NEXT-1: Alg. 1 model selection on this step's embeddings (whole graph, N = 1)
     select = None

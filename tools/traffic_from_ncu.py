@@ -1,7 +1,7 @@
 """Per-launch DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) of the hop kernels from an ncu
 --set full report, averaged per kernel family as bench.py's roofline uses them:
   feature_hop = hop_kernel<0|1|2|5,...> (feature kinds), gcn_hop = hop_kernel<3|6,...> (GCN, paired GCN).
-Usage: python tools/traffic_from_ncu.py <report.ncu-rep> <config> [out.json]"""
+Usage: python tools/traffic_from_ncu.py <report.ncu-rep | raw-page.csv> <config> [out.json]"""
 import csv
 import json
 import subprocess
@@ -9,7 +9,8 @@ import sys
 
 rep, cfg = sys.argv[1], sys.argv[2]
 out = sys.argv[3] if len(sys.argv) > 3 else "profiles/ncu_traffic.json"
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+raw = (open(rep).read() if rep.endswith(".csv") else
+       subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout)
 rows = list(csv.reader(raw.splitlines()))
 hdr, units, data = rows[0], rows[1], rows[2:]
 mul = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
