@@ -50,18 +50,45 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
+def _compile_one(args):
+    cmd, obj = args
+    subprocess.check_call(cmd)
+    return obj
+
+
 def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """One object per .cu (compiled in parallel, reused while the .cu, the headers and the defines are unchanged),
+    then one shared-library link. The .cu files share no device code, so no relocatable device code is needed."""
     if out == LIB and not force and not _stale():
         return LIB
+    import hashlib
+    from concurrent.futures import ThreadPoolExecutor
     nvcc = os.environ.get("NVCC", "nvcc")
     tmp = out + ".tmp"
     nh = nccl_home()
     nlib = os.path.join(nh, "lib")
-    cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-I", os.path.join(nh, "include"),
-           "-o", tmp, *sources(), "-Xlinker", os.path.join(nlib, "libnccl.so.2"), "-Xlinker", f"-rpath,{nlib}"]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
+    key = hashlib.sha1(" ".join([*NVCC_FLAGS, *defines, nh]).encode()).hexdigest()[:10]
+    objdir = os.path.join(os.path.dirname(HERE), "build", "obj")
+    os.makedirs(objdir, exist_ok=True)
+    hdrs = glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(INCLUDE, "raftgp.h"), __file__]
+    hdr_t = max(os.path.getmtime(p) for p in hdrs)
+    jobs, objs = [], []
+    cflags = [f for f in NVCC_FLAGS if f != "-shared"]
+    for src in sources():
+        obj = os.path.join(objdir, f"{os.path.basename(src)}.{key}.o")
+        objs.append(obj)
+        if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(hdr_t, os.path.getmtime(src)):
+            cmd = [nvcc, *cflags, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-I", os.path.join(nh, "include"),
+                   "-c", src, "-o", obj]
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+                print(" ".join(cmd), file=sys.stderr)
+            jobs.append((cmd, obj))
+    if jobs:
+        with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
+            list(ex.map(_compile_one, jobs))
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
+           "-Xlinker", os.path.join(nlib, "libnccl.so.2"), "-Xlinker", f"-rpath,{nlib}"]
     subprocess.check_call(cmd)
     os.replace(tmp, out)
     return out

@@ -490,6 +490,213 @@ __global__ void __launch_bounds__(1024) csr_partition(const int32_t *__restrict_
     }
 }
 
+// ---------------------------------------------------------------- two-level partition (default)
+// The one-level partition above writes every entry straight to its bucket front: with ~10^4 buckets shared by all
+// SMs each warp store touches 32 different sectors that other SMs are writing too, and the stores bound it
+// (microbenchmark, 10^8 pairs: ranks alone 0.6 ms, with the scattered stores 5 ms). The two-level path stages
+// every tile in shared memory in bucket order and writes each bucket's run of the tile with coalesced stores
+// into a region no other CTA writes:
+//   level 1 (csr_coarse_part): CTA c takes the same contiguous range of raw pairs as in the count pass, whose
+//            per-(coarse bucket, CTA) counts give it a private region of every coarse bucket (2^cs rows, <=
+//            kMaxCoarse buckets); per tile of kCT pairs: warp-private counts -> scan over buckets -> ranks into
+//            the stage (shared-memory atomics on the warp's own counters) -> runs copied out. Entries are
+//            (row in coarse bucket, neighbour) int2.
+//   level 2 (csr_fine_part): one CTA per coarse bucket counts its F = 2^(cs - shift) fine buckets (2^shift rows,
+//            the bucket sort's unit), writes their starts, then splits the coarse bucket tile by tile the same
+//            way into Entry<PACKED> form.
+// Both are deterministic (no global atomics); the bucket sort makes the result canonical anyway.
+constexpr int kPT = 512;           // threads of the level-1 / level-2 CTAs (2 CTAs per SM: one stages while the other loads)
+constexpr int kPW = kPT / 32;
+constexpr int kCT = 4096;          // level-1 tile: pairs (8 per thread)
+constexpr int kFT = 4096;          // level-2 tile: entries (8 per thread)
+constexpr int kMaxCoarse = 512;    // level-1 buckets (kPW warp-private counters each: 32 KB)
+constexpr int kMaxFine = 256;      // fine buckets per coarse bucket
+
+// bins <= kPT bucket counters held per warp in cnt[kPW][nb]: totals -> tot, exclusive scan over the buckets ->
+// ls, and every warp's counter becomes its first slot (ls + the counts of the lower warps). kPT threads; the
+// caller syncs before (counts complete) and after.
+__device__ __forceinline__ void bins_scan(unsigned *cnt, int nbins, unsigned *ls, unsigned *tot, unsigned *wsum) {
+    const int b = threadIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned t = 0u;
+    if (b < nbins)
+#pragma unroll 8
+        for (int w = 0; w < kPW; ++w) t += cnt[w * nbins + b];
+    unsigned x = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        const unsigned y = lane < kPW ? wsum[lane] : 0u;
+        unsigned z = y;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned q = __shfl_up_sync(0xffffffffu, z, o);
+            if (lane >= o) z += q;
+        }
+        if (lane < kPW) wsum[lane] = z - y;
+    }
+    __syncthreads();
+    if (b < nbins) {
+        unsigned p = wsum[wid] + x - t;
+        ls[b] = p;
+        tot[b] = t;
+#pragma unroll 8
+        for (int w = 0; w < kPW; ++w) {
+            const unsigned c = cnt[w * nbins + b];
+            cnt[w * nbins + b] = p;
+            p += c;
+        }
+    }
+}
+
+__host__ __device__ constexpr size_t coarse_smem(int nc) { return (size_t)2 * kCT * 8 + ((size_t)(kPW + 3) * nc) * 4; }
+__host__ __device__ constexpr size_t fine_smem(int F) { return (size_t)kFT * 8 + ((size_t)(kPW + 3) * F) * 4; }
+
+__global__ void __launch_bounds__(kPT) csr_coarse_part(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
+                                                        int64_t m, int64_t n, int64_t rb, int64_t re, int cs, int nc,
+                                                        const int64_t *__restrict__ bstart, int2 *__restrict__ out) {
+    extern __shared__ __align__(16) unsigned char cp_raw[];
+    int2 *stage = reinterpret_cast<int2 *>(cp_raw);              // 2 kCT entries in coarse-bucket order
+    unsigned *cnt = reinterpret_cast<unsigned *>(stage + 2 * kCT);   // [kPW][nc] warp-private counters
+    unsigned *ls = cnt + kPW * nc, *tot = ls + nc, *gcur = tot + nc;  // tile run starts / lengths, region cursors
+    __shared__ unsigned wsum[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned *my = cnt + wid * nc;
+    const int cmask = (1 << cs) - 1;
+    int64_t e0, e1;
+    cta_range(m, e0, e1);
+    for (int b = threadIdx.x; b < nc; b += blockDim.x) gcur[b] = (unsigned)bstart[(int64_t)b * gridDim.x + blockIdx.x];
+    for (int64_t t0 = e0; t0 < e1; t0 += kCT) {
+        const int64_t w0 = min(e1, t0 + (int64_t)wid * (kCT / kPW)), w1 = min(e1, w0 + kCT / kPW);
+        for (int b = lane; b < nc; b += 32) my[b] = 0u;
+        __syncwarp();
+        int32_t lu[kCT / kPT], lv[kCT / kPT];   // local rows (or -1: no entry for this orientation)
+        int32_t us[kCT / kPT], vs[kCT / kPT];
+#pragma unroll
+        for (int k = 0; k < kCT / kPT; ++k) {
+            const int64_t e = w0 + lane + 32 * k;
+            us[k] = e < w1 ? __ldg(src + e) : -1;
+            vs[k] = e < w1 ? __ldg(dst + e) : -1;
+        }
+#pragma unroll
+        for (int k = 0; k < kCT / kPT; ++k) {
+            const int32_t u = us[k], v = vs[k];
+            const bool valid = u >= 0 && v >= 0 && u < n && v < n && u != v;
+            lu[k] = (valid && u >= rb && u < re) ? static_cast<int32_t>(u - rb) : -1;
+            lv[k] = (valid && v >= rb && v < re) ? static_cast<int32_t>(v - rb) : -1;
+            if (lu[k] >= 0) atomicAdd(&my[lu[k] >> cs], 1u);
+            if (lv[k] >= 0) atomicAdd(&my[lv[k] >> cs], 1u);
+        }
+        __syncthreads();
+        bins_scan(cnt, nc, ls, tot, wsum);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kCT / kPT; ++k) {
+            if (lu[k] >= 0) stage[atomicAdd(&my[lu[k] >> cs], 1u)] = make_int2(lu[k], vs[k]);
+            if (lv[k] >= 0) stage[atomicAdd(&my[lv[k] >> cs], 1u)] = make_int2(lv[k], us[k]);
+        }
+        __syncthreads();
+        const unsigned ntile = ls[nc - 1] + tot[nc - 1];
+        for (unsigned i = threadIdx.x; i < ntile; i += blockDim.x) {
+            const int2 e = stage[i];
+            const int b = e.x >> cs;
+            out[gcur[b] + (i - ls[b])] = make_int2(e.x & cmask, e.y);
+        }
+        __syncthreads();
+        for (int b = threadIdx.x; b < nc; b += blockDim.x) gcur[b] += tot[b];
+    }
+}
+
+#ifndef RG_FINE_SLOTS
+#define RG_FINE_SLOTS 8
+#endif
+constexpr int kFineSlots = RG_FINE_SLOTS;   // CTAs per coarse bucket in level 2 (blockIdx.x), tiles dealt round robin
+
+// Level 2a: fine bucket sizes. CTA (j, c) counts the tiles j, j + J, ... of coarse bucket c into its warp-private
+// counters and adds the CTA totals to fcnt[c * F + f] (one global atomic per fine bucket and CTA).
+__global__ void __launch_bounds__(kPT) csr_fine_count(const int2 *__restrict__ in, const int64_t *__restrict__ cstart,
+                                                       int pgrid, int shift, int fbits, int nb,
+                                                       int32_t *__restrict__ fcnt) {
+    __shared__ unsigned cnt[kPW][kMaxFine];
+    const int F = 1 << fbits, c = blockIdx.y;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t cb = cstart[(int64_t)c * pgrid], ce = cstart[(int64_t)(c + 1) * pgrid];
+    for (int f = lane; f < F; f += 32) cnt[wid][f] = 0u;
+    __syncwarp();
+    constexpr int kPer = kFT / kPT;
+    for (int64_t t0 = cb + (int64_t)blockIdx.x * kFT; t0 < ce; t0 += (int64_t)gridDim.x * kFT) {
+        const int64_t t1 = min(ce, t0 + kFT);
+        int2 p[kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int64_t e = t0 + threadIdx.x + (int64_t)k * kPT;
+            p[k] = e < t1 ? __ldg(in + e) : make_int2(-1, 0);
+        }
+#pragma unroll
+        for (int k = 0; k < kPer; ++k)
+            if (p[k].x >= 0) atomicAdd(&cnt[wid][p[k].x >> shift], 1u);
+    }
+    __syncthreads();
+    for (int f = threadIdx.x; f < F; f += blockDim.x) {
+        unsigned t = 0u;
+        for (int w = 0; w < kPW; ++w) t += cnt[w][f];
+        const int64_t gf = (int64_t)c * F + f;
+        if (t && gf < nb) atomicAdd(&fcnt[gf], (int32_t)t);
+    }
+}
+
+// Level 2b: CTA (j, c) splits the tiles j, j + J, ... of coarse bucket c: per tile warp-private counts, a scan over
+// the F fine buckets, one global claim per fine bucket on its cursor, ranks into the stage, runs copied out.
+template <bool PACKED>
+__global__ void __launch_bounds__(kPT) csr_fine_part(const int2 *__restrict__ in, const int64_t *__restrict__ cstart,
+                                                      int pgrid, int shift, int fbits, int vbits,
+                                                      unsigned long long *__restrict__ fcur,
+                                                      typename Entry<PACKED>::T *__restrict__ out) {
+    using E = Entry<PACKED>;
+    extern __shared__ __align__(16) unsigned char fp_raw[];
+    const int F = 1 << fbits, fmask = (1 << shift) - 1, c = blockIdx.y;
+    int2 *stage = reinterpret_cast<int2 *>(fp_raw);               // kFT entries in fine-bucket order
+    unsigned *cnt = reinterpret_cast<unsigned *>(stage + kFT);    // [kPW][F]
+    unsigned *ls = cnt + kPW * F, *tot = ls + F, *gcur = tot + F;
+    __shared__ unsigned wsum[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned *my = cnt + wid * F;
+    constexpr int kPer = kFT / kPT;
+    const int64_t cb = cstart[(int64_t)c * pgrid], ce = cstart[(int64_t)(c + 1) * pgrid];
+    for (int64_t t0 = cb + (int64_t)blockIdx.x * kFT; t0 < ce; t0 += (int64_t)gridDim.x * kFT) {
+        const int64_t t1 = min(ce, t0 + kFT);
+        for (int f = lane; f < F; f += 32) my[f] = 0u;
+        __syncwarp();
+        int2 p[kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int64_t e = t0 + wid * (kFT / kPW) + lane + 32 * k;
+            p[k] = e < t1 ? __ldg(in + e) : make_int2(-1, 0);
+            if (p[k].x >= 0) atomicAdd(&my[p[k].x >> shift], 1u);
+        }
+        __syncthreads();
+        bins_scan(cnt, F, ls, tot, wsum);
+        for (int f = threadIdx.x; f < F; f += blockDim.x)
+            if (tot[f]) gcur[f] = (unsigned)atomicAdd(&fcur[(int64_t)c * F + f], (unsigned long long)tot[f]);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kPer; ++k)
+            if (p[k].x >= 0) stage[atomicAdd(&my[p[k].x >> shift], 1u)] = p[k];
+        __syncthreads();
+        const unsigned ntile = static_cast<unsigned>(t1 - t0);
+        for (unsigned i = threadIdx.x; i < ntile; i += blockDim.x) {
+            const int2 e = stage[i];
+            const int f = e.x >> shift;
+            out[gcur[f] + (i - ls[f])] = E::make(e.x & fmask, e.y, vbits);
+        }
+        __syncthreads();
+    }
+}
+
 // Register bitonic sort of up to 32*E values per warp: element e of lane l has index e*32 + l; stages with
 // j >= 32 swap inside a lane, the others exchange by shuffle. Then dedup and write the unique prefix.
 template <int E>
@@ -965,6 +1172,119 @@ raftgp_status degrees_finalize(raftgp_graph g) {
     return RAFTGP_OK;
 }
 
+// Two-level partition + bucket sort (see csr_coarse_part / csr_fine_part): bucket count by COARSE bucket ->
+// scan -> level 1 -> level 2 (skipped when one coarse bucket is one fine bucket) -> csr_bucket_sort on the fine
+// buckets -> warp-sort fallback for rows longer than a shared-memory window. Leaves raw_ptr / col_raw / deg as
+// the one-level path does; *fb_rows / *fb_count are allocated here and freed by the caller.
+raftgp_status csr_partition_two_level(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src, const int32_t *dst,
+                                      int64_t rb, int64_t re, int shift, int fbits, int nb, int vbits, int64_t cap,
+                                      int64_t *raw_ptr, int32_t *col_raw, int32_t *deg, int *err, int64_t **fb_rows_out,
+                                      int32_t **fb_count_out) {
+    cudaStream_t st = ctx->stream;
+    const int64_t nl = re - rb;
+    const int cs = shift + fbits;
+    const int nc = static_cast<int>(ceil_div(nl, (int64_t)1 << cs));
+    const bool packed = fbits > 0 && shift + vbits <= 32;
+    // level-1 CTAs (2 per SM) and the count pass share the raw-pair ranges
+    const int pgrid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 32768), 2 * (int64_t)ctx->sm_count)));
+    int2 *p1 = nullptr;
+    void *p2 = nullptr;
+    int32_t *bcnt = nullptr;
+    int64_t *bstart = nullptr, *fst = nullptr, *fb_rows = nullptr;
+    int32_t *fb_count = nullptr;
+    unsigned int *bnext = nullptr;
+    RG_TRY(dalloc_t(ctx, &bnext, 1));
+    RG_TRY(dzero(ctx, bnext, sizeof(unsigned int), st));
+    RG_TRY(dalloc_t(ctx, &bcnt, (size_t)nc * pgrid));
+    RG_TRY(dalloc_t(ctx, &bstart, (size_t)nc * pgrid + 1));
+    RG_TRY(dalloc_t(ctx, &p1, (size_t)std::max<int64_t>(cap, 1)));
+    int32_t *fcnt = nullptr;
+    unsigned long long *fcur = nullptr;
+    if (fbits > 0) {
+        RG_TRY(dalloc(ctx, &p2, (size_t)std::max<int64_t>(cap, 1) * (packed ? 4 : 8)));
+        RG_TRY(dalloc_t(ctx, &fst, (size_t)nb + 1));
+        RG_TRY(dalloc_t(ctx, &fcnt, (size_t)nb));
+        RG_TRY(dalloc_t(ctx, &fcur, (size_t)nb));
+        RG_TRY(dzero(ctx, fcnt, sizeof(int32_t) * nb, st));
+    }
+    RG_TRY(dalloc_t(ctx, &fb_rows, (size_t)nl));
+    RG_TRY(dalloc_t(ctx, &fb_count, 1));
+    RG_TRY(dzero(ctx, fb_count, sizeof(int32_t), st));
+    *fb_rows_out = fb_rows;
+    *fb_count_out = fb_count;
+    const size_t bsmem = (size_t)(kBucketCap + 3 * kMaxBucketRows + 1) * 4;
+    const size_t cpsmem = coarse_smem(nc), fpsmem = fine_smem(1 << fbits);
+    static const char attrs_key = 0;
+    RG_TRY(per_device(ctx->device, &attrs_key, nullptr, [&](int *) -> raftgp_status {
+        RG_CUDA(cudaFuncSetAttribute(csr_bucket_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets32 * 4));
+        RG_CUDA(cudaFuncSetAttribute(csr_coarse_part, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coarse_smem(kMaxCoarse)));
+        RG_CUDA(cudaFuncSetAttribute(csr_fine_part<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fine_smem(kMaxFine)));
+        RG_CUDA(cudaFuncSetAttribute(csr_fine_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 0));
+        RG_CUDA(cudaFuncSetAttribute(csr_fine_part<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fine_smem(kMaxFine)));
+        RG_CUDA(cudaFuncSetAttribute(csr_bucket_sort<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
+        RG_CUDA(cudaFuncSetAttribute(csr_bucket_sort<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
+        return RAFTGP_OK;
+    }));
+    {
+        LaunchScope L(ctx, K_CSR_COUNT);
+        csr_bucket_count<<<pgrid, 1024, (size_t)nc * 4, st>>>(src, dst, m, n, rb, re, cs, nc, bcnt, err);
+    }
+    RG_CHECK_LAUNCH(ctx);
+    RG_TRY(scan_i32_to_i64(ctx, bcnt, bstart, (int64_t)nc * pgrid));
+    if (m > 0) {
+        LaunchScope L(ctx, K_CSR_PARTITION);
+        csr_coarse_part<<<pgrid, kPT, cpsmem, st>>>(src, dst, m, n, rb, re, cs, nc, bstart, p1);
+    }
+    RG_CHECK_LAUNCH(ctx);
+    if (fbits > 0) {
+        const dim3 fgrid(kFineSlots, nc);
+        {
+            LaunchScope L(ctx, K_CSR_FINE);
+            csr_fine_count<<<fgrid, kPT, 0, st>>>(p1, bstart, pgrid, shift, fbits, nb, fcnt);
+        }
+        RG_CHECK_LAUNCH(ctx);
+        RG_TRY(scan_i32_to_i64(ctx, fcnt, fst, nb));
+        LaunchScope L(ctx, K_CSR_FINE);
+        csr_bucket_cursor<<<(nb + 255) / 256, 256, 0, st>>>(fst, 1, nb, fcur);
+        if (packed)
+            csr_fine_part<true><<<fgrid, kPT, fpsmem, st>>>(p1, bstart, pgrid, shift, fbits, vbits, fcur,
+                                                             static_cast<uint32_t *>(p2));
+        else
+            csr_fine_part<false><<<fgrid, kPT, fpsmem, st>>>(p1, bstart, pgrid, shift, fbits, vbits, fcur,
+                                                              static_cast<int2 *>(p2));
+    }
+    RG_CHECK_LAUNCH(ctx);
+    static const int bcap = [] {   // RAFTGP_BUCKET_CAP: smaller shared-memory windows (tests)
+        const char *e = getenv("RAFTGP_BUCKET_CAP");
+        return e ? std::max(256, std::min(kBucketCap, atoi(e))) : kBucketCap;
+    }();
+    {
+        LaunchScope L(ctx, K_CSR_BUCKET);
+        const int bgrid = std::min(nb, ctx->sm_count);
+        if (fbits == 0)
+            csr_bucket_sort<false><<<bgrid, 1024, bsmem, st>>>(p1, bstart, pgrid, raw_ptr, nl, shift, nb, vbits, col_raw,
+                                                               deg, fb_rows, fb_count, bnext, bcap);
+        else if (packed)
+            csr_bucket_sort<true><<<bgrid, 1024, bsmem, st>>>(static_cast<const uint32_t *>(p2), fst, 1, raw_ptr, nl,
+                                                              shift, nb, vbits, col_raw, deg, fb_rows, fb_count, bnext,
+                                                              bcap);
+        else
+            csr_bucket_sort<false><<<bgrid, 1024, bsmem, st>>>(static_cast<const int2 *>(p2), fst, 1, raw_ptr, nl,
+                                                               shift, nb, vbits, col_raw, deg, fb_rows, fb_count, bnext,
+                                                               bcap);
+    }
+    RG_CHECK_LAUNCH(ctx);
+    dfree(ctx, bcnt);
+    dfree(ctx, bstart);
+    dfree(ctx, bnext);
+    dfree(ctx, p1);
+    if (p2) dfree(ctx, p2);
+    if (fst) dfree(ctx, fst);
+    if (fcnt) dfree(ctx, fcnt);
+    if (fcur) dfree(ctx, fcur);
+    return RAFTGP_OK;
+}
+
 raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src, const int32_t *dst, int64_t rb,
                         int64_t re, raftgp_graph g) {
     cudaStream_t st = ctx->stream;
@@ -992,7 +1312,13 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
     // 32-bit partition cursors when every raw entry position fits: twice the buckets in the same shared memory,
     // so huge graphs (C5) get buckets half as large; then buckets grow while a typical one still fits a window
     const bool b32 = cap < ((int64_t)1 << 32);
-    const int kMaxB = b32 ? kMaxBuckets32 : kMaxBuckets;
+    static const bool two_level_env = [] {   // RAFTGP_CSR_TWO_LEVEL=0: the one-level partition (A/B runs, tests)
+        const char *e = getenv("RAFTGP_CSR_TWO_LEVEL");
+        return !e || atoi(e) != 0;
+    }();
+    // two-level partition: needs 32-bit positions and at most kMaxCoarse x kMaxFine buckets of 512 rows
+    const bool two_level = two_level_env && b32 && nl > 0 && ceil_div(nl, (int64_t)512) <= (int64_t)kMaxCoarse * kMaxFine;
+    const int kMaxB = two_level ? INT_MAX : b32 ? kMaxBuckets32 : kMaxBuckets;
     int shift = 0;
     while (shift < 31 && ceil_div(nl, (int64_t)1 << shift) > kMaxB) ++shift;
     while (nl > 0 && shift < 12 && (cap / nl + 1) * ((int64_t)2 << shift) <= kBucketCap / 2 &&
@@ -1015,6 +1341,21 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
         const int nb = static_cast<int>(ceil_div(nl, (int64_t)1 << shift));
         int vbits = 1;
         while (vbits < 31 && ((int64_t)1 << vbits) < n) ++vbits;
+        // two-level: fine buckets = the bucket sort's buckets (2^shift rows), coarse = 2^fbits fine buckets
+        static const int64_t max_coarse = [] {   // RAFTGP_CSR_COARSE: fewer coarse buckets (tests force level 2)
+            const char *e = getenv("RAFTGP_CSR_COARSE");
+            return e ? std::max<int64_t>(1, std::min<int64_t>(kMaxCoarse, atoll(e))) : (int64_t)kMaxCoarse;
+        }();
+        int fbits = 0;
+        if (two_level)
+            while (fbits < 8 && ceil_div((int64_t)nb, (int64_t)1 << fbits) > max_coarse) ++fbits;
+        const bool use2 = two_level && ceil_div((int64_t)nb, (int64_t)1 << fbits) <= max_coarse;
+        if (use2) {
+            RG_TRY(csr_partition_two_level(ctx, n, m, src, dst, rb, re, shift, fbits, nb, vbits, cap, raw_ptr, col_raw,
+                                           g->deg_local, err, &fb_rows, &fb_count));
+            LaunchScope L(ctx, K_CSR_SORT_WARP);
+            csr_sort_warp<<<rgrid, 256, 0, st>>>(nl, fb_rows, fb_count, raw_ptr, col_raw, g->deg_local, big_rows, big_count);
+        } else {
         const bool packed = shift + vbits <= 32;
         const int pgrid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 65536), ctx->sm_count)));
         void *pairs = nullptr;
@@ -1099,6 +1440,7 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
         dfree(ctx, bcur);
         dfree(ctx, bnext);
         dfree(ctx, pairs);
+        }
     } else {
         if (m > 0) {
             LaunchScope L(ctx, K_CSR_SCATTER);

@@ -48,6 +48,7 @@ enum KernelId : int {
     K_STREAM,
     K_EXCHANGE,     // NCCL collectives of the row-partitioned path (barrier, all-gathers; not counted as our launches)
     K_PUSH_COPY,    // deferred push of a finished operand block into the peers' copies (dist.cu)
+    K_CSR_FINE,     // second level of the two-level CSR partition (csr.cu)
     K_NUM
 };
 extern const char *const kKernelNames[K_NUM];

@@ -130,7 +130,10 @@ cases = [synth.generate('C2', 3, n=30000), synth.generate('C1', 1)]
 rng = np.random.default_rng(3)
 hub_src = np.concatenate([np.zeros(5000, np.int32), rng.integers(0, 20000, 40000).astype(np.int32)])
 hub_dst = np.concatenate([rng.integers(1, 20000, 5000).astype(np.int32), rng.integers(0, 20000, 40000).astype(np.int32)])
-for n, src, dst in [(c.n, c.src, c.dst) for c in cases] + [(20000, hub_src, hub_dst)]:
+empty = np.zeros(0, np.int32)
+ragged = rng.integers(0, 777, (2, 3000)).astype(np.int32)
+for n, src, dst in [(c.n, c.src, c.dst) for c in cases] + [(20000, hub_src, hub_dst), (5000, empty, empty),
+                                                           (777, ragged[0], ragged[1])]:
     g = rg.raftgp_build_csr(ctx, n, torch.from_numpy(src), torch.from_numpy(dst))
     rp, col, deg = g.export()
     ref = oracle.build_csr(n, src, dst)
@@ -139,15 +142,21 @@ print('ok')
 """
 
 
-@pytest.mark.parametrize("cap", ["300", "2048"])
-def test_bucket_windows(rg, cap):
+@pytest.mark.parametrize("env", [
+    {"RAFTGP_BUCKET_CAP": "300"}, {"RAFTGP_BUCKET_CAP": "2048"},
+    # level 2 of the two-level partition on small graphs (at most 2 / 3 coarse buckets), alone and with windows
+    {"RAFTGP_CSR_COARSE": "2"}, {"RAFTGP_CSR_COARSE": "3", "RAFTGP_BUCKET_CAP": "300"},
+    # the one-level partition (shared-memory atomics), kept for A/B runs
+    {"RAFTGP_CSR_TWO_LEVEL": "0"}, {"RAFTGP_CSR_TWO_LEVEL": "0", "RAFTGP_BUCKET_CAP": "2048"}])
+def test_bucket_windows(rg, env):
     """Buckets larger than the shared-memory window (RAFTGP_BUCKET_CAP shrinks it) are sorted window by
-    window; rows longer than a window go to the fallback kernels. The CSR must stay bit-exact."""
+    window; rows longer than a window go to the fallback kernels; both partition paths and both levels of
+    the two-level one. The CSR must stay bit-exact."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", _WINDOW_SCRIPT], cwd=root, env=dict(os.environ, RAFTGP_BUCKET_CAP=cap),
+    r = subprocess.run([sys.executable, "-c", _WINDOW_SCRIPT], cwd=root, env=dict(os.environ, **env),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
