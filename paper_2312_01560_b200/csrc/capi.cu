@@ -253,6 +253,11 @@ static void ctx_teardown(raftgp_ctx ctx) {
     release_cache(ctx);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->pool) cudaMemPoolDestroy(ctx->pool);   // blocks still live (caller never freed them) are released too
+    if (ctx->hip) {
+        cudaStreamSynchronize(ctx->hip);
+        cudaStreamDestroy(ctx->hip);
+        ctx->hip = nullptr;
+    }
     if (ctx->side) {
         cudaStreamSynchronize(ctx->side);
         cudaStreamDestroy(ctx->side);
@@ -1100,16 +1105,35 @@ static raftgp_status build_embed_partitioned(raftgp_ctx ctx, int32_t P, bool loo
 // raftgp_build_csr + raftgp_embed_multi in one call. Theta' = Theta W^(1) depends only on the seed, so it is
 // generated on a side stream (tensor cores / ALUs) while the CSR build (atomics / HBM) runs on the context
 // stream; the results are those of the two separate calls.
-// CTAs of the Theta' kernel while it overlaps the CSR build (RAFTGP_OVERLAP_CTAS; default measured)
-static int build_overlap_ctas(raftgp_ctx ctx) {
+// How Theta' overlaps the CSR build (RAFTGP_OVERLAP_MODE):
+//   prio  (default): the CSR build runs on a high-priority library stream, Theta' on the (default-priority) side stream
+//                    as many short CTAs (16 tiles each): the block scheduler gives every SM that frees up to the CSR
+//                    kernels first, and Theta' fills the gaps (host read-backs, small kernels, kernel tails);
+//   split:           Theta' as persistent CTAs on RAFTGP_OVERLAP_CTAS SMs (default half), the CSR build beside it;
+//   serial:          Theta' on every SM, then the CSR build (also RAFTGP_BUILD_OVERLAP=0).
+enum class OverlapMode { prio, split, serial };
+static OverlapMode overlap_mode() {
+    static const OverlapMode m = [] {
+        const char *b = getenv("RAFTGP_BUILD_OVERLAP");
+        if (b && b[0] == '0') return OverlapMode::serial;
+        const char *e = getenv("RAFTGP_OVERLAP_MODE");
+        if (e && !strcmp(e, "split")) return OverlapMode::split;
+        if (e && !strcmp(e, "serial")) return OverlapMode::serial;
+        return OverlapMode::prio;
+    }();
+    return m;
+}
+static int build_overlap_ctas(raftgp_ctx ctx, int64_t n) {
     static const int env = [] {
         const char *e = getenv("RAFTGP_OVERLAP_CTAS");
         return e ? atoi(e) : -1;
     }();
     if (env >= 0) return env;
-    // half the SMs: C4 step 72.5 ms vs 73.9 with every SM (the CSR kernels then queue behind the 1-CTA-per-SM
-    // sketch) and 74.2 serial; 112 / 96 / 48 / 32 CTAs: 74.1 / 74.6 / 73.9 / 76.6 ms (profiles/r02/overlap_sweep.txt)
-    return std::max(1, ctx->sm_count / 2);
+    switch (overlap_mode()) {
+        case OverlapMode::prio: return (int)std::max<int64_t>(ctx->sm_count, ceil_div(n, (int64_t)128 * 16));
+        case OverlapMode::split: return std::max(1, ctx->sm_count / 2);
+        default: return ctx->sm_count;
+    }
 }
 
 raftgp_status raftgp_build_embed(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src, const int32_t *dst,
@@ -1142,13 +1166,10 @@ raftgp_status raftgp_build_embed(raftgp_ctx ctx, int64_t n, int64_t m, const int
         if (st == RAFTGP_OK) {
             RG_CUDA(cudaEventRecord(ev_fork, ctx->stream));
             RG_CUDA(cudaStreamWaitEvent(ctx->side, ev_fork, 0));
-            static const bool serial = [] {   // RAFTGP_BUILD_OVERLAP=0: Theta' before the CSR build, same stream
-                const char *e = getenv("RAFTGP_BUILD_OVERLAP");
-                return e && e[0] == '0';
-            }();
+            const bool serial = overlap_mode() == OverlapMode::serial;
             cudaStream_t main = ctx->stream;
             if (!serial) ctx->stream = ctx->side;   // the sketch kernels enqueue on the side stream
-            ctx->sketch_ctas = build_overlap_ctas(ctx);   // leave SMs to the CSR build that runs beside it
+            ctx->sketch_ctas = build_overlap_ctas(ctx, n);
             st = sketch_fill(ctx, seed, 1u, 0, r, l1, r, W1);
             if (st == RAFTGP_OK) st = sketch_w_any(ctx, seed, n, r, W1, l1, thw);
             ctx->sketch_ctas = 0;
@@ -1157,7 +1178,26 @@ raftgp_status raftgp_build_embed(raftgp_ctx ctx, int64_t n, int64_t m, const int
         }
     }
     raftgp_graph g = nullptr;
-    if (st == RAFTGP_OK) st = raftgp_build_csr(ctx, n, m, src, dst, 0, n, flags, &g);
+    if (st == RAFTGP_OK && overlap && overlap_mode() == OverlapMode::prio) {
+        // the CSR build on the high-priority stream, forked from and joined back into the caller's stream
+        if (!ctx->hip) {
+            int lo = 0, hi = 0;
+            RG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            RG_CUDA(cudaStreamCreateWithPriority(&ctx->hip, cudaStreamNonBlocking, hi));
+        }
+        cudaEvent_t ev_b = nullptr;
+        RG_CUDA(cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming));
+        RG_CUDA(cudaStreamWaitEvent(ctx->hip, ev_fork, 0));
+        cudaStream_t main = ctx->stream;
+        ctx->stream = ctx->hip;
+        st = raftgp_build_csr(ctx, n, m, src, dst, 0, n, flags, &g);
+        ctx->stream = main;
+        cudaEventRecord(ev_b, ctx->hip);
+        cudaStreamWaitEvent(main, ev_b, 0);
+        cudaEventDestroy(ev_b);
+    } else if (st == RAFTGP_OK) {
+        st = raftgp_build_csr(ctx, n, m, src, dst, 0, n, flags, &g);
+    }
     if (overlap && ev_join) cudaStreamWaitEvent(ctx->stream, ev_join, 0);   // Theta' ready (also on failure)
     if (st == RAFTGP_OK) {
         int where[3] = {-1, -1, -1};

@@ -80,6 +80,7 @@ struct raftgp_ctx_s {
     void *mbox_d = nullptr;
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;   // library-owned side stream (overlapped work inside one call)
+    cudaStream_t hip = nullptr;    // library-owned high-priority stream (the CSR build beside the Theta' kernel)
     cudaMemPool_t pool = nullptr;  // this context's own stream-ordered pool (release threshold: keep everything)
     bool own_stream = false;
     int sm_count = 148;

@@ -60,6 +60,7 @@ struct HopArgs {
                                // null: static grid-stride
     PushSpec push;             // push.nrep > 0: the T output (out/out2 when WN == 0, Tn/Tn2 when WN > 0) goes to
                                // the replicas at global rows instead of the local buffers
+    int claim = 8;             // row groups per dynamic claim (kClaim; 1 for short row lists: every warp gets work)
 };
 
 constexpr int kClaim = 8;      // row groups per dynamic claim
@@ -204,9 +205,9 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
     for (;; grp += a.ctr ? 1 : gw) {
         if (a.ctr && grp >= glim) {   // dynamic: the warp's next kClaim groups
             unsigned long long g0 = 0;
-            if (lane == 0) g0 = atomicAdd(a.ctr, (unsigned long long)kClaim);
+            if (lane == 0) g0 = atomicAdd(a.ctr, (unsigned long long)a.claim);
             grp = (int64_t)__shfl_sync(FULL, g0, 0);
-            glim = grp + kClaim;
+            glim = grp + a.claim;
         }
         if (grp >= ngroups) break;
         const int64_t row0 = grp * RB;
@@ -616,12 +617,19 @@ raftgp_status feature_hop_pre(raftgp_graph g, int variant_or_dual, int32_t l1, c
 
 // Row-list variants (NEXT-4 streaming): the same kernels over `count` local rows listed in `rows` (the
 // kernels' visiting-order hook; every row's arithmetic is unchanged, so the rows come out bit-identical).
+// Short lists (the changed rows' 1- and 2-hop closures, biased to hubs) are claimed one group at a time so every
+// warp gets rows: with 8-group claims a 1,000-row list kept ~34 warps busy, each summing ~32 long rows in turn.
+static int row_list_claim(raftgp_ctx ctx, int64_t count) {
+    return count < (int64_t)ctx->sm_count * 64 * 4 * 8 ? 1 : kClaim;
+}
+
 raftgp_status feature_hop_pre_rows(raftgp_graph g, int variant, int32_t l1, const float *theta_w, const double *gvec_w,
                                    float *T, const int32_t *rows, int64_t count) {
     if (count == 0) return RAFTGP_OK;
     HopArgs a = base_args(g, l1);
     a.nl = count;
     a.order = rows;
+    a.claim = row_list_claim(g->ctx, count);
     a.X = theta_w;
     a.gvec = gvec_w;
     a.out = T;
@@ -649,6 +657,7 @@ raftgp_status gcn_hop_rows(raftgp_graph g, const float *Tfull, int32_t w, float 
     HopArgs a = base_args(g, w);
     a.nl = count;
     a.order = rows;
+    a.claim = row_list_claim(g->ctx, count);
     a.X = Tfull;
     a.out = Zout;
     a.Wn = Wn;

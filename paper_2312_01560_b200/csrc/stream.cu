@@ -332,6 +332,16 @@ __global__ void new_degrees(int64_t n, const int32_t *__restrict__ odeg, const i
         ndeg[i] = odeg[i] + add[i];
 }
 
+// sum of the degrees of the frontier rows rows[f0 .. f0 + fc) (how many entries the next expansion would visit)
+__global__ void frontier_degsum(const int32_t *__restrict__ rows, int64_t f0, int64_t fc, const int32_t *__restrict__ deg,
+                                unsigned long long *__restrict__ out) {
+    unsigned long long s = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < fc; i += (int64_t)gridDim.x * blockDim.x)
+        s += (unsigned long long)deg[rows[f0 + i]];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
 // R_k in natural row order (for large sets: the hop then streams row_ptr / col_idx like a full pass)
 __global__ void level_flags(int64_t n, const int32_t *__restrict__ level, int k, int32_t *__restrict__ flag) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -534,7 +544,41 @@ raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const i
     if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &hop_rows, (size_t)std::max<int64_t>(1, n));
     if (rc == RAFTGP_OK) rc = dalloc_t(ctx, &nat_rows, (size_t)std::max<int64_t>(1, n));
     int64_t f0 = 0, fc = head[0];
+    // The last level: when the frontier's entries reach most of the graph (sum of its degrees >= 1.5 n: a random
+    // reach of 1 - e^-1.5 = 78 % or more), the last hop runs over every row with the full-graph kernel instead of
+    // expanding the closure and listing it (rows outside the closure have unchanged inputs and come out bit-identical;
+    // |R_{L+1}| is then reported as n). RAFTGP_STREAM_FULL_LAST=0 / 1 forces the listed / full last hop (tests).
+    static const int full_last_env = [] {
+        const char *e = getenv("RAFTGP_STREAM_FULL_LAST");
+        return e ? atoi(e) : -1;
+    }();
     for (int k = 1; k <= L + 1 && rc == RAFTGP_OK; ++k) {
+        if (k == L + 1 && fc > 0 && full_last_env != 0) {
+            bool full = full_last_env == 1;
+            if (!full) {
+                unsigned long long *ds = nullptr, hs = 0;
+                rc = dalloc_t(ctx, &ds, 1);
+                if (rc == RAFTGP_OK) rc = dzero(ctx, ds, sizeof(unsigned long long), st);
+                if (rc == RAFTGP_OK) {
+                    LaunchScope LS(ctx, K_STREAM);
+                    const unsigned eg = (unsigned)std::max<int64_t>(1, std::min<int64_t>(g256(fc), (int64_t)ctx->sm_count * 8));
+                    frontier_degsum<<<eg, 256, 0, st>>>(rows, f0, fc, ng->deg_local, ds);
+                }
+                if (rc == RAFTGP_OK) rc = dread(ctx, &hs, ds, sizeof(hs), st);
+                dfree(ctx, ds);
+                if (rc != RAFTGP_OK) break;
+                full = (double)hs >= 1.5 * (double)n;
+            }
+            if (full) {
+                counts[k] = n;
+                const auto &d = s->dims;
+                int32_t *own = ng->order;   // the old graph's visiting order, borrowed for this launch
+                if (!own && g->nl == ng->nl) ng->order = g->order;
+                rc = gcn_hop(ng, s->T[L], d[L], s->Z, nullptr, 0, nullptr, 0, nullptr);
+                ng->order = own;
+                break;
+            }
+        }
         if (fc > 0) {
             LaunchScope LS(ctx, K_STREAM);
             const unsigned eg = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(fc, 8), (int64_t)ctx->sm_count * 16));
@@ -590,7 +634,12 @@ raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const i
         delete ng;
         return rc;   // the stream keeps its previous graph; rows already recomputed for the new graph are stale
     }
-    // the stream now owns the merged graph
+    // the stream now owns the merged graph; it inherits the visiting order (any permutation gives bit-identical
+    // rows; this one spreads the old graph's heavy rows, which are still the heavy rows)
+    if (!ng->order && g->order && g->nl == ng->nl) {
+        ng->order = g->order;
+        g->order = nullptr;
+    }
     drop(*g);
     delete g;
     s->g = ng;

@@ -83,7 +83,10 @@ def test_stream_equals_full_recompute(rg, ctx, cfg, n, dims, batches):
                               cur_d[:-part_d.size] if part_d.size else cur_d)
         changed = go.deg != gb.deg
         assert st["changed"] == int(changed.sum())
-        assert st["affected"] == _closures(gr.n, cur_s, cur_d, changed, len(dims) - 1)
+        clo = _closures(gr.n, cur_s, cur_d, changed, len(dims) - 1)
+        # the last level is either the exact closure or n (the last hop ran over every row: its frontier's entries
+        # covered the graph 1.5 times or more)
+        assert st["affected"][:-1] == clo[:-1] and st["affected"][-1] in (clo[-1], gr.n), (st["affected"], clo)
         assert st["nnz"] == go.nnz
     Zo = oracle.gcn(go, list(dims), 5, oracle.project(go, "ncut", dims[0], 5))[-1]
     e = np.linalg.norm(Zs.cpu().numpy() - Zo) / np.linalg.norm(Zo)
@@ -116,3 +119,48 @@ def test_stream_errors(rg, ctx):
     with pytest.raises(rg.RaftGPError) as e:
         stream.add_edges(_t([0]), _t([gr.n + 5]))
     assert e.value.code == rg.RAFTGP_ERR_DATA
+
+
+_LAST_SCRIPT = r"""
+import sys, os, numpy as np, torch
+sys.path.insert(0, '.')
+import synth, scipy.sparse as sp
+from paper_2312_01560_b200 import raftgp as rg
+ctx = rg.Context(0)
+mode = os.environ['RAFTGP_STREAM_FULL_LAST']
+gr = synth.generate('C2', 4, n=20000)
+dims = (64, 64, 32)
+t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.int32))
+m = gr.src.size
+keep = np.arange(m - 30)
+g = rg.raftgp_build_csr(ctx, gr.n, t(gr.src[keep]), t(gr.dst[keep]))
+s = rg.Stream(g, dims, 3)
+st = s.add_edges(t(gr.src[m - 30:]), t(gr.dst[m - 30:]))
+g2 = rg.raftgp_build_csr(ctx, gr.n, t(gr.src), t(gr.dst))
+_, Z = rg.raftgp_embed_multi(g2, ['ncut'], dims, 3)
+assert torch.equal(s.embedding(), Z['ncut'])
+a = sp.coo_matrix((np.ones(m), (gr.src, gr.dst)), shape=(gr.n, gr.n)).tocsr()
+a = ((a + a.T) > 0).astype(np.int8); a.setdiag(0); a.eliminate_zeros()
+import oracle
+cur = oracle.build_csr(gr.n, gr.src, gr.dst).deg != oracle.build_csr(gr.n, gr.src[keep], gr.dst[keep]).deg
+sizes = []
+for _ in range(len(dims)):
+    cur = cur | (a @ cur.astype(np.int8) > 0)
+    sizes.append(int(cur.sum()))
+assert st['affected'][:-1] == sizes[:-1], (st, sizes)
+assert st['affected'][-1] == (gr.n if mode == '1' else sizes[-1]), (st, sizes)
+print('ok', st)
+"""
+
+
+@pytest.mark.parametrize("mode", ["0", "1"])
+def test_stream_last_hop_listed_or_full(rg, mode):
+    """The last GCN hop over the listed closure (RAFTGP_STREAM_FULL_LAST=0) or over every row with the full-graph
+    kernel (=1, the default when the frontier covers the graph): both bit-identical to the full recompute."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _LAST_SCRIPT], cwd=root,
+                       env=dict(os.environ, RAFTGP_STREAM_FULL_LAST=mode), capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
