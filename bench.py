@@ -828,7 +828,8 @@ def main():
         ctx.trim()
         torch.cuda.empty_cache()
         free_b, _ = torch.cuda.mem_get_info(dev)
-        lane_b = 2 * int(sum(rows * dims[-1] * 4 for _ in variants)) + 2 * 8 * m + 40 * m   # Z x2, edges x2, workspace
+        ws_b = 4 * rows * (dims[1] * (1 + len(variants)) + sum(dims[2:]) * len(variants)) + 56 * m   # Theta', T_k, CSR build
+        lane_b = 2 * int(sum(rows * dims[-1] * 4 for _ in variants)) + 2 * 8 * m + ws_b   # Z x2, edges x2, workspace
         lanes_fit = int(free_b // max(1, lane_b))
         if lanes_fit < args.e2e_lanes:
             args.e2e_lanes = max(1, min(args.e2e_lanes, lanes_fit))

@@ -1106,20 +1106,22 @@ static raftgp_status build_embed_partitioned(raftgp_ctx ctx, int32_t P, bool loo
 // generated on a side stream (tensor cores / ALUs) while the CSR build (atomics / HBM) runs on the context
 // stream; the results are those of the two separate calls.
 // How Theta' overlaps the CSR build (RAFTGP_OVERLAP_MODE):
-//   prio  (default): the CSR build runs on a high-priority library stream, Theta' on the (default-priority) side stream
+//   split (default): Theta' as persistent CTAs on RAFTGP_OVERLAP_CTAS SMs (default half), the CSR build beside it;
+//   prio:            the CSR build runs on a high-priority library stream, Theta' on the (default-priority) side stream
 //                    as many short CTAs (16 tiles each): the block scheduler gives every SM that frees up to the CSR
 //                    kernels first, and Theta' fills the gaps (host read-backs, small kernels, kernel tails);
-//   split:           Theta' as persistent CTAs on RAFTGP_OVERLAP_CTAS SMs (default half), the CSR build beside it;
 //   serial:          Theta' on every SM, then the CSR build (also RAFTGP_BUILD_OVERLAP=0).
+// All three measured within 0.4 ms of each other at C4 (72.8-73.2 ms) and C5 (780 ms): the two phases' work adds up
+// whatever the arrangement (profiles/r02/overlap_modes.txt).
 enum class OverlapMode { prio, split, serial };
 static OverlapMode overlap_mode() {
     static const OverlapMode m = [] {
         const char *b = getenv("RAFTGP_BUILD_OVERLAP");
         if (b && b[0] == '0') return OverlapMode::serial;
         const char *e = getenv("RAFTGP_OVERLAP_MODE");
-        if (e && !strcmp(e, "split")) return OverlapMode::split;
+        if (e && !strcmp(e, "prio")) return OverlapMode::prio;
         if (e && !strcmp(e, "serial")) return OverlapMode::serial;
-        return OverlapMode::prio;
+        return OverlapMode::split;
     }();
     return m;
 }

@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t 
     };
 
     const int64_t ntiles = (n + kTM - 1) / kTM;
+    const PhiloxKeys keys = philox_keys(seed);
     int64_t it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int64_t r0 = tile * kTM;
@@ -159,7 +160,7 @@ __global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t 
                 const int row = tid % kTM, qq = tid / kTM;
                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (r0 + row < n)
-                    v = spec_quad(seed, 0u, static_cast<uint64_t>(row0 + r0 + row),
+                    v = spec_quad(keys, 0u, static_cast<uint64_t>(row0 + r0 + row),
                                   static_cast<uint32_t>(q * (KQ / 4) + qq), sigma);
                 const float4 hi = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
                 const float4 lo = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);

@@ -198,3 +198,35 @@ def test_trim_returns_memory_to_the_device(rg):
     assert released > 0 and free1 < free0
     assert free2 >= free1 + 0.9 * released
     c.close()
+
+
+_OVERLAP_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, '.')
+import synth
+from paper_2312_01560_b200 import raftgp as rg
+ctx = rg.Context(0)
+gr = synth.generate('C2', 1, n=40000)
+Z, _ = rg.raftgp_build_embed(ctx, gr.n, torch.from_numpy(gr.src).cuda(), torch.from_numpy(gr.dst).cuda(),
+                             ['ncut', 'mod'], (64, 64, 32), 2)
+np.save(sys.argv[1], np.concatenate([Z['ncut'].cpu().numpy(), Z['mod'].cpu().numpy()], 1))
+print('ok')
+"""
+
+
+def test_build_embed_overlap_modes_identical(rg, tmp_path):
+    """raftgp_build_embed gives the same bits whether Theta' runs beside the CSR build on half the SMs (split, the
+    default), in short CTAs behind a high-priority CSR stream (prio), or before it (serial)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for mode in ("split", "prio", "serial"):
+        f = str(tmp_path / f"{mode}.npy")
+        r = subprocess.run([sys.executable, "-c", _OVERLAP_SCRIPT, f], cwd=root,
+                           env=dict(os.environ, RAFTGP_OVERLAP_MODE=mode), capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+        outs[mode] = np.load(f)
+    assert np.array_equal(outs["split"].view(np.uint32), outs["prio"].view(np.uint32))
+    assert np.array_equal(outs["split"].view(np.uint32), outs["serial"].view(np.uint32))
