@@ -20,7 +20,9 @@
 //             pushed to the peers by a copy kernel on the side stream while GCN hop 1 of NCut runs (overlap of the
 //             second variant's exchange with the first variant's compute);
 //   T_k       each GCN hop pushes its T_{k+1} rows (for two variants with a pairable last width, into one
-//             interleaved [T_a | T_b] operand, so the last hop is one 2d-wide gather).
+//             interleaved [T_a | T_b] operand, so the last hop is one 2d-wide gather). With the deferred T_1(Mod)
+//             push, NCut's last hop (its half of the pair operand) runs right after NCut's hop L-1, under that push,
+//             and Mod's half after Mod's hop L-1 (RAFTGP_DIST_SPLIT_LAST=0: one paired launch at the end).
 // Without peer mappings (IPC refused), every rank writes its own copy only and each barrier becomes an in-place
 // ncclAllGather of the produced operands (same values).
 //
@@ -72,6 +74,14 @@ int theta_mode() {   // 0: each rank generates its rows and pushes them (default
         return (e && std::string(e) == "regen") ? 1 : 0;
     }();
     return m;
+}
+
+bool split_last_mode() {   // RAFTGP_DIST_SPLIT_LAST=0: both variants' last hops as one paired launch at the end
+    static const bool d = [] {
+        const char *e = getenv("RAFTGP_DIST_SPLIT_LAST");
+        return !(e && e[0] == '0');
+    }();
+    return d;
 }
 
 bool deferred_push() {   // RAFTGP_DIST_DEFER=0: the dual feature hop pushes both variants at once
@@ -418,7 +428,11 @@ raftgp_status dist_build_embed(raftgp_ctx ctx, int P, bool loopback, int64_t n, 
     }
     if (st == RAFTGP_OK) st = barrier(produced);
     produced.clear();
-    // ---- a5: GCN hops 1 .. L-1 (each pushes T_{k+1}), then the last hop into Z
+    // ---- a5: GCN hops 1 .. L-1 (each pushes T_{k+1}), then the last hop into Z.
+    // split_last: NCut's last hop (its half of the interleaved pair operand) runs right after NCut's hop L-1 and a
+    // barrier, i.e. while Mod's T_1 push is still crossing NVLink; Mod's half follows its own hop L-1. Each half is the
+    // paired kernel with the other half's lanes idle, so every row comes out bit-identical to the paired hop.
+    const bool split_last = pair && defer && split_last_mode();
     for (int k = 1; k < L && st == RAFTGP_OK; ++k) {
         // NCut first: with the deferred push, Mod's hop 1 waits for its operand (joined below)
         std::vector<int> order;
@@ -447,6 +461,16 @@ raftgp_status dist_build_embed(raftgp_ctx ctx, int P, bool loopback, int64_t n, 
                 st = gcn_hop(G[p], own(s_in, p), dims[k], nullptr, Wk[k + 1], dims[k + 1], nullptr, 0, &ps);
             }
             produced.push_back(s_out);
+            if (split_last && k == L - 1 && v == vA && st == RAFTGP_OK) {   // NCut's half complete everywhere
+                st = barrier(produced);
+                produced.clear();
+                for (int p : mine) {
+                    if (st != RAFTGP_OK) break;
+                    const int64_t off = loopback ? rb_of(p) : 0;
+                    st = gcn_final_pair(G[p], own(sl.pair, p), dims[L], Z_dev[vA] + off * dims[L],
+                                        Z_dev[vB] + off * dims[L], 1);
+                }
+            }
         }
         if (st == RAFTGP_OK) st = barrier(produced);
         produced.clear();
@@ -455,7 +479,8 @@ raftgp_status dist_build_embed(raftgp_ctx ctx, int P, bool loopback, int64_t n, 
         if (st != RAFTGP_OK) break;
         const int64_t off = loopback ? rb_of(p) : 0;   // loopback: Z holds all n rows
         if (pair) {
-            st = gcn_final_pair(G[p], own(sl.pair, p), dims[L], Z_dev[vA] + off * dims[L], Z_dev[vB] + off * dims[L]);
+            st = gcn_final_pair(G[p], own(sl.pair, p), dims[L], Z_dev[vA] + off * dims[L], Z_dev[vB] + off * dims[L],
+                                split_last ? 2 : 0);
         }
         for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v) {
             if (pair && (v == vA || v == vB)) continue;

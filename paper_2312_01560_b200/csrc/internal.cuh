@@ -276,7 +276,7 @@ raftgp_status gcn_hop_rows(raftgp_graph g, const float *Tfull, int32_t w, float 
                            float *Tnext, const int32_t *rows, int64_t count);
 // last GCN hop of two variants over the interleaved operand [T_a | T_b] (n x 2d); d in {32, 64}
 bool gcn_pair_supported(int32_t d);
-raftgp_status gcn_final_pair(raftgp_graph g, const float *Tboth, int32_t d, float *Za, float *Zb);
+raftgp_status gcn_final_pair(raftgp_graph g, const float *Tboth, int32_t d, float *Za, float *Zb, int half = 0);
 // NEXT-2: tensor-core 3xTF32 GEMM on pre-split, pre-tiled operands (wide.cu)
 int gemm_nt(int N);
 int64_t gemm_pad_rows(int64_t M);

@@ -36,7 +36,10 @@ constexpr unsigned FULL = 0xffffffffu;
 // GCN2: the last GCN hop of two variants at once over an interleaved operand [T_a | T_b] (one 2d-wide
 // gather per neighbour instead of two d-wide ones); each half is tanh'd and l2-normalised on its own.
 enum Kind : int { KIND_NCUT = 0, KIND_MOD = 1, KIND_MOD_REDUCED = 2, KIND_GCN = 3, KIND_LOAD = 4, KIND_DUAL = 5,
-                  KIND_GCN2 = 6 };
+                  KIND_GCN2 = 6, KIND_GCN2H = 7 };
+// KIND_GCN2H: KIND_GCN2 restricted to one half of the interleaved operand (HopArgs::half = 1 or 2), a separate
+// instantiation so the paired kernel of the one-GPU step carries no half predicate
+__host__ __device__ constexpr bool is_pair_kind(int k) { return k == KIND_GCN2 || k == KIND_GCN2H; }
 
 struct HopArgs {
     int64_t nl, rb, n;
@@ -61,6 +64,8 @@ struct HopArgs {
     PushSpec push;             // push.nrep > 0: the T output (out/out2 when WN == 0, Tn/Tn2 when WN > 0) goes to
                                // the replicas at global rows instead of the local buffers
     int claim = 8;             // row groups per dynamic claim (kClaim; 1 for short row lists: every warp gets work)
+    int half = 0;              // KIND_GCN2H: 1 / 2 only the first / second half of [T_a | T_b] (the other
+                               // half's lanes load nothing; each half's arithmetic is unchanged)
 };
 
 constexpr int kClaim = 8;      // row groups per dynamic claim
@@ -93,7 +98,7 @@ enum Mode : int { M_SUM = 0, M_S = 1, M_SUM_D = 2, M_SUM_S = 3 };
 // `c0` is this row's first 32-entry col chunk, loaded by the caller one row ahead; later chunks are
 // prefetched one chunk ahead, so col latency overlaps the row gathers. (L2 eviction-priority hints for
 // high-degree rows were measured and made every hop slower; plain read-only loads are used.)
-template <int W, int U_REQ, int MODE>
+template <int W, int U_REQ, int MODE, bool HALF = false>
 __device__ __forceinline__ void gather_row(const HopArgs &a, int64_t beg, int64_t end, int32_t c0, int lane,
                                            float4 &acc, float4 &acc2) {
     constexpr int LPN = W / 4, NPW = 32 / LPN;
@@ -101,6 +106,8 @@ __device__ __forceinline__ void gather_row(const HopArgs &a, int64_t beg, int64_
     static_assert(NPW * U <= 32 && 32 % (NPW * U) == 0, "unroll must tile a 32-entry col chunk");
     const int sub = lane / LPN, cl = lane % LPN;
     const float4 *X4 = reinterpret_cast<const float4 *>(a.X);
+    // HALF (KIND_GCN2H): only the lanes of the selected half of the interleaved row load
+    const bool act = !HALF || ((cl < LPN / 2) == (a.half == 1));
     acc = make_float4(0.f, 0.f, 0.f, 0.f);
     acc2 = make_float4(0.f, 0.f, 0.f, 0.f);
 #if RG_PREFETCH
@@ -123,7 +130,7 @@ __device__ __forceinline__ void gather_row(const HopArgs &a, int64_t beg, int64_
             for (int u = 0; u < U; ++u) {
                 const int k = k0 + u * NPW + sub;
                 const int32_t j = __shfl_sync(FULL, myj, k);
-                v[u] = (k < cnt) ? ldg4(X4 + (int64_t)j * LPN + cl) : make_float4(0.f, 0.f, 0.f, 0.f);
+                v[u] = (k < cnt && act) ? ldg4(X4 + (int64_t)j * LPN + cl) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -238,9 +245,12 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
                     if (RG_PREFETCH) nc0 = (nbeg + lane < nend) ? __ldg(a.col + nbeg + lane) : 0;
                 }
                 float4 self = make_float4(0.f, 0.f, 0.f, 0.f);
-                if constexpr (KIND == KIND_GCN || KIND == KIND_GCN2)
+                if constexpr (KIND == KIND_GCN)
                     self = ldg4(reinterpret_cast<const float4 *>(a.X) + gi * LPN + cl);
-                gather_row<W, U, KindTraits<KIND>::MODE>(a, beg, end, c0, lane, acc, acc2);
+                if constexpr (KIND == KIND_GCN2) self = ldg4(reinterpret_cast<const float4 *>(a.X) + gi * LPN + cl);
+                if constexpr (KIND == KIND_GCN2H)
+                    if ((cl < LPN / 2) == (a.half == 1)) self = ldg4(reinterpret_cast<const float4 *>(a.X) + gi * LPN + cl);
+                gather_row<W, U, KindTraits<KIND>::MODE, KIND == KIND_GCN2H>(a, beg, end, c0, lane, acc, acc2);
                 beg = nbeg;
                 end = nend;
                 c0 = nc0;
@@ -270,7 +280,7 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
                     const float shi = __ldg(a.sh_all + gi);
                     y = make_float4(tanhf(shi * acc.x), tanhf(shi * acc.y), tanhf(shi * acc.z), tanhf(shi * acc.w));
                     float ss = y.x * y.x + y.y * y.y + y.z * y.z + y.w * y.w;
-                    constexpr int RL = KIND == KIND_GCN2 ? LPN / 2 : LPN;   // lanes of one normalised row
+                    constexpr int RL = is_pair_kind(KIND) ? LPN / 2 : LPN;   // lanes of one normalised row
 #pragma unroll
                     for (int o = 1; o < RL; o <<= 1) ss += __shfl_xor_sync(FULL, ss, o);
                     if (ss > 0.f) {
@@ -279,14 +289,14 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
                     }
                 }
             }
-            if constexpr (WN == 0 && KIND != KIND_GCN && KIND != KIND_GCN2 && KIND != KIND_LOAD) {
+            if constexpr (WN == 0 && KIND != KIND_GCN && !is_pair_kind(KIND) && KIND != KIND_LOAD) {
                 if (a.scale_sh) {
                     const float shi = __ldg(a.sh_all + gi);
                     y = make_float4(shi * y.x, shi * y.y, shi * y.z, shi * y.w);
                     y2 = make_float4(shi * y2.x, shi * y2.y, shi * y2.z, shi * y2.w);
                 }
             }
-            if constexpr (KIND == KIND_GCN2) {
+            if constexpr (is_pair_kind(KIND)) {
                 constexpr int HL = LPN / 2;
                 float *o = cl < HL ? a.out : a.out2;
                 if (sub == 0 && o != nullptr) reinterpret_cast<float4 *>(o)[row * HL + (cl % HL)] = y;
@@ -462,7 +472,7 @@ raftgp_status launch_fast(raftgp_ctx ctx, const HopArgs &a) {
     const int64_t groups = ceil_div(a.nl, RB);
     const int64_t want = ceil_div(groups, WPB);
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sm_count * blocks_per_sm)));
-    const int kid = (KIND == KIND_GCN || KIND == KIND_GCN2) ? K_GCN_HOP : (KIND == KIND_LOAD ? K_TRANSFORM : K_FEATURE_HOP);
+    const int kid = (KIND == KIND_GCN || is_pair_kind(KIND)) ? K_GCN_HOP : (KIND == KIND_LOAD ? K_TRANSFORM : K_FEATURE_HOP);
     HopArgs b = a;
     b.ctr = nullptr;
     static const bool dyn = [] {   // RAFTGP_HOP_DYN=0: static grid-stride groups
@@ -704,14 +714,17 @@ raftgp_status gcn_hop(raftgp_graph g, const float *Tfull, int32_t w, float *Zout
 
 bool gcn_pair_supported(int32_t d) { return d == 32 || d == 64; }
 
-raftgp_status gcn_final_pair(raftgp_graph g, const float *Tboth, int32_t d, float *Za, float *Zb) {
+raftgp_status gcn_final_pair(raftgp_graph g, const float *Tboth, int32_t d, float *Za, float *Zb, int half) {
     if (g->nl == 0) return RAFTGP_OK;
     HopArgs a = base_args(g, 2 * d);
     a.X = Tboth;
-    a.out = Za;
-    a.out2 = Zb;
+    a.out = half == 2 ? nullptr : Za;
+    a.out2 = half == 1 ? nullptr : Zb;
+    a.half = half;
     if (!(gcn_pair_supported(d) && aligned16(Tboth) && aligned16(Za) && aligned16(Zb)))
         return fail(RAFTGP_ERR_INTERNAL, "gcn_final_pair: unsupported width/alignment");
+    if (half != 0)
+        return d == 32 ? launch_fast<KIND_GCN2H, 64, 0>(g->ctx, a) : launch_fast<KIND_GCN2H, 128, 0>(g->ctx, a);
     return d == 32 ? launch_fast<KIND_GCN2, 64, 0>(g->ctx, a) : launch_fast<KIND_GCN2, 128, 0>(g->ctx, a);
 }
 

@@ -111,7 +111,8 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("env", [{"RAFTGP_DIST_THETA": "regen"}, {"RAFTGP_DIST_DEFER": "0"}])
+@pytest.mark.parametrize("env", [{"RAFTGP_DIST_THETA": "regen"}, {"RAFTGP_DIST_DEFER": "0"},
+                                 {"RAFTGP_DIST_SPLIT_LAST": "0"}])
 def test_loopback_schedule_switches(cuda_required, env):
     out = subprocess.run([sys.executable, "-c", _SWITCH.format(root=ROOT)], capture_output=True, text=True,
                          timeout=600, env={**os.environ, **env})
