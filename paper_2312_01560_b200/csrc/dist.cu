@@ -13,9 +13,9 @@
 //   Theta'    each rank generates its own rows (tcgen05) and pushes them, on a side stream, WHILE the CSR build
 //             runs (NVLink is otherwise idle then); with RAFTGP_DIST_THETA=regen every rank generates all rows;
 //   degrees   ncclAllGather of the local degree blocks (n int32);
-//   g         MOD's g = d^T Theta' over fixed global 2048-row chunks: each rank sums the chunks that START in its
+//   g         MOD's g = d^T Theta' over fixed global 512-row chunks: each rank sums the chunks that START in its
 //             rows (reading past its end in its full Theta' copy), the partials are broadcast, every rank adds
-//             all chunks in chunk order (identical to one GPU);
+//             all chunks in g_final's fixed order (identical to one GPU);
 //   T_1       the dual feature hop pushes T_1(NCut) to every copy; T_1(Mod) goes to this rank's copy only and is
 //             pushed to the peers by a copy kernel on the side stream while GCN hop 1 of NCut runs (overlap of the
 //             second variant's exchange with the first variant's compute);

@@ -7,7 +7,7 @@
 //
 // For the MOD variant the rank-1 term needs g = d^T Theta = sum_j d_j Theta_j (fp64). It is reduced
 // deterministically: fixed chunks of kGChunk global rows, each summed sequentially per column by one
-// thread (fp64), then the chunk partials summed in chunk order. The result depends only on (graph,
+// thread (fp64), then the chunk partials combined in a fixed order (g_final). The result depends only on (graph,
 // seed, r) — not on the launch configuration or on the number of ranks.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -23,7 +23,10 @@ namespace raftgp {
 
 namespace {
 
-constexpr int kGChunk = 2048;
+#ifndef RG_G_CHUNK
+#define RG_G_CHUNK 512
+#endif
+constexpr int kGChunk = RG_G_CHUNK;   // rows per g partial (512: 4x the blocks of round 2's 2048, same bytes)
 
 __global__ void __launch_bounds__(256) gauss_fill(uint64_t seed, uint32_t tag, int64_t row_begin, int64_t rows,
                                                   int32_t cols, float sigma, float *__restrict__ out, bool vec4) {
@@ -47,7 +50,8 @@ __global__ void __launch_bounds__(256) gauss_fill(uint64_t seed, uint32_t tag, i
     }
 }
 
-// partial[chunk][c] = sum_{j in chunk, sequential} d_j * theta[j][c]   (fp64)
+// partial[chunk][c] = sum_{j in chunk, sequential} d_j * theta[j][c]   (fp64); rows loaded 16 ahead so the fp64 add
+// chain, not the load latency, sets the pace
 __global__ void __launch_bounds__(128) g_partials(const float *__restrict__ theta, const int32_t *__restrict__ deg,
                                                   int64_t n, int32_t r, int64_t chunk0, double *__restrict__ partial) {
     const int64_t chunk = chunk0 + blockIdx.x;
@@ -55,26 +59,41 @@ __global__ void __launch_bounds__(128) g_partials(const float *__restrict__ thet
     // blockIdx.y picks a 128-column slice (wide operands); each (chunk, column) sum stays sequential in j
     for (int c = blockIdx.y * blockDim.x + threadIdx.x; c < r; c += gridDim.y * blockDim.x) {
         double acc = 0.0;
-        for (int64_t j = j0; j < j1; ++j) acc += static_cast<double>(deg[j]) * static_cast<double>(theta[j * r + c]);
+        int64_t j = j0;
+        for (; j + 16 <= j1; j += 16) {
+            float t[16];
+            int32_t d[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                t[u] = __ldg(theta + (j + u) * r + c);
+                d[u] = __ldg(deg + j + u);
+            }
+#pragma unroll
+            for (int u = 0; u < 16; ++u) acc += static_cast<double>(d[u]) * static_cast<double>(t[u]);
+        }
+        for (; j < j1; ++j) acc += static_cast<double>(deg[j]) * static_cast<double>(theta[j * r + c]);
         partial[chunk * r + c] = acc;
     }
 }
 
-// g[c] = sum over chunks in chunk order (sequential per column; operands loaded 8 ahead so the fp64 add chain,
-// not the load latency, sets the pace)
-__global__ void g_final(const double *__restrict__ partial, int64_t nchunks, int32_t r, double *__restrict__ g) {
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < r; c += gridDim.x * blockDim.x) {
+// g[c] = the chunk partials of column c combined in a FIXED order: block c, thread t sums the chunks t, t + 256, ...
+// in sequence, then a fixed shared-memory tree over the 256 threads (deterministic; every path uses this kernel)
+constexpr int kGFinalThreads = 256;
+__global__ void __launch_bounds__(kGFinalThreads) g_final(const double *__restrict__ partial, int64_t nchunks, int32_t r,
+                                                          double *__restrict__ g) {
+    __shared__ double red[kGFinalThreads];
+    for (int c = blockIdx.x; c < r; c += gridDim.x) {
         double acc = 0.0;
-        int64_t k = 0;
-        for (; k + 8 <= nchunks; k += 8) {
-            double v[8];
+        for (int64_t k = threadIdx.x; k < nchunks; k += kGFinalThreads) acc += __ldg(partial + k * r + c);
+        red[threadIdx.x] = acc;
+        __syncthreads();
 #pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = __ldg(partial + (k + j) * r + c);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) acc += v[j];
+        for (int o = kGFinalThreads / 2; o > 0; o >>= 1) {
+            if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+            __syncthreads();
         }
-        for (; k < nchunks; ++k) acc += partial[k * r + c];
-        g[c] = acc;
+        if (threadIdx.x == 0) g[c] = red[0];
+        __syncthreads();
     }
 }
 
@@ -255,7 +274,7 @@ raftgp_status g_final_chunks(raftgp_ctx ctx, const double *partial, int64_t nchu
     if (nchunks == 0) return dzero(ctx, g_out, sizeof(double) * r);
     {
         LaunchScope L(ctx, K_G_FINAL);
-        g_final<<<(unsigned)ceil_div(r, 32), 32, 0, ctx->stream>>>(partial, nchunks, r, g_out);
+        g_final<<<(unsigned)r, kGFinalThreads, 0, ctx->stream>>>(partial, nchunks, r, g_out);
     }
     RG_CHECK_LAUNCH(ctx);
     return RAFTGP_OK;
