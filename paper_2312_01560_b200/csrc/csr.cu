@@ -3,14 +3,15 @@
 // Eq. 6's propagation matrix).
 //
 // Build pipeline (all on the ctx stream; csr_build, the default path for every graph whose buckets fit):
-//   bucket count : one CTA per SM histograms its contiguous range of raw pairs into shared memory by BUCKET of
-//                  2^shift consecutive local rows (both orientations of every u != v pair whose row is local) and
-//                  writes per-(bucket, CTA) counts; ids outside [0, n) raise a device data-error flag.
-//   scan         : exclusive scan of the counts -> bucket starts.
-//   partition    : tiles of 16K pairs claimed round robin: shared-memory tile histogram, one global atomic per
-//                  (tile, bucket) on the bucket cursor, then the entries (row-in-bucket, neighbour) are written
-//                  into their bucket's slots (32-bit packed when log2(B) + id bits <= 32).
-//   bucket sort  : one CTA per bucket (persistent): counts its own rows, writes the raw row pointers, places the
+//   count        : CTA c (2 per SM) histograms its contiguous range of raw pairs into shared memory by COARSE bucket
+//                  (2^cs consecutive local rows, <= kMaxCoarse buckets; both orientations of every u != v pair whose row
+//                  is local) and writes per-(bucket, CTA) counts; ids outside [0, n) raise a device data-error flag.
+//   scan         : exclusive scan of the counts -> every CTA's private region of every coarse bucket.
+//   level 1      : csr_coarse_part, the same ranges: per tile, warp-private counts, a scan over the buckets, ranks into a
+//                  shared-memory stage in bucket order, runs copied out with coalesced stores into the CTA's regions.
+//   level 2      : csr_fine_count + scan + csr_fine_part split each coarse bucket into its fine buckets (2^shift rows,
+//                  the bucket sort's unit) the same staged way; entries 32-bit packed when log2(B) + id bits <= 32.
+//   bucket sort  : one CTA per fine bucket (persistent): counts its own rows, writes the raw row pointers, places the
 //                  entries into rows in shared memory, sorts each row (one warp in registers up to 128 entries,
 //                  groups of 4 warps by value sub-ranges beyond) and removes duplicates; the unique count is the
 //                  degree. Buckets larger than shared memory are processed window by window; single rows longer
@@ -21,8 +22,9 @@
 //                  dropped: the raw layout is then the CSR).
 //   order        : degree-aware visiting order of the rows for the hop kernels (order.cu; one read-back).
 //   degrees      : deg -> 2e, s, s^ and a degree histogram (whole-graph builds; one read-back).
-// Graphs whose rows cannot be bucketed (a bucket larger than kMaxBucketRows rows) take the older per-row path:
-// count (global atomics) -> scan -> scatter -> per-row warp / block sorts.
+// RAFTGP_CSR_TWO_LEVEL=0 (or > 2^32 raw entries) takes round 1's one-level partition instead (count by fine bucket,
+// csr_partition: shared-memory ranks straight into bucket fronts claimed per tile). Graphs whose rows cannot be
+// bucketed take the older per-row path: count (global atomics) -> scan -> scatter -> per-row warp / block sorts.
 // The result is canonical (sorted, unique), hence independent of atomic ordering: bit-exact.
 #include <cuda_runtime.h>
 #include <stdint.h>
