@@ -304,11 +304,16 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
                 if (WN == 0 && a.push.nrep > 0) {   // fused exchange: this row into every rank's copy of T
                     const int64_t grow = a.push.row0 + row;
                     const int64_t ld4 = a.push.ld > 0 ? a.push.ld / 4 : LPN;
-                    for (int r = 0; r < a.push.nrep; ++r)
-                        reinterpret_cast<float4 *>(a.push.rep[r])[grow * ld4 + cl] = y;
+                    // replica loops unrolled over kMaxPush with constant indices: the pointer arrays stay in the
+                    // parameter bank (a runtime index made the compiler copy them to local memory and spill)
+#pragma unroll
+                    for (int r = 0; r < kMaxPush; ++r)
+                        if (r < a.push.nrep) reinterpret_cast<float4 *>(a.push.rep[r])[grow * ld4 + cl] = y;
                     if constexpr (NV == 2) {
                         const int n2 = a.push.nrep2 > 0 ? a.push.nrep2 : a.push.nrep;
-                        for (int r = 0; r < n2; ++r) reinterpret_cast<float4 *>(a.push.rep2[r])[grow * ld4 + cl] = y2;
+#pragma unroll
+                        for (int r = 0; r < kMaxPush; ++r)
+                            if (r < n2) reinterpret_cast<float4 *>(a.push.rep2[r])[grow * ld4 + cl] = y2;
                     }
                 } else {
                     if (a.out != nullptr) reinterpret_cast<float4 *>(a.out)[row * LPN + cl] = y;
@@ -367,8 +372,10 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
                             const int64_t grow = a.push.row0 + row;
                             const int64_t pl4 = a.push.ld > 0 ? a.push.ld / 4 : OL;
                             const int nr = (v == 0 || a.push.nrep2 == 0) ? a.push.nrep : a.push.nrep2;
-                            for (int r = 0; r < nr; ++r)
-                                reinterpret_cast<float4 *>(v == 0 ? a.push.rep[r] : a.push.rep2[r])[grow * pl4 + oc] = t4;
+#pragma unroll
+                            for (int r = 0; r < kMaxPush; ++r)
+                                if (r < nr)
+                                    reinterpret_cast<float4 *>(v == 0 ? a.push.rep[r] : a.push.rep2[r])[grow * pl4 + oc] = t4;
                         } else {
                             float4 *T4 = reinterpret_cast<float4 *>(v == 0 ? a.Tn : a.Tn2);
                             const int64_t ld4 = a.tn_ld > 0 ? a.tn_ld / 4 : OL;
