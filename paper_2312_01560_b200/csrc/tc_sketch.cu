@@ -35,6 +35,9 @@ using namespace tc;
 #endif
 constexpr int kTM = 128;       // rows per tile (MMA M)
 constexpr int kKQ = 32;        // K columns per quarter (one of two A buffers)
+#ifndef RG_TC_DRAIN_SPREAD
+#define RG_TC_DRAIN_SPREAD 1
+#endif
 
 // Global rows row0 .. row0 + n - 1 of Theta' (Theta's generator row = the global row); each finished row is stored at
 // its global row into every one of the nout output copies (nout > 1: the row-partitioned path pushes its share of
@@ -121,27 +124,40 @@ __global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t 
     const uint32_t tmem_d = tmem_base_sh;
 
     // drain the accumulator of local tile `it` (global tile index `tile`) into Theta' (drain warps only)
-    auto drain = [&](int64_t it, int64_t tile) {
+    // drain of local tile `it` (global tile index `tile`) into Theta', spread over the next tile's quarters: at quarter
+    // q the drain warps store the 32-column chunks [q CPQ, (q + 1) CPQ) (RG_TC_DRAIN_SPREAD=0: all chunks at q = 0),
+    // so they never fall a whole accumulator behind the generating warps (the ring waits for every warp's arrival)
+    constexpr int NCH = L1 / 32 > 0 ? L1 / 32 : 1;                 // 32-column chunks of one accumulator
+    constexpr int CPQ = RG_TC_DRAIN_SPREAD ? (NCH + NQK - 1) / NQK : NCH;
+    auto drain = [&](int64_t it, int64_t tile, int q) {
         const int acc = (int)(it & 1);
-        mbar_wait(&accf[acc], (uint32_t)((it >> 1) & 1));
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int k0 = q * CPQ, k1 = min(NCH, k0 + CPQ);
+        if (k0 >= k1) return;
+        if (k0 == 0) {
+            mbar_wait(&accf[acc], (uint32_t)((it >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        }
         const int lq = warp & 3;
         const int64_t row = tile * kTM + lq * 32 + lane;
 #pragma unroll 1
-        for (int c0 = 0; c0 < L1; c0 += 32) {
+        for (int kc = k0; kc < k1; ++kc) {
+            const int c0 = kc * 32;
             float v[32];
             tmem_ld32(tmem_d + (static_cast<uint32_t>(lq * 32) << 16) + (uint32_t)(acc * NCOL + c0), v);
-            if (row < n) {
-                for (int q = 0; q < outs.nout; ++q) {
-                    float4 *o = reinterpret_cast<float4 *>(outs.out[q] + (row0 + row) * L1 + c0);
+            if (row < n && c0 < L1) {
+                for (int o = 0; o < outs.nout; ++o) {
+                    float4 *dst = reinterpret_cast<float4 *>(outs.out[o] + (row0 + row) * L1 + c0);
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                    for (int i = 0; i < 8; ++i)
+                        if (c0 + 4 * i < L1) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
                 }
             }
         }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&acce[acc]);
+        if (k1 == NCH) {   // the accumulator is free for tile it + 2
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acce[acc]);
+        }
     };
 
     const int64_t ntiles = (n + kTM - 1) / kTM;
@@ -196,10 +212,11 @@ __global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t 
                 }
                 __syncwarp();
             }
-            if (q == 0 && warp >= EPI0 && it >= 1) drain(it - 1, tile - gridDim.x);
+            if (warp >= EPI0 && it >= 1) drain(it - 1, tile - gridDim.x, q);
         }
     }
-    if (warp >= EPI0 && it >= 1) drain(it - 1, (int64_t)blockIdx.x + (it - 1) * gridDim.x);
+    if (warp >= EPI0 && it >= 1)
+        for (int q = 0; q < NQK; ++q) drain(it - 1, (int64_t)blockIdx.x + (it - 1) * gridDim.x, q);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0)
