@@ -7,12 +7,12 @@
 // mantissa bits cleared, lo = x - hi exactly): A B ~ A_hi B_hi + A_hi B_lo + A_lo B_hi, accumulated in fp32
 // in TMEM (error ~2^-20 relative, far inside the 1e-4 parity bar).
 //
-// Per CTA (1024 threads, one per SM): a persistent loop over 128-row tiles, each split into K-quarters of at most
-// 32 columns. Every thread generates one Philox quad (4 normals) per quarter and stores its hi / lo tf32 parts in
+// Per CTA (512 threads, one per SM): a persistent loop over 128-row tiles, each split into K-quarters of at most
+// 32 columns. Every thread generates two Philox quads (8 normals) per quarter and stores their hi / lo tf32 parts in
 // the canonical no-swizzle K-major layout (8-row x 16-byte core matrices) into a ring of NS quarter stages; one
 // thread issues tcgen05.mma (M = 128, N = L1, K = 8) x 3 products per K-step into one of two TMEM accumulators as
-// soon as a stage is complete; four warps drain the previous tile's accumulator with tcgen05.ld and store its rows
-// of Theta'. The warps meet only at the ring's mbarriers (see the kernel). Every mbarrier wait is bounded (trap on
+// soon as a stage is complete; four warps drain the previous tile's accumulator with tcgen05.ld, one 32-column chunk
+// per quarter of the next tile, and store its rows of Theta'. The warps meet only at the ring's mbarriers (see the kernel). Every mbarrier wait is bounded (trap on
 // timeout) so a descriptor mistake fails loudly instead of hanging the GPU.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -31,12 +31,15 @@ namespace {
 using namespace tc;
 
 #ifndef RG_TC_THREADS
-#define RG_TC_THREADS 1024
+#define RG_TC_THREADS 512   // 16 warps, 2 independent Philox quads per thread per quarter (1024 / 256: 2.37 / 2.33 ms vs 2.21 at C4)
 #endif
 constexpr int kTM = 128;       // rows per tile (MMA M)
 constexpr int kKQ = 32;        // K columns per quarter (one of two A buffers)
 #ifndef RG_TC_DRAIN_SPREAD
 #define RG_TC_DRAIN_SPREAD 1
+#endif
+#ifndef RG_TC_NO_STORE
+#define RG_TC_NO_STORE 0   // timing experiments only: the drain skips its stores (Theta' is NOT written)
 #endif
 
 // Global rows row0 .. row0 + n - 1 of Theta' (Theta's generator row = the global row); each finished row is stored at
@@ -61,14 +64,15 @@ struct TcCfg {
     static_assert(NS >= 2, "A ring needs two stages");
 };
 
-// Warp roles inside one CTA (RG_TC_THREADS = 1024, 32 warps):
-//   every warp generates: one Philox call -> 4 normals per thread per quarter (128 rows x KQ columns = 1024 quads),
+// Warp roles inside one CTA (RG_TC_THREADS = 512, 16 warps; QPT = 2 quads per thread per quarter):
+//   every warp generates: QPT Philox calls -> 4 QPT normals per thread per quarter (128 rows x KQ columns = 1024 quads),
 //     stored as hi / lo K-chunks into the quarter's ring stage, then the warp arrives on full[stage];
-//   warp 0, lane 0 also issues the MMAs of each quarter as soon as full[stage] completes (all 32 warps' stores are
+//   warp 0, lane 0 also issues the MMAs of each quarter as soon as full[stage] completes (all NW warps' stores are
 //     in), and commits them to empty[stage] (the stage may be rewritten) and, after a tile's last quarter, to
 //     accf[acc];
-//   warps 28..31 (lane quarters 0..3 of TMEM) also drain the previous tile's accumulator into Theta' after
-//     generating the first quarter of a tile (wait accf, tcgen05.ld, store, arrive on acce[acc]).
+//   the last 4 warps (lane quarters 0..3 of TMEM) also drain the previous tile's accumulator into Theta', one
+//     32-column chunk after each quarter they generate (wait accf before the first, tcgen05.ld, store; arrive on
+//     acce[acc] after the last).
 // No block-wide barrier inside the loop: the warps only meet at the ring's mbarriers, so generation is never held
 // up by the MMA issue or the drain (the round-1 version's per-quarter __syncthreads was its largest stall).
 template <int R, int L1>
@@ -79,7 +83,8 @@ __global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t 
     constexpr uint32_t A_BYTES = C::A_BYTES, B_BYTES = C::B_BYTES;
     constexpr int NW = RG_TC_THREADS / 32;
     constexpr int EPI0 = NW - 4;                          // first drain warp (its index is 0 mod 4)
-    static_assert(NW % 4 == 0 && kTM * (KQ / 4) == RG_TC_THREADS, "one quad per thread per quarter");
+    constexpr int QPT = kTM * (KQ / 4) / RG_TC_THREADS;   // Philox quads per thread per quarter (independent chains)
+    static_assert(NW % 4 == 0 && QPT >= 1 && QPT * RG_TC_THREADS == kTM * (KQ / 4), "whole quads per thread per quarter");
     // instruction descriptor: D f32, A/B tf32, both K-major, N = L1, M = 128
     constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(L1 >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
 
@@ -144,7 +149,7 @@ __global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t 
             const int c0 = kc * 32;
             float v[32];
             tmem_ld32(tmem_d + (static_cast<uint32_t>(lq * 32) << 16) + (uint32_t)(acc * NCOL + c0), v);
-            if (row < n && c0 < L1) {
+            if (row < n && c0 < L1 && !RG_TC_NO_STORE) {
                 for (int o = 0; o < outs.nout; ++o) {
                     float4 *dst = reinterpret_cast<float4 *>(outs.out[o] + (row0 + row) * L1 + c0);
 #pragma unroll
@@ -172,8 +177,10 @@ __global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t 
             unsigned char *a_hi = a_base + (size_t)st * 2 * A_BYTES;
             unsigned char *a_lo = a_hi + A_BYTES;
             if (g >= NS) mbar_wait(&empty[st], (uint32_t)(((g / NS) - 1) & 1));   // its previous MMAs retired
-            {   // Theta[r0 .. r0+127][q*KQ .. q*KQ+KQ-1]: thread t -> row t % 128, column quad t / 128
-                const int row = tid % kTM, qq = tid / kTM;
+#pragma unroll
+            for (int j = 0; j < QPT; ++j) {   // Theta[r0 .. r0+127][q*KQ .. q*KQ+KQ-1]: quad t -> row t % 128, column quad t / 128
+                const int t = tid + j * RG_TC_THREADS;
+                const int row = t % kTM, qq = t / kTM;
                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (r0 + row < n)
                     v = spec_quad(keys, 0u, static_cast<uint64_t>(row0 + r0 + row),
