@@ -428,8 +428,8 @@ TABLE1_DIMS = (4096, 2048, 1024, 512, 256)   # PAPER.md:268-273, Table I row 2E5
 
 # SASS thread-instructions executed per generated normal by sketch_w_tc_kernel<128, 128> (Philox4x32-10, Box-Muller
 # with the spec's polynomials, hi/lo split, shared-memory stores, MMA issue and drain), from ncu's
-# smsp__inst_executed.sum x 32 / (n r) at C4 (profiles/r02/ncu_sketch_v4.md)
-SKETCH_THREAD_INST_PER_NORMAL = 76.7
+# smsp__inst_executed.sum x 32 / (n r) at C4 (profiles/r02/ncu_C4_v5.md: 1.254e9 warp-instructions, 512-thread CTAs, two quads per thread)
+SKETCH_THREAD_INST_PER_NORMAL = 62.7
 
 
 def measure_sketch(args, rg, ctx, n, r, l1, barrier, sm_mhz):
