@@ -368,6 +368,7 @@ RAFTGP_API raftgp_status raftgp_ipc_open(raftgp_ctx ctx, const void *handle64, v
 RAFTGP_API raftgp_status raftgp_ipc_close(raftgp_ctx ctx, void *dev_ptr);
 RAFTGP_API raftgp_status raftgp_copy(raftgp_ctx ctx, void *dst_dev, const void *src_dev, size_t bytes);
 
+
 #ifdef __cplusplus
 }
 #endif

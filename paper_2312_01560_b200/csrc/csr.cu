@@ -1155,7 +1155,9 @@ raftgp_status scan_i32_to_i64(raftgp_ctx ctx, const int32_t *in, int64_t *out, i
     return RAFTGP_OK;
 }
 
-raftgp_status degrees_finalize(raftgp_graph g) {
+// known_2e >= 0: the caller knows 2e (a whole-graph build: 2e = nnz of the symmetric CSR), so the scalars are
+// launched without the host read-back of the degree sum (no host sync; the histogram is not kept then)
+raftgp_status degrees_finalize(raftgp_graph g, int64_t known_2e) {
     raftgp_ctx ctx = g->ctx;
     unsigned long long *d_buf = nullptr;   // [0] = 2e, [1..] = degree histogram
     RG_TRY(dalloc_t(ctx, &d_buf, 1 + kDegHistBins));
@@ -1166,6 +1168,12 @@ raftgp_status degrees_finalize(raftgp_graph g) {
         degree_scalars<<<grid, 256, 0, ctx->stream>>>(g->deg_all, g->n, g->s_all, g->sh_all, d_buf, d_buf + 1);
     }
     RG_CHECK_LAUNCH(ctx);
+    if (known_2e >= 0) {
+        dfree(ctx, d_buf);   // stream-ordered: the kernel's scratch returns to the pool after it
+        g->two_e = known_2e;
+        g->deg_hist.clear();
+        return RAFTGP_OK;
+    }
     std::vector<unsigned long long> h(1 + kDegHistBins, 0);
     RG_TRY(dread(ctx, h.data(), d_buf, sizeof(unsigned long long) * h.size()));
     dfree(ctx, d_buf);
@@ -1509,7 +1517,7 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
     RG_TRY(compute_order(g));
     if (rb == 0 && re == n) {
         if (n > 0) RG_TRY(dcopy(ctx, g->deg_all, g->deg_local, sizeof(int32_t) * n, st));
-        RG_TRY(degrees_finalize(g));
+        RG_TRY(degrees_finalize(g, g->nnz_local));   // whole graph: 2e = nnz (no second read-back)
     }
     return RAFTGP_OK;
 }

@@ -210,7 +210,7 @@ inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 
 raftgp_status scan_i32_to_i64(raftgp_ctx ctx, const int32_t *in, int64_t *out, int64_t n);
 raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src, const int32_t *dst, int64_t rb,
                         int64_t re, raftgp_graph g);
-raftgp_status degrees_finalize(raftgp_graph g);
+raftgp_status degrees_finalize(raftgp_graph g, int64_t known_2e = -1);
 raftgp_status compute_order(raftgp_graph g);
 // a row list reordered for the hop kernels: heavy rows spread from the front (order.cu)
 raftgp_status spread_heavy_list(raftgp_ctx ctx, const int32_t *rows, int64_t count, const int32_t *deg, int32_t *out);

@@ -114,21 +114,6 @@ __global__ void heavy_flags(const int32_t *__restrict__ deg, int64_t nl, int32_t
     if (i < nl) flag[i] = deg[i] > kHeavyDeg ? 1 : 0;
 }
 
-__global__ void heavy_place(const int32_t *__restrict__ flag, const int64_t *__restrict__ hrank, int64_t nl,
-                            int64_t H, int32_t *__restrict__ order) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nl) return;
-    const int64_t h = hrank[i];   // heavy rows before row i
-    int64_t pos;
-    if (flag[i]) {
-        pos = 32 * h;
-    } else {
-        const int64_t j = i - h;   // light index
-        pos = j < 31 * H ? j + j / 31 + 1 : j + H;
-    }
-    order[pos] = (int32_t)i;
-}
-
 // The same spreading for a LIST of rows (the streamed hops, stream.cu): heavy rows every s positions from the front,
 // s = min(32, count / H) (>= 1), the light rows in list order around them. H is read on the device (no host sync).
 __global__ void heavy_flags_list(const int32_t *__restrict__ rows, int64_t count, const int32_t *__restrict__ deg,
@@ -150,7 +135,7 @@ __global__ void heavy_place_list(const int32_t *__restrict__ rows, const int32_t
             const int64_t j = t - h;   // light index
             pos = (sp > 1 && j < (sp - 1) * H) ? (j / (sp - 1)) * sp + j % (sp - 1) + 1 : j + H;
         }
-        out[pos] = rows[t];
+        out[pos] = rows ? rows[t] : (int32_t)t;
     }
 }
 
@@ -242,12 +227,13 @@ raftgp_status compute_order(raftgp_graph g) {
         }
         RG_CHECK_LAUNCH(ctx);
         RG_TRY(scan_i32_to_i64(ctx, flag, hrank, nl));
-        int64_t H = 0;
-        RG_TRY(dread(ctx, &H, hrank + nl, sizeof(int64_t), st));
-        if (H > 0) {
-            if (g->order == nullptr) RG_TRY(dalloc_t(ctx, &g->order, (size_t)nl));
+        // the heavy count H stays on the device (no host read-back): the placement reads it and spaces the heavy rows
+        // min(32, nl / H) apart (every 32nd position for C4's 1.8 % heavy rows; identity order when H = 0)
+        if (g->order == nullptr) RG_TRY(dalloc_t(ctx, &g->order, (size_t)nl));
+        {
             LaunchScope L(ctx, K_ORDER);
-            heavy_place<<<grid, 256, 0, st>>>(flag, hrank, nl, H, g->order);
+            const unsigned pg = (unsigned)std::min<int64_t>(grid, (int64_t)ctx->sm_count * 16);
+            heavy_place_list<<<pg, 256, 0, st>>>(nullptr, flag, hrank, nl, g->order);
         }
         RG_CHECK_LAUNCH(ctx);
         dfree(ctx, flag);
