@@ -1194,7 +1194,11 @@ raftgp_status csr_partition_two_level(raftgp_ctx ctx, int64_t n, int64_t m, cons
     const int64_t nl = re - rb;
     const int cs = shift + fbits;
     const int nc = static_cast<int>(ceil_div(nl, (int64_t)1 << cs));
-    const bool packed = fbits > 0 && shift + vbits <= 32;
+    static const bool force_unpacked = [] {   // RAFTGP_CSR_UNPACKED=1: int2 fine entries even when packing fits (tests)
+        const char *e = getenv("RAFTGP_CSR_UNPACKED");
+        return e && e[0] == '1';
+    }();
+    const bool packed = fbits > 0 && shift + vbits <= 32 && !force_unpacked;
     // level-1 CTAs (2 per SM) and the count pass share the raw-pair ranges
     const int pgrid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 32768), 2 * (int64_t)ctx->sm_count)));
     int2 *p1 = nullptr;

@@ -146,6 +146,9 @@ print('ok')
     {"RAFTGP_BUCKET_CAP": "300"}, {"RAFTGP_BUCKET_CAP": "2048"},
     # level 2 of the two-level partition on small graphs (at most 2 / 3 coarse buckets), alone and with windows
     {"RAFTGP_CSR_COARSE": "2"}, {"RAFTGP_CSR_COARSE": "3", "RAFTGP_BUCKET_CAP": "300"},
+    # level 2 writing int2 entries (the C5 form: row-in-bucket and id bits do not fit 32 bits)
+    {"RAFTGP_CSR_COARSE": "2", "RAFTGP_CSR_UNPACKED": "1"},
+    {"RAFTGP_CSR_COARSE": "3", "RAFTGP_CSR_UNPACKED": "1", "RAFTGP_BUCKET_CAP": "2048"},
     # the one-level partition (shared-memory atomics), kept for A/B runs
     {"RAFTGP_CSR_TWO_LEVEL": "0"}, {"RAFTGP_CSR_TWO_LEVEL": "0", "RAFTGP_BUCKET_CAP": "2048"}])
 def test_bucket_windows(rg, env):
