@@ -492,6 +492,7 @@ raftgp_status raftgp_graph_destroy(raftgp_graph g) {
     dfree(ctx, g->deg_all);
     dfree(ctx, g->s_all);
     dfree(ctx, g->sh_all);
+    drop_slots(g);
     delete g;
     ctx_release(ctx);
     return RAFTGP_OK;
@@ -725,7 +726,10 @@ static raftgp_status first_transform_pre(raftgp_graph g, int32_t nvariants, cons
         st = dalloc_t(ctx, &W1, (size_t)r * l1);
         if (st == RAFTGP_OK) st = sketch_fill(ctx, seed, 1u, 0, r, l1, r, W1);
         if (st == RAFTGP_OK) st = dalloc_t(ctx, &thw, (size_t)g->n * l1);
-        if (st == RAFTGP_OK) st = sketch_w_any(ctx, seed, g->n, r, W1, l1, thw);
+        if (st == RAFTGP_OK && g->slots_active)   // Theta' rows written into the slot layout (relabel.cu)
+            st = sketch_w_tc_rows(ctx, seed, 0, g->n, r, W1, l1, &thw, 1, g->slot);
+        else if (st == RAFTGP_OK)
+            st = sketch_w_any(ctx, seed, g->n, r, W1, l1, thw);
     }
     const float *tw = thw_pre ? thw_pre : thw;
     if (st == RAFTGP_OK && where[RAFTGP_MOD] >= 0) st = dalloc_t(ctx, &gw, (size_t)l1);
@@ -758,6 +762,17 @@ static raftgp_status first_transform_pre(raftgp_graph g, int32_t nvariants, cons
     return st;
 }
 
+// the slot layout applies to whole-graph embeddings with the tcgen05 Theta' kernel (it writes the slots)
+static bool slots_usable(raftgp_graph g, int32_t nvariants, const int32_t *variants, int32_t layers,
+                         const int32_t *dims) {
+    for (int v = 0; v < nvariants; ++v)
+        if (variants[v] != RAFTGP_NCUT && variants[v] != RAFTGP_MOD) return false;   // MOD_REDUCED gathers by node id
+    for (int k = 1; k <= layers; ++k)   // every hop on the fast kernels (the generic one gathers by node id)
+        if (dims[k] != 32 && dims[k] != 64 && dims[k] != 128) return false;
+    return slots_enabled() && sketch_tc_enabled() && g->row_begin == 0 && g->row_end == g->n && g->n > 0 &&
+           g->nnz_local > 0;
+}
+
 static raftgp_status embed_pre(raftgp_graph g, int32_t nvariants, const int32_t *variants, int32_t layers,
                                const int32_t *dims, uint64_t seed, float *const *Z_dev, const int where[3],
                                const float *thw_pre = nullptr) {
@@ -765,6 +780,12 @@ static raftgp_status embed_pre(raftgp_graph g, int32_t nvariants, const int32_t 
     const int32_t r = dims[0], l1 = dims[1];
     std::vector<float *> T1(nvariants, nullptr);
     raftgp_status st = RAFTGP_OK;
+    // slot layout of the operands (relabel.cu): the hub rows first, so the hops keep them in L2. Theta' must then be
+    // generated here (in slots), not handed in
+    if (!thw_pre && slots_usable(g, nvariants, variants, layers, dims)) {
+        st = ensure_slots(g);
+        g->slots_active = st == RAFTGP_OK;
+    }
     for (int v = 0; v < nvariants && st == RAFTGP_OK; ++v) st = dalloc_t(ctx, &T1[v], (size_t)g->n * l1);
     if (st == RAFTGP_OK) st = first_transform_pre(g, nvariants, variants, r, l1, seed, T1.data(), where, thw_pre);
     const bool dual = where[RAFTGP_NCUT] >= 0 && where[RAFTGP_MOD] >= 0;
@@ -778,6 +799,7 @@ static raftgp_status embed_pre(raftgp_graph g, int32_t nvariants, const int32_t 
         }
     }
     for (auto t : T1) dfree(ctx, t);
+    g->slots_active = false;
     return st;
 }
 
@@ -1155,7 +1177,10 @@ raftgp_status raftgp_build_embed(raftgp_ctx ctx, int64_t n, int64_t m, const int
                                        seed, Z_dev);
     }
     const int32_t r = dims[0], l1 = dims[1];
-    const bool overlap = sketch_w_supported(r, l1) && !wide_supported(layers, dims) && n > 0;
+    // with the slot layout Theta' is generated after the CSR build (its rows go to slots that need the degrees);
+    // the arrangements measured the same step time
+    const bool overlap = sketch_w_supported(r, l1) && !wide_supported(layers, dims) && n > 0 &&
+                         !(slots_enabled() && sketch_tc_enabled());
     float *W1 = nullptr, *thw = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     raftgp_status st = RAFTGP_OK;

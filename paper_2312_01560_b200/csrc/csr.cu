@@ -1159,6 +1159,7 @@ raftgp_status scan_i32_to_i64(raftgp_ctx ctx, const int32_t *in, int64_t *out, i
 // launched without the host read-back of the degree sum (no host sync; the histogram is not kept then)
 raftgp_status degrees_finalize(raftgp_graph g, int64_t known_2e) {
     raftgp_ctx ctx = g->ctx;
+    drop_slots(g);   // the slot layout follows the degrees
     unsigned long long *d_buf = nullptr;   // [0] = 2e, [1..] = degree histogram
     RG_TRY(dalloc_t(ctx, &d_buf, 1 + kDegHistBins));
     RG_TRY(dzero(ctx, d_buf, sizeof(unsigned long long) * (1 + kDegHistBins), ctx->stream));

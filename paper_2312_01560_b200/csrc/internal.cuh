@@ -113,6 +113,14 @@ struct raftgp_graph_s {
     int32_t *deg_all = nullptr;    // device int32[n] (global degrees)
     float *s_all = nullptr;        // device fp32[n]: deg^-1/2, 0 for isolated nodes
     float *sh_all = nullptr;       // device fp32[n]: (deg+1)^-1/2
+    // slot layout of the hop operands (relabel.cu, whole-graph embeddings): node i's operand row lives at slot[i], the
+    // highest-degree rows (the hubs, up to a byte budget) in the first slots, so the hop gathers can keep them in L2
+    // (gathers of slots >= *hubk are loaded evict-first); built lazily, dropped when the degrees change
+    int32_t *slot = nullptr;       // device int32[n]
+    int32_t *colx = nullptr;       // device int32[nnz_local]: slot[col[p]]
+    float *s_slot = nullptr;       // device fp32[n]: s by slot (the NCut weight of a gathered row)
+    int32_t *hubk = nullptr;       // device int32[1]: number of hub slots
+    bool slots_active = false;     // set while embed_pre runs the hops on the slot layout
     std::vector<int64_t> deg_hist;   // host: #nodes per degree (last bin = degree >= kDegHistBins-1)
     // host mirror (scoring), filled lazily
     bool host_valid = false;
@@ -211,6 +219,10 @@ raftgp_status scan_i32_to_i64(raftgp_ctx ctx, const int32_t *in, int64_t *out, i
 raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src, const int32_t *dst, int64_t rb,
                         int64_t re, raftgp_graph g);
 raftgp_status degrees_finalize(raftgp_graph g, int64_t known_2e = -1);
+raftgp_status ensure_slots(raftgp_graph g);   // relabel.cu: g->slot / colx / s_slot / hubk for a whole graph
+void drop_slots(raftgp_graph g);
+bool slots_enabled();                          // RAFTGP_RELABEL (default 1)
+bool sketch_tc_enabled();                      // RAFTGP_TC (default 1; sketch.cu)
 raftgp_status compute_order(raftgp_graph g);
 // a row list reordered for the hop kernels: heavy rows spread from the front (order.cu)
 raftgp_status spread_heavy_list(raftgp_ctx ctx, const int32_t *rows, int64_t count, const int32_t *deg, int32_t *out);
@@ -235,7 +247,7 @@ bool sketch_w_supported(int32_t r, int32_t l1);
 raftgp_status sketch_w_tc(raftgp_ctx ctx, uint64_t seed, int64_t n, int32_t r, const float *W1, int32_t l1, float *out);
 // rows row0 .. row0 + rows - 1 of Theta', each stored at its global row into all nout copies (row-partitioned path)
 raftgp_status sketch_w_tc_rows(raftgp_ctx ctx, uint64_t seed, int64_t row0, int64_t rows, int32_t r, const float *W1,
-                               int32_t l1, float *const *outs, int nout);
+                               int32_t l1, float *const *outs, int nout, const int32_t *slot = nullptr);
 raftgp_status sketch_w_any(raftgp_ctx ctx, uint64_t seed, int64_t n, int32_t r, const float *W1, int32_t l1, float *out);
 raftgp_status sketch_theta_w(raftgp_graph g, uint64_t seed, int32_t r, const float *W1, int32_t l1, float *out,
                              double *g_out);

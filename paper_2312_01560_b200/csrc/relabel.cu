@@ -1,0 +1,141 @@
+// relabel.cu — slot layout of the hop operands (a scheduling / layout choice: every row's arithmetic is unchanged).
+//
+// The hops gather one operand row per CSR entry (Eq. 5-6); on the power-law graphs of the
+// workloads a few rows are gathered very often (at C4 the 131 K rows of degree >= 186 — 64 MB of 512-byte rows —
+// take 29 % of all gathers). In node order those rows are scattered over the 2.56 GB operand and compete for L2 with
+// the one-off rows. The slot layout stores node i's operand row at slot[i]: the hubs (the highest degrees, up to
+// kHubBytes of rows) first, in node order, then every other row in node order. The hops then gather
+// operand[colx[p]] with colx = slot[col] (built once per graph), and load the non-hub slots evict-first, so the hub
+// rows stay in L2 (microbenchmark on C4's degree sequence: 13.8 -> 12.1 ms per gather pass). Outputs that are
+// embeddings (Z) stay in node order; the sketch writes Theta' into slots, the epilogues write T into slots.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "internal.cuh"
+
+namespace raftgp {
+
+namespace {
+
+constexpr int kDegBins = 4096;                       // degree histogram (degrees >= kDegBins - 1 share the last bin)
+constexpr int64_t kHubBytes = (int64_t)64 << 20;     // operand bytes of hub rows kept in L2 (of 126 MB)
+constexpr int kRowBytes = 512;                       // the widest gathered operand row (128 fp32)
+
+__global__ void slot_hist(const int32_t *__restrict__ deg, int64_t n, unsigned int *__restrict__ hist) {
+    __shared__ unsigned int h[kDegBins];
+    for (int b = threadIdx.x; b < kDegBins; b += blockDim.x) h[b] = 0u;
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&h[min(deg[i], kDegBins - 1)], 1u);
+    __syncthreads();
+    for (int b = threadIdx.x; b < kDegBins; b += blockDim.x)
+        if (h[b]) atomicAdd(&hist[b], h[b]);
+}
+
+// one thread: the smallest degree threshold t >= 1 with #(deg >= t) <= kmax (t = kDegBins: no hubs)
+__global__ void slot_threshold(const unsigned int *__restrict__ hist, int64_t kmax, int32_t *__restrict__ thr) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int64_t cum = 0;
+    int t = kDegBins;
+    for (int d = kDegBins - 1; d >= 1; --d) {
+        if (cum + hist[d] > kmax) break;
+        cum += hist[d];
+        t = d;
+    }
+    thr[0] = t;
+}
+
+__global__ void slot_flags(const int32_t *__restrict__ deg, int64_t n, const int32_t *__restrict__ thr,
+                           int32_t *__restrict__ flag) {
+    const int32_t t = thr[0];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = (t < kDegBins && deg[i] >= t) ? 1 : 0;
+}
+
+// stable partition: hubs first in node order, then the rest in node order
+__global__ void slot_place(const int32_t *__restrict__ flag, const int64_t *__restrict__ hrank, int64_t n,
+                           const float *__restrict__ s_all, int32_t *__restrict__ slot, float *__restrict__ s_slot,
+                           int32_t *__restrict__ hubk) {
+    const int64_t K = hrank[n];
+    if (blockIdx.x == 0 && threadIdx.x == 0) hubk[0] = (int32_t)K;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t h = hrank[i];
+        const int64_t sl = flag[i] ? h : K + (i - h);
+        slot[i] = (int32_t)sl;
+        s_slot[sl] = s_all[i];
+    }
+}
+
+__global__ void slot_cols(const int32_t *__restrict__ col, int64_t nnz, const int32_t *__restrict__ slot,
+                          int32_t *__restrict__ colx) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
+        colx[p] = __ldg(slot + __ldg(col + p));
+}
+
+}  // namespace
+
+bool slots_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("RAFTGP_RELABEL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+void drop_slots(raftgp_graph g) {
+    raftgp_ctx ctx = g->ctx;
+    dfree(ctx, g->slot);
+    dfree(ctx, g->colx);
+    dfree(ctx, g->s_slot);
+    dfree(ctx, g->hubk);
+    g->slot = g->colx = g->hubk = nullptr;
+    g->s_slot = nullptr;
+}
+
+raftgp_status ensure_slots(raftgp_graph g) {
+    if (g->slot) return RAFTGP_OK;
+    if (g->row_begin != 0 || g->row_end != g->n || g->n == 0) return fail(RAFTGP_ERR_INTERNAL, "slots: whole graph only");
+    raftgp_ctx ctx = g->ctx;
+    cudaStream_t st = ctx->stream;
+    const int64_t n = g->n, nnz = g->nnz_local;
+    unsigned int *hist = nullptr;
+    int32_t *thr = nullptr, *flag = nullptr;
+    int64_t *hrank = nullptr;
+    RG_TRY(dalloc_t(ctx, &g->slot, (size_t)n));
+    RG_TRY(dalloc_t(ctx, &g->s_slot, (size_t)n));
+    RG_TRY(dalloc_t(ctx, &g->hubk, 1));
+    RG_TRY(dalloc_t(ctx, &g->colx, (size_t)std::max<int64_t>(1, nnz)));
+    RG_TRY(dalloc_t(ctx, &hist, kDegBins));
+    RG_TRY(dalloc_t(ctx, &thr, 1));
+    RG_TRY(dalloc_t(ctx, &flag, (size_t)n));
+    RG_TRY(dalloc_t(ctx, &hrank, (size_t)n + 1));
+    RG_TRY(dzero(ctx, hist, sizeof(unsigned int) * kDegBins, st));
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), (int64_t)ctx->sm_count * 8));
+    {
+        LaunchScope L(ctx, K_ORDER);
+        slot_hist<<<std::min<unsigned>(grid, (unsigned)ctx->sm_count * 2), 256, 0, st>>>(g->deg_all, n, hist);
+        slot_threshold<<<1, 32, 0, st>>>(hist, kHubBytes / kRowBytes, thr);
+        slot_flags<<<grid, 256, 0, st>>>(g->deg_all, n, thr, flag);
+    }
+    RG_CHECK_LAUNCH(ctx);
+    RG_TRY(scan_i32_to_i64(ctx, flag, hrank, n));
+    {
+        LaunchScope L(ctx, K_ORDER);
+        slot_place<<<grid, 256, 0, st>>>(flag, hrank, n, g->s_all, g->slot, g->s_slot, g->hubk);
+        if (nnz > 0) {
+            const unsigned cg = (unsigned)std::min<int64_t>(ceil_div(nnz, 256), (int64_t)ctx->sm_count * 16);
+            slot_cols<<<cg, 256, 0, st>>>(g->col, nnz, g->slot, g->colx);
+        }
+    }
+    RG_CHECK_LAUNCH(ctx);
+    dfree(ctx, hist);
+    dfree(ctx, thr);
+    dfree(ctx, flag);
+    dfree(ctx, hrank);
+    return RAFTGP_OK;
+}
+
+}  // namespace raftgp

@@ -546,7 +546,7 @@ raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c,
     int32_t *mmem = nullptr;
     auto drop_members = [&]() {
         dfree(ctx, members.row_ptr); dfree(ctx, members.col); dfree(ctx, members.deg_local); dfree(ctx, members.order);
-        dfree(ctx, members.deg_all); dfree(ctx, members.s_all); dfree(ctx, members.sh_all);
+        dfree(ctx, members.deg_all); dfree(ctx, members.s_all); dfree(ctx, members.sh_all); drop_slots(&members);
         dfree(ctx, mboff); dfree(ctx, mmem);
     };
     if (K <= kMemMaxK) {   // stable counting sort

@@ -53,7 +53,8 @@ __global__ void __launch_bounds__(256) gauss_fill(uint64_t seed, uint32_t tag, i
 // partial[chunk][c] = sum_{j in chunk, sequential} d_j * theta[j][c]   (fp64); rows loaded 16 ahead so the fp64 add
 // chain, not the load latency, sets the pace
 __global__ void __launch_bounds__(128) g_partials(const float *__restrict__ theta, const int32_t *__restrict__ deg,
-                                                  int64_t n, int32_t r, int64_t chunk0, double *__restrict__ partial) {
+                                                  int64_t n, int32_t r, int64_t chunk0, double *__restrict__ partial,
+                                                  const int32_t *__restrict__ slot) {
     const int64_t chunk = chunk0 + blockIdx.x;
     const int64_t j0 = chunk * kGChunk, j1 = min(n, j0 + (int64_t)kGChunk);
     // blockIdx.y picks a 128-column slice (wide operands); each (chunk, column) sum stays sequential in j
@@ -64,14 +65,15 @@ __global__ void __launch_bounds__(128) g_partials(const float *__restrict__ thet
             float t[16];
             int32_t d[16];
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
-                t[u] = __ldg(theta + (j + u) * r + c);
+            for (int u = 0; u < 16; ++u) {   // row j of theta is at slot[j] in the slot layout (relabel.cu)
+                t[u] = __ldg(theta + (slot ? (int64_t)__ldg(slot + j + u) : (j + u)) * r + c);
                 d[u] = __ldg(deg + j + u);
             }
 #pragma unroll
             for (int u = 0; u < 16; ++u) acc += static_cast<double>(d[u]) * static_cast<double>(t[u]);
         }
-        for (; j < j1; ++j) acc += static_cast<double>(deg[j]) * static_cast<double>(theta[j * r + c]);
+        for (; j < j1; ++j)
+            acc += static_cast<double>(deg[j]) * static_cast<double>(theta[(slot ? (int64_t)slot[j] : j) * r + c]);
         partial[chunk * r + c] = acc;
     }
 }
@@ -211,11 +213,16 @@ bool sketch_w_supported(int32_t r, int32_t l1) {
 }
 
 // tcgen05 path by default (RAFTGP_TC=0 selects the FFMA kernel)
-raftgp_status sketch_w_any(raftgp_ctx ctx, uint64_t seed, int64_t n, int32_t r, const float *W1, int32_t l1, float *out) {
+bool sketch_tc_enabled() {   // RAFTGP_TC=0: the FFMA Theta' kernel
     static const bool use_tc = [] {
         const char *e = getenv("RAFTGP_TC");
         return !(e && e[0] == '0');
     }();
+    return use_tc;
+}
+
+raftgp_status sketch_w_any(raftgp_ctx ctx, uint64_t seed, int64_t n, int32_t r, const float *W1, int32_t l1, float *out) {
+    const bool use_tc = sketch_tc_enabled();
     if (n == 0) return RAFTGP_OK;
     if (use_tc) return sketch_w_tc(ctx, seed, n, r, W1, l1, out);
     const float sigma = spec_sigma(r);
@@ -263,8 +270,8 @@ raftgp_status g_partials_range(raftgp_graph g, const float *theta, int32_t r, in
     if (count <= 0) return RAFTGP_OK;
     {
         LaunchScope L(ctx, K_SKETCH_G);
-        g_partials<<<dim3((unsigned)count, (unsigned)ceil_div(r, 128)), 128, 0, ctx->stream>>>(theta, g->deg_all, g->n,
-                                                                                               r, chunk0, partial);
+        g_partials<<<dim3((unsigned)count, (unsigned)ceil_div(r, 128)), 128, 0, ctx->stream>>>(
+            theta, g->deg_all, g->n, r, chunk0, partial, g->slots_active ? g->slot : nullptr);
     }
     RG_CHECK_LAUNCH(ctx);
     return RAFTGP_OK;

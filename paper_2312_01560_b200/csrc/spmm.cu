@@ -64,6 +64,10 @@ struct HopArgs {
     PushSpec push;             // push.nrep > 0: the T output (out/out2 when WN == 0, Tn/Tn2 when WN > 0) goes to
                                // the replicas at global rows instead of the local buffers
     int claim = 8;             // row groups per dynamic claim (kClaim; 1 for short row lists: every warp gets work)
+    const int32_t *colx = nullptr;   // slot layout (relabel.cu): gathered operand rows by slot (colx = slot[col]) ...
+    const int32_t *slot = nullptr;   // ... node -> slot (the self term's row; T outputs are written at slots)
+    const float *s_slot = nullptr;   // ... s by slot (NCut weights of the gathered rows)
+    const int32_t *hubk = nullptr;   // ... number of hub slots: gathers of slots >= *hubk load evict-first
     int half = 0;              // KIND_GCN2H: 1 / 2 only the first / second half of [T_a | T_b] (the other
                                // half's lanes load nothing; each half's arithmetic is unchanged)
 };
@@ -71,6 +75,18 @@ struct HopArgs {
 constexpr int kClaim = 8;      // row groups per dynamic claim
 
 __device__ __forceinline__ float4 ldg4(const float4 *p) { return __ldg(p); }
+// read-only load with an L2 eviction-priority policy (createpolicy), for the one-off rows of the slot layout
+__device__ __forceinline__ float4 ldg4_pol(const float4 *p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 
 __device__ __forceinline__ void fma4(float4 &a, float w, const float4 &v) {
     a.x = fmaf(w, v.x, a.x);
@@ -98,9 +114,12 @@ enum Mode : int { M_SUM = 0, M_S = 1, M_SUM_D = 2, M_SUM_S = 3 };
 // `c0` is this row's first 32-entry col chunk, loaded by the caller one row ahead; later chunks are
 // prefetched one chunk ahead, so col latency overlaps the row gathers. (L2 eviction-priority hints for
 // high-degree rows were measured and made every hop slower; plain read-only loads are used.)
-template <int W, int U_REQ, int MODE, bool HALF = false>
+template <int W, int U_REQ, int MODE, bool HALF = false, bool SL = false>
 __device__ __forceinline__ void gather_row(const HopArgs &a, int64_t beg, int64_t end, int32_t c0, int lane,
-                                           float4 &acc, float4 &acc2) {
+                                           float4 &acc, float4 &acc2, int32_t hk = 0, uint64_t pol = 0) {
+    static_assert(!SL || MODE != M_SUM_D, "the slot layout has no by-slot degree vector");
+    const int32_t *cg = SL ? a.colx : a.col;   // gathered operand rows: slots or node ids
+    const float *sw = SL ? a.s_slot : a.s_all;
     constexpr int LPN = W / 4, NPW = 32 / LPN;
     constexpr int U = (NPW * U_REQ <= 32) ? U_REQ : 32 / NPW;
     static_assert(NPW * U <= 32 && 32 % (NPW * U) == 0, "unroll must tile a 32-entry col chunk");
@@ -113,16 +132,16 @@ __device__ __forceinline__ void gather_row(const HopArgs &a, int64_t beg, int64_
 #if RG_PREFETCH
     int32_t mycur = c0;
 #else
-    int32_t mycur = (beg + lane < end) ? __ldg(a.col + beg + lane) : 0;
+    int32_t mycur = (beg + lane < end) ? __ldg(cg + beg + lane) : 0;
     (void)c0;
 #endif
     for (int64_t base = beg; base < end; base += 32) {
         const int cnt = (end - base < 32) ? static_cast<int>(end - base) : 32;
         const int64_t nb = base + 32;
-        const int32_t mynext = (nb < end && nb + lane < end) ? __ldg(a.col + nb + lane) : 0;
+        const int32_t mynext = (nb < end && nb + lane < end) ? __ldg(cg + nb + lane) : 0;
         const int32_t myj = mycur;
         float myw = 0.f;
-        if (MODE == M_S || MODE == M_SUM_S) myw = lane < cnt ? __ldg(a.s_all + myj) : 0.f;
+        if (MODE == M_S || MODE == M_SUM_S) myw = lane < cnt ? __ldg(sw + myj) : 0.f;
         if (MODE == M_SUM_D) myw = lane < cnt ? static_cast<float>(__ldg(a.deg_all + myj)) : 0.f;
         for (int k0 = 0; k0 < cnt; k0 += NPW * U) {
             float4 v[U];
@@ -130,7 +149,12 @@ __device__ __forceinline__ void gather_row(const HopArgs &a, int64_t beg, int64_
             for (int u = 0; u < U; ++u) {
                 const int k = k0 + u * NPW + sub;
                 const int32_t j = __shfl_sync(FULL, myj, k);
-                v[u] = (k < cnt && act) ? ldg4(X4 + (int64_t)j * LPN + cl) : make_float4(0.f, 0.f, 0.f, 0.f);
+                if constexpr (SL)
+                    v[u] = (k < cnt && act) ? (j >= hk ? ldg4_pol(X4 + (int64_t)j * LPN + cl, pol)
+                                                       : ldg4(X4 + (int64_t)j * LPN + cl))
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+                else
+                    v[u] = (k < cnt && act) ? ldg4(X4 + (int64_t)j * LPN + cl) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -187,9 +211,19 @@ struct KindTraits {
 
 // One hop for groups of RB consecutive visiting positions per warp; warps claim kClaim groups at a time from a
 // per-launch counter (dynamic, a.ctr) or walk them grid-stride (a.ctr == null).
-template <int KIND, int W, int WN, int RB, int U, int THREADS>
+template <int KIND, int W, int WN, int RB, int U, int THREADS, bool SL = false>
 __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREADS) > 0 ? KindTraits<KIND>::WARPS * 32 / THREADS : 1)
     hop_kernel(HopArgs a) {
+    // slot layout: the hub-slot count and the evict-first policy, once per thread
+    int32_t hk = 0;
+    uint64_t pol = 0;
+    if constexpr (SL) {
+        hk = __ldg(a.hubk);
+        pol = policy_evict_first();
+    }
+    // operand outputs (the feature hop's T_1, the epilogue's T_next) go to the row's slot; embeddings (Z) keep node
+    // order. Each row's slot is loaded one row ahead (with the next row's CSR offsets), so no load waits on it
+    constexpr bool FEAT = KIND == KIND_NCUT || KIND == KIND_MOD || KIND == KIND_MOD_REDUCED || KIND == KIND_DUAL;
     extern __shared__ float4 smem4[];
     float *smem = reinterpret_cast<float *>(smem4);
     constexpr int LPN = W / 4;
@@ -221,16 +255,21 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
         const int rows_here = (a.nl - row0 < RB) ? static_cast<int>(a.nl - row0) : RB;
         // first col chunk of the group's first row; each row prefetches the next row's first chunk
         int64_t beg = 0, end = 0;
-        int32_t c0 = 0;
+        int32_t c0 = 0, sl_cur = 0, my_sl = 0;
         if constexpr (KIND != KIND_LOAD) {
             const int64_t r = a.order ? static_cast<int64_t>(__ldg(a.order + row0)) : row0;
             beg = a.row_ptr[r];
             end = a.row_ptr[r + 1];
             c0 = (RG_PREFETCH && beg + lane < end) ? __ldg(a.col + beg + lane) : 0;
+            if constexpr (SL) sl_cur = __ldg(a.slot + a.rb + r);
         }
         for (int rr = 0; rr < rows_here; ++rr) {
             const int64_t row = a.order ? static_cast<int64_t>(__ldg(a.order + row0 + rr)) : row0 + rr;   // local row
             const int64_t gi = a.rb + row;          // global row id
+            const int64_t srow = SL ? (int64_t)sl_cur : gi;   // this row's operand row (self term, T outputs)
+            if constexpr (SL) {
+                if (lane == rr) my_sl = sl_cur;     // lane rr keeps row rr's slot for the epilogue
+            }
             float4 acc, acc2;
             float4 y, y2 = make_float4(0.f, 0.f, 0.f, 0.f);
             if constexpr (KIND == KIND_LOAD) {
@@ -243,14 +282,15 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
                     nbeg = a.row_ptr[r];
                     nend = a.row_ptr[r + 1];
                     if (RG_PREFETCH) nc0 = (nbeg + lane < nend) ? __ldg(a.col + nbeg + lane) : 0;
+                    if constexpr (SL) sl_cur = __ldg(a.slot + a.rb + r);
                 }
                 float4 self = make_float4(0.f, 0.f, 0.f, 0.f);
                 if constexpr (KIND == KIND_GCN)
-                    self = ldg4(reinterpret_cast<const float4 *>(a.X) + gi * LPN + cl);
-                if constexpr (KIND == KIND_GCN2) self = ldg4(reinterpret_cast<const float4 *>(a.X) + gi * LPN + cl);
+                    self = ldg4(reinterpret_cast<const float4 *>(a.X) + srow * LPN + cl);
+                if constexpr (KIND == KIND_GCN2) self = ldg4(reinterpret_cast<const float4 *>(a.X) + srow * LPN + cl);
                 if constexpr (KIND == KIND_GCN2H)
-                    if ((cl < LPN / 2) == (a.half == 1)) self = ldg4(reinterpret_cast<const float4 *>(a.X) + gi * LPN + cl);
-                gather_row<W, U, KindTraits<KIND>::MODE, KIND == KIND_GCN2H>(a, beg, end, c0, lane, acc, acc2);
+                    if ((cl < LPN / 2) == (a.half == 1)) self = ldg4(reinterpret_cast<const float4 *>(a.X) + srow * LPN + cl);
+                gather_row<W, U, KindTraits<KIND>::MODE, KIND == KIND_GCN2H, SL>(a, beg, end, c0, lane, acc, acc2, hk, pol);
                 beg = nbeg;
                 end = nend;
                 c0 = nc0;
@@ -316,9 +356,10 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
                             if (r < n2) reinterpret_cast<float4 *>(a.push.rep2[r])[grow * ld4 + cl] = y2;
                     }
                 } else {
-                    if (a.out != nullptr) reinterpret_cast<float4 *>(a.out)[row * LPN + cl] = y;
+                    const int64_t orow = (SL && FEAT) ? srow : row;   // slot (whole graph) or local row
+                    if (a.out != nullptr) reinterpret_cast<float4 *>(a.out)[orow * LPN + cl] = y;
                     if constexpr (NV == 2) {
-                        if (a.out2 != nullptr) reinterpret_cast<float4 *>(a.out2)[row * LPN + cl] = y2;
+                        if (a.out2 != nullptr) reinterpret_cast<float4 *>(a.out2)[orow * LPN + cl] = y2;
                     }
                 }
                 if constexpr (WN > 0) {
@@ -364,6 +405,7 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
                 for (int q = 0; q < RC; ++q) {
                     const int rr = rs + (q0 + q) * RS;
                     const int v = rr / RB, r_in = rr % RB;
+                    const int32_t tslot = SL ? __shfl_sync(FULL, my_sl, r_in) : 0;   // slot of row r_in
                     if (r_in < rows_here) {
                         const int64_t row = a.order ? static_cast<int64_t>(__ldg(a.order + row0 + r_in)) : row0 + r_in;
                         const float shi = __ldg(a.sh_all + a.rb + row);
@@ -379,7 +421,7 @@ __global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREA
                         } else {
                             float4 *T4 = reinterpret_cast<float4 *>(v == 0 ? a.Tn : a.Tn2);
                             const int64_t ld4 = a.tn_ld > 0 ? a.tn_ld / 4 : OL;
-                            T4[row * ld4 + oc] = t4;
+                            T4[(SL ? (int64_t)tslot : row) * ld4 + oc] = t4;
                         }
                     }
                 }
@@ -458,8 +500,8 @@ __global__ void __launch_bounds__(128) hop_generic(HopArgs a, int W, int WN) {
 }
 
 // ---------------------------------------------------------------- launch helpers
-template <int KIND, int W, int WN>
-raftgp_status launch_fast(raftgp_ctx ctx, const HopArgs &a) {
+template <int KIND, int W, int WN, bool SL>
+raftgp_status launch_fast_sl(raftgp_ctx ctx, const HopArgs &a) {
     constexpr int RB = 4;
     constexpr int U = KindTraits<KIND>::U;
     constexpr int THREADS = WN > 0 ? 512 : 256;
@@ -468,7 +510,7 @@ raftgp_status launch_fast(raftgp_ctx ctx, const HopArgs &a) {
     const size_t smem = sizeof(float) * ((size_t)W * WN + (WN > 0 ? (size_t)WPB * NV * RB * W : 0));
     static const char occ_key = 0;   // per-(device, instantiation) key
     int blocks_per_sm = 1;
-    auto kern = hop_kernel<KIND, W, WN, RB, U, THREADS>;
+    auto kern = hop_kernel<KIND, W, WN, RB, U, THREADS, SL>;
     RG_TRY(per_device(ctx->device, &occ_key, &blocks_per_sm, [&](int *v) -> raftgp_status {
         RG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int b = 0;
@@ -499,6 +541,22 @@ raftgp_status launch_fast(raftgp_ctx ctx, const HopArgs &a) {
     return RAFTGP_OK;
 }
 
+// the slot-layout instantiation exists for the kinds of the whole-graph embedding path only
+template <int KIND, int W, int WN>
+raftgp_status launch_fast(raftgp_ctx ctx, const HopArgs &a) {
+    constexpr bool SLOTTABLE = (KIND == KIND_DUAL || KIND == KIND_NCUT || KIND == KIND_MOD || KIND == KIND_GCN ||
+                                KIND == KIND_GCN2 || KIND == KIND_GCN2H);
+    if constexpr (SLOTTABLE) {
+        if (a.colx) {
+            if (a.push.nrep > 0) return fail(RAFTGP_ERR_INTERNAL, "hop: slot layout with pushed replicas");
+            return launch_fast_sl<KIND, W, WN, true>(ctx, a);
+        }
+    } else {
+        if (a.colx) return fail(RAFTGP_ERR_INTERNAL, "hop: this kind has no slot-layout kernel");
+    }
+    return launch_fast_sl<KIND, W, WN, false>(ctx, a);
+}
+
 template <int KIND, int W>
 raftgp_status dispatch_wn(raftgp_ctx ctx, const HopArgs &a, int wn) {
     switch (wn) {
@@ -525,7 +583,7 @@ raftgp_status dispatch(raftgp_ctx ctx, const HopArgs &a, int w, int wn) {
     }
     // the generic kernel implements the plain hop only: the fused exchange, strided T_next and the s^ row scale
     // of the pre-transformed feature hop exist only in the fast kernels (their callers check the fast path first)
-    if (a.push.nrep > 0 || a.scale_sh || (a.tn_ld > 0 && a.tn_ld != wn))
+    if (a.push.nrep > 0 || a.scale_sh || (a.tn_ld > 0 && a.tn_ld != wn) || a.colx)
         return fail(RAFTGP_ERR_INTERNAL, "hop: push / strided output / s^ scale need the fast kernel");
     const size_t smem = sizeof(float) * ((size_t)w + 32);
     if (smem > 48 * 1024) {
@@ -554,6 +612,12 @@ HopArgs base_args(raftgp_graph g, int32_t /*w*/) {
     a.col = g->col;
     a.s_all = g->s_all;
     a.sh_all = g->sh_all;
+    if (g->slots_active) {   // slot layout of the operands (embed_pre with RAFTGP_RELABEL)
+        a.colx = g->colx;
+        a.slot = g->slot;
+        a.s_slot = g->s_slot;
+        a.hubk = g->hubk;
+    }
     a.deg_all = g->deg_all;
     a.inv2e = g->two_e > 0 ? 1.0 / static_cast<double>(g->two_e) : 0.0;
     return a;

@@ -417,7 +417,7 @@ raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const i
     ng->nl = n;
     auto drop = [&](raftgp_graph_s &x) {
         dfree(ctx, x.row_ptr); dfree(ctx, x.col); dfree(ctx, x.deg_local); dfree(ctx, x.order); dfree(ctx, x.deg_all);
-        dfree(ctx, x.s_all); dfree(ctx, x.sh_all);
+        dfree(ctx, x.s_all); dfree(ctx, x.sh_all); drop_slots(&x);
     };
     int32_t *add = nullptr, *level = nullptr, *rows = nullptr, *cnt = nullptr, *nkeys = nullptr;
     int *err = nullptr;
@@ -660,7 +660,7 @@ void stream_destroy(raftgp_stream s) {
     if (s->g) {
         raftgp_graph_s &x = *s->g;
         dfree(ctx, x.row_ptr); dfree(ctx, x.col); dfree(ctx, x.deg_local); dfree(ctx, x.order); dfree(ctx, x.deg_all);
-        dfree(ctx, x.s_all); dfree(ctx, x.sh_all);
+        dfree(ctx, x.s_all); dfree(ctx, x.sh_all); drop_slots(&x);
         delete s->g;
         ctx_release(ctx);
     }

@@ -48,6 +48,7 @@ constexpr int kKQ = 32;        // K columns per quarter (one of two A buffers)
 struct SketchOut {
     float *out[kMaxPush];
     int nout;
+    const int32_t *slot;   // slot layout (relabel.cu): row i stored at slot[i]; null = row order
 };
 
 template <int R, int L1>
@@ -151,7 +152,8 @@ __global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t 
             tmem_ld32(tmem_d + (static_cast<uint32_t>(lq * 32) << 16) + (uint32_t)(acc * NCOL + c0), v);
             if (row < n && c0 < L1 && !RG_TC_NO_STORE) {
                 for (int o = 0; o < outs.nout; ++o) {
-                    float4 *dst = reinterpret_cast<float4 *>(outs.out[o] + (row0 + row) * L1 + c0);
+                    const int64_t orow = outs.slot ? (int64_t)__ldg(outs.slot + row0 + row) : row0 + row;
+                    float4 *dst = reinterpret_cast<float4 *>(outs.out[o] + orow * L1 + c0);
 #pragma unroll
                     for (int i = 0; i < 8; ++i)
                         if (c0 + 4 * i < L1) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
@@ -269,11 +271,12 @@ raftgp_status dispatch_tc(raftgp_ctx ctx, uint64_t seed, int64_t row0, int64_t n
 }  // namespace
 
 raftgp_status sketch_w_tc_rows(raftgp_ctx ctx, uint64_t seed, int64_t row0, int64_t rows, int32_t r, const float *W1,
-                               int32_t l1, float *const *outs, int nout) {
+                               int32_t l1, float *const *outs, int nout, const int32_t *slot) {
     if (rows == 0) return RAFTGP_OK;
     if (nout < 1 || nout > kMaxPush) return fail(RAFTGP_ERR_INTERNAL, "sketch_w_tc_rows: 1..8 outputs");
     SketchOut so{};
     so.nout = nout;
+    so.slot = slot;
     for (int q = 0; q < nout; ++q) so.out[q] = outs[q];
     const float sigma = spec_sigma(r);
     switch (r) {

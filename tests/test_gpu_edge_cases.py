@@ -233,3 +233,49 @@ def test_build_embed_overlap_modes_identical(rg, tmp_path):
         outs[mode] = np.load(f)
     assert np.array_equal(outs["split"].view(np.uint32), outs["prio"].view(np.uint32))
     assert np.array_equal(outs["split"].view(np.uint32), outs["serial"].view(np.uint32))
+
+
+_RELABEL_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, '.')
+import synth
+from paper_2312_01560_b200 import raftgp as rg
+ctx = rg.Context(0)
+out = []
+rng = np.random.default_rng(7)
+hub_s = np.concatenate([np.zeros(3000, np.int32), rng.integers(0, 9000, 30000).astype(np.int32)])
+hub_d = np.concatenate([rng.integers(1, 9000, 3000).astype(np.int32), rng.integers(0, 9000, 30000).astype(np.int32)])
+cases = [(g.n, g.src, g.dst) for g in (synth.generate('C1', 2), synth.generate('C2', 5, n=60000))]
+cases += [(9000, hub_s, hub_d), (12000, hub_s, hub_d)]   # hub-heavy; the second has 3000 isolated nodes
+for n, s, d in cases:
+    for dims in ((64, 64, 32), (128, 128, 64), (128, 128, 64, 32)):
+        Z, _ = rg.raftgp_build_embed(ctx, n, torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda(),
+                                     ['ncut', 'mod'], dims, 3)
+        out.append(torch.cat([Z['ncut'], Z['mod']], 1).cpu().numpy())
+        g = rg.raftgp_build_csr(ctx, n, torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda())
+        _, Zs = rg.raftgp_embed_multi(g, ['ncut'], dims, 3)
+        out.append(Zs['ncut'].cpu().numpy())
+np.savez(sys.argv[1], *out)
+print('ok')
+"""
+
+
+def test_slot_layout_bit_identical(rg, tmp_path):
+    """The slot layout of the hop operands (RAFTGP_RELABEL=1, the default: hub rows first, non-hub gathers
+    evict-first) changes only where operand rows live: every embedding is bit-identical to the node-order layout
+    (both variants and NCut alone, 2- and 3-layer stacks, hub-heavy graphs and isolated nodes)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for mode in ("0", "1"):
+        f = str(tmp_path / f"r{mode}.npz")
+        r = subprocess.run([sys.executable, "-c", _RELABEL_SCRIPT, f], cwd=root,
+                           env=dict(os.environ, RAFTGP_RELABEL=mode), capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+        z = np.load(f)
+        res[mode] = [z[k] for k in sorted(z.files, key=lambda k: int(k.split("_")[1]))]
+    assert len(res["0"]) == len(res["1"])
+    for a, b in zip(res["0"], res["1"]):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
