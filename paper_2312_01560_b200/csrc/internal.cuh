@@ -222,6 +222,7 @@ raftgp_status degrees_finalize(raftgp_graph g, int64_t known_2e = -1);
 raftgp_status ensure_slots(raftgp_graph g);   // relabel.cu: g->slot / colx / s_slot / hubk for a whole graph
 void drop_slots(raftgp_graph g);
 bool slots_enabled();                          // RAFTGP_RELABEL (default 1)
+int64_t slot_hub_bytes();                      // operand bytes of hub slots (RAFTGP_HUB_MB, default 64 MB)
 bool sketch_tc_enabled();                      // RAFTGP_TC (default 1; sketch.cu)
 raftgp_status compute_order(raftgp_graph g);
 // a row list reordered for the hop kernels: heavy rows spread from the front (order.cu)

@@ -21,7 +21,7 @@ namespace raftgp {
 namespace {
 
 constexpr int kDegBins = 4096;                       // degree histogram (degrees >= kDegBins - 1 share the last bin)
-constexpr int64_t kHubBytes = (int64_t)64 << 20;     // operand bytes of hub rows kept in L2 (of 126 MB)
+constexpr int64_t kHubBytes = (int64_t)64 << 20;     // operand bytes of hub rows kept in L2 (of 126 MB); RAFTGP_HUB_MB
 constexpr int kRowBytes = 512;                       // the widest gathered operand row (128 fp32)
 
 __global__ void slot_hist(const int32_t *__restrict__ deg, int64_t n, unsigned int *__restrict__ hist) {
@@ -77,6 +77,14 @@ __global__ void slot_cols(const int32_t *__restrict__ col, int64_t nnz, const in
 
 }  // namespace
 
+int64_t slot_hub_bytes() {
+    static const int64_t b = [] {
+        const char *e = getenv("RAFTGP_HUB_MB");
+        return e ? (int64_t)std::max(0, atoi(e)) << 20 : kHubBytes;
+    }();
+    return b;
+}
+
 bool slots_enabled() {
     static const bool on = [] {
         const char *e = getenv("RAFTGP_RELABEL");
@@ -117,7 +125,7 @@ raftgp_status ensure_slots(raftgp_graph g) {
     {
         LaunchScope L(ctx, K_ORDER);
         slot_hist<<<std::min<unsigned>(grid, (unsigned)ctx->sm_count * 2), 256, 0, st>>>(g->deg_all, n, hist);
-        slot_threshold<<<1, 32, 0, st>>>(hist, kHubBytes / kRowBytes, thr);
+        slot_threshold<<<1, 32, 0, st>>>(hist, slot_hub_bytes() / kRowBytes, thr);
         slot_flags<<<grid, 256, 0, st>>>(g->deg_all, n, thr, flag);
     }
     RG_CHECK_LAUNCH(ctx);
