@@ -211,8 +211,17 @@ struct KindTraits {
 
 // One hop for groups of RB consecutive visiting positions per warp; warps claim kClaim groups at a time from a
 // per-launch counter (dynamic, a.ctr) or walk them grid-stride (a.ctr == null).
+#ifndef RG_WARPS_SL
+#define RG_WARPS_SL 32
+#endif
+// resident warps per SM a hop kernel is compiled for (the register cap): the slot-layout GCN hops may differ
+template <int KIND, bool SL>
+__host__ __device__ constexpr int hop_warps() {
+    return (SL && (KIND == KIND_GCN || KIND == KIND_GCN2 || KIND == KIND_GCN2H)) ? RG_WARPS_SL : KindTraits<KIND>::WARPS;
+}
+
 template <int KIND, int W, int WN, int RB, int U, int THREADS, bool SL = false>
-__global__ void __launch_bounds__(THREADS, (KindTraits<KIND>::WARPS * 32 / THREADS) > 0 ? KindTraits<KIND>::WARPS * 32 / THREADS : 1)
+__global__ void __launch_bounds__(THREADS, (hop_warps<KIND, SL>() * 32 / THREADS) > 0 ? hop_warps<KIND, SL>() * 32 / THREADS : 1)
     hop_kernel(HopArgs a) {
     // slot layout: the hub-slot count and the evict-first policy, once per thread
     int32_t hk = 0;
@@ -500,10 +509,16 @@ __global__ void __launch_bounds__(128) hop_generic(HopArgs a, int W, int WN) {
 }
 
 // ---------------------------------------------------------------- launch helpers
+#ifndef RG_U_SUM_SL
+#define RG_U_SUM_SL 8
+#endif
 template <int KIND, int W, int WN, bool SL>
 raftgp_status launch_fast_sl(raftgp_ctx ctx, const HopArgs &a) {
     constexpr int RB = 4;
-    constexpr int U = KindTraits<KIND>::U;
+    // GCN hops on the slot layout: 8 gathers in flight per lane (the L2-resident hub rows leave DRAM latency, not its
+    // bandwidth, as the bound: C4 GCN hops 42.4 -> 38.8 ms; in node order U = 8 was slower)
+    constexpr bool GCNK = KIND == KIND_GCN || KIND == KIND_GCN2 || KIND == KIND_GCN2H;
+    constexpr int U = (SL && GCNK) ? RG_U_SUM_SL : KindTraits<KIND>::U;
     constexpr int THREADS = WN > 0 ? 512 : 256;
     constexpr int WPB = THREADS / 32;
     constexpr int NV = KindTraits<KIND>::NV;
