@@ -386,40 +386,60 @@ def measure_sbm(args, rg, dev, barrier):
 
 def measure_stream(args, rg, dev, barrier, gr, src_d, dst_d, dims):
     """NEXT-4: streaming updates on the C4 graph, NCut embedding with the bench dims: the
-    time of raftgp_stream_add_edges for batches of B new random edges against a full rebuild + embed of the
-    same final graph (raftgp_build_csr + raftgp_embed_multi(ncut)), with the recomputed set sizes."""
+    time of raftgp_stream_add_edges for batches of B new random edges (one untimed batch, then the median of three,
+    each with fresh edges) against a full rebuild + embed of a graph with one batch added (raftgp_build_csr +
+    raftgp_embed_multi(ncut), median of two after an untimed one), in both stream modes: "exact" (Z bit-identical to the rebuild) and
+    "delta" (the last hop from stored sums plus the changed rows only; equal up to fp32 rounding order)."""
     import numpy as np
     import torch
     rng = np.random.default_rng(args.seed + 17)
     out = {"workload": f"C4 graph (N={gr.n:,}), NCut, dims {list(dims)}", "batches": []}
     ctx = rg.Context(dev.index)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+
+    def edges(B):
+        return (torch.from_numpy(rng.integers(0, gr.n, B).astype(np.int32)).to(dev),
+                torch.from_numpy(rng.integers(0, gr.n, B).astype(np.int32)).to(dev))
+
+    full = {}
     for B in (10, 1000):
-        g = rg.raftgp_build_csr(ctx, gr.n, src_d, dst_d)
-        stream = rg.Stream(g, dims, args.seed)
-        es = torch.from_numpy(rng.integers(0, gr.n, B).astype(np.int32)).to(dev)
-        ed = torch.from_numpy(rng.integers(0, gr.n, B).astype(np.int32)).to(dev)
-        barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(ctx.stream)
-        st = stream.add_edges(es, ed)
-        e1.record(ctx.stream)
-        barrier()
-        t_stream = e0.elapsed_time(e1)
-        stream.close()
+        es, ed = edges(B)
         s_all, d_all = torch.cat([src_d, es]), torch.cat([dst_d, ed])
         Z = {"ncut": torch.empty((gr.n, dims[-1]), dtype=torch.float32, device=dev)}
-        barrier()
-        e0.record(ctx.stream)
-        g2 = rg.raftgp_build_csr(ctx, gr.n, s_all, d_all)
-        rg.raftgp_embed_multi(g2, ["ncut"], dims, args.seed, Z=Z)
-        e1.record(ctx.stream)
-        barrier()
-        t_full = e0.elapsed_time(e1)
-        g2.close()
-        out["batches"].append({"new_edges": B, "stream_ms": t_stream, "full_rebuild_ms": t_full,
-                               "speedup": t_full / t_stream, "changed_nodes": st["changed"],
-                               "recomputed_rows": st["affected"]})
+        ts = []
+        for _ in range(3):   # the first (workspace growth, cold caches) untimed
+            barrier()
+            e0.record(ctx.stream)
+            g2 = rg.raftgp_build_csr(ctx, gr.n, s_all, d_all)
+            rg.raftgp_embed_multi(g2, ["ncut"], dims, args.seed, Z=Z)
+            e1.record(ctx.stream)
+            barrier()
+            ts.append(e0.elapsed_time(e1))
+            g2.close()
+        full[B] = float(np.median(ts[1:]))
+    for mode in ("exact", "delta"):
+        g = rg.raftgp_build_csr(ctx, gr.n, src_d, dst_d)
+        stream = rg.Stream(g, dims, args.seed)
+        if mode == "delta":
+            stream.set_mode("delta")
+        for B in (10, 1000):
+            ts, st = [], None
+            for rep in range(4):
+                es, ed = edges(B)
+                barrier()
+                e0.record(ctx.stream)
+                st = stream.add_edges(es, ed)
+                e1.record(ctx.stream)
+                barrier()
+                if rep:
+                    ts.append(e0.elapsed_time(e1))
+            t_stream = float(np.median(ts))
+            out["batches"].append({"mode": mode, "new_edges": B, "stream_ms": t_stream,
+                                   "ms_per_batch": [round(t, 3) for t in ts], "full_rebuild_ms": full[B],
+                                   "speedup": full[B] / t_stream, "changed_nodes": st["changed"],
+                                   "recomputed_rows": st["affected"]})
+        stream.close()
     return out
 
 

@@ -21,7 +21,7 @@ namespace raftgp {
 
 const char *const kKernelNames[K_NUM] = {
     "csr_count", "scan", "csr_scatter", "csr_sort_warp", "csr_sort_block", "csr_compact", "degree_scalars",
-    "sketch", "g_partials", "g_final", "feature_hop", "transform", "gcn_hop", "hop_generic", "misc", "csr_partition", "csr_bucket_sort", "row_order", "model_select", "select_seed", "select_lloyd", "select_split", "gemm_tf32x3", "gemm_tile", "wide_hop", "sbm_setup", "sbm_walk", "stream_update", "exchange", "push_copy", "csr_fine_part"};
+    "sketch", "g_partials", "g_final", "feature_hop", "transform", "gcn_hop", "hop_generic", "misc", "csr_partition", "csr_bucket_sort", "row_order", "model_select", "select_seed", "select_lloyd", "select_split", "gemm_tf32x3", "gemm_tile", "wide_hop", "sbm_setup", "sbm_walk", "stream_update", "exchange", "push_copy", "csr_fine_part", "stream_last_hop"};
 
 static thread_local std::string g_last_error;
 
@@ -1088,6 +1088,15 @@ raftgp_status raftgp_stream_graph(raftgp_stream s, raftgp_graph *g_out) {
     if (!s || !g_out) return fail(RAFTGP_ERR_PARAM, "null argument");
     *g_out = s->g;
     return RAFTGP_OK;
+}
+
+raftgp_status raftgp_stream_set_mode(raftgp_stream s, int32_t mode) {
+    RG_GUARD_BEGIN
+    if (!s) return fail(RAFTGP_ERR_PARAM, "null stream");
+    if (mode != RAFTGP_STREAM_EXACT && mode != RAFTGP_STREAM_DELTA) return fail(RAFTGP_ERR_PARAM, "unknown stream mode");
+    RG_TRY(set_device(s->ctx));
+    return stream_set_mode(s, mode);
+    RG_GUARD_END
 }
 
 raftgp_status raftgp_stream_destroy(raftgp_stream s) {

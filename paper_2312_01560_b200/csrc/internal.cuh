@@ -49,6 +49,7 @@ enum KernelId : int {
     K_EXCHANGE,     // NCCL collectives of the row-partitioned path (barrier, all-gathers; not counted as our launches)
     K_PUSH_COPY,    // deferred push of a finished operand block into the peers' copies (dist.cu)
     K_CSR_FINE,     // second level of the two-level CSR partition (csr.cu)
+    K_STREAM_LAST,  // the incrementally updated last GCN hop of a delta-mode stream (stream.cu)
     K_NUM
 };
 extern const char *const kKernelNames[K_NUM];
@@ -139,6 +140,9 @@ struct raftgp_stream_s {
     std::vector<float *> T;             // T[k], k = 1..layers (n x dims[k])
     std::vector<float *> W;             // W[k], k = 2..layers (dims[k-1] x dims[k])
     float *Z = nullptr;                 // n x dims[layers]
+    int32_t mode = 0;                   // RAFTGP_STREAM_EXACT / RAFTGP_STREAM_DELTA
+    float *A = nullptr;                 // delta mode: the last hop's pre-activation sums T_i + sum_j T_j (n x dims[L])
+    int32_t *pos = nullptr;             // delta mode: row -> index into this batch's dT (-1: T_L row unchanged)
 };
 
 namespace raftgp {
@@ -309,6 +313,7 @@ raftgp_status embed_wide(raftgp_graph g, int32_t nvariants, const int32_t *varia
 raftgp_status stream_create(raftgp_graph g, int32_t layers, const int32_t *dims, uint64_t seed, raftgp_stream *out);
 raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const int32_t *dst, int64_t *stats);
 void stream_destroy(raftgp_stream s);
+raftgp_status stream_set_mode(raftgp_stream s, int32_t mode);
 // NEXT-3: Alg. 2 exact SBM sampler (sbm.cu)
 raftgp_status sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K, const int32_t *c, const double *theta,
                          const double *omega, uint64_t seed, int32_t q, int32_t *src, int32_t *dst, int64_t cap,

@@ -16,6 +16,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "internal.cuh"
@@ -76,6 +77,10 @@ __global__ void merge_write(int64_t n, const int64_t *__restrict__ orp, const in
 // level k are appended to one list right after those of level k - 1, so R_k = V' u ... u N^k(V') is a PREFIX of
 // the list and the hops of step 3 read prefixes. Only frontier rows are visited (the round-1 version scanned all n
 // rows per level with a thread per row, so a hub's neighbour loop ran serially in one thread).
+__global__ void fill_value(int64_t n, int32_t *a, int32_t v) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = v;
+}
 __global__ void fill_level(int64_t n, int32_t *level) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         level[i] = 127;
@@ -354,9 +359,200 @@ __global__ void compact_rows(int64_t n, const int32_t *__restrict__ flag, const 
         if (flag[i]) out[pos[i]] = (int32_t)i;
 }
 
+// ---- delta mode (raftgp_stream_set_mode(RAFTGP_STREAM_DELTA)): the last GCN hop updated incrementally.
+// Eq. 6 as the hop kernels compute it: H_i = s^_i A_i with A_i = T_i + sum_{j in N(i)} T_j
+// (T = s^ (.) (Z W), T_j already carries s^_j). After a batch only the T_L rows of R_L changed (listed), and only
+// the rows of V' changed their neighbour list or s^_i. So for i outside V'
+//     A_i(new) = A_i(old) + sum_{j in (N(i) u {i}) n R_L} (T_j(new) - T_j(old)),
+// and the rows of V' are summed in full. The stream keeps A (n x d_L); the dT rows of R_L are tiny (L2-resident) and
+// a row gathers only its neighbours in R_L, found through pos[] (row -> dT index, -1 elsewhere). The last hop then
+// reads col_idx once instead of gathering one operand row per entry. Exact up to fp32 rounding order (the sums are
+// re-associated), not bit-identical: the exact mode stays the default.
+__global__ void delta_save(const int32_t *__restrict__ rows, int64_t cnt, const float4 *__restrict__ T, int lpn,
+                           int32_t *__restrict__ pos, float4 *__restrict__ dT) {
+    const int64_t tot = cnt * lpn;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t idx = t / lpn;
+        const int c = (int)(t - idx * lpn);
+        const int64_t r = rows[idx];
+        dT[t] = T[r * lpn + c];
+        if (c == 0) pos[r] = (int32_t)idx;
+    }
+}
+
+__global__ void delta_finish(const int32_t *__restrict__ rows, int64_t cnt, const float4 *__restrict__ T, int lpn,
+                             float4 *__restrict__ dT) {
+    const int64_t tot = cnt * lpn;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t idx = t / lpn;
+        const float4 nw = T[(int64_t)rows[idx] * lpn + (t - idx * lpn)], od = dT[t];
+        dT[t] = make_float4(nw.x - od.x, nw.y - od.y, nw.z - od.z, nw.w - od.w);
+    }
+}
+
+__global__ void delta_clear(const int32_t *__restrict__ rows, int64_t cnt, int32_t *__restrict__ pos) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += (int64_t)gridDim.x * blockDim.x)
+        pos[rows[t]] = -1;
+}
+
+__device__ __forceinline__ void add4s(float4 &a, const float4 &v) {
+    a.x += v.x;
+    a.y += v.y;
+    a.z += v.z;
+    a.w += v.w;
+}
+
+// warp per row, rows claimed kDeltaRows at a time in the graph's visiting order. all_full = 1: every row summed in full
+// (state build / resync); otherwise the rows of V' (level 0) in full and the rest by their changed neighbours. Rows
+// with no changed neighbour (and an unchanged own T row) are not written.
+constexpr int kDeltaRows = 4;
+#ifndef RG_HIT_SLOTS
+#define RG_HIT_SLOTS 4
+#endif
+constexpr int kHitSlots = RG_HIT_SLOTS;   // dT loads in flight per lane in the delta pass
+template <int W>
+__global__ void __launch_bounds__(256, 8) last_hop_delta(int64_t n, const int64_t *__restrict__ rp,
+                                                      const int32_t *__restrict__ col, const int32_t *__restrict__ order,
+                                                      const float *__restrict__ T, const int32_t *__restrict__ pos,
+                                                      const float *__restrict__ dT, const int32_t *__restrict__ level,
+                                                      const float *__restrict__ sh, float *__restrict__ A,
+                                                      float *__restrict__ Z, int all_full,
+                                                      unsigned long long *__restrict__ ctr,
+                                                      unsigned long long *__restrict__ touched) {
+    constexpr int LPN = W / 4, NB = 32 / LPN;
+    const unsigned FULLM = 0xffffffffu;
+    __shared__ int32_t hitq[8][32];   // per warp: the dT indices of a chunk's changed neighbours, compacted
+    const int lane = threadIdx.x & 31, sub = lane / LPN, cl = lane % LPN;
+    int32_t *q = hitq[threadIdx.x >> 5];
+    const float4 *T4 = reinterpret_cast<const float4 *>(T);
+    const float4 *D4 = reinterpret_cast<const float4 *>(dT);
+    unsigned long long mine = 0;
+    for (;;) {
+        unsigned long long g0 = 0;
+        if (lane == 0) g0 = atomicAdd(ctr, (unsigned long long)kDeltaRows);
+        const int64_t q0 = (int64_t)__shfl_sync(FULLM, g0, 0);
+        if (q0 >= n) break;
+        const int64_t q1 = min(n, q0 + kDeltaRows);
+        for (int64_t qq = q0; qq < q1; ++qq) {
+            const int64_t i = order ? (int64_t)order[qq] : qq;
+            const bool full = all_full || level[i] == 0;
+            const int64_t b = rp[i], e = rp[i + 1];
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f), ao = acc;
+            bool any = full;
+            if (full) {
+                for (int64_t p0 = b; p0 < e; p0 += 32) {
+                    const int cnt = (int)(e - p0 < 32 ? e - p0 : 32);
+                    const int32_t c = lane < cnt ? __ldg(col + p0 + lane) : 0;
+#pragma unroll 4
+                    for (int t = 0; t < 32; t += NB) {
+                        if (t >= cnt) break;
+                        const int k = t + sub;
+                        const int32_t j = __shfl_sync(FULLM, c, k);
+                        if (k < cnt) add4s(acc, __ldg(T4 + (int64_t)j * LPN + cl));
+                    }
+                }
+            } else {
+                ao = reinterpret_cast<const float4 *>(A)[i * LPN + cl];   // issued before the neighbour walk
+                for (int64_t p0 = b; p0 < e; p0 += 32) {
+                    const int64_t p = p0 + lane;
+                    const int32_t pj = p < e ? __ldg(pos + __ldg(col + p)) : -1;
+                    const unsigned hits = __ballot_sync(FULLM, pj >= 0);
+                    if (!hits) continue;
+                    any = true;
+                    if (pj >= 0) q[__popc(hits & ((1u << lane) - 1u))] = pj;
+                    __syncwarp();
+                    const int nh = __popc(hits);
+                    for (int t = 0; t < nh; t += kHitSlots * NB) {   // kHitSlots loads in flight per lane
+                        float4 v[kHitSlots];
+#pragma unroll
+                        for (int h = 0; h < kHitSlots; ++h) {
+                            const int x = t + h * NB + sub;
+                            v[h] = x < nh ? __ldg(D4 + (int64_t)q[x] * LPN + cl) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
+#pragma unroll
+                        for (int h = 0; h < kHitSlots; ++h) add4s(acc, v[h]);
+                    }
+                    __syncwarp();
+                }
+            }
+#pragma unroll
+            for (int o = LPN; o < 32; o <<= 1) {
+                acc.x += __shfl_xor_sync(FULLM, acc.x, o);
+                acc.y += __shfl_xor_sync(FULLM, acc.y, o);
+                acc.z += __shfl_xor_sync(FULLM, acc.z, o);
+                acc.w += __shfl_xor_sync(FULLM, acc.w, o);
+            }
+            if (full) {
+                add4s(acc, __ldg(T4 + i * LPN + cl));   // the self term (A + I)
+            } else {
+                const int32_t pi = __ldg(pos + i);
+                if (pi >= 0) {
+                    add4s(acc, __ldg(D4 + (int64_t)pi * LPN + cl));
+                    any = true;
+                }
+                if (!any) continue;
+                acc = make_float4(ao.x + acc.x, ao.y + acc.y, ao.z + acc.z, ao.w + acc.w);
+            }
+            const float s = __ldg(sh + i);
+            float4 y = make_float4(tanhf(s * acc.x), tanhf(s * acc.y), tanhf(s * acc.z), tanhf(s * acc.w));
+            float ss = y.x * y.x + y.y * y.y + y.z * y.z + y.w * y.w;
+#pragma unroll
+            for (int o = 1; o < LPN; o <<= 1) ss += __shfl_xor_sync(FULLM, ss, o);
+            if (ss > 0.f) {   // one reciprocal square root (this mode is not bit-identical to the hop kernels anyway)
+                const float inv = rsqrtf(ss);
+                y = make_float4(y.x * inv, y.y * inv, y.z * inv, y.w * inv);
+            }
+            if (sub == 0) {
+                reinterpret_cast<float4 *>(A)[i * LPN + cl] = acc;
+                reinterpret_cast<float4 *>(Z)[i * LPN + cl] = y;
+            }
+            ++mine;
+        }
+    }
+    if (lane == 0 && mine) atomicAdd(touched, mine);
+}
+
 inline unsigned g256(int64_t n) { return (unsigned)std::max<int64_t>(1, ceil_div(n, 256)); }
 
 bool fast_width(int32_t w) { return w == 32 || w == 64 || w == 128; }
+
+// the delta-mode last hop over every row (all_full = 1: the state build / resync; 0: a batch's update)
+raftgp_status launch_last_delta(raftgp_stream s, raftgp_graph g, const int32_t *level, const float *dT, int all_full,
+                                int64_t *touched_out) {
+    raftgp_ctx ctx = g->ctx;
+    const int64_t n = g->n;
+    if (n == 0) {
+        if (touched_out) *touched_out = 0;
+        return RAFTGP_OK;
+    }
+    const int d = s->dims[s->layers];
+    unsigned long long *ctr = nullptr;
+    RG_TRY(dalloc_t(ctx, &ctr, 2));
+    raftgp_status rc = dzero(ctx, ctr, 2 * sizeof(unsigned long long));
+    if (rc == RAFTGP_OK) {
+        const unsigned grid = (unsigned)std::max<int64_t>(
+            1, std::min<int64_t>(ceil_div(ceil_div(n, kDeltaRows), 8), (int64_t)ctx->sm_count * 8));
+        LaunchScope LS(ctx, K_STREAM_LAST);
+        const char *ne = getenv("RAFTGP_DELTA_NAT");
+        const bool nat = !all_full && ne && ne[0] == '1';
+        auto go = [&](auto kern) {
+            kern<<<grid, 256, 0, ctx->stream>>>(n, g->row_ptr, g->col, nat ? nullptr : g->order, s->T[s->layers], s->pos, dT, level,
+                                                g->sh_all, s->A, s->Z, all_full, ctr, ctr + 1);
+        };
+        if (d == 32) go(last_hop_delta<32>);
+        else if (d == 64) go(last_hop_delta<64>);
+        else go(last_hop_delta<128>);
+    }
+    if (rc == RAFTGP_OK) {
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) rc = cuda_fail(e, "kernel launch");
+    }
+    unsigned long long t = 0;
+    if (rc == RAFTGP_OK && touched_out) rc = dread(ctx, &t, ctr + 1, sizeof(t), ctx->stream);
+    if (touched_out) *touched_out = (int64_t)t;
+    dfree(ctx, ctr);
+    return rc;
+}
 
 }  // namespace
 
@@ -552,7 +748,25 @@ raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const i
         const char *e = getenv("RAFTGP_STREAM_FULL_LAST");
         return e ? atoi(e) : -1;
     }();
+    const bool delta_mode = s->mode == RAFTGP_STREAM_DELTA;
+    float *dT = nullptr;   // delta mode: T_L(new) - T_L(old) for the rows of R_L (list order)
     for (int k = 1; k <= L + 1 && rc == RAFTGP_OK; ++k) {
+        if (k == L + 1 && delta_mode) {   // the last hop by its changed inputs only (no level L + 1 expansion)
+            if (counts[0] > 0) {
+                int32_t *own = ng->order;
+                if (!own && g->nl == ng->nl) ng->order = g->order;
+                int64_t touched = 0;
+                rc = launch_last_delta(s, ng, level, dT, dT ? 0 : 1, &touched);
+                ng->order = own;
+                counts[k] = touched;   // rows whose Z was rewritten
+                if (rc == RAFTGP_OK && dT) {
+                    LaunchScope LS(ctx, K_STREAM);
+                    delta_clear<<<(unsigned)std::min<int64_t>(g256(counts[L]), (int64_t)ctx->sm_count * 8), 256, 0, st>>>(
+                        rows, counts[L], s->pos);
+                }
+            }
+            break;
+        }
         if (k == L + 1 && fc > 0 && full_last_env != 0) {
             bool full = full_last_env == 1;
             if (!full) {
@@ -618,6 +832,20 @@ raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const i
             dfree(ctx, pos);
         }
         if (rc == RAFTGP_OK) rc = spread_heavy_list(ctx, list, counts[k], ng->deg_local, hop_rows);
+        const int lpn = s->dims[L] / 4;
+        // keep T_L(old) of the rows about to change; when R_L holds 1/8 of the rows or more, the changed rows' gathers
+        // would cost as much as a full pass: the last hop then sums every row in full (A rebuilt, no dT)
+        // (RAFTGP_STREAM_DELTA_FRAC = f: the full pass when |R_L| * f >= n, default 8; 0: never)
+        const char *fe = getenv("RAFTGP_STREAM_DELTA_FRAC");
+        const int64_t frac = fe ? atoll(fe) : 8;
+        if (rc == RAFTGP_OK && delta_mode && k == L && counts[k] > 0 && (frac <= 0 || counts[k] * frac < n)) {
+            rc = dalloc_t(ctx, &dT, (size_t)counts[k] * s->dims[L]);
+            if (rc == RAFTGP_OK) {
+                LaunchScope LS(ctx, K_STREAM);
+                delta_save<<<(unsigned)std::min<int64_t>(g256(counts[k] * lpn), (int64_t)ctx->sm_count * 8), 256, 0, st>>>(
+                    rows, counts[k], reinterpret_cast<const float4 *>(s->T[L]), lpn, s->pos, reinterpret_cast<float4 *>(dT));
+            }
+        }
         if (rc != RAFTGP_OK) break;
         if (k == 1) {
             rc = feature_hop_pre_rows(ng, RAFTGP_NCUT, d[1], s->thw, nullptr, s->T[1], hop_rows, counts[1]);
@@ -627,7 +855,13 @@ raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const i
             rc = gcn_hop_rows(ng, s->T[h], d[h], last ? s->Z : nullptr, last ? nullptr : s->W[h + 1],
                               last ? 0 : d[h + 1], last ? nullptr : s->T[h + 1], hop_rows, counts[k]);
         }
+        if (rc == RAFTGP_OK && dT && k == L) {
+            LaunchScope LS(ctx, K_STREAM);
+            delta_finish<<<(unsigned)std::min<int64_t>(g256(counts[k] * lpn), (int64_t)ctx->sm_count * 8), 256, 0, st>>>(
+                rows, counts[k], reinterpret_cast<const float4 *>(s->T[L]), lpn, reinterpret_cast<float4 *>(dT));
+        }
     }
+    dfree(ctx, dT);
     dfree(ctx, add); dfree(ctx, level); dfree(ctx, rows); dfree(ctx, cnt); dfree(ctx, hop_rows); dfree(ctx, nat_rows);
     if (rc != RAFTGP_OK) {
         drop(*ng);
@@ -657,6 +891,8 @@ void stream_destroy(raftgp_stream s) {
     for (auto t : s->T) dfree(ctx, t);
     for (auto w : s->W) dfree(ctx, w);
     dfree(ctx, s->Z);
+    dfree(ctx, s->A);
+    dfree(ctx, s->pos);
     if (s->g) {
         raftgp_graph_s &x = *s->g;
         dfree(ctx, x.row_ptr); dfree(ctx, x.col); dfree(ctx, x.deg_local); dfree(ctx, x.order); dfree(ctx, x.deg_all);
@@ -666,6 +902,35 @@ void stream_destroy(raftgp_stream s) {
     }
     delete s;
     ctx_release(ctx);
+}
+
+// RAFTGP_STREAM_DELTA: the state A of the last hop (and pos = -1) is built by a full pass that also rewrites Z (each call
+// is therefore a resync); RAFTGP_STREAM_EXACT drops it and recomputes Z with the exact hop kernel (bit-identical to
+// raftgp_embed again)
+raftgp_status stream_set_mode(raftgp_stream s, int32_t mode) {
+    raftgp_graph g = s->g;
+    raftgp_ctx ctx = s->ctx;
+    const int64_t n = g->n;
+    const int L = s->layers, d = s->dims[L];
+    if (mode == RAFTGP_STREAM_DELTA) {
+        if (!s->A) RG_TRY(dalloc_t(ctx, &s->A, (size_t)std::max<int64_t>(1, n) * d));
+        if (!s->pos) RG_TRY(dalloc_t(ctx, &s->pos, (size_t)std::max<int64_t>(1, n)));
+        if (n > 0) {
+            LaunchScope LS(ctx, K_STREAM);
+            fill_value<<<(unsigned)std::min<int64_t>(g256(n), (int64_t)ctx->sm_count * 8), 256, 0, ctx->stream>>>(n, s->pos,
+                                                                                                                -1);
+        }
+        RG_CHECK_LAUNCH(ctx);
+        RG_TRY(launch_last_delta(s, g, nullptr, nullptr, 1, nullptr));
+        s->mode = mode;
+        return RAFTGP_OK;
+    }
+    dfree(ctx, s->A);
+    dfree(ctx, s->pos);
+    s->A = nullptr;
+    s->pos = nullptr;
+    s->mode = RAFTGP_STREAM_EXACT;
+    return gcn_hop(g, s->T[L], d, s->Z, nullptr, 0, nullptr, 0, nullptr);
 }
 
 }  // namespace raftgp

@@ -37,6 +37,7 @@ EXPORTS = (
     "raftgp_embed", "raftgp_embed_multi", "raftgp_feature_transform", "raftgp_modularity", "raftgp_ncut", "raftgp_local_modularity",
     "raftgp_model_select", "raftgp_gemm_tf32x3", "raftgp_sbm_sample", "raftgp_stream_create",
     "raftgp_stream_add_edges", "raftgp_stream_embedding", "raftgp_stream_graph", "raftgp_stream_destroy",
+    "raftgp_stream_set_mode",
     "raftgp_build_embed", "raftgp_ctx_trim", "raftgp_feature_transform_push", "raftgp_gcn_hop_push",
     "raftgp_ipc_alloc", "raftgp_ipc_free", "raftgp_ipc_open", "raftgp_ipc_close", "raftgp_copy",
     "raftgp_nccl_unique_id", "raftgp_ctx_create_dist", "raftgp_ctx_rank", "raftgp_barrier", "raftgp_allgather",
@@ -106,6 +107,7 @@ _SIGS = {
     "raftgp_stream_embedding": (ctypes.c_int, [c_vp, c_vp]),
     "raftgp_stream_graph": (ctypes.c_int, [c_vp, P(c_vp)]),
     "raftgp_stream_destroy": (ctypes.c_int, [c_vp]),
+    "raftgp_stream_set_mode": (ctypes.c_int, [c_vp, c_i32]),
     "raftgp_build_embed": (ctypes.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_u32, c_i32, c_vp, c_i32, c_vp, c_u64, c_vp,
                                           P(c_vp)]),
     "raftgp_build_embed_loopback": (ctypes.c_int, [c_vp, c_i32, c_i64, c_i64, c_vp, c_vp, c_u32, c_i32, c_vp, c_i32, c_vp,
@@ -699,6 +701,13 @@ class Stream:
         s, d = _own(src, self.ctx.stream), _own(dst, self.ctx.stream)
         _ck(load_library().raftgp_stream_add_edges(self.h, s.numel(), _ptr(s), _ptr(d), flags, c_vp(st.ctypes.data)))
         return {"changed": int(st[0]), "affected": [int(x) for x in st[1:L + 2]], "nnz": int(st[L + 2])}
+
+    MODES = {"exact": 0, "delta": 1}
+
+    def set_mode(self, mode: str) -> None:
+        """raftgp_stream_set_mode: "exact" (bit-identical last hop, the default) or "delta" (the last hop updated by
+        the changed rows only; setting it again resyncs)."""
+        _ck(load_library().raftgp_stream_set_mode(self.h, self.MODES[mode]))
 
     def embedding(self) -> torch.Tensor:
         n = self.graph().n

@@ -164,3 +164,110 @@ def test_stream_last_hop_listed_or_full(rg, mode):
     r = subprocess.run([sys.executable, "-c", _LAST_SCRIPT], cwd=root,
                        env=dict(os.environ, RAFTGP_STREAM_FULL_LAST=mode), capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+# ---------------------------------------------------------------- delta mode (raftgp_stream_set_mode)
+def _delta_case(rg, ctx, cfg, n, dims, batches, per_batch, seed):
+    gr = synth.generate(cfg, seed, n=n)
+    rng = np.random.default_rng(seed + 100)
+    m = gr.src.size
+    held = rng.choice(m, size=min(m // 50, batches * per_batch), replace=False)
+    keep = np.setdiff1d(np.arange(m), held)
+    return gr, gr.src[keep], gr.dst[keep], np.array_split(gr.src[held], batches), np.array_split(gr.dst[held], batches)
+
+
+@pytest.mark.parametrize("cfg,n,dims,batches", [("C1", None, (64, 64, 32), 3), ("C2", 20000, (64, 64, 32), 2),
+                                                ("C1", None, (128, 64, 32, 32), 2), ("C1", None, (64, 128), 2),
+                                                ("C1", None, (32, 64, 128), 2)])
+@pytest.mark.parametrize("frac", ["0", "8"])
+def test_stream_delta_matches_exact(rg, ctx, cfg, n, dims, batches, frac, monkeypatch):
+    """Delta mode: the last hop from the stored sums A_i plus the changed rows of T_L only. Every batch: Z within
+    fp32 re-association error of the exact stream (itself bit-identical to a fresh embed), rows outside the closure
+    R_{L+1} bit-identical, the rewritten-row count equal to |R_{L+1}| (row i is rewritten iff i or a neighbour is in
+    R_L), and the oracle within 1e-4 at the end. frac = "0": always the delta pass; "8" (default): the full pass when
+    R_L holds 1/8 of the rows or more (every row rewritten)."""
+    monkeypatch.setenv("RAFTGP_STREAM_DELTA_FRAC", frac)
+    gr, s0, d0, bs, bd = _delta_case(rg, ctx, cfg, n, dims, batches, 60, 6)
+    ex = rg.Stream(rg.raftgp_build_csr(ctx, gr.n, _t(s0), _t(d0)), dims, 7)
+    de = rg.Stream(rg.raftgp_build_csr(ctx, gr.n, _t(s0), _t(d0)), dims, 7)
+    de.set_mode("delta")
+    e0 = (de.embedding() - ex.embedding()).abs().max().item()
+    assert e0 <= 2e-6, e0   # the state build's own summation order
+    cur_s, cur_d = s0, d0
+    L = len(dims) - 1
+    for ps, pd in zip(bs, bd):
+        Zprev = de.embedding().clone()
+        st_e = ex.add_edges(_t(ps), _t(pd))
+        st_d = de.add_edges(_t(ps), _t(pd))
+        gb = oracle.build_csr(gr.n, cur_s, cur_d)
+        cur_s, cur_d = np.concatenate([cur_s, ps]), np.concatenate([cur_d, pd])
+        go = oracle.build_csr(gr.n, cur_s, cur_d)
+        changed = go.deg != gb.deg
+        clo = _closures(gr.n, cur_s, cur_d, changed, L)
+        assert st_d["changed"] == st_e["changed"] == int(changed.sum())
+        full_pass = frac != "0" and clo[L - 1] * int(frac) >= gr.n
+        assert st_d["affected"][:-1] == clo[:-1], (st_d, clo)
+        assert st_d["affected"][-1] == (gr.n if full_pass else clo[-1]), (st_d, clo)
+        Ze, Zd = ex.embedding(), de.embedding()
+        diff = (Zd - Ze).abs().max().item()
+        rel = ((Zd - Ze).norm() / Ze.norm()).item()
+        assert diff <= 5e-6 and rel <= 2e-6, (diff, rel)
+        # rows outside R_{L+1} are not rewritten
+        a = sp.coo_matrix((np.ones(cur_s.size), (cur_s, cur_d)), shape=(gr.n, gr.n)).tocsr()
+        a = ((a + a.T) > 0).astype(np.int8)
+        cl = changed.copy()
+        for _ in range(L + 1):
+            cl = cl | (a @ cl.astype(np.int8) > 0)
+        out = torch.from_numpy(~cl).cuda()
+        if not full_pass:
+            assert torch.equal(Zd[out], Zprev[out])
+        elif int(out.sum()) > 0:
+            assert (Zd[out] - Zprev[out]).abs().max().item() <= 2e-6
+    Zo = oracle.gcn(go, list(dims), 7, oracle.project(go, "ncut", dims[0], 7))[-1]
+    e = np.linalg.norm(de.embedding().cpu().numpy() - Zo) / np.linalg.norm(Zo)
+    assert e <= 1e-4
+
+
+def test_stream_delta_drift_resync_and_exact(rg, ctx, monkeypatch):
+    """40 small batches in delta mode stay within 1e-5 of a fresh embed; set_mode("delta") again resyncs (a full
+    pass); set_mode("exact") recomputes Z bit-identically to raftgp_embed; no-op batches change nothing."""
+    monkeypatch.setenv("RAFTGP_STREAM_DELTA_FRAC", "0")
+    dims = (64, 64, 32)
+    gr, s0, d0, bs, bd = _delta_case(rg, ctx, "C1", None, dims, 40, 5, 11)
+    de = rg.Stream(rg.raftgp_build_csr(ctx, gr.n, _t(s0), _t(d0)), dims, 2)
+    de.set_mode("delta")
+    Z0 = de.embedding().clone()
+    for st in (de.add_edges(_t(s0[:20]), _t(d0[:20])), de.add_edges(_t(np.arange(5)), _t(np.arange(5))),
+               de.add_edges(_t(np.zeros(0)), _t(np.zeros(0)))):
+        assert st["changed"] == 0 and st["affected"][-1] == 0
+    assert torch.equal(de.embedding(), Z0)
+    cur_s, cur_d = s0, d0
+    for ps, pd in zip(bs, bd):
+        de.add_edges(_t(ps), _t(pd))
+        cur_s, cur_d = np.concatenate([cur_s, ps]), np.concatenate([cur_d, pd])
+    fresh = _fresh_ncut(rg, ctx, gr.n, cur_s, cur_d, dims, 2)
+    Zd = de.embedding()
+    assert ((Zd - fresh).norm() / fresh.norm()).item() <= 1e-5
+    de.set_mode("delta")
+    assert (de.embedding() - fresh).abs().max().item() <= 2e-6
+    de.set_mode("exact")
+    assert torch.equal(de.embedding(), fresh)
+    st = de.add_edges(_t([0, 3]), _t([500, 900]))   # exact again: bit-identical
+    fresh2 = _fresh_ncut(rg, ctx, gr.n, np.concatenate([cur_s, [0, 3]]), np.concatenate([cur_d, [500, 900]]), dims, 2)
+    assert torch.equal(de.embedding(), fresh2), st
+
+
+def test_stream_delta_large_batch_and_errors(rg, ctx):
+    """A batch above the one-CTA delta sort (> 2048 pairs: the CSR-build merge path) in delta mode, and a bad mode."""
+    dims = (64, 64, 32)
+    gr, s0, d0, bs, bd = _delta_case(rg, ctx, "C2", 20000, dims, 1, 3000, 12)
+    ex = rg.Stream(rg.raftgp_build_csr(ctx, gr.n, _t(s0), _t(d0)), dims, 4)
+    de = rg.Stream(rg.raftgp_build_csr(ctx, gr.n, _t(s0), _t(d0)), dims, 4)
+    de.set_mode("delta")
+    ex.add_edges(_t(bs[0]), _t(bd[0]))
+    de.add_edges(_t(bs[0]), _t(bd[0]))
+    Ze = ex.embedding()
+    assert ((de.embedding() - Ze).norm() / Ze.norm()).item() <= 2e-6
+    with pytest.raises(rg.RaftGPError) as e:
+        rg._ck(rg.load_library().raftgp_stream_set_mode(de.h, 7))
+    assert e.value.code == rg.RAFTGP_ERR_PARAM
