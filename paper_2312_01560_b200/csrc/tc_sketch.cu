@@ -33,6 +33,10 @@ using namespace tc;
 #ifndef RG_TC_THREADS
 #define RG_TC_THREADS 512   // 16 warps, 2 independent Philox quads per thread per quarter (1024 / 256: 2.37 / 2.33 ms vs 2.21 at C4)
 #endif
+#ifndef RG_TC_MMA_WARP
+#define RG_TC_MMA_WARP 1   // 1: a 17th warp only issues the MMAs (0: warp 0's lane 0 issues them between its own quarters)
+#endif
+constexpr int kTcBlock = RG_TC_THREADS + (RG_TC_MMA_WARP ? 32 : 0);
 constexpr int kTM = 128;       // rows per tile (MMA M)
 constexpr int kKQ = 32;        // K columns per quarter (one of two A buffers)
 #ifndef RG_TC_DRAIN_SPREAD
@@ -77,7 +81,7 @@ struct TcCfg {
 // No block-wide barrier inside the loop: the warps only meet at the ring's mbarriers, so generation is never held
 // up by the MMA issue or the drain (the round-1 version's per-quarter __syncthreads was its largest stall).
 template <int R, int L1>
-__global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t seed, int64_t row0, int64_t n, float sigma,
+__global__ void __launch_bounds__(kTcBlock, 1) sketch_w_tc_kernel(uint64_t seed, int64_t row0, int64_t n, float sigma,
                                                              const float *__restrict__ W1, SketchOut outs) {
     using C = TcCfg<R, L1>;
     constexpr int KQ = C::KQ, NQK = C::NQK, NCOL = C::NCOL, NS = C::NS;
@@ -167,10 +171,48 @@ __global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t 
         }
     };
 
+    // the MMAs of quarter q of local tile it (ring stage st, quarter counter g): one thread
+    auto issue = [&](int64_t it, int q, int64_t g, int st) {
+        const int acc = (int)(it & 1);
+        unsigned char *a_hi = a_base + (size_t)st * 2 * A_BYTES;
+        unsigned char *a_lo = a_hi + A_BYTES;
+        if (q == 0 && it >= 2) mbar_wait(&acce[acc], (uint32_t)(((it - 2) >> 1) & 1));   // drained
+        mbar_wait(&full[st], (uint32_t)((g / NS) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo);
+        const uint32_t bh = smem_u32(b_hi), bl = smem_u32(b_lo);
+        constexpr uint32_t A_LBO = (kTM / 8) * 128, B_LBO = (L1 / 8) * 128, SBO = 128;
+        const uint32_t dacc = tmem_d + (uint32_t)(acc * NCOL);
+#pragma unroll
+        for (int s8 = 0; s8 < KQ / 8; ++s8) {
+            const uint32_t aoff = s8 * 2 * A_LBO;
+            const uint32_t boff = (q * (KQ / 8) + s8) * 2 * B_LBO;
+            const uint64_t dah = smem_desc(ah + aoff, A_LBO, SBO), dal = smem_desc(al + aoff, A_LBO, SBO);
+            const uint64_t dbh = smem_desc(bh + boff, B_LBO, SBO), dbl = smem_desc(bl + boff, B_LBO, SBO);
+            const uint32_t acc0 = (q > 0 || s8 > 0) ? 1u : 0u;
+            mma_tf32(dacc, dah, dbh, IDESC, acc0);
+            mma_tf32(dacc, dah, dbl, IDESC, 1u);
+            mma_tf32(dacc, dal, dbh, IDESC, 1u);
+        }
+        mma_commit(&empty[st]);
+        if (q == NQK - 1) mma_commit(&accf[acc]);
+    };
+
     const int64_t ntiles = (n + kTM - 1) / kTM;
+    if (RG_TC_MMA_WARP && warp == NW) {   // the MMA warp: issue every quarter as soon as its stage is complete
+        if (lane == 0) {
+            int64_t itm = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++itm)
+                for (int q = 0; q < NQK; ++q) {
+                    const int64_t g = itm * NQK + q;
+                    issue(itm, q, g, (int)(g % NS));
+                }
+        }
+        __syncwarp();
+    }
     const PhiloxKeys keys = philox_keys(seed);
     int64_t it = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    for (int64_t tile = (RG_TC_MMA_WARP && warp == NW) ? ntiles : blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int64_t r0 = tile * kTM;
         const int acc = (int)(it & 1);
         for (int q = 0; q < NQK; ++q) {
@@ -196,35 +238,14 @@ __global__ void __launch_bounds__(RG_TC_THREADS, 1) sketch_w_tc_kernel(uint64_t 
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic stores -> async proxy (MMA)
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[st]);
-            if (warp == 0) {
-                if (lane == 0) {
-                    if (q == 0 && it >= 2) mbar_wait(&acce[acc], (uint32_t)(((it - 2) >> 1) & 1));   // drained
-                    mbar_wait(&full[st], (uint32_t)((g / NS) & 1));
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo);
-                    const uint32_t bh = smem_u32(b_hi), bl = smem_u32(b_lo);
-                    constexpr uint32_t A_LBO = (kTM / 8) * 128, B_LBO = (L1 / 8) * 128, SBO = 128;
-                    const uint32_t dacc = tmem_d + (uint32_t)(acc * NCOL);
-#pragma unroll
-                    for (int s8 = 0; s8 < KQ / 8; ++s8) {
-                        const uint32_t aoff = s8 * 2 * A_LBO;
-                        const uint32_t boff = (q * (KQ / 8) + s8) * 2 * B_LBO;
-                        const uint64_t dah = smem_desc(ah + aoff, A_LBO, SBO), dal = smem_desc(al + aoff, A_LBO, SBO);
-                        const uint64_t dbh = smem_desc(bh + boff, B_LBO, SBO), dbl = smem_desc(bl + boff, B_LBO, SBO);
-                        const uint32_t acc0 = (q > 0 || s8 > 0) ? 1u : 0u;
-                        mma_tf32(dacc, dah, dbh, IDESC, acc0);
-                        mma_tf32(dacc, dah, dbl, IDESC, 1u);
-                        mma_tf32(dacc, dal, dbh, IDESC, 1u);
-                    }
-                    mma_commit(&empty[st]);
-                    if (q == NQK - 1) mma_commit(&accf[acc]);
-                }
+            if (!RG_TC_MMA_WARP && warp == 0) {
+                if (lane == 0) issue(it, q, g, st);
                 __syncwarp();
             }
-            if (warp >= EPI0 && it >= 1) drain(it - 1, tile - gridDim.x, q);
+            if (warp >= EPI0 && warp < NW && it >= 1) drain(it - 1, tile - gridDim.x, q);
         }
     }
-    if (warp >= EPI0 && it >= 1)
+    if (warp >= EPI0 && warp < NW && it >= 1)
         for (int q = 0; q < NQK; ++q) drain(it - 1, (int64_t)blockIdx.x + (it - 1) * gridDim.x, q);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -252,7 +273,7 @@ raftgp_status launch_tc(raftgp_ctx ctx, uint64_t seed, int64_t row0, int64_t n, 
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kTM), want)));
     {
         LaunchScope L(ctx, K_SKETCH);
-        sketch_w_tc_kernel<R, L1><<<grid, RG_TC_THREADS, smem, ctx->stream>>>(seed, row0, n, sigma, W1, outs);
+        sketch_w_tc_kernel<R, L1><<<grid, kTcBlock, smem, ctx->stream>>>(seed, row0, n, sigma, W1, outs);
     }
     RG_CHECK_LAUNCH(ctx);
     return RAFTGP_OK;
