@@ -281,10 +281,11 @@ RAFTGP_API raftgp_status raftgp_local_modularity(raftgp_graph g, const int64_t *
  *   rule: RAFTGP_LMOD_GLOBAL (2e = 2|E|: m_1 > m_2 iff splitting U lowers the modularity of G, PAPER.md:203;
  *         DESIGN.md reading #28) or RAFTGP_LMOD_LOCAL (2e = total degree of U, PAPER.md:167 as printed).
  *   labels_dev: device int32[n] out: block of every node, blocks numbered 0..K-1 by their smallest member.
- *   num_blocks: host out, K.  stats: host int64[7] out or NULL: {blocks, splits, Lloyd iterations summed
+ *   num_blocks: host out, K.  stats: host int64[9] out or NULL: {blocks, splits, Lloyd iterations summed
  *          over levels (lock-step), levels, rows visited by Lloyd passes (rows of unconverged segments),
  *          rows per seeding pass summed over levels, Z rows read by Lloyd passes (the others are skipped
- *          by exact distance bounds)}.
+ *          by exact distance bounds), segments whose Lloyd iterations stopped at max_iter without converging
+ *          (summed over levels; the convergence diagnostic), their rows}.
  * Whole-graph handle only. Synchronous (the host drives the levels). Workspace from the context pool.
  * Errors: PARAM (L, eps, max_iter, rule, null/misaligned pointers, partial graph), DATA (|z| > 1 or NaN),
  * STATE, NOMEM, CUDA. */

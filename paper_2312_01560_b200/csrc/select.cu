@@ -524,7 +524,13 @@ __global__ void sel_update(SegState st, int S, int t, int max_iter, const int32_
         __syncwarp();
     }
     if ((t > 1 && st.changed[s] == 0) || t >= max_iter) {
-        if (lane == 0) st.done[s] = 1;
+        if (lane == 0) {
+            st.done[s] = 1;
+            if (t >= max_iter && (t == 1 || st.changed[s] != 0)) {   // stopped by the cap, not converged: counted
+                atomicAdd(active, 1ull);                                 // into iteration max_iter's counters
+                atomicAdd(active + 1, (unsigned long long)(seg_off[s + 1] - seg_off[s]));
+            }
+        }
         return;
     }
     const unsigned long long n0 = st.cnt[s * 2], n1 = st.cnt[s * 2 + 1];
@@ -836,6 +842,7 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
 
     int32_t blocks = 0;
     int64_t splits = 0, lloyd_iters = 0, levels = 0, lloyd_rows = 0, seed_rows = 0, act_rows = 0;
+    int64_t capped_segs = 0, capped_rows = 0;
     int32_t h_small[2] = {0, 0};
     std::vector<unsigned long long> h_iter(2 * ((size_t)max_iter + 1), 0);
     unsigned long long *iter_act = nullptr;   // [t][2]: active segments / rows after update t
@@ -960,6 +967,10 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
                 lloyd_rows += act_rows;
                 act_rows = (int64_t)h_iter[2 * t + 1];
                 stop = h_iter[2 * t] == 0;
+                if (t == max_iter) {   // the segments the cap stopped before convergence, and their rows
+                    capped_segs += (int64_t)h_iter[2 * t];
+                    capped_rows += (int64_t)h_iter[2 * t + 1];
+                }
             }
             if (stop) break;
         }
@@ -1073,6 +1084,8 @@ raftgp_status model_select_L(raftgp_graph g, const float *Z, int32_t eps, int32_
         stats[4] = lloyd_rows;   // rows of not-yet-converged segments visited by the Lloyd passes
         stats[5] = seed_rows;    // rows visited per seeding pass (3 passes: mean, 2 x farthest)
         stats[6] = rows_read;    // Z rows actually read by the Lloyd passes (the rest were pruned by bounds)
+        stats[7] = capped_segs;  // segments whose Lloyd iteration stopped at max_iter without converging (all levels)
+        stats[8] = capped_rows;  // their rows
     }
     return RAFTGP_OK;
 }

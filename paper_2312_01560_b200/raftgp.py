@@ -623,11 +623,12 @@ def raftgp_model_select(g: Graph, Z: torch.Tensor, eps: int = 5, max_iter: int =
     if labels is None:
         labels = torch.empty(max(1, g.rows), dtype=torch.int32, device=g.ctx.device)[: g.rows]
     k = c_i32(0)
-    st = np.zeros(7, np.int64)
+    st = np.zeros(9, np.int64)
     Zc = _own(Z, g.ctx.stream)
     _ck(load_library().raftgp_model_select(g.h, _ptr(Zc), Z.shape[1], eps, max_iter, r, _ptr(labels),
                                            ctypes.byref(k), c_vp(st.ctypes.data)))
-    return labels, int(k.value), dict(zip(("blocks", "splits", "lloyd_iters", "levels", "lloyd_rows", "seed_rows", "rows_read"),
+    return labels, int(k.value), dict(zip(("blocks", "splits", "lloyd_iters", "levels", "lloyd_rows", "seed_rows", "rows_read",
+                                           "capped_segments", "capped_rows"),
                                  (int(x) for x in st)))
 
 

@@ -186,3 +186,20 @@ def test_parity_small_sweep(rg, ctx, max_iter):
         src, dst = synth.random_edges(n, 6 * n, seed=seed)
         Z = _blob_Z(rng, n, 8, k=4, spread=0.7)
         _check(*_both(rg, ctx, n, src, dst, Z, max_iter=max_iter))
+
+
+def test_lloyd_cap_diagnostic(rg, ctx):
+    """stats capped_segments / capped_rows: the segments whose Lloyd iterations the max_iter cap stopped before
+    convergence. With max_iter = 1 every Lloyd run is stopped by the cap (the root segment alone holds all n rows);
+    a larger cap leaves fewer (or as many) capped segments; the partition still equals the oracle's either way."""
+    gr = synth.generate("C1", 3)
+    go = oracle.build_csr(gr.n, gr.src, gr.dst)
+    Z = oracle.gcn(go, [64, 64, 32], 3, oracle.project(go, "ncut", 64, 3))[-1].astype(np.float32)
+    res = {}
+    for cap in (1, 100):
+        ref, K, st, lab, Kg, stg = _both(rg, ctx, gr.n, gr.src, gr.dst, Z, max_iter=cap)
+        _check(ref, K, st, lab, Kg, stg)
+        res[cap] = stg
+    assert res[1]["capped_segments"] >= 1 and res[1]["capped_rows"] >= gr.n
+    assert 0 <= res[100]["capped_segments"] <= res[1]["capped_segments"] + res[100]["splits"]
+    assert 0 <= res[100]["capped_rows"] <= res[100]["lloyd_rows"] + gr.n
