@@ -339,15 +339,17 @@ RAFTGP_API raftgp_status raftgp_stream_add_edges(raftgp_stream s, int64_t m, con
 RAFTGP_API raftgp_status raftgp_stream_embedding(raftgp_stream s, float *Z_dev);
 RAFTGP_API raftgp_status raftgp_stream_graph(raftgp_stream s, raftgp_graph *g_out);
 RAFTGP_API raftgp_status raftgp_stream_destroy(raftgp_stream s);
-/* raftgp_stream_set_mode: how raftgp_stream_add_edges updates the LAST GCN hop (Eq. 6).
- *   RAFTGP_STREAM_EXACT (the default): the hop is recomputed over R_{L+1} (or every row) with the hop kernels, so Z
- *     stays bit-identical to raftgp_embed(NCUT) on the new graph. Setting it recomputes Z that way.
- *   RAFTGP_STREAM_DELTA: the stream keeps the last hop's pre-activation sums A_i = T_i + sum_{j in N(i)} T_j
- *     (n x dims[layers] fp32, device, library-owned); after a batch, rows outside V' add the changes
- *     T_j(new) - T_j(old) of their neighbours in R_L only, and the rows of V' are summed in full. The last hop then
- *     reads col_idx once instead of one operand row per CSR entry. Z equals the full recompute up to fp32 rounding
- *     order (re-associated sums; the error grows slowly with the number of batches), not bit-identically. Setting it
- *     (again) builds A and Z by a full pass: a resync.
+/* raftgp_stream_set_mode: how raftgp_stream_add_edges updates the GCN hops (Eq. 6).
+ *   RAFTGP_STREAM_EXACT (the default): the hops are recomputed over R_{k} (or every row) with the hop kernels, so Z
+ *     stays bit-identical to raftgp_embed(NCUT) on the new graph.
+ *   RAFTGP_STREAM_DELTA: the stream keeps every GCN hop's pre-activation sums A^h_i = T^h_i + sum_{j in N(i)} T^h_j
+ *     (n x dims[h] fp32 each, device, library-owned); after a batch, rows outside V' add the changes
+ *     T^h_j(new) - T^h_j(old) of their neighbours in R_h only, and the rows of V' are summed in full. Hop h < L visits
+ *     the rows of R_{h+1}, the last hop every row, each reading col_idx once instead of one operand row per CSR
+ *     entry. Z equals the full recompute up to fp32 rounding order (re-associated sums; the error grows slowly with
+ *     the number of batches), not bit-identically.
+ *   Setting either mode (again) first recomputes the exact chain over every row (Z bit-identical to raftgp_embed:
+ *   a resync); DELTA then builds the sums by a full pass.
  *   stats[layers + 1] of raftgp_stream_add_edges is then the number of rows whose Z was rewritten.
  * Errors: PARAM (null stream, unknown mode), NOMEM, CUDA. Asynchronous on the context stream. */
 #define RAFTGP_STREAM_EXACT 0

@@ -141,8 +141,9 @@ struct raftgp_stream_s {
     std::vector<float *> W;             // W[k], k = 2..layers (dims[k-1] x dims[k])
     float *Z = nullptr;                 // n x dims[layers]
     int32_t mode = 0;                   // RAFTGP_STREAM_EXACT / RAFTGP_STREAM_DELTA
-    float *A = nullptr;                 // delta mode: the last hop's pre-activation sums T_i + sum_j T_j (n x dims[L])
-    int32_t *pos = nullptr;             // delta mode: row -> index into this batch's dT (-1: T_L row unchanged)
+    std::vector<float *> A;             // delta mode: A[h] = GCN hop h's pre-activation sums T_i + sum_j T_j (n x dims[h])
+    int32_t *pos = nullptr;             // delta mode: row -> index into the current dT (-1: row unchanged)
+    float *Zs = nullptr;                // delta mode: Z_h rows of a hop h < L (n x max dims[1..L-1]), transform input
 };
 
 namespace raftgp {
@@ -289,6 +290,9 @@ bool push_fusable(int32_t w, int32_t wn);
 // the same hops over a list of local rows (NEXT-4 streaming)
 raftgp_status feature_hop_pre_rows(raftgp_graph g, int variant, int32_t l1, const float *theta_w, const double *gvec_w,
                                    float *T, const int32_t *rows, int64_t count);
+// T_next rows = s^ (.) (Z rows W) for the listed local rows (Z and T_next full-size, indexed by row)
+raftgp_status gcn_transform_rows(raftgp_graph g, const float *Z, int32_t lin, const float *W, int32_t lout, float *T,
+                                 const int32_t *rows, int64_t count);
 raftgp_status gcn_hop_rows(raftgp_graph g, const float *Tfull, int32_t w, float *Zout, const float *Wn, int32_t wn,
                            float *Tnext, const int32_t *rows, int64_t count);
 // last GCN hop of two variants over the interleaved operand [T_a | T_b] (n x 2d); d in {32, 64}

@@ -764,6 +764,22 @@ raftgp_status gcn_hop_rows(raftgp_graph g, const float *Tfull, int32_t w, float 
     return dispatch<KIND_GCN>(g->ctx, a, w, Wn ? wn : 0);
 }
 
+raftgp_status gcn_transform_rows(raftgp_graph g, const float *Z, int32_t lin, const float *W, int32_t lout, float *T,
+                                 const int32_t *rows, int64_t count) {
+    if (count == 0) return RAFTGP_OK;
+    HopArgs a = base_args(g, lin);
+    a.nl = count;
+    a.order = rows;
+    a.X = Z;
+    a.out = nullptr;
+    a.Wn = W;
+    a.Tn = T;
+    if (!((lin == 32 || lin == 64 || lin == 128) && (lout == 32 || lout == 64 || lout == 128) && aligned16(Z) &&
+          aligned16(W) && aligned16(T)))
+        return fail(RAFTGP_ERR_INTERNAL, "gcn_transform_rows: unsupported width/alignment");
+    return dispatch<KIND_LOAD>(g->ctx, a, lin, lout);
+}
+
 raftgp_status gcn_transform(raftgp_graph g, const float *Z, int32_t lin, const float *W, int32_t lout, float *T) {
     HopArgs a = base_args(g, lin);
     a.X = Z;

@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(256, 8) last_hop_delta(int64_t n, const int64_
             }
             if (sub == 0) {
                 reinterpret_cast<float4 *>(A)[i * LPN + cl] = acc;
-                reinterpret_cast<float4 *>(Z)[i * LPN + cl] = y;
+                if (Z) reinterpret_cast<float4 *>(Z)[i * LPN + cl] = y;
             }
             ++mine;
         }
@@ -516,28 +516,28 @@ inline unsigned g256(int64_t n) { return (unsigned)std::max<int64_t>(1, ceil_div
 
 bool fast_width(int32_t w) { return w == 32 || w == 64 || w == 128; }
 
-// the delta-mode last hop over every row (all_full = 1: the state build / resync; 0: a batch's update)
-raftgp_status launch_last_delta(raftgp_stream s, raftgp_graph g, const int32_t *level, const float *dT, int all_full,
-                                int64_t *touched_out) {
+// GCN hop h of a delta-mode stream (A[h] updated, Zout = rownorm(tanh(s^ A)) or null) over the listed rows, or over
+// every row in the graph's visiting order (rows = null, count = n); all_full = 1: every row summed in full (state
+// build / resync, or when the changed rows of T_h are too many for dT); touched_out: rows rewritten
+raftgp_status launch_hop_delta(raftgp_stream s, raftgp_graph g, int h, const int32_t *rows, int64_t count,
+                               const int32_t *level, const float *dT, int all_full, float *Zout, int64_t *touched_out) {
     raftgp_ctx ctx = g->ctx;
-    const int64_t n = g->n;
-    if (n == 0) {
+    if (count == 0) {
         if (touched_out) *touched_out = 0;
         return RAFTGP_OK;
     }
-    const int d = s->dims[s->layers];
+    const int d = s->dims[h];
     unsigned long long *ctr = nullptr;
     RG_TRY(dalloc_t(ctx, &ctr, 2));
     raftgp_status rc = dzero(ctx, ctr, 2 * sizeof(unsigned long long));
     if (rc == RAFTGP_OK) {
         const unsigned grid = (unsigned)std::max<int64_t>(
-            1, std::min<int64_t>(ceil_div(ceil_div(n, kDeltaRows), 8), (int64_t)ctx->sm_count * 8));
-        LaunchScope LS(ctx, K_STREAM_LAST);
-        const char *ne = getenv("RAFTGP_DELTA_NAT");
-        const bool nat = !all_full && ne && ne[0] == '1';
+            1, std::min<int64_t>(ceil_div(ceil_div(count, kDeltaRows), 8), (int64_t)ctx->sm_count * 8));
+        LaunchScope LS(ctx, h == s->layers ? K_STREAM_LAST : K_STREAM);
+        const int32_t *order = rows ? rows : g->order;
         auto go = [&](auto kern) {
-            kern<<<grid, 256, 0, ctx->stream>>>(n, g->row_ptr, g->col, nat ? nullptr : g->order, s->T[s->layers], s->pos, dT, level,
-                                                g->sh_all, s->A, s->Z, all_full, ctr, ctr + 1);
+            kern<<<grid, 256, 0, ctx->stream>>>(count, g->row_ptr, g->col, order, s->T[h], s->pos, dT, level, g->sh_all,
+                                                s->A[h], Zout, all_full, ctr, ctr + 1);
         };
         if (d == 32) go(last_hop_delta<32>);
         else if (d == 64) go(last_hop_delta<64>);
@@ -552,6 +552,20 @@ raftgp_status launch_last_delta(raftgp_stream s, raftgp_graph g, const int32_t *
     if (touched_out) *touched_out = (int64_t)t;
     dfree(ctx, ctr);
     return rc;
+}
+
+// the exact chain over every row (stream_create's state build; EXACT / DELTA mode switches restore it)
+raftgp_status exact_chain(raftgp_stream s) {
+    raftgp_graph g = s->g;
+    const auto &dims = s->dims;
+    const int L = s->layers;
+    RG_TRY(feature_hop_pre(g, RAFTGP_NCUT, dims[1], s->thw, nullptr, s->T[1], nullptr));
+    for (int k = 1; k <= L; ++k) {
+        const bool last = k == L;
+        RG_TRY(gcn_hop(g, s->T[k], dims[k], last ? s->Z : nullptr, last ? nullptr : s->W[k + 1], last ? 0 : dims[k + 1],
+                       last ? nullptr : s->T[k + 1]));
+    }
+    return RAFTGP_OK;
 }
 
 }  // namespace
@@ -749,21 +763,29 @@ raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const i
         return e ? atoi(e) : -1;
     }();
     const bool delta_mode = s->mode == RAFTGP_STREAM_DELTA;
-    float *dT = nullptr;   // delta mode: T_L(new) - T_L(old) for the rows of R_L (list order)
+    // delta mode: dT[k] = T_k(new) - T_k(old) for the rows of R_k (list order; pos[] indexes it), or null when R_k is
+    // too large for the changed-row gathers to pay (RAFTGP_STREAM_DELTA_FRAC = f: none when |R_k| f >= n, default 8;
+    // 0: always kept) — the hop reading T_k then sums its rows in full
+    std::vector<float *> dT(L + 2, nullptr);
+    const char *fe = getenv("RAFTGP_STREAM_DELTA_FRAC");
+    const int64_t frac = fe ? atoll(fe) : 8;
+    float *Zs = s->Zs;     // delta mode: Z_h of the listed rows (full size, indexed by row), input of the transform
+    auto clear_pos = [&](int k) {
+        if (!dT[k] || counts[k] == 0) return;
+        LaunchScope LS(ctx, K_STREAM);
+        delta_clear<<<(unsigned)std::min<int64_t>(g256(counts[k]), (int64_t)ctx->sm_count * 8), 256, 0, st>>>(rows, counts[k],
+                                                                                                        s->pos);
+    };
     for (int k = 1; k <= L + 1 && rc == RAFTGP_OK; ++k) {
         if (k == L + 1 && delta_mode) {   // the last hop by its changed inputs only (no level L + 1 expansion)
             if (counts[0] > 0) {
                 int32_t *own = ng->order;
                 if (!own && g->nl == ng->nl) ng->order = g->order;
                 int64_t touched = 0;
-                rc = launch_last_delta(s, ng, level, dT, dT ? 0 : 1, &touched);
+                rc = launch_hop_delta(s, ng, L, nullptr, n, level, dT[L], dT[L] ? 0 : 1, s->Z, &touched);
                 ng->order = own;
                 counts[k] = touched;   // rows whose Z was rewritten
-                if (rc == RAFTGP_OK && dT) {
-                    LaunchScope LS(ctx, K_STREAM);
-                    delta_clear<<<(unsigned)std::min<int64_t>(g256(counts[L]), (int64_t)ctx->sm_count * 8), 256, 0, st>>>(
-                        rows, counts[L], s->pos);
-                }
+                if (rc == RAFTGP_OK) clear_pos(L);
             }
             break;
         }
@@ -832,36 +854,38 @@ raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const i
             dfree(ctx, pos);
         }
         if (rc == RAFTGP_OK) rc = spread_heavy_list(ctx, list, counts[k], ng->deg_local, hop_rows);
-        const int lpn = s->dims[L] / 4;
-        // keep T_L(old) of the rows about to change; when R_L holds 1/8 of the rows or more, the changed rows' gathers
-        // would cost as much as a full pass: the last hop then sums every row in full (A rebuilt, no dT)
-        // (RAFTGP_STREAM_DELTA_FRAC = f: the full pass when |R_L| * f >= n, default 8; 0: never)
-        const char *fe = getenv("RAFTGP_STREAM_DELTA_FRAC");
-        const int64_t frac = fe ? atoll(fe) : 8;
-        if (rc == RAFTGP_OK && delta_mode && k == L && counts[k] > 0 && (frac <= 0 || counts[k] * frac < n)) {
-            rc = dalloc_t(ctx, &dT, (size_t)counts[k] * s->dims[L]);
+        if (rc == RAFTGP_OK && delta_mode && k >= 2) {   // GCN hop h = k - 1 over R_k from A_h and T_h's changed rows
+            const int h = k - 1;
+            if (rc == RAFTGP_OK) rc = launch_hop_delta(s, ng, h, hop_rows, counts[k], level, dT[h], dT[h] ? 0 : 1, Zs, nullptr);
+            if (rc == RAFTGP_OK) clear_pos(h);
+        }
+        const int lpn = s->dims[k <= L ? k : L] / 4;
+        if (rc == RAFTGP_OK && delta_mode && counts[k] > 0 && (frac <= 0 || counts[k] * frac < n)) {   // keep T_k(old)
+            rc = dalloc_t(ctx, &dT[k], (size_t)counts[k] * s->dims[k]);
             if (rc == RAFTGP_OK) {
                 LaunchScope LS(ctx, K_STREAM);
                 delta_save<<<(unsigned)std::min<int64_t>(g256(counts[k] * lpn), (int64_t)ctx->sm_count * 8), 256, 0, st>>>(
-                    rows, counts[k], reinterpret_cast<const float4 *>(s->T[L]), lpn, s->pos, reinterpret_cast<float4 *>(dT));
+                    rows, counts[k], reinterpret_cast<const float4 *>(s->T[k]), lpn, s->pos, reinterpret_cast<float4 *>(dT[k]));
             }
         }
         if (rc != RAFTGP_OK) break;
         if (k == 1) {
             rc = feature_hop_pre_rows(ng, RAFTGP_NCUT, d[1], s->thw, nullptr, s->T[1], hop_rows, counts[1]);
+        } else if (delta_mode) {   // T_k = s^ (.) (Z_{k-1} W_k) for the rows of R_k
+            rc = gcn_transform_rows(ng, Zs, d[k - 1], s->W[k], d[k], s->T[k], hop_rows, counts[k]);
         } else {
             const int h = k - 1;   // GCN hop h reads T_h, writes T_{h+1} (or Z after the last layer)
             const bool last = h == L;
             rc = gcn_hop_rows(ng, s->T[h], d[h], last ? s->Z : nullptr, last ? nullptr : s->W[h + 1],
                               last ? 0 : d[h + 1], last ? nullptr : s->T[h + 1], hop_rows, counts[k]);
         }
-        if (rc == RAFTGP_OK && dT && k == L) {
+        if (rc == RAFTGP_OK && dT[k]) {
             LaunchScope LS(ctx, K_STREAM);
             delta_finish<<<(unsigned)std::min<int64_t>(g256(counts[k] * lpn), (int64_t)ctx->sm_count * 8), 256, 0, st>>>(
-                rows, counts[k], reinterpret_cast<const float4 *>(s->T[L]), lpn, reinterpret_cast<float4 *>(dT));
+                rows, counts[k], reinterpret_cast<const float4 *>(s->T[k]), lpn, reinterpret_cast<float4 *>(dT[k]));
         }
     }
-    dfree(ctx, dT);
+    for (float *p : dT) dfree(ctx, p);
     dfree(ctx, add); dfree(ctx, level); dfree(ctx, rows); dfree(ctx, cnt); dfree(ctx, hop_rows); dfree(ctx, nat_rows);
     if (rc != RAFTGP_OK) {
         drop(*ng);
@@ -891,8 +915,9 @@ void stream_destroy(raftgp_stream s) {
     for (auto t : s->T) dfree(ctx, t);
     for (auto w : s->W) dfree(ctx, w);
     dfree(ctx, s->Z);
-    dfree(ctx, s->A);
+    for (float *a : s->A) dfree(ctx, a);
     dfree(ctx, s->pos);
+    dfree(ctx, s->Zs);
     if (s->g) {
         raftgp_graph_s &x = *s->g;
         dfree(ctx, x.row_ptr); dfree(ctx, x.col); dfree(ctx, x.deg_local); dfree(ctx, x.order); dfree(ctx, x.deg_all);
@@ -904,33 +929,42 @@ void stream_destroy(raftgp_stream s) {
     ctx_release(ctx);
 }
 
-// RAFTGP_STREAM_DELTA: the state A of the last hop (and pos = -1) is built by a full pass that also rewrites Z (each call
-// is therefore a resync); RAFTGP_STREAM_EXACT drops it and recomputes Z with the exact hop kernel (bit-identical to
-// raftgp_embed again)
+// Both modes first recompute the exact chain over every row (so a switch, or setting DELTA again, removes any drift);
+// RAFTGP_STREAM_DELTA then builds A[h] for every GCN hop by a full pass (Z keeps the exact values) and pos = -1.
 raftgp_status stream_set_mode(raftgp_stream s, int32_t mode) {
     raftgp_graph g = s->g;
     raftgp_ctx ctx = s->ctx;
     const int64_t n = g->n;
-    const int L = s->layers, d = s->dims[L];
+    const int L = s->layers;
+    RG_TRY(exact_chain(s));
     if (mode == RAFTGP_STREAM_DELTA) {
-        if (!s->A) RG_TRY(dalloc_t(ctx, &s->A, (size_t)std::max<int64_t>(1, n) * d));
+        s->A.resize(L + 1, nullptr);
+        for (int h = 1; h <= L; ++h)
+            if (!s->A[h]) RG_TRY(dalloc_t(ctx, &s->A[h], (size_t)std::max<int64_t>(1, n) * s->dims[h]));
         if (!s->pos) RG_TRY(dalloc_t(ctx, &s->pos, (size_t)std::max<int64_t>(1, n)));
+        int32_t maxd = 0;
+        for (int q = 1; q < L; ++q) maxd = std::max(maxd, s->dims[q]);
+        if (!s->Zs && maxd > 0) RG_TRY(dalloc_t(ctx, &s->Zs, (size_t)std::max<int64_t>(1, n) * maxd));
         if (n > 0) {
             LaunchScope LS(ctx, K_STREAM);
             fill_value<<<(unsigned)std::min<int64_t>(g256(n), (int64_t)ctx->sm_count * 8), 256, 0, ctx->stream>>>(n, s->pos,
                                                                                                                 -1);
         }
         RG_CHECK_LAUNCH(ctx);
-        RG_TRY(launch_last_delta(s, g, nullptr, nullptr, 1, nullptr));
+        for (int h = 1; h <= L; ++h) RG_TRY(launch_hop_delta(s, g, h, nullptr, n, nullptr, nullptr, 1, nullptr, nullptr));
         s->mode = mode;
         return RAFTGP_OK;
     }
-    dfree(ctx, s->A);
+    for (float *&a : s->A) {
+        dfree(ctx, a);
+        a = nullptr;
+    }
     dfree(ctx, s->pos);
-    s->A = nullptr;
+    dfree(ctx, s->Zs);
     s->pos = nullptr;
+    s->Zs = nullptr;
     s->mode = RAFTGP_STREAM_EXACT;
-    return gcn_hop(g, s->T[L], d, s->Z, nullptr, 0, nullptr, 0, nullptr);
+    return RAFTGP_OK;
 }
 
 }  // namespace raftgp

@@ -229,8 +229,9 @@ def test_stream_delta_matches_exact(rg, ctx, cfg, n, dims, batches, frac, monkey
 
 
 def test_stream_delta_drift_resync_and_exact(rg, ctx, monkeypatch):
-    """40 small batches in delta mode stay within 1e-5 of a fresh embed; set_mode("delta") again resyncs (a full
-    pass); set_mode("exact") recomputes Z bit-identically to raftgp_embed; no-op batches change nothing."""
+    """40 small batches in delta mode stay within 1e-5 of a fresh embed; set_mode("delta") again resyncs (the exact
+    chain, then the sums: Z bit-identical to raftgp_embed); set_mode("exact") after a delta batch recomputes Z
+    bit-identically; no-op batches change nothing."""
     monkeypatch.setenv("RAFTGP_STREAM_DELTA_FRAC", "0")
     dims = (64, 64, 32)
     gr, s0, d0, bs, bd = _delta_case(rg, ctx, "C1", None, dims, 40, 5, 11)
@@ -248,10 +249,12 @@ def test_stream_delta_drift_resync_and_exact(rg, ctx, monkeypatch):
     fresh = _fresh_ncut(rg, ctx, gr.n, cur_s, cur_d, dims, 2)
     Zd = de.embedding()
     assert ((Zd - fresh).norm() / fresh.norm()).item() <= 1e-5
-    de.set_mode("delta")
-    assert (de.embedding() - fresh).abs().max().item() <= 2e-6
-    de.set_mode("exact")
+    de.set_mode("delta")   # a resync: the exact chain, then the sums rebuilt
     assert torch.equal(de.embedding(), fresh)
+    de.add_edges(_t([1, 4]), _t([600, 800]))
+    de.set_mode("exact")
+    cur_s, cur_d = np.concatenate([cur_s, [1, 4]]), np.concatenate([cur_d, [600, 800]])
+    assert torch.equal(de.embedding(), _fresh_ncut(rg, ctx, gr.n, cur_s, cur_d, dims, 2))
     st = de.add_edges(_t([0, 3]), _t([500, 900]))   # exact again: bit-identical
     fresh2 = _fresh_ncut(rg, ctx, gr.n, np.concatenate([cur_s, [0, 3]]), np.concatenate([cur_d, [500, 900]]), dims, 2)
     assert torch.equal(de.embedding(), fresh2), st
