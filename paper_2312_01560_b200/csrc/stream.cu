@@ -12,6 +12,8 @@
 // is BIT-IDENTICAL to a full recompute on G u E'. This holds for X = M (NCut): Q and Q~ depend on 2e,
 // which changes every row when an edge is added, so their exact update is the full recompute (the paper's
 // O(|E'|) update of Q~ ignores that change).
+// Delta mode (raftgp_stream_set_mode): every GCN hop is updated from its stored pre-activation sums plus the changed
+// rows of its input (last_hop_delta below) — equal up to fp32 re-association instead of bit-identical.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
