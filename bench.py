@@ -845,10 +845,12 @@ def main():
     e2e = None
     e2e_skip = None
     e2e_steps = max(args.steps, args.e2e_steps)
+    e2e_seq = world > 1
+    e2e_note = None
     if not args.no_e2e:
         # each pipelined lane holds its own context (workspace) and two Z buffer sets; at C5 sizes that does
-        # not fit next to the main context, so the lane count drops, and the leg is skipped (with the reason)
-        # when even one lane would not fit
+        # not fit next to the main context, so the lane count drops, and when even one lane would not fit the
+        # leg runs sequential steps on the main context (the reason goes into e2e.mode)
         ctx.trim()
         torch.cuda.empty_cache()
         free_b, _ = torch.cuda.mem_get_info(dev)
@@ -857,11 +859,13 @@ def main():
         lanes_fit = int(free_b // max(1, lane_b))
         if lanes_fit < args.e2e_lanes:
             args.e2e_lanes = max(1, min(args.e2e_lanes, lanes_fit))
-        if lanes_fit < 1:
-            e2e_skip = f"needs ~{lane_b / 2**30:.0f} GiB per pipeline lane, {free_b / 2**30:.0f} GiB free"
+        if lanes_fit < 1:   # no room for a pipeline lane (C5): sequential steps on the main context instead
+            e2e_seq = True
+            e2e_steps = args.steps
+            e2e_note = f"a pipeline lane needs ~{lane_b / 2**30:.0f} GiB, {free_b / 2**30:.0f} GiB free"
     if not args.no_e2e and e2e_skip is None:
         d2h = int(sum(rows * dims[-1] * 4 for _ in variants))
-        if world == 1 and not args.no_fuse_variants and args.e2e_lanes == 1:
+        if not e2e_seq and world == 1 and not args.no_fuse_variants and args.e2e_lanes == 1:
             # one compute stream (steps back to back, no kernel interleaving across steps) with the copies on
             # their own streams: H2D of step k+1 and D2H of step k-1 run under step k's kernels; inputs and
             # outputs double-buffered, ordered by events
@@ -920,7 +924,7 @@ def main():
             torch.cuda.synchronize()
             mode = ("one compute stream (raftgp_build_embed per step) + H2D and D2H streams: step k+1's inputs and "
                     "step k-1's outputs cross PCIe under step k's kernels")
-        elif world == 1 and not args.no_fuse_variants:
+        elif not e2e_seq and world == 1 and not args.no_fuse_variants:
             lanes = []
             for _ in range(args.e2e_lanes):
                 s_ = torch.cuda.Stream(dev)
@@ -983,7 +987,7 @@ def main():
             for _ in range(e2e_steps):
                 step(src_h, dst_h, out_host)
             e1.record(stream)
-            mode = "sequential on one stream"
+            mode = "sequential on one stream" + (f" ({e2e_note})" if e2e_note else "")
         barrier()
         ems = max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
         e2e = {"value": units / (ems * 1e-3), "unit": UNIT, "ms_per_step": ems, "h2d_bytes_per_step": 8 * m,
