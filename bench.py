@@ -485,7 +485,7 @@ def measure_sketch(args, rg, ctx, n, r, l1, barrier, sm_mhz):
             "normals": normals, "bound": "alu", "achieved": ach, "unit": "normals/s", "peak": peak, "frac": ach / peak,
             "peak_rule": (f"{sms} SMs x 4 warp-instructions/clock x 32 lanes x {clk / 1e6:.0f} MHz / "
                           f"{SKETCH_THREAD_INST_PER_NORMAL} thread-instructions per normal (ncu, this kernel)"),
-            "in_step": "runs on half the SMs on a side stream while the CSR build runs (DESIGN.md §6)"}
+            "in_step": "runs on all SMs after the CSR build and the slot build (rows stored at slots chosen by degree; DESIGN.md §6)"}
 
 
 def measure_table1(args, rg, dev, barrier, peak, peak_src):
