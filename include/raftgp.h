@@ -331,7 +331,8 @@ RAFTGP_API raftgp_status raftgp_sbm_sample(raftgp_ctx ctx, int64_t n, int32_t K,
  *     {|V'|, |R_1|, ..., |R_{layers+1}|, nnz of the new graph}. Synchronous.
  *   raftgp_stream_embedding: copies Z (n x dims[layers], device) out (async on the context stream).
  *   raftgp_stream_graph: borrowed handle of the current graph (export / scoring), valid until the next add.
- * Errors: PARAM (widths, arguments), DATA (node id outside [0, n)), STATE, NOMEM, CUDA. */
+ * Errors: PARAM (widths, arguments), DATA (node id outside [0, n); nothing is changed), STATE (a previous batch failed
+ * after its hops started: the state is partly updated and raftgp_stream_set_mode must recompute it first), NOMEM, CUDA. */
 RAFTGP_API raftgp_status raftgp_stream_create(raftgp_graph g, int32_t layers, const int32_t *dims, uint64_t seed,
                                               raftgp_stream *out);
 RAFTGP_API raftgp_status raftgp_stream_add_edges(raftgp_stream s, int64_t m, const int32_t *src, const int32_t *dst,

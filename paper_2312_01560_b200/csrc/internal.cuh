@@ -141,6 +141,7 @@ struct raftgp_stream_s {
     std::vector<float *> W;             // W[k], k = 2..layers (dims[k-1] x dims[k])
     float *Z = nullptr;                 // n x dims[layers]
     int32_t mode = 0;                   // RAFTGP_STREAM_EXACT / RAFTGP_STREAM_DELTA
+    bool stale = false;                 // a failed batch rewrote part of the state: add_edges refused until set_mode
     std::vector<float *> A;             // delta mode: A[h] = GCN hop h's pre-activation sums T_i + sum_j T_j (n x dims[h])
     int32_t *pos = nullptr;             // delta mode: row -> index into the current dT (-1: row unchanged)
     float *Zs = nullptr;                // delta mode: Z_h rows of a hop h < L (n x max dims[1..L-1]), transform input

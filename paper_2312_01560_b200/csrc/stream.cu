@@ -615,6 +615,8 @@ raftgp_status stream_create(raftgp_graph g, int32_t layers, const int32_t *dims,
 }
 
 raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const int32_t *dst, int64_t *stats) {
+    if (s->stale)
+        return fail(RAFTGP_ERR_STATE, "stream: a failed batch left the state partly updated; call raftgp_stream_set_mode");
     raftgp_graph g = s->g;
     raftgp_ctx ctx = g->ctx;
     cudaStream_t st = ctx->stream;
@@ -764,6 +766,7 @@ raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const i
         const char *e = getenv("RAFTGP_STREAM_FULL_LAST");
         return e ? atoi(e) : -1;
     }();
+    const bool hops_started = rc == RAFTGP_OK;   // from here on the embedding state is being rewritten
     const bool delta_mode = s->mode == RAFTGP_STREAM_DELTA;
     // delta mode: dT[k] = T_k(new) - T_k(old) for the rows of R_k (list order; pos[] indexes it), or null when R_k is
     // too large for the changed-row gathers to pay (RAFTGP_STREAM_DELTA_FRAC = f: none when |R_k| f >= n, default 8;
@@ -892,7 +895,10 @@ raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const i
     if (rc != RAFTGP_OK) {
         drop(*ng);
         delete ng;
-        return rc;   // the stream keeps its previous graph; rows already recomputed for the new graph are stale
+        // the stream keeps its previous graph; once the hops ran, some rows (and the delta state) belong to the new
+        // graph: further batches are refused until raftgp_stream_set_mode recomputes the state on the kept graph
+        if (hops_started) s->stale = true;
+        return rc;
     }
     // the stream now owns the merged graph; it inherits the visiting order (any permutation gives bit-identical
     // rows; this one spreads the old graph's heavy rows, which are still the heavy rows)
@@ -939,6 +945,7 @@ raftgp_status stream_set_mode(raftgp_stream s, int32_t mode) {
     const int64_t n = g->n;
     const int L = s->layers;
     RG_TRY(exact_chain(s));
+    s->stale = false;
     if (mode == RAFTGP_STREAM_DELTA) {
         s->A.resize(L + 1, nullptr);
         for (int h = 1; h <= L; ++h)

@@ -119,6 +119,10 @@ def test_stream_errors(rg, ctx):
     with pytest.raises(rg.RaftGPError) as e:
         stream.add_edges(_t([0]), _t([gr.n + 5]))
     assert e.value.code == rg.RAFTGP_ERR_DATA
+    # a data error is caught before the state is touched: the stream goes on, still bit-identical
+    stream.add_edges(_t([0, 7]), _t([400, 900]))
+    assert torch.equal(stream.embedding(), _fresh_ncut(rg, ctx, gr.n, np.concatenate([gr.src, [0, 7]]),
+                                                       np.concatenate([gr.dst, [400, 900]]), (64, 64, 32), 1))
 
 
 _LAST_SCRIPT = r"""
