@@ -278,6 +278,62 @@ __global__ void merge_copy(int64_t nnz, const int32_t *__restrict__ ocol, const 
     }
 }
 
+// the same copy by chunks: a warp takes 32 x kMcVec consecutive entries, one lane locates the chunk start among the
+// changed rows (binary search, once per chunk instead of per entry), and a chunk that lies inside one unchanged
+// segment (all but ~2 per changed row) is moved with 16-byte loads and a constant shift; the others go entry by entry
+constexpr int kMcVec = 8;   // entries per lane and chunk (two int4 loads)
+__global__ void merge_copy_chunks(int64_t nnz, const int32_t *__restrict__ ocol, const int32_t *__restrict__ sorted,
+                                  const int64_t *__restrict__ orp, const int64_t *__restrict__ ends,
+                                  const int64_t *__restrict__ shift, int nc, int32_t *__restrict__ ncol) {
+    const int lane = threadIdx.x & 31;
+    constexpr int64_t CH = 32 * kMcVec;
+    const int64_t nch = (nnz + CH - 1) / CH;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = wid; c < nch; c += nw) {
+        const int64_t p0 = c * CH, p1 = min(nnz, p0 + CH);
+        int seg = 0;
+        bool clean = false;
+        if (lane == 0) {
+            int lo = 0, hi = nc;   // changed rows ending at or before p0
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (ends[mid] <= p0) lo = mid + 1;
+                else hi = mid;
+            }
+            seg = lo;
+            // clean: the chunk ends before the next changed row starts (and does not start inside one)
+            clean = lo >= nc || orp[sorted[lo]] >= p1;
+        }
+        seg = __shfl_sync(0xffffffffu, seg, 0);
+        clean = __shfl_sync(0xffffffffu, clean, 0);
+        if (clean && p1 - p0 == CH) {
+            const int64_t sh = shift[seg];
+            const int4 *src = reinterpret_cast<const int4 *>(ocol + p0);
+#pragma unroll
+            for (int h = 0; h < kMcVec / 4; ++h) {
+                const int4 v = __ldcs(src + h * 32 + lane);
+                int32_t *d = ncol + p0 + sh + (int64_t)(h * 32 + lane) * 4;
+                d[0] = v.x;
+                d[1] = v.y;
+                d[2] = v.z;
+                d[3] = v.w;
+            }
+        } else {
+            for (int64_t p = p0 + lane; p < p1; p += 32) {
+                int lo = 0, hi = nc;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (ends[mid] <= p) lo = mid + 1;
+                    else hi = mid;
+                }
+                if (lo < nc && orp[sorted[lo]] <= p) continue;   // inside a changed row
+                ncol[p + shift[lo]] = ocol[p];
+            }
+        }
+    }
+}
+
 // the changed rows: warp per row. The row's new entries d_0 < d_1 < ... are a contiguous run of the sorted keys
 // (flagged new); every old entry moves by the number of new entries below it and every new entry lands after the old
 // entries below it (binary searches, all lanes in parallel: a hub row is not merged by one lane)
@@ -714,7 +770,12 @@ raftgp_status stream_add(raftgp_stream s, int64_t m, const int32_t *src, const i
                 LaunchScope LS(ctx, K_STREAM);
                 changed_table<<<1, 1024, 0, st>>>(rows, nc, g->row_ptr, add, sorted, ends, shift);
             }
-            if (g->nnz_local > 0 && nc <= 64) {   // few changed rows: a streaming element-wise copy
+            if (g->nnz_local > 0 && nc <= 64 && aligned16(g->col)) {   // few changed rows: a streaming chunked copy
+                LaunchScope LS(ctx, K_STREAM);
+                merge_copy_chunks<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(g->nnz_local, 256 * kMcVec * 8),
+                                                                                   (int64_t)ctx->sm_count * 16)),
+                                    256, 0, st>>>(g->nnz_local, g->col, sorted, g->row_ptr, ends, shift, nc, ng->col);
+            } else if (g->nnz_local > 0 && nc <= 64) {
                 LaunchScope LS(ctx, K_STREAM);
                 merge_copy<<<(unsigned)std::min<int64_t>(ceil_div(g->nnz_local, 256), (int64_t)ctx->sm_count * 16), 256, 0,
                              st>>>(g->nnz_local, g->col, sorted, g->row_ptr, ends, shift, nc, ng->col);
