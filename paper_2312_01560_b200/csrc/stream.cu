@@ -552,17 +552,51 @@ __global__ void __launch_bounds__(256, 8) last_hop_delta(int64_t n, const int64_
                 acc = make_float4(ao.x + acc.x, ao.y + acc.y, ao.z + acc.z, ao.w + acc.w);
             }
             const float s = __ldg(sh + i);
-            float4 y = make_float4(tanhf(s * acc.x), tanhf(s * acc.y), tanhf(s * acc.z), tanhf(s * acc.w));
-            float ss = y.x * y.x + y.y * y.y + y.z * y.z + y.w * y.w;
+            if constexpr (NB == 1) {
+                float4 y = make_float4(tanhf(s * acc.x), tanhf(s * acc.y), tanhf(s * acc.z), tanhf(s * acc.w));
+                float ss = y.x * y.x + y.y * y.y + y.z * y.z + y.w * y.w;
 #pragma unroll
-            for (int o = 1; o < LPN; o <<= 1) ss += __shfl_xor_sync(FULLM, ss, o);
-            if (ss > 0.f) {   // one reciprocal square root (this mode is not bit-identical to the hop kernels anyway)
-                const float inv = rsqrtf(ss);
-                y = make_float4(y.x * inv, y.y * inv, y.z * inv, y.w * inv);
-            }
-            if (sub == 0) {
+                for (int o = 1; o < 32; o <<= 1) ss += __shfl_xor_sync(FULLM, ss, o);
+                if (ss > 0.f) {   // one reciprocal square root (this mode is not bit-identical to the hop kernels anyway)
+                    const float inv = rsqrtf(ss);
+                    y = make_float4(y.x * inv, y.y * inv, y.z * inv, y.w * inv);
+                }
                 reinterpret_cast<float4 *>(A)[i * LPN + cl] = acc;
                 if (Z) reinterpret_cast<float4 *>(Z)[i * LPN + cl] = y;
+            } else {
+                // every sub-slot holds the whole row sum after the butterfly: sub-slot s finishes columns
+                // 4 cl + s CPL .. + CPL - 1 only, so the tanh / norm work is not repeated NB times
+                constexpr int CPL = 4 / NB;
+                const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+                float v[CPL], y[CPL], ss = 0.f;
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) {
+                    float x = a4[c];
+#pragma unroll
+                    for (int q2 = 1; q2 < NB; ++q2)
+                        if (sub == q2) x = a4[q2 * CPL + c];
+                    v[c] = x;
+                    y[c] = tanhf(s * x);
+                    ss += y[c] * y[c];
+                }
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) ss += __shfl_xor_sync(FULLM, ss, o);
+                if (ss > 0.f) {
+                    const float inv = rsqrtf(ss);
+#pragma unroll
+                    for (int c = 0; c < CPL; ++c) y[c] *= inv;
+                }
+                const int64_t f0 = i * W + cl * 4 + sub * CPL;   // this lane's first column
+                if constexpr (CPL == 2) {
+                    reinterpret_cast<float2 *>(A + f0)[0] = make_float2(v[0], v[1]);
+                    if (Z) reinterpret_cast<float2 *>(Z + f0)[0] = make_float2(y[0], y[1]);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < CPL; ++c) {
+                        A[f0 + c] = v[c];
+                        if (Z) Z[f0 + c] = y[c];
+                    }
+                }
             }
             ++mine;
         }
