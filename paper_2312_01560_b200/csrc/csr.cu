@@ -214,9 +214,11 @@ struct GroupSync {
 };
 
 // warp register bitonic sort of 32 values (ascending by lane)
+// ascending bitonic sort of the first N lanes' values (N = 8, 16, 32; the other lanes hold INT_MAX padding)
+template <int N = 32>
 __device__ __forceinline__ int32_t warp_sort32(int32_t v, int lane) {
 #pragma unroll
-    for (int k = 2; k <= 32; k <<= 1) {
+    for (int k = 2; k <= N; k <<= 1) {
 #pragma unroll
         for (int j = k >> 1; j >= 1; j >>= 1) {
             const int32_t o = __shfl_xor_sync(0xffffffffu, v, j);
@@ -750,9 +752,9 @@ __device__ __forceinline__ int warp_sort_dedup_reg(const int32_t *a, int len, in
 
 // warp sort + dedup of one row held in shared memory; writes the unique prefix to outp, returns its length
 __device__ __forceinline__ int warp_sort_dedup(int32_t *a, int len, int32_t *outp, int lane) {
-    if (len <= 32) {
+    if (len <= 32) {   // rows of <= 8 / 16 entries (a third of C4's rows) take the shorter networks
         int32_t v = lane < len ? a[lane] : INT_MAX;
-        v = warp_sort32(v, lane);
+        v = len <= 8 ? warp_sort32<8>(v, lane) : len <= 16 ? warp_sort32<16>(v, lane) : warp_sort32<32>(v, lane);
         const int32_t prev = __shfl_up_sync(0xffffffffu, v, 1);
         const bool keep = lane < len && (lane == 0 || v != prev);
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
@@ -817,7 +819,7 @@ __device__ __forceinline__ void warp_sort_inplace(int32_t *a, int len, int lane)
     if (len <= 1) return;
     if (len <= 32) {
         int32_t v = lane < len ? a[lane] : INT_MAX;
-        v = warp_sort32(v, lane);
+        v = len <= 8 ? warp_sort32<8>(v, lane) : len <= 16 ? warp_sort32<16>(v, lane) : warp_sort32<32>(v, lane);
         __syncwarp();
         if (lane < len) a[lane] = v;
         __syncwarp();
