@@ -1064,30 +1064,48 @@ __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PAC
 
 __global__ void csr_compact(int64_t nl, const int64_t *__restrict__ raw_ptr, const int32_t *__restrict__ col_raw,
                             const int64_t *__restrict__ row_ptr, int32_t *__restrict__ col) {
-    // a warp takes 32 consecutive rows: their offsets are loaded once, coalesced (lane = row), then the rows
-    // are copied one after the other with the offsets broadcast by shuffle, two rows' loads in flight
+    // a warp takes 32 consecutive rows (offsets loaded once, coalesced, lane = row) and copies their unique prefixes as
+    // ONE flat range of entries, 32 x 4 at a time: entry x belongs to the row whose prefix sum of lengths brackets it
+    // (a 5-step search over the lanes' sums), so every lane moves an entry on every step and the stores, whose
+    // destination range is contiguous, are fully coalesced
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t r0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; r0 < nl; r0 += warps * 32) {
         const int64_t row = r0 + lane;
-        int64_t src = 0, dst = 0;
+        int64_t src = 0;
         int len = 0;
         if (row < nl) {
             src = raw_ptr[row];
-            dst = row_ptr[row];
-            len = static_cast<int>(row_ptr[row + 1] - dst);
+            len = static_cast<int>(row_ptr[row + 1] - row_ptr[row]);
         }
-        for (int j = 0; j < 32; j += 2) {
-            const int64_t s0 = __shfl_sync(0xffffffffu, src, j), d0 = __shfl_sync(0xffffffffu, dst, j);
-            const int64_t s1 = __shfl_sync(0xffffffffu, src, j + 1), d1 = __shfl_sync(0xffffffffu, dst, j + 1);
-            const int l0 = __shfl_sync(0xffffffffu, len, j), l1 = __shfl_sync(0xffffffffu, len, j + 1);
-            const int lm = max(l0, l1);
-            for (int x = lane; x < lm; x += 32) {
-                const int32_t a = x < l0 ? col_raw[s0 + x] : 0;
-                const int32_t b = x < l1 ? col_raw[s1 + x] : 0;
-                if (x < l0) col[d0 + x] = a;
-                if (x < l1) col[d1 + x] = b;
+        int incl = len;   // inclusive prefix of the lengths over the lanes
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        const int64_t dst0 = row_ptr[min(r0, nl - 1)];   // the 32 rows' unique entries are contiguous from here
+        const int64_t sb = src - (incl - len);            // raw start minus the row's flat offset
+        for (int x0 = 0; x0 < total; x0 += 32 * 4) {
+            int32_t v[4];
+            int xs[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int x = x0 + u * 32 + lane;
+                int k = 0;   // the first lane whose inclusive prefix exceeds x
+#pragma unroll
+                for (int st = 16; st >= 1; st >>= 1) {
+                    const int p = __shfl_sync(0xffffffffu, incl, k + st - 1);
+                    if (p <= x) k += st;
+                }
+                const int64_t base = __shfl_sync(0xffffffffu, sb, k & 31);
+                xs[u] = x;
+                v[u] = x < total ? col_raw[base + x] : 0;
             }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (xs[u] < total) col[dst0 + xs[u]] = v[u];
         }
     }
 }
