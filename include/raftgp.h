@@ -344,7 +344,8 @@ RAFTGP_API raftgp_status raftgp_stream_destroy(raftgp_stream s);
  *   RAFTGP_STREAM_EXACT (the default): the hops are recomputed over R_{k} (or every row) with the hop kernels, so Z
  *     stays bit-identical to raftgp_embed(NCUT) on the new graph.
  *   RAFTGP_STREAM_DELTA: the stream keeps every GCN hop's pre-activation sums A^h_i = T^h_i + sum_{j in N(i)} T^h_j
- *     (n x dims[h] fp32 each, device, library-owned); after a batch, rows outside V' add the changes
+ *     (n x dims[h] fp32 each, device, library-owned, plus an n x max(dims[1..L-1]) scratch and an int32[n] index);
+ *     after a batch, rows outside V' add the changes
  *     T^h_j(new) - T^h_j(old) of their neighbours in R_h only, and the rows of V' are summed in full. Hop h < L visits
  *     the rows of R_{h+1}, the last hop every row, each reading col_idx once instead of one operand row per CSR
  *     entry. Z equals the full recompute up to fp32 rounding order (re-associated sums; the error grows slowly with
