@@ -14,6 +14,8 @@ C5 (N = 5e7, ~1.94e9 CSR entries): raftgp_build_embed on sampled rows against th
     receptive-field computation (oracle.embed_rows; MOD's g from one streaming pass over Theta).
 Table I widths 4096->2048->1024->512->256 at N = 2E5 (the C3 graph, bench's table1 leg):
     both Z matrices in full against oracle.project + oracle.gcn_np.
+Streaming at C4 (bench's streaming leg): the exact stream bit-identical to a fresh embed of the merged graph, the
+    delta-mode stream within fp32 re-association error of it.
 The oracle runs with all host cores (OpenMP over rows; bit-identical to one thread, see oracle.c header).
 """
 import numpy as np
@@ -243,3 +245,34 @@ def test_table1_widths_2e5(rg):
         e = rel_fro(Zh[v], Zo)
         assert e <= TOL, f"{v}: relative Frobenius error {e:.3e}"
         assert row_err(Zh[v], Zo).max() <= ROW_TOL
+
+
+# ------------------------------------------------------------------ NEXT-4 streaming at C4 (bench's streaming leg)
+def test_c4_stream_exact_and_delta(rg, c4):
+    """Streams at the bench's size: after 10-edge batches and a 1000-edge batch the exact stream's Z equals
+    raftgp_embed_multi(ncut) on the merged graph BIT FOR BIT, and the delta-mode stream (every GCN hop from stored
+    sums + changed rows) stays within fp32 re-association error of it (reading #32)."""
+    ctx, gr, _, _, src, dst = c4
+    dims = list(synth.CONFIGS["C4"].dims)
+    rng = np.random.default_rng(41)
+    ex = rg.Stream(rg.raftgp_build_csr(ctx, gr.n, src, dst), dims, 0)
+    de = rg.Stream(rg.raftgp_build_csr(ctx, gr.n, src, dst), dims, 0)
+    de.set_mode("delta")
+    s_all, d_all = src, dst
+    for B in (10, 10, 1000):
+        es = torch.from_numpy(rng.integers(0, gr.n, B).astype(np.int32)).cuda()
+        ed = torch.from_numpy(rng.integers(0, gr.n, B).astype(np.int32)).cuda()
+        st_e = ex.add_edges(es, ed)
+        st_d = de.add_edges(es, ed)
+        assert st_e["changed"] == st_d["changed"] and st_e["affected"][:-1] == st_d["affected"][:-1]
+        s_all, d_all = torch.cat([s_all, es]), torch.cat([d_all, ed])
+        Ze, Zd = ex.embedding(), de.embedding()
+        assert (Zd - Ze).abs().max().item() <= 5e-6
+        assert ((Zd - Ze).norm() / Ze.norm()).item() <= 2e-6
+    g2 = rg.raftgp_build_csr(ctx, gr.n, s_all, d_all)
+    _, Z = rg.raftgp_embed_multi(g2, ["ncut"], dims, 0)
+    assert torch.equal(ex.embedding(), Z["ncut"])
+    assert ex.graph().info()["nnz_local"] == g2.info()["nnz_local"]
+    ex.close()
+    de.close()
+    g2.close()
