@@ -226,6 +226,8 @@ raftgp_status csr_build(raftgp_ctx ctx, int64_t n, int64_t m, const int32_t *src
                         int64_t re, raftgp_graph g);
 raftgp_status degrees_finalize(raftgp_graph g, int64_t known_2e = -1);
 raftgp_status ensure_slots(raftgp_graph g);   // relabel.cu: g->slot / colx / s_slot / hubk for a whole graph
+// relabel.cu: the smallest degree t with #(deg >= t) <= kmax (device int32[1]) for L2 hints on hub rows
+raftgp_status hub_degree_threshold(raftgp_ctx ctx, const int32_t *deg, int64_t n, int64_t kmax, int32_t *thr_dev);
 void drop_slots(raftgp_graph g);
 bool slots_enabled();                          // RAFTGP_RELABEL (default 1)
 int64_t slot_hub_bytes();                      // operand bytes of hub slots (RAFTGP_HUB_MB, default 64 MB)

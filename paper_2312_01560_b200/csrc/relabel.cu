@@ -141,6 +141,25 @@ __global__ void slot_cols(const int32_t *__restrict__ col, int64_t nnz, const ui
 
 }  // namespace
 
+// the smallest degree t with #(deg >= t) <= kmax into thr_dev (device int32[1]; kDegBins = no hubs), on the ctx stream
+raftgp_status hub_degree_threshold(raftgp_ctx ctx, const int32_t *deg, int64_t n, int64_t kmax, int32_t *thr_dev) {
+    unsigned int *hist = nullptr;
+    RG_TRY(dalloc_t(ctx, &hist, kDegBins));
+    raftgp_status st = dzero(ctx, hist, sizeof(unsigned int) * kDegBins, ctx->stream);
+    if (st == RAFTGP_OK) {
+        const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), (int64_t)ctx->sm_count * 2));
+        LaunchScope L(ctx, K_ORDER);
+        slot_hist<<<grid, 256, 0, ctx->stream>>>(deg, n, hist);
+        slot_threshold<<<1, 1024, 0, ctx->stream>>>(hist, kmax, thr_dev);
+    }
+    if (st == RAFTGP_OK) {
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) st = cuda_fail(e, "kernel launch");
+    }
+    dfree(ctx, hist);
+    return st;
+}
+
 int64_t slot_hub_bytes() {
     static const int64_t b = [] {
         const char *e = getenv("RAFTGP_HUB_MB");

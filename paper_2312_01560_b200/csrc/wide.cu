@@ -265,11 +265,29 @@ struct WideArgs {
     float *ssq;              // GCN, deferred normalisation: per-row, per-slice sums of squares (n x NW) or null
     unsigned long long *ctr; // zeroed row counter: CTAs claim rows dynamically (degree skew), or null (grid-stride)
     const int32_t *order;    // visiting order of the rows (heavy rows spread, order.cu), or null
+    const int32_t *hub_thr;  // device int32[1]: gathered rows of degree >= *hub_thr are loaded L2-evict-last, the
+                             // others evict-first (the hub rows then stay in L2), or null: plain loads
 };
+
+__device__ __forceinline__ float4 ldg4_hint(const float4 *p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
 
 template <int KIND, int V, int U>
 __global__ void __launch_bounds__(512) hop_wide(WideArgs a) {
     constexpr int CW = 128 * V;
+    // hub rows (degree >= *hub_thr, a byte budget of the widest rows) are loaded evict-last and the rest evict-first,
+    // so the often-gathered rows stay in L2 (Table I leg at 2E5: wide hops 50.4 -> 48.4 ms)
+    const bool hinted = a.hub_thr != nullptr;
+    const int32_t hthr = hinted ? __ldg(a.hub_thr) : 0x7fffffff;
+    uint64_t pol_last = 0, pol_first = 0;
+    if (hinted) {
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+    }
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int NW = a.W / CW;                 // warps (slices) per row
     const int rpc = (int)(blockDim.x >> 5) / NW;   // rows per CTA iteration
@@ -297,6 +315,7 @@ __global__ void __launch_bounds__(512) hop_wide(WideArgs a) {
             for (int64_t base = beg; base < end; base += 32) {
                 const int cnt = (int)min((int64_t)32, end - base);
                 const int32_t myj = lane < cnt ? __ldg(a.col + base + lane) : 0;
+                const int myhub = (hinted && lane < cnt) ? (__ldg(a.deg_all + myj) >= hthr) : 0;
                 float myw = 0.f;
                 if (KIND == W_NCUT || KIND == W_DUAL) myw = lane < cnt ? __ldg(a.s_all + myj) : 0.f;
                 if (KIND == W_MOD_REDUCED) myw = lane < cnt ? (float)__ldg(a.deg_all + myj) : 0.f;
@@ -306,10 +325,19 @@ __global__ void __launch_bounds__(512) hop_wide(WideArgs a) {
                     for (int u = 0; u < U; ++u) {
                         const int k = k0 + u;
                         const int32_t j = __shfl_sync(0xffffffffu, myj, k & 31);
+                        const int hub = __shfl_sync(0xffffffffu, myhub, k & 31);
+                        if (hinted) {
+                            const uint64_t pol = hub ? pol_last : pol_first;
 #pragma unroll
-                        for (int v = 0; v < V; ++v)
-                            x[u][v] = k < cnt ? __ldg(X4 + (int64_t)j * W4 + cbase + v * 32 + lane)
-                                              : make_float4(0.f, 0.f, 0.f, 0.f);
+                            for (int v = 0; v < V; ++v)
+                                x[u][v] = k < cnt ? ldg4_hint(X4 + (int64_t)j * W4 + cbase + v * 32 + lane, pol)
+                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+                        } else {
+#pragma unroll
+                            for (int v = 0; v < V; ++v)
+                                x[u][v] = k < cnt ? __ldg(X4 + (int64_t)j * W4 + cbase + v * 32 + lane)
+                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
                     }
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
@@ -674,6 +702,17 @@ raftgp_status launch_wide(raftgp_ctx ctx, const WideArgs &a) {
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.n, rpc), ctx->sm_count * per_sm));
     WideArgs b = a;
     b.ctr = nullptr;
+    // hub threshold for this width: the highest-degree rows up to RAFTGP_WIDE_HUB_MB (default 64) MB of operand rows
+    static const int64_t hub_mb = [] {
+        const char *e = getenv("RAFTGP_WIDE_HUB_MB");
+        return e ? (int64_t)std::max(0, atoi(e)) : (int64_t)64;
+    }();
+    int32_t *thr = nullptr;
+    if (hub_mb > 0 && a.deg_all && a.n > 0) {
+        RG_TRY(dalloc_t(ctx, &thr, 1));
+        RG_TRY(hub_degree_threshold(ctx, a.deg_all, a.n, (hub_mb << 20) / ((int64_t)a.W * 4), thr));
+        b.hub_thr = thr;
+    }
     static const bool dyn = [] {   // RAFTGP_WIDE_DYN=0: static grid-stride rows
         const char *e = getenv("RAFTGP_WIDE_DYN");
         return !(e && e[0] == '0');
@@ -691,6 +730,7 @@ raftgp_status launch_wide(raftgp_ctx ctx, const WideArgs &a) {
         else hop_wide<KIND, 4, U4><<<grid, 32 * warps, 0, ctx->stream>>>(b);
     }
     dfree(ctx, b.ctr);
+    dfree(ctx, thr);
     return RAFTGP_OK;
 }
 
