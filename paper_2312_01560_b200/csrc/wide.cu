@@ -269,6 +269,13 @@ struct WideArgs {
                              // others evict-first (the hub rows then stay in L2), or null: plain loads
 };
 
+#ifndef RG_WIDE_STCS
+#define RG_WIDE_STCS 1
+#endif
+__device__ __forceinline__ void wst4(float4 *p, const float4 &v, bool hinted) {
+    if (RG_WIDE_STCS && hinted) __stcs(p, v);
+    else *p = v;
+}
 __device__ __forceinline__ float4 ldg4_hint(const float4 *p, uint64_t pol) {
     float4 v;
     asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
@@ -420,21 +427,23 @@ __global__ void __launch_bounds__(512) hop_wide(WideArgs a) {
 #pragma unroll
             for (int v = 0; v < V; ++v) {
                 const int64_t c4 = cbase + v * 32 + lane;
+                // outputs are written once and read by a later launch: streamed (evict-first) when the gathers
+                // keep hub rows in L2 (RG_WIDE_STCS)
                 if (KIND == W_DUAL) {
                     // DUAL: out = NCut's T (acc2 path), out2 = MOD's T
-                    if (a.out) reinterpret_cast<float4 *>(a.out)[i * W4 + c4] = y2[v];
-                    if (a.out2) reinterpret_cast<float4 *>(a.out2)[i * W4 + c4] = y[v];
+                    if (a.out) wst4(reinterpret_cast<float4 *>(a.out) + i * W4 + c4, y2[v], hinted);
+                    if (a.out2) wst4(reinterpret_cast<float4 *>(a.out2) + i * W4 + c4, y[v], hinted);
                 } else if (a.out) {
-                    reinterpret_cast<float4 *>(a.out)[i * W4 + c4] = y[v];
+                    wst4(reinterpret_cast<float4 *>(a.out) + i * W4 + c4, y[v], hinted);
                 }
                 if (KIND == W_GCN && a.zhi) {
                     const int k = (int)(c4 * 4);
                     const int64_t chunk = (i / kGM) * (a.W / kKB) + k / kKB;
                     const size_t off = (size_t)chunk * chunk_bytes(kGM) + kmajor_off((int)(i % kGM), k % kKB, kGM);
                     const float4 h = make_float4(tf32_hi(y[v].x), tf32_hi(y[v].y), tf32_hi(y[v].z), tf32_hi(y[v].w));
-                    *reinterpret_cast<float4 *>(reinterpret_cast<char *>(a.zhi) + off) = h;
-                    *reinterpret_cast<float4 *>(reinterpret_cast<char *>(a.zlo) + off) =
-                        make_float4(y[v].x - h.x, y[v].y - h.y, y[v].z - h.z, y[v].w - h.w);
+                    wst4(reinterpret_cast<float4 *>(reinterpret_cast<char *>(a.zhi) + off), h, hinted);
+                    wst4(reinterpret_cast<float4 *>(reinterpret_cast<char *>(a.zlo) + off),
+                         make_float4(y[v].x - h.x, y[v].y - h.y, y[v].z - h.z, y[v].w - h.w), hinted);
                 }
             }
         }
