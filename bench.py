@@ -421,6 +421,9 @@ def measure_stream(args, rg, dev, barrier, gr, src_d, dst_d, dims):
             ts.append(e0.elapsed_time(e1))
             g2.close()
         full[B] = float(np.median(ts[1:]))
+    # the same batches for both modes, so the delta stream's final Z can be compared with the exact one's
+    batches = {B: [edges(B) for _ in range(4)] for B in (10, 1000)}
+    z_exact = None
     for mode in ("exact", "delta"):
         g = rg.raftgp_build_csr(ctx, gr.n, src_d, dst_d)
         stream = rg.Stream(g, dims, args.seed)
@@ -429,7 +432,7 @@ def measure_stream(args, rg, dev, barrier, gr, src_d, dst_d, dims):
         for B in (10, 1000):
             ts, st = [], None
             for rep in range(4):
-                es, ed = edges(B)
+                es, ed = batches[B][rep]
                 barrier()
                 e0.record(ctx.stream)
                 st = stream.add_edges(es, ed)
@@ -442,6 +445,13 @@ def measure_stream(args, rg, dev, barrier, gr, src_d, dst_d, dims):
                                    "ms_per_batch": [round(t, 3) for t in ts], "full_rebuild_ms": full[B],
                                    "speedup": full[B] / t_stream, "changed_nodes": st["changed"],
                                    "recomputed_rows": st["affected"]})
+        Z = stream.embedding()
+        if mode == "exact":
+            z_exact = Z.clone()
+        else:   # after the same 8 batches: the delta stream against the exact (bit-identical to a rebuild) one
+            dz = (Z - z_exact).abs()
+            out["delta_vs_exact"] = {"batches": 8, "max_abs": float(dz.max().item()),
+                                     "rel_frobenius": float(((Z - z_exact).norm() / z_exact.norm()).item())}
         stream.close()
     return out
 
