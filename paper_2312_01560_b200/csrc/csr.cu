@@ -751,10 +751,17 @@ __device__ __forceinline__ int warp_sort_dedup_reg(const int32_t *a, int len, in
 }
 
 // warp sort + dedup of one row held in shared memory; writes the unique prefix to outp, returns its length
+// SHORT: rows of <= 8 / 16 entries take the 6- / 10-stage networks (the packed-entry kernel, C4's: bucket sort
+// 3.48 -> 3.29 ms); the unpacked kernel (C5's) keeps the single network — with the extra branches the compiler
+// gave it 32 registers and spills instead of 55 (bucket sort 36.5 -> 39.8 ms at C5)
+template <bool SHORT>
 __device__ __forceinline__ int warp_sort_dedup(int32_t *a, int len, int32_t *outp, int lane) {
     if (len <= 32) {   // rows of <= 8 / 16 entries (a third of C4's rows) take the shorter networks
         int32_t v = lane < len ? a[lane] : INT_MAX;
-        v = len <= 8 ? warp_sort32<8>(v, lane) : len <= 16 ? warp_sort32<16>(v, lane) : warp_sort32<32>(v, lane);
+        if constexpr (SHORT)
+            v = len <= 8 ? warp_sort32<8>(v, lane) : len <= 16 ? warp_sort32<16>(v, lane) : warp_sort32<32>(v, lane);
+        else
+            v = warp_sort32<32>(v, lane);
         const int32_t prev = __shfl_up_sync(0xffffffffu, v, 1);
         const bool keep = lane < len && (lane == 0 || v != prev);
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
@@ -815,11 +822,15 @@ __device__ __forceinline__ void warp_sort_reg_inplace(int32_t *a, int len, int l
     __syncwarp();
 }
 
+template <bool SHORT>
 __device__ __forceinline__ void warp_sort_inplace(int32_t *a, int len, int lane) {
     if (len <= 1) return;
     if (len <= 32) {
         int32_t v = lane < len ? a[lane] : INT_MAX;
-        v = len <= 8 ? warp_sort32<8>(v, lane) : len <= 16 ? warp_sort32<16>(v, lane) : warp_sort32<32>(v, lane);
+        if constexpr (SHORT)
+            v = len <= 8 ? warp_sort32<8>(v, lane) : len <= 16 ? warp_sort32<16>(v, lane) : warp_sort32<32>(v, lane);
+        else
+            v = warp_sort32<32>(v, lane);
         __syncwarp();
         if (lane < len) a[lane] = v;
         __syncwarp();
@@ -1015,7 +1026,7 @@ __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PAC
                     // cnt[k] now ends sub-range k; sort each range into place
                     for (int k = gw; k < nsub; k += 4) {
                         const int b0 = k ? cnt[k - 1] : 0, b1 = cnt[k];
-                        warp_sort_inplace(tmp + b0, b1 - b0, lane);
+                        warp_sort_inplace<PACKED>(tmp + b0, b1 - b0, lane);
                         for (int i = b0 + lane; i < b1; i += 32) a[i] = tmp[i];
                     }
                     gsync();
@@ -1052,7 +1063,7 @@ __global__ void __launch_bounds__(1024) csr_bucket_sort(const typename Entry<PAC
                 if (t >= we) break;
                 const int len = off[t + 1] - off[t];
                 if (len > kGroupRow) continue;
-                const int w = warp_sort_dedup(s + off[t] - wbase, len, col_raw + e0 + off[t], lane);
+                const int w = warp_sort_dedup<PACKED>(s + off[t] - wbase, len, col_raw + e0 + off[t], lane);
                 if (lane == 0) deg[r0 + t] = w;
             }
             __syncthreads();
